@@ -1,0 +1,306 @@
+#!/usr/bin/env python3
+"""Benchmark: UCCSD energy evals/sec at 18 qubits (complex128) + rotation-pass HBM GB/s.
+
+Step = one VQE gradient evaluation of BASELINE.json config 3 (18 qubits, 10
+electrons, 560 generators): the parameter-shift set {theta, theta +- pi/2 e_k}
+= 1121 energy evaluations in one batched call through the C-ABI.
+
+  value     device-resident theta/energies (ffq_energy_batch_device), CUDA events
+  e2e       host theta in, host energies out (ffq_energy_batch), H2D+D2H timed
+  roofline  the generic Pauli-rotation pass (k_pauli_rotation) on a 28-qubit
+            state (4 GiB >> L2), algorithmic 32*2^n bytes per pass
+  cpu_baseline  the C oracle on this host's cores, bounded sample
+
+Multi-GPU (torchrun): every rank runs its own gradient set (weak scaling, no
+data-path collective); the step time is the max over ranks.
+`--impl reference` times the CPU oracle (the reference has no implementation
+of this path) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "UCCSD energy evals/sec at 18 qubits (c128); rotation-pass HBM GB/s vs peak"
+UNIT = "evals/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload(rank=0):
+    from paper_2402_17993_b200 import parameter_shift_set, problems
+
+    P = problems.config_problem(3)
+    th0 = P.thetas[0].copy()
+    if rank:  # weak scaling: each rank its own seeded theta (same plan)
+        th0 = np.array(__import__("paper_2402_17993_b200").uniform_vector(problems.ham_seed(3) + 100 + rank,
+                                                                        P.n_gen, -0.1, 0.1))
+    rows = np.array(parameter_shift_set(list(th0))).reshape(-1, P.n_gen)
+    return P, rows
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        self.out = os.path.join("/tmp", f"ffq_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=open(self.out, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in open(self.out).read().strip().splitlines()]
+            sm = [float(r[1]) for r in rows]
+            mx = float(rows[0][2])
+            reasons = set()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in rows:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(nm)
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(rows)}
+        except Exception as e:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
+
+
+def cpu_oracle_rate(P, rows, n_evals, threads=None):
+    from oracle import ffo
+
+    if threads:
+        ffo.set_threads(threads)
+    x, z, c = P.ham_arrays()
+    H = ffo.PauliSum.from_terms(P.n_qubits, x, z, c)
+    kind, idx = ffo.build_generators(P.n_qubits, P.n_elec)
+    order = np.array(P.plan.order, np.int32)
+    t = time.perf_counter()
+    es = []
+    for r in range(n_evals):
+        es.append(ffo.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, rows[r], H)[0])
+    dt = time.perf_counter() - t
+    return n_evals / dt, es, ffo.get_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    P, rows = workload(0)
+    cores = os.cpu_count() or 1
+    evals_per_step = 1
+    for _ in range(args.warmup):
+        cpu_oracle_rate(P, rows, evals_per_step, cores)
+    t = time.perf_counter()
+    for s in range(args.steps):
+        cpu_oracle_rate(P, rows[s % len(rows):], evals_per_step, cores)
+    dt = time.perf_counter() - t
+    v = args.steps * evals_per_step / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded, BASELINE.json config 3)",
+        "config": {"workload": "config3 18q/10e/560 generators; CPU oracle (SPEC restatement, C+OpenMP), "
+                               f"{evals_per_step} energy evaluation of the parameter-shift set per step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} x {evals_per_step} evaluation(s) of config 3"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rot-qubits", type=int, default=28)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    from paper_2402_17993_b200 import capi
+
+    ctx = capi.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    P, rows = workload(rank)
+    B = rows.shape[0]
+    plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
+    th_host = P.plan_thetas(rows)
+    th_dev = torch.from_numpy(th_host).to(f"cuda:{local}")
+    e_dev = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # 2x L2
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step_device():
+        capi.energy_batch_device(ctx, plan, ham, P.hf, B, th_dev.data_ptr(), e_dev.data_ptr())
+
+    def timed(fn, k):
+        ms = []
+        with torch.cuda.stream(stream):
+            for _ in range(k):
+                flush.fill_(1)  # L2 flush between timed iterations (untimed)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+        return ms
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    l0 = ctx.launches()
+    with Clocks(local) as clk:
+        barrier()
+        ms = timed(step_device, args.steps)
+        barrier()
+    launches = ctx.launches() - l0
+    tot_ms = sum(ms)
+    if dist:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    e_first = e_dev.cpu().numpy().copy()
+    value = world * B * args.steps / (tot_ms / 1e3)
+
+    # e2e: host buffers through ffq_energy_batch (pinned staging + H2D + D2H inside)
+    def step_host():
+        step_host.out = capi.energy_batch(ctx, plan, ham, P.hf, th_host)
+
+    step_host()
+    barrier()
+    ms_e2e = timed(step_host, args.steps)
+    barrier()
+    tot_e2e = sum(ms_e2e)
+    if dist:
+        t = torch.tensor([tot_e2e], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_e2e = float(t.item())
+    e2e = world * B * args.steps / (tot_e2e / 1e3)
+    assert np.array_equal(step_host.out, e_first), "device and host paths disagree"
+
+    # roofline: the generic rotation pass on a state >> L2
+    peak, peak_src = peaks()
+    nq = args.rot_qubits
+    st = capi.State(ctx, nq, 1)
+    st.set_basis(0)
+    x, z = (0b1011 << 9), (0b111 << 4)
+    for _ in range(3):
+        st.rotate(x, z, 0.1)
+    ctx.synchronize()
+    rot_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(10):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st.rotate(x, z, 0.1 * (k % 2 * 2 - 1))
+            b.record(stream)
+            b.synchronize()
+            rot_ms.append(a.elapsed_time(b))
+    del st
+    rot_bytes = 32 * (1 << nq)
+    rot_avg = statistics.mean(rot_ms[2:])
+    achieved = rot_bytes / (rot_avg / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_cpu = 2
+        rate, es, cores = cpu_oracle_rate(P, rows, n_cpu, os.cpu_count())
+        parity = max(abs(es[i] - e_first[i]) for i in range(n_cpu))
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{n_cpu} energy evaluations of the config-3 parameter-shift set (C oracle, OpenMP)",
+               "parity_max_abs_hartree": parity}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded h~N(0,1), g~N(0,0.1), theta~U(-0.1,0.1); BASELINE.json config 3)",
+            "config": {"workload": "config3: 18 qubits, 10 electrons, 560 UCCSD generators, 9316-term JW "
+                                   "Hamiltonian; one step = parameter-shift gradient set (1121 energy "
+                                   "evaluations) per GPU",
+                       "evals_per_step_per_gpu": B, "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"replicas x{world} (independent gradient sets)"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(th_host.nbytes),
+                    "d2h_bytes_per_step": int(16 * B)},
+            "roofline": {"bound": "hbm", "kernel": "k_pauli_rotation (generic rotation pass)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
+                         "avg_launch_ms": rot_avg},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,46 @@
+// fragfield/hamiltonian.hpp -- spin-orbital Hamiltonians
+// and the seeded synthetic inputs of BASELINE.json's configs.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "fragfield/pauli.hpp"
+
+namespace fragfield {
+
+/// Spatial-orbital integrals: h (m x m, symmetric) and chemists' (pq|rs)
+/// stored at ((p*m+q)*m+r)*m+s with 8-fold symmetry.
+struct SpatialIntegrals {
+  int m = 0;
+  std::vector<double> h, g;
+  double e_const = 0.0;
+};
+
+/// SPEC.md:266-270, interleaved ordering: spin orbital 2P is
+/// alpha of spatial P, 2P+1 is beta.
+///   H = sum h_pq a+_p a_q + 1/2 sum g_pqrs a+_p a+_q a_s a_r + E_const,
+///   g_pqrs = (PR|QS) delta(sigma_p, sigma_r) delta(sigma_q, sigma_s).
+struct SpinOrbitalHamiltonian {
+  int n_so = 0;
+  int n_elec = 0;
+  std::vector<double> h;  // n_so^2
+  std::vector<double> g;  // n_so^4, physicists' order [p][q][r][s]
+  double e_const = 0.0;
+};
+
+/// Seeded synthetic integrals (BASELINE.json configs): h ~ N(0, sigma_h),
+/// (pq|rs) ~ N(0, sigma_g); std::mt19937_64 raw output, U = (x>>11)*2^-53,
+/// Box-Muller cosine branch, canonical quadruple loop -- see DESIGN.md.
+SpatialIntegrals synthetic_integrals(int m, uint64_t seed, double sigma_h = 1.0,
+                                     double sigma_g = 0.1);
+SpinOrbitalHamiltonian to_spin_orbitals(const SpatialIntegrals& ints, int n_elec);
+/// JW image of the spin-orbital Hamiltonian.
+PauliSum qubit_hamiltonian(const SpinOrbitalHamiltonian& H);
+/// Config 5: n_terms seeded random {I,X,Y,Z}^n strings, real c ~ N(0, sigma).
+PauliSum random_pauli_hamiltonian(int n_qubits, int n_terms, uint64_t seed, double sigma = 0.1);
+
+/// Uniform draws U(lo, hi) from mt19937_64(seed), same value mapping.
+std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double hi);
+
+}  // namespace fragfield

@@ -1,0 +1,143 @@
+/*
+ * fragfield_cuda.h -- C-ABI of the B200 UCCSD state-vector hot path
+ * (libfragfield_cuda.so). Plain pointers and sizes only; no torch/CUDA types.
+ *
+ * The reference (fragfield, /root/reference/proj) has no code or FFI for this
+ * path: its simulator / vqe-uccsd modules exist only as SPEC contracts. Each
+ * entry point below names the SPEC operation it replaces, so a maintainer can
+ * bind it from the reference's C++ side:
+ *
+ *   ffq_state_set_basis            hf_state
+ *   ffq_state_apply_pauli_rotation apply_pauli_rotation
+ *   ffq_state_expectation          expectation
+ *   ffq_plan_upload                TrotterPlan
+ *   ffq_state_apply_plan           energy_trotter (state) SPEC.md:508-516
+ *   ffq_energy_batch               energy_trotter, batched over amplitude
+ *                                  vectors (VQE objective / gradient sets /
+ *                                  FMO fragments)
+ *
+ * Conventions: a Pauli string is a pair of bitmasks
+ * (x, z) over qubits, qubit 0 = least-significant bit of the amplitude index;
+ * letter X where only x is set, Z where only z is set, Y where both are set;
+ * the string carries no phase (phase lives in the coefficient). State vectors
+ * are complex128, interleaved (re, im), natural binary order, laid out
+ * [batch][2^n].
+ *
+ * Errors: every call returns FFQ_OK (0) or a negative code; ffq_last_error()
+ * returns a message. The C++ facade maps FFQ_EINVAL / FFQ_ENONHERMITIAN to
+ * fragfield::ContractViolation (errors.hpp convention of the reference,
+ * proj/core/include/fragfield/errors.hpp:23-25) and the rest to
+ * std::runtime_error.
+ *
+ * Threading: one context per device, bound to one CUDA stream; a context is
+ * not re-entrant. Distinct contexts may be driven from different host threads.
+ * Determinism: energies are bitwise identical for any batch split or device
+ * count (fixed work decomposition and fixed-shape reduction trees).
+ */
+#ifndef FRAGFIELD_CUDA_H
+#define FRAGFIELD_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFQ_OK 0
+#define FFQ_EINVAL (-1)
+#define FFQ_ENONHERMITIAN (-2)
+#define FFQ_ECUDA (-3)
+#define FFQ_ENOMEM (-4)
+#define FFQ_ENCCL (-5)
+#define FFQ_ENODEV (-6)
+
+typedef struct ffq_ctx_s* ffq_ctx_t;
+typedef struct ffq_ham_s* ffq_ham_t;
+typedef struct ffq_plan_s* ffq_plan_t;
+typedef struct ffq_state_s* ffq_state_t;
+
+/* ---- library / context ---------------------------------------------------- */
+int ffq_version(void);
+int ffq_device_count(int* n_out);
+int ffq_ctx_create(int device, ffq_ctx_t* out);
+int ffq_ctx_destroy(ffq_ctx_t ctx);
+int ffq_ctx_synchronize(ffq_ctx_t ctx);
+/* Message of the last failing call on this context (ctx == NULL: last failing
+ * call on this host thread). Never NULL. */
+const char* ffq_last_error(ffq_ctx_t ctx);
+/* Number of kernels this context has launched so far (graph nodes counted). */
+int64_t ffq_ctx_kernel_launches(ffq_ctx_t ctx);
+/* The context's cudaStream_t, as an opaque pointer (for event timing). */
+int ffq_ctx_stream(ffq_ctx_t ctx, void** stream);
+/* Environment: FFQ_SMEM_MAX_QUBITS (default 13) caps the qubit count that
+ * uses the shared-memory-resident evaluator; read at ffq_ctx_create. */
+
+/* ---- qubit Hamiltonian (PauliSum) ------------------------ */
+/* Flat Pauli sum, any order; duplicate strings are summed. The library groups
+ * the terms by flip mask x. Non-Hermitian input (|Im c| > 1e-12) is rejected
+ * with FFQ_ENONHERMITIAN. */
+int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t* x,
+                   const uint64_t* z, const double* c_re, const double* c_im, ffq_ham_t* out);
+int ffq_ham_destroy(ffq_ham_t ham);
+/* n_groups = distinct flip masks; n_classes = (group, z outside the flip
+ * mask) classes the kernels evaluate per amplitude. */
+int ffq_ham_info(ffq_ham_t ham, int* n_groups, int64_t* n_terms, int64_t* n_classes);
+
+/* ---- Trotter plan (TrotterPlan) -------------------------- */
+/* n_gen generators in EXECUTION order. Generator g is the anti-Hermitian Pauli
+ * sum sum_j (c_re + i c_im)_j P_j over terms [term_off[g], term_off[g+1]),
+ * normally the JW image of tau - tau^dag; it is applied as exp(theta_g * A_g)
+ * (equivalently prod_j e^{i theta_g c_j P_j} in canonical term order,
+ * SPEC.md:511). Real parts must vanish (|c_re| <= 1e-12) -> else FFQ_EINVAL.
+ * Generators whose strings share one flip mask and commute are fused into one
+ * exact rotation pass; any other generator runs string by string. */
+int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_off,
+                    const uint64_t* x, const uint64_t* z, const double* c_re,
+                    const double* c_im, ffq_plan_t* out);
+int ffq_plan_destroy(ffq_plan_t plan);
+int ffq_plan_info(ffq_plan_t plan, int* n_fused, int* n_string_ops);
+
+/* ---- batched energy (energy_trotter) --------------------- */
+/* e_out[b] = <psi_b|H|psi_b>, psi_b = prod_g exp(theta[b][g] A_g) |hf_bits>.
+ * theta is [batch][n_gen] in plan order. Host pointers; the call returns when
+ * e_out is written. Imaginary residue above 1e-10 -> FFQ_ENONHERMITIAN. */
+int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
+                     int batch, const double* theta, double* e_out);
+/* Same with device pointers (inputs resident in HBM); asynchronous on the
+ * context stream; imag_dev (optional, [batch]) receives imaginary residues. */
+int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
+                            int batch, const double* theta_dev, double* e_dev,
+                            double* imag_dev);
+
+/* ---- state-level operations (simulator) ------------------ */
+int ffq_state_alloc(ffq_ctx_t ctx, int n_qubits, int batch, ffq_state_t* out);
+int ffq_state_free(ffq_state_t st);
+int ffq_state_set_basis(ffq_state_t st, uint64_t bits);
+int ffq_state_upload(ffq_state_t st, const double* psi);   /* [batch][2^n][2] */
+int ffq_state_download(ffq_state_t st, double* psi);       /* [batch][2^n][2] */
+/* psi <- cos(theta) psi + i sin(theta) P psi  (e^{i theta P}), every batch row */
+int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, double theta);
+/* Apply the plan with theta [batch][n_gen] (host pointer). */
+int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta);
+/* re_out/im_out [batch] (host) */
+int ffq_state_expectation(ffq_state_t st, ffq_ham_t ham, double* re_out, double* im_out);
+/* Device pointer to the amplitudes (for zero-copy interop in tests/bench). */
+int ffq_state_device_ptr(ffq_state_t st, void** ptr);
+
+/* ---- host-only diagnostics (no device needed) ----------------------------- */
+/* Compile a Hamiltonian / plan exactly as the upload calls do and report the
+ * table shapes. ham stats[8]: groups, terms, classes, active patterns,
+ * work items, pair visits per evaluation, class evaluations per evaluation,
+ * amplitude bytes read per evaluation. plan stats[6]: fused ops, string ops,
+ * active pattern pairs, pair updates per evaluation, bytes moved per
+ * evaluation (read+write), ops. */
+int ffq_ham_compile_stats(int n_qubits, int64_t n_terms, const uint64_t* x, const uint64_t* z,
+                          const double* c_re, const double* c_im, int64_t* stats);
+int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* x,
+                           const uint64_t* z, const double* c_re, const double* c_im,
+                           int64_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRAGFIELD_CUDA_H */

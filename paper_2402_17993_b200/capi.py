@@ -1,0 +1,232 @@
+"""ctypes binding of the C-ABI in include/fragfield_cuda.h.
+
+This is the binding a reference-side maintainer would write:
+plain pointers and sizes, return codes mapped to exceptions. The GPU parity
+tests and bench.py's end-to-end leg call the hot path through it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+from . import ContractViolation, DeviceError, native_library_path
+
+FFQ_OK, FFQ_EINVAL, FFQ_ENONHERMITIAN, FFQ_ECUDA, FFQ_ENOMEM, FFQ_ENCCL, FFQ_ENODEV = 0, -1, -2, -3, -4, -5, -6
+
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+_SIGS = {
+    "ffq_version": (C.c_int, []),
+    "ffq_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "ffq_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "ffq_ctx_destroy": (C.c_int, [_vp]),
+    "ffq_ctx_synchronize": (C.c_int, [_vp]),
+    "ffq_last_error": (C.c_char_p, [_vp]),
+    "ffq_ctx_kernel_launches": (C.c_int64, [_vp]),
+    "ffq_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ffq_ham_upload": (C.c_int, [_vp, C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, C.POINTER(_vp)]),
+    "ffq_ham_destroy": (C.c_int, [_vp]),
+    "ffq_ham_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ffq_plan_upload": (C.c_int, [_vp, C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.POINTER(_vp)]),
+    "ffq_plan_destroy": (C.c_int, [_vp]),
+    "ffq_plan_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ffq_energy_batch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, _f64p, _f64p]),
+    "ffq_energy_batch_device": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, _vp, _vp, _vp]),
+    "ffq_state_alloc": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "ffq_state_free": (C.c_int, [_vp]),
+    "ffq_state_set_basis": (C.c_int, [_vp, C.c_uint64]),
+    "ffq_state_upload": (C.c_int, [_vp, _f64p]),
+    "ffq_state_download": (C.c_int, [_vp, _f64p]),
+    "ffq_state_apply_pauli_rotation": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_double]),
+    "ffq_state_apply_plan": (C.c_int, [_vp, _vp, _f64p]),
+    "ffq_state_expectation": (C.c_int, [_vp, _vp, _f64p, _f64p]),
+    "ffq_state_device_ptr": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ffq_ham_compile_stats": (C.c_int, [C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, _i64p]),
+    "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(native_library_path())
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def header_symbols(path=None):
+    """Every function the public header declares."""
+    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "include", "fragfield_cuda.h")
+    src = open(path).read()
+    return sorted(set(re.findall(r"\b(ffq_[a-z0-9_]+)\s*\(", src)))
+
+
+def check(rc, ctx=None):
+    if rc == FFQ_OK:
+        return
+    msg = lib().ffq_last_error(ctx).decode()
+    if rc in (FFQ_EINVAL, FFQ_ENONHERMITIAN):
+        raise ContractViolation(msg)
+    raise DeviceError(f"[{rc}] {msg}")
+
+
+def _terms(x, z, c):
+    c = np.asarray(c, np.complex128)
+    return (np.ascontiguousarray(x, np.uint64), np.ascontiguousarray(z, np.uint64),
+            np.ascontiguousarray(c.real), np.ascontiguousarray(c.imag))
+
+
+def ham_compile_stats(n, x, z, c):
+    x, z, re_, im = _terms(x, z, c)
+    st = np.zeros(8, np.int64)
+    check(lib().ffq_ham_compile_stats(n, len(x), x, z, re_, im, st))
+    keys = ["groups", "terms", "classes", "active_patterns", "work_items", "pair_visits",
+            "class_evals", "bytes_read"]
+    return dict(zip(keys, st.tolist()))
+
+
+def plan_compile_stats(n, off, x, z, c):
+    x, z, re_, im = _terms(x, z, c)
+    off = np.ascontiguousarray(off, np.int64)
+    st = np.zeros(6, np.int64)
+    check(lib().ffq_plan_compile_stats(n, len(off) - 1, off, x, z, re_, im, st))
+    keys = ["fused", "string_ops", "pattern_pairs", "pair_updates", "bytes", "ops"]
+    return dict(zip(keys, st.tolist()))
+
+
+class Context:
+    """One device + stream (ffq_ctx_t)."""
+
+    def __init__(self, device=0):
+        h = _vp()
+        check(lib().ffq_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().ffq_ctx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def launches(self):
+        return lib().ffq_ctx_kernel_launches(self.h)
+
+    def stream_ptr(self):
+        p = _vp()
+        check(lib().ffq_ctx_stream(self.h, C.byref(p)), self.h)
+        return p.value or 0
+
+    def synchronize(self):
+        check(lib().ffq_ctx_synchronize(self.h), self.h)
+
+
+class Hamiltonian:
+    def __init__(self, ctx: Context, n, x, z, c):
+        self.ctx = ctx
+        x, z, re_, im = _terms(x, z, c)
+        h = _vp()
+        check(lib().ffq_ham_upload(ctx.h, n, len(x), x, z, re_, im, C.byref(h)), ctx.h)
+        self.h = h
+
+    def info(self):
+        g = C.c_int(); t = C.c_int64(); cl = C.c_int64()
+        check(lib().ffq_ham_info(self.h, C.byref(g), C.byref(t), C.byref(cl)))
+        return g.value, t.value, cl.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ffq_ham_destroy(self.h)
+            self.h = None
+
+
+class Plan:
+    def __init__(self, ctx: Context, n, off, x, z, c):
+        self.ctx = ctx
+        x, z, re_, im = _terms(x, z, c)
+        off = np.ascontiguousarray(off, np.int64)
+        self.n_gen = len(off) - 1
+        h = _vp()
+        check(lib().ffq_plan_upload(ctx.h, n, self.n_gen, off, x, z, re_, im, C.byref(h)), ctx.h)
+        self.h = h
+
+    def info(self):
+        f = C.c_int(); s = C.c_int()
+        check(lib().ffq_plan_info(self.h, C.byref(f), C.byref(s)))
+        return f.value, s.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ffq_plan_destroy(self.h)
+            self.h = None
+
+
+def energy_batch(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, theta):
+    theta = np.ascontiguousarray(theta, np.float64)
+    batch = theta.shape[0] if theta.ndim == 2 else 1
+    out = np.zeros(batch)
+    check(lib().ffq_energy_batch(ctx.h, plan.h, ham.h, hf_bits, batch, theta.ravel(), out), ctx.h)
+    return out
+
+
+def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, batch, theta_ptr,
+                        e_ptr, im_ptr=None):
+    check(lib().ffq_energy_batch_device(ctx.h, plan.h, ham.h, hf_bits, batch, theta_ptr, e_ptr, im_ptr),
+          ctx.h)
+
+
+class State:
+    def __init__(self, ctx: Context, n, batch=1):
+        self.ctx, self.n, self.batch = ctx, n, batch
+        h = _vp()
+        check(lib().ffq_state_alloc(ctx.h, n, batch, C.byref(h)), ctx.h)
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ffq_state_free(self.h)
+            self.h = None
+
+    def set_basis(self, bits):
+        check(lib().ffq_state_set_basis(self.h, bits), self.ctx.h)
+
+    def upload(self, psi):
+        buf = np.ascontiguousarray(psi, np.complex128).reshape(-1)
+        if buf.size != self.batch << self.n:
+            raise ContractViolation("state size mismatch")
+        check(lib().ffq_state_upload(self.h, buf.view(np.float64)), self.ctx.h)
+
+    def download(self):
+        out = np.zeros(2 * (self.batch << self.n))
+        check(lib().ffq_state_download(self.h, out), self.ctx.h)
+        return out.view(np.complex128).reshape(self.batch, 1 << self.n)
+
+    def rotate(self, x, z, theta):
+        check(lib().ffq_state_apply_pauli_rotation(self.h, x, z, theta), self.ctx.h)
+
+    def apply_plan(self, plan: Plan, theta):
+        check(lib().ffq_state_apply_plan(self.h, plan.h, np.ascontiguousarray(theta, np.float64).ravel()),
+              self.ctx.h)
+
+    def expectation(self, ham: Hamiltonian):
+        re_ = np.zeros(self.batch); im = np.zeros(self.batch)
+        check(lib().ffq_state_expectation(self.h, ham.h, re_, im), self.ctx.h)
+        return re_ + 1j * im
+
+    def device_ptr(self):
+        p = _vp()
+        check(lib().ffq_state_device_ptr(self.h, C.byref(p)))
+        return p.value

@@ -1,0 +1,714 @@
+// ffq_capi.cu -- C-ABI of libfragfield_cuda.so (include/fragfield_cuda.h).
+//
+// Host orchestration of the sm_100a kernels in ffq_kernels.cuh: contexts own a
+// device + stream, plans/Hamiltonians own their compiled device tables, and
+// batched energy evaluation picks one of two execution paths:
+//   * n <= kSmemMaxQubits: k_smem_eval, one CTA per evaluation;
+//   * otherwise: a CUDA graph of per-op kernels over a [chunk][2^n] slab
+//     (HF build -> fused/string passes -> grouped expectation -> fixed-tree
+//     reduction), replayed for every chunk of the batch.
+// There is no CPU fallback: without a device every call fails with
+// FFQ_ENODEV / FFQ_ECUDA.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fragfield_cuda.h"
+#include "ffq_compile.hpp"
+#include "ffq_kernels.cuh"
+
+using namespace ffq;
+
+namespace {
+
+constexpr int kSmemMaxQubitsDefault = 13;
+constexpr int kThreads = 256;
+constexpr int kVersion = 1;
+
+thread_local std::string g_thread_err = "no error";
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));               \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw CudaError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+}  // namespace
+
+struct ffq_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n_sm = 148;
+  size_t smem_optin = 0;
+  int smem_max_qubits = kSmemMaxQubitsDefault;  // env FFQ_SMEM_MAX_QUBITS overrides
+  std::string err = "no error";
+  int64_t launches = 0;
+  // scratch
+  DevBuf<double> theta, eout, eim, io_theta, io_e;
+  DevBuf<double2> cs, partial, slab;
+  double* pinned = nullptr;
+  size_t pinned_n = 0;
+  void ensure_pinned(size_t n) {
+    if (n <= pinned_n) return;
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    CK(cudaMallocHost(&pinned, n * sizeof(double)));
+    pinned_n = n;
+  }
+};
+
+// a captured graph bakes in every scratch pointer, so all of them are key parts
+using GraphKey = std::vector<uintptr_t>;
+
+struct ffq_plan_s {
+  ffq_ctx_t ctx;
+  CompiledPlan cp;
+  DevBuf<int32_t> op_kind, op_gen, op_idx, str_ny;
+  DevBuf<double> op_cfac, op_sscale;
+  DevBuf<FusedDesc> fused;
+  DevBuf<uint64_t> pair_bits, str_x, str_z;
+  DevBuf<double2> pair_f;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int64_t> graph_nodes;
+  PlanDev dev() const {
+    PlanDev d;
+    d.n_ops = (int)cp.op_kind.size();
+    d.op_kind = op_kind.p; d.op_gen = op_gen.p; d.op_idx = op_idx.p;
+    d.op_cfac = op_cfac.p; d.op_sscale = op_sscale.p;
+    d.fused = fused.p; d.pair_bits = pair_bits.p; d.pair_f = pair_f.p;
+    d.str_x = str_x.p; d.str_z = str_z.p; d.str_ny = str_ny.p;
+    return d;
+  }
+  ~ffq_plan_s() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  }
+};
+
+struct ffq_ham_s {
+  ffq_ctx_t ctx;
+  CompiledHam ch;
+  DevBuf<GroupDesc> groups;
+  DevBuf<uint64_t> act_bits, cls_z;
+  DevBuf<double2> cls_f;
+  DevBuf<int32_t> item_g, item_p;
+  DevBuf<int64_t> item_u0;
+  HamDev dev() const {
+    HamDev d;
+    d.n_groups = (int)ch.groups.size();
+    d.groups = groups.p; d.act_bits = act_bits.p; d.cls_z = cls_z.p; d.cls_f = cls_f.p;
+    d.n_items = (int64_t)ch.item_g.size();
+    d.item_g = item_g.p; d.item_p = item_p.p; d.item_u0 = item_u0.p;
+    d.item_chunk = ch.item_chunk;
+    return d;
+  }
+};
+
+struct ffq_state_s {
+  ffq_ctx_t ctx;
+  int n = 0, batch = 0;
+  DevBuf<double2> psi;
+};
+
+namespace {
+
+int fail(ffq_ctx_t ctx, int code, const std::string& msg) {
+  g_thread_err = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(ffq_ctx_t ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    return f();
+  } catch (const BadInput& e) {
+    return fail(ctx, e.code, e.what());
+  } catch (const CudaError& e) {
+    std::string w = e.what();
+    bool oom = w.find("out of memory") != std::string::npos;
+    return fail(ctx, oom ? FFQ_ENOMEM : FFQ_ECUDA, w);
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, FFQ_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, FFQ_EINVAL, e.what());
+  }
+}
+
+int grid_for(int64_t work, int n_sm, int per_sm = 8) {
+  int64_t g = (work + kThreads - 1) / kThreads;
+  int64_t cap = (int64_t)n_sm * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <typename T>
+std::vector<T> as_vec(const T* p, size_t n) { return std::vector<T>(p, p + n); }
+
+// rotation-pass dispatch for a single string (state API and plan string ops)
+void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, uint64_t z, int ny,
+                   const double2* cs, int cs_stride, int op) {
+  int mode, hbit = 0;
+  int64_t nvec;
+  if (n < 2) throw BadInput("rotation kernels need n_qubits >= 2", FFQ_EINVAL);
+  if (x == 0) { mode = 0; nvec = 1LL << (n - 1); }
+  else if (!(x & 1ULL)) { mode = 1; hbit = __builtin_ctzll(x); nvec = 1LL << (n - 2); }
+  else if (x == 1ULL) { mode = 2; nvec = 1LL << (n - 1); }
+  else { mode = 3; hbit = __builtin_ctzll(x & ~1ULL); nvec = 1LL << (n - 2); }
+  dim3 grid(grid_for(nvec, ctx->n_sm), batch);
+  k_pauli_rotation<<<grid, kThreads, 0, ctx->stream>>>(psi, n, x, z, ny, cs, cs_stride, op, mode,
+                                                        hbit);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
+void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, int n, int batch,
+                  const FusedDesc& d, const double2* cs, int cs_stride, int op) {
+  const bool vec = !(d.x & 1ULL) && (n - d.w) >= 1;
+  const int64_t work = ((int64_t)d.npair << (n - d.w)) >> (vec ? 1 : 0);
+  dim3 grid(grid_for(work, ctx->n_sm), batch);
+  if (vec)
+    k_fused_gen<true><<<grid, kThreads, 0, ctx->stream>>>(psi, n, d, pl->pair_bits.p, pl->pair_f.p,
+                                                          cs, cs_stride, op);
+  else
+    k_fused_gen<false><<<grid, kThreads, 0, ctx->stream>>>(psi, n, d, pl->pair_bits.p,
+                                                           pl->pair_f.p, cs, cs_stride, op);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
+// apply every op of the plan to a [batch][2^n] slab; cs already computed
+void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, int batch, const double2* cs) {
+  const CompiledPlan& cp = pl->cp;
+  const int n = cp.n_qubits;
+  const int n_ops = (int)cp.op_kind.size();
+  for (int op = 0; op < n_ops; ++op) {
+    if (cp.op_kind[op] == 0) {
+      launch_fused(ctx, pl, psi, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op);
+    } else {
+      const int si = cp.op_idx[op];
+      launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
+    }
+  }
+}
+
+void launch_cs(ffq_ctx_t ctx, const ffq_plan_s* pl, const double* theta, int batch, double2* cs) {
+  const int n_ops = (int)pl->cp.op_kind.size();
+  if (n_ops == 0) return;
+  const int64_t work = (int64_t)n_ops * batch;
+  k_op_cs<<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+      theta, pl->cp.n_gen, n_ops, pl->op_gen.p, pl->op_cfac.p, pl->op_sscale.p, cs, batch);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
+void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, int n, int batch,
+                   double2* partial, double* e, double* im) {
+  const int64_t items = (int64_t)h->ch.item_g.size();
+  if (items == 0) {
+    CK(cudaMemsetAsync(e, 0, sizeof(double) * batch, ctx->stream));
+    if (im) CK(cudaMemsetAsync(im, 0, sizeof(double) * batch, ctx->stream));
+    return;
+  }
+  dim3 grid((unsigned)items, batch);
+  k_expect_items<kThreads><<<grid, kThreads, 0, ctx->stream>>>(psi, n, h->dev(), partial);
+  CK(cudaGetLastError());
+  k_reduce_partials<kThreads><<<batch, kThreads, 0, ctx->stream>>>(partial, items, e, im);
+  CK(cudaGetLastError());
+  ctx->launches += 2;
+}
+
+size_t smem_bytes(const ffq_plan_s* pl) {
+  return ((size_t(1) << pl->cp.n_qubits) + pl->cp.op_kind.size()) * sizeof(double2);
+}
+
+bool use_smem_path(ffq_ctx_t ctx, const ffq_plan_s* pl) {
+  return pl->cp.n_qubits <= ctx->smem_max_qubits && smem_bytes(pl) <= ctx->smem_optin;
+}
+
+// energies of `batch` rows of theta (device) into e/im (device), async
+void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int batch,
+                   const double* theta_dev, double* e_dev, double* im_dev) {
+  const int n = pl->cp.n_qubits;
+  if (h->ch.n_qubits != n) throw BadInput("plan and Hamiltonian qubit counts differ", FFQ_EINVAL);
+  if (n < 64 && (hf >> n) != 0) throw BadInput("hf_bits exceeds n_qubits", FFQ_EINVAL);
+  if (batch <= 0) return;
+  if (use_smem_path(ctx, pl)) {
+    const size_t sb = smem_bytes(pl);
+    CK(cudaFuncSetAttribute(k_smem_eval<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sb));
+    k_smem_eval<kThreads><<<batch, kThreads, sb, ctx->stream>>>(n, pl->dev(), h->dev(), hf,
+                                                                theta_dev, pl->cp.n_gen, e_dev,
+                                                                im_dev);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
+  // global path: chunk the batch so the slab stays L2-resident (<= 64 MiB)
+  const int64_t dim = 1LL << n;
+  const int64_t slab_cap = (64LL << 20) / (dim * (int64_t)sizeof(double2));
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(batch, std::max<int64_t>(1, slab_cap)));
+  const int n_ops = (int)pl->cp.op_kind.size();
+  const int64_t items = (int64_t)h->ch.item_g.size();
+  ctx->slab.alloc((size_t)chunk * dim);
+  ctx->cs.alloc((size_t)chunk * std::max(1, n_ops));
+  ctx->partial.alloc((size_t)chunk * std::max<int64_t>(1, items));
+  ctx->theta.alloc((size_t)chunk * std::max(1, pl->cp.n_gen));
+  ctx->eout.alloc(chunk);
+  ctx->eim.alloc(chunk);
+  GraphKey key{(uintptr_t)h, (uintptr_t)chunk, (uintptr_t)hf, (uintptr_t)ctx->theta.p,
+               (uintptr_t)ctx->slab.p, (uintptr_t)ctx->cs.p, (uintptr_t)ctx->partial.p,
+               (uintptr_t)ctx->eout.p, (uintptr_t)ctx->eim.p};
+  auto it = pl->graphs.find(key);
+  if (it == pl->graphs.end()) {
+    cudaGraph_t graph;
+    const int64_t before = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      k_set_basis<<<grid_for(dim * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(ctx->slab.p, dim,
+                                                                                 chunk, hf);
+      ctx->launches++;
+      launch_cs(ctx, pl, ctx->theta.p, chunk, ctx->cs.p);
+      run_plan_ops(ctx, pl, ctx->slab.p, chunk, ctx->cs.p);
+      launch_expect(ctx, h, ctx->slab.p, n, chunk, ctx->partial.p, ctx->eout.p, ctx->eim.p);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(ctx->stream, &graph));
+    cudaGraphExec_t exec;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    pl->graph_nodes[key] = ctx->launches - before;
+    ctx->launches = before;
+    it = pl->graphs.emplace(key, exec).first;
+  }
+  const int64_t nodes = pl->graph_nodes[key];
+  for (int b0 = 0; b0 < batch; b0 += chunk) {
+    const int nb = std::min(chunk, batch - b0);
+    CK(cudaMemcpyAsync(ctx->theta.p, theta_dev + (int64_t)b0 * pl->cp.n_gen,
+                       sizeof(double) * (size_t)nb * pl->cp.n_gen, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    // rows past nb in the last chunk recompute stale theta; their outputs are dropped
+    CK(cudaGraphLaunch(it->second, ctx->stream));
+    ctx->launches += nodes;
+    CK(cudaMemcpyAsync(e_dev + b0, ctx->eout.p, sizeof(double) * nb, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    if (im_dev)
+      CK(cudaMemcpyAsync(im_dev + b0, ctx->eim.p, sizeof(double) * nb, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffq_version(void) { return kVersion; }
+
+int ffq_device_count(int* n_out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    if (n_out) *n_out = 0;
+    return fail(nullptr, FFQ_ENODEV, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  if (n_out) *n_out = n;
+  return FFQ_OK;
+}
+
+int ffq_ctx_create(int device, ffq_ctx_t* out) {
+  if (!out) return fail(nullptr, FFQ_EINVAL, "ffq_ctx_create: null out");
+  *out = nullptr;
+  int n = 0;
+  if (ffq_device_count(&n) != FFQ_OK || n == 0)
+    return fail(nullptr, FFQ_ENODEV, "no CUDA device available (the hot path has no CPU fallback)");
+  if (device < 0 || device >= n) return fail(nullptr, FFQ_EINVAL, "device ordinal out of range");
+  auto* c = new ffq_ctx_s();
+  c->device = device;
+  int rc = guarded(c, [&] {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device));
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    c->smem_optin = (size_t)optin - 2048;  // static smem of the reduction scratch
+    if (const char* e = std::getenv("FFQ_SMEM_MAX_QUBITS")) c->smem_max_qubits = std::atoi(e);
+    return FFQ_OK;
+  });
+  if (rc != FFQ_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return FFQ_OK;
+}
+
+int ffq_ctx_destroy(ffq_ctx_t ctx) {
+  if (!ctx) return FFQ_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return FFQ_OK;
+}
+
+int ffq_ctx_synchronize(ffq_ctx_t ctx) {
+  if (!ctx) return fail(nullptr, FFQ_EINVAL, "null context");
+  return guarded(ctx, [&] {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+const char* ffq_last_error(ffq_ctx_t ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
+
+int64_t ffq_ctx_kernel_launches(ffq_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+int ffq_ctx_stream(ffq_ctx_t ctx, void** stream) {
+  if (!ctx || !stream) return fail(ctx, FFQ_EINVAL, "null argument");
+  *stream = (void*)ctx->stream;
+  return FFQ_OK;
+}
+
+int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t* x,
+                   const uint64_t* z, const double* c_re, const double* c_im, ffq_ham_t* out) {
+  if (!ctx || !out || (n_terms > 0 && (!x || !z || !c_re || !c_im)))
+    return fail(ctx, FFQ_EINVAL, "ffq_ham_upload: null argument");
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    auto h = std::make_unique<ffq_ham_s>();
+    h->ctx = ctx;
+    h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im);
+    const auto& ch = h->ch;
+    h->groups.upload(ch.groups, ctx->stream);
+    h->act_bits.upload(ch.act_bits, ctx->stream);
+    h->cls_z.upload(ch.cls_z, ctx->stream);
+    std::vector<double2> f(ch.cls_f.size() / 2);
+    for (size_t i = 0; i < f.size(); ++i) f[i] = make_double2(ch.cls_f[2 * i], ch.cls_f[2 * i + 1]);
+    h->cls_f.upload(f, ctx->stream);
+    h->item_g.upload(ch.item_g, ctx->stream);
+    h->item_p.upload(ch.item_p, ctx->stream);
+    h->item_u0.upload(ch.item_u0, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = h.release();
+    return FFQ_OK;
+  });
+}
+
+int ffq_ham_destroy(ffq_ham_t ham) {
+  if (ham) {
+    cudaSetDevice(ham->ctx->device);
+    delete ham;
+  }
+  return FFQ_OK;
+}
+
+int ffq_ham_info(ffq_ham_t ham, int* n_groups, int64_t* n_terms, int64_t* n_classes) {
+  if (!ham) return fail(nullptr, FFQ_EINVAL, "null Hamiltonian");
+  if (n_groups) *n_groups = (int)ham->ch.groups.size();
+  if (n_terms) *n_terms = ham->ch.n_terms;
+  if (n_classes) *n_classes = ham->ch.n_classes();
+  return FFQ_OK;
+}
+
+int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_off,
+                    const uint64_t* x, const uint64_t* z, const double* c_re, const double* c_im,
+                    ffq_plan_t* out) {
+  if (!ctx || !out || (n_gen > 0 && !term_off)) return fail(ctx, FFQ_EINVAL, "ffq_plan_upload: null argument");
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    if (n_gen > 0 && term_off[n_gen] > 0 && (!x || !z || !c_re || !c_im))
+      throw BadInput("ffq_plan_upload: null term arrays", FFQ_EINVAL);
+    auto p = std::make_unique<ffq_plan_s>();
+    p->ctx = ctx;
+    p->cp = compile_plan(n_qubits, n_gen, term_off, x, z, c_re, c_im);
+    const auto& cp = p->cp;
+    p->op_kind.upload(cp.op_kind, ctx->stream);
+    p->op_gen.upload(cp.op_gen, ctx->stream);
+    p->op_idx.upload(cp.op_idx, ctx->stream);
+    p->op_cfac.upload(cp.op_cfac, ctx->stream);
+    p->op_sscale.upload(cp.op_sscale, ctx->stream);
+    p->fused.upload(cp.fused, ctx->stream);
+    p->pair_bits.upload(cp.pair_bits, ctx->stream);
+    std::vector<double2> pf(cp.pair_f.size() / 2);
+    for (size_t i = 0; i < pf.size(); ++i) pf[i] = make_double2(cp.pair_f[2 * i], cp.pair_f[2 * i + 1]);
+    p->pair_f.upload(pf, ctx->stream);
+    p->str_x.upload(cp.str_x, ctx->stream);
+    p->str_z.upload(cp.str_z, ctx->stream);
+    p->str_ny.upload(cp.str_ny, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = p.release();
+    return FFQ_OK;
+  });
+}
+
+int ffq_plan_destroy(ffq_plan_t plan) {
+  if (plan) {
+    cudaSetDevice(plan->ctx->device);
+    delete plan;
+  }
+  return FFQ_OK;
+}
+
+int ffq_plan_info(ffq_plan_t plan, int* n_fused, int* n_string_ops) {
+  if (!plan) return fail(nullptr, FFQ_EINVAL, "null plan");
+  if (n_fused) *n_fused = plan->cp.n_fused();
+  if (n_string_ops) *n_string_ops = plan->cp.n_string_ops();
+  return FFQ_OK;
+}
+
+int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
+                            int batch, const double* theta_dev, double* e_dev, double* imag_dev) {
+  if (!ctx || !plan || !ham || batch < 0 || (batch > 0 && (!e_dev || (!theta_dev && plan->cp.n_gen > 0))))
+    return fail(ctx, FFQ_EINVAL, "ffq_energy_batch_device: invalid argument");
+  return guarded(ctx, [&] {
+    energy_device(ctx, plan, ham, hf_bits, batch, theta_dev, e_dev, imag_dev);
+    return FFQ_OK;
+  });
+}
+
+int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int batch,
+                     const double* theta, double* e_out) {
+  if (!ctx || !plan || !ham || batch < 0 || (batch > 0 && (!e_out || (!theta && plan->cp.n_gen > 0))))
+    return fail(ctx, FFQ_EINVAL, "ffq_energy_batch: invalid argument");
+  if (batch == 0) return FFQ_OK;
+  return guarded(ctx, [&] {
+    const int ng = plan->cp.n_gen;
+    const size_t nth = (size_t)batch * ng;
+    // host -> pinned staging -> device (one H2D), energies + residues back (one D2H)
+    ctx->ensure_pinned(std::max<size_t>(nth, 2 * (size_t)batch));
+    DevBuf<double>& th = ctx->io_theta;
+    DevBuf<double>& eo = ctx->io_e;
+    th.alloc(std::max<size_t>(1, nth));
+    eo.alloc(2 * (size_t)batch);
+    if (nth) {
+      std::memcpy(ctx->pinned, theta, nth * sizeof(double));
+      CK(cudaMemcpyAsync(th.p, ctx->pinned, nth * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    energy_device(ctx, plan, ham, hf_bits, batch, th.p, eo.p, eo.p + batch);
+    CK(cudaMemcpyAsync(ctx->pinned, eo.p, 2 * sizeof(double) * batch, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(e_out, ctx->pinned, sizeof(double) * batch);
+    for (int b = 0; b < batch; ++b)
+      if (std::abs(ctx->pinned[batch + b]) > 1e-10)
+        throw BadInput("energy has imaginary residue " + std::to_string(ctx->pinned[batch + b]) +
+                           " > 1e-10 (non-Hermitian Hamiltonian?)",
+                       FFQ_ENONHERMITIAN);
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_alloc(ffq_ctx_t ctx, int n_qubits, int batch, ffq_state_t* out) {
+  if (!ctx || !out || n_qubits < 2 || n_qubits > 40 || batch < 1 || batch > 65535)
+    return fail(ctx, FFQ_EINVAL,
+                "ffq_state_alloc: invalid argument (need n_qubits in [2,40], batch in [1,65535])");
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    auto s = std::make_unique<ffq_state_s>();
+    s->ctx = ctx;
+    s->n = n_qubits;
+    s->batch = batch;
+    s->psi.alloc((size_t)batch << n_qubits);
+    *out = s.release();
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_free(ffq_state_t st) {
+  if (st) {
+    cudaSetDevice(st->ctx->device);
+    delete st;
+  }
+  return FFQ_OK;
+}
+
+int ffq_state_set_basis(ffq_state_t st, uint64_t bits) {
+  if (!st) return fail(nullptr, FFQ_EINVAL, "null state");
+  ffq_ctx_t ctx = st->ctx;
+  if (st->n < 64 && (bits >> st->n)) return fail(ctx, FFQ_EINVAL, "basis index exceeds n_qubits");
+  return guarded(ctx, [&] {
+    const int64_t dim = 1LL << st->n;
+    k_set_basis<<<grid_for(dim * st->batch, ctx->n_sm), kThreads, 0, ctx->stream>>>(st->psi.p, dim,
+                                                                                   st->batch, bits);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_upload(ffq_state_t st, const double* psi) {
+  if (!st || !psi) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
+  return guarded(st->ctx, [&] {
+    CK(cudaMemcpyAsync(st->psi.p, psi, sizeof(double2) * ((size_t)st->batch << st->n),
+                       cudaMemcpyHostToDevice, st->ctx->stream));
+    CK(cudaStreamSynchronize(st->ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_download(ffq_state_t st, double* psi) {
+  if (!st || !psi) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
+  return guarded(st->ctx, [&] {
+    CK(cudaMemcpyAsync(psi, st->psi.p, sizeof(double2) * ((size_t)st->batch << st->n),
+                       cudaMemcpyDeviceToHost, st->ctx->stream));
+    CK(cudaStreamSynchronize(st->ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, double theta) {
+  if (!st) return fail(nullptr, FFQ_EINVAL, "null state");
+  ffq_ctx_t ctx = st->ctx;
+  if (st->n < 64 && ((x | z) >> st->n)) return fail(ctx, FFQ_EINVAL, "Pauli string exceeds n_qubits");
+  return guarded(ctx, [&] {
+    std::vector<double2> cs(st->batch, make_double2(std::cos(theta), std::sin(theta)));
+    ctx->cs.upload(cs, ctx->stream);
+    launch_string(ctx, st->psi.p, st->n, st->batch, x, z, __builtin_popcountll(x & z) & 3, ctx->cs.p,
+                  1, 0);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta) {
+  if (!st || !plan || (!theta && plan->cp.n_gen > 0)) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
+  ffq_ctx_t ctx = st->ctx;
+  if (plan->cp.n_qubits != st->n) return fail(ctx, FFQ_EINVAL, "plan and state qubit counts differ");
+  return guarded(ctx, [&] {
+    const int ng = plan->cp.n_gen, n_ops = (int)plan->cp.op_kind.size();
+    if (n_ops == 0) return FFQ_OK;
+    ctx->theta.alloc((size_t)std::max(1, ng) * st->batch);
+    CK(cudaMemcpyAsync(ctx->theta.p, theta, sizeof(double) * (size_t)ng * st->batch,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    ctx->cs.alloc((size_t)n_ops * st->batch);
+    launch_cs(ctx, plan, ctx->theta.p, st->batch, ctx->cs.p);
+    run_plan_ops(ctx, plan, st->psi.p, st->batch, ctx->cs.p);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_expectation(ffq_state_t st, ffq_ham_t ham, double* re_out, double* im_out) {
+  if (!st || !ham || !re_out) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
+  ffq_ctx_t ctx = st->ctx;
+  if (ham->ch.n_qubits != st->n) return fail(ctx, FFQ_EINVAL, "Hamiltonian and state qubit counts differ");
+  return guarded(ctx, [&] {
+    const int64_t items = (int64_t)ham->ch.item_g.size();
+    ctx->partial.alloc((size_t)std::max<int64_t>(1, items) * st->batch);
+    DevBuf<double> eo;
+    eo.alloc(2 * (size_t)st->batch);
+    launch_expect(ctx, ham, st->psi.p, st->n, st->batch, ctx->partial.p, eo.p, eo.p + st->batch);
+    std::vector<double> host(2 * (size_t)st->batch);
+    CK(cudaMemcpyAsync(host.data(), eo.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < st->batch; ++b) {
+      re_out[b] = host[b];
+      if (im_out) im_out[b] = host[st->batch + b];
+    }
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_device_ptr(ffq_state_t st, void** ptr) {
+  if (!st || !ptr) return fail(nullptr, FFQ_EINVAL, "null argument");
+  *ptr = st->psi.p;
+  return FFQ_OK;
+}
+
+int ffq_ham_compile_stats(int n_qubits, int64_t n_terms, const uint64_t* x, const uint64_t* z,
+                          const double* c_re, const double* c_im, int64_t* stats) {
+  if (!stats || (n_terms > 0 && (!x || !z || !c_re || !c_im))) return fail(nullptr, FFQ_EINVAL, "null argument");
+  return guarded(nullptr, [&] {
+    const CompiledHam H = compile_ham(n_qubits, n_terms, x, z, c_re, c_im);
+    int64_t act = 0, visits = 0, cls_evals = 0;
+    for (const auto& d : H.groups) {
+      act += d.nact;
+      const int64_t pairs = (int64_t)d.nact << (n_qubits - d.w);
+      visits += pairs;
+      cls_evals += pairs * d.ncls;
+    }
+    stats[0] = (int64_t)H.groups.size();
+    stats[1] = H.n_terms;
+    stats[2] = H.n_classes();
+    stats[3] = act;
+    stats[4] = (int64_t)H.item_g.size();
+    stats[5] = visits;
+    stats[6] = cls_evals;
+    stats[7] = visits * 2 * (int64_t)sizeof(double2);
+    return FFQ_OK;
+  });
+}
+
+int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* x,
+                           const uint64_t* z, const double* c_re, const double* c_im,
+                           int64_t* stats) {
+  if (!stats || (n_gen > 0 && !term_off)) return fail(nullptr, FFQ_EINVAL, "null argument");
+  return guarded(nullptr, [&] {
+    const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, x, z, c_re, c_im);
+    int64_t pairs = 0, upd = 0, bytes = 0;
+    for (const auto& d : P.fused) {
+      pairs += d.npair;
+      const int64_t u = (int64_t)d.npair << (n_qubits - d.w);
+      upd += u;
+      bytes += u * 4 * (int64_t)sizeof(double2);
+    }
+    const int64_t string_bytes = (int64_t)P.n_string_ops() * (32LL << n_qubits);
+    stats[0] = P.n_fused();
+    stats[1] = P.n_string_ops();
+    stats[2] = pairs;
+    stats[3] = upd + (int64_t)P.n_string_ops() * (1LL << (n_qubits - 1));
+    stats[4] = bytes + string_bytes;
+    stats[5] = (int64_t)P.op_kind.size();
+    return FFQ_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,346 @@
+// ffq_compile.hpp -- host-side compilation of Pauli data into the device
+// tables the kernels stream over. Pure C++ (no CUDA), unit-testable on CPU.
+//
+// Two objects are compiled:
+//  * a Trotter plan: each generator A_g (the JW
+//    image of tau - tau^dag, anti-Hermitian) becomes either ONE fused pass
+//    (all strings share flip mask X, commute, and have a single "outside" Z
+//    class -- true for every UCCSD generator) or a run of single-string
+//    rotations e^{i phi P} in canonical term order (the general fallback).
+//  * a qubit Hamiltonian: terms grouped by flip mask X; in
+//    each group, terms are split into classes by their Z part outside X and
+//    tabulated over the 2^|X| bit patterns of the amplitude index on X, so
+//    the kernel evaluates one popcount per class per amplitude pair and only
+//    visits patterns with a non-zero table entry.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ffq {
+
+using cplx = std::complex<double>;
+constexpr int kMaxTableBits = 6;  // |X| up to 6 -> pattern tables of <= 64 entries
+
+struct BadInput : std::invalid_argument {
+  int code;
+  BadInput(const std::string& w, int c) : std::invalid_argument(w), code(c) {}
+};
+
+inline int popc64(uint64_t v) { return __builtin_popcountll(v); }
+
+// i^k as a complex number
+inline cplx ipow(int k) {
+  switch (k & 3) {
+    case 0: return {1, 0};
+    case 1: return {0, 1};
+    case 2: return {-1, 0};
+    default: return {0, -1};
+  }
+}
+
+// bits of pattern index pi (bit i of pi -> qubit q[i]) as an amplitude mask
+inline uint64_t pattern_bits(uint32_t pi, const int* q, int w) {
+  uint64_t b = 0;
+  for (int i = 0; i < w; ++i)
+    if ((pi >> i) & 1u) b |= 1ULL << q[i];
+  return b;
+}
+
+// ---- plan ------------------------------------------------------------------
+struct FusedDesc {  // POD, copied to the device
+  uint64_t x, zout;
+  int32_t w, npair, pair_off, pad;
+  int32_t q[kMaxTableBits];
+  uint64_t qpack;  // q[i] in bits [6i, 6i+6): register-friendly copy for kernels
+  double alpha;
+};
+
+inline uint64_t pack_q(const int32_t* q, int w) {
+  uint64_t v = 0;
+  for (int i = 0; i < w; ++i) v |= (uint64_t)q[i] << (6 * i);
+  return v;
+}
+
+struct CompiledPlan {
+  int n_qubits = 0, n_gen = 0;
+  // op stream in execution order
+  std::vector<int32_t> op_kind;  // 0 fused, 1 string
+  std::vector<int32_t> op_gen;   // generator index (theta column)
+  std::vector<int32_t> op_idx;   // index into fused[] or str_*[]
+  std::vector<double> op_cfac;   // phi = theta * cfac
+  std::vector<double> op_sscale; // s = sin(phi) * sscale
+  std::vector<FusedDesc> fused;
+  std::vector<uint64_t> pair_bits;  // pattern bits of the "low" member
+  std::vector<double> pair_f;       // [pair][4]: F[pi] re,im, F[~pi] re,im
+  std::vector<uint64_t> str_x, str_z;
+  std::vector<int32_t> str_ny;
+  int n_fused() const { return (int)fused.size(); }
+  int n_string_ops() const { return (int)str_x.size(); }
+};
+
+inline CompiledPlan compile_plan(int n, int n_gen, const int64_t* off, const uint64_t* x,
+                                 const uint64_t* z, const double* cr, const double* ci) {
+  if (n < 1 || n > 40) throw BadInput("plan: n_qubits out of range [1, 40]", -1);
+  if (n_gen < 0) throw BadInput("plan: negative generator count", -1);
+  const uint64_t full = (n == 64) ? ~0ULL : ((1ULL << n) - 1ULL);
+  CompiledPlan P;
+  P.n_qubits = n;
+  P.n_gen = n_gen;
+  for (int g = 0; g < n_gen; ++g) {
+    const int64_t b = off[g], e = off[g + 1];
+    if (e < b) throw BadInput("plan: term_off not monotone", -1);
+    // merge duplicates, canonical order (x, z) ascending
+    std::map<std::pair<uint64_t, uint64_t>, cplx> terms;
+    double scale = 0.0;
+    for (int64_t t = b; t < e; ++t) {
+      if ((x[t] | z[t]) & ~full) throw BadInput("plan: Pauli string exceeds n_qubits", -1);
+      terms[{x[t], z[t]}] += cplx(cr[t], ci[t]);
+      scale = std::max(scale, std::abs(cplx(cr[t], ci[t])));
+    }
+    std::vector<std::pair<std::pair<uint64_t, uint64_t>, cplx>> tl;
+    for (auto& kv : terms)
+      if (std::abs(kv.second) > 1e-14 * std::max(1.0, scale)) tl.push_back(kv);
+    for (auto& kv : tl)
+      if (std::abs(kv.second.real()) > 1e-12)
+        throw BadInput("plan: generator " + std::to_string(g) +
+                           " is not anti-Hermitian (real coefficient)", -1);
+    if (tl.empty()) continue;  // identity rotation
+    // fused eligibility
+    bool fuse = true;
+    const uint64_t X = tl[0].first.first;
+    const int w = popc64(X);
+    if (X == 0 || w > kMaxTableBits) fuse = false;
+    const uint64_t zout = tl[0].first.second & ~X;
+    for (auto& kv : tl) {
+      if (kv.first.first != X || (kv.first.second & ~X) != zout) { fuse = false; break; }
+    }
+    if (fuse) {
+      for (size_t i = 0; i < tl.size() && fuse; ++i)
+        for (size_t j = i + 1; j < tl.size(); ++j)
+          if (popc64(X & (tl[i].first.second ^ tl[j].first.second)) & 1) { fuse = false; break; }
+    }
+    FusedDesc d{};
+    std::vector<cplx> F;
+    if (fuse) {
+      d.x = X; d.zout = zout; d.w = w;
+      int wi = 0;
+      for (int qb = 0; qb < 64; ++qb)
+        if ((X >> qb) & 1ULL) d.q[wi++] = qb;
+      d.qpack = pack_q(d.q, w);
+      const uint32_t np = 1u << w;
+      F.assign(np, cplx(0, 0));
+      // F[pi] = <k^X|A|k> / s_out(k) = sum_j (i c_j) i^{ny_j} (-1)^{popc(pibits & z_j)}
+      for (uint32_t pi = 0; pi < np; ++pi) {
+        const uint64_t pb = pattern_bits(pi, d.q, w);
+        cplx acc(0, 0);
+        for (auto& kv : tl) {
+          const uint64_t zj = kv.first.second;
+          const int ny = popc64(X & zj);
+          const double sg = (popc64(pb & zj) & 1) ? -1.0 : 1.0;
+          acc += kv.second * ipow(ny) * sg;
+        }
+        F[pi] = acc;
+      }
+      double amax = 0;
+      for (auto& f : F) amax = std::max(amax, std::abs(f));
+      const double tol = 1e-12 * std::max(amax, 1e-300);
+      double alpha = 0;
+      for (auto& f : F)
+        if (std::abs(f) > tol) {
+          if (alpha == 0) alpha = std::abs(f);
+          else if (std::abs(std::abs(f) - alpha) > 1e-12 * alpha) { fuse = false; break; }
+        }
+      if (alpha == 0) continue;  // A == 0 on every pattern: identity
+      d.alpha = alpha;
+      if (fuse) {
+        d.pair_off = (int32_t)P.pair_bits.size();
+        for (uint32_t pi = 0; pi < np; ++pi) {
+          const uint32_t pb = pi ^ (np - 1u);
+          if (pi > pb) continue;
+          if (std::abs(F[pi]) <= tol && std::abs(F[pb]) <= tol) continue;
+          P.pair_bits.push_back(pattern_bits(pi, d.q, w));
+          P.pair_f.push_back(F[pi].real()); P.pair_f.push_back(F[pi].imag());
+          P.pair_f.push_back(F[pb].real()); P.pair_f.push_back(F[pb].imag());
+        }
+        d.npair = (int32_t)P.pair_bits.size() - d.pair_off;
+      }
+    }
+    if (fuse) {
+      P.op_kind.push_back(0);
+      P.op_gen.push_back(g);
+      P.op_idx.push_back((int32_t)P.fused.size());
+      P.op_cfac.push_back(d.alpha);
+      P.op_sscale.push_back(1.0 / d.alpha);
+      P.fused.push_back(d);
+    } else {
+      for (auto& kv : tl) {  // canonical order, e^{i theta c_j P_j}
+        P.op_kind.push_back(1);
+        P.op_gen.push_back(g);
+        P.op_idx.push_back((int32_t)P.str_x.size());
+        P.op_cfac.push_back(kv.second.imag());
+        P.op_sscale.push_back(1.0);
+        P.str_x.push_back(kv.first.first);
+        P.str_z.push_back(kv.first.second);
+        P.str_ny.push_back(popc64(kv.first.first & kv.first.second) & 3);
+      }
+    }
+  }
+  return P;
+}
+
+// ---- Hamiltonian -------------------------------------------------------------
+struct GroupDesc {  // POD
+  uint64_t x;
+  int32_t w;        // inserted bits (0 in generic mode)
+  int32_t nact;     // active patterns
+  int32_t act_off;  // into act_bits
+  int32_t cls_off;  // into cls_z
+  int32_t ncls;
+  int32_t val_off;  // into cls_f (complex), layout [cls][nact]
+  int32_t q[kMaxTableBits];
+  uint64_t qpack;
+};
+
+struct CompiledHam {
+  int n_qubits = 0;
+  int64_t n_terms = 0;
+  std::vector<GroupDesc> groups;
+  std::vector<uint64_t> act_bits;
+  std::vector<uint64_t> cls_z;
+  std::vector<double> cls_f;  // interleaved complex
+  // global-path work items (group, active pattern, first u); fixed decomposition
+  int64_t item_chunk = 0;
+  std::vector<int32_t> item_g, item_p;
+  std::vector<int64_t> item_u0;
+  int64_t n_classes() const { return (int64_t)cls_z.size(); }
+};
+
+constexpr int64_t kItemChunk = 4096;
+
+inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint64_t* z,
+                               const double* cr, const double* ci) {
+  if (n < 1 || n > 40) throw BadInput("hamiltonian: n_qubits out of range [1, 40]", -1);
+  const uint64_t full = (1ULL << n) - 1ULL;
+  std::map<uint64_t, std::map<uint64_t, double>> byx;  // x -> z -> real coefficient
+  for (int64_t t = 0; t < nt; ++t) {
+    if ((x[t] | z[t]) & ~full) throw BadInput("hamiltonian: Pauli string exceeds n_qubits", -1);
+    if (std::abs(ci[t]) > 1e-12)
+      throw BadInput("hamiltonian: non-Hermitian term (imaginary coefficient)", -2);
+    byx[x[t]][z[t]] += cr[t];
+  }
+  // Each x-group G = sum_t c_t P_t (c_t real) is Hermitian, so with
+  //   b(m) = sum_t c_t i^{ny_t} (-1)^{popc(m & z_t)},   b(m ^ X) = conj(b(m)),
+  // <G> = sum_m conj(psi[m^X]) psi[m] b(m) visits every unordered pair
+  // {m, m^X} once as 2 Re(conj(psi[m^X]) psi[m] b(m)) (X != 0) and the
+  // diagonal group as |psi[m]|^2 b(m). m runs over the inserted bits Q:
+  //   table mode (|X| <= 6): Q = X, b(m) = sum_o sgn(m & zout_o) F_o[pattern]
+  //   generic mode:          Q = {lowest bit of X}, one class per term.
+  CompiledHam H;
+  H.n_qubits = n;
+  H.n_terms = 0;
+  for (auto& gx : byx) {
+    const uint64_t X = gx.first;
+    std::vector<std::pair<uint64_t, double>> terms;
+    double sabs = 0;
+    for (auto& kv : gx.second)
+      if (kv.second != 0.0) { terms.push_back(kv); sabs += std::abs(kv.second); }
+    if (terms.empty()) continue;
+    H.n_terms += (int64_t)terms.size();
+    GroupDesc d{};
+    d.x = X;
+    const int w = popc64(X);
+    const double wgt = (X == 0) ? 1.0 : 2.0;
+    d.cls_off = (int32_t)H.cls_z.size();
+    d.val_off = (int32_t)(H.cls_f.size() / 2);
+    d.act_off = (int32_t)H.act_bits.size();
+    if (w <= kMaxTableBits) {
+      d.w = w;
+      int wi = 0;
+      for (int qb = 0; qb < 64; ++qb)
+        if ((X >> qb) & 1ULL) d.q[wi++] = qb;
+      d.qpack = pack_q(d.q, w);
+      const uint32_t np = 1u << w;
+      std::map<uint64_t, std::vector<std::pair<uint64_t, double>>> cls;  // by z outside X
+      for (auto& t : terms) cls[t.first & ~X].push_back(t);
+      std::vector<std::vector<cplx>> tab;
+      for (auto& c : cls) {
+        std::vector<cplx> F(np, cplx(0, 0));
+        for (uint32_t pi = 0; pi < np; ++pi) {
+          const uint64_t pb = pattern_bits(pi, d.q, w);
+          cplx acc(0, 0);
+          for (auto& t : c.second) {
+            const int ny = popc64(X & t.first);
+            const double sg = (popc64(pb & t.first) & 1) ? -1.0 : 1.0;
+            acc += t.second * sg * ipow(ny);
+          }
+          F[pi] = acc;
+        }
+        tab.push_back(F);
+      }
+      // rounding-level residues of exact cancellations are dropped
+      const double tol = 64.0 * 2.220446049250313e-16 * sabs;
+      std::vector<uint32_t> act;  // lower member of each active pattern pair
+      for (uint32_t pi = 0; pi < np; ++pi) {
+        const uint32_t pb = pi ^ (np - 1u);
+        if (X != 0 && pi > pb) continue;
+        bool any = false;
+        for (auto& F : tab) any |= std::abs(F[pi]) > tol || std::abs(F[pb]) > tol;
+        if (any) act.push_back(pi);
+      }
+      if (act.empty()) continue;
+      d.nact = (int32_t)act.size();
+      for (uint32_t pi : act) H.act_bits.push_back(pattern_bits(pi, d.q, w));
+      int ci2 = 0;
+      for (auto& c : cls) {
+        bool used = false;
+        for (uint32_t pi : act) used |= std::abs(tab[ci2][pi]) > tol;
+        if (used) {
+          H.cls_z.push_back(c.first);
+          for (uint32_t pi : act) {
+            const cplx f = std::abs(tab[ci2][pi]) > tol ? wgt * tab[ci2][pi] : cplx(0, 0);
+            H.cls_f.push_back(f.real());
+            H.cls_f.push_back(f.imag());
+          }
+        }
+        ++ci2;
+      }
+    } else {
+      d.w = 1;
+      d.q[0] = __builtin_ctzll(X);
+      d.qpack = pack_q(d.q, 1);
+      d.nact = 1;
+      H.act_bits.push_back(0);
+      const uint64_t keep = ~(1ULL << d.q[0]);
+      for (auto& t : terms) {
+        const cplx f = wgt * t.second * ipow(popc64(X & t.first));
+        H.cls_z.push_back(t.first & keep);
+        H.cls_f.push_back(f.real());
+        H.cls_f.push_back(f.imag());
+      }
+    }
+    d.ncls = (int32_t)H.cls_z.size() - d.cls_off;
+    H.groups.push_back(d);
+  }
+  // fixed work decomposition for the global (large-state) path
+  H.item_chunk = kItemChunk;
+  for (size_t g = 0; g < H.groups.size(); ++g) {
+    const auto& d = H.groups[g];
+    const int64_t U = 1LL << (n - d.w);
+    for (int p = 0; p < d.nact; ++p)
+      for (int64_t u0 = 0; u0 < U; u0 += kItemChunk) {
+        H.item_g.push_back((int32_t)g);
+        H.item_p.push_back(p);
+        H.item_u0.push_back(u0);
+      }
+  }
+  return H;
+}
+
+}  // namespace ffq

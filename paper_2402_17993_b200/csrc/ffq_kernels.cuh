@@ -1,0 +1,417 @@
+// ffq_kernels.cuh -- sm_100a kernels of the UCCSD state-vector hot path.
+//
+// State layout in HBM: [batch][2^n] complex128 (double2), natural binary
+// order, qubit 0 = LSB. Every kernel is an HBM/L2 stream over
+// amplitude pairs (k, k ^ X); none uses tensor cores (north_star).
+//
+//   k_pauli_rotation  e^{i phi P} on one string: 32-byte vector loads of two
+//                     neighbouring amplitudes (ld.global.v4.f64), one pass of
+//                     32 * 2^n bytes -- the "rotation pass" of the roofline.
+//   k_fused_gen       one UCCSD generator exp(theta (tau - tau^dag)) as an
+//                     exact rotation over the active bit patterns of X only
+//                     (1/8 of the state for a double, 1/2 for a single).
+//   k_expect_items    <psi|H|psi> over (group, pattern, chunk) work items;
+//                     each amplitude pair read once per x-group; block
+//                     partials in fixed slots -> k_reduce_partials (fixed tree).
+//   k_smem_eval       n <= 13: one CTA per energy evaluation, state resident
+//                     in shared memory from HF build to the final reduction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ffq_compile.hpp"
+
+namespace ffq {
+
+struct PlanDev {
+  int n_ops;
+  const int32_t* op_kind;
+  const int32_t* op_gen;
+  const int32_t* op_idx;
+  const double* op_cfac;
+  const double* op_sscale;
+  const FusedDesc* fused;
+  const uint64_t* pair_bits;
+  const double2* pair_f;  // [pair][2]: F[pi], F[~pi]
+  const uint64_t* str_x;
+  const uint64_t* str_z;
+  const int32_t* str_ny;
+};
+
+struct HamDev {
+  int n_groups;
+  const GroupDesc* groups;
+  const uint64_t* act_bits;
+  const uint64_t* cls_z;
+  const double2* cls_f;
+  int64_t n_items;
+  const int32_t* item_g;
+  const int32_t* item_p;
+  const int64_t* item_u0;
+  int64_t item_chunk;
+};
+
+// ---- small helpers -----------------------------------------------------------
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cfma(double s, double2 a, double2 acc) {
+  return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
+// i^k
+__device__ __forceinline__ double2 ipow_d(int k) {
+  k &= 3;
+  return make_double2(k == 0 ? 1.0 : (k == 2 ? -1.0 : 0.0), k == 1 ? 1.0 : (k == 3 ? -1.0 : 0.0));
+}
+// insert zero bits at the ascending positions packed 6 bits apiece in qpack
+template <typename I>
+__device__ __forceinline__ I insert_bits(I u, uint64_t qpack, int w) {
+  for (int i = 0; i < w; ++i) {
+    const int b = (int)((qpack >> (6 * i)) & 63u);
+    u = ((u >> b) << (b + 1)) | (u & ((I(1) << b) - I(1)));
+  }
+  return u;
+}
+template <typename I>
+__device__ __forceinline__ I insert_zero(I u, int b) {
+  return ((u >> b) << (b + 1)) | (u & ((I(1) << b) - I(1)));
+}
+__device__ __forceinline__ double sgn_par(uint64_t v) { return (__popcll(v) & 1) ? -1.0 : 1.0; }
+
+// 32-byte vector access (two complex128 amplitudes): LDG.E.ENL2.256 on sm_100a
+__device__ __forceinline__ void ld256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x),
+               "d"(b.y)
+               : "memory");
+}
+
+// ---- per-op rotation coefficients: cs[b][op] = (cos phi, sin phi * sscale) --
+__global__ void k_op_cs(const double* __restrict__ theta, int theta_stride, int n_ops,
+                        const int32_t* __restrict__ op_gen, const double* __restrict__ op_cfac,
+                        const double* __restrict__ op_sscale, double2* __restrict__ cs, int batch) {
+  const int64_t total = (int64_t)n_ops * batch;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t / n_ops), op = (int)(t % n_ops);
+    const double phi = theta[(int64_t)b * theta_stride + op_gen[op]] * op_cfac[op];
+    double s, c;
+    sincos(phi, &s, &c);
+    cs[t] = make_double2(c, s * op_sscale[op]);
+  }
+}
+
+// ---- basis state -------------------------------------------------------------
+__global__ void k_set_basis(double2* __restrict__ psi, int64_t dim, int batch, uint64_t bits) {
+  const int64_t total = dim * batch;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t % dim;
+    psi[t] = make_double2(k == (int64_t)bits ? 1.0 : 0.0, 0.0);
+  }
+}
+
+// ---- single Pauli-string rotation e^{i phi P} --------------------------------
+// new[k]  = c a + s w sgn(k') b,  new[k'] = c b + s w sgn(k) a,  w = i * i^{ny}
+// mode 0: x == 0 (diagonal phase), mode 1: bit 0 of x clear, mode 2: x == 1,
+// mode 3: bit 0 of x set with other bits. Each thread owns one 32-byte vector
+// pair so every global access is a full LDG/STG.256.
+__global__ void __launch_bounds__(256) k_pauli_rotation(double2* __restrict__ psi, int n,
+                                                        uint64_t x, uint64_t z, int ny,
+                                                        const double2* __restrict__ cs,
+                                                        int cs_stride, int op, int mode,
+                                                        int hbit) {
+  const int b = blockIdx.y;
+  double2* s = psi + ((int64_t)b << n);
+  const double2 csv = cs[(int64_t)b * cs_stride + op];
+  const double c = csv.x, sn = csv.y;
+  const double2 w = ipow_d(ny + 1);
+  const int64_t nvec = (mode == 0 || mode == 2) ? (1LL << (n - 1)) : (1LL << (n - 2));
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nvec;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (mode == 0) {
+      const uint64_t k = (uint64_t)t << 1;
+      double2 a0, a1;
+      ld256(s + k, a0, a1);
+      // (c + i s sgn) a
+      const double s0 = sn * sgn_par(k & z), s1 = sn * sgn_par((k + 1) & z);
+      const double2 r0 = make_double2(c * a0.x - s0 * a0.y, c * a0.y + s0 * a0.x);
+      const double2 r1 = make_double2(c * a1.x - s1 * a1.y, c * a1.y + s1 * a1.x);
+      st256(s + k, r0, r1);
+    } else if (mode == 1) {
+      const uint64_t k = insert_zero<uint64_t>((uint64_t)t << 1, hbit);  // even, bit h clear
+      const uint64_t kp = k ^ x;
+      double2 a0, a1, b0, b1;
+      ld256(s + k, a0, a1);
+      ld256(s + kp, b0, b1);
+      const double sk0 = sn * sgn_par(k & z), sk1 = sn * sgn_par((k + 1) & z);
+      const double sp0 = sn * sgn_par(kp & z), sp1 = sn * sgn_par((kp + 1) & z);
+      const double2 wb0 = cmul(w, b0), wb1 = cmul(w, b1), wa0 = cmul(w, a0), wa1 = cmul(w, a1);
+      const double2 na0 = make_double2(c * a0.x + sp0 * wb0.x, c * a0.y + sp0 * wb0.y);
+      const double2 na1 = make_double2(c * a1.x + sp1 * wb1.x, c * a1.y + sp1 * wb1.y);
+      const double2 nb0 = make_double2(c * b0.x + sk0 * wa0.x, c * b0.y + sk0 * wa0.y);
+      const double2 nb1 = make_double2(c * b1.x + sk1 * wa1.x, c * b1.y + sk1 * wa1.y);
+      st256(s + k, na0, na1);
+      st256(s + kp, nb0, nb1);
+    } else if (mode == 2) {
+      const uint64_t k = (uint64_t)t << 1;  // pair (k, k+1) inside one vector
+      double2 a, bb;
+      ld256(s + k, a, bb);
+      const double sk = sn * sgn_par(k & z), sp = sn * sgn_par((k + 1) & z);
+      const double2 wb = cmul(w, bb), wa = cmul(w, a);
+      const double2 na = make_double2(c * a.x + sp * wb.x, c * a.y + sp * wb.y);
+      const double2 nb = make_double2(c * bb.x + sk * wa.x, c * bb.y + sk * wa.y);
+      st256(s + k, na, nb);
+    } else {
+      // k even with bit h' (lowest bit of x & ~1) clear; j = k ^ (x & ~1)
+      // pairs: (k, j+1) and (k+1, j)
+      const uint64_t k = insert_zero<uint64_t>((uint64_t)t << 1, hbit);
+      const uint64_t j = k ^ (x & ~1ULL);
+      double2 a0, a1, b0, b1;
+      ld256(s + k, a0, a1);
+      ld256(s + j, b0, b1);
+      // pair (k, j+1): a = a0, b = b1
+      const double sA_k = sn * sgn_par(k & z), sA_p = sn * sgn_par((j + 1) & z);
+      // pair (k+1, j): a = a1, b = b0
+      const double sB_k = sn * sgn_par((k + 1) & z), sB_p = sn * sgn_par(j & z);
+      const double2 wb1 = cmul(w, b1), wa0 = cmul(w, a0), wb0 = cmul(w, b0), wa1 = cmul(w, a1);
+      const double2 na0 = make_double2(c * a0.x + sA_p * wb1.x, c * a0.y + sA_p * wb1.y);
+      const double2 nb1 = make_double2(c * b1.x + sA_k * wa0.x, c * b1.y + sA_k * wa0.y);
+      const double2 na1 = make_double2(c * a1.x + sB_p * wb0.x, c * a1.y + sB_p * wb0.y);
+      const double2 nb0 = make_double2(c * b0.x + sB_k * wa1.x, c * b0.y + sB_k * wa1.y);
+      st256(s + k, na0, na1);
+      st256(s + j, nb0, nb1);
+    }
+  }
+}
+
+// ---- fused generator: exp(theta A) on the active patterns of X ----------------
+// pair (k, kb = k ^ X), k = insert(u) | bits(pi_lo):
+//   new[k]  = c a + s' sgn_out(k) F[pi_hi] b,  new[kb] = c b + s' sgn_out(k) F[pi_lo] a
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_fused_gen(double2* __restrict__ psi, int n, FusedDesc d,
+                                                   const uint64_t* __restrict__ pair_bits,
+                                                   const double2* __restrict__ pair_f,
+                                                   const double2* __restrict__ cs, int cs_stride,
+                                                   int op) {
+  const int b = blockIdx.y;
+  double2* s = psi + ((int64_t)b << n);
+  const double2 csv = cs[(int64_t)b * cs_stride + op];
+  const double c = csv.x, sn = csv.y;
+  const int ub = n - d.w;
+  const int64_t per_pair = VEC ? (1LL << (ub - 1)) : (1LL << ub);
+  const int64_t total = per_pair * d.npair;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(t / per_pair);
+    const int64_t u = t - (int64_t)p * per_pair;
+    const uint64_t pb = pair_bits[d.pair_off + p];
+    const double2 flo = pair_f[2 * (d.pair_off + p)], fhi = pair_f[2 * (d.pair_off + p) + 1];
+    if (VEC) {
+      const uint64_t k = insert_bits<uint64_t>((uint64_t)u << 1, d.qpack, d.w) | pb;
+      const uint64_t kb = k ^ d.x;
+      double2 a0, a1, b0, b1;
+      ld256(s + k, a0, a1);
+      ld256(s + kb, b0, b1);
+      const double g0 = sn * sgn_par(k & d.zout), g1 = sn * sgn_par((k + 1) & d.zout);
+      const double2 hb0 = cmul(fhi, b0), hb1 = cmul(fhi, b1);
+      const double2 la0 = cmul(flo, a0), la1 = cmul(flo, a1);
+      st256(s + k, make_double2(c * a0.x + g0 * hb0.x, c * a0.y + g0 * hb0.y),
+            make_double2(c * a1.x + g1 * hb1.x, c * a1.y + g1 * hb1.y));
+      st256(s + kb, make_double2(c * b0.x + g0 * la0.x, c * b0.y + g0 * la0.y),
+            make_double2(c * b1.x + g1 * la1.x, c * b1.y + g1 * la1.y));
+    } else {
+      const uint64_t k = insert_bits<uint64_t>((uint64_t)u, d.qpack, d.w) | pb;
+      const uint64_t kb = k ^ d.x;
+      const double2 a = s[k], bb = s[kb];
+      const double g = sn * sgn_par(k & d.zout);
+      const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
+      s[k] = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
+      s[kb] = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
+    }
+  }
+}
+
+// ---- block reduction with a fixed tree (deterministic) -----------------------
+template <int NT>
+__device__ __forceinline__ double2 block_sum(double2 v, double2* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < NT / 32 ? sh[lane] : make_double2(0, 0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+      v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+    }
+  }
+  return v;  // valid in thread 0
+}
+
+// ---- expectation over work items ---------------------------------------------
+// partial[b][item] = sum_{u in item} Re(conj(psi[m ^ X]) psi[m] sum_o sgn(m & z_o) F[o][p]);
+// the imaginary lane stays 0 (Hermitian groups are enforced at upload)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_expect_items(const double2* __restrict__ psi, int n,
+                                                     HamDev h, double2* __restrict__ partial) {
+  __shared__ double2 red[NT / 32];
+  const int64_t item = blockIdx.x;
+  const int b = blockIdx.y;
+  const double2* s = psi + ((int64_t)b << n);
+  const int g = h.item_g[item], p = h.item_p[item];
+  const int64_t u0 = h.item_u0[item];
+  const GroupDesc d = h.groups[g];
+  const int64_t U = 1LL << (n - d.w);
+  const int64_t u1 = min(U, u0 + h.item_chunk);
+  const uint64_t pb = h.act_bits[d.act_off + p];
+  double2 acc = make_double2(0, 0);
+  for (int64_t u = u0 + threadIdx.x; u < u1; u += NT) {
+    const uint64_t m = insert_bits<uint64_t>((uint64_t)u, d.qpack, d.w) | pb;
+    const double2 a = s[m], bb = s[m ^ d.x];
+    double2 f = make_double2(0, 0);
+    for (int o = 0; o < d.ncls; ++o) {
+      const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);
+      const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
+      f.x = fma(sg, fo.x, f.x);
+      f.y = fma(sg, fo.y, f.y);
+    }
+    // Re(conj(bb) * a * f); the weight 2 of off-diagonal pairs is folded into F
+    const double2 pr = make_double2(bb.x * a.x + bb.y * a.y, bb.x * a.y - bb.y * a.x);
+    acc.x = fma(pr.x, f.x, acc.x);
+    acc.x = fma(-pr.y, f.y, acc.x);
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)b * gridDim.x + item] = acc;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_reduce_partials(const double2* __restrict__ partial,
+                                                        int64_t n_items,
+                                                        double* __restrict__ e_out,
+                                                        double* __restrict__ im_out) {
+  __shared__ double2 red[NT / 32];
+  const int b = blockIdx.x;
+  const double2* pp = partial + (int64_t)b * n_items;
+  double2 acc = make_double2(0, 0);
+  for (int64_t i = threadIdx.x; i < n_items; i += NT) {
+    acc.x += pp[i].x;
+    acc.y += pp[i].y;
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) {
+    e_out[b] = acc.x;
+    if (im_out) im_out[b] = acc.y;
+  }
+}
+
+// ---- shared-memory-resident evaluator (n <= 13) ------------------------------
+// One CTA per evaluation: HF build, every plan op, and the grouped expectation
+// run on the smem copy of the state; the only HBM traffic is theta in and E out.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_smem_eval(int n, PlanDev pl, HamDev h, uint64_t hf_bits,
+                                                  const double* __restrict__ theta,
+                                                  int theta_stride, double* __restrict__ e_out,
+                                                  double* __restrict__ im_out) {
+  extern __shared__ double2 sm[];
+  __shared__ double2 red[NT / 32];
+  const int b = blockIdx.x;
+  const uint32_t dim = 1u << n;
+  double2* st = sm;                 // [dim]
+  double2* cs = sm + dim;           // [n_ops]
+  for (uint32_t k = threadIdx.x; k < dim; k += NT)
+    st[k] = make_double2(k == (uint32_t)hf_bits ? 1.0 : 0.0, 0.0);
+  for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
+    const double phi = theta[(int64_t)b * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
+    double s, c;
+    sincos(phi, &s, &c);
+    cs[op] = make_double2(c, s * pl.op_sscale[op]);
+  }
+  __syncthreads();
+  for (int op = 0; op < pl.n_ops; ++op) {
+    const double2 csv = cs[op];
+    const double c = csv.x, sn = csv.y;
+    if (pl.op_kind[op] == 0) {
+      const FusedDesc d = pl.fused[pl.op_idx[op]];
+      const int w = d.w;
+      const uint64_t X = d.x, zo = d.zout;
+      const int ub = n - w;
+      const uint32_t total = (uint32_t)d.npair << ub;
+      for (uint32_t t = threadIdx.x; t < total; t += NT) {
+        const int p = (int)(t >> ub);
+        const uint32_t u = t & ((1u << ub) - 1u);
+        const uint32_t k = insert_bits<uint32_t>(u, d.qpack, w) | (uint32_t)pl.pair_bits[d.pair_off + p];
+        const uint32_t kb = k ^ (uint32_t)X;
+        const double2 flo = pl.pair_f[2 * (d.pair_off + p)], fhi = pl.pair_f[2 * (d.pair_off + p) + 1];
+        const double2 a = st[k], bb = st[kb];
+        const double g = sn * sgn_par(k & zo);
+        const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
+        st[k] = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
+        st[kb] = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
+      }
+    } else {
+      const int si = pl.op_idx[op];
+      const uint32_t x = (uint32_t)pl.str_x[si], z = (uint32_t)pl.str_z[si];
+      const double2 w = ipow_d(pl.str_ny[si] + 1);
+      if (x == 0) {
+        for (uint32_t k = threadIdx.x; k < dim; k += NT) {
+          const double2 a = st[k];
+          const double sg = sn * sgn_par(k & z);
+          st[k] = make_double2(c * a.x - sg * a.y, c * a.y + sg * a.x);
+        }
+      } else {
+        const int hb = __ffs(x) - 1;
+        for (uint32_t t = threadIdx.x; t < dim / 2; t += NT) {
+          const uint32_t k = insert_zero<uint32_t>(t, hb), kp = k ^ x;
+          const double2 a = st[k], bb = st[kp];
+          const double sk = sn * sgn_par(k & z), sp = sn * sgn_par(kp & z);
+          const double2 wb = cmul(w, bb), wa = cmul(w, a);
+          st[k] = make_double2(c * a.x + sp * wb.x, c * a.y + sp * wb.y);
+          st[kp] = make_double2(c * bb.x + sk * wa.x, c * bb.y + sk * wa.y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // grouped expectation, fixed per-thread order
+  double2 acc = make_double2(0, 0);
+  for (int g = 0; g < h.n_groups; ++g) {
+    const GroupDesc d = h.groups[g];
+    const uint32_t X = (uint32_t)d.x;
+    const int ub = n - d.w;
+    const uint32_t total = (uint32_t)d.nact << ub;
+    for (uint32_t t = threadIdx.x; t < total; t += NT) {
+      const int p = (int)(t >> ub);
+      const uint32_t u = t & ((1u << ub) - 1u);
+      const uint32_t m = insert_bits<uint32_t>(u, d.qpack, d.w) | (uint32_t)h.act_bits[d.act_off + p];
+      const double2 a = st[m], bb = st[m ^ X];
+      double2 f = make_double2(0, 0);
+      for (int o = 0; o < d.ncls; ++o) {
+        const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);
+        const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
+        f.x = fma(sg, fo.x, f.x);
+        f.y = fma(sg, fo.y, f.y);
+      }
+      const double2 pr = make_double2(bb.x * a.x + bb.y * a.y, bb.x * a.y - bb.y * a.x);
+      acc.x = fma(pr.x, f.x, acc.x);
+      acc.x = fma(-pr.y, f.y, acc.x);
+    }
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) {
+    e_out[b] = acc.x;
+    if (im_out) im_out[b] = acc.y;
+  }
+}
+
+}  // namespace ffq

@@ -1,0 +1,807 @@
+// fragfield_host.cpp -- host side of the operator API (include/fragfield/*.hpp):
+// Pauli algebra + Jordan-Wigner, synthetic Hamiltonians
+// (BASELINE.json configs), UCCSD generators and magnitude
+// ordering, the device facade over fragfield_cuda.h,
+// optimizers and the FMO two-body assembly
+// (reference proj/core/src/fmo.cpp:28-48).
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <random>
+#include <sstream>
+#include <string>
+
+#include "fragfield/errors.hpp"
+#include "fragfield/fmo_batch.hpp"
+#include "fragfield/hamiltonian.hpp"
+#include "fragfield/pauli.hpp"
+#include "fragfield/statevector.hpp"
+#include "fragfield/uccsd.hpp"
+#include "fragfield/vqe.hpp"
+
+namespace fragfield {
+
+namespace {
+inline int popc(uint64_t v) { return __builtin_popcountll(v); }
+inline Complex ipow(int k) {
+  switch (k & 3) {
+    case 0: return {1, 0};
+    case 1: return {0, 1};
+    case 2: return {-1, 0};
+    default: return {0, -1};
+  }
+}
+inline uint64_t below(int p) { return p > 0 ? ((1ULL << p) - 1ULL) : 0ULL; }
+
+// value mapping of the pinned RNG
+inline double u01(std::mt19937_64& g) { return (double)(g() >> 11) * (1.0 / 9007199254740992.0); }
+inline double normal01(std::mt19937_64& g) {
+  const double u1 = u01(g);
+  const double u2 = u01(g);
+  return std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+}
+}  // namespace
+
+// ---- Pauli algebra -------------------------------------------------------------
+std::string PauliString::letters() const {
+  std::string s(n_qubits, 'I');
+  for (int q = 0; q < n_qubits; ++q) {
+    const bool xb = (x >> q) & 1ULL, zb = (z >> q) & 1ULL;
+    s[q] = xb && zb ? 'Y' : xb ? 'X' : zb ? 'Z' : 'I';
+  }
+  return s;
+}
+
+PauliString PauliString::parse(const std::string& letters) {
+  PauliString p;
+  p.n_qubits = (int)letters.size();
+  if (p.n_qubits > 64) throw ContractViolation("PauliString: more than 64 qubits");
+  for (int q = 0; q < p.n_qubits; ++q) {
+    switch (letters[q]) {
+      case 'I': break;
+      case 'X': p.x |= 1ULL << q; break;
+      case 'Y': p.x |= 1ULL << q; p.z |= 1ULL << q; break;
+      case 'Z': p.z |= 1ULL << q; break;
+      default: throw ContractViolation(std::string("PauliString: bad letter '") + letters[q] + "'");
+    }
+  }
+  return p;
+}
+
+// P(x,z) = i^{popc(x&z)} X^x Z^z;  P1 P2 = i^{y1+y2+2 popc(z1&x2)-y3} P3
+std::pair<int, PauliString> pauli_mul(const PauliString& a, const PauliString& b) {
+  if (a.n_qubits != b.n_qubits) throw ContractViolation("pauli_mul: mismatched n_qubits");
+  PauliString c;
+  c.n_qubits = a.n_qubits;
+  c.x = a.x ^ b.x;
+  c.z = a.z ^ b.z;
+  const int k = popc(a.x & a.z) + popc(b.x & b.z) + 2 * popc(a.z & b.x) - popc(c.x & c.z);
+  return {((k % 4) + 4) % 4, c};
+}
+
+void PauliSum::add(uint64_t x, uint64_t z, Complex c) {
+  if (n_ < 64 && ((x | z) >> n_)) throw ContractViolation("PauliSum: string exceeds n_qubits");
+  terms_[{x, z}] += c;
+}
+
+void PauliSum::simplify(double tol) {
+  for (auto it = terms_.begin(); it != terms_.end();) {
+    if (std::abs(it->second) <= tol) it = terms_.erase(it);
+    else ++it;
+  }
+}
+
+PauliSum PauliSum::operator+(const PauliSum& o) const {
+  if (o.n_ != n_) throw ContractViolation("PauliSum +: mismatched n_qubits");
+  PauliSum r = *this;
+  for (auto& kv : o.terms_) r.terms_[kv.first] += kv.second;
+  r.simplify();
+  return r;
+}
+
+PauliSum PauliSum::operator*(const PauliSum& o) const {
+  if (o.n_ != n_) throw ContractViolation("PauliSum *: mismatched n_qubits");
+  PauliSum r(n_);
+  for (auto& a : terms_)
+    for (auto& b : o.terms_) {
+      auto pr = pauli_mul(PauliString{n_, a.first.first, a.first.second},
+                          PauliString{n_, b.first.first, b.first.second});
+      r.terms_[{pr.second.x, pr.second.z}] += a.second * b.second * ipow(pr.first);
+    }
+  r.simplify();
+  return r;
+}
+
+PauliSum PauliSum::scaled(Complex s) const {
+  PauliSum r = *this;
+  for (auto& kv : r.terms_) kv.second *= s;
+  return r;
+}
+
+void PauliSum::flatten(std::vector<uint64_t>& x, std::vector<uint64_t>& z, std::vector<double>& re,
+                       std::vector<double>& im) const {
+  for (auto& kv : terms_) {
+    x.push_back(kv.first.first);
+    z.push_back(kv.first.second);
+    re.push_back(kv.second.real());
+    im.push_back(kv.second.imag());
+  }
+}
+
+std::string PauliSum::to_text() const {
+  std::ostringstream os;
+  os.precision(17);
+  for (auto& kv : terms_)
+    os << kv.second.real() << ' ' << kv.second.imag() << ' '
+       << PauliString{n_, kv.first.first, kv.first.second}.letters() << '\n';
+  return os.str();
+}
+
+PauliSum PauliSum::from_text(const std::string& text) {
+  std::istringstream is(text);
+  std::string line;
+  PauliSum r(0);
+  bool first = true;
+  while (std::getline(is, line)) {
+    if (line.empty()) continue;
+    std::istringstream ls(line);
+    double re, im;
+    std::string letters;
+    if (!(ls >> re >> im >> letters)) throw ContractViolation("PauliSum::from_text: malformed line");
+    PauliString p = PauliString::parse(letters);
+    if (first) { r = PauliSum(p.n_qubits); first = false; }
+    if (p.n_qubits != r.n_) throw ContractViolation("PauliSum::from_text: mixed qubit counts");
+    r.add(p, Complex(re, im));
+  }
+  r.simplify();
+  return r;
+}
+
+bool PauliSum::is_hermitian(double tol) const {
+  for (auto& kv : terms_)
+    if (std::abs(kv.second.imag()) > tol) return false;
+  return true;
+}
+bool PauliSum::is_antihermitian(double tol) const {
+  for (auto& kv : terms_)
+    if (std::abs(kv.second.real()) > tol) return false;
+  return true;
+}
+
+PauliSum jordan_wigner_ladder(const LadderOp& op, int n_so) {
+  if (op.index < 0 || op.index >= n_so || n_so > 64)
+    throw ContractViolation("jordan_wigner: index out of range");
+  PauliSum s(n_so);
+  const int p = op.index;
+  s.add(1ULL << p, below(p), Complex(0.5, 0.0));                              // X_p Z_<p
+  s.add(1ULL << p, below(p) | (1ULL << p), Complex(0.0, op.dagger ? -0.5 : 0.5));  // Y_p Z_<p
+  return s;
+}
+
+PauliSum jordan_wigner(const FermionOperator& op, int n_so) {
+  PauliSum total(n_so);
+  for (auto& t : op) {
+    PauliSum prod(n_so);
+    prod.add(0, 0, t.coef);
+    for (auto& l : t.ops) prod = prod * jordan_wigner_ladder(l, n_so);
+    for (auto& kv : prod.terms()) total.add(kv.first.first, kv.first.second, kv.second);
+  }
+  total.simplify();
+  return total;
+}
+
+// ---- Hamiltonians --------------------------------------------------------------
+SpatialIntegrals synthetic_integrals(int m, uint64_t seed, double sigma_h, double sigma_g) {
+  if (m < 1 || m > 32) throw ContractViolation("synthetic_integrals: m out of range");
+  SpatialIntegrals I;
+  I.m = m;
+  I.h.assign((size_t)m * m, 0.0);
+  I.g.assign((size_t)m * m * m * m, 0.0);
+  std::mt19937_64 gen(seed);
+  for (int p = 0; p < m; ++p)
+    for (int q = 0; q <= p; ++q) {
+      const double v = sigma_h * normal01(gen);
+      I.h[(size_t)p * m + q] = v;
+      I.h[(size_t)q * m + p] = v;
+    }
+  auto G = [&](int a, int b, int c, int d) -> double& {
+    return I.g[(((size_t)a * m + b) * m + c) * m + d];
+  };
+  for (int p = 0; p < m; ++p)
+    for (int q = 0; q <= p; ++q)
+      for (int r = 0; r <= p; ++r) {
+        const int smax = (r == p) ? q : r;
+        for (int s = 0; s <= smax; ++s) {
+          const double v = sigma_g * normal01(gen);
+          G(p, q, r, s) = v; G(q, p, r, s) = v; G(p, q, s, r) = v; G(q, p, s, r) = v;
+          G(r, s, p, q) = v; G(s, r, p, q) = v; G(r, s, q, p) = v; G(s, r, q, p) = v;
+        }
+      }
+  return I;
+}
+
+std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double hi) {
+  std::mt19937_64 gen(seed);
+  std::vector<double> v((size_t)std::max(0, count));
+  for (auto& e : v) e = lo + (hi - lo) * u01(gen);
+  return v;
+}
+
+SpinOrbitalHamiltonian to_spin_orbitals(const SpatialIntegrals& I, int n_elec) {
+  const int m = I.m, n = 2 * m;
+  if (n_elec < 0 || n_elec > n) throw ContractViolation("to_spin_orbitals: bad electron count");
+  SpinOrbitalHamiltonian H;
+  H.n_so = n;
+  H.n_elec = n_elec;
+  H.e_const = I.e_const;
+  H.h.assign((size_t)n * n, 0.0);
+  H.g.assign((size_t)n * n * n * n, 0.0);
+  for (int p = 0; p < n; ++p)
+    for (int q = 0; q < n; ++q)
+      if ((p & 1) == (q & 1)) H.h[(size_t)p * n + q] = I.h[(size_t)(p >> 1) * m + (q >> 1)];
+  for (int p = 0; p < n; ++p)
+    for (int q = 0; q < n; ++q)
+      for (int r = 0; r < n; ++r)
+        for (int s = 0; s < n; ++s)
+          if ((p & 1) == (r & 1) && (q & 1) == (s & 1))
+            H.g[(((size_t)p * n + q) * n + r) * n + s] =
+                I.g[(((size_t)(p >> 1) * m + (r >> 1)) * m + (q >> 1)) * m + (s >> 1)];
+  return H;
+}
+
+PauliSum qubit_hamiltonian(const SpinOrbitalHamiltonian& H) {
+  const int n = H.n_so;
+  if (n > 64) throw ContractViolation("qubit_hamiltonian: more than 64 spin orbitals");
+  std::vector<PauliSum> a, ad;
+  for (int p = 0; p < n; ++p) {
+    a.push_back(jordan_wigner_ladder({p, false}, n));
+    ad.push_back(jordan_wigner_ladder({p, true}, n));
+  }
+  PauliSum out(n);
+  if (H.e_const != 0.0) out.add(0, 0, H.e_const);
+  auto accumulate = [&](const PauliSum& s) {
+    for (auto& kv : s.terms()) out.add(kv.first.first, kv.first.second, kv.second);
+  };
+  for (int p = 0; p < n; ++p)
+    for (int q = 0; q < n; ++q) {
+      const double v = H.h[(size_t)p * n + q];
+      if (v != 0.0) accumulate((ad[p] * a[q]).scaled(v));
+    }
+  std::vector<PauliSum> asr((size_t)n * n, PauliSum(n));  // a_s a_r
+  for (int s = 0; s < n; ++s)
+    for (int r = 0; r < n; ++r)
+      if (r != s) asr[(size_t)s * n + r] = a[s] * a[r];
+  for (int p = 0; p < n; ++p)
+    for (int q = 0; q < n; ++q) {
+      if (p == q) continue;
+      const PauliSum apq = ad[p] * ad[q];
+      for (int r = 0; r < n; ++r)
+        for (int s = 0; s < n; ++s) {
+          if (r == s) continue;
+          const double v = H.g[(((size_t)p * n + q) * n + r) * n + s];
+          if (v == 0.0) continue;
+          accumulate((apq * asr[(size_t)s * n + r]).scaled(0.5 * v));
+        }
+    }
+  out.simplify();
+  return out;
+}
+
+PauliSum random_pauli_hamiltonian(int n_qubits, int n_terms, uint64_t seed, double sigma) {
+  if (n_qubits < 1 || n_qubits > 64) throw ContractViolation("random_pauli_hamiltonian: bad n");
+  std::mt19937_64 gen(seed);
+  PauliSum H(n_qubits);
+  for (int t = 0; t < n_terms; ++t) {
+    uint64_t x = 0, z = 0;
+    for (int q = 0; q < n_qubits; ++q) {
+      const uint64_t l = gen() >> 62;  // 0 I, 1 X, 2 Y, 3 Z
+      if (l == 1 || l == 2) x |= 1ULL << q;
+      if (l == 2 || l == 3) z |= 1ULL << q;
+    }
+    H.add(x, z, sigma * normal01(gen));
+  }
+  H.simplify();
+  return H;
+}
+
+// ---- UCCSD ---------------------------------------------------------------------
+std::vector<Generator> build_generators(int n_so, int n_elec) {
+  if (n_elec < 0 || n_elec > n_so || n_so > 64) throw ContractViolation("build_generators: bad sizes");
+  std::vector<Excitation> ex;
+  for (int i = 0; i < n_elec; ++i)
+    for (int a = n_elec; a < n_so; ++a)
+      if ((i & 1) == (a & 1)) ex.push_back({1, i, -1, a, -1});
+  for (int i = 0; i < n_elec; ++i)
+    for (int j = i + 1; j < n_elec; ++j)
+      for (int a = n_elec; a < n_so; ++a)
+        for (int b = a + 1; b < n_so; ++b)
+          if ((i & 1) + (j & 1) == (a & 1) + (b & 1)) ex.push_back({2, i, j, a, b});
+  std::vector<Generator> gens;
+  gens.reserve(ex.size());
+  for (size_t k = 0; k < ex.size(); ++k) {
+    const Excitation& e = ex[k];
+    FermionOperator op;
+    if (e.kind == 1) {
+      op.push_back({Complex(1, 0), {{e.a, true}, {e.i, false}}});
+      op.push_back({Complex(-1, 0), {{e.i, true}, {e.a, false}}});
+    } else {
+      op.push_back({Complex(1, 0), {{e.a, true}, {e.b, true}, {e.j, false}, {e.i, false}}});
+      op.push_back({Complex(-1, 0), {{e.i, true}, {e.j, true}, {e.b, false}, {e.a, false}}});
+    }
+    gens.push_back({(int)k, e, jordan_wigner(op, n_so)});
+  }
+  return gens;
+}
+
+TrotterPlan magnitude_order(const std::vector<Generator>& gens, const std::vector<double>& amps,
+                            int n_qubits) {
+  if (amps.size() > gens.size()) throw ContractViolation("magnitude_order: more amplitudes than generators");
+  TrotterPlan P;
+  P.n_qubits = n_qubits;
+  P.generators = gens;
+  P.order.resize(gens.size());
+  std::iota(P.order.begin(), P.order.end(), 0);
+  auto amp = [&](int g) { return g < (int)amps.size() ? std::abs(amps[g]) : 0.0; };
+  std::stable_sort(P.order.begin(), P.order.end(), [&](int u, int v) {
+    const double fu = amp(u), fv = amp(v);
+    if (fu != fv) return fu > fv;
+    return u < v;
+  });
+  return P;
+}
+
+std::vector<double> TrotterPlan::plan_theta(const std::vector<double>& amps) const {
+  if (amps.size() != generators.size()) throw ContractViolation("plan_theta: amplitude count mismatch");
+  std::vector<double> t(order.size());
+  for (size_t s = 0; s < order.size(); ++s) t[s] = amps[order[s]];
+  return t;
+}
+
+void TrotterPlan::flatten(std::vector<int64_t>& off, std::vector<uint64_t>& x,
+                          std::vector<uint64_t>& z, std::vector<double>& re,
+                          std::vector<double>& im) const {
+  off.assign(1, 0);
+  for (int gid : order) {
+    generators[gid].image.flatten(x, z, re, im);
+    off.push_back((int64_t)x.size());
+  }
+}
+
+uint64_t hf_bits(int n_elec) {
+  if (n_elec < 0 || n_elec > 63) throw ContractViolation("hf_bits: electron count out of range");
+  return (n_elec == 0) ? 0ULL : ((1ULL << n_elec) - 1ULL);
+}
+
+// ---- device facade ---------------------------------------------------------------
+void check_ffq(int rc, ffq_ctx_t ctx) {
+  if (rc == FFQ_OK) return;
+  const std::string msg = ffq_last_error(ctx);
+  if (rc == FFQ_EINVAL || rc == FFQ_ENONHERMITIAN) throw ContractViolation(msg);
+  throw DeviceError(msg, rc);
+}
+
+Device::Device(int ordinal) : ordinal_(ordinal) { check_ffq(ffq_ctx_create(ordinal, &ctx_), nullptr); }
+Device::~Device() { ffq_ctx_destroy(ctx_); }
+void Device::synchronize() const { check_ffq(ffq_ctx_synchronize(ctx_), ctx_); }
+int Device::count() {
+  int n = 0;
+  return ffq_device_count(&n) == FFQ_OK ? n : 0;
+}
+
+DeviceHamiltonian::DeviceHamiltonian(Device& dev, const PauliSum& H) : dev_(dev), n_(H.n_qubits()) {
+  std::vector<uint64_t> x, z;
+  std::vector<double> re, im;
+  H.flatten(x, z, re, im);
+  check_ffq(ffq_ham_upload(dev.handle(), n_, (int64_t)x.size(), x.data(), z.data(), re.data(),
+                           im.data(), &h_),
+            dev.handle());
+}
+DeviceHamiltonian::~DeviceHamiltonian() { ffq_ham_destroy(h_); }
+int DeviceHamiltonian::n_groups() const {
+  int g = 0;
+  ffq_ham_info(h_, &g, nullptr, nullptr);
+  return g;
+}
+int64_t DeviceHamiltonian::n_classes() const {
+  int64_t c = 0;
+  ffq_ham_info(h_, nullptr, nullptr, &c);
+  return c;
+}
+
+DevicePlan::DevicePlan(Device& dev, const TrotterPlan& plan) : dev_(dev), plan_(plan) {
+  std::vector<int64_t> off;
+  std::vector<uint64_t> x, z;
+  std::vector<double> re, im;
+  plan.flatten(off, x, z, re, im);
+  check_ffq(ffq_plan_upload(dev.handle(), plan.n_qubits, (int)plan.order.size(), off.data(),
+                            x.data(), z.data(), re.data(), im.data(), &p_),
+            dev.handle());
+}
+DevicePlan::~DevicePlan() { ffq_plan_destroy(p_); }
+int DevicePlan::n_fused() const {
+  int f = 0;
+  ffq_plan_info(p_, &f, nullptr);
+  return f;
+}
+int DevicePlan::n_string_ops() const {
+  int s = 0;
+  ffq_plan_info(p_, nullptr, &s);
+  return s;
+}
+
+Statevector::Statevector(Device& dev, int n_qubits, int batch) : dev_(dev), n_(n_qubits), batch_(batch) {
+  check_ffq(ffq_state_alloc(dev.handle(), n_qubits, batch, &s_), dev.handle());
+}
+Statevector::~Statevector() { ffq_state_free(s_); }
+void Statevector::set_basis(uint64_t bits) { check_ffq(ffq_state_set_basis(s_, bits), dev_.handle()); }
+void Statevector::apply_pauli_rotation(const PauliString& p, double theta) {
+  if (p.n_qubits != n_) throw ContractViolation("apply_pauli_rotation: qubit count mismatch");
+  check_ffq(ffq_state_apply_pauli_rotation(s_, p.x, p.z, theta), dev_.handle());
+}
+void Statevector::apply_plan(const DevicePlan& plan, const std::vector<double>& theta) {
+  if (theta.size() != plan.plan().order.size() * (size_t)batch_)
+    throw ContractViolation("apply_plan: theta must be [batch][n_gen]");
+  check_ffq(ffq_state_apply_plan(s_, plan.handle(), theta.data()), dev_.handle());
+}
+std::vector<double> Statevector::expectation(const DeviceHamiltonian& H) const {
+  std::vector<double> re(batch_), im(batch_);
+  check_ffq(ffq_state_expectation(s_, H.handle(), re.data(), im.data()), dev_.handle());
+  for (double v : im)
+    if (std::abs(v) > 1e-10) throw ContractViolation("expectation: imaginary residue above 1e-10");
+  return re;
+}
+std::vector<Complex> Statevector::download() const {
+  std::vector<Complex> v((size_t)batch_ << n_);
+  check_ffq(ffq_state_download(s_, reinterpret_cast<double*>(v.data())), dev_.handle());
+  return v;
+}
+void Statevector::upload(const std::vector<Complex>& amps) {
+  if (amps.size() != ((size_t)batch_ << n_)) throw ContractViolation("upload: size mismatch");
+  check_ffq(ffq_state_upload(s_, reinterpret_cast<const double*>(amps.data())), dev_.handle());
+}
+
+std::vector<double> energy_batch(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H,
+                                 uint64_t hf, const std::vector<double>& theta, int batch) {
+  const size_t ng = plan.plan().order.size();
+  if (theta.size() != ng * (size_t)batch) throw ContractViolation("energy_batch: theta must be [batch][n_gen]");
+  std::vector<double> e((size_t)batch);
+  check_ffq(ffq_energy_batch(dev.handle(), plan.handle(), H.handle(), hf, batch, theta.data(), e.data()),
+            dev.handle());
+  return e;
+}
+
+double energy_trotter(Device& dev, const std::vector<double>& amps, const DevicePlan& plan,
+                      const DeviceHamiltonian& H, uint64_t hf) {
+  return energy_batch(dev, plan, H, hf, plan.plan().plan_theta(amps), 1)[0];
+}
+
+// ---- optimizers ------------------------------------------------------------------
+namespace {
+
+struct Counted {
+  const Objective& f;
+  int evals = 0;
+  int max_evals;
+  double best = std::numeric_limits<double>::infinity();
+  std::vector<double> best_x;
+  double operator()(const std::vector<double>& x) {
+    ++evals;
+    const double v = f(x);
+    if (v < best) { best = v; best_x = x; }
+    return v;
+  }
+  bool exhausted() const { return evals >= max_evals; }
+};
+
+// Brent's method on f(x0 + t d) after a golden-section bracket.
+double line_minimize(Counted& F, std::vector<double>& x, const std::vector<double>& d, double fx,
+                     double step) {
+  const double gold = 1.618033988749895, cgold = 0.3819660112501051, tiny = 1e-20;
+  auto at = [&](double t) {
+    std::vector<double> y(x);
+    for (size_t i = 0; i < y.size(); ++i) y[i] += t * d[i];
+    return F(y);
+  };
+  double a = 0.0, b = step, fa = fx, fb = at(b);
+  if (fb > fa) { std::swap(a, b); std::swap(fa, fb); }
+  double c = b + gold * (b - a), fc = at(c);
+  while (fb > fc && !F.exhausted()) {
+    const double r = (b - a) * (fb - fc), q = (b - c) * (fb - fa);
+    double u = b - ((b - c) * q - (b - a) * r) / (2.0 * std::copysign(std::max(std::abs(q - r), tiny), q - r));
+    const double ulim = b + 100.0 * (c - b);
+    double fu;
+    if ((b - u) * (u - c) > 0.0) {
+      fu = at(u);
+      if (fu < fc) { a = b; fa = fb; b = u; fb = fu; break; }
+      if (fu > fb) { c = u; fc = fu; break; }
+      u = c + gold * (c - b); fu = at(u);
+    } else if ((c - u) * (u - ulim) > 0.0) {
+      fu = at(u);
+      if (fu < fc) { b = c; c = u; u = c + gold * (c - b); fb = fc; fc = fu; fu = at(u); }
+    } else if ((u - ulim) * (ulim - c) >= 0.0) {
+      u = ulim; fu = at(u);
+    } else {
+      u = c + gold * (c - b); fu = at(u);
+    }
+    a = b; b = c; c = u; fa = fb; fb = fc; fc = fu;
+  }
+  // Brent
+  double lo = std::min(a, c), hi = std::max(a, c);
+  double xb = b, w = b, v = b, fxb = fb, fw = fb, fv = fb, e = 0.0, dd = 0.0;
+  for (int it = 0; it < 100 && !F.exhausted(); ++it) {
+    const double xm = 0.5 * (lo + hi);
+    const double tol1 = 1e-8 * std::abs(xb) + 1e-12, tol2 = 2.0 * tol1;
+    if (std::abs(xb - xm) <= tol2 - 0.5 * (hi - lo)) break;
+    if (std::abs(e) > tol1) {
+      double r = (xb - w) * (fxb - fv), q = (xb - v) * (fxb - fw), p = (xb - v) * q - (xb - w) * r;
+      q = 2.0 * (q - r);
+      if (q > 0.0) p = -p;
+      q = std::abs(q);
+      const double etemp = e;
+      e = dd;
+      if (std::abs(p) >= std::abs(0.5 * q * etemp) || p <= q * (lo - xb) || p >= q * (hi - xb)) {
+        e = (xb >= xm) ? lo - xb : hi - xb;
+        dd = cgold * e;
+      } else {
+        dd = p / q;
+        const double u = xb + dd;
+        if (u - lo < tol2 || hi - u < tol2) dd = std::copysign(tol1, xm - xb);
+      }
+    } else {
+      e = (xb >= xm) ? lo - xb : hi - xb;
+      dd = cgold * e;
+    }
+    const double u = std::abs(dd) >= tol1 ? xb + dd : xb + std::copysign(tol1, dd);
+    const double fu = at(u);
+    if (fu <= fxb) {
+      if (u >= xb) lo = xb; else hi = xb;
+      v = w; w = xb; xb = u; fv = fw; fw = fxb; fxb = fu;
+    } else {
+      if (u < xb) lo = u; else hi = u;
+      if (fu <= fw || w == xb) { v = w; w = u; fv = fw; fw = fu; }
+      else if (fu <= fv || v == xb || v == w) { v = u; fv = fu; }
+    }
+  }
+  if (fxb < fx) {
+    for (size_t i = 0; i < x.size(); ++i) x[i] += xb * d[i];
+    return fxb;
+  }
+  return fx;
+}
+
+}  // namespace
+
+OptimizeResult powell_minimize(const Objective& f, std::vector<double> x, const OptimizerOptions& opts) {
+  const size_t n = x.size();
+  Counted F{f, 0, opts.max_evals};
+  OptimizeResult R;
+  std::vector<std::vector<double>> dirs(n, std::vector<double>(n, 0.0));
+  for (size_t i = 0; i < n; ++i) dirs[i][i] = 1.0;
+  double fx = F(x);
+  while (!F.exhausted()) {
+    ++R.n_iterations;
+    const double f0 = fx;
+    const std::vector<double> x0 = x;
+    size_t ibig = 0;
+    double big = 0.0;
+    for (size_t i = 0; i < n && !F.exhausted(); ++i) {
+      const double fold = fx;
+      fx = line_minimize(F, x, dirs[i], fx, opts.initial_step);
+      if (fold - fx > big) { big = fold - fx; ibig = i; }
+    }
+    if (f0 - fx <= opts.ftol) { R.converged = true; break; }
+    std::vector<double> dnew(n), xe(n);
+    for (size_t i = 0; i < n; ++i) { dnew[i] = x[i] - x0[i]; xe[i] = 2.0 * x[i] - x0[i]; }
+    const double fe = F(xe);
+    if (fe < f0) {
+      const double t = 2.0 * (f0 - 2.0 * fx + fe) * (f0 - fx - big) * (f0 - fx - big) -
+                       big * (f0 - fe) * (f0 - fe);
+      if (t < 0.0) {
+        fx = line_minimize(F, x, dnew, fx, 1.0);
+        dirs[ibig] = dirs[n - 1];
+        dirs[n - 1] = dnew;
+      }
+    }
+  }
+  R.energy = F.best;
+  R.x = F.best_x;
+  R.n_evals = F.evals;
+  return R;
+}
+
+OptimizeResult neldermead_minimize(const Objective& f, std::vector<double> x0,
+                                   const OptimizerOptions& opts) {
+  const size_t n = x0.size();
+  Counted F{f, 0, opts.max_evals};
+  OptimizeResult R;
+  // adaptive coefficients (Gao & Han)
+  const double dn = (double)std::max<size_t>(n, 1);
+  const double alpha = 1.0, beta = 1.0 + 2.0 / dn, gamma = 0.75 - 0.5 / dn, delta = 1.0 - 1.0 / dn;
+  std::vector<std::vector<double>> s(n + 1, x0);
+  std::vector<double> fs(n + 1);
+  for (size_t i = 0; i < n; ++i) s[i + 1][i] += opts.initial_step;
+  for (size_t i = 0; i <= n; ++i) fs[i] = F(s[i]);
+  std::vector<size_t> idx(n + 1);
+  while (!F.exhausted()) {
+    ++R.n_iterations;
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return fs[a] < fs[b]; });
+    const size_t ib = idx[0], iw = idx[n], isw = idx[n > 0 ? n - 1 : 0];
+    double xspread = 0.0;
+    for (size_t i = 0; i <= n; ++i)
+      for (size_t k = 0; k < n; ++k) xspread = std::max(xspread, std::abs(s[i][k] - s[ib][k]));
+    if (fs[iw] - fs[ib] <= opts.ftol && xspread <= std::max(opts.xtol, 1e-4)) { R.converged = true; break; }
+    std::vector<double> c(n, 0.0);
+    for (size_t i = 0; i <= n; ++i)
+      if (i != iw)
+        for (size_t k = 0; k < n; ++k) c[k] += s[i][k] / dn;
+    auto lerp = [&](double t) {
+      std::vector<double> y(n);
+      for (size_t k = 0; k < n; ++k) y[k] = c[k] + t * (s[iw][k] - c[k]);
+      return y;
+    };
+    std::vector<double> xr = lerp(-alpha);
+    const double fr = F(xr);
+    if (fr < fs[ib]) {
+      std::vector<double> xe = lerp(-alpha * beta);
+      const double fe = F(xe);
+      if (fe < fr) { s[iw] = xe; fs[iw] = fe; } else { s[iw] = xr; fs[iw] = fr; }
+    } else if (fr < fs[isw]) {
+      s[iw] = xr; fs[iw] = fr;
+    } else {
+      const bool outside = fr < fs[iw];
+      std::vector<double> xc = lerp(outside ? -alpha * gamma : gamma);
+      const double fc = F(xc);
+      if (fc < std::min(fr, fs[iw])) {
+        s[iw] = xc; fs[iw] = fc;
+      } else {
+        for (size_t i = 0; i <= n; ++i) {
+          if (i == ib) continue;
+          for (size_t k = 0; k < n; ++k) s[i][k] = s[ib][k] + delta * (s[i][k] - s[ib][k]);
+          fs[i] = F(s[i]);
+        }
+      }
+    }
+  }
+  R.energy = F.best;
+  R.x = F.best_x;
+  R.n_evals = F.evals;
+  return R;
+}
+
+OptimizeResult vqe_minimize(const Objective& f, std::vector<double> x0, Optimizer method,
+                            const OptimizerOptions& opts) {
+  return method == Optimizer::powell ? powell_minimize(f, std::move(x0), opts)
+                                     : neldermead_minimize(f, std::move(x0), opts);
+}
+
+std::vector<double> parameter_shift_set(const std::vector<double>& th) {
+  const size_t P = th.size();
+  std::vector<double> rows;
+  rows.reserve((1 + 2 * P) * P);
+  rows.insert(rows.end(), th.begin(), th.end());
+  const double h = 1.5707963267948966;
+  for (size_t k = 0; k < P; ++k)
+    for (double s : {h, -h}) {
+      std::vector<double> r(th);
+      r[k] += s;
+      rows.insert(rows.end(), r.begin(), r.end());
+    }
+  return rows;
+}
+
+std::vector<double> exact_gradient_set(const std::vector<double>& th) {
+  const size_t P = th.size();
+  std::vector<double> rows;
+  rows.reserve(4 * P * P);
+  const double s1 = 1.5707963267948966, s2 = 0.7853981633974483;
+  for (size_t k = 0; k < P; ++k)
+    for (double s : {s1, -s1, s2, -s2}) {
+      std::vector<double> r(th);
+      r[k] += s;
+      rows.insert(rows.end(), r.begin(), r.end());
+    }
+  return rows;
+}
+
+// dE/dt = c1 [E(+pi/2) - E(-pi/2)] + c2 [E(+pi/4) - E(-pi/4)],
+// c1 = (1 - sqrt 2)/2, c2 = 1: exact for frequencies {1, 2}.
+std::vector<double> exact_gradient_from_energies(const std::vector<double>& e, int P) {
+  if ((int)e.size() != 4 * P) throw ContractViolation("exact_gradient_from_energies: need 4P energies");
+  const double c1 = 0.5 * (1.0 - std::sqrt(2.0)), c2 = 1.0;
+  std::vector<double> g((size_t)P);
+  for (int k = 0; k < P; ++k)
+    g[k] = c1 * (e[4 * k] - e[4 * k + 1]) + c2 * (e[4 * k + 2] - e[4 * k + 3]);
+  return g;
+}
+
+OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, const OptimizerOptions& opts) {
+  const int P = (int)x.size();
+  OptimizeResult R;
+  auto energy = [&](const std::vector<double>& y) {
+    ++R.n_evals;
+    return f(y, 1)[0];
+  };
+  auto grad = [&](const std::vector<double>& y) {
+    R.n_evals += 4 * P;
+    return exact_gradient_from_energies(f(exact_gradient_set(y), 4 * P), P);
+  };
+  std::vector<double> Hinv((size_t)P * P, 0.0);
+  for (int i = 0; i < P; ++i) Hinv[(size_t)i * P + i] = 1.0;
+  double fx = energy(x);
+  std::vector<double> g = grad(x);
+  while (R.n_evals < opts.max_evals) {
+    ++R.n_iterations;
+    std::vector<double> d(P, 0.0);
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j) d[i] -= Hinv[(size_t)i * P + j] * g[j];
+    double slope = 0.0;
+    for (int i = 0; i < P; ++i) slope += d[i] * g[i];
+    if (slope >= 0.0) {  // reset to steepest descent
+      for (int i = 0; i < P; ++i) { d[i] = -g[i]; }
+      std::fill(Hinv.begin(), Hinv.end(), 0.0);
+      for (int i = 0; i < P; ++i) Hinv[(size_t)i * P + i] = 1.0;
+      slope = 0.0;
+      for (int i = 0; i < P; ++i) slope -= g[i] * g[i];
+    }
+    double t = 1.0, fn = fx;
+    std::vector<double> xn(P);
+    for (int ls = 0; ls < 40; ++ls) {
+      for (int i = 0; i < P; ++i) xn[i] = x[i] + t * d[i];
+      fn = energy(xn);
+      if (fn <= fx + 1e-4 * t * slope) break;
+      t *= 0.5;
+    }
+    if (!(fn < fx)) { R.converged = true; break; }
+    std::vector<double> gn = grad(xn), s(P), y(P);
+    for (int i = 0; i < P; ++i) { s[i] = xn[i] - x[i]; y[i] = gn[i] - g[i]; }
+    const double df = fx - fn;
+    x = xn; fx = fn; g = gn;
+    double gnorm = 0.0;
+    for (double v : g) gnorm = std::max(gnorm, std::abs(v));
+    if (df <= opts.ftol || gnorm <= 1e-6) { R.converged = true; break; }
+    double sy = 0.0;
+    for (int i = 0; i < P; ++i) sy += s[i] * y[i];
+    if (sy > 1e-14) {
+      std::vector<double> Hy(P, 0.0);
+      for (int i = 0; i < P; ++i)
+        for (int j = 0; j < P; ++j) Hy[i] += Hinv[(size_t)i * P + j] * y[j];
+      double yHy = 0.0;
+      for (int i = 0; i < P; ++i) yHy += y[i] * Hy[i];
+      for (int i = 0; i < P; ++i)
+        for (int j = 0; j < P; ++j)
+          Hinv[(size_t)i * P + j] += ((sy + yHy) * s[i] * s[j]) / (sy * sy) - (Hy[i] * s[j] + s[i] * Hy[j]) / sy;
+    }
+  }
+  R.energy = fx;
+  R.x = x;
+  return R;
+}
+
+// ---- FMO two-body assembly -----------------------------------------------------------
+double assemble_two_body(int n_fragments, const std::map<std::string, double>& monomers,
+                         const std::map<std::string, double>& dimers) {
+  if ((int)monomers.size() != n_fragments)
+    throw ContractViolation("assemble: expected " + std::to_string(n_fragments) +
+                            " monomer energies, got " + std::to_string(monomers.size()));
+  const size_t want = (size_t)n_fragments * (n_fragments - 1) / 2;
+  if (dimers.size() != want)
+    throw ContractViolation("assemble: expected " + std::to_string(want) + " dimer energies, got " +
+                            std::to_string(dimers.size()));
+  double e = 0.0, em = 0.0;
+  for (auto& kv : dimers) e += kv.second;
+  for (auto& kv : monomers) em += kv.second;
+  return e - (n_fragments - 2) * em;
+}
+
+double FragmentLedger::assemble_corr() const { return assemble_two_body(n_fragments, corr_I, corr_IJ); }
+
+std::vector<std::string> dimer_labels(int n_fragments) {
+  std::vector<std::string> out;
+  for (int j = 1; j <= n_fragments; ++j)
+    for (int i = j + 1; i <= n_fragments; ++i) out.push_back(std::to_string(i) + std::to_string(j));
+  return out;
+}
+
+}  // namespace fragfield

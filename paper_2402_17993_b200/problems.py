@@ -1,0 +1,93 @@
+"""Seeded synthetic workloads of BASELINE.json's configs (DESIGN.md pins them).
+
+Each problem bundles the JW qubit Hamiltonian, the UCCSD generators, the
+magnitude-ordered plan and the theta vectors, all built by the C++ host API.
+Seeds: ham_seed = 2402179930 + 1000*config + 10*fragment; theta_seed = ham_seed + 1.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import build_generators, hf_bits, magnitude_order, qubit_hamiltonian, synthetic_integrals, uniform_vector
+
+SEED_BASE = 2402179930
+
+# config -> (spatial orbitals m, electrons, theta half-width)
+CONFIGS = {1: (4, 4, 0.1), 2: (6, 6, 0.1), 3: (9, 10, 0.1)}
+
+
+def ham_seed(config: int, fragment: int = 0) -> int:
+    return SEED_BASE + 1000 * config + 10 * fragment
+
+
+@dataclass
+class Problem:
+    name: str
+    m: int
+    n_elec: int
+    h: np.ndarray
+    g: np.ndarray
+    H: object  # PauliSum
+    gens: list
+    plan: object  # TrotterPlan
+    thetas: np.ndarray  # [batch][n_gen], canonical generator order
+    seed: int
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n_qubits(self):
+        return 2 * self.m
+
+    @property
+    def n_gen(self):
+        return len(self.gens)
+
+    @property
+    def hf(self):
+        return hf_bits(self.n_elec)
+
+    def plan_thetas(self, thetas=None):
+        """[batch][n_gen] in plan (execution) order."""
+        t = self.thetas if thetas is None else np.atleast_2d(thetas)
+        return np.ascontiguousarray(t[:, np.asarray(self.plan.order)])
+
+    def plan_arrays(self):
+        """Flat C-ABI arrays of the plan: term_off, x, z, c (execution order)."""
+        off = [0]; xs = []; zs = []; cs = []
+        for gid in self.plan.order:
+            x, z, c = self.gens[gid].image.arrays()
+            xs.append(x); zs.append(z); cs.append(c)
+            off.append(off[-1] + len(x))
+        return (np.array(off, np.int64), np.concatenate(xs).astype(np.uint64),
+                np.concatenate(zs).astype(np.uint64), np.concatenate(cs))
+
+    def ham_arrays(self):
+        return self.H.arrays()
+
+
+def make_problem(m: int, n_elec: int, seed: int, batch: int = 1, theta_hw: float = 0.1,
+                 name: str = "") -> Problem:
+    h, g = synthetic_integrals(m, seed)
+    H = qubit_hamiltonian(h, g, n_elec)
+    gens = build_generators(2 * m, n_elec)
+    th = np.array(uniform_vector(seed + 1, batch * len(gens), -theta_hw, theta_hw)).reshape(batch, len(gens))
+    plan = magnitude_order(gens, list(th[0]), 2 * m)
+    return Problem(name or f"m{m}e{n_elec}", m, n_elec, h, g, H, gens, plan, th, seed)
+
+
+def config_problem(config: int, batch: int = 1, fragment: int = 0) -> Problem:
+    m, ne, hw = CONFIGS[config]
+    return make_problem(m, ne, ham_seed(config, fragment), batch, hw, name=f"config{config}")
+
+
+def fmo_fragments():
+    """Config 4: monomers "1".."3" (12 qubits, 6 e) and dimers "21","31","32"
+    (18 qubits, 10 e), each with its own seed."""
+    frags = {}
+    for f in (1, 2, 3):
+        frags[str(f)] = make_problem(6, 6, ham_seed(4, f), name=f"monomer{f}")
+    for k, lab in enumerate(("21", "31", "32")):
+        frags[lab] = make_problem(9, 10, ham_seed(4, 10 + k), name=f"dimer{lab}")
+    return frags

@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path, called through the C-ABI (capi = ctypes over
+libfragfield_cuda.so), against the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star): energies <= 1e-10 Hartree absolute, amplitudes
+<= 1e-12 max-abs. Full-size configs are checked through size-independent
+properties (norm, HF limit, determinism, inverse rotations)."""
+import os
+import time
+
+import numpy as np
+import pytest
+
+import paper_2402_17993_b200 as ff
+from paper_2402_17993_b200 import capi, problems
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-10
+A_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return capi.Context(0)
+
+
+def oracle_H(oracle, P):
+    x, z, c = P.ham_arrays()
+    return oracle.PauliSum.from_terms(P.n_qubits, x, z, c)
+
+
+def upload(ctx, P):
+    return (capi.Plan(ctx, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays()))
+
+
+def oracle_energy(oracle, P, theta_canonical, want_state=False):
+    kind, idx = oracle.build_generators(P.n_qubits, P.n_elec)
+    return oracle.energy_trotter(P.n_qubits, P.n_elec, kind, idx, np.array(P.plan.order, np.int32),
+                                 theta_canonical, oracle_H(oracle, P), want_state=want_state)
+
+
+@pytest.mark.parametrize("n", [2, 3, 6, 11])
+def test_pauli_rotation_all_modes_vs_oracle(ctx, oracle, n):
+    rng = np.random.default_rng(n)
+    dim = 1 << n
+    psi = rng.normal(size=(2, dim)) + 1j * rng.normal(size=(2, dim))
+    psi /= np.linalg.norm(psi, axis=1, keepdims=True)
+    st = capi.State(ctx, n, 2)
+    st.upload(psi)
+    ref = psi.copy()
+    strings = [(0, 1), (1, 0), (1, 3), (dim - 1, dim - 1), (2 % dim, 1), (dim - 2, 5 % dim), (3, 0)]
+    for k, (x, z) in enumerate(strings):
+        th = 0.3 + 0.17 * k
+        st.rotate(x, z, th)
+        for b in range(2):
+            ref[b] = oracle.apply_pauli_rotation(n, ref[b], x, z, th)
+    assert np.abs(st.download() - ref).max() <= A_TOL
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_plan_amplitudes_and_energy_vs_oracle(ctx, oracle, config):
+    P = problems.config_problem(config)
+    plan, ham = upload(ctx, P)
+    e_ref, im_ref, psi_ref = oracle_energy(oracle, P, P.thetas[0], want_state=True)
+    st = capi.State(ctx, P.n_qubits, 1)
+    st.set_basis(P.hf)
+    st.apply_plan(plan, P.plan_thetas())
+    assert np.abs(st.download()[0] - psi_ref).max() <= A_TOL
+    assert abs(st.expectation(ham)[0].real - e_ref) <= E_TOL
+    assert abs(capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0] - e_ref) <= E_TOL
+
+
+def test_config2_batch_of_64_vs_oracle(ctx, oracle):
+    P = problems.config_problem(2, batch=64)
+    plan, ham = upload(ctx, P)
+    e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())
+    for b in (0, 17, 63):
+        assert abs(e[b] - oracle_energy(oracle, P, P.thetas[b])[0]) <= E_TOL
+
+
+def test_parameter_shift_set_vs_oracle(ctx, oracle):
+    P = problems.config_problem(1)
+    plan, ham = upload(ctx, P)
+    rows = np.array(ff.parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)
+    e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas(rows))
+    for r in (0, 1, 2, len(rows) - 1):
+        assert abs(e[r] - oracle_energy(oracle, P, rows[r])[0]) <= E_TOL
+
+
+def test_global_path_matches_smem_path_and_oracle(oracle, monkeypatch):
+    # the same 12-qubit problem through the graph-of-kernels path
+    monkeypatch.setenv("FFQ_SMEM_MAX_QUBITS", "0")
+    gctx = capi.Context(0)
+    P = problems.config_problem(2, batch=5)
+    plan, ham = upload(gctx, P)
+    e_glob = capi.energy_batch(gctx, plan, ham, P.hf, P.plan_thetas())
+    monkeypatch.delenv("FFQ_SMEM_MAX_QUBITS")
+    sctx = capi.Context(0)
+    plan2, ham2 = upload(sctx, P)
+    e_smem = capi.energy_batch(sctx, plan2, ham2, P.hf, P.plan_thetas())
+    assert np.abs(e_glob - e_smem).max() <= 1e-12
+    assert abs(e_glob[3] - oracle_energy(oracle, P, P.thetas[3])[0]) <= E_TOL
+
+
+def test_18_qubit_energy_vs_oracle(ctx, oracle):
+    P = problems.config_problem(3)
+    plan, ham = upload(ctx, P)
+    t = time.time()
+    e_ref = oracle_energy(oracle, P, P.thetas[0])[0]
+    e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())
+    assert abs(e[0] - e_ref) <= E_TOL, (e[0], e_ref, time.time() - t)
+
+
+def test_determinism_across_batch_splits(ctx):
+    P = problems.config_problem(3, batch=20)
+    plan, ham = upload(ctx, P)
+    th = P.plan_thetas()
+    full = capi.energy_batch(ctx, plan, ham, P.hf, th)
+    parts = np.concatenate([capi.energy_batch(ctx, plan, ham, P.hf, th[i:i + 7]) for i in range(0, 20, 7)])
+    single = capi.energy_batch(ctx, plan, ham, P.hf, th[11:12])
+    assert np.array_equal(full, parts) and full[11] == single[0]
+
+
+def test_full_size_properties_18q(ctx):
+    P = problems.config_problem(3)
+    plan, ham = upload(ctx, P)
+    # zero amplitudes -> HF energy = diagonal element
+    e0 = capi.energy_batch(ctx, plan, ham, P.hf, np.zeros((1, P.n_gen)))[0]
+    st = capi.State(ctx, 18, 1)
+    st.set_basis(P.hf)
+    assert abs(st.expectation(ham)[0].real - e0) <= 1e-12
+    # norm preservation after the full plan
+    st.apply_plan(plan, P.plan_thetas())
+    psi = st.download()[0]
+    assert abs(np.linalg.norm(psi) - 1.0) <= 1e-12
+    # particle number and S_z are conserved: support only on 5 alpha + 5 beta
+    idx = np.nonzero(np.abs(psi) > 1e-14)[0]
+    alpha = np.array([bin(k & 0x15555).count("1") for k in idx])
+    beta = np.array([bin(k & 0x2AAAA).count("1") for k in idx])
+    assert np.all(alpha == 5) and np.all(beta == 5)
+
+
+def test_large_state_rotation_roundtrip(ctx):
+    # 26 qubits (1 GiB): e^{-i t P} e^{i t P} = I on a random state
+    n = 26
+    st = capi.State(ctx, n, 1)
+    rng = np.random.default_rng(0)
+    psi = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)) / np.sqrt(2 << n)
+    st.upload(psi)
+    for x, z in ((0b1010 << 20, 0b11), (1 | (1 << 25), 1 << 3), (0, (1 << 26) - 1), (1, 2)):
+        st.rotate(x, z, 0.41)
+        st.rotate(x, z, -0.41)
+    assert np.abs(st.download()[0] - psi).max() <= A_TOL
+
+
+def test_error_paths(ctx):
+    with pytest.raises(ff.ContractViolation):
+        capi.Hamiltonian(ctx, 2, [1], [0], [0.5j])  # non-Hermitian
+    with pytest.raises(ff.ContractViolation):
+        capi.Plan(ctx, 2, [0, 1], [1], [0], [0.5])  # generator not anti-Hermitian
+    P1 = problems.config_problem(1)
+    P2 = problems.config_problem(2)
+    plan = capi.Plan(ctx, P1.n_qubits, *P1.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P2.n_qubits, *P2.ham_arrays())
+    with pytest.raises(ff.ContractViolation):
+        capi.energy_batch(ctx, plan, ham, P1.hf, P1.plan_thetas())
+    with pytest.raises(ff.ContractViolation):
+        capi.State(ctx, 1, 1)
+
+
+def test_cpp_facade_energy_and_vqe(oracle):
+    dev = ff.Device(0)
+    P = problems.config_problem(1)
+    H = ff.DeviceHamiltonian(dev, P.H)
+    plan = ff.DevicePlan(dev, P.plan)
+    assert plan.n_fused == P.n_gen
+    e = ff.energy_trotter(dev, list(P.thetas[0]), plan, H, P.hf)
+    assert abs(e - oracle_energy(oracle, P, P.thetas[0])[0]) <= E_TOL
+    # config 1: full VQE to convergence (Powell, ftol 1e-8); variational bound
+    f = lambda t: ff.energy_trotter(dev, list(t), plan, H, P.hf)  # noqa: E731
+    r = ff.vqe_minimize(f, list(P.thetas[0]), "powell")
+    assert r.converged and r.energy < e
+    from dense import psum_dense
+
+    E0 = np.linalg.eigvalsh(psum_dense(8, *P.H.arrays()))[0]
+    assert r.energy >= E0 - 1e-10
+    assert dev.kernel_launches() > 0

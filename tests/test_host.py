@@ -1,0 +1,168 @@
+"""Host-side logic of the product (C++ operator API via pybind11, no device):
+compared term-by-term against the independent C oracle."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_2402_17993_b200 as ff
+from paper_2402_17993_b200 import capi, problems
+
+
+@pytest.mark.parametrize("m,ne", [(2, 2), (4, 4), (6, 6), (9, 10)])
+def test_hamiltonian_and_generators_match_oracle(oracle, m, ne):
+    seed = problems.ham_seed(1) + m
+    h, g = ff.synthetic_integrals(m, seed)
+    ho, go = oracle.synthetic_integrals(m, seed)
+    assert np.array_equal(h, ho) and np.array_equal(g, go)  # bitwise: same pinned RNG mapping
+    x, z, c = ff.qubit_hamiltonian(h, g, ne).arrays()
+    xo, zo, co = oracle.hamiltonian_jw(ho, go).terms()
+    assert np.array_equal(x, xo) and np.array_equal(z, zo)
+    assert np.abs(c - co).max() < 1e-13
+    gens = ff.build_generators(2 * m, ne)
+    kind, idx = oracle.build_generators(2 * m, ne)
+    assert len(gens) == len(kind)
+    for gen in gens[:: max(1, len(gens) // 40)]:
+        e = gen.exc
+        assert (e.kind, e.i, e.j, e.a, e.b) == (kind[gen.id], *idx[gen.id])
+        gx, gz, gc = gen.image.arrays()
+        ox, oz, oc = oracle.generator_image(2 * m, kind[gen.id], idx[gen.id]).terms()
+        assert np.array_equal(gx, ox) and np.array_equal(gz, oz) and np.abs(gc - oc).max() < 1e-15
+
+
+def test_uniform_vector_matches_oracle(oracle):
+    a = np.array(ff.uniform_vector(77, 1000, -0.1, 0.1))
+    assert np.array_equal(a, oracle.uniform_array(77, 1000, -0.1, 0.1))
+    assert a.min() >= -0.1 and a.max() < 0.1
+
+
+def test_magnitude_order_matches_oracle(oracle):
+    P = problems.config_problem(2)
+    assert list(P.plan.order) == oracle.magnitude_order(P.thetas[0]).tolist()
+    gens = ff.build_generators(4, 2)
+    assert list(ff.magnitude_order(gens, [0.1, -0.3, 0.0], 4).order) == [1, 0, 2]
+
+
+def test_pauli_mul_matches_oracle(oracle):
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        n = int(rng.integers(1, 20))
+        x1, z1, x2, z2 = (int(v) for v in rng.integers(0, 1 << n, 4))
+        k, p = ff.pauli_mul(ff.PauliString(n, x1, z1), ff.PauliString(n, x2, z2))
+        assert (k, p.x, p.z) == oracle.pauli_mul(n, x1, z1, x2, z2)
+
+
+def test_jordan_wigner_api():
+    s = ff.jordan_wigner([(1.0, [(0, True), (0, False)])], 2)
+    assert s.to_text().split("\n")[:2] == ["0.5 0 II", "-0.5 0 ZI"]
+    t = ff.PauliSum.from_text(s.to_text())
+    assert np.array_equal(t.arrays()[0], s.arrays()[0])
+    with pytest.raises(ff.ContractViolation):
+        ff.jordan_wigner([(1.0, [(5, True)])], 4)
+    assert ff.PauliString.parse("XZIY").letters() == "XZIY"
+    assert ff.PauliString.parse("XZIY").x == 0b1001
+
+
+def test_plan_compile_fuses_every_uccsd_generator():
+    for c in (1, 2, 3):
+        P = problems.config_problem(c)
+        st = capi.plan_compile_stats(P.n_qubits, *P.plan_arrays())
+        assert st["fused"] == P.n_gen and st["string_ops"] == 0 and st["pattern_pairs"] == P.n_gen
+        n = P.n_qubits
+        n_single = sum(1 for gen in P.gens if gen.exc.kind == 1)
+        # singles update 1/4 of the pairs' index space (pattern 10 <-> 01), doubles 1/16
+        assert st["pair_updates"] == n_single * (1 << (n - 2)) + (P.n_gen - n_single) * (1 << (n - 4))
+
+
+def test_plan_compile_falls_back_to_strings_for_noncommuting_generator():
+    # X0 and Y0 Z1 share no flip mask pattern that commutes -> string mode
+    off = np.array([0, 2], np.int64)
+    x = np.array([1, 1], np.uint64)
+    z = np.array([0, 3], np.uint64)
+    st = capi.plan_compile_stats(2, off, x, z, np.array([0.3j, 0.2j]))
+    assert st["fused"] == 0 and st["string_ops"] == 2
+    with pytest.raises(ff.ContractViolation):
+        capi.plan_compile_stats(2, off, x, z, np.array([0.3, 0.2j]))  # not anti-Hermitian
+
+
+def test_ham_compile_stats_and_hermiticity():
+    P = problems.config_problem(3)
+    st = capi.ham_compile_stats(18, *P.ham_arrays())
+    assert st["groups"] == 1621 and st["terms"] == 9316
+    with pytest.raises(ff.ContractViolation):
+        capi.ham_compile_stats(2, [1], [0], [0.5j])
+
+
+def test_capi_library_exports_every_header_symbol():
+    L = ctypes.CDLL(ff.native_library_path())
+    syms = capi.header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    assert capi.lib().ffq_version() == 1
+
+
+def test_no_device_fails_loudly():
+    if ff.Device.count() > 0:
+        pytest.skip("a device is present")
+    with pytest.raises(ff.DeviceError):
+        ff.Device(0)
+    h = ctypes.c_void_p()
+    assert capi.lib().ffq_ctx_create(0, ctypes.byref(h)) == capi.FFQ_ENODEV
+
+
+def test_optimizers_quadratic_and_rosenbrock():
+    c = np.array([0.3, -1.2, 2.0])
+    f = lambda x: float(np.sum((np.asarray(x) - c) ** 2))  # noqa: E731
+    for meth in ("powell", "neldermead"):
+        r = ff.vqe_minimize(f, [0.0, 0.0, 0.0], meth)
+        assert r.converged and np.abs(np.array(r.x) - c).max() < 1e-3 and r.n_evals < 2000
+    rosen = lambda x: (1 - x[0]) ** 2 + 100 * (x[1] - x[0] ** 2) ** 2  # noqa: E731
+    o = ff.OptimizerOptions()
+    o.ftol = 1e-14
+    o.xtol = 1e-9
+    r = ff.powell_minimize(rosen, [-1.2, 1.0], o)
+    assert np.abs(np.array(r.x) - 1).max() < 1e-5
+
+
+def test_exact_gradient_rule_on_trig_polynomial():
+    # E(t) with frequencies {1, 2}: the four-term rule is exact
+    rng = np.random.default_rng(0)
+    a = rng.normal(size=(3, 5))
+
+    def E(th):
+        th = np.asarray(th)
+        return float(sum(a[0, k] * np.cos(th[k]) + a[1, k] * np.sin(th[k]) + a[2, k] * np.sin(2 * th[k] + 0.3)
+                         for k in range(5)))
+
+    th = rng.normal(size=5)
+    rows = np.array(ff.exact_gradient_set(list(th))).reshape(-1, 5)
+    g = ff.exact_gradient_from_energies([E(r) for r in rows], 5)
+    ga = [-a[0, k] * np.sin(th[k]) + a[1, k] * np.cos(th[k]) + 2 * a[2, k] * np.cos(2 * th[k] + 0.3) for k in range(5)]
+    assert np.abs(np.array(g) - ga).max() < 1e-12
+    ps = np.array(ff.parameter_shift_set(list(th))).reshape(-1, 5)
+    assert ps.shape == (11, 5) and np.array_equal(ps[0], th)
+
+
+def test_bfgs_with_batched_objective():
+    c = np.array([0.2, -0.1])
+
+    def fb(X, B):
+        X = np.asarray(X).reshape(B, 2)
+        return list(np.sum(np.sin(X - c) ** 2, axis=1))
+
+    r = ff.bfgs_minimize(fb, [0.5, 0.4])
+    assert r.converged and np.abs(np.array(r.x) - c).max() < 1e-4
+
+
+def test_fmo_assembly_matches_reference_golden():
+    # proj/tests/test_fmo.cpp:182-185
+    mono = {"1": -0.026884, "2": -0.026164, "3": -0.026899}
+    dim = {"21": -0.049880, "31": -0.051554, "32": -0.051952}
+    assert abs(ff.assemble_two_body(3, mono, dim) - (-0.073439)) <= 1e-9
+    assert ff.dimer_labels(3) == ["21", "31", "32"]
+    bad = dict(dim)
+    bad.pop("21")
+    with pytest.raises(ff.ContractViolation):
+        ff.assemble_two_body(3, mono, bad)
