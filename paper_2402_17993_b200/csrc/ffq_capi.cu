@@ -23,6 +23,7 @@
 #include "../../include/fragfield_cuda.h"
 #include "ffq_compile.hpp"
 #include "ffq_kernels.cuh"
+#include "ffq_sparse.cuh"
 
 using namespace ffq;
 
@@ -83,11 +84,15 @@ struct ffq_ctx_s {
   int n_sm = 148;
   size_t smem_optin = 0;
   int smem_max_qubits = kSmemMaxQubitsDefault;  // env FFQ_SMEM_MAX_QUBITS overrides
+  int tile_bits = kDefaultTileBits;              // env FFQ_TILE_BITS (0 disables tiling)
+  int64_t slab_bytes = 256LL << 20;              // env FFQ_SLAB_MB: batch chunk of the graph path
+  int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
+  DevBuf<uint32_t> slab_sup;
   double* pinned = nullptr;
   size_t pinned_n = 0;
   void ensure_pinned(size_t n) {
@@ -109,6 +114,7 @@ struct ffq_plan_s {
   DevBuf<double> op_cfac, op_sscale;
   DevBuf<FusedDesc> fused;
   DevBuf<uint64_t> pair_bits, str_x, str_z;
+  DevBuf<uint32_t> pair_low;
   DevBuf<double2> pair_f;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int64_t> graph_nodes;
@@ -134,6 +140,13 @@ struct ffq_ham_s {
   DevBuf<double2> cls_f;
   DevBuf<int32_t> item_g, item_p;
   DevBuf<int64_t> item_u0;
+  DevBuf<uint32_t> bucket_h, titem_u, act_low;
+  DevBuf<int32_t> bucket_goff, bucket_groups, titem_bucket, sitem_g, sitem_p;
+  DevBuf<int64_t> sitem_w0;
+  int64_t n_partials(bool support) const {
+    if (support) return (int64_t)ch.sitem_g.size();
+    return ch.tile_bits ? (int64_t)ch.titem_u.size() : (int64_t)ch.item_g.size();
+  }
   HamDev dev() const {
     HamDev d;
     d.n_groups = (int)ch.groups.size();
@@ -141,6 +154,9 @@ struct ffq_ham_s {
     d.n_items = (int64_t)ch.item_g.size();
     d.item_g = item_g.p; d.item_p = item_p.p; d.item_u0 = item_u0.p;
     d.item_chunk = ch.item_chunk;
+    d.tile_bits = ch.tile_bits;
+    d.bucket_h = bucket_h.p; d.bucket_goff = bucket_goff.p; d.bucket_groups = bucket_groups.p;
+    d.titem_bucket = titem_bucket.p; d.titem_u = titem_u.p;
     return d;
   }
 };
@@ -149,6 +165,8 @@ struct ffq_state_s {
   ffq_ctx_t ctx;
   int n = 0, batch = 0;
   DevBuf<double2> psi;
+  DevBuf<uint32_t> sup;   // support bitmap [batch][2^(n-5)] (support mode only)
+  bool sup_valid = false; // false after a dense pass: rebuilt lazily from the data
 };
 
 namespace {
@@ -188,6 +206,15 @@ int grid_for(int64_t work, int n_sm, int per_sm = 8) {
 template <typename T>
 std::vector<T> as_vec(const T* p, size_t n) { return std::vector<T>(p, p + n); }
 
+bool use_support(ffq_ctx_t ctx, int n) { return ctx->support && n >= 6 && n <= 32; }
+
+void launch_support_from_state(ffq_ctx_t ctx, const double2* psi, uint32_t* sup, int n, int batch) {
+  const int64_t total = (int64_t)batch << n;
+  k_support_from_state<<<grid_for(total, ctx->n_sm), kThreads, 0, ctx->stream>>>(psi, sup, total);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
 // rotation-pass dispatch for a single string (state API and plan string ops)
 void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, uint64_t z, int ny,
                    const double2* cs, int cs_stride, int op) {
@@ -205,8 +232,17 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
   ctx->launches++;
 }
 
-void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, int n, int batch,
+void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* sup, int n, int batch,
                   const FusedDesc& d, const double2* cs, int cs_stride, int op) {
+  if (sup) {
+    const int64_t work = (int64_t)d.npair << (n - 5 - d.whi);
+    dim3 grid(grid_for(work, ctx->n_sm), batch);
+    k_fused_gen_support<<<grid, kThreads, 0, ctx->stream>>>(psi, sup, n, d, pl->pair_bits.p, pl->pair_low.p,
+                                                            pl->pair_f.p, cs, cs_stride, op);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   const bool vec = !(d.x & 1ULL) && (n - d.w) >= 1;
   const int64_t work = ((int64_t)d.npair << (n - d.w)) >> (vec ? 1 : 0);
   dim3 grid(grid_for(work, ctx->n_sm), batch);
@@ -221,18 +257,28 @@ void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, int n, int 
 }
 
 // apply every op of the plan to a [batch][2^n] slab; cs already computed
-void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, int batch, const double2* cs) {
+// sup != nullptr: support-tracked fused passes; string ops are dense and are
+// followed by an exact support rebuild before the next support-tracked op
+void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* sup, int batch,
+                  const double2* cs) {
   const CompiledPlan& cp = pl->cp;
   const int n = cp.n_qubits;
   const int n_ops = (int)cp.op_kind.size();
+  bool stale = false;
   for (int op = 0; op < n_ops; ++op) {
     if (cp.op_kind[op] == 0) {
-      launch_fused(ctx, pl, psi, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op);
+      if (sup && stale) {
+        launch_support_from_state(ctx, psi, sup, n, batch);
+        stale = false;
+      }
+      launch_fused(ctx, pl, psi, sup, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op);
     } else {
       const int si = cp.op_idx[op];
       launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
+      stale = true;
     }
   }
+  if (sup && stale) launch_support_from_state(ctx, psi, sup, n, batch);
 }
 
 void launch_cs(ffq_ctx_t ctx, const ffq_plan_s* pl, const double* theta, int batch, double2* cs) {
@@ -245,20 +291,45 @@ void launch_cs(ffq_ctx_t ctx, const ffq_plan_s* pl, const double* theta, int bat
   ctx->launches++;
 }
 
-void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, int n, int batch,
-                   double2* partial, double* e, double* im) {
-  const int64_t items = (int64_t)h->ch.item_g.size();
+void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, const uint32_t* sup, int n,
+                   int batch, double2* partial, double* e, double* im) {
+  const int64_t items = h->n_partials(sup != nullptr);
   if (items == 0) {
     CK(cudaMemsetAsync(e, 0, sizeof(double) * batch, ctx->stream));
     if (im) CK(cudaMemsetAsync(im, 0, sizeof(double) * batch, ctx->stream));
     return;
   }
-  dim3 grid((unsigned)items, batch);
-  k_expect_items<kThreads><<<grid, kThreads, 0, ctx->stream>>>(psi, n, h->dev(), partial);
-  CK(cudaGetLastError());
+  if (sup) {
+    k_expect_support<kThreads><<<dim3((unsigned)items, batch), kThreads, 0, ctx->stream>>>(
+        psi, sup, n, h->dev(), h->sitem_g.p, h->sitem_p.p, h->sitem_w0.p, h->act_low.p, partial);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  } else if (h->ch.tile_bits) {
+    constexpr int NT = 512;
+    const size_t tile = sizeof(double2) << h->ch.tile_bits;
+    CK(cudaFuncSetAttribute(k_expect_tiles<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * tile)));
+    const int64_t n0 = h->ch.n_titems_h0, n1 = items - n0;
+    if (n0 > 0) {
+      k_expect_tiles<NT><<<dim3((unsigned)n0, batch), NT, tile, ctx->stream>>>(psi, n, h->dev(), 0, 0,
+                                                                               partial, items);
+      CK(cudaGetLastError());
+      ctx->launches++;
+    }
+    if (n1 > 0) {
+      k_expect_tiles<NT><<<dim3((unsigned)n1, batch), NT, 2 * tile, ctx->stream>>>(psi, n, h->dev(), n0, 1,
+                                                                                   partial, items);
+      CK(cudaGetLastError());
+      ctx->launches++;
+    }
+  } else {
+    dim3 grid((unsigned)items, batch);
+    k_expect_items<kThreads><<<grid, kThreads, 0, ctx->stream>>>(psi, n, h->dev(), partial);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
   k_reduce_partials<kThreads><<<batch, kThreads, 0, ctx->stream>>>(partial, items, e, im);
   CK(cudaGetLastError());
-  ctx->launches += 2;
+  ctx->launches++;
 }
 
 size_t smem_bytes(const ffq_plan_s* pl) {
@@ -289,11 +360,14 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   }
   // global path: chunk the batch so the slab stays L2-resident (<= 64 MiB)
   const int64_t dim = 1LL << n;
-  const int64_t slab_cap = (64LL << 20) / (dim * (int64_t)sizeof(double2));
+  const int64_t slab_cap = ctx->slab_bytes / (dim * (int64_t)sizeof(double2));
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(batch, std::max<int64_t>(1, slab_cap)));
   const int n_ops = (int)pl->cp.op_kind.size();
-  const int64_t items = (int64_t)h->ch.item_g.size();
+  const bool sp = use_support(ctx, n);
+  const int64_t items = h->n_partials(sp);
   ctx->slab.alloc((size_t)chunk * dim);
+  if (sp) ctx->slab_sup.alloc((size_t)chunk * (dim >> 5));
+  uint32_t* sup = sp ? ctx->slab_sup.p : nullptr;
   ctx->cs.alloc((size_t)chunk * std::max(1, n_ops));
   ctx->partial.alloc((size_t)chunk * std::max<int64_t>(1, items));
   ctx->theta.alloc((size_t)chunk * std::max(1, pl->cp.n_gen));
@@ -301,7 +375,7 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   ctx->eim.alloc(chunk);
   GraphKey key{(uintptr_t)h, (uintptr_t)chunk, (uintptr_t)hf, (uintptr_t)ctx->theta.p,
                (uintptr_t)ctx->slab.p, (uintptr_t)ctx->cs.p, (uintptr_t)ctx->partial.p,
-               (uintptr_t)ctx->eout.p, (uintptr_t)ctx->eim.p};
+               (uintptr_t)ctx->eout.p, (uintptr_t)ctx->eim.p, (uintptr_t)sup};
   auto it = pl->graphs.find(key);
   if (it == pl->graphs.end()) {
     cudaGraph_t graph;
@@ -311,9 +385,14 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
       k_set_basis<<<grid_for(dim * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(ctx->slab.p, dim,
                                                                                  chunk, hf);
       ctx->launches++;
+      if (sup) {
+        k_support_basis<<<grid_for((dim >> 5) * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+            sup, dim >> 5, chunk, hf);
+        ctx->launches++;
+      }
       launch_cs(ctx, pl, ctx->theta.p, chunk, ctx->cs.p);
-      run_plan_ops(ctx, pl, ctx->slab.p, chunk, ctx->cs.p);
-      launch_expect(ctx, h, ctx->slab.p, n, chunk, ctx->partial.p, ctx->eout.p, ctx->eim.p);
+      run_plan_ops(ctx, pl, ctx->slab.p, sup, chunk, ctx->cs.p);
+      launch_expect(ctx, h, ctx->slab.p, sup, n, chunk, ctx->partial.p, ctx->eout.p, ctx->eim.p);
     } catch (...) {
       cudaStreamEndCapture(ctx->stream, &graph);
       throw;
@@ -344,6 +423,18 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
 }
 
 }  // namespace
+
+// support bitmap of a state, rebuilt from the data if a dense pass left it stale
+uint32_t* state_support(ffq_state_s* st) {
+  ffq_ctx_t ctx = st->ctx;
+  if (!use_support(ctx, st->n)) return nullptr;
+  st->sup.alloc((size_t)st->batch << (st->n - 5));
+  if (!st->sup_valid) {
+    launch_support_from_state(ctx, st->psi.p, st->sup.p, st->n, st->batch);
+    st->sup_valid = true;
+  }
+  return st->sup.p;
+}
 
 extern "C" {
 
@@ -377,6 +468,9 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     c->smem_optin = (size_t)optin - 2048;  // static smem of the reduction scratch
     if (const char* e = std::getenv("FFQ_SMEM_MAX_QUBITS")) c->smem_max_qubits = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
+    if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
     return FFQ_OK;
   });
   if (rc != FFQ_OK) {
@@ -423,7 +517,7 @@ int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t*
   return guarded(ctx, [&] {
     auto h = std::make_unique<ffq_ham_s>();
     h->ctx = ctx;
-    h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im);
+    h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im, ctx->tile_bits);
     const auto& ch = h->ch;
     h->groups.upload(ch.groups, ctx->stream);
     h->act_bits.upload(ch.act_bits, ctx->stream);
@@ -434,6 +528,15 @@ int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t*
     h->item_g.upload(ch.item_g, ctx->stream);
     h->item_p.upload(ch.item_p, ctx->stream);
     h->item_u0.upload(ch.item_u0, ctx->stream);
+    h->bucket_h.upload(ch.bucket_h, ctx->stream);
+    h->bucket_goff.upload(ch.bucket_goff, ctx->stream);
+    h->bucket_groups.upload(ch.bucket_groups, ctx->stream);
+    h->titem_bucket.upload(ch.titem_bucket, ctx->stream);
+    h->titem_u.upload(ch.titem_u, ctx->stream);
+    h->act_low.upload(ch.act_low, ctx->stream);
+    h->sitem_g.upload(ch.sitem_g, ctx->stream);
+    h->sitem_p.upload(ch.sitem_p, ctx->stream);
+    h->sitem_w0.upload(ch.sitem_w0, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     *out = h.release();
     return FFQ_OK;
@@ -475,6 +578,7 @@ int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_
     p->op_sscale.upload(cp.op_sscale, ctx->stream);
     p->fused.upload(cp.fused, ctx->stream);
     p->pair_bits.upload(cp.pair_bits, ctx->stream);
+    p->pair_low.upload(cp.pair_low, ctx->stream);
     std::vector<double2> pf(cp.pair_f.size() / 2);
     for (size_t i = 0; i < pf.size(); ++i) pf[i] = make_double2(cp.pair_f[2 * i], cp.pair_f[2 * i + 1]);
     p->pair_f.upload(pf, ctx->stream);
@@ -578,6 +682,14 @@ int ffq_state_set_basis(ffq_state_t st, uint64_t bits) {
                                                                                    st->batch, bits);
     CK(cudaGetLastError());
     ctx->launches++;
+    if (use_support(ctx, st->n)) {
+      st->sup.alloc((size_t)st->batch << (st->n - 5));
+      k_support_basis<<<grid_for((dim >> 5) * st->batch, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+          st->sup.p, dim >> 5, st->batch, bits);
+      CK(cudaGetLastError());
+      ctx->launches++;
+      st->sup_valid = true;
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     return FFQ_OK;
   });
@@ -588,6 +700,7 @@ int ffq_state_upload(ffq_state_t st, const double* psi) {
   return guarded(st->ctx, [&] {
     CK(cudaMemcpyAsync(st->psi.p, psi, sizeof(double2) * ((size_t)st->batch << st->n),
                        cudaMemcpyHostToDevice, st->ctx->stream));
+    st->sup_valid = false;
     CK(cudaStreamSynchronize(st->ctx->stream));
     return FFQ_OK;
   });
@@ -612,6 +725,7 @@ int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, doubl
     ctx->cs.upload(cs, ctx->stream);
     launch_string(ctx, st->psi.p, st->n, st->batch, x, z, __builtin_popcountll(x & z) & 3, ctx->cs.p,
                   1, 0);
+    st->sup_valid = false;  // dense pass: the support is rebuilt lazily
     CK(cudaStreamSynchronize(ctx->stream));
     return FFQ_OK;
   });
@@ -629,7 +743,7 @@ int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta) {
                        cudaMemcpyHostToDevice, ctx->stream));
     ctx->cs.alloc((size_t)n_ops * st->batch);
     launch_cs(ctx, plan, ctx->theta.p, st->batch, ctx->cs.p);
-    run_plan_ops(ctx, plan, st->psi.p, st->batch, ctx->cs.p);
+    run_plan_ops(ctx, plan, st->psi.p, state_support(st), st->batch, ctx->cs.p);
     CK(cudaStreamSynchronize(ctx->stream));
     return FFQ_OK;
   });
@@ -640,11 +754,12 @@ int ffq_state_expectation(ffq_state_t st, ffq_ham_t ham, double* re_out, double*
   ffq_ctx_t ctx = st->ctx;
   if (ham->ch.n_qubits != st->n) return fail(ctx, FFQ_EINVAL, "Hamiltonian and state qubit counts differ");
   return guarded(ctx, [&] {
-    const int64_t items = (int64_t)ham->ch.item_g.size();
+    uint32_t* sup = state_support(st);
+    const int64_t items = ham->n_partials(sup != nullptr);
     ctx->partial.alloc((size_t)std::max<int64_t>(1, items) * st->batch);
     DevBuf<double> eo;
     eo.alloc(2 * (size_t)st->batch);
-    launch_expect(ctx, ham, st->psi.p, st->n, st->batch, ctx->partial.p, eo.p, eo.p + st->batch);
+    launch_expect(ctx, ham, st->psi.p, sup, st->n, st->batch, ctx->partial.p, eo.p, eo.p + st->batch);
     std::vector<double> host(2 * (size_t)st->batch);
     CK(cudaMemcpyAsync(host.data(), eo.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost,
                        ctx->stream));

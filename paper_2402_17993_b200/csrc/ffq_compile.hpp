@@ -56,11 +56,28 @@ inline uint64_t pattern_bits(uint32_t pi, const int* q, int w) {
 // ---- plan ------------------------------------------------------------------
 struct FusedDesc {  // POD, copied to the device
   uint64_t x, zout;
-  int32_t w, npair, pair_off, pad;
+  int32_t w, npair, pair_off, whi;  // whi: flip bits at positions >= 5 (word-index bits)
   int32_t q[kMaxTableBits];
-  uint64_t qpack;  // q[i] in bits [6i, 6i+6): register-friendly copy for kernels
+  uint64_t qpack;     // q[i] in bits [6i, 6i+6): register-friendly copy for kernels
+  uint64_t qpack_hi;  // positions - 5 of the flip bits >= 5 (support-word insertion)
   double alpha;
 };
+
+// 32-amplitude support words: offsets o in a word whose bits on X & 31 equal
+// those of pattern bits pb
+inline uint32_t low_pattern_mask(uint64_t X, uint64_t pb) {
+  const uint32_t L = (uint32_t)(X & 31u), P = (uint32_t)(pb & 31u) & L;
+  uint32_t m = 0;
+  for (uint32_t o = 0; o < 32; ++o)
+    if ((o & L) == P) m |= 1u << o;
+  return m;
+}
+inline void hi_positions(uint64_t X, int32_t& whi, uint64_t& qpack_hi) {
+  whi = 0;
+  qpack_hi = 0;
+  for (int qb = 5; qb < 64; ++qb)
+    if ((X >> qb) & 1ULL) qpack_hi |= (uint64_t)(qb - 5) << (6 * whi++);
+}
 
 inline uint64_t pack_q(const int32_t* q, int w) {
   uint64_t v = 0;
@@ -78,6 +95,7 @@ struct CompiledPlan {
   std::vector<double> op_sscale; // s = sin(phi) * sscale
   std::vector<FusedDesc> fused;
   std::vector<uint64_t> pair_bits;  // pattern bits of the "low" member
+  std::vector<uint32_t> pair_low;   // low_pattern_mask of each pair's low member
   std::vector<double> pair_f;       // [pair][4]: F[pi] re,im, F[~pi] re,im
   std::vector<uint64_t> str_x, str_z;
   std::vector<int32_t> str_ny;
@@ -134,6 +152,7 @@ inline CompiledPlan compile_plan(int n, int n_gen, const int64_t* off, const uin
       for (int qb = 0; qb < 64; ++qb)
         if ((X >> qb) & 1ULL) d.q[wi++] = qb;
       d.qpack = pack_q(d.q, w);
+      hi_positions(X, d.whi, d.qpack_hi);
       const uint32_t np = 1u << w;
       F.assign(np, cplx(0, 0));
       // F[pi] = <k^X|A|k> / s_out(k) = sum_j (i c_j) i^{ny_j} (-1)^{popc(pibits & z_j)}
@@ -166,6 +185,7 @@ inline CompiledPlan compile_plan(int n, int n_gen, const int64_t* off, const uin
           if (pi > pb) continue;
           if (std::abs(F[pi]) <= tol && std::abs(F[pb]) <= tol) continue;
           P.pair_bits.push_back(pattern_bits(pi, d.q, w));
+          P.pair_low.push_back(low_pattern_mask(X, pattern_bits(pi, d.q, w)));
           P.pair_f.push_back(F[pi].real()); P.pair_f.push_back(F[pi].imag());
           P.pair_f.push_back(F[pb].real()); P.pair_f.push_back(F[pb].imag());
         }
@@ -206,6 +226,8 @@ struct GroupDesc {  // POD
   int32_t val_off;  // into cls_f (complex), layout [cls][nact]
   int32_t q[kMaxTableBits];
   uint64_t qpack;
+  uint64_t qpack_hi;  // flip-bit positions >= 5, minus 5 (support-word insertion)
+  int32_t whi, pad;
 };
 
 struct CompiledHam {
@@ -213,19 +235,37 @@ struct CompiledHam {
   int64_t n_terms = 0;
   std::vector<GroupDesc> groups;
   std::vector<uint64_t> act_bits;
+  std::vector<uint32_t> act_low;  // low_pattern_mask per active pattern
   std::vector<uint64_t> cls_z;
   std::vector<double> cls_f;  // interleaved complex
   // global-path work items (group, active pattern, first u); fixed decomposition
   int64_t item_chunk = 0;
   std::vector<int32_t> item_g, item_p;
   std::vector<int64_t> item_u0;
+  // tiled path: low `tile_bits` qubits form a contiguous tile; groups are
+  // bucketed by their out-of-tile flip pattern h = X >> tile_bits and every
+  // (bucket, tile pair {u, u^h}) is one work item (0 = tiling disabled)
+  int tile_bits = 0;
+  std::vector<uint32_t> bucket_h;
+  std::vector<int32_t> bucket_goff;  // [n_buckets + 1] into bucket_groups
+  std::vector<int32_t> bucket_groups;
+  std::vector<int32_t> titem_bucket;  // items with h == 0 first, then h != 0
+  std::vector<uint32_t> titem_u;
+  int64_t n_titems_h0 = 0;
+  // support-tracked path: items (group, pattern, first support word)
+  std::vector<int32_t> sitem_g, sitem_p;
+  std::vector<int64_t> sitem_w0;
   int64_t n_classes() const { return (int64_t)cls_z.size(); }
 };
 
+constexpr int kDefaultTileBits = 12;
+
 constexpr int64_t kItemChunk = 4096;
+constexpr int64_t kSupportWordsPerItem = 2048;
 
 inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint64_t* z,
-                               const double* cr, const double* ci) {
+                               const double* cr, const double* ci,
+                               int tile_bits = kDefaultTileBits) {
   if (n < 1 || n > 40) throw BadInput("hamiltonian: n_qubits out of range [1, 40]", -1);
   const uint64_t full = (1ULL << n) - 1ULL;
   std::map<uint64_t, std::map<uint64_t, double>> byx;  // x -> z -> real coefficient
@@ -296,7 +336,10 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
       }
       if (act.empty()) continue;
       d.nact = (int32_t)act.size();
-      for (uint32_t pi : act) H.act_bits.push_back(pattern_bits(pi, d.q, w));
+      for (uint32_t pi : act) {
+        H.act_bits.push_back(pattern_bits(pi, d.q, w));
+        H.act_low.push_back(low_pattern_mask(X, pattern_bits(pi, d.q, w)));
+      }
       int ci2 = 0;
       for (auto& c : cls) {
         bool used = false;
@@ -317,6 +360,7 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
       d.qpack = pack_q(d.q, 1);
       d.nact = 1;
       H.act_bits.push_back(0);
+      H.act_low.push_back(low_pattern_mask(X & (1ULL << d.q[0]), 0));
       const uint64_t keep = ~(1ULL << d.q[0]);
       for (auto& t : terms) {
         const cplx f = wgt * t.second * ipow(popc64(X & t.first));
@@ -326,6 +370,8 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
       }
     }
     d.ncls = (int32_t)H.cls_z.size() - d.cls_off;
+    // support words: generic mode inserts only q[0], so only that bit is fixed
+    hi_positions(d.w == popc64(X) ? X : (X & (1ULL << d.q[0])), d.whi, d.qpack_hi);
     H.groups.push_back(d);
   }
   // fixed work decomposition for the global (large-state) path
@@ -338,6 +384,47 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
         H.item_g.push_back((int32_t)g);
         H.item_p.push_back(p);
         H.item_u0.push_back(u0);
+      }
+  }
+  // support-tracked decomposition: fixed word ranges per (group, pattern)
+  if (n >= 6) {
+    for (size_t g = 0; g < H.groups.size(); ++g) {
+      const auto& d = H.groups[g];
+      const int64_t W = 1LL << (n - 5 - d.whi);
+      for (int p = 0; p < d.nact; ++p)
+        for (int64_t w0 = 0; w0 < W; w0 += kSupportWordsPerItem) {
+          H.sitem_g.push_back((int32_t)g);
+          H.sitem_p.push_back(p);
+          H.sitem_w0.push_back(w0);
+        }
+    }
+  }
+  // tiled decomposition (table-mode groups only, n <= 32, at least one out bit)
+  bool tileable = tile_bits > 0 && n > tile_bits && n <= 32;
+  for (const auto& d : H.groups)
+    if (popc64(d.x) > kMaxTableBits) tileable = false;
+  if (tileable) {
+    H.tile_bits = tile_bits;
+    std::map<uint32_t, std::vector<int32_t>> buckets;
+    for (size_t g = 0; g < H.groups.size(); ++g)
+      buckets[(uint32_t)(H.groups[g].x >> tile_bits)].push_back((int32_t)g);
+    H.bucket_goff.push_back(0);
+    for (auto& b : buckets) {
+      H.bucket_h.push_back(b.first);
+      H.bucket_groups.insert(H.bucket_groups.end(), b.second.begin(), b.second.end());
+      H.bucket_goff.push_back((int32_t)H.bucket_groups.size());
+    }
+    const uint32_t n_out = 1u << (n - tile_bits);
+    for (int pass = 0; pass < 2; ++pass)
+      for (size_t b = 0; b < H.bucket_h.size(); ++b) {
+        const uint32_t h = H.bucket_h[b];
+        if ((pass == 0) != (h == 0)) continue;
+        for (uint32_t u = 0; u < n_out; ++u)
+          if (h == 0 || u < (u ^ h)) {
+            H.titem_bucket.push_back((int32_t)b);
+            H.titem_u.push_back(u);
+          }
+        if (pass == 0) H.n_titems_h0 = (int64_t)H.titem_u.size();
       }
   }
   return H;

@@ -185,3 +185,39 @@ def test_cpp_facade_energy_and_vqe(oracle):
     E0 = np.linalg.eigvalsh(psum_dense(8, *P.H.arrays()))[0]
     assert r.energy >= E0 - 1e-10
     assert dev.kernel_launches() > 0
+
+
+def test_support_tracked_matches_dense_passes(monkeypatch):
+    P = problems.config_problem(3, batch=4)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FFQ_SUPPORT", mode)
+        c = capi.Context(0)
+        plan, ham = upload(c, P)
+        out[mode] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    assert np.abs(out["0"] - out["1"]).max() <= 1e-12
+
+
+def test_dense_random_state_plan_and_expectation_vs_oracle(ctx, oracle):
+    # an arbitrary dense state: the support bitmap is rebuilt from the data
+    P = problems.make_problem(7, 6, problems.ham_seed(9), batch=1, name="m7e6")
+    n = P.n_qubits
+    rng = np.random.default_rng(4)
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi /= np.linalg.norm(psi)
+    plan, ham = upload(ctx, P)
+    st = capi.State(ctx, n, 1)
+    st.upload(psi)
+    st.apply_plan(plan, P.plan_thetas())
+    ref = psi.copy()
+    for gid in P.plan.order:
+        x, z, c = P.gens[gid].image.arrays()
+        for xx, zz, cc in zip(x, z, c):
+            ref = oracle.apply_pauli_rotation(n, ref, int(xx), int(zz), P.thetas[0][gid] * cc.imag)
+    assert np.abs(st.download()[0] - ref).max() <= A_TOL
+    e = st.expectation(ham)[0].real
+    assert abs(e - oracle.expectation(n, ref, oracle_H(oracle, P)).real) <= E_TOL
+    # a dense rotation then a support-tracked expectation on the same state
+    st.rotate(0b101 << 3, 0b11, 0.3)
+    ref = oracle.apply_pauli_rotation(n, ref, 0b101 << 3, 0b11, 0.3)
+    assert abs(st.expectation(ham)[0].real - oracle.expectation(n, ref, oracle_H(oracle, P)).real) <= E_TOL
