@@ -32,6 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "UCCSD energy evals/sec at 18 qubits (c128); rotation-pass HBM GB/s vs peak"
+# ncu --set full of k_pauli_rotation at 28 qubits (profiles/r01): dram__bytes_read.sum
+# + dram__bytes_write.sum per launch (4.294980 + 4.236504 GB); algorithmic = 8.589934592 GB
+ROT_TRAFFIC_BYTES = 8531484000
 UNIT = "evals/s"
 
 
@@ -288,7 +291,9 @@ def main():
                     "d2h_bytes_per_step": int(16 * B)},
             "roofline": {"bound": "hbm", "kernel": "k_pauli_rotation (generic rotation pass)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": ROT_TRAFFIC_BYTES if nq == 28 else None,
+                         "traffic_source": "profiles/r01/ncu_full_summaries.txt (dram read+write per launch)",
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
             "gpu_launches": int(launches),

@@ -87,12 +87,17 @@ struct ffq_ctx_s {
   int tile_bits = kDefaultTileBits;              // env FFQ_TILE_BITS (0 disables tiling)
   int64_t slab_bytes = 256LL << 20;              // env FFQ_SLAB_MB: batch chunk of the graph path
   int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
+  int persist = 0;                               // env FFQ_PERSIST=1: k_eval_persistent instead of the graph path
+  int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
+  int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
   DevBuf<uint32_t> slab_sup;
+  DevBuf<double2> pslab;        // persistent-path slab, all-zero between evaluations
+  bool pslab_clean = false;
   double* pinned = nullptr;
   size_t pinned_n = 0;
   void ensure_pinned(size_t n) {
@@ -336,6 +341,23 @@ size_t smem_bytes(const ffq_plan_s* pl) {
   return ((size_t(1) << pl->cp.n_qubits) + pl->cp.op_kind.size()) * sizeof(double2);
 }
 
+constexpr int kPersistThreadsMax = 1024;
+
+size_t persistent_smem(const ffq_plan_s* pl) {
+  const int n = pl->cp.n_qubits;
+  return (size_t(1) << (n - 5)) * sizeof(uint32_t) + pl->cp.op_kind.size() * sizeof(double2) +
+         (kPersistThreadsMax / 32) * kQ * sizeof(uint64_t);
+}
+
+bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
+  const int n = pl->cp.n_qubits;
+  if (!ctx->persist || !use_support(ctx, n) || n > kPersistMaxQubits) return false;
+  if (persistent_smem(pl) > ctx->smem_optin) return false;
+  for (const auto& g : h->ch.groups)
+    if (g.w != __builtin_popcountll(g.x)) return false;  // generic-mode groups: graph path
+  return true;
+}
+
 bool use_smem_path(ffq_ctx_t ctx, const ffq_plan_s* pl) {
   return pl->cp.n_qubits <= ctx->smem_max_qubits && smem_bytes(pl) <= ctx->smem_optin;
 }
@@ -356,6 +378,49 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
                                                                 im_dev);
     CK(cudaGetLastError());
     ctx->launches++;
+    return;
+  }
+  if (use_persistent(ctx, pl, h)) {
+    const int64_t dim = 1LL << n;
+    const int64_t cap = std::max<int64_t>(1, ctx->persist_bytes / (dim * (int64_t)sizeof(double2)));
+    const int64_t n_chunks = (batch + cap - 1) / cap;
+    const int chunk = (int)((batch + n_chunks - 1) / n_chunks);
+    if (ctx->pslab.n < (size_t)chunk * dim) {
+      ctx->pslab.alloc((size_t)chunk * dim);
+      ctx->pslab_clean = false;
+    }
+    if (!ctx->pslab_clean) {
+      CK(cudaMemsetAsync(ctx->pslab.p, 0, ctx->pslab.n * sizeof(double2), ctx->stream));
+      ctx->pslab_clean = true;
+    }
+    const size_t sb = persistent_smem(pl);
+    auto kern = ctx->persist_nt == 1024 ? k_eval_persistent<1024> : k_eval_persistent<512>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
+    DevBuf<long long> clk;
+    if (clocks) clk.alloc(2 * (size_t)chunk);
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+      const int nb = std::min(chunk, batch - b0);
+      kern<<<nb, ctx->persist_nt, sb, ctx->stream>>>(
+          n, pl->dev(), h->dev(), hf, pl->pair_low.p, h->act_low.p, theta_dev + (int64_t)b0 * pl->cp.n_gen,
+          pl->cp.n_gen, ctx->pslab.p, e_dev + b0, im_dev ? im_dev + b0 : nullptr, nb,
+          clocks ? clk.p : nullptr);
+      if (clocks) {
+        std::vector<long long> hc(2 * (size_t)nb);
+        CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        double g = 0, e = 0;
+        for (int r = 0; r < nb; ++r) { g += (double)hc[2 * r]; e += (double)hc[2 * r + 1]; }
+        std::fprintf(stderr, "[ffq] persistent rows=%d avg cycles: generators %.0f expectation %.0f\n", nb,
+                     g / nb, e / nb);
+      }
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        ctx->pslab_clean = false;
+        throw CudaError(std::string("k_eval_persistent: ") + cudaGetErrorString(e));
+      }
+      ctx->launches++;
+    }
     return;
   }
   // global path: chunk the batch so the slab stays L2-resident (<= 64 MiB)
@@ -471,6 +536,9 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
+    if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     return FFQ_OK;
   });
   if (rc != FFQ_OK) {

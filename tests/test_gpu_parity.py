@@ -187,15 +187,24 @@ def test_cpp_facade_energy_and_vqe(oracle):
     assert dev.kernel_launches() > 0
 
 
-def test_support_tracked_matches_dense_passes(monkeypatch):
-    P = problems.config_problem(3, batch=4)
+@pytest.mark.parametrize("config", [2, 3])
+def test_execution_paths_agree(monkeypatch, config):
+    # dense graph path, support-tracked graph path, persistent per-state path
+    P = problems.config_problem(config, batch=6)
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("FFQ_SUPPORT", mode)
+    for name, env in (("dense", {"FFQ_SUPPORT": "0", "FFQ_PERSIST": "0"}),
+                      ("graph", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "0"}),
+                      ("persistent", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "1"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        monkeypatch.setenv("FFQ_SMEM_MAX_QUBITS", "0")
         c = capi.Context(0)
         plan, ham = upload(c, P)
-        out[mode] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
-    assert np.abs(out["0"] - out["1"]).max() <= 1e-12
+        out[name] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        out[name + "2"] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas()[::-1])[::-1]
+    for name in ("graph", "persistent"):
+        assert np.abs(out[name] - out["dense"]).max() <= 1e-12
+        assert np.array_equal(out[name], out[name + "2"])  # the slab is left clean
 
 
 def test_dense_random_state_plan_and_expectation_vs_oracle(ctx, oracle):

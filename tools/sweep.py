@@ -18,9 +18,16 @@ e = torch.zeros(B, dtype=torch.float64, device="cuda")
 ref = None
 slabs = [int(v) for v in os.environ.get("SWEEP_SLAB", "16,64,256,1024").split(",")]
 tiles = [int(v) for v in os.environ.get("SWEEP_TILE", "12").split(",")]
-for slab, tb in itertools.product(slabs, tiles):
+envs = [e for e in os.environ.get("SWEEP_ENV", "").split(";")]
+base_env = dict(os.environ)
+for slab, tb, env in itertools.product(slabs, tiles, envs):
+    os.environ.clear()
+    os.environ.update(base_env)
     os.environ["FFQ_SLAB_MB"] = str(slab)
     os.environ["FFQ_TILE_BITS"] = str(tb)
+    for kv in filter(None, env.split(",")):
+        k, v = kv.split("=")
+        os.environ[k] = v
     ctx = capi.Context(0)
     plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
     ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
@@ -38,6 +45,6 @@ for slab, tb in itertools.product(slabs, tiles):
     out = e.cpu().numpy()
     if ref is None:
         ref = out.copy()
-    print(json.dumps({"slab_mb": slab, "tile_bits": tb, "ms_per_batch": ms, "evals_per_s": B / ms * 1e3,
+    print(json.dumps({"slab_mb": slab, "tile_bits": tb, "env": env, "ms_per_batch": ms, "evals_per_s": B / ms * 1e3,
                       "max_dev_vs_first": float(np.abs(out - ref).max())}), flush=True)
     del plan, ham, ctx
