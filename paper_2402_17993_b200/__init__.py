@@ -21,7 +21,7 @@ try:
 except ImportError as e:  # pragma: no cover - exercised only on a broken install
     raise ImportError(
         "paper_2402_17993_b200: native library not built "
-        "(run `python -m paper_2402_17993_b200._build`): " + str(e)
+        "(run `python paper_2402_17993_b200/_build.py`): " + str(e)
     ) from e
 
 from .lib._fragfield import (  # noqa: E402,F401
@@ -32,6 +32,7 @@ from .lib._fragfield import (  # noqa: E402,F401
     DeviceHamiltonian,
     DevicePlan,
     Excitation,
+    FragmentProblem,
     Generator,
     OptimizerOptions,
     OptimizeResult,
@@ -39,13 +40,16 @@ from .lib._fragfield import (  # noqa: E402,F401
     PauliSum,
     Statevector,
     TrotterPlan,
+    assemble_fragments,
     assemble_two_body,
     bfgs_minimize,
     build_generators,
     dimer_labels,
     energy_batch,
     energy_trotter,
+    evaluate_fragments,
     exact_gradient_from_energies,
+    fragment_cost,
     exact_gradient_set,
     hf_bits,
     jordan_wigner,
@@ -56,6 +60,7 @@ from .lib._fragfield import (  # noqa: E402,F401
     powell_minimize,
     qubit_hamiltonian,
     random_pauli_hamiltonian,
+    shard_by_cost,
     synthetic_integrals,
     uniform_vector,
 )

@@ -4,7 +4,8 @@ Outputs (git-ignored, but shipped to the GPU box by gpurun):
   lib/libfragfield_cuda.so   C-ABI + sm_100a kernels + C++ host facade
   lib/_fragfield*.so         pybind11 module over the C++ facade
 
-Usage: python -m paper_2402_17993_b200._build [--force]
+Usage: python paper_2402_17993_b200/_build.py [--force]   (by path: the package
+import itself needs the built libraries)
 """
 from __future__ import annotations
 

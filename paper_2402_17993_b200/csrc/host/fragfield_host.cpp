@@ -797,6 +797,54 @@ double assemble_two_body(int n_fragments, const std::map<std::string, double>& m
 
 double FragmentLedger::assemble_corr() const { return assemble_two_body(n_fragments, corr_I, corr_IJ); }
 
+double fragment_cost(const FragmentProblem& f) {
+  std::map<uint64_t, int> groups;
+  for (auto& kv : f.hamiltonian.terms()) groups[kv.first.first] = 1;
+  return std::ldexp(1.0, f.plan.n_qubits) * (double)(f.plan.order.size() + groups.size());
+}
+
+std::vector<int> shard_by_cost(const std::vector<double>& costs, int world) {
+  if (world < 1) throw ContractViolation("shard_by_cost: world must be >= 1");
+  std::vector<int> idx(costs.size()), owner(costs.size(), 0);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return costs[a] > costs[b]; });
+  std::vector<double> load((size_t)world, 0.0);
+  for (int i : idx) {
+    int best = 0;
+    for (int r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[i] = best;
+    load[best] += costs[i];
+  }
+  return owner;
+}
+
+std::map<std::string, double> evaluate_fragments(Device& dev, const std::vector<FragmentProblem>& frags,
+                                                 int rank, int world) {
+  std::vector<double> costs;
+  for (auto& f : frags) costs.push_back(fragment_cost(f));
+  const std::vector<int> owner = shard_by_cost(costs, world);
+  std::map<std::string, double> out;
+  for (size_t i = 0; i < frags.size(); ++i) {
+    if (owner[i] != rank) continue;
+    const FragmentProblem& f = frags[i];
+    DeviceHamiltonian H(dev, f.hamiltonian);
+    DevicePlan P(dev, f.plan);
+    out[f.label] = energy_trotter(dev, f.amplitudes, P, H, f.hf) - f.e_reference;
+  }
+  return out;
+}
+
+double assemble_fragments(int n_fragments, const std::map<std::string, double>& energies,
+                          FragmentLedger* ledger) {
+  FragmentLedger L;
+  L.n_fragments = n_fragments;
+  for (auto& kv : energies) (kv.first.size() == 1 ? L.corr_I : L.corr_IJ)[kv.first] = kv.second;
+  const double e = L.assemble_corr();
+  if (ledger) *ledger = L;
+  return e;
+}
+
 std::vector<std::string> dimer_labels(int n_fragments) {
   std::vector<std::string> out;
   for (int j = 1; j <= n_fragments; ++j)

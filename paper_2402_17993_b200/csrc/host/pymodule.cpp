@@ -218,4 +218,20 @@ PYBIND11_MODULE(_fragfield, m) {
   // ---- FMO ----
   m.def("assemble_two_body", &assemble_two_body);
   m.def("dimer_labels", &dimer_labels);
+  py::class_<FragmentProblem>(m, "FragmentProblem")
+      .def(py::init([](std::string label, const PauliSum& H, const TrotterPlan& plan, uint64_t hf,
+                       std::vector<double> amps, double e_ref) {
+             return FragmentProblem{std::move(label), H, plan, hf, std::move(amps), e_ref};
+           }),
+           py::arg("label"), py::arg("hamiltonian"), py::arg("plan"), py::arg("hf"), py::arg("amplitudes"),
+           py::arg("e_reference") = 0.0)
+      .def_readonly("label", &FragmentProblem::label)
+      .def_readonly("hf", &FragmentProblem::hf)
+      .def_readonly("amplitudes", &FragmentProblem::amplitudes);
+  m.def("fragment_cost", &fragment_cost);
+  m.def("shard_by_cost", &shard_by_cost, py::arg("costs"), py::arg("world"));
+  m.def("evaluate_fragments", &evaluate_fragments, py::arg("device"), py::arg("fragments"),
+        py::arg("rank") = 0, py::arg("world") = 1);
+  m.def("assemble_fragments",
+        [](int nf, const std::map<std::string, double>& e) { return assemble_fragments(nf, e, nullptr); });
 }

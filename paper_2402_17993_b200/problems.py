@@ -91,3 +91,13 @@ def fmo_fragments():
     for k, lab in enumerate(("21", "31", "32")):
         frags[lab] = make_problem(9, 10, ham_seed(4, 10 + k), name=f"dimer{lab}")
     return frags
+
+
+def fmo_fragment_problems():
+    """Config 4 as FragmentProblem objects (C++ FMO batch input)."""
+    from . import FragmentProblem
+
+    out = []
+    for label, P in fmo_fragments().items():
+        out.append(FragmentProblem(label, P.H, P.plan, P.hf, list(P.thetas[0])))
+    return out
