@@ -124,6 +124,32 @@ int ffq_state_expectation(ffq_state_t st, ffq_ham_t ham, double* re_out, double*
 /* Device pointer to the amplitudes (for zero-copy interop in tests/bench). */
 int ffq_state_device_ptr(ffq_state_t st, void** ptr);
 
+/* ---- sharded state (global qubits; BASELINE.json config 5) ----------------- */
+/* A state of n qubits split on n_global physical qubits over R = 2^n_global
+ * ranks. ffq_shard_create keeps all R shards on this context's device
+ * (exchanges are device-side swaps); ffq_shard_create_nccl holds one rank's
+ * shard per process and exchanges half shards over NCCL (ncclSend/ncclRecv)
+ * for global-qubit swaps and whole shards per out-of-shard flip pattern in the
+ * expectation; per-rank partial energies are all-gathered and summed in rank
+ * order. */
+typedef struct ffq_shard_s* ffq_shard_t;
+int ffq_shard_create(ffq_ctx_t ctx, int n_qubits, int n_global, ffq_shard_t* out);
+int ffq_nccl_unique_id(void* id128); /* ncclUniqueId bytes (128) from rank 0 */
+int ffq_shard_create_nccl(ffq_ctx_t ctx, int n_qubits, int n_global, int rank, const void* id128,
+                          ffq_shard_t* out);
+int ffq_shard_destroy(ffq_shard_t sh);
+/* One energy evaluation; theta [n_gen] in plan order (host), e_out on every rank. */
+int ffq_shard_energy(ffq_shard_t sh, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
+                     const double* theta, double* e_out);
+/* Group mode only: the full state in LOGICAL order [2^n][2] after the last evaluation. */
+int ffq_shard_download(ffq_shard_t sh, double* psi);
+/* Swaps performed by the last evaluation and the current logical->physical map [n]. */
+int ffq_shard_info(ffq_shard_t sh, int* last_swaps, int* perm);
+/* Host-only: the swap schedule a plan gets (initial/final permutation, swaps). */
+int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* term_off,
+                       const uint64_t* x, const uint64_t* z, const double* c_re, const double* c_im,
+                       int* init_perm, int* final_perm, int* n_swaps, int* n_steps);
+
 /* ---- host-only diagnostics (no device needed) ----------------------------- */
 /* Compile a Hamiltonian / plan exactly as the upload calls do and report the
  * table shapes. ham stats[8]: groups, terms, classes, active patterns,

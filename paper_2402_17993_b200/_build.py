@@ -25,12 +25,20 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # The image exports CXX=/opt/gcc/bin/g++ (a wrapper); the system toolchain is the one nvcc uses.
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL: the torch-bundled 2.28.9 (headers + libnccl.so.2 in the venv)
+import importlib.util as _ilu
+
+_nv = _ilu.find_spec("nvidia")
+NCCL_DIR = os.path.join(list(_nv.submodule_search_locations)[0], "nccl") if _nv else "/usr"
+NCCL_INC = os.path.join(NCCL_DIR, "include")
+NCCL_LIB = os.path.join(NCCL_DIR, "lib")
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INC,
-                  "-ccbin", CXX]
+                  "-I" + NCCL_INC, "-ccbin", CXX]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-I" + INC, "-I/usr/local/cuda/include"]
 
 CUDA_SOURCES = [os.path.join(CSRC, "ffq_capi.cu")]
-CUDA_DEPS = [os.path.join(CSRC, f) for f in ("ffq_compile.hpp", "ffq_kernels.cuh")] + [
+CUDA_DEPS = [os.path.join(CSRC, f) for f in ("ffq_compile.hpp", "ffq_kernels.cuh", "ffq_sparse.cuh",
+                                               "ffq_shard.inl")] + [
     os.path.join(INC, "fragfield_cuda.h")]
 HOST_SOURCES = [os.path.join(CSRC, "host", "fragfield_host.cpp")]
 HOST_DEPS = [os.path.join(INC, "fragfield", f) for f in os.listdir(os.path.join(INC, "fragfield"))]
@@ -69,7 +77,8 @@ def build(force: bool = False) -> None:
             _run([CXX] + CXXFLAGS + ["-c", src, "-o", o])
         objs.append(o)
     if force or _stale(LIBCUDA, objs):
-        _run([NVCC] + ARCH + ["-shared", "-ccbin", CXX, "-o", LIBCUDA] + objs)
+        _run([NVCC] + ARCH + ["-shared", "-ccbin", CXX, "-o", LIBCUDA] + objs +
+             ["-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB])
     import pybind11
 
     if force or _stale(PYMOD, [PY_SOURCE, LIBCUDA] + HOST_DEPS):

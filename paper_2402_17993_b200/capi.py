@@ -47,6 +47,17 @@ _SIGS = {
     "ffq_state_apply_plan": (C.c_int, [_vp, _vp, _f64p]),
     "ffq_state_expectation": (C.c_int, [_vp, _vp, _f64p, _f64p]),
     "ffq_state_device_ptr": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ffq_shard_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "ffq_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "ffq_shard_create_nccl": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
+    "ffq_shard_destroy": (C.c_int, [_vp]),
+    "ffq_shard_energy": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, C.POINTER(C.c_double)]),
+    "ffq_shard_download": (C.c_int, [_vp, _f64p]),
+    "ffq_shard_info": (C.c_int, [_vp, C.POINTER(C.c_int), np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]),
+    "ffq_shard_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p,
+                                     np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                     np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ffq_ham_compile_stats": (C.c_int, [C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, _i64p]),
     "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
 }
@@ -230,3 +241,55 @@ class State:
         p = _vp()
         check(lib().ffq_state_device_ptr(self.h, C.byref(p)))
         return p.value
+
+
+def shard_schedule(n, n_global, off, x, z, c):
+    """Host-only swap schedule: (init_perm, final_perm, n_swaps, n_steps)."""
+    x, z, re_, im = _terms(x, z, c)
+    off = np.ascontiguousarray(off, np.int64)
+    ip = np.zeros(n, np.int32); fp = np.zeros(n, np.int32)
+    ns = C.c_int(); st = C.c_int()
+    check(lib().ffq_shard_schedule(n, n_global, len(off) - 1, off, x, z, re_, im, ip, fp, C.byref(ns), C.byref(st)))
+    return ip, fp, ns.value, st.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().ffq_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ShardedState:
+    """A state split on n_global physical qubits over 2^n_global ranks.
+    nccl_id=None: every rank on this context's device (group mode);
+    else this process is `rank` of an NCCL communicator."""
+
+    def __init__(self, ctx: Context, n, n_global, rank=None, nccl_id=None):
+        self.ctx, self.n, self.g = ctx, n, n_global
+        h = _vp()
+        if nccl_id is None:
+            check(lib().ffq_shard_create(ctx.h, n, n_global, C.byref(h)), ctx.h)
+        else:
+            check(lib().ffq_shard_create_nccl(ctx.h, n, n_global, rank, nccl_id, C.byref(h)), ctx.h)
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ffq_shard_destroy(self.h)
+            self.h = None
+
+    def energy(self, plan: Plan, ham: Hamiltonian, hf_bits, theta):
+        e = C.c_double()
+        check(lib().ffq_shard_energy(self.h, plan.h, ham.h, hf_bits,
+                                     np.ascontiguousarray(theta, np.float64).ravel(), C.byref(e)), self.ctx.h)
+        return e.value
+
+    def download(self):
+        out = np.zeros(2 << self.n)
+        check(lib().ffq_shard_download(self.h, out), self.ctx.h)
+        return out.view(np.complex128)
+
+    def info(self):
+        sw = C.c_int(); perm = np.zeros(self.n, np.int32)
+        check(lib().ffq_shard_info(self.h, C.byref(sw), perm))
+        return sw.value, perm

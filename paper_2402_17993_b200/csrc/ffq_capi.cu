@@ -140,6 +140,8 @@ struct ffq_plan_s {
 struct ffq_ham_s {
   ffq_ctx_t ctx;
   CompiledHam ch;
+  std::vector<uint64_t> raw_x, raw_z;  // the uploaded terms (sharded path recompiles them)
+  std::vector<double> raw_re, raw_im;
   DevBuf<GroupDesc> groups;
   DevBuf<uint64_t> act_bits, cls_z;
   DevBuf<double2> cls_f;
@@ -253,10 +255,10 @@ void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
   dim3 grid(grid_for(work, ctx->n_sm), batch);
   if (vec)
     k_fused_gen<true><<<grid, kThreads, 0, ctx->stream>>>(psi, n, d, pl->pair_bits.p, pl->pair_f.p,
-                                                          cs, cs_stride, op);
+                                                          cs, cs_stride, op, 0);
   else
     k_fused_gen<false><<<grid, kThreads, 0, ctx->stream>>>(psi, n, d, pl->pair_bits.p,
-                                                           pl->pair_f.p, cs, cs_stride, op);
+                                                           pl->pair_f.p, cs, cs_stride, op, 0);
   CK(cudaGetLastError());
   ctx->launches++;
 }
@@ -586,6 +588,10 @@ int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t*
     auto h = std::make_unique<ffq_ham_s>();
     h->ctx = ctx;
     h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im, ctx->tile_bits);
+    h->raw_x.assign(x, x + n_terms);
+    h->raw_z.assign(z, z + n_terms);
+    h->raw_re.assign(c_re, c_re + n_terms);
+    h->raw_im.assign(c_im, c_im + n_terms);
     const auto& ch = h->ch;
     h->groups.upload(ch.groups, ctx->stream);
     h->act_bits.upload(ch.act_bits, ctx->stream);
@@ -895,3 +901,5 @@ int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, con
 }
 
 }  // extern "C"
+
+#include "ffq_shard.inl"

@@ -431,3 +431,110 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
 }
 
 }  // namespace ffq
+
+namespace ffq {
+
+// ---- sharded state: global-qubit swap schedule -----------------------------------
+// The state of n qubits is split over R = 2^g ranks: physical index bits
+// [0, l) are local (l = n - g), bits [l, n) are the rank. perm[q] = physical
+// position of logical qubit q. An op whose flip mask touches a global
+// position first swaps it with a free local position (pairwise half-shard
+// exchange between ranks r and r ^ (1 << j)); the local position chosen is the
+// one whose logical qubit is next used furthest in the future (Belady).
+struct ShardStep {
+  int kind;      // 0 = swap physical global position gpos (>= l) with local lpos; 1 = apply plan op
+  int gpos, lpos, op;
+};
+
+struct ShardSchedule {
+  int n = 0, g = 0;
+  std::vector<int> init_perm, final_perm;
+  std::vector<ShardStep> steps;
+  int n_swaps() const {
+    int s = 0;
+    for (auto& st : steps) s += st.kind == 0;
+    return s;
+  }
+};
+
+inline uint64_t permute_mask(uint64_t m, const std::vector<int>& perm) {
+  uint64_t r = 0;
+  for (size_t q = 0; q < perm.size(); ++q)
+    if ((m >> q) & 1ULL) r |= 1ULL << perm[q];
+  return r;
+}
+
+// logical flip mask of plan op `op`
+inline uint64_t op_flip_mask(const CompiledPlan& P, int op) {
+  return P.op_kind[op] == 0 ? P.fused[P.op_idx[op]].x : P.str_x[P.op_idx[op]];
+}
+
+inline ShardSchedule schedule_shards(const CompiledPlan& P, int g) {
+  const int n = P.n_qubits, l = n - g;
+  if (g < 0 || l < 2) throw BadInput("shard: need 0 <= n_global <= n_qubits - 2", -1);
+  ShardSchedule S;
+  S.n = n;
+  S.g = g;
+  const int n_ops = (int)P.op_kind.size();
+  // global = the g logical qubits least often flipped by the plan (ties: higher index)
+  std::vector<int> uses(n, 0);
+  for (int op = 0; op < n_ops; ++op)
+    for (int q = 0; q < n; ++q) uses[q] += (op_flip_mask(P, op) >> q) & 1ULL;
+  std::vector<int> order(n);
+  for (int q = 0; q < n; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return uses[a] != uses[b] ? uses[a] < uses[b] : a > b;
+  });
+  std::vector<int> perm(n, -1);
+  std::vector<bool> is_global(n, false);
+  for (int i = 0; i < g; ++i) is_global[order[i]] = true;
+  int nl = 0, ng = 0;
+  for (int q = 0; q < n; ++q) perm[q] = is_global[q] ? l + ng++ : nl++;
+  S.init_perm = perm;
+  std::vector<int> inv(n);
+  for (int q = 0; q < n; ++q) inv[perm[q]] = q;
+  auto next_use = [&](int logical, int from) {
+    for (int op = from; op < n_ops; ++op)
+      if ((op_flip_mask(P, op) >> logical) & 1ULL) return op;
+    return n_ops + n;  // never again
+  };
+  for (int op = 0; op < n_ops; ++op) {
+    const uint64_t X = op_flip_mask(P, op);
+    uint64_t xphys = permute_mask(X, perm);
+    for (int gpos = l; gpos < n; ++gpos) {
+      if (!((xphys >> gpos) & 1ULL)) continue;
+      int best = -1, best_d = -1;
+      for (int lpos = 0; lpos < l; ++lpos) {
+        if ((xphys >> lpos) & 1ULL) continue;
+        const int d = next_use(inv[lpos], op + 1);
+        if (d > best_d) { best_d = d; best = lpos; }
+      }
+      if (best < 0) throw BadInput("shard: flip mask wider than the local qubits", -1);
+      S.steps.push_back({0, gpos, best, -1});
+      const int qa = inv[gpos], qb = inv[best];
+      std::swap(perm[qa], perm[qb]);
+      inv[perm[qa]] = qa;
+      inv[perm[qb]] = qb;
+      xphys = permute_mask(X, perm);
+    }
+    S.steps.push_back({1, -1, -1, op});
+  }
+  S.final_perm = perm;
+  return S;
+}
+
+// Plan op descriptors mapped to physical positions (pattern tables unchanged:
+// they are attached to pattern pairs, whose bits are permuted with the masks).
+inline FusedDesc physical_fused(const FusedDesc& d, const std::vector<int>& perm) {
+  FusedDesc p = d;
+  p.x = permute_mask(d.x, perm);
+  p.zout = permute_mask(d.zout, perm);
+  int wi = 0;
+  for (int qb = 0; qb < 64; ++qb)
+    if ((p.x >> qb) & 1ULL) p.q[wi++] = qb;
+  p.qpack = pack_q(p.q, p.w);
+  hi_positions(p.x, p.whi, p.qpack_hi);
+  return p;
+}
+
+}  // namespace ffq

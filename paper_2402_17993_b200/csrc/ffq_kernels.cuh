@@ -200,12 +200,13 @@ __global__ void __launch_bounds__(256) k_pauli_rotation(double2* __restrict__ ps
 // ---- fused generator: exp(theta A) on the active patterns of X ----------------
 // pair (k, kb = k ^ X), k = insert(u) | bits(pi_lo):
 //   new[k]  = c a + s' sgn_out(k) F[pi_hi] b,  new[kb] = c b + s' sgn_out(k) F[pi_lo] a
+// sign_base: rank bits of a shard (k | sign_base is the full index), 0 unsharded
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_fused_gen(double2* __restrict__ psi, int n, FusedDesc d,
                                                    const uint64_t* __restrict__ pair_bits,
                                                    const double2* __restrict__ pair_f,
                                                    const double2* __restrict__ cs, int cs_stride,
-                                                   int op) {
+                                                   int op, uint64_t sign_base) {
   const int b = blockIdx.y;
   double2* s = psi + ((int64_t)b << n);
   const double2 csv = cs[(int64_t)b * cs_stride + op];
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(256) k_fused_gen(double2* __restrict__ psi, in
       if (a0.x == 0.0 && a0.y == 0.0 && a1.x == 0.0 && a1.y == 0.0 && b0.x == 0.0 && b0.y == 0.0 &&
           b1.x == 0.0 && b1.y == 0.0)
         continue;
-      const double g0 = sn * sgn_par(k & d.zout), g1 = sn * sgn_par((k + 1) & d.zout);
+      const double g0 = sn * sgn_par((k | sign_base) & d.zout), g1 = sn * sgn_par(((k + 1) | sign_base) & d.zout);
       const double2 hb0 = cmul(fhi, b0), hb1 = cmul(fhi, b1);
       const double2 la0 = cmul(flo, a0), la1 = cmul(flo, a1);
       st256(s + k, make_double2(c * a0.x + g0 * hb0.x, c * a0.y + g0 * hb0.y),
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(256) k_fused_gen(double2* __restrict__ psi, in
       const uint64_t kb = k ^ d.x;
       const double2 a = s[k], bb = s[kb];
       if (a.x == 0.0 && a.y == 0.0 && bb.x == 0.0 && bb.y == 0.0) continue;
-      const double g = sn * sgn_par(k & d.zout);
+      const double g = sn * sgn_par((k | sign_base) & d.zout);
       const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
       s[k] = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
       s[kb] = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
@@ -324,6 +325,83 @@ __global__ void __launch_bounds__(NT) k_reduce_partials(const double2* __restric
   if (threadIdx.x == 0) {
     e_out[b] = acc.x;
     if (im_out) im_out[b] = acc.y;
+  }
+}
+
+// ---- sharded expectation -------------------------------------------------------
+// One rank's contribution for the groups of one out-of-shard flip pattern hG:
+// items (group, pattern, chunk); the enumerated member m lives on this rank
+// (its pattern's rank bits must equal this rank's bits on hG), its partner
+// m ^ X lives at local index m_local ^ X_local on rank r ^ hG (`partner`).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_expect_shard(const double2* __restrict__ own,
+                                                     const double2* __restrict__ partner, int l,
+                                                     uint32_t rank, HamDev h, int64_t item0,
+                                                     double2* __restrict__ partial) {
+  __shared__ double2 red[NT / 32];
+  const int64_t item = item0 + blockIdx.x;
+  const int g = h.item_g[item], p = h.item_p[item];
+  const int64_t u0 = h.item_u0[item];
+  const GroupDesc d = h.groups[g];
+  const uint64_t lmask = (1ULL << l) - 1ULL;
+  const uint64_t XL = d.x & lmask;
+  const uint32_t hG = (uint32_t)(d.x >> l);
+  const uint64_t pb = h.act_bits[d.act_off + p];
+  double acc = 0.0;
+  if ((rank & hG) == (uint32_t)(pb >> l)) {
+    const int wl = __popcll(XL);
+    const int64_t U = 1LL << (l - wl);
+    const int64_t u1 = min(U, u0 + h.item_chunk);
+    const uint64_t base = (uint64_t)rank << l;
+    for (int64_t u = u0 + threadIdx.x; u < u1; u += NT) {
+      const uint64_t ml = insert_bits<uint64_t>((uint64_t)u, d.qpack, wl) | (pb & lmask);
+      const double2 a = own[ml];
+      if (a.x == 0.0 && a.y == 0.0) continue;
+      const double2 bb = partner[ml ^ XL];
+      const uint64_t m = base | ml;
+      double fx = 0.0, fy = 0.0;
+      for (int o = 0; o < d.ncls; ++o) {
+        const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);
+        const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
+        fx = fma(sg, fo.x, fx);
+        fy = fma(sg, fo.y, fy);
+      }
+      const double prx = bb.x * a.x + bb.y * a.y, pry = bb.x * a.y - bb.y * a.x;
+      acc = fma(prx, fx, acc);
+      acc = fma(-pry, fy, acc);
+    }
+  }
+  const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
+  if (threadIdx.x == 0) partial[item] = tot;
+}
+
+// ---- global-qubit swap ------------------------------------------------------------
+// Pack / unpack the half shard whose local bit `lpos` differs from this rank's
+// bit `gbit` (it moves to the partner r ^ (1 << gbit)); in-place after exchange.
+__global__ void k_swap_pack(const double2* __restrict__ s, double2* __restrict__ buf, int l, int lpos,
+                            int val) {
+  const int64_t half = 1LL << (l - 1);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < half;
+       u += (int64_t)gridDim.x * blockDim.x)
+    buf[u] = s[insert_zero<uint64_t>((uint64_t)u, lpos) | ((uint64_t)val << lpos)];
+}
+__global__ void k_swap_unpack(double2* __restrict__ s, const double2* __restrict__ buf, int l, int lpos,
+                              int val) {
+  const int64_t half = 1LL << (l - 1);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < half;
+       u += (int64_t)gridDim.x * blockDim.x)
+    s[insert_zero<uint64_t>((uint64_t)u, lpos) | ((uint64_t)val << lpos)] = buf[u];
+}
+// both ranks of a pair on one device: exchange in place
+__global__ void k_swap_pair(double2* __restrict__ s0, double2* __restrict__ s1, int l, int lpos) {
+  const int64_t half = 1LL << (l - 1);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < half;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = insert_zero<uint64_t>((uint64_t)u, lpos);
+    const uint64_t k0 = k | (1ULL << lpos), k1 = k;  // rank bit 0 sends lpos=1, rank bit 1 sends lpos=0
+    const double2 t = s0[k0];
+    s0[k0] = s1[k1];
+    s1[k1] = t;
   }
 }
 

@@ -1,0 +1,419 @@
+// ffq_shard.inl -- sharded state vector (BASELINE.json config 5).
+// Included at the end of ffq_capi.cu (same translation unit).
+//
+// A state of n qubits is split on its g highest *physical* qubits over
+// R = 2^g ranks; rank r holds the 2^l amplitudes (l = n - g) whose physical
+// index is (r << l) | k. Plan ops whose flip mask reaches a global position
+// are preceded by a qubit swap with a free local position (schedule_shards):
+// ranks r and r ^ (1 << j) exchange the half shard whose local bit differs
+// from their rank bit. Z on global qubits is a per-rank sign (sign_base).
+// The expectation exchanges whole shards once per distinct out-of-shard flip
+// pattern hG and evaluates that bucket of x-groups locally.
+//
+// Transport: "group" mode keeps all R shards on one device (exchanges are
+// device-side swaps; used for 1-GPU validation); "nccl" mode is one shard per
+// process with ncclSend/ncclRecv over NVLink and an allgather of the per-rank
+// partial energies summed in rank order (deterministic).
+#include <nccl.h>
+
+struct ffq_shard_s {
+  ffq_ctx_t ctx = nullptr;
+  int n = 0, g = 0, l = 0, R = 1;
+  int rank = -1;  // nccl mode: this process's rank; group mode: -1
+  std::vector<std::unique_ptr<DevBuf<double2>>> shards;  // group: R, nccl: 1
+  DevBuf<double2> sendbuf, recvbuf;
+  DevBuf<double2> cs, partial;
+  DevBuf<double> eloc;
+  DevBuf<uint64_t> pbits;
+  ncclComm_t comm = nullptr;
+  std::vector<int> perm;
+  int last_swaps = 0;
+  // cache: physical Hamiltonian per (ham, final perm)
+  const void* ham_key = nullptr;
+  std::vector<int> ham_perm;
+  std::unique_ptr<ffq_ham_s> hphys;
+  ~ffq_shard_s() {
+    if (comm) ncclCommDestroy(comm);
+  }
+  bool group() const { return rank < 0; }
+  int n_local() const { return group() ? R : 1; }
+  int rank_of(int i) const { return group() ? i : rank; }
+};
+
+namespace {
+
+#define NCK(call)                                                                      \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      throw NcclError(std::string(#call) + ": " + ncclGetErrorString(r_));             \
+  } while (0)
+
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int guarded_shard(ffq_ctx_t ctx, F&& f) {
+  try {
+    return guarded(ctx, f);
+  } catch (const NcclError& e) {
+    return fail(ctx, FFQ_ENCCL, e.what());
+  }
+}
+
+void shard_alloc(ffq_shard_s* sh) {
+  const size_t dim = size_t(1) << sh->l;
+  for (int i = 0; i < sh->n_local(); ++i) {
+    sh->shards.emplace_back(new DevBuf<double2>());
+    sh->shards.back()->alloc(dim);
+  }
+  if (!sh->group()) {
+    sh->sendbuf.alloc(dim);
+    sh->recvbuf.alloc(dim);
+  }
+}
+
+// swap physical global position gpos with local lpos on every rank pair
+void shard_swap(ffq_shard_s* sh, int gpos, int lpos) {
+  ffq_ctx_t ctx = sh->ctx;
+  const int j = gpos - sh->l;
+  const int64_t half = 1LL << (sh->l - 1);
+  const int grid = grid_for(half, ctx->n_sm);
+  if (sh->group()) {
+    // same pack/unpack kernels as the NCCL transport, with a device copy as the wire
+    sh->sendbuf.alloc((size_t)2 * half);
+    sh->recvbuf.alloc((size_t)2 * half);
+    for (int r = 0; r < sh->R; ++r) {
+      if ((r >> j) & 1) continue;
+      const int r1 = r ^ (1 << j);
+      k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r]->p, sh->sendbuf.p, sh->l, lpos, 1);
+      k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r1]->p, sh->sendbuf.p + half, sh->l, lpos, 0);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(sh->recvbuf.p, sh->sendbuf.p + half, sizeof(double2) * half, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      CK(cudaMemcpyAsync(sh->recvbuf.p + half, sh->sendbuf.p, sizeof(double2) * half, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r]->p, sh->recvbuf.p, sh->l, lpos, 1);
+      k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r1]->p, sh->recvbuf.p + half, sh->l, lpos, 0);
+      CK(cudaGetLastError());
+      ctx->launches += 4;
+    }
+    return;
+  }
+  const int bit = (sh->rank >> j) & 1, partner = sh->rank ^ (1 << j);
+  k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[0]->p, sh->sendbuf.p, sh->l, lpos, 1 - bit);
+  CK(cudaGetLastError());
+  NCK(ncclGroupStart());
+  NCK(ncclSend(sh->sendbuf.p, (size_t)half * 2, ncclDouble, partner, sh->comm, ctx->stream));
+  NCK(ncclRecv(sh->recvbuf.p, (size_t)half * 2, ncclDouble, partner, sh->comm, ctx->stream));
+  NCK(ncclGroupEnd());
+  k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[0]->p, sh->recvbuf.p, sh->l, lpos, 1 - bit);
+  CK(cudaGetLastError());
+  ctx->launches += 2;
+}
+
+double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, const double* theta) {
+  ffq_ctx_t ctx = sh->ctx;
+  const CompiledPlan& cp = pl->cp;
+  if (cp.n_qubits != sh->n || h->ch.n_qubits != sh->n)
+    throw BadInput("shard: plan / Hamiltonian / shard qubit counts differ", FFQ_EINVAL);
+  const int l = sh->l, n_ops = (int)cp.op_kind.size();
+  const ShardSchedule S = schedule_shards(cp, sh->g);
+  // per-rank rotation coefficients; string ops fold the global Z sign into sin
+  std::vector<double2> cs((size_t)sh->n_local() * std::max(1, n_ops));
+  std::vector<uint64_t> pbits(cp.pair_bits.size());
+  std::vector<FusedDesc> phys(cp.fused.size());
+  std::vector<int> perm = S.init_perm;
+  std::vector<std::vector<int>> op_perm(n_ops);
+  for (const auto& st : S.steps) {
+    if (st.kind == 0) {
+      int qa = -1, qb = -1;
+      for (int q = 0; q < sh->n; ++q) {
+        if (perm[q] == st.gpos) qa = q;
+        if (perm[q] == st.lpos) qb = q;
+      }
+      std::swap(perm[qa], perm[qb]);
+    } else {
+      op_perm[st.op] = perm;
+    }
+  }
+  for (int op = 0; op < n_ops; ++op) {
+    const double phi = theta[cp.op_gen[op]] * cp.op_cfac[op];
+    for (int i = 0; i < sh->n_local(); ++i) {
+      double sg = 1.0;
+      if (cp.op_kind[op] == 1) {
+        const uint64_t zp = permute_mask(cp.str_z[cp.op_idx[op]], op_perm[op]);
+        sg = (__builtin_popcountll(((uint64_t)sh->rank_of(i) << l) & zp) & 1) ? -1.0 : 1.0;
+      }
+      cs[(size_t)i * n_ops + op] = make_double2(std::cos(phi), std::sin(phi) * cp.op_sscale[op] * sg);
+    }
+    if (cp.op_kind[op] == 0) {
+      const FusedDesc& d = cp.fused[cp.op_idx[op]];
+      phys[cp.op_idx[op]] = physical_fused(d, op_perm[op]);
+      for (int p = 0; p < d.npair; ++p)
+        pbits[d.pair_off + p] = permute_mask(cp.pair_bits[d.pair_off + p], op_perm[op]);
+    }
+  }
+  sh->cs.upload(cs, ctx->stream);
+  sh->pbits.upload(pbits, ctx->stream);
+  // |HF> on its owner rank
+  const uint64_t hf_phys = permute_mask(hf, S.init_perm);
+  for (int i = 0; i < sh->n_local(); ++i) {
+    CK(cudaMemsetAsync(sh->shards[i]->p, 0, sizeof(double2) << l, ctx->stream));
+    if ((uint64_t)sh->rank_of(i) == (hf_phys >> l)) {
+      const double2 one = make_double2(1.0, 0.0);
+      CK(cudaMemcpyAsync(sh->shards[i]->p + (hf_phys & ((1ULL << l) - 1)), &one, sizeof(one),
+                         cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  sh->last_swaps = 0;
+  for (const auto& st : S.steps) {
+    if (st.kind == 0) {
+      shard_swap(sh, st.gpos, st.lpos);
+      ++sh->last_swaps;
+      continue;
+    }
+    const int op = st.op;
+    for (int i = 0; i < sh->n_local(); ++i) {
+      const double2* csr = sh->cs.p + (size_t)i * n_ops;
+      if (cp.op_kind[op] == 0) {
+        const FusedDesc& d = phys[cp.op_idx[op]];
+        const bool vec = !(d.x & 1ULL) && (l - d.w) >= 1;
+        const int64_t work = ((int64_t)d.npair << (l - d.w)) >> (vec ? 1 : 0);
+        const uint64_t base = (uint64_t)sh->rank_of(i) << l;
+        if (vec)
+          k_fused_gen<true><<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, base);
+        else
+          k_fused_gen<false><<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, base);
+        CK(cudaGetLastError());
+        ctx->launches++;
+      } else {
+        const int si = cp.op_idx[op];
+        const uint64_t lm = (1ULL << l) - 1ULL;
+        const uint64_t xp = permute_mask(cp.str_x[si], op_perm[op]);
+        const uint64_t zp = permute_mask(cp.str_z[si], op_perm[op]) & lm;
+        launch_string(ctx, sh->shards[i]->p, l, 1, xp, zp, cp.str_ny[si], csr, n_ops, op);
+      }
+    }
+  }
+  sh->perm = S.final_perm;
+  // physical Hamiltonian for the final permutation (cached)
+  if (sh->ham_key != (const void*)h || sh->ham_perm != S.final_perm || !sh->hphys) {
+    std::vector<uint64_t> x(h->raw_x.size()), z(h->raw_z.size());
+    for (size_t t = 0; t < x.size(); ++t) {
+      x[t] = permute_mask(h->raw_x[t], S.final_perm);
+      z[t] = permute_mask(h->raw_z[t], S.final_perm);
+    }
+    auto hp = std::make_unique<ffq_ham_s>();
+    hp->ctx = ctx;
+    hp->ch = compile_ham(sh->n, (int64_t)x.size(), x.data(), z.data(), h->raw_re.data(), h->raw_im.data(), 0);
+    const auto& ch = hp->ch;
+    hp->groups.upload(ch.groups, ctx->stream);
+    hp->act_bits.upload(ch.act_bits, ctx->stream);
+    hp->cls_z.upload(ch.cls_z, ctx->stream);
+    std::vector<double2> f(ch.cls_f.size() / 2);
+    for (size_t i = 0; i < f.size(); ++i) f[i] = make_double2(ch.cls_f[2 * i], ch.cls_f[2 * i + 1]);
+    hp->cls_f.upload(f, ctx->stream);
+    // items over the local index space (the global part of X picks the partner)
+    std::vector<int32_t> ig, ip;
+    std::vector<int64_t> iu;
+    for (size_t gi = 0; gi < ch.groups.size(); ++gi) {
+      const auto& d = ch.groups[gi];
+      const int wl = __builtin_popcountll(d.x & ((1ULL << l) - 1ULL));
+      const int64_t U = 1LL << (l - wl);
+      for (int p = 0; p < d.nact; ++p)
+        for (int64_t u0 = 0; u0 < U; u0 += kItemChunk) {
+          ig.push_back((int32_t)gi);
+          ip.push_back(p);
+          iu.push_back(u0);
+        }
+    }
+    hp->ch.item_g = ig;
+    hp->ch.item_p = ip;
+    hp->ch.item_u0 = iu;
+    hp->item_g.upload(ig, ctx->stream);
+    hp->item_p.upload(ip, ctx->stream);
+    hp->item_u0.upload(iu, ctx->stream);
+    sh->hphys = std::move(hp);
+    sh->ham_key = h;
+    sh->ham_perm = S.final_perm;
+  }
+  const ffq_ham_s* hp = sh->hphys.get();
+  const int64_t items = (int64_t)hp->ch.item_g.size();
+  sh->partial.alloc((size_t)std::max<int64_t>(1, items) * sh->n_local());
+  sh->eloc.alloc(std::max<size_t>(2 * (size_t)sh->n_local(), (size_t)sh->R + 1));
+  if (items > 0) CK(cudaMemsetAsync(sh->partial.p, 0, sizeof(double2) * items * sh->n_local(), ctx->stream));
+  // buckets of items sharing hG are contiguous (groups sorted by X)
+  int64_t i0 = 0;
+  while (i0 < items) {
+    const uint32_t hG = (uint32_t)(hp->ch.groups[hp->ch.item_g[i0]].x >> l);
+    int64_t i1 = i0;
+    while (i1 < items && (uint32_t)(hp->ch.groups[hp->ch.item_g[i1]].x >> l) == hG) ++i1;
+    const double2* partner_nccl = nullptr;
+    if (!sh->group() && hG != 0) {
+      const int partner = sh->rank ^ (int)hG;
+      NCK(ncclGroupStart());
+      NCK(ncclSend(sh->shards[0]->p, (size_t)2 << l, ncclDouble, partner, sh->comm, ctx->stream));
+      NCK(ncclRecv(sh->recvbuf.p, (size_t)2 << l, ncclDouble, partner, sh->comm, ctx->stream));
+      NCK(ncclGroupEnd());
+      partner_nccl = sh->recvbuf.p;
+    }
+    for (int i = 0; i < sh->n_local(); ++i) {
+      const int r = sh->rank_of(i);
+      const double2* partner = hG == 0 ? sh->shards[i]->p
+                               : sh->group() ? sh->shards[r ^ (int)hG]->p
+                                             : partner_nccl;
+      k_expect_shard<kThreads><<<(unsigned)(i1 - i0), kThreads, 0, ctx->stream>>>(
+          sh->shards[i]->p, partner, l, (uint32_t)r, hp->dev(), i0, sh->partial.p + (size_t)i * items);
+      CK(cudaGetLastError());
+      ctx->launches++;
+    }
+    i0 = i1;
+  }
+  for (int i = 0; i < sh->n_local(); ++i) {
+    k_reduce_partials<kThreads><<<1, kThreads, 0, ctx->stream>>>(sh->partial.p + (size_t)i * std::max<int64_t>(1, items),
+                                                                 std::max<int64_t>(1, items),
+                                                                 sh->eloc.p + i, nullptr);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
+  std::vector<double> e_rank((size_t)sh->R, 0.0);
+  if (sh->group()) {
+    CK(cudaMemcpyAsync(e_rank.data(), sh->eloc.p, sizeof(double) * sh->R, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    NCK(ncclAllGather(sh->eloc.p, sh->eloc.p + 1, 1, ncclDouble, sh->comm, ctx->stream));
+    CK(cudaMemcpyAsync(e_rank.data(), sh->eloc.p + 1, sizeof(double) * sh->R, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  double e = 0.0;
+  for (double v : e_rank) e += v;  // rank order: deterministic
+  return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffq_shard_create(ffq_ctx_t ctx, int n_qubits, int n_global, ffq_shard_t* out) {
+  if (!ctx || !out || n_global < 0 || n_global > 6 || n_qubits - n_global < 2 || n_qubits > 40)
+    return fail(ctx, FFQ_EINVAL, "ffq_shard_create: need 0 <= n_global <= 6 and n_qubits - n_global >= 2");
+  *out = nullptr;
+  return guarded_shard(ctx, [&] {
+    auto sh = std::make_unique<ffq_shard_s>();
+    sh->ctx = ctx;
+    sh->n = n_qubits;
+    sh->g = n_global;
+    sh->l = n_qubits - n_global;
+    sh->R = 1 << n_global;
+    shard_alloc(sh.get());
+    *out = sh.release();
+    return FFQ_OK;
+  });
+}
+
+int ffq_nccl_unique_id(void* id128) {
+  if (!id128) return fail(nullptr, FFQ_EINVAL, "null argument");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, FFQ_ENCCL, ncclGetErrorString(r));
+  std::memcpy(id128, &id, sizeof(id));
+  return FFQ_OK;
+}
+
+int ffq_shard_create_nccl(ffq_ctx_t ctx, int n_qubits, int n_global, int rank, const void* id128,
+                          ffq_shard_t* out) {
+  if (!ctx || !out || !id128 || n_global < 0 || n_global > 6 || n_qubits - n_global < 2 || rank < 0 ||
+      rank >= (1 << n_global))
+    return fail(ctx, FFQ_EINVAL, "ffq_shard_create_nccl: invalid argument");
+  *out = nullptr;
+  return guarded_shard(ctx, [&] {
+    auto sh = std::make_unique<ffq_shard_s>();
+    sh->ctx = ctx;
+    sh->n = n_qubits;
+    sh->g = n_global;
+    sh->l = n_qubits - n_global;
+    sh->R = 1 << n_global;
+    sh->rank = rank;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    NCK(ncclCommInitRank(&sh->comm, sh->R, id, rank));
+    shard_alloc(sh.get());
+    *out = sh.release();
+    return FFQ_OK;
+  });
+}
+
+int ffq_shard_destroy(ffq_shard_t sh) {
+  if (sh) {
+    cudaSetDevice(sh->ctx->device);
+    cudaStreamSynchronize(sh->ctx->stream);
+    delete sh;
+  }
+  return FFQ_OK;
+}
+
+int ffq_shard_energy(ffq_shard_t sh, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, const double* theta,
+                     double* e_out) {
+  if (!sh || !plan || !ham || !e_out || (!theta && plan->cp.n_gen > 0))
+    return fail(sh ? sh->ctx : nullptr, FFQ_EINVAL, "ffq_shard_energy: null argument");
+  return guarded_shard(sh->ctx, [&] {
+    *e_out = shard_energy(sh, plan, ham, hf_bits, theta);
+    return FFQ_OK;
+  });
+}
+
+int ffq_shard_download(ffq_shard_t sh, double* psi) {
+  if (!sh || !psi) return fail(sh ? sh->ctx : nullptr, FFQ_EINVAL, "null argument");
+  if (!sh->group()) return fail(sh->ctx, FFQ_EINVAL, "ffq_shard_download: group mode only");
+  return guarded_shard(sh->ctx, [&] {
+    const size_t dim = size_t(1) << sh->l;
+    std::vector<double2> host(dim);
+    std::vector<int> inv(sh->n);
+    const std::vector<int>& perm = sh->perm.empty() ? std::vector<int>() : sh->perm;
+    for (int q = 0; q < sh->n; ++q) inv[perm.empty() ? q : perm[q]] = q;
+    for (int r = 0; r < sh->R; ++r) {
+      CK(cudaMemcpyAsync(host.data(), sh->shards[r]->p, sizeof(double2) * dim, cudaMemcpyDeviceToHost,
+                         sh->ctx->stream));
+      CK(cudaStreamSynchronize(sh->ctx->stream));
+      for (size_t k = 0; k < dim; ++k) {
+        const uint64_t phys = ((uint64_t)r << sh->l) | k;
+        uint64_t logical = 0;
+        for (int pq = 0; pq < sh->n; ++pq)
+          if ((phys >> pq) & 1ULL) logical |= 1ULL << inv[pq];
+        psi[2 * logical] = host[k].x;
+        psi[2 * logical + 1] = host[k].y;
+      }
+    }
+    return FFQ_OK;
+  });
+}
+
+int ffq_shard_info(ffq_shard_t sh, int* last_swaps, int* perm_out) {
+  if (!sh) return fail(nullptr, FFQ_EINVAL, "null shard");
+  if (last_swaps) *last_swaps = sh->last_swaps;
+  if (perm_out)
+    for (int q = 0; q < sh->n; ++q) perm_out[q] = sh->perm.empty() ? q : sh->perm[q];
+  return FFQ_OK;
+}
+
+int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* term_off, const uint64_t* x,
+                       const uint64_t* z, const double* c_re, const double* c_im, int* init_perm,
+                       int* final_perm, int* n_swaps, int* n_steps) {
+  return guarded(nullptr, [&] {
+    const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, x, z, c_re, c_im);
+    const ShardSchedule S = schedule_shards(P, n_global);
+    for (int q = 0; q < n_qubits; ++q) {
+      if (init_perm) init_perm[q] = S.init_perm[q];
+      if (final_perm) final_perm[q] = S.final_perm[q];
+    }
+    if (n_swaps) *n_swaps = S.n_swaps();
+    if (n_steps) *n_steps = (int)S.steps.size();
+    return FFQ_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+"""Sharded state (a15): 2^g ranks emulated on one device through the same
+pack/unpack exchange kernels the NCCL transport uses; energies and amplitudes
+must match the unsharded path. The NCCL transport itself runs with world = 1
+here (one GPU per gpurun call)."""
+import numpy as np
+import pytest
+
+from paper_2402_17993_b200 import capi, problems
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return capi.Context(0)
+
+
+@pytest.mark.parametrize("config,g", [(2, 1), (2, 2), (2, 3), (3, 2)])
+def test_sharded_energy_and_state_match_unsharded(ctx, config, g):
+    P = problems.config_problem(config)
+    plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
+    th = P.plan_thetas()[0]
+    sh = capi.ShardedState(ctx, P.n_qubits, g)
+    e = sh.energy(plan, ham, P.hf, th)
+    e_ref = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0]
+    assert abs(e - e_ref) <= 1e-12
+    st = capi.State(ctx, P.n_qubits, 1)
+    st.set_basis(P.hf)
+    st.apply_plan(plan, P.plan_thetas())
+    assert np.abs(sh.download() - st.download()[0]).max() <= 1e-12
+    swaps, perm = sh.info()
+    assert sorted(perm.tolist()) == list(range(P.n_qubits))
+    assert (swaps > 0) == (g > 0)
+
+
+def test_sharded_random_pauli_hamiltonian(ctx, oracle):
+    # config-5-style H (random {I,X,Y,Z} strings: generic x-groups) at 14 qubits
+    import paper_2402_17993_b200 as ff
+
+    P = problems.make_problem(7, 6, problems.ham_seed(5), name="c5small")
+    H = ff.random_pauli_hamiltonian(14, 300, problems.ham_seed(5) + 7)
+    x, z, c = H.arrays()
+    plan = capi.Plan(ctx, 14, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, 14, x, z, c)
+    th = P.plan_thetas()[0]
+    e1 = capi.ShardedState(ctx, 14, 0).energy(plan, ham, P.hf, th)
+    e3 = capi.ShardedState(ctx, 14, 3).energy(plan, ham, P.hf, th)
+    kind, idx = oracle.build_generators(14, 6)
+    ref = oracle.energy_trotter(14, 6, kind, idx, np.array(P.plan.order, np.int32), P.thetas[0],
+                                oracle.PauliSum.from_terms(14, x, z, c))[0]
+    assert abs(e1 - ref) <= 1e-10 and abs(e3 - ref) <= 1e-10
+
+
+def test_nccl_transport_world_one(ctx):
+    P = problems.config_problem(2)
+    plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
+    sh = capi.ShardedState(ctx, P.n_qubits, 0, rank=0, nccl_id=capi.nccl_unique_id())
+    e = sh.energy(plan, ham, P.hf, P.plan_thetas()[0])
+    assert abs(e - capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0]) <= 1e-12

@@ -166,3 +166,20 @@ def test_fmo_assembly_matches_reference_golden():
     bad.pop("21")
     with pytest.raises(ff.ContractViolation):
         ff.assemble_two_body(3, mono, bad)
+
+
+@pytest.mark.parametrize("g", [0, 1, 2, 3])
+def test_shard_schedule_is_a_valid_swap_sequence(g):
+    P = problems.config_problem(3)
+    ip, fp, ns, st = capi.shard_schedule(18, g, *P.plan_arrays())
+    assert sorted(ip.tolist()) == list(range(18)) and sorted(fp.tolist()) == list(range(18))
+    assert st == P.n_gen + ns  # every generator applied once, preceded by its swaps
+    # the initial global qubits are the least-flipped logical qubits
+    uses = np.zeros(18, int)
+    for gen in P.gens:
+        x = int(gen.image.arrays()[0][0])
+        uses += [(x >> q) & 1 for q in range(18)]
+    glob = [q for q in range(18) if ip[q] >= 18 - g]
+    assert all(uses[q] <= min(uses[[r for r in range(18) if r not in glob]]) for q in glob)
+    if g == 0:
+        assert ns == 0 and ip.tolist() == list(range(18))
