@@ -345,11 +345,14 @@ __global__ void __launch_bounds__(NT) k_expect_shard(const double2* __restrict__
   const GroupDesc d = h.groups[g];
   const uint64_t lmask = (1ULL << l) - 1ULL;
   const uint64_t XL = d.x & lmask;
-  const uint32_t hG = (uint32_t)(d.x >> l);
+  // inserted (pattern-fixed) positions: all of X in table mode, X's lowest bit in generic mode
+  uint64_t Q = 0;
+  for (int i = 0; i < d.w; ++i) Q |= 1ULL << ((d.qpack >> (6 * i)) & 63u);
+  const uint32_t QG = (uint32_t)(Q >> l);
   const uint64_t pb = h.act_bits[d.act_off + p];
   double acc = 0.0;
-  if ((rank & hG) == (uint32_t)(pb >> l)) {
-    const int wl = __popcll(XL);
+  if ((rank & QG) == ((uint32_t)(pb >> l) & QG)) {
+    const int wl = __popcll(Q & lmask);
     const int64_t U = 1LL << (l - wl);
     const int64_t u1 = min(U, u0 + h.item_chunk);
     const uint64_t base = (uint64_t)rank << l;

@@ -222,7 +222,9 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     std::vector<int64_t> iu;
     for (size_t gi = 0; gi < ch.groups.size(); ++gi) {
       const auto& d = ch.groups[gi];
-      const int wl = __builtin_popcountll(d.x & ((1ULL << l) - 1ULL));
+      uint64_t Q = 0;  // inserted positions (see k_expect_shard)
+      for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
+      const int wl = __builtin_popcountll(Q & ((1ULL << l) - 1ULL));
       const int64_t U = 1LL << (l - wl);
       for (int p = 0; p < d.nact; ++p)
         for (int64_t u0 = 0; u0 < U; u0 += kItemChunk) {
