@@ -127,8 +127,11 @@ class Context:
         self.h = h
 
     def close(self):
-        if self.h:
-            lib().ffq_ctx_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.ffq_ctx_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
     __del__ = close
@@ -159,8 +162,11 @@ class Hamiltonian:
         return g.value, t.value, cl.value
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ffq_ham_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.ffq_ham_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
 
@@ -180,8 +186,11 @@ class Plan:
         return f.value, s.value
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ffq_plan_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.ffq_plan_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
 
@@ -207,8 +216,11 @@ class State:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ffq_state_free(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.ffq_state_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
     def set_basis(self, bits):
@@ -274,8 +286,11 @@ class ShardedState:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ffq_shard_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.ffq_shard_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
     def energy(self, plan: Plan, ham: Hamiltonian, hf_bits, theta):

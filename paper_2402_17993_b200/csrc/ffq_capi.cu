@@ -161,6 +161,7 @@ struct ffq_ham_s {
     d.n_items = (int64_t)ch.item_g.size();
     d.item_g = item_g.p; d.item_p = item_p.p; d.item_u0 = item_u0.p;
     d.item_chunk = ch.item_chunk;
+    d.sitem_words = ch.sitem_words;
     d.tile_bits = ch.tile_bits;
     d.bucket_h = bucket_h.p; d.bucket_goff = bucket_goff.p; d.bucket_groups = bucket_groups.p;
     d.titem_bucket = titem_bucket.p; d.titem_u = titem_u.p;

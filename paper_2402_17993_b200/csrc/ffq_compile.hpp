@@ -246,6 +246,7 @@ struct CompiledHam {
   // bucketed by their out-of-tile flip pattern h = X >> tile_bits and every
   // (bucket, tile pair {u, u^h}) is one work item (0 = tiling disabled)
   int tile_bits = 0;
+  bool has_generic = false;  // some group has |X| > kMaxTableBits (random Pauli strings)
   std::vector<uint32_t> bucket_h;
   std::vector<int32_t> bucket_goff;  // [n_buckets + 1] into bucket_groups
   std::vector<int32_t> bucket_groups;
@@ -255,6 +256,7 @@ struct CompiledHam {
   // support-tracked path: items (group, pattern, first support word)
   std::vector<int32_t> sitem_g, sitem_p;
   std::vector<int64_t> sitem_w0;
+  int64_t sitem_words = 0;
   int64_t n_classes() const { return (int64_t)cls_z.size(); }
 };
 
@@ -355,6 +357,7 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
         ++ci2;
       }
     } else {
+      H.has_generic = true;
       d.w = 1;
       d.q[0] = __builtin_ctzll(X);
       d.qpack = pack_q(d.q, 1);
@@ -374,25 +377,28 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
     hi_positions(d.w == popc64(X) ? X : (X & (1ULL << d.q[0])), d.whi, d.qpack_hi);
     H.groups.push_back(d);
   }
-  // fixed work decomposition for the global (large-state) path
-  H.item_chunk = kItemChunk;
+  // fixed work decomposition for the global (large-state) path: chunks of
+  // 4096 pairs, at most 256 chunks per (group, pattern) for very large n
+  H.item_chunk = std::max<int64_t>(kItemChunk, (1LL << (n - 1)) / 256);
   for (size_t g = 0; g < H.groups.size(); ++g) {
     const auto& d = H.groups[g];
     const int64_t U = 1LL << (n - d.w);
     for (int p = 0; p < d.nact; ++p)
-      for (int64_t u0 = 0; u0 < U; u0 += kItemChunk) {
+      for (int64_t u0 = 0; u0 < U; u0 += H.item_chunk) {
         H.item_g.push_back((int32_t)g);
         H.item_p.push_back(p);
         H.item_u0.push_back(u0);
       }
   }
-  // support-tracked decomposition: fixed word ranges per (group, pattern)
+  // support-tracked decomposition: fixed word ranges per (group, pattern),
+  // 2048 words per item, at most 256 items per (group, pattern) for large n
   if (n >= 6) {
+    H.sitem_words = std::max<int64_t>(kSupportWordsPerItem, (1LL << (n - 5)) / 256);
     for (size_t g = 0; g < H.groups.size(); ++g) {
       const auto& d = H.groups[g];
       const int64_t W = 1LL << (n - 5 - d.whi);
       for (int p = 0; p < d.nact; ++p)
-        for (int64_t w0 = 0; w0 < W; w0 += kSupportWordsPerItem) {
+        for (int64_t w0 = 0; w0 < W; w0 += H.sitem_words) {
           H.sitem_g.push_back((int32_t)g);
           H.sitem_p.push_back(p);
           H.sitem_w0.push_back(w0);

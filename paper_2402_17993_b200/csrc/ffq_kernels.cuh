@@ -50,6 +50,7 @@ struct HamDev {
   const int32_t* item_p;
   const int64_t* item_u0;
   int64_t item_chunk;
+  int64_t sitem_words;  // support words per support-path item
   // tiled path
   int tile_bits;
   const uint32_t* bucket_h;
@@ -291,7 +292,9 @@ __global__ void __launch_bounds__(NT) k_expect_items(const double2* __restrict__
   double2 acc = make_double2(0, 0);
   for (int64_t u = u0 + threadIdx.x; u < u1; u += NT) {
     const uint64_t m = insert_bits<uint64_t>((uint64_t)u, d.qpack, d.w) | pb;
-    const double2 a = s[m], bb = s[m ^ d.x];
+    const double2 a = s[m];
+    if (a.x == 0.0 && a.y == 0.0) continue;  // zero product: skip partner load and classes
+    const double2 bb = s[m ^ d.x];
     double2 f = make_double2(0, 0);
     for (int o = 0; o < d.ncls; ++o) {
       const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);

@@ -210,6 +210,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     auto hp = std::make_unique<ffq_ham_s>();
     hp->ctx = ctx;
     hp->ch = compile_ham(sh->n, (int64_t)x.size(), x.data(), z.data(), h->raw_re.data(), h->raw_im.data(), 0);
+    hp->ch.item_chunk = std::max<int64_t>(kItemChunk, (1LL << (l - 1)) / 256);
     const auto& ch = hp->ch;
     hp->groups.upload(ch.groups, ctx->stream);
     hp->act_bits.upload(ch.act_bits, ctx->stream);
@@ -227,7 +228,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
       const int wl = __builtin_popcountll(Q & ((1ULL << l) - 1ULL));
       const int64_t U = 1LL << (l - wl);
       for (int p = 0; p < d.nact; ++p)
-        for (int64_t u0 = 0; u0 < U; u0 += kItemChunk) {
+        for (int64_t u0 = 0; u0 < U; u0 += hp->ch.item_chunk) {
           ig.push_back((int32_t)gi);
           ip.push_back(p);
           iu.push_back(u0);

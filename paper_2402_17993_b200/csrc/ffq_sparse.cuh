@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(NT) k_expect_support(const double2* __restrict
   const uint64_t pb = h.act_bits[d.act_off + p];
   const uint32_t lm = act_low[d.act_off + p];
   const int64_t W = 1LL << (n - 5 - d.whi);
-  const int64_t w0 = it_w0[item], w1 = min(W, w0 + (int64_t)kSupportWordsPerItem);
+  const int64_t w0 = it_w0[item], w1 = min(W, w0 + h.sitem_words);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* wq = q_m + warp * 32;
   double acc = 0.0;

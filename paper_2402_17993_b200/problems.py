@@ -101,3 +101,21 @@ def fmo_fragment_problems():
     for label, P in fmo_fragments().items():
         out.append(FragmentProblem(label, P.H, P.plan, P.hf, list(P.thetas[0])))
     return out
+
+
+def config5_problem(n_doubles: int = 2000, n_terms: int = 5000, n_qubits: int = 32, n_elec: int = 16):
+    """BASELINE.json config 5: all singles + the first `n_doubles` doubles in
+    canonical generator order (pinned reading of "first 2000 seeded doubles"),
+    theta ~ U(-0.05, 0.05), H = `n_terms` seeded random {I,X,Y,Z}^n strings with
+    real c ~ N(0, 0.1)."""
+    from . import random_pauli_hamiltonian
+
+    seed = ham_seed(5)
+    gens_all = build_generators(n_qubits, n_elec)
+    singles = [g for g in gens_all if g.exc.kind == 1]
+    doubles = [g for g in gens_all if g.exc.kind == 2][:n_doubles]
+    gens = singles + doubles
+    th = np.array(uniform_vector(seed + 1, len(gens), -0.05, 0.05)).reshape(1, len(gens))
+    plan = magnitude_order(gens, list(th[0]), n_qubits)
+    H = random_pauli_hamiltonian(n_qubits, n_terms, seed + 2, 0.1)
+    return Problem(f"config5_{n_qubits}q", n_qubits // 2, n_elec, None, None, H, gens, plan, th, seed)

@@ -59,3 +59,21 @@ def test_nccl_transport_world_one(ctx):
     sh = capi.ShardedState(ctx, P.n_qubits, 0, rank=0, nccl_id=capi.nccl_unique_id())
     e = sh.energy(plan, ham, P.hf, P.plan_thetas()[0])
     assert abs(e - capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0]) <= 1e-12
+
+
+def test_config5_structure_small_vs_oracle(ctx, oracle):
+    # config 5 recipe (singles + first doubles, random Pauli H) at 16 qubits,
+    # through both the support-tracked graph path and the sharded path
+    P = problems.config5_problem(n_doubles=150, n_terms=400, n_qubits=16, n_elec=8)
+    x, z, c = P.ham_arrays()
+    plan = capi.Plan(ctx, 16, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, 16, x, z, c)
+    e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0]
+    e_sh = capi.ShardedState(ctx, 16, 2).energy(plan, ham, P.hf, P.plan_thetas()[0])
+    psi = oracle.hf_state(16, P.hf)
+    for gid in P.plan.order:
+        gx, gz, gc = P.gens[gid].image.arrays()
+        for xx, zz, cc in zip(gx, gz, gc):
+            psi = oracle.apply_pauli_rotation(16, psi, int(xx), int(zz), P.thetas[0][gid] * cc.imag)
+    ref = oracle.expectation(16, psi, oracle.PauliSum.from_terms(16, x, z, c)).real
+    assert abs(e - ref) <= 1e-10 and abs(e_sh - ref) <= 1e-10
