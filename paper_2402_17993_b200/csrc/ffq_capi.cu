@@ -87,6 +87,7 @@ struct ffq_ctx_s {
   int tile_bits = kDefaultTileBits;              // env FFQ_TILE_BITS (0 disables tiling)
   int64_t slab_bytes = 256LL << 20;              // env FFQ_SLAB_MB: batch chunk of the graph path
   int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
+  int64_t row_pad = 0;                           // env FFQ_ROW_PAD: slab row stride = 2^n + pad (support path)
   int persist = 0;                               // env FFQ_PERSIST=1: k_eval_persistent instead of the graph path
   int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
   int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
@@ -96,6 +97,7 @@ struct ffq_ctx_s {
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
   DevBuf<uint32_t> slab_sup;
+  bool slab_clean = false;      // support path: slab all-zero between graph replays
   DevBuf<double2> pslab;        // persistent-path slab, all-zero between evaluations
   bool pslab_clean = false;
   double* pinned = nullptr;
@@ -241,12 +243,12 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
 }
 
 void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* sup, int n, int batch,
-                  const FusedDesc& d, const double2* cs, int cs_stride, int op) {
+                  const FusedDesc& d, const double2* cs, int cs_stride, int op, int64_t rstride) {
   if (sup) {
     const int64_t work = (int64_t)d.npair << (n - 5 - d.whi);
     dim3 grid(grid_for(work, ctx->n_sm), batch);
     k_fused_gen_support<<<grid, kThreads, 0, ctx->stream>>>(psi, sup, n, d, pl->pair_bits.p, pl->pair_low.p,
-                                                            pl->pair_f.p, cs, cs_stride, op);
+                                                            pl->pair_f.p, cs, cs_stride, op, rstride);
     CK(cudaGetLastError());
     ctx->launches++;
     return;
@@ -268,7 +270,7 @@ void launch_fused(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
 // sup != nullptr: support-tracked fused passes; string ops are dense and are
 // followed by an exact support rebuild before the next support-tracked op
 void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* sup, int batch,
-                  const double2* cs) {
+                  const double2* cs, int64_t rstride = 0) {
   const CompiledPlan& cp = pl->cp;
   const int n = cp.n_qubits;
   const int n_ops = (int)cp.op_kind.size();
@@ -279,7 +281,8 @@ void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
         launch_support_from_state(ctx, psi, sup, n, batch);
         stale = false;
       }
-      launch_fused(ctx, pl, psi, sup, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op);
+      launch_fused(ctx, pl, psi, sup, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op,
+                   rstride ? rstride : (1LL << n));
     } else {
       const int si = cp.op_idx[op];
       launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
@@ -300,7 +303,7 @@ void launch_cs(ffq_ctx_t ctx, const ffq_plan_s* pl, const double* theta, int bat
 }
 
 void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, const uint32_t* sup, int n,
-                   int batch, double2* partial, double* e, double* im) {
+                   int batch, double2* partial, double* e, double* im, int64_t rstride = 0) {
   const int64_t items = h->n_partials(sup != nullptr);
   if (items == 0) {
     CK(cudaMemsetAsync(e, 0, sizeof(double) * batch, ctx->stream));
@@ -309,7 +312,8 @@ void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, const 
   }
   if (sup) {
     k_expect_support<kThreads><<<dim3((unsigned)items, batch), kThreads, 0, ctx->stream>>>(
-        psi, sup, n, h->dev(), h->sitem_g.p, h->sitem_p.p, h->sitem_w0.p, h->act_low.p, partial);
+        psi, sup, n, h->dev(), h->sitem_g.p, h->sitem_p.p, h->sitem_w0.p, h->act_low.p, partial,
+        rstride ? rstride : (1LL << n));
     CK(cudaGetLastError());
     ctx->launches++;
   } else if (h->ch.tile_bits) {
@@ -433,8 +437,14 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   const int n_ops = (int)pl->cp.op_kind.size();
   const bool sp = use_support(ctx, n);
   const int64_t items = h->n_partials(sp);
-  ctx->slab.alloc((size_t)chunk * dim);
+  const int64_t rstride = (sp && pl->cp.n_string_ops() == 0) ? dim + ctx->row_pad : dim;
+  if (ctx->slab.n < (size_t)chunk * rstride) ctx->slab_clean = false;
+  ctx->slab.alloc((size_t)chunk * rstride);
   if (sp) ctx->slab_sup.alloc((size_t)chunk * (dim >> 5));
+  if (sp && !ctx->slab_clean) {
+    CK(cudaMemsetAsync(ctx->slab.p, 0, sizeof(double2) * ctx->slab.n, ctx->stream));
+    ctx->slab_clean = true;
+  }
   uint32_t* sup = sp ? ctx->slab_sup.p : nullptr;
   ctx->cs.alloc((size_t)chunk * std::max(1, n_ops));
   ctx->partial.alloc((size_t)chunk * std::max<int64_t>(1, items));
@@ -450,17 +460,26 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
     const int64_t before = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      k_set_basis<<<grid_for(dim * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(ctx->slab.p, dim,
-                                                                                 chunk, hf);
-      ctx->launches++;
       if (sup) {
+        // clean slab: only the HF amplitudes are written; the support is zeroed at the end
+        k_set_basis_sparse<<<grid_for(chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(ctx->slab.p, n, chunk, hf,
+                                                                                      rstride);
         k_support_basis<<<grid_for((dim >> 5) * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(
             sup, dim >> 5, chunk, hf);
+        ctx->launches += 2;
+      } else {
+        k_set_basis<<<grid_for(dim * chunk, ctx->n_sm), kThreads, 0, ctx->stream>>>(ctx->slab.p, dim,
+                                                                                   chunk, hf);
         ctx->launches++;
       }
       launch_cs(ctx, pl, ctx->theta.p, chunk, ctx->cs.p);
-      run_plan_ops(ctx, pl, ctx->slab.p, sup, chunk, ctx->cs.p);
-      launch_expect(ctx, h, ctx->slab.p, sup, n, chunk, ctx->partial.p, ctx->eout.p, ctx->eim.p);
+      run_plan_ops(ctx, pl, ctx->slab.p, sup, chunk, ctx->cs.p, rstride);
+      launch_expect(ctx, h, ctx->slab.p, sup, n, chunk, ctx->partial.p, ctx->eout.p, ctx->eim.p, rstride);
+      if (sup) {
+        k_support_zero<<<grid_for(((dim >> 5) * chunk) * 32, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+            ctx->slab.p, sup, n, chunk, rstride);
+        ctx->launches++;
+      }
     } catch (...) {
       cudaStreamEndCapture(ctx->stream, &graph);
       throw;
@@ -480,7 +499,10 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
                        sizeof(double) * (size_t)nb * pl->cp.n_gen, cudaMemcpyDeviceToDevice,
                        ctx->stream));
     // rows past nb in the last chunk recompute stale theta; their outputs are dropped
-    CK(cudaGraphLaunch(it->second, ctx->stream));
+    if (cudaGraphLaunch(it->second, ctx->stream) != cudaSuccess) {
+      ctx->slab_clean = false;
+      throw CudaError("cudaGraphLaunch failed");
+    }
     ctx->launches += nodes;
     CK(cudaMemcpyAsync(e_dev + b0, ctx->eout.p, sizeof(double) * nb, cudaMemcpyDeviceToDevice,
                        ctx->stream));
@@ -539,6 +561,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_ROW_PAD")) c->row_pad = std::atoll(e);
     if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
