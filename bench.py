@@ -267,6 +267,25 @@ def main():
     rot_avg = statistics.mean(rot_ms[2:])
     achieved = rot_bytes / (rot_avg / 1e3) / 1e9
 
+    # secondary: BASELINE.json config 2 -- 64 theta vectors x (1 + 2*117) shifts
+    # = 15040 evaluations at 12 qubits in one batched call (smem-resident path)
+    from paper_2402_17993_b200 import parameter_shift_set, problems as _pb
+
+    P2 = _pb.config_problem(2, batch=64)
+    rows2 = np.concatenate([np.array(parameter_shift_set(list(t))).reshape(-1, P2.n_gen) for t in P2.thetas])
+    plan2 = capi.Plan(ctx, P2.n_qubits, *P2.plan_arrays())
+    ham2 = capi.Hamiltonian(ctx, P2.n_qubits, *P2.ham_arrays())
+    th2 = torch.from_numpy(P2.plan_thetas(rows2)).to(f"cuda:{local}")
+    e2 = torch.zeros(rows2.shape[0], dtype=torch.float64, device=f"cuda:{local}")
+    f2 = lambda: capi.energy_batch_device(ctx, plan2, ham2, P2.hf, rows2.shape[0], th2.data_ptr(),  # noqa: E731
+                                         e2.data_ptr())
+    for _ in range(2):
+        f2()
+    ms2 = timed(f2, 3)
+    config2 = {"evals": int(rows2.shape[0]), "ms_per_call": statistics.mean(ms2),
+               "evals_per_s": rows2.shape[0] / (statistics.mean(ms2) / 1e3),
+               "path": "k_smem_eval (one CTA per evaluation, state in shared memory)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = 2
@@ -297,6 +316,7 @@ def main():
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
             "gpu_launches": int(launches),
+            "secondary": {"config2_12q": config2},
             "clocks": clk.summary(),
         }
         if cpu:

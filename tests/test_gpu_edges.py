@@ -1,0 +1,130 @@
+"""Edge cases of the C-ABI on the GPU, each checked against the CPU oracle:
+empty batches and Hamiltonians, plans without generators, identity-only H,
+non-UCCSD generators (string fallback) through every execution path, and the
+2-pi periodicity of exp(theta A)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2402_17993_b200 import capi, problems
+
+pytestmark = pytest.mark.gpu
+
+PATHS = {
+    "smem": {},
+    "graph-dense": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SUPPORT": "0"},
+    "graph-support": {"FFQ_SMEM_MAX_QUBITS": "0"},
+    "persistent": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_PERSIST": "1"},
+}
+
+
+def _ctx(monkeypatch, env):
+    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    return capi.Context(0)
+
+
+def _oracle_state(oracle, n, hf, gens, theta):
+    """gens: list of (x[], z[], c[]) per generator in execution order."""
+    psi = oracle.hf_state(n, hf)
+    for (x, z, c), t in zip(gens, theta):
+        order = np.lexsort((z, x))  # canonical (x, z) order
+        for i in order:
+            psi = oracle.apply_pauli_rotation(n, psi, int(x[i]), int(z[i]), t * c[i].imag)
+    return psi
+
+
+def _plan_arrays(gens):
+    off = [0]
+    for g in gens:
+        off.append(off[-1] + len(g[0]))
+    x = np.concatenate([g[0] for g in gens]).astype(np.uint64)
+    z = np.concatenate([g[1] for g in gens]).astype(np.uint64)
+    c = np.concatenate([g[2] for g in gens])
+    return np.array(off, np.int64), x, z, c
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_non_uccsd_generators_all_paths(monkeypatch, oracle, path):
+    # generators that do not fuse: several flip masks, non-commuting strings
+    n = 10
+    rng = np.random.default_rng(7)
+    gens = [
+        (np.array([0b11, 0b1100]), np.array([0b10, 0b100]), np.array([0.3j, -0.2j])),  # two flip masks
+        (np.array([1, 1]), np.array([0, 1]), np.array([0.25j, 0.4j])),  # X0 and Y0: anticommute
+        (np.array([0b101 << 5]), np.array([0b111]), np.array([0.5j])),  # single string
+    ]
+    P = problems.config_problem(1)
+    hx = rng.integers(0, 1 << n, 40).astype(np.uint64)
+    hz = rng.integers(0, 1 << n, 40).astype(np.uint64)
+    hc = rng.normal(size=40)
+    theta = np.array([0.7, -1.1, 0.35])
+    hf = 0b0000001111
+    c = _ctx(monkeypatch, PATHS[path])
+    plan = capi.Plan(c, n, *_plan_arrays(gens))
+    assert plan.info() == (1, 4)  # the single-string generator fuses; the other two run string by string
+    ham = capi.Hamiltonian(c, n, hx, hz, hc)
+    e = capi.energy_batch(c, plan, ham, hf, theta[None, :])[0]
+    psi = _oracle_state(oracle, n, hf, gens, theta)
+    ref = oracle.expectation(n, psi, oracle.PauliSum.from_terms(n, hx, hz, hc)).real
+    assert abs(e - ref) <= 1e-10
+    st = capi.State(c, n, 1)
+    st.set_basis(hf)
+    st.apply_plan(plan, theta[None, :])
+    assert np.abs(st.download()[0] - psi).max() <= 1e-12
+    del P
+
+
+def test_empty_batch_empty_hamiltonian_and_no_generators(ctx_default, oracle):
+    c = ctx_default
+    P = problems.config_problem(2)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    assert capi.energy_batch(c, plan, ham, P.hf, np.zeros((0, P.n_gen))).shape == (0,)
+    empty = capi.Hamiltonian(c, P.n_qubits, np.zeros(0, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    assert capi.energy_batch(c, plan, empty, P.hf, P.plan_thetas())[0] == 0.0
+    noplan = capi.Plan(c, P.n_qubits, np.zeros(1, np.int64), np.zeros(0, np.uint64), np.zeros(0, np.uint64),
+                       np.zeros(0))
+    e_hf = capi.energy_batch(c, noplan, ham, P.hf, np.zeros((1, 0)))[0]
+    x, z, co = P.ham_arrays()
+    ref = oracle.expectation(P.n_qubits, oracle.hf_state(P.n_qubits, P.hf),
+                             oracle.PauliSum.from_terms(P.n_qubits, x, z, co)).real
+    assert abs(e_hf - ref) <= 1e-12
+    ident = capi.Hamiltonian(c, P.n_qubits, [0], [0], [2.5])
+    assert abs(capi.energy_batch(c, plan, ident, P.hf, P.plan_thetas())[0] - 2.5) <= 1e-12  # norm 1
+
+
+@pytest.fixture(scope="module")
+def ctx_default():
+    return capi.Context(0)
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_theta_periodicity_and_zero(ctx_default, config):
+    c = ctx_default
+    P = problems.config_problem(config)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    th = P.plan_thetas()
+    rows = np.vstack([th, th + 2 * np.pi, np.zeros_like(th)])
+    e = capi.energy_batch(c, plan, ham, P.hf, rows)
+    assert abs(e[0] - e[1]) <= 1e-10
+    st = capi.State(c, P.n_qubits, 1)
+    st.set_basis(P.hf)
+    assert abs(e[2] - st.expectation(ham)[0].real) <= 1e-12
+
+
+def test_batch_not_multiple_of_chunk(monkeypatch):
+    # the graph path's last chunk recomputes stale rows; their outputs must not leak
+    c = _ctx(monkeypatch, {"FFQ_SMEM_MAX_QUBITS": "0"})
+    monkeypatch.setenv("FFQ_SLAB_MB", "1")  # 1 MiB slab: 16 rows of 12 qubits per chunk
+    c = capi.Context(0)
+    P = problems.config_problem(2, batch=37)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    full = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    one = np.array([capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas()[i:i + 1])[0] for i in range(37)])
+    assert np.array_equal(full, one)
