@@ -24,6 +24,7 @@
 #include "ffq_compile.hpp"
 #include "ffq_kernels.cuh"
 #include "ffq_sparse.cuh"
+#include "ffq_sector.cuh"
 
 using namespace ffq;
 
@@ -89,6 +90,7 @@ struct ffq_ctx_s {
   int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
   int64_t row_pad = 0;                           // env FFQ_ROW_PAD: slab row stride = 2^n + pad (support path)
   int persist = 0;                               // env FFQ_PERSIST=1: k_eval_persistent instead of the graph path
+  int sector = 1;                                // env FFQ_SECTOR=0: no support-closure cluster evaluator
   int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
   int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
   std::string err = "no error";
@@ -125,6 +127,14 @@ struct ffq_plan_s {
   DevBuf<double2> pair_f;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int64_t> graph_nodes;
+  struct SectorDevBufs {
+    SectorProgram prog;
+    DevBuf<int64_t> gen_off;
+    DevBuf<uint32_t> gen_pairs, exp_pairs;
+    DevBuf<uint8_t> gen_flags;
+    DevBuf<double> exp_fre, exp_fim;
+  };
+  std::map<std::pair<const void*, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;
   PlanDev dev() const {
     PlanDev d;
     d.n_ops = (int)cp.op_kind.size();
@@ -365,6 +375,71 @@ bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
   return true;
 }
 
+constexpr int kSectorThreads = 1024;
+constexpr uint32_t kSectorMaxSize = 32768;  // 2 CTAs x 16384 amplitudes (256 KiB) in DSMEM
+
+// compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
+// nullptr when the closure does not fit a 2-CTA cluster (then other paths run)
+const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
+  auto key = std::make_pair((const void*)h, hf);
+  auto it = pl->sectors.find(key);
+  if (it == pl->sectors.end()) {
+    auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize);
+    if (b->prog.ok) {
+      const size_t half = (b->prog.size + 1) / 2;
+      if ((half + pl->cp.op_kind.size()) * sizeof(double2) > ctx->smem_optin) b->prog.ok = false;
+    }
+    if (b->prog.ok) {
+      b->gen_off.upload(b->prog.gen_off, ctx->stream);
+      b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
+      b->gen_flags.upload(b->prog.gen_flags, ctx->stream);
+      b->exp_pairs.upload(b->prog.exp_pairs, ctx->stream);
+      b->exp_fre.upload(b->prog.exp_fre, ctx->stream);
+      if (!b->prog.f_real) b->exp_fim.upload(b->prog.exp_fim, ctx->stream);
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    it = pl->sectors.emplace(key, std::move(b)).first;
+  }
+  auto& b = *it->second;
+  if (!b.prog.ok) return nullptr;
+  static thread_local SectorDev sd;
+  sd.size = b.prog.size;
+  sd.half = (b.prog.size + 1) / 2;
+  sd.hf_idx = b.prog.hf_idx;
+  sd.n_ops = (int)pl->cp.op_kind.size();
+  sd.gen_off = b.gen_off.p;
+  sd.gen_pairs = b.gen_pairs.p;
+  sd.gen_flags = b.gen_flags.p;
+  sd.n_exp = (int64_t)b.prog.exp_pairs.size();
+  sd.exp_pairs = b.exp_pairs.p;
+  sd.exp_fre = b.exp_fre.p;
+  sd.exp_fim = b.prog.f_real ? nullptr : b.exp_fim.p;
+  return &sd;
+}
+
+void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
+                   double* e, double* im) {
+  constexpr int CL = 2, NT = kSectorThreads;
+  const size_t sb = ((size_t)sd.half + pl->cp.op_kind.size()) * sizeof(double2);
+  CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)batch * CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sb;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_sector_eval<CL, NT>, sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch));
+  ctx->launches++;
+}
+
 bool use_smem_path(ffq_ctx_t ctx, const ffq_plan_s* pl) {
   return pl->cp.n_qubits <= ctx->smem_max_qubits && smem_bytes(pl) <= ctx->smem_optin;
 }
@@ -386,6 +461,12 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
     CK(cudaGetLastError());
     ctx->launches++;
     return;
+  }
+  if (ctx->sector && n > ctx->smem_max_qubits) {
+    if (const SectorDev* sd = sector_program(ctx, pl, h, hf)) {
+      launch_sector(ctx, pl, *sd, theta_dev, batch, e_dev, im_dev);
+      return;
+    }
   }
   if (use_persistent(ctx, pl, h)) {
     const int64_t dim = 1LL << n;
@@ -563,6 +644,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
     if (const char* e = std::getenv("FFQ_ROW_PAD")) c->row_pad = std::atoll(e);
     if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_SECTOR")) c->sector = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     return FFQ_OK;

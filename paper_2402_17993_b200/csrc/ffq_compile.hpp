@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstring>
 #include <cstdint>
 #include <map>
 #include <stdexcept>
@@ -541,6 +542,120 @@ inline FusedDesc physical_fused(const FusedDesc& d, const std::vector<int>& perm
   p.qpack = pack_q(p.q, p.w);
   hi_positions(p.x, p.whi, p.qpack_hi);
   return p;
+}
+
+}  // namespace ffq
+
+#include <unordered_map>
+
+namespace ffq {
+
+// ---- support-closure ("sector") program ------------------------------------------
+// S = amplitudes reachable from |hf> through the plan's pair maps (k <-> k ^ X
+// on the active patterns of each fused generator), computed once per
+// (plan, Hamiltonian, hf). Every amplitude outside S is identically zero for
+// ANY theta, so an evaluation only needs the |S| amplitudes of S:
+//  * generator g updates its pairs (i, j) inside S (indices into S, ascending k),
+//  * <H> = sum over pairs (m, m ^ X) with both members in S of
+//    Re(conj(psi[m ^ X]) psi[m] f(m)),  f(m) = sum_o sgn(m & z_o) F_o[p]
+//    precomputed per pair and deduplicated into a table.
+struct SectorProgram {
+  bool ok = false;
+  std::string why;  // reason when !ok
+  int n = 0;
+  uint32_t size = 0, hf_idx = 0;
+  std::vector<uint32_t> basis;      // S, ascending
+  std::vector<int64_t> gen_off;     // [n_ops + 1] into gen_pairs
+  std::vector<uint32_t> gen_pairs;  // i | j << 16 (i: low-pattern member)
+  std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
+  std::vector<uint32_t> exp_pairs;  // i | j << 16 (i: enumerated m, j: m ^ X)
+  std::vector<double> exp_fre, exp_fim;  // f per pair (exp_fim empty when every f is real)
+  bool f_real = true;
+};
+
+inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
+                                    uint32_t max_size) {
+  SectorProgram S;
+  const int n = P.n_qubits;
+  S.n = n;
+  if (n > 26 || H.n_qubits != n) { S.why = "qubit count"; return S; }
+  if (P.n_string_ops() > 0) { S.why = "plan has non-fused generators"; return S; }
+  const size_t dim = size_t(1) << n;
+  std::vector<int32_t> idx(dim, -1);
+  std::vector<uint32_t> list{(uint32_t)hf};
+  idx[hf] = 0;
+  // closure in plan order; record each generator's pairs in terms of k values
+  const int n_ops = (int)P.op_kind.size();
+  std::vector<std::vector<std::pair<uint32_t, uint8_t>>> gk(n_ops);
+  // pos[k] = position of k in `list` (insertion order), -1 if absent; the
+  // support before op g is list[0, cur)
+  std::vector<int32_t> pos(dim, -1);
+  pos[hf] = 0;
+  for (int op = 0; op < n_ops; ++op) {
+    const FusedDesc& d = P.fused[P.op_idx[op]];
+    const size_t cur = list.size();
+    for (size_t t = 0; t < cur; ++t) {
+      const uint32_t k = list[t];
+      const uint64_t pat = k & d.x;
+      for (int p = 0; p < d.npair; ++p) {
+        const uint64_t lo = P.pair_bits[d.pair_off + p], hi = lo ^ d.x;
+        if (pat != lo && pat != hi) continue;
+        const uint32_t kl = (pat == lo) ? k : (uint32_t)(k ^ d.x);  // low-pattern member
+        const uint32_t kh = kl ^ (uint32_t)d.x;
+        // record each pair once: from its low member when that was already supported
+        if (pat == hi && pos[kl] >= 0 && (size_t)pos[kl] < cur) continue;
+        const uint8_t flag = (uint8_t)(((__builtin_popcountll(kl & d.zout) & 1) ? 1 : 0) | (p << 1));
+        gk[op].push_back({kl, flag});
+        if (pos[kh] < 0) { pos[kh] = (int32_t)list.size(); list.push_back(kh); }
+        if (pos[kl] < 0) { pos[kl] = (int32_t)list.size(); list.push_back(kl); }
+      }
+      if (list.size() > max_size) { S.why = "support closure too large"; return S; }
+    }
+  }
+  std::sort(list.begin(), list.end());
+  S.basis = list;
+  S.size = (uint32_t)list.size();
+  if (S.size > 65535) { S.why = "support closure exceeds 16-bit indices"; return S; }
+  for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
+  S.hf_idx = (uint32_t)idx[hf];
+  S.gen_off.push_back(0);
+  for (int op = 0; op < n_ops; ++op) {
+    const FusedDesc& d = P.fused[P.op_idx[op]];
+    for (auto& e : gk[op]) {
+      const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
+      S.gen_pairs.push_back(i | (j << 16));
+      S.gen_flags.push_back(e.second);
+    }
+    S.gen_off.push_back((int64_t)S.gen_pairs.size());
+  }
+  // expectation pairs with their class sums f(m)
+  for (const auto& d : H.groups) {
+    uint64_t Q = 0;
+    for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
+    for (int p = 0; p < d.nact; ++p) {
+      const uint64_t pb = H.act_bits[d.act_off + p];
+      for (uint32_t i = 0; i < S.size; ++i) {
+        const uint32_t m = list[i];
+        if ((m & Q) != pb) continue;
+        const int32_t j = idx[m ^ (uint32_t)d.x];
+        if (j < 0) continue;
+        double fr = 0.0, fi = 0.0;
+        for (int o = 0; o < d.ncls; ++o) {
+          const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
+          fr += sg * H.cls_f[2 * (d.val_off + o * d.nact + p)];
+          fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
+        }
+        if (fr == 0.0 && fi == 0.0) continue;
+        S.exp_pairs.push_back(i | ((uint32_t)j << 16));
+        S.exp_fre.push_back(fr);
+        S.exp_fim.push_back(fi);
+        if (fi != 0.0) S.f_real = false;
+      }
+    }
+  }
+  if (S.f_real) S.exp_fim.clear();
+  S.ok = true;
+  return S;
 }
 
 }  // namespace ffq

@@ -13,14 +13,15 @@ pytestmark = pytest.mark.gpu
 
 PATHS = {
     "smem": {},
-    "graph-dense": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SUPPORT": "0"},
-    "graph-support": {"FFQ_SMEM_MAX_QUBITS": "0"},
-    "persistent": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_PERSIST": "1"},
+    "graph-dense": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SUPPORT": "0", "FFQ_SECTOR": "0"},
+    "graph-support": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SECTOR": "0"},
+    "persistent": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_PERSIST": "1", "FFQ_SECTOR": "0"},
+    "sector": {"FFQ_SMEM_MAX_QUBITS": "0"},
 }
 
 
 def _ctx(monkeypatch, env):
-    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST"):
+    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST", "FFQ_SECTOR"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -119,7 +120,7 @@ def test_theta_periodicity_and_zero(ctx_default, config):
 
 def test_batch_not_multiple_of_chunk(monkeypatch):
     # the graph path's last chunk recomputes stale rows; their outputs must not leak
-    c = _ctx(monkeypatch, {"FFQ_SMEM_MAX_QUBITS": "0"})
+    c = _ctx(monkeypatch, {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SECTOR": "0"})
     monkeypatch.setenv("FFQ_SLAB_MB", "1")  # 1 MiB slab: 16 rows of 12 qubits per chunk
     c = capi.Context(0)
     P = problems.config_problem(2, batch=37)

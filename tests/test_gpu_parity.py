@@ -192,9 +192,10 @@ def test_execution_paths_agree(monkeypatch, config):
     # dense graph path, support-tracked graph path, persistent per-state path
     P = problems.config_problem(config, batch=6)
     out = {}
-    for name, env in (("dense", {"FFQ_SUPPORT": "0", "FFQ_PERSIST": "0"}),
-                      ("graph", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "0"}),
-                      ("persistent", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "1"})):
+    for name, env in (("dense", {"FFQ_SUPPORT": "0", "FFQ_PERSIST": "0", "FFQ_SECTOR": "0"}),
+                      ("graph", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "0", "FFQ_SECTOR": "0"}),
+                      ("persistent", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "1", "FFQ_SECTOR": "0"}),
+                      ("sector", {"FFQ_SUPPORT": "1", "FFQ_PERSIST": "0", "FFQ_SECTOR": "1"})):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         monkeypatch.setenv("FFQ_SMEM_MAX_QUBITS", "0")
@@ -202,7 +203,7 @@ def test_execution_paths_agree(monkeypatch, config):
         plan, ham = upload(c, P)
         out[name] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
         out[name + "2"] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas()[::-1])[::-1]
-    for name in ("graph", "persistent"):
+    for name in ("graph", "persistent", "sector"):
         assert np.abs(out[name] - out["dense"]).max() <= 1e-12
         assert np.array_equal(out[name], out[name + "2"])  # the slab is left clean
 
@@ -230,3 +231,16 @@ def test_dense_random_state_plan_and_expectation_vs_oracle(ctx, oracle):
     st.rotate(0b101 << 3, 0b11, 0.3)
     ref = oracle.apply_pauli_rotation(n, ref, 0b101 << 3, 0b11, 0.3)
     assert abs(st.expectation(ham)[0].real - oracle.expectation(n, ref, oracle_H(oracle, P)).real) <= E_TOL
+
+
+def test_sector_path_18q_vs_oracle_and_dense(monkeypatch, oracle):
+    P = problems.config_problem(3, batch=3)
+    monkeypatch.setenv("FFQ_SECTOR", "1")
+    c = capi.Context(0)
+    plan, ham = upload(c, P)
+    e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    assert abs(e[1] - oracle_energy(oracle, P, P.thetas[1])[0]) <= E_TOL
+    monkeypatch.setenv("FFQ_SECTOR", "0")
+    c2 = capi.Context(0)
+    plan2, ham2 = upload(c2, P)
+    assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
