@@ -385,11 +385,10 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   auto it = pl->sectors.find(key);
   if (it == pl->sectors.end()) {
     auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
-    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize);
-    if (b->prog.ok) {
-      const size_t half = (b->prog.size + 1) / 2;
-      if ((half + pl->cp.op_kind.size()) * sizeof(double2) > ctx->smem_optin) b->prog.ok = false;
-    }
+    const size_t tables = 3 * pl->cp.op_kind.size() * sizeof(double2);
+    const uint32_t max_half =
+        ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_half);
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
@@ -405,7 +404,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   if (!b.prog.ok) return nullptr;
   static thread_local SectorDev sd;
   sd.size = b.prog.size;
-  sd.half = (b.prog.size + 1) / 2;
+  sd.half = b.prog.split;
+  for (int r = 0; r < 3; ++r) sd.exp_off[r] = b.prog.exp_off[r];
   sd.hf_idx = b.prog.hf_idx;
   sd.n_ops = (int)pl->cp.op_kind.size();
   sd.gen_off = b.gen_off.p;
@@ -421,7 +421,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
 void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
                    double* e, double* im) {
   constexpr int CL = 2, NT = kSectorThreads;
-  const size_t sb = ((size_t)sd.half + pl->cp.op_kind.size()) * sizeof(double2);
+  const size_t hmax = std::max<size_t>(sd.half, sd.size - sd.half);
+  const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2);
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -436,8 +437,21 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_sector_eval<CL, NT>, sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch));
+  static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
+  DevBuf<long long> clk;
+  if (clocks) clk.alloc(2 * (size_t)batch);
+  CK(cudaLaunchKernelEx(&cfg, k_sector_eval<CL, NT>, sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
+                        clocks ? clk.p : (long long*)nullptr));
   ctx->launches++;
+  if (clocks) {
+    std::vector<long long> hc(2 * (size_t)batch);
+    CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double g = 0, x = 0;
+    for (int r = 0; r < batch; ++r) { g += (double)hc[2 * r]; x += (double)hc[2 * r + 1]; }
+    std::fprintf(stderr, "[ffq] sector rows=%d avg cycles: generators %.0f expectation %.0f\n", batch,
+                 g / batch, x / batch);
+  }
 }
 
 bool use_smem_path(ffq_ctx_t ctx, const ffq_plan_s* pl) {

@@ -564,17 +564,21 @@ struct SectorProgram {
   std::string why;  // reason when !ok
   int n = 0;
   uint32_t size = 0, hf_idx = 0;
-  std::vector<uint32_t> basis;      // S, ascending
-  std::vector<int64_t> gen_off;     // [n_ops + 1] into gen_pairs
+  int split_bit = -1;               // S ordered by (bit split_bit of k, k): CTA 0 holds bit = 0
+  uint32_t split = 0;               // |{k in S : bit = 0}|
+  std::vector<uint32_t> basis;      // S in (split bit, k) order
+  std::vector<int64_t> gen_off;     // [2 * n_ops + 1]: op g, owner rank r -> gen_off[2g + r]
   std::vector<uint32_t> gen_pairs;  // i | j << 16 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
   std::vector<uint32_t> exp_pairs;  // i | j << 16 (i: enumerated m, j: m ^ X)
   std::vector<double> exp_fre, exp_fim;  // f per pair (exp_fim empty when every f is real)
+  int64_t exp_off[3] = {0, 0, 0};   // pairs owned (by i) by rank 0, rank 1
   bool f_real = true;
+  int64_t cross_pairs = 0;          // pairs whose members live in different CTAs
 };
 
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
-                                    uint32_t max_size) {
+                                    uint32_t max_size, uint32_t max_half = 0xFFFFFFFFu) {
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -612,33 +616,19 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       if (list.size() > max_size) { S.why = "support closure too large"; return S; }
     }
   }
-  std::sort(list.begin(), list.end());
-  S.basis = list;
-  S.size = (uint32_t)list.size();
-  if (S.size > 65535) { S.why = "support closure exceeds 16-bit indices"; return S; }
-  for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
-  S.hf_idx = (uint32_t)idx[hf];
-  S.gen_off.push_back(0);
-  for (int op = 0; op < n_ops; ++op) {
-    const FusedDesc& d = P.fused[P.op_idx[op]];
-    for (auto& e : gk[op]) {
-      const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
-      S.gen_pairs.push_back(i | (j << 16));
-      S.gen_flags.push_back(e.second);
-    }
-    S.gen_off.push_back((int64_t)S.gen_pairs.size());
-  }
-  // expectation pairs with their class sums f(m)
-  for (const auto& d : H.groups) {
+  // expectation pairs in k space (m, X index) with f(m)
+  std::vector<int32_t>& inS = pos;  // pos[k] >= 0 <=> k in S
+  struct EP { uint32_t m; int g; double fr, fi; };
+  std::vector<EP> ek;
+  for (size_t gi = 0; gi < H.groups.size(); ++gi) {
+    const auto& d = H.groups[gi];
     uint64_t Q = 0;
     for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
     for (int p = 0; p < d.nact; ++p) {
       const uint64_t pb = H.act_bits[d.act_off + p];
-      for (uint32_t i = 0; i < S.size; ++i) {
-        const uint32_t m = list[i];
+      for (uint32_t m : list) {
         if ((m & Q) != pb) continue;
-        const int32_t j = idx[m ^ (uint32_t)d.x];
-        if (j < 0) continue;
+        if (inS[m ^ (uint32_t)d.x] < 0) continue;
         double fr = 0.0, fi = 0.0;
         for (int o = 0; o < d.ncls; ++o) {
           const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
@@ -646,12 +636,62 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
           fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
         }
         if (fr == 0.0 && fi == 0.0) continue;
-        S.exp_pairs.push_back(i | ((uint32_t)j << 16));
-        S.exp_fre.push_back(fr);
-        S.exp_fim.push_back(fi);
-        if (fi != 0.0) S.f_real = false;
+        ek.push_back({m, (int)gi, fr, fi});
       }
     }
+  }
+  // split bit: fewest pairs crossing the two CTAs, both halves within max_half
+  S.size = (uint32_t)list.size();
+  int best = -1;
+  int64_t best_cross = -1;
+  for (int b = 0; b < n; ++b) {
+    uint32_t zero = 0;
+    for (uint32_t k : list) zero += !((k >> b) & 1u);
+    if (zero > max_half || S.size - zero > max_half) continue;
+    int64_t cross = 0;
+    for (int op = 0; op < n_ops; ++op)
+      if ((P.fused[P.op_idx[op]].x >> b) & 1ULL) cross += (int64_t)gk[op].size();
+    for (const auto& e : ek)
+      if ((H.groups[e.g].x >> b) & 1ULL) ++cross;
+    if (best < 0 || cross < best_cross) { best = b; best_cross = cross; }
+  }
+  if (best < 0) { S.why = "no qubit splits the support closure into two halves that fit"; return S; }
+  S.split_bit = best;
+  S.cross_pairs = best_cross;
+  std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t c) {
+    const uint32_t ba = (a >> best) & 1u, bc = (c >> best) & 1u;
+    return ba != bc ? ba < bc : a < c;
+  });
+  S.basis = list;
+  if (S.size > 65535) { S.why = "support closure exceeds 16-bit indices"; return S; }
+  S.split = 0;
+  for (uint32_t k : list) S.split += !((k >> best) & 1u);
+  for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
+  S.hf_idx = (uint32_t)idx[hf];
+  auto owner = [&](uint32_t i) { return i < S.split ? 0 : 1; };
+  S.gen_off.assign(1, 0);
+  for (int op = 0; op < n_ops; ++op) {
+    const FusedDesc& d = P.fused[P.op_idx[op]];
+    for (int r = 0; r < 2; ++r) {
+      for (auto& e : gk[op]) {
+        const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
+        if (owner(i) != r) continue;
+        S.gen_pairs.push_back(i | (j << 16));
+        S.gen_flags.push_back(e.second);
+      }
+      S.gen_off.push_back((int64_t)S.gen_pairs.size());
+    }
+  }
+  for (int r = 0; r < 2; ++r) {
+    for (const auto& e : ek) {
+      const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
+      if (owner(i) != r) continue;
+      S.exp_pairs.push_back(i | (j << 16));
+      S.exp_fre.push_back(e.fr);
+      S.exp_fim.push_back(e.fi);
+      if (e.fi != 0.0) S.f_real = false;
+    }
+    S.exp_off[r + 1] = (int64_t)S.exp_pairs.size();
   }
   if (S.f_real) S.exp_fim.clear();
   S.ok = true;

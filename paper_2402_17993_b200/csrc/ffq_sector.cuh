@@ -23,9 +23,10 @@ namespace ffq {
 namespace cg = cooperative_groups;
 
 struct SectorDev {
-  uint32_t size, half, hf_idx;
+  uint32_t size, half, hf_idx;  // half = split: CTA 0 holds S[0, half), CTA 1 holds S[half, size)
   int n_ops;
-  const int64_t* gen_off;
+  int64_t exp_off[3];
+  const int64_t* gen_off;       // [2 * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;
   const uint8_t* gen_flags;
   int64_t n_exp;
@@ -37,47 +38,76 @@ struct SectorDev {
 template <int CL, int NT>
 __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl, const double* __restrict__ theta,
                                                        int theta_stride, double* __restrict__ e_out,
-                                                       double* __restrict__ im_out, int n_rows) {
-  extern __shared__ __align__(16) double2 sm_c[];  // [half] amplitudes, then [n_ops] rotation coefficients
+                                                       double* __restrict__ im_out, int n_rows,
+                                                       long long* __restrict__ phase_clk) {
+  // dynamic smem: [half] amplitudes | [n_ops] (cos, sin*scale) | [n_ops] (F_lo, F_hi) of pattern pair 0
+  extern __shared__ __align__(16) double2 sm_c[];
   __shared__ double2 red[NT / 32];
   __shared__ double cl_part[CL];
+  const long long clk0 = clock64();
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int row = blockIdx.x / CL;
   if (row >= n_rows) return;  // whole clusters exit together (grid = n_rows * CL)
   const uint32_t H = sd.half;
-  double2* cs = sm_c + H;
-  // base pointers of both halves (local smem and the peer CTA's, via DSMEM)
+  const uint32_t Hmax = CL == 1 ? sd.size : max(H, sd.size - H);
+  double2* cs = sm_c + Hmax;
+  double2* fz = cs + pl.n_ops;  // [2 * n_ops]
+  // base pointers of both halves: this CTA's half through the plain shared
+  // window (LDS/STS), the peer's through the distributed-shared window
   double2* part[CL];
 #pragma unroll
-  for (int r = 0; r < CL; ++r) part[r] = cluster.map_shared_rank(sm_c, r);
+  for (int r = 0; r < CL; ++r) part[r] = (r == rank) ? sm_c : cluster.map_shared_rank(sm_c, r);
   auto at = [&](uint32_t i) -> double2* {
     if (CL == 1) return sm_c + i;
     return i < H ? part[0] + i : part[1] + (i - H);
   };
-  for (uint32_t i = threadIdx.x; i < H; i += NT) sm_c[i] = make_double2(0.0, 0.0);
+  for (uint32_t i = threadIdx.x; i < Hmax; i += NT) sm_c[i] = make_double2(0.0, 0.0);
   for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
     const double phi = theta[(int64_t)row * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
     double sv, cv;
     sincos(phi, &sv, &cv);
     cs[op] = make_double2(cv, sv * pl.op_sscale[op]);
+    const int po = pl.fused[pl.op_idx[op]].pair_off;
+    fz[2 * op] = pl.pair_f[2 * po];
+    fz[2 * op + 1] = pl.pair_f[2 * po + 1];
   }
   cluster.sync();
-  if (rank == 0 && threadIdx.x == 0) *at(sd.hf_idx) = make_double2(1.0, 0.0);
+  if (threadIdx.x == 0 && (CL == 1 || (int)(sd.hf_idx >= H) == rank)) *at(sd.hf_idx) = make_double2(1.0, 0.0);
   cluster.sync();
-  const int tid = rank * NT + threadIdx.x;
-  constexpr int NTC = CL * NT;
+  // each CTA processes the pairs whose first member it owns (mostly local:
+  // S is split on the qubit the fewest flip masks touch)
+  const int tid = threadIdx.x;
+  int64_t nx0 = sd.gen_off[rank] + tid, nx1 = sd.gen_off[rank + 1];
+  uint32_t nij = nx0 < nx1 ? sd.gen_pairs[nx0] : 0u;
+  uint8_t nfl = nx0 < nx1 ? sd.gen_flags[nx0] : (uint8_t)0;
   for (int op = 0; op < sd.n_ops; ++op) {
     const double2 csv = cs[op];
     const double c = csv.x, sn = csv.y;
-    const FusedDesc d = pl.fused[pl.op_idx[op]];
-    const int64_t t0 = sd.gen_off[op], t1 = sd.gen_off[op + 1];
-    for (int64_t t = t0 + tid; t < t1; t += NTC) {
-      const uint32_t ij = sd.gen_pairs[t];
-      const uint8_t fl = sd.gen_flags[t];
-      const int p = fl >> 1;
+    const int64_t t0 = nx0, t1 = nx1;
+    uint32_t ij = nij;
+    uint8_t fl = nfl;
+    if (op + 1 < sd.n_ops) {
+      nx0 = sd.gen_off[2 * (op + 1) + rank] + tid;
+      nx1 = sd.gen_off[2 * (op + 1) + rank + 1];
+      nij = nx0 < nx1 ? __ldg(sd.gen_pairs + nx0) : 0u;
+      nfl = nx0 < nx1 ? __ldg(sd.gen_flags + nx0) : (uint8_t)0;
+    }
+    for (int64_t t = t0; t < t1; t += NT) {
+      if (t != t0) {
+        ij = __ldg(sd.gen_pairs + t);
+        fl = __ldg(sd.gen_flags + t);
+      }
+      double2 flo, fhi;
+      if ((fl >> 1) == 0) {
+        flo = fz[2 * op];
+        fhi = fz[2 * op + 1];
+      } else {  // more than one active pattern pair (not UCCSD)
+        const int po = pl.fused[pl.op_idx[op]].pair_off + (fl >> 1);
+        flo = pl.pair_f[2 * po];
+        fhi = pl.pair_f[2 * po + 1];
+      }
       const double g = (fl & 1u) ? -sn : sn;
-      const double2 flo = pl.pair_f[2 * (d.pair_off + p)], fhi = pl.pair_f[2 * (d.pair_off + p) + 1];
       double2* pa = at(ij & 0xFFFFu);
       double2* pb = at(ij >> 16);
       const double2 a = *pa, bb = *pb;
@@ -85,18 +115,36 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
       *pa = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
       *pb = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
     }
-    cluster.sync();
+    if (CL > 1) cluster.sync(); else __syncthreads();
   }
-  // <H>: sum over (m, m ^ X) pairs of Re(conj(psi[j]) psi[i] f)
+  const long long clk1 = clock64();
+  // <H>: sum over (m, m ^ X) pairs of Re(conj(psi[j]) psi[i] f); four pairs per
+  // trip with every table and amplitude load issued before the arithmetic
   double acc = 0.0;
-  for (int64_t t = tid; t < sd.n_exp; t += NTC) {
-    const uint32_t ij = sd.exp_pairs[t];
-    const double2 a = *at(ij & 0xFFFFu), bb = *at(ij >> 16);
-    const double prx = bb.x * a.x + bb.y * a.y;
-    acc = fma(prx, sd.exp_fre[t], acc);
-    if (sd.exp_fim) {
-      const double pry = bb.x * a.y - bb.y * a.x;
-      acc = fma(-pry, sd.exp_fim[t], acc);
+  const int64_t e1 = sd.exp_off[rank + 1];
+  for (int64_t t = sd.exp_off[rank] + tid; t < e1; t += 4 * NT) {
+    uint32_t ij[4];
+    double fr[4], fi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t tu = t + (int64_t)u * NT;
+      const bool ok = tu < e1;
+      ij[u] = ok ? __ldg(sd.exp_pairs + tu) : 0u;
+      fr[u] = ok ? __ldg(sd.exp_fre + tu) : 0.0;
+      fi[u] = (ok && sd.exp_fim) ? __ldg(sd.exp_fim + tu) : 0.0;
+    }
+    double2 a[4], bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = *at(ij[u] & 0xFFFFu);
+      bb[u] = *at(ij[u] >> 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double prx = bb[u].x * a[u].x + bb[u].y * a[u].y;
+      const double pry = bb[u].x * a[u].y - bb[u].y * a[u].x;
+      acc = fma(prx, fr[u], acc);
+      acc = fma(-pry, fi[u], acc);
     }
   }
   const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
@@ -109,6 +157,10 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     for (int r = 0; r < CL; ++r) e += cl_part[r];
     e_out[row] = e;
     if (im_out) im_out[row] = 0.0;
+    if (phase_clk) {  // diagnostics (FFQ_PHASE_CLOCKS): generator / expectation cycles
+      phase_clk[2 * row] = clk1 - clk0;
+      phase_clk[2 * row + 1] = clock64() - clk1;
+    }
   }
 }
 
