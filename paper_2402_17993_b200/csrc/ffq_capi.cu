@@ -132,7 +132,8 @@ struct ffq_plan_s {
     DevBuf<int64_t> gen_off;
     DevBuf<uint32_t> gen_pairs, exp_pairs;
     DevBuf<uint8_t> gen_flags;
-    DevBuf<double> exp_fre, exp_fim;
+    DevBuf<double> exp_fre, exp_fim, seg_fre, seg_fim;
+    DevBuf<int64_t> seg_start, seg_foff;
   };
   std::map<std::pair<const void*, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;
   PlanDev dev() const {
@@ -385,7 +386,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   auto it = pl->sectors.find(key);
   if (it == pl->sectors.end()) {
     auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
-    const size_t tables = 3 * pl->cp.op_kind.size() * sizeof(double2);
+    const size_t tables = 3 * pl->cp.op_kind.size() * sizeof(double2) + pl->cp.op_kind.size() + 16;
     const uint32_t max_half =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_half);
@@ -396,6 +397,10 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
       b->exp_pairs.upload(b->prog.exp_pairs, ctx->stream);
       b->exp_fre.upload(b->prog.exp_fre, ctx->stream);
       if (!b->prog.f_real) b->exp_fim.upload(b->prog.exp_fim, ctx->stream);
+      b->seg_start.upload(b->prog.seg_start, ctx->stream);
+      b->seg_foff.upload(b->prog.seg_foff, ctx->stream);
+      b->seg_fre.upload(b->prog.seg_fre, ctx->stream);
+      b->seg_fim.upload(b->prog.seg_fim, ctx->stream);
       CK(cudaStreamSynchronize(ctx->stream));
     }
     it = pl->sectors.emplace(key, std::move(b)).first;
@@ -405,7 +410,15 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   static thread_local SectorDev sd;
   sd.size = b.prog.size;
   sd.half = b.prog.split;
-  for (int r = 0; r < 3; ++r) sd.exp_off[r] = b.prog.exp_off[r];
+  for (int r = 0; r < 3; ++r) {
+    sd.exp_off[r] = b.prog.exp_off[r];
+    sd.seg_off[r] = b.prog.seg_off[r];
+  }
+  sd.split_bit = b.prog.split_bit;
+  sd.seg_start = b.seg_start.p;
+  sd.seg_foff = b.seg_foff.p;
+  sd.seg_fre = b.seg_fre.p;
+  sd.seg_fim = b.seg_fim.p;
   sd.hf_idx = b.prog.hf_idx;
   sd.n_ops = (int)pl->cp.op_kind.size();
   sd.gen_off = b.gen_off.p;
@@ -422,7 +435,7 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
                    double* e, double* im) {
   constexpr int CL = 2, NT = kSectorThreads;
   const size_t hmax = std::max<size_t>(sd.half, sd.size - sd.half);
-  const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2);
+  const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2) + pl->cp.op_kind.size() + 16;
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};

@@ -559,6 +559,8 @@ namespace ffq {
 //  * <H> = sum over pairs (m, m ^ X) with both members in S of
 //    Re(conj(psi[m ^ X]) psi[m] f(m)),  f(m) = sum_o sgn(m & z_o) F_o[p]
 //    precomputed per pair and deduplicated into a table.
+constexpr size_t kSegChunk = 512;
+
 struct SectorProgram {
   bool ok = false;
   std::string why;  // reason when !ok
@@ -570,8 +572,15 @@ struct SectorProgram {
   std::vector<int64_t> gen_off;     // [2 * n_ops + 1]: op g, owner rank r -> gen_off[2g + r]
   std::vector<uint32_t> gen_pairs;  // i | j << 16 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
-  std::vector<uint32_t> exp_pairs;  // i | j << 16 (i: enumerated m, j: m ^ X)
-  std::vector<double> exp_fre, exp_fim;  // f per pair (exp_fim empty when every f is real)
+  // expectation pairs, i | j << 15 | sign << 30 (i: enumerated m, j: m ^ X),
+  // in segments of one (group, pattern) and owner rank. A segment whose pairs
+  // share |f| stores f once (seg_fre/fim) and a sign bit per pair; otherwise
+  // f is stored per pair at seg_foff.
+  std::vector<uint32_t> exp_pairs;
+  std::vector<double> exp_fre, exp_fim;  // per-pair f of per-pair segments (exp_fim empty if all real)
+  std::vector<int64_t> seg_start, seg_foff;  // seg_foff < 0: shared-f segment
+  std::vector<double> seg_fre, seg_fim;
+  int32_t seg_off[3] = {0, 0, 0};   // segments of rank 0, rank 1
   int64_t exp_off[3] = {0, 0, 0};   // pairs owned (by i) by rank 0, rank 1
   bool f_real = true;
   int64_t cross_pairs = 0;          // pairs whose members live in different CTAs
@@ -618,7 +627,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   }
   // expectation pairs in k space (m, X index) with f(m)
   std::vector<int32_t>& inS = pos;  // pos[k] >= 0 <=> k in S
-  struct EP { uint32_t m; int g; double fr, fi; };
+  struct EP { uint32_t m; int g, p; double fr, fi; };
   std::vector<EP> ek;
   for (size_t gi = 0; gi < H.groups.size(); ++gi) {
     const auto& d = H.groups[gi];
@@ -636,7 +645,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
           fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
         }
         if (fr == 0.0 && fi == 0.0) continue;
-        ek.push_back({m, (int)gi, fr, fi});
+        ek.push_back({m, (int)gi, p, fr, fi});
       }
     }
   }
@@ -682,17 +691,50 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
     }
   }
+  if (S.size > 32767) { S.why = "support closure exceeds 15-bit indices"; return S; }
+  for (const auto& e : ek)
+    if (e.fi != 0.0) S.f_real = false;
+  // ek is ordered by (group, pattern): cut it into segments per owner rank
+  size_t a = 0;
+  std::vector<std::vector<size_t>> segs;  // boundaries of (group, pattern) runs
+  while (a < ek.size()) {
+    size_t b = a + 1;
+    while (b < ek.size() && ek[b].g == ek[a].g && ek[b].p == ek[a].p) ++b;
+    segs.push_back({a, b});
+    a = b;
+  }
   for (int r = 0; r < 2; ++r) {
-    for (const auto& e : ek) {
-      const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
-      if (owner(i) != r) continue;
-      S.exp_pairs.push_back(i | (j << 16));
-      S.exp_fre.push_back(e.fr);
-      S.exp_fim.push_back(e.fi);
-      if (e.fi != 0.0) S.f_real = false;
+    for (const auto& sg : segs) {
+      std::vector<size_t> mine;
+      for (size_t t = sg[0]; t < sg[1]; ++t)
+        if (owner((uint32_t)idx[ek[t].m]) == r) mine.push_back(t);
+      if (mine.empty()) continue;
+      const double fr0 = ek[mine[0]].fr, fi0 = ek[mine[0]].fi;
+      bool shared = true;
+      for (size_t t : mine)
+        if (!((ek[t].fr == fr0 && ek[t].fi == fi0) || (ek[t].fr == -fr0 && ek[t].fi == -fi0))) { shared = false; break; }
+      // chunks of <= kSegChunk pairs, one warp each on the device
+      for (size_t c0 = 0; c0 < mine.size(); c0 += kSegChunk) {
+        S.seg_start.push_back((int64_t)S.exp_pairs.size() + (int64_t)c0);
+        S.seg_foff.push_back(shared ? -1 : (int64_t)S.exp_fre.size() + (int64_t)c0);
+        S.seg_fre.push_back(shared ? fr0 : 0.0);
+        S.seg_fim.push_back(shared ? fi0 : 0.0);
+      }
+      for (size_t t : mine) {
+        const auto& e = ek[t];
+        const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
+        const uint32_t neg = shared && (e.fr != fr0 || e.fi != fi0) ? 1u : 0u;
+        S.exp_pairs.push_back(i | (j << 15) | (neg << 30));
+        if (!shared) {
+          S.exp_fre.push_back(e.fr);
+          S.exp_fim.push_back(e.fi);
+        }
+      }
     }
+    S.seg_off[r + 1] = (int32_t)S.seg_start.size();
     S.exp_off[r + 1] = (int64_t)S.exp_pairs.size();
   }
+  S.seg_start.push_back((int64_t)S.exp_pairs.size());  // sentinel
   if (S.f_real) S.exp_fim.clear();
   S.ok = true;
   return S;

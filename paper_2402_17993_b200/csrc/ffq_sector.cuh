@@ -25,7 +25,13 @@ namespace cg = cooperative_groups;
 struct SectorDev {
   uint32_t size, half, hf_idx;  // half = split: CTA 0 holds S[0, half), CTA 1 holds S[half, size)
   int n_ops;
+  int split_bit;                // generators flipping it need a cluster barrier
   int64_t exp_off[3];
+  int32_t seg_off[3];
+  const int64_t* seg_start;     // [n_seg + 1]
+  const int64_t* seg_foff;      // < 0: shared |f| (seg_fre/fim), else per-pair f offset
+  const double* seg_fre;
+  const double* seg_fim;
   const int64_t* gen_off;       // [2 * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;
   const uint8_t* gen_flags;
@@ -53,6 +59,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   const uint32_t Hmax = CL == 1 ? sd.size : max(H, sd.size - H);
   double2* cs = sm_c + Hmax;
   double2* fz = cs + pl.n_ops;  // [2 * n_ops]
+  uint8_t* crossf = reinterpret_cast<uint8_t*>(fz + 2 * pl.n_ops);  // [n_ops]
   // base pointers of both halves: this CTA's half through the plain shared
   // window (LDS/STS), the peer's through the distributed-shared window
   double2* part[CL];
@@ -68,9 +75,10 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     double sv, cv;
     sincos(phi, &sv, &cv);
     cs[op] = make_double2(cv, sv * pl.op_sscale[op]);
-    const int po = pl.fused[pl.op_idx[op]].pair_off;
-    fz[2 * op] = pl.pair_f[2 * po];
-    fz[2 * op + 1] = pl.pair_f[2 * po + 1];
+    const FusedDesc& d = pl.fused[pl.op_idx[op]];
+    fz[2 * op] = pl.pair_f[2 * d.pair_off];
+    fz[2 * op + 1] = pl.pair_f[2 * d.pair_off + 1];
+    crossf[op] = (uint8_t)((d.x >> sd.split_bit) & 1ULL);
   }
   cluster.sync();
   if (threadIdx.x == 0 && (CL == 1 || (int)(sd.hf_idx >= H) == rank)) *at(sd.hf_idx) = make_double2(1.0, 0.0);
@@ -115,36 +123,55 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
       *pa = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
       *pb = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
     }
-    if (CL > 1) cluster.sync(); else __syncthreads();
+    // a generator whose flip mask avoids the split bit only touches this CTA's
+    // half: a CTA barrier suffices unless it or the next one crosses the split
+    const bool cross = crossf[op] != 0;
+    const bool next_cross = op + 1 < sd.n_ops && crossf[op + 1] != 0;
+    if (CL > 1 && (cross || next_cross)) cluster.sync(); else __syncthreads();
   }
   const long long clk1 = clock64();
   // <H>: sum over (m, m ^ X) pairs of Re(conj(psi[j]) psi[i] f); four pairs per
   // trip with every table and amplitude load issued before the arithmetic
+  // warp w takes this rank's segment chunks w, w + NT/32, ... (<= 512 pairs each);
+  // lanes stride the chunk four pairs at a time
   double acc = 0.0;
-  const int64_t e1 = sd.exp_off[rank + 1];
-  for (int64_t t = sd.exp_off[rank] + tid; t < e1; t += 4 * NT) {
-    uint32_t ij[4];
-    double fr[4], fi[4];
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int sg = sd.seg_off[rank] + warp; sg < sd.seg_off[rank + 1]; sg += NT / 32) {
+      const int64_t s0 = sd.seg_start[sg], s1 = sd.seg_start[sg + 1];
+      const int64_t foff = sd.seg_foff[sg];
+      const double Fr = sd.seg_fre[sg], Fi = sd.seg_fim[sg];
+      for (int64_t t = s0 + lane; t < s1; t += 128) {
+        uint32_t ij[4];
+        double fr[4], fi[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t tu = t + (int64_t)u * NT;
-      const bool ok = tu < e1;
-      ij[u] = ok ? __ldg(sd.exp_pairs + tu) : 0u;
-      fr[u] = ok ? __ldg(sd.exp_fre + tu) : 0.0;
-      fi[u] = (ok && sd.exp_fim) ? __ldg(sd.exp_fim + tu) : 0.0;
-    }
-    double2 a[4], bb[4];
+        for (int u = 0; u < 4; ++u) {
+          const int64_t tu = t + 32 * u;
+          const bool ok = tu < s1;
+          ij[u] = ok ? __ldg(sd.exp_pairs + tu) : 0u;
+          if (foff < 0) {
+            const double sg2 = (ij[u] >> 30) ? -1.0 : 1.0;
+            fr[u] = ok ? sg2 * Fr : 0.0;
+            fi[u] = ok ? sg2 * Fi : 0.0;
+          } else {
+            fr[u] = ok ? __ldg(sd.exp_fre + foff + (tu - s0)) : 0.0;
+            fi[u] = (ok && sd.exp_fim) ? __ldg(sd.exp_fim + foff + (tu - s0)) : 0.0;
+          }
+        }
+        double2 a[4], bb[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a[u] = *at(ij[u] & 0xFFFFu);
-      bb[u] = *at(ij[u] >> 16);
-    }
+        for (int u = 0; u < 4; ++u) {
+          a[u] = *at(ij[u] & 0x7FFFu);
+          bb[u] = *at((ij[u] >> 15) & 0x7FFFu);
+        }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double prx = bb[u].x * a[u].x + bb[u].y * a[u].y;
-      const double pry = bb[u].x * a[u].y - bb[u].y * a[u].x;
-      acc = fma(prx, fr[u], acc);
-      acc = fma(-pry, fi[u], acc);
+        for (int u = 0; u < 4; ++u) {
+          const double prx = bb[u].x * a[u].x + bb[u].y * a[u].y;
+          const double pry = bb[u].x * a[u].y - bb[u].y * a[u].x;
+          acc = fma(prx, fr[u], acc);
+          acc = fma(-pry, fi[u], acc);
+        }
+      }
     }
   }
   const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
