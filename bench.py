@@ -309,7 +309,7 @@ def main():
     ms2 = timed(f2, 3)
     config2 = {"evals": int(rows2.shape[0]), "ms_per_call": statistics.mean(ms2),
                "evals_per_s": rows2.shape[0] / (statistics.mean(ms2) / 1e3),
-               "path": "k_smem_eval (one CTA per evaluation, state in shared memory)"}
+               "path": "k_sector_eval<1,256> (one CTA per evaluation, support closure of 400 amplitudes)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

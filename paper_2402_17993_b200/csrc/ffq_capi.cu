@@ -377,6 +377,8 @@ bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
 }
 
 constexpr int kSectorThreads = 1024;
+// small closures run one CTA per evaluation (many per SM); large ones a 2-CTA cluster
+constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA
 constexpr uint32_t kSectorMaxSize = 32768;  // 2 CTAs x 16384 amplitudes (256 KiB) in DSMEM
 
 // compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
@@ -390,6 +392,10 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     const uint32_t max_half =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_half);
+    if (b->prog.ok && b->prog.size <= kSectorSingleMax) {
+      // one CTA holds all of S: every pair is local, rank 0 owns everything
+      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, /*single=*/true);
+    }
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
@@ -431,13 +437,14 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   return &sd;
 }
 
-void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
-                   double* e, double* im) {
-  constexpr int CL = 2, NT = kSectorThreads;
-  const size_t hmax = std::max<size_t>(sd.half, sd.size - sd.half);
+
+template <int CL, int NT>
+void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
+                     double* e, double* im, long long* clk) {
+  const size_t hmax = CL == 1 ? sd.size : std::max<size_t>(sd.half, sd.size - sd.half);
   const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2) + pl->cp.op_kind.size() + 16;
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (CL > 1) CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)batch * CL);
   cfg.blockDim = dim3(NT);
@@ -450,12 +457,19 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_sector_eval<CL, NT>, sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk));
+  ctx->launches++;
+}
+
+void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
+                   double* e, double* im) {
   static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
   DevBuf<long long> clk;
   if (clocks) clk.alloc(2 * (size_t)batch);
-  CK(cudaLaunchKernelEx(&cfg, k_sector_eval<CL, NT>, sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
-                        clocks ? clk.p : (long long*)nullptr));
-  ctx->launches++;
+  if (sd.size <= kSectorSingleMax)
+    launch_sector_t<1, 256>(ctx, pl, sd, theta, batch, e, im, clocks ? clk.p : nullptr);
+  else
+    launch_sector_t<2, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, clocks ? clk.p : nullptr);
   if (clocks) {
     std::vector<long long> hc(2 * (size_t)batch);
     CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
@@ -478,6 +492,14 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   if (h->ch.n_qubits != n) throw BadInput("plan and Hamiltonian qubit counts differ", FFQ_EINVAL);
   if (n < 64 && (hf >> n) != 0) throw BadInput("hf_bits exceeds n_qubits", FFQ_EINVAL);
   if (batch <= 0) return;
+  // support-closure evaluator first (FFQ_SECTOR=0 disables it); plans it cannot
+  // take (non-fused generators, closures beyond 32768 amplitudes) fall through
+  if (ctx->sector) {
+    if (const SectorDev* sd = sector_program(ctx, pl, h, hf)) {
+      launch_sector(ctx, pl, *sd, theta_dev, batch, e_dev, im_dev);
+      return;
+    }
+  }
   if (use_smem_path(ctx, pl)) {
     const size_t sb = smem_bytes(pl);
     CK(cudaFuncSetAttribute(k_smem_eval<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -488,12 +510,6 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
     CK(cudaGetLastError());
     ctx->launches++;
     return;
-  }
-  if (ctx->sector && n > ctx->smem_max_qubits) {
-    if (const SectorDev* sd = sector_program(ctx, pl, h, hf)) {
-      launch_sector(ctx, pl, *sd, theta_dev, batch, e_dev, im_dev);
-      return;
-    }
   }
   if (use_persistent(ctx, pl, h)) {
     const int64_t dim = 1LL << n;

@@ -587,7 +587,8 @@ struct SectorProgram {
 };
 
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
-                                    uint32_t max_size, uint32_t max_half = 0xFFFFFFFFu) {
+                                    uint32_t max_size, uint32_t max_half = 0xFFFFFFFFu,
+                                    bool single = false) {
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -653,7 +654,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   S.size = (uint32_t)list.size();
   int best = -1;
   int64_t best_cross = -1;
-  for (int b = 0; b < n; ++b) {
+  for (int b = 0; b < n && !single; ++b) {
     uint32_t zero = 0;
     for (uint32_t k : list) zero += !((k >> b) & 1u);
     if (zero > max_half || S.size - zero > max_half) continue;
@@ -664,17 +665,22 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       if ((H.groups[e.g].x >> b) & 1ULL) ++cross;
     if (best < 0 || cross < best_cross) { best = b; best_cross = cross; }
   }
+  if (single) {
+    // one CTA: no split; bit 63 is never set, so split_bit flips nothing
+    best = 63;
+    best_cross = 0;
+  }
   if (best < 0) { S.why = "no qubit splits the support closure into two halves that fit"; return S; }
   S.split_bit = best;
   S.cross_pairs = best_cross;
   std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t c) {
-    const uint32_t ba = (a >> best) & 1u, bc = (c >> best) & 1u;
+    const uint32_t ba = best < 32 ? (a >> best) & 1u : 0u, bc = best < 32 ? (c >> best) & 1u : 0u;
     return ba != bc ? ba < bc : a < c;
   });
   S.basis = list;
   if (S.size > 65535) { S.why = "support closure exceeds 16-bit indices"; return S; }
   S.split = 0;
-  for (uint32_t k : list) S.split += !((k >> best) & 1u);
+  for (uint32_t k : list) S.split += best < 32 ? !((k >> best) & 1u) : 1u;
   for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
   S.hf_idx = (uint32_t)idx[hf];
   auto owner = [&](uint32_t i) { return i < S.split ? 0 : 1; };

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   const int row = blockIdx.x / CL;
   if (row >= n_rows) return;  // whole clusters exit together (grid = n_rows * CL)
   const uint32_t H = sd.half;
-  const uint32_t Hmax = CL == 1 ? sd.size : max(H, sd.size - H);
+  const uint32_t Hmax = CL == 1 ? sd.size : max(H, sd.size - H);  // CL == 1: H == size
   double2* cs = sm_c + Hmax;
   double2* fz = cs + pl.n_ops;  // [2 * n_ops]
   uint8_t* crossf = reinterpret_cast<uint8_t*>(fz + 2 * pl.n_ops);  // [n_ops]

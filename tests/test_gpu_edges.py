@@ -12,7 +12,8 @@ from paper_2402_17993_b200 import capi, problems
 pytestmark = pytest.mark.gpu
 
 PATHS = {
-    "smem": {},
+    "sector-default": {},
+    "smem": {"FFQ_SECTOR": "0"},
     "graph-dense": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SUPPORT": "0", "FFQ_SECTOR": "0"},
     "graph-support": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SECTOR": "0"},
     "persistent": {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_PERSIST": "1", "FFQ_SECTOR": "0"},
@@ -129,3 +130,17 @@ def test_batch_not_multiple_of_chunk(monkeypatch):
     full = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
     one = np.array([capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas()[i:i + 1])[0] for i in range(37)])
     assert np.array_equal(full, one)
+
+
+def test_sector_single_cta_small_closure(monkeypatch, oracle):
+    # 12 qubits: closure of 400 amplitudes -> the one-CTA sector kernel (default),
+    # against the dense shared-memory evaluator (FFQ_SECTOR=0)
+    P = problems.config_problem(2, batch=9)
+    c = _ctx(monkeypatch, {})
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    c2 = _ctx(monkeypatch, {"FFQ_SECTOR": "0"})
+    plan2 = capi.Plan(c2, P.n_qubits, *P.plan_arrays())
+    ham2 = capi.Hamiltonian(c2, P.n_qubits, *P.ham_arrays())
+    assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12

@@ -89,6 +89,7 @@ def test_parameter_shift_set_vs_oracle(ctx, oracle):
 
 def test_global_path_matches_smem_path_and_oracle(oracle, monkeypatch):
     # the same 12-qubit problem through the graph-of-kernels path
+    monkeypatch.setenv("FFQ_SECTOR", "0")
     monkeypatch.setenv("FFQ_SMEM_MAX_QUBITS", "0")
     gctx = capi.Context(0)
     P = problems.config_problem(2, batch=5)

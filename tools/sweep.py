@@ -12,7 +12,9 @@ import torch  # noqa: E402
 from paper_2402_17993_b200 import capi, problems  # noqa: E402
 
 B = int(os.environ.get("SWEEP_BATCH", "256"))
-P = problems.config_problem(int(os.environ.get("SWEEP_CONFIG", "3")), batch=B)
+P = problems.config_problem(int(os.environ.get("SWEEP_CONFIG", "3")), batch=max(1, min(B, 64)))
+if B > P.thetas.shape[0]:  # tile the seeded theta rows up to the batch size
+    P.thetas = np.tile(P.thetas, (-(-B // P.thetas.shape[0]), 1))[:B]
 th = torch.from_numpy(P.plan_thetas()).cuda()
 e = torch.zeros(B, dtype=torch.float64, device="cuda")
 ref = None
