@@ -709,11 +709,24 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     segs.push_back({a, b});
     a = b;
   }
+  // owner of each expectation pair: a local pair goes to the CTA holding both
+  // members; cross pairs go to whichever CTA has less work so far (balance)
+  std::vector<uint8_t> eown(ek.size());
+  {
+    int64_t load[2] = {0, 0};
+    for (size_t t = 0; t < ek.size(); ++t) {
+      const uint32_t i = (uint32_t)idx[ek[t].m], j = (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x];
+      const int oi = owner(i), oj = owner(j);
+      const int o = oi == oj ? oi : (load[0] <= load[1] ? 0 : 1);
+      eown[t] = (uint8_t)o;
+      load[o] += oi == oj ? 2 : 3;  // a cross pair costs one slow DSMEM access
+    }
+  }
   for (int r = 0; r < 2; ++r) {
     for (const auto& sg : segs) {
       std::vector<size_t> mine;
       for (size_t t = sg[0]; t < sg[1]; ++t)
-        if (owner((uint32_t)idx[ek[t].m]) == r) mine.push_back(t);
+        if (eown[t] == r) mine.push_back(t);
       if (mine.empty()) continue;
       const double fr0 = ek[mine[0]].fr, fi0 = ek[mine[0]].fi;
       bool shared = true;
