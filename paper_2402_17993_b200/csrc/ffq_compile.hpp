@@ -687,10 +687,21 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   S.gen_off.assign(1, 0);
   for (int op = 0; op < n_ops; ++op) {
     const FusedDesc& d = P.fused[P.op_idx[op]];
+    // per-step balance: local pairs stay with their CTA, cross pairs go to the lighter one
+    std::vector<uint8_t> own(gk[op].size());
+    int64_t load[2] = {0, 0};
+    for (size_t t = 0; t < gk[op].size(); ++t) {
+      const uint32_t i = (uint32_t)idx[gk[op][t].first], j = (uint32_t)idx[gk[op][t].first ^ (uint32_t)d.x];
+      const int oi = owner(i), oj = owner(j);
+      const int o = oi == oj ? oi : (load[0] <= load[1] ? 0 : 1);
+      own[t] = (uint8_t)o;
+      load[o] += oi == oj ? 2 : 3;
+    }
     for (int r = 0; r < 2; ++r) {
-      for (auto& e : gk[op]) {
+      for (size_t t = 0; t < gk[op].size(); ++t) {
+        const auto& e = gk[op][t];
         const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
-        if (owner(i) != r) continue;
+        if (own[t] != r) continue;
         S.gen_pairs.push_back(i | (j << 16));
         S.gen_flags.push_back(e.second);
       }
