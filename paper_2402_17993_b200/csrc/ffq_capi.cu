@@ -88,7 +88,6 @@ struct ffq_ctx_s {
   int tile_bits = kDefaultTileBits;              // env FFQ_TILE_BITS (0 disables tiling)
   int64_t slab_bytes = 256LL << 20;              // env FFQ_SLAB_MB: batch chunk of the graph path
   int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
-  int64_t row_pad = 0;                           // env FFQ_ROW_PAD: slab row stride = 2^n + pad (support path)
   int persist = 0;                               // env FFQ_PERSIST=1: k_eval_persistent instead of the graph path
   int sector = 1;                                // env FFQ_SECTOR=0: no support-closure cluster evaluator
   int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
@@ -224,8 +223,6 @@ int grid_for(int64_t work, int n_sm, int per_sm = 8) {
   return (int)g;
 }
 
-template <typename T>
-std::vector<T> as_vec(const T* p, size_t n) { return std::vector<T>(p, p + n); }
 
 bool use_support(ffq_ctx_t ctx, int n) { return ctx->support && n >= 6 && n <= 32; }
 
@@ -561,7 +558,7 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   const int n_ops = (int)pl->cp.op_kind.size();
   const bool sp = use_support(ctx, n);
   const int64_t items = h->n_partials(sp);
-  const int64_t rstride = (sp && pl->cp.n_string_ops() == 0) ? dim + ctx->row_pad : dim;
+  const int64_t rstride = dim;  // slab row stride (the support kernels take it explicitly)
   if (ctx->slab.n < (size_t)chunk * rstride) ctx->slab_clean = false;
   ctx->slab.alloc((size_t)chunk * rstride);
   if (sp) ctx->slab_sup.alloc((size_t)chunk * (dim >> 5));
@@ -685,7 +682,6 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
-    if (const char* e = std::getenv("FFQ_ROW_PAD")) c->row_pad = std::atoll(e);
     if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SECTOR")) c->sector = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;

@@ -64,9 +64,6 @@ struct HamDev {
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ double2 cfma(double s, double2 a, double2 acc) {
-  return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
-}
 // i^k
 __device__ __forceinline__ double2 ipow_d(int k) {
   k &= 3;
