@@ -107,4 +107,16 @@ std::vector<double> energy_batch(Device& dev, const DevicePlan& plan, const Devi
 double energy_trotter(Device& dev, const std::vector<double>& amps, const DevicePlan& plan,
                       const DeviceHamiltonian& H, uint64_t hf);
 
+/// Trotter-free UCCSD energy, amplitudes by canonical id.
+double energy_exact(Device& dev, const std::vector<double>& amps, const DevicePlan& plan,
+                    const DeviceHamiltonian& H, uint64_t hf, double tol = 1e-12);
+
+/// CAS-CI ground energy in the Krylov space of |hf>.
+struct GroundState {
+  double energy = 0.0;
+  int iterations = 0, dimension = 0;
+};
+GroundState lanczos_ground(Device& dev, const DeviceHamiltonian& H, uint64_t hf, double tol = 1e-10,
+                           int max_iter = 500);
+
 }  // namespace fragfield

@@ -150,6 +150,18 @@ int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* ter
                        const uint64_t* x, const uint64_t* z, const double* c_re, const double* c_im,
                        int* init_perm, int* final_perm, int* n_swaps, int* n_steps);
 
+/* ---- exact references -------------------------- */
+/* Ground energy of H in the Krylov space of |hf_bits> (CAS-CI in the HF
+ * particle/spin sector): Lanczos with full reorthogonalisation, converged when
+ * the lowest Ritz value moves by <= tol between iterations (lanczos_ground). */
+int ffq_lanczos_ground(ffq_ctx_t ctx, ffq_ham_t ham, uint64_t hf_bits, double tol, int max_iter,
+                       double* e0, int* iters, int* dim);
+/* Trotter-free UCCSD energy <hf| e^{-A} H e^{A} |hf>, A = sum_g theta_g A_g
+ * (energy_exact via apply_exp_antihermitian: Taylor series of sparse
+ * matrix-vector products, remainder norm <= tol, at most 200 terms). */
+int ffq_energy_exact(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
+                     const double* theta, double tol, double* e_out);
+
 /* ---- host-only diagnostics (no device needed) ----------------------------- */
 /* Compile a Hamiltonian / plan exactly as the upload calls do and report the
  * table shapes. ham stats[8]: groups, terms, classes, active patterns,

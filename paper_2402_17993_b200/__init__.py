@@ -46,8 +46,11 @@ from .lib._fragfield import (  # noqa: E402,F401
     build_generators,
     dimer_labels,
     energy_batch,
+    energy_exact,
     energy_trotter,
     evaluate_fragments,
+    GroundState,
+    lanczos_ground,
     exact_gradient_from_energies,
     fragment_cost,
     exact_gradient_set,

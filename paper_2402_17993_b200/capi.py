@@ -58,6 +58,9 @@ _SIGS = {
                                      np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
                                      np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ffq_lanczos_ground": (C.c_int, [_vp, _vp, C.c_uint64, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ffq_energy_exact": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, C.c_double, C.POINTER(C.c_double)]),
     "ffq_ham_compile_stats": (C.c_int, [C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, _i64p]),
     "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
 }
@@ -308,3 +311,19 @@ class ShardedState:
         sw = C.c_int(); perm = np.zeros(self.n, np.int32)
         check(lib().ffq_shard_info(self.h, C.byref(sw), perm))
         return sw.value, perm
+
+
+def lanczos_ground(ctx: Context, ham: Hamiltonian, hf_bits, tol=1e-10, max_iter=500):
+    """CAS-CI ground energy in the Krylov space of |hf>."""
+    e = C.c_double(); it = C.c_int(); dim = C.c_int()
+    check(lib().ffq_lanczos_ground(ctx.h, ham.h, hf_bits, tol, max_iter, C.byref(e), C.byref(it), C.byref(dim)),
+          ctx.h)
+    return e.value, it.value, dim.value
+
+
+def energy_exact(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits, theta, tol=1e-12):
+    """Trotter-free UCCSD energy; theta in plan order."""
+    e = C.c_double()
+    check(lib().ffq_energy_exact(ctx.h, plan.h, ham.h, hf_bits, np.ascontiguousarray(theta, np.float64).ravel(),
+                                 tol, C.byref(e)), ctx.h)
+    return e.value

@@ -1048,3 +1048,4 @@ int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, con
 }  // extern "C"
 
 #include "ffq_shard.inl"
+#include "ffq_krylov.inl"

@@ -771,3 +771,145 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
 }
 
 }  // namespace ffq
+
+namespace ffq {
+
+// ---- Krylov space of a Hamiltonian (lanczos_ground / energy_exact) ---------------
+// Basis = closure of |hf> under the Hamiltonian's pair maps (m <-> m ^ X on the
+// active patterns of every x-group) and, optionally, a plan's generator maps;
+// H and the generator matrix A = sum_g theta_g A_g restricted to it are kept as
+// CSR (rows = basis states, deterministic row-wise sums on the device).
+struct KrylovSpace {
+  bool ok = false;
+  std::string why;
+  std::vector<uint32_t> basis;  // ascending
+  uint32_t hf_idx = 0;
+  // H: row i, entries (col, value) with value = <basis[i]|H|basis[col]>
+  std::vector<int64_t> h_row;
+  std::vector<uint32_t> h_col;
+  std::vector<double> h_re, h_im;
+  // A_g: entries (row, col, value, generator column in theta)
+  std::vector<int64_t> a_row;
+  std::vector<uint32_t> a_col;
+  std::vector<double> a_re, a_im;
+  std::vector<int32_t> a_gen;
+};
+
+// Closure under H's maps (lanczos_ground) or under the plan's maps only
+// (energy_exact: <psi|H|psi> only needs H restricted to psi's support).
+inline KrylovSpace compile_krylov(const CompiledHam& H, const CompiledPlan* P, uint64_t hf, uint32_t max_size,
+                                  bool close_under_h) {
+  KrylovSpace K;
+  const int n = H.n_qubits;
+  if (n > 26) { K.why = "qubit count"; return K; }
+  if (P && P->n_string_ops() > 0) { K.why = "plan has non-fused generators"; return K; }
+  const size_t dim = size_t(1) << n;
+  std::vector<int32_t> pos(dim, -1);
+  std::vector<uint32_t> list{(uint32_t)hf};
+  pos[hf] = 0;
+  // breadth-first closure under all maps
+  for (size_t t = 0; t < list.size(); ++t) {
+    const uint32_t k = list[t];
+    auto add = [&](uint32_t m) {
+      if (pos[m] < 0) { pos[m] = (int32_t)list.size(); list.push_back(m); }
+    };
+    for (const auto& d : H.groups) {
+      if (d.x == 0 || !close_under_h) continue;
+      uint64_t Q = 0;
+      for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
+      for (int p = 0; p < d.nact; ++p) {
+        const uint64_t pb = H.act_bits[d.act_off + p];
+        if ((k & Q) == pb || ((k ^ d.x) & Q) == pb) add(k ^ (uint32_t)d.x);
+      }
+    }
+    if (P)
+      for (const auto& d : P->fused)
+        for (int p = 0; p < d.npair; ++p) {
+          const uint64_t lo = P->pair_bits[d.pair_off + p];
+          const uint64_t pat = k & d.x;
+          if (pat == lo || pat == (lo ^ d.x)) add(k ^ (uint32_t)d.x);
+        }
+    if (list.size() > max_size) { K.why = "Krylov space too large"; return K; }
+  }
+  std::sort(list.begin(), list.end());
+  for (size_t i = 0; i < list.size(); ++i) pos[list[i]] = (int32_t)i;
+  K.basis = list;
+  K.hf_idx = (uint32_t)pos[hf];
+  // H entries: for pair (m, m^X) with pattern p (lower member m), <m^X|H|m> = f/2
+  // (off-diagonal, f carries the pair weight 2) and its conjugate transpose
+  std::vector<std::vector<std::tuple<uint32_t, double, double>>> rows(list.size());
+  for (const auto& d : H.groups) {
+    uint64_t Q = 0;
+    for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
+    for (int p = 0; p < d.nact; ++p) {
+      const uint64_t pb = H.act_bits[d.act_off + p];
+      for (uint32_t i = 0; i < list.size(); ++i) {
+        const uint32_t m = list[i];
+        if ((m & Q) != pb) continue;
+        const int32_t j = pos[m ^ (uint32_t)d.x];
+        if (j < 0) continue;
+        double fr = 0.0, fi = 0.0;
+        for (int o = 0; o < d.ncls; ++o) {
+          const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
+          fr += sg * H.cls_f[2 * (d.val_off + o * d.nact + p)];
+          fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
+        }
+        if (d.x == 0) {
+          rows[i].emplace_back(i, fr, fi);
+        } else {
+          // <m^X|H|m> = b(m) = f/2; <m|H|m^X> = conj(b(m))
+          rows[j].emplace_back(i, 0.5 * fr, 0.5 * fi);
+          rows[i].emplace_back((uint32_t)j, 0.5 * fr, -0.5 * fi);
+        }
+      }
+    }
+  }
+  K.h_row.push_back(0);
+  for (auto& r : rows) {
+    std::sort(r.begin(), r.end(), [](const auto& a, const auto& b) { return std::get<0>(a) < std::get<0>(b); });
+    for (auto& e : r) {
+      K.h_col.push_back(std::get<0>(e));
+      K.h_re.push_back(std::get<1>(e));
+      K.h_im.push_back(std::get<2>(e));
+    }
+    K.h_row.push_back((int64_t)K.h_col.size());
+  }
+  // A_g entries: <k^X|A_g|k> = s_out(k) F[pattern(k)], k on either pattern of a pair
+  if (P) {
+    std::vector<std::vector<std::tuple<uint32_t, double, double, int32_t>>> arows(list.size());
+    for (size_t op = 0; op < P->op_kind.size(); ++op) {
+      const FusedDesc& d = P->fused[P->op_idx[op]];
+      for (int p = 0; p < d.npair; ++p) {
+        const uint64_t lo = P->pair_bits[d.pair_off + p];
+        const double flr = P->pair_f[4 * (d.pair_off + p)], fli = P->pair_f[4 * (d.pair_off + p) + 1];
+        const double fhr = P->pair_f[4 * (d.pair_off + p) + 2], fhi = P->pair_f[4 * (d.pair_off + p) + 3];
+        for (uint32_t i = 0; i < list.size(); ++i) {
+          const uint32_t k = list[i];
+          const uint64_t pat = k & d.x;
+          if (pat != lo && pat != (lo ^ d.x)) continue;
+          const int32_t j = pos[k ^ (uint32_t)d.x];
+          if (j < 0) continue;
+          const double sg = (__builtin_popcountll(k & d.zout) & 1) ? -1.0 : 1.0;
+          const bool low = pat == lo;
+          // A_g |k> = a(k) |k^X>, a(k) = s_out(k) F[pattern(k)] (compile_plan's F table)
+          const double ar = sg * (low ? flr : fhr), ai = sg * (low ? fli : fhi);
+          arows[j].emplace_back(i, ar, ai, P->op_gen[op]);
+        }
+      }
+    }
+    K.a_row.push_back(0);
+    for (auto& r : arows) {
+      for (auto& e : r) {
+        K.a_col.push_back(std::get<0>(e));
+        K.a_re.push_back(std::get<1>(e));
+        K.a_im.push_back(std::get<2>(e));
+        K.a_gen.push_back(std::get<3>(e));
+      }
+      K.a_row.push_back((int64_t)K.a_col.size());
+    }
+  }
+  K.ok = true;
+  return K;
+}
+
+}  // namespace ffq

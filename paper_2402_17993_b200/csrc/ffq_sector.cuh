@@ -192,3 +192,38 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
 }
 
 }  // namespace ffq
+
+namespace ffq {
+
+// ---- sparse row-wise matvec on a Krylov basis (lanczos_ground, energy_exact) ----
+// y[r] = sum_e val[e] * (gen ? theta[gen[e]] : 1) * x[col[e]]; one warp per row,
+// lanes stride the row, fixed shuffle tree (deterministic).
+__global__ void k_csr_matvec(int64_t rows, const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                             const double* __restrict__ vre, const double* __restrict__ vim,
+                             const int32_t* __restrict__ gen, const double* __restrict__ theta,
+                             const double2* __restrict__ x, double2* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+      double ar = vre[e], ai = vim[e];
+      if (gen) {
+        const double t = theta[gen[e]];
+        ar *= t;
+        ai *= t;
+      }
+      const double2 v = x[col[e]];
+      acc.x = fma(ar, v.x, fma(-ai, v.y, acc.x));
+      acc.y = fma(ar, v.y, fma(ai, v.x, acc.y));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) y[r] = acc;
+  }
+}
+
+}  // namespace ffq

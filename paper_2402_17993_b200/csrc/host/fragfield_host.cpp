@@ -476,6 +476,22 @@ double energy_trotter(Device& dev, const std::vector<double>& amps, const Device
   return energy_batch(dev, plan, H, hf, plan.plan().plan_theta(amps), 1)[0];
 }
 
+double energy_exact(Device& dev, const std::vector<double>& amps, const DevicePlan& plan,
+                    const DeviceHamiltonian& H, uint64_t hf, double tol) {
+  const std::vector<double> th = plan.plan().plan_theta(amps);
+  double e = 0.0;
+  check_ffq(ffq_energy_exact(dev.handle(), plan.handle(), H.handle(), hf, th.data(), tol, &e), dev.handle());
+  return e;
+}
+
+GroundState lanczos_ground(Device& dev, const DeviceHamiltonian& H, uint64_t hf, double tol, int max_iter) {
+  GroundState g;
+  check_ffq(ffq_lanczos_ground(dev.handle(), H.handle(), hf, tol, max_iter, &g.energy, &g.iterations,
+                               &g.dimension),
+            dev.handle());
+  return g;
+}
+
 // ---- optimizers ------------------------------------------------------------------
 namespace {
 

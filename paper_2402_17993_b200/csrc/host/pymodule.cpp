@@ -193,6 +193,14 @@ PYBIND11_MODULE(_fragfield, m) {
       },
       py::arg("device"), py::arg("plan"), py::arg("hamiltonian"), py::arg("hf_bits"), py::arg("theta"));
   m.def("energy_trotter", &energy_trotter);
+  m.def("energy_exact", &energy_exact, py::arg("device"), py::arg("amplitudes"), py::arg("plan"),
+        py::arg("hamiltonian"), py::arg("hf_bits"), py::arg("tol") = 1e-12);
+  py::class_<GroundState>(m, "GroundState")
+      .def_readonly("energy", &GroundState::energy)
+      .def_readonly("iterations", &GroundState::iterations)
+      .def_readonly("dimension", &GroundState::dimension);
+  m.def("lanczos_ground", &lanczos_ground, py::arg("device"), py::arg("hamiltonian"), py::arg("hf_bits"),
+        py::arg("tol") = 1e-10, py::arg("max_iter") = 500);
 
   // ---- vqe ----
   py::class_<OptimizerOptions>(m, "OptimizerOptions")
