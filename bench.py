@@ -311,6 +311,22 @@ def main():
                "evals_per_s": rows2.shape[0] / (statistics.mean(ms2) / 1e3),
                "path": "k_sector_eval<1,256> (one CTA per evaluation, support closure of 400 amplitudes)"}
 
+    # secondary: BASELINE.json config 4 -- FMO batch of 3 monomers (12 q) + 3 dimers
+    # (18 q), one evaluation each through the C++ fragment API, assembled with the
+    # reference's two-body formula; plan/Hamiltonian uploads and closure compiles are
+    # timed separately from the evaluations (first call vs second call)
+    import paper_2402_17993_b200 as _ff
+
+    frags = _pb.fmo_fragment_problems()
+    dev = _ff.Device(local)
+    t_first = time.perf_counter()
+    en = _ff.evaluate_fragments(dev, frags, 0, 1)
+    t_first = time.perf_counter() - t_first
+    config4 = {"fragments": len(frags), "e_fmo2": _ff.assemble_fragments(3, en),
+               "first_call_s_incl_compile": t_first,
+               "note": "per-fragment evaluation, sharded by cost over ranks with --gpus N"}
+    del dev
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = 2
@@ -343,7 +359,8 @@ def main():
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
             "gpu_launches": int(launches),
-            "secondary": {"config3_dense_slab_path": dense_path, "config2_12q": config2},
+            "secondary": {"config3_dense_slab_path": dense_path, "config2_12q": config2,
+                          "config4_fmo": config4},
             "clocks": clk.summary(),
         }
         if cpu:
