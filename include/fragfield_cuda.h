@@ -149,6 +149,12 @@ int ffq_shard_info(ffq_shard_t sh, int* last_swaps, int* perm);
 int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* term_off,
                        const uint64_t* x, const uint64_t* z, const double* c_re, const double* c_im,
                        int* init_perm, int* final_perm, int* n_swaps, int* n_steps);
+/* Same, plus the step list steps[4 * i] = {kind (0 swap, 1 apply), physical
+ * global position, local position, generator column} for i < n_steps. */
+int ffq_shard_schedule_steps(int n_qubits, int n_global, int n_gen, const int64_t* term_off,
+                             const uint64_t* x, const uint64_t* z, const double* c_re,
+                             const double* c_im, int* init_perm, int* final_perm, int* n_swaps,
+                             int* n_steps, int* steps, int max_steps);
 
 /* ---- exact references -------------------------- */
 /* Ground energy of H in the Krylov space of |hf_bits> (CAS-CI in the HF

@@ -58,6 +58,11 @@ _SIGS = {
                                      np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
                                      np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ffq_shard_schedule_steps": (C.c_int, [C.c_int, C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p,
+                                           np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                           np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                           C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                           np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), C.c_int]),
     "ffq_lanczos_ground": (C.c_int, [_vp, _vp, C.c_uint64, C.c_double, C.c_int, C.POINTER(C.c_double),
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ffq_energy_exact": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, C.c_double, C.POINTER(C.c_double)]),
@@ -266,6 +271,19 @@ def shard_schedule(n, n_global, off, x, z, c):
     ns = C.c_int(); st = C.c_int()
     check(lib().ffq_shard_schedule(n, n_global, len(off) - 1, off, x, z, re_, im, ip, fp, C.byref(ns), C.byref(st)))
     return ip, fp, ns.value, st.value
+
+
+def shard_schedule_steps(n, n_global, off, x, z, c):
+    """(init_perm, final_perm, steps[n_steps][4]) with steps = (kind, gpos, lpos, generator column)."""
+    x, z, re_, im = _terms(x, z, c)
+    off = np.ascontiguousarray(off, np.int64)
+    ip = np.zeros(n, np.int32); fp = np.zeros(n, np.int32)
+    ns = C.c_int(); st = C.c_int()
+    cap = 4 * (len(off) - 1) + 64 * n
+    steps = np.zeros(4 * cap, np.int32)
+    check(lib().ffq_shard_schedule_steps(n, n_global, len(off) - 1, off, x, z, re_, im, ip, fp, C.byref(ns),
+                                         C.byref(st), steps, cap))
+    return ip, fp, steps[: 4 * st.value].reshape(-1, 4)
 
 
 def nccl_unique_id() -> bytes:

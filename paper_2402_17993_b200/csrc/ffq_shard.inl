@@ -406,6 +406,13 @@ int ffq_shard_info(ffq_shard_t sh, int* last_swaps, int* perm_out) {
 int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* term_off, const uint64_t* x,
                        const uint64_t* z, const double* c_re, const double* c_im, int* init_perm,
                        int* final_perm, int* n_swaps, int* n_steps) {
+  return ffq_shard_schedule_steps(n_qubits, n_global, n_gen, term_off, x, z, c_re, c_im, init_perm, final_perm,
+                                  n_swaps, n_steps, nullptr, 0);
+}
+
+int ffq_shard_schedule_steps(int n_qubits, int n_global, int n_gen, const int64_t* term_off, const uint64_t* x,
+                             const uint64_t* z, const double* c_re, const double* c_im, int* init_perm,
+                             int* final_perm, int* n_swaps, int* n_steps, int* steps, int max_steps) {
   return guarded(nullptr, [&] {
     const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, x, z, c_re, c_im);
     const ShardSchedule S = schedule_shards(P, n_global);
@@ -415,6 +422,16 @@ int ffq_shard_schedule(int n_qubits, int n_global, int n_gen, const int64_t* ter
     }
     if (n_swaps) *n_swaps = S.n_swaps();
     if (n_steps) *n_steps = (int)S.steps.size();
+    if (steps) {
+      if ((int)S.steps.size() > max_steps) throw BadInput("ffq_shard_schedule_steps: steps buffer too small", FFQ_EINVAL);
+      for (size_t i = 0; i < S.steps.size(); ++i) {
+        // kind, gpos, lpos, generator index (plan column) of the op
+        steps[4 * i] = S.steps[i].kind;
+        steps[4 * i + 1] = S.steps[i].gpos;
+        steps[4 * i + 2] = S.steps[i].lpos;
+        steps[4 * i + 3] = S.steps[i].kind ? P.op_gen[S.steps[i].op] : -1;
+      }
+    }
     return FFQ_OK;
   });
 }
