@@ -374,25 +374,36 @@ bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
 }
 
 constexpr int kSectorThreads = 1024;
-// small closures run one CTA per evaluation (many per SM); large ones a 2-CTA cluster
+// small closures run one CTA per evaluation (many per SM); large ones a 2^s-CTA cluster
 constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA
-constexpr uint32_t kSectorMaxSize = 32768;  // 2 CTAs x 16384 amplitudes (256 KiB) in DSMEM
+constexpr uint32_t kSectorMaxSize = 32767;   // 15-bit pair indices
+
+// cluster size for a closure of `size` amplitudes: 1 when it fits a small CTA,
+// else env FFQ_SECTOR_CL (2, 4 or 8), default 2 (throughput-optimal at 18 qubits)
+int sector_parts(uint32_t size) {
+  if (size <= kSectorSingleMax) return 1;
+  static const int env_cl = [] {
+    const char* e = std::getenv("FFQ_SECTOR_CL");
+    const int v = e ? std::atoi(e) : 2;
+    return (v == 4 || v == 8) ? v : 2;
+  }();
+  return env_cl;
+}
 
 // compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
-// nullptr when the closure does not fit a 2-CTA cluster (then other paths run)
+// nullptr when the closure does not fit the cluster (then other paths run)
 const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
   auto key = std::make_pair((const void*)h, hf);
   auto it = pl->sectors.find(key);
   if (it == pl->sectors.end()) {
     auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
     const size_t tables = 3 * pl->cp.op_kind.size() * sizeof(double2) + pl->cp.op_kind.size() + 16;
-    const uint32_t max_half =
+    const uint32_t max_part =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
-    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_half);
-    if (b->prog.ok && b->prog.size <= kSectorSingleMax) {
-      // one CTA holds all of S: every pair is local, rank 0 owns everything
-      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, /*single=*/true);
-    }
+    // closure size first (one part, no size limit on the part), then the real split
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1);
+    if (b->prog.ok && sector_parts(b->prog.size) > 1)
+      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(b->prog.size));
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
@@ -411,13 +422,13 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   auto& b = *it->second;
   if (!b.prog.ok) return nullptr;
   static thread_local SectorDev sd;
+  sd = SectorDev{};
   sd.size = b.prog.size;
-  sd.half = b.prog.split;
-  for (int r = 0; r < 3; ++r) {
-    sd.exp_off[r] = b.prog.exp_off[r];
+  for (int r = 0; r <= b.prog.n_parts; ++r) {
+    sd.part_start[r] = b.prog.part_start[r];
     sd.seg_off[r] = b.prog.seg_off[r];
   }
-  sd.split_bit = b.prog.split_bit;
+  sd.split_mask = b.prog.split_mask;
   sd.seg_start = b.seg_start.p;
   sd.seg_foff = b.seg_foff.p;
   sd.seg_fre = b.seg_fre.p;
@@ -427,18 +438,18 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.gen_off = b.gen_off.p;
   sd.gen_pairs = b.gen_pairs.p;
   sd.gen_flags = b.gen_flags.p;
-  sd.n_exp = (int64_t)b.prog.exp_pairs.size();
   sd.exp_pairs = b.exp_pairs.p;
   sd.exp_fre = b.exp_fre.p;
   sd.exp_fim = b.prog.f_real ? nullptr : b.exp_fim.p;
+  sd.n_parts = b.prog.n_parts;
   return &sd;
 }
-
 
 template <int CL, int NT>
 void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
                      double* e, double* im, long long* clk) {
-  const size_t hmax = CL == 1 ? sd.size : std::max<size_t>(sd.half, sd.size - sd.half);
+  size_t hmax = 0;
+  for (int r = 0; r < CL; ++r) hmax = std::max<size_t>(hmax, sd.part_start[r + 1] - sd.part_start[r]);
   const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2) + pl->cp.op_kind.size() + 16;
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   if (CL > 1) CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -463,10 +474,13 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
   static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
   DevBuf<long long> clk;
   if (clocks) clk.alloc(2 * (size_t)batch);
-  if (sd.size <= kSectorSingleMax)
-    launch_sector_t<1, 256>(ctx, pl, sd, theta, batch, e, im, clocks ? clk.p : nullptr);
-  else
-    launch_sector_t<2, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, clocks ? clk.p : nullptr);
+  long long* cp = clocks ? clk.p : nullptr;
+  switch (sd.n_parts) {
+    case 1: launch_sector_t<1, 256>(ctx, pl, sd, theta, batch, e, im, cp); break;
+    case 2: launch_sector_t<2, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
+    case 4: launch_sector_t<4, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
+    default: launch_sector_t<8, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
+  }
   if (clocks) {
     std::vector<long long> hc(2 * (size_t)batch);
     CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));

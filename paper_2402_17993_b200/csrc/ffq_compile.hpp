@@ -566,10 +566,14 @@ struct SectorProgram {
   std::string why;  // reason when !ok
   int n = 0;
   uint32_t size = 0, hf_idx = 0;
-  int split_bit = -1;               // S ordered by (bit split_bit of k, k): CTA 0 holds bit = 0
-  uint32_t split = 0;               // |{k in S : bit = 0}|
-  std::vector<uint32_t> basis;      // S in (split bit, k) order
-  std::vector<int64_t> gen_off;     // [2 * n_ops + 1]: op g, owner rank r -> gen_off[2g + r]
+  // S is split over n_parts = 2^s CTAs by the values of the s qubits in
+  // split_mask (chosen to minimise pairs that cross CTAs); part r holds
+  // S[part_start[r], part_start[r + 1]), ordered by (part, k)
+  int n_parts = 1;
+  uint64_t split_mask = 0;
+  std::vector<uint32_t> part_start;  // [n_parts + 1]
+  std::vector<uint32_t> basis;
+  std::vector<int64_t> gen_off;     // [n_ops * n_parts + 1]: op g, owner rank r -> gen_off[g * n_parts + r]
   std::vector<uint32_t> gen_pairs;  // i | j << 16 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
   // expectation pairs, i | j << 15 | sign << 30 (i: enumerated m, j: m ^ X),
@@ -580,20 +584,19 @@ struct SectorProgram {
   std::vector<double> exp_fre, exp_fim;  // per-pair f of per-pair segments (exp_fim empty if all real)
   std::vector<int64_t> seg_start, seg_foff;  // seg_foff < 0: shared-f segment
   std::vector<double> seg_fre, seg_fim;
-  int32_t seg_off[3] = {0, 0, 0};   // segments of rank 0, rank 1
-  int64_t exp_off[3] = {0, 0, 0};   // pairs owned (by i) by rank 0, rank 1
+  std::vector<int32_t> seg_off;     // [n_parts + 1] segments per rank
   bool f_real = true;
   int64_t cross_pairs = 0;          // pairs whose members live in different CTAs
 };
 
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
-                                    uint32_t max_size, uint32_t max_half = 0xFFFFFFFFu,
-                                    bool single = false) {
+                                    uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2) {
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
   if (n > 26 || H.n_qubits != n) { S.why = "qubit count"; return S; }
   if (P.n_string_ops() > 0) { S.why = "plan has non-fused generators"; return S; }
+  if (n_parts != 1 && n_parts != 2 && n_parts != 4 && n_parts != 8) { S.why = "parts must be 1, 2, 4 or 8"; return S; }
   const size_t dim = size_t(1) << n;
   std::vector<int32_t> idx(dim, -1);
   std::vector<uint32_t> list{(uint32_t)hf};
@@ -626,8 +629,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       if (list.size() > max_size) { S.why = "support closure too large"; return S; }
     }
   }
-  // expectation pairs in k space (m, X index) with f(m)
-  std::vector<int32_t>& inS = pos;  // pos[k] >= 0 <=> k in S
+  // expectation pairs in k space with their class sums f(m)
   struct EP { uint32_t m; int g, p; double fr, fi; };
   std::vector<EP> ek;
   for (size_t gi = 0; gi < H.groups.size(); ++gi) {
@@ -638,7 +640,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       const uint64_t pb = H.act_bits[d.act_off + p];
       for (uint32_t m : list) {
         if ((m & Q) != pb) continue;
-        if (inS[m ^ (uint32_t)d.x] < 0) continue;
+        if (pos[m ^ (uint32_t)d.x] < 0) continue;
         double fr = 0.0, fi = 0.0;
         for (int o = 0; o < d.ncls; ++o) {
           const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
@@ -650,93 +652,111 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       }
     }
   }
-  // split bit: fewest pairs crossing the two CTAs, both halves within max_half
   S.size = (uint32_t)list.size();
-  int best = -1;
-  int64_t best_cross = -1;
-  for (int b = 0; b < n && !single; ++b) {
-    uint32_t zero = 0;
-    for (uint32_t k : list) zero += !((k >> b) & 1u);
-    if (zero > max_half || S.size - zero > max_half) continue;
-    int64_t cross = 0;
-    for (int op = 0; op < n_ops; ++op)
-      if ((P.fused[P.op_idx[op]].x >> b) & 1ULL) cross += (int64_t)gk[op].size();
-    for (const auto& e : ek)
-      if ((H.groups[e.g].x >> b) & 1ULL) ++cross;
-    if (best < 0 || cross < best_cross) { best = b; best_cross = cross; }
+  if (S.size > 32767) { S.why = "support closure exceeds 15-bit indices"; return S; }
+  // split qubits, greedily: each added bit minimises the pairs whose flip mask
+  // touches the split, with every part within max_part amplitudes
+  auto part_of = [&](uint32_t k, uint64_t mask) {
+    uint32_t r = 0, b = 0;
+    for (int q = 0; q < n; ++q)
+      if ((mask >> q) & 1ULL) r |= ((k >> q) & 1u) << b++;
+    return r;
+  };
+  uint64_t mask = 0;
+  int64_t cross = 0;
+  for (int s = 0; (1 << s) < n_parts; ++s) {
+    int best = -1;
+    int64_t best_cross = -1;
+    for (int b = 0; b < n; ++b) {
+      if ((mask >> b) & 1ULL) continue;
+      const uint64_t m2 = mask | (1ULL << b);
+      std::vector<uint32_t> cnt(size_t(1) << (s + 1), 0);
+      for (uint32_t k : list) ++cnt[part_of(k, m2)];
+      bool fits = true;
+      if (s + 1 == __builtin_ctz(n_parts))  // final level: every part non-empty and within a CTA
+        for (uint32_t c : cnt) fits &= c > 0 && c <= max_part;
+      if (!fits) continue;
+      int64_t cr = 0;
+      for (int op = 0; op < n_ops; ++op)
+        if (P.fused[P.op_idx[op]].x & m2) cr += (int64_t)gk[op].size();
+      for (const auto& e : ek)
+        if (H.groups[e.g].x & m2) ++cr;
+      if (best < 0 || cr < best_cross) { best = b; best_cross = cr; }
+    }
+    if (best < 0) { S.why = "no split of the support closure fits the CTAs"; return S; }
+    mask |= 1ULL << best;
+    cross = best_cross;
   }
-  if (single) {
-    // one CTA: no split; bit 63 is never set, so split_bit flips nothing
-    best = 63;
-    best_cross = 0;
-  }
-  if (best < 0) { S.why = "no qubit splits the support closure into two halves that fit"; return S; }
-  S.split_bit = best;
-  S.cross_pairs = best_cross;
+  if (n_parts == 1 && S.size > max_part) { S.why = "support closure does not fit one CTA"; return S; }
+  S.n_parts = n_parts;
+  S.split_mask = mask;
+  S.cross_pairs = cross;
   std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t c) {
-    const uint32_t ba = best < 32 ? (a >> best) & 1u : 0u, bc = best < 32 ? (c >> best) & 1u : 0u;
-    return ba != bc ? ba < bc : a < c;
+    const uint32_t pa = part_of(a, mask), pc = part_of(c, mask);
+    return pa != pc ? pa < pc : a < c;
   });
   S.basis = list;
-  if (S.size > 65535) { S.why = "support closure exceeds 16-bit indices"; return S; }
-  S.split = 0;
-  for (uint32_t k : list) S.split += best < 32 ? !((k >> best) & 1u) : 1u;
+  S.part_start.assign((size_t)n_parts + 1, 0);
+  for (uint32_t k : list) ++S.part_start[part_of(k, mask) + 1];
+  for (int r = 0; r < n_parts; ++r) S.part_start[r + 1] += S.part_start[r];
   for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
   S.hf_idx = (uint32_t)idx[hf];
-  auto owner = [&](uint32_t i) { return i < S.split ? 0 : 1; };
+  auto owner = [&](uint32_t i) {
+    int r = 0;
+    while (i >= S.part_start[r + 1]) ++r;
+    return r;
+  };
+  // a local pair stays with its CTA; a cross pair goes to the lighter of its two CTAs
+  auto assign = [&](uint32_t i, uint32_t j, std::vector<int64_t>& load) {
+    const int oi = owner(i), oj = owner(j);
+    const int o = oi == oj ? oi : (load[oi] <= load[oj] ? oi : oj);
+    load[o] += oi == oj ? 2 : 3;  // a cross pair costs one slow DSMEM access
+    return o;
+  };
   S.gen_off.assign(1, 0);
   for (int op = 0; op < n_ops; ++op) {
     const FusedDesc& d = P.fused[P.op_idx[op]];
-    // per-step balance: local pairs stay with their CTA, cross pairs go to the lighter one
     std::vector<uint8_t> own(gk[op].size());
-    int64_t load[2] = {0, 0};
+    std::vector<int64_t> load((size_t)n_parts, 0);
     for (size_t t = 0; t < gk[op].size(); ++t) {
       const uint32_t i = (uint32_t)idx[gk[op][t].first], j = (uint32_t)idx[gk[op][t].first ^ (uint32_t)d.x];
-      const int oi = owner(i), oj = owner(j);
-      const int o = oi == oj ? oi : (load[0] <= load[1] ? 0 : 1);
-      own[t] = (uint8_t)o;
-      load[o] += oi == oj ? 2 : 3;
+      own[t] = (uint8_t)assign(i, j, load);
     }
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < n_parts; ++r) {
       for (size_t t = 0; t < gk[op].size(); ++t) {
+        if (own[t] != r) continue;
         const auto& e = gk[op][t];
         const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
-        if (own[t] != r) continue;
         S.gen_pairs.push_back(i | (j << 16));
         S.gen_flags.push_back(e.second);
       }
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
     }
   }
-  if (S.size > 32767) { S.why = "support closure exceeds 15-bit indices"; return S; }
   for (const auto& e : ek)
     if (e.fi != 0.0) S.f_real = false;
-  // ek is ordered by (group, pattern): cut it into segments per owner rank
+  // ek is ordered by (group, pattern): segments of one (group, pattern) per owner
   size_t a = 0;
-  std::vector<std::vector<size_t>> segs;  // boundaries of (group, pattern) runs
+  std::vector<std::pair<size_t, size_t>> segs;
   while (a < ek.size()) {
     size_t b = a + 1;
     while (b < ek.size() && ek[b].g == ek[a].g && ek[b].p == ek[a].p) ++b;
     segs.push_back({a, b});
     a = b;
   }
-  // owner of each expectation pair: a local pair goes to the CTA holding both
-  // members; cross pairs go to whichever CTA has less work so far (balance)
   std::vector<uint8_t> eown(ek.size());
   {
-    int64_t load[2] = {0, 0};
+    std::vector<int64_t> load((size_t)n_parts, 0);
     for (size_t t = 0; t < ek.size(); ++t) {
       const uint32_t i = (uint32_t)idx[ek[t].m], j = (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x];
-      const int oi = owner(i), oj = owner(j);
-      const int o = oi == oj ? oi : (load[0] <= load[1] ? 0 : 1);
-      eown[t] = (uint8_t)o;
-      load[o] += oi == oj ? 2 : 3;  // a cross pair costs one slow DSMEM access
+      eown[t] = (uint8_t)assign(i, j, load);
     }
   }
-  for (int r = 0; r < 2; ++r) {
+  S.seg_off.assign(1, 0);
+  for (int r = 0; r < n_parts; ++r) {
     for (const auto& sg : segs) {
       std::vector<size_t> mine;
-      for (size_t t = sg[0]; t < sg[1]; ++t)
+      for (size_t t = sg.first; t < sg.second; ++t)
         if (eown[t] == r) mine.push_back(t);
       if (mine.empty()) continue;
       const double fr0 = ek[mine[0]].fr, fi0 = ek[mine[0]].fi;
@@ -761,8 +781,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         }
       }
     }
-    S.seg_off[r + 1] = (int32_t)S.seg_start.size();
-    S.exp_off[r + 1] = (int64_t)S.exp_pairs.size();
+    S.seg_off.push_back((int32_t)S.seg_start.size());
   }
   S.seg_start.push_back((int64_t)S.exp_pairs.size());  // sentinel
   if (S.f_real) S.exp_fim.clear();

@@ -22,20 +22,21 @@ namespace ffq {
 
 namespace cg = cooperative_groups;
 
+constexpr int kSectorMaxParts = 8;
+
 struct SectorDev {
-  uint32_t size, half, hf_idx;  // half = split: CTA 0 holds S[0, half), CTA 1 holds S[half, size)
-  int n_ops;
-  int split_bit;                // generators flipping it need a cluster barrier
-  int64_t exp_off[3];
-  int32_t seg_off[3];
+  uint32_t size, hf_idx;
+  uint32_t part_start[kSectorMaxParts + 1];  // CTA r holds S[part_start[r], part_start[r + 1])
+  int n_ops, n_parts;
+  uint64_t split_mask;          // generators flipping any of these qubits need a cluster barrier
+  int32_t seg_off[kSectorMaxParts + 1];
   const int64_t* seg_start;     // [n_seg + 1]
   const int64_t* seg_foff;      // < 0: shared |f| (seg_fre/fim), else per-pair f offset
   const double* seg_fre;
   const double* seg_fim;
-  const int64_t* gen_off;       // [2 * n_ops + 1], per op and owner rank
+  const int64_t* gen_off;       // [CL * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;
   const uint8_t* gen_flags;
-  int64_t n_exp;
   const uint32_t* exp_pairs;
   const double* exp_fre;
   const double* exp_fim;  // nullptr when every f is real
@@ -55,19 +56,29 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   const int rank = (int)cluster.block_rank();
   const int row = blockIdx.x / CL;
   if (row >= n_rows) return;  // whole clusters exit together (grid = n_rows * CL)
-  const uint32_t H = sd.half;
-  const uint32_t Hmax = CL == 1 ? sd.size : max(H, sd.size - H);  // CL == 1: H == size
+  uint32_t pstart[CL + 1];
+  uint32_t Hmax = 0;
+#pragma unroll
+  for (int r = 0; r <= CL; ++r) pstart[r] = sd.part_start[r];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) Hmax = max(Hmax, pstart[r + 1] - pstart[r]);
   double2* cs = sm_c + Hmax;
   double2* fz = cs + pl.n_ops;  // [2 * n_ops]
   uint8_t* crossf = reinterpret_cast<uint8_t*>(fz + 2 * pl.n_ops);  // [n_ops]
-  // base pointers of both halves: this CTA's half through the plain shared
-  // window (LDS/STS), the peer's through the distributed-shared window
+  // base pointers of the parts: this CTA's part through the plain shared
+  // window (LDS/STS), the peers' through the distributed-shared window
   double2* part[CL];
 #pragma unroll
   for (int r = 0; r < CL; ++r) part[r] = (r == rank) ? sm_c : cluster.map_shared_rank(sm_c, r);
+  // unrolled select chain (no dynamic index into part[]: it stays in registers)
   auto at = [&](uint32_t i) -> double2* {
     if (CL == 1) return sm_c + i;
-    return i < H ? part[0] + i : part[1] + (i - H);
+    double2* p = part[0];
+    uint32_t base = 0;
+#pragma unroll
+    for (int q = 1; q < CL; ++q)
+      if (i >= pstart[q]) { p = part[q]; base = pstart[q]; }
+    return p + (i - base);
   };
   for (uint32_t i = threadIdx.x; i < Hmax; i += NT) sm_c[i] = make_double2(0.0, 0.0);
   for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
@@ -78,15 +89,16 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     const FusedDesc& d = pl.fused[pl.op_idx[op]];
     fz[2 * op] = pl.pair_f[2 * d.pair_off];
     fz[2 * op + 1] = pl.pair_f[2 * d.pair_off + 1];
-    crossf[op] = (uint8_t)((d.x >> sd.split_bit) & 1ULL);
+    crossf[op] = (uint8_t)((d.x & sd.split_mask) != 0);
   }
   cluster.sync();
-  if (threadIdx.x == 0 && (CL == 1 || (int)(sd.hf_idx >= H) == rank)) *at(sd.hf_idx) = make_double2(1.0, 0.0);
+  if (threadIdx.x == 0 && sd.hf_idx >= pstart[rank] && sd.hf_idx < pstart[rank + 1])
+    *at(sd.hf_idx) = make_double2(1.0, 0.0);
   cluster.sync();
   // each CTA processes the pairs whose first member it owns (mostly local:
   // S is split on the qubit the fewest flip masks touch)
   const int tid = threadIdx.x;
-  int64_t nx0 = sd.gen_off[rank] + tid, nx1 = sd.gen_off[rank + 1];
+  int64_t nx0 = sd.gen_off[rank] + tid, nx1 = sd.gen_off[rank + 1];  // op 0
   uint32_t nij = nx0 < nx1 ? sd.gen_pairs[nx0] : 0u;
   uint8_t nfl = nx0 < nx1 ? sd.gen_flags[nx0] : (uint8_t)0;
   for (int op = 0; op < sd.n_ops; ++op) {
@@ -96,8 +108,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     uint32_t ij = nij;
     uint8_t fl = nfl;
     if (op + 1 < sd.n_ops) {
-      nx0 = sd.gen_off[2 * (op + 1) + rank] + tid;
-      nx1 = sd.gen_off[2 * (op + 1) + rank + 1];
+      nx0 = sd.gen_off[CL * (op + 1) + rank] + tid;
+      nx1 = sd.gen_off[CL * (op + 1) + rank + 1];
       nij = nx0 < nx1 ? __ldg(sd.gen_pairs + nx0) : 0u;
       nfl = nx0 < nx1 ? __ldg(sd.gen_flags + nx0) : (uint8_t)0;
     }
@@ -123,8 +135,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
       *pa = make_double2(c * a.x + g * hb.x, c * a.y + g * hb.y);
       *pb = make_double2(c * bb.x + g * la.x, c * bb.y + g * la.y);
     }
-    // a generator whose flip mask avoids the split bit only touches this CTA's
-    // half: a CTA barrier suffices unless it or the next one crosses the split
+    // a generator whose flip mask avoids the split qubits only touches this
+    // CTA's part: a CTA barrier suffices unless it or the next one crosses
     const bool cross = crossf[op] != 0;
     const bool next_cross = op + 1 < sd.n_ops && crossf[op + 1] != 0;
     if (CL > 1 && (cross || next_cross)) cluster.sync(); else __syncthreads();

@@ -144,3 +144,22 @@ def test_sector_single_cta_small_closure(monkeypatch, oracle):
     plan2 = capi.Plan(c2, P.n_qubits, *P.plan_arrays())
     ham2 = capi.Hamiltonian(c2, P.n_qubits, *P.ham_arrays())
     assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
+
+
+@pytest.mark.parametrize("cl", ["4", "8"])
+def test_sector_cluster_sizes_agree(monkeypatch, cl):
+    P = problems.config_problem(3, batch=3)
+    c2 = _ctx(monkeypatch, {})
+    plan, ham = capi.Plan(c2, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c2, P.n_qubits, *P.ham_arrays())
+    e2 = capi.energy_batch(c2, plan, ham, P.hf, P.plan_thetas())
+    import subprocess
+    import sys
+    # FFQ_SECTOR_CL is read once per process: evaluate in a child process
+    code = ("import numpy as np;from paper_2402_17993_b200 import capi, problems;"
+            "P=problems.config_problem(3,batch=3);c=capi.Context(0);"
+            "pl=capi.Plan(c,P.n_qubits,*P.plan_arrays());h=capi.Hamiltonian(c,P.n_qubits,*P.ham_arrays());"
+            "print(repr(capi.energy_batch(c,pl,h,P.hf,P.plan_thetas()).tolist()))")
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FFQ_SECTOR_CL": cl},
+                         capture_output=True, text=True, check=True, cwd=os.path.dirname(os.path.dirname(__file__)))
+    e = np.array(eval(out.stdout.strip().splitlines()[-1]))
+    assert np.abs(e - e2).max() <= 1e-12
