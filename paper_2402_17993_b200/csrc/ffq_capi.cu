@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -134,7 +135,7 @@ struct ffq_plan_s {
     DevBuf<double> exp_fre, exp_fim, seg_fre, seg_fim;
     DevBuf<int64_t> seg_start, seg_foff;
   };
-  std::map<std::pair<const void*, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;
+  std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
   PlanDev dev() const {
     PlanDev d;
     d.n_ops = (int)cp.op_kind.size();
@@ -149,8 +150,13 @@ struct ffq_plan_s {
   }
 };
 
+// process-unique id per uploaded Hamiltonian: the compiled-program caches key on
+// it, never on the handle's address (a destroyed handle's address can be reused)
+static std::atomic<uint64_t> g_ham_uid{1};
+
 struct ffq_ham_s {
   ffq_ctx_t ctx;
+  uint64_t uid = g_ham_uid.fetch_add(1);
   CompiledHam ch;
   std::vector<uint64_t> raw_x, raw_z;  // the uploaded terms (sharded path recompiles them)
   std::vector<double> raw_re, raw_im;
@@ -393,7 +399,7 @@ int sector_parts(uint32_t size) {
 // compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
 // nullptr when the closure does not fit the cluster (then other paths run)
 const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
-  auto key = std::make_pair((const void*)h, hf);
+  auto key = std::make_pair(h->uid, hf);
   auto it = pl->sectors.find(key);
   if (it == pl->sectors.end()) {
     auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
@@ -586,7 +592,7 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   ctx->theta.alloc((size_t)chunk * std::max(1, pl->cp.n_gen));
   ctx->eout.alloc(chunk);
   ctx->eim.alloc(chunk);
-  GraphKey key{(uintptr_t)h, (uintptr_t)chunk, (uintptr_t)hf, (uintptr_t)ctx->theta.p,
+  GraphKey key{(uintptr_t)h->uid, (uintptr_t)chunk, (uintptr_t)hf, (uintptr_t)ctx->theta.p,
                (uintptr_t)ctx->slab.p, (uintptr_t)ctx->cs.p, (uintptr_t)ctx->partial.p,
                (uintptr_t)ctx->eout.p, (uintptr_t)ctx->eim.p, (uintptr_t)sup};
   auto it = pl->graphs.find(key);

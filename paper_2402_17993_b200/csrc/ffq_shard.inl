@@ -29,7 +29,7 @@ struct ffq_shard_s {
   std::vector<int> perm;
   int last_swaps = 0;
   // cache: physical Hamiltonian per (ham, final perm)
-  const void* ham_key = nullptr;
+  uint64_t ham_key = 0;  // ffq_ham_s::uid of the cached physical Hamiltonian
   std::vector<int> ham_perm;
   std::unique_ptr<ffq_ham_s> hphys;
   ~ffq_shard_s() {
@@ -201,7 +201,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   }
   sh->perm = S.final_perm;
   // physical Hamiltonian for the final permutation (cached)
-  if (sh->ham_key != (const void*)h || sh->ham_perm != S.final_perm || !sh->hphys) {
+  if (sh->ham_key != h->uid || sh->ham_perm != S.final_perm || !sh->hphys) {
     std::vector<uint64_t> x(h->raw_x.size()), z(h->raw_z.size());
     for (size_t t = 0; t < x.size(); ++t) {
       x[t] = permute_mask(h->raw_x[t], S.final_perm);
@@ -241,7 +241,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     hp->item_p.upload(ip, ctx->stream);
     hp->item_u0.upload(iu, ctx->stream);
     sh->hphys = std::move(hp);
-    sh->ham_key = h;
+    sh->ham_key = h->uid;
     sh->ham_perm = S.final_perm;
   }
   const ffq_ham_s* hp = sh->hphys.get();

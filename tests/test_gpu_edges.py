@@ -163,3 +163,38 @@ def test_sector_cluster_sizes_agree(monkeypatch, cl):
                          capture_output=True, text=True, check=True, cwd=os.path.dirname(os.path.dirname(__file__)))
     e = np.array(eval(out.stdout.strip().splitlines()[-1]))
     assert np.abs(e - e2).max() <= 1e-12
+
+
+@pytest.mark.parametrize("env", [{}, {"FFQ_SECTOR": "0"}, {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SECTOR": "0"}])
+def test_reuploaded_hamiltonian_never_hits_stale_cache(monkeypatch, oracle, env):
+    # plans cache compiled programs / captured graphs per Hamiltonian; a handle
+    # destroyed and re-uploaded (often at the same address) must not reuse them
+    c = _ctx(monkeypatch, env)
+    P = problems.config_problem(2, batch=2)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    x, z, co = P.ham_arrays()
+    rng = np.random.default_rng(11)
+    for it in range(6):
+        scale = 1.0 + it
+        ham = capi.Hamiltonian(c, P.n_qubits, x, z, co * scale)
+        e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        if it == 0:
+            base = e.copy()
+        assert np.abs(e - base * scale).max() <= 1e-10 * scale
+        del ham
+    # a structurally different Hamiltonian (different groups) after the same churn
+    hx = rng.integers(0, 1 << P.n_qubits, 30).astype(np.uint64)
+    hz = rng.integers(0, 1 << P.n_qubits, 30).astype(np.uint64)
+    hc = rng.normal(size=30)
+    ham = capi.Hamiltonian(c, P.n_qubits, hx, hz, hc)
+    e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    hs = oracle.PauliSum.from_terms(P.n_qubits, hx, hz, hc)
+    kind, idx = oracle.build_generators(P.n_qubits, P.n_elec)
+    for b in range(2):
+        ref, _ = oracle.energy_trotter(P.n_qubits, P.n_elec, kind, idx, np.array(P.plan.order, np.int32),
+                                       P.thetas[b], hs)
+        assert abs(e[b] - ref) <= 1e-10
+    c2 = capi.Context(0)
+    plan2 = capi.Plan(c2, P.n_qubits, *P.plan_arrays())
+    ham2 = capi.Hamiltonian(c2, P.n_qubits, hx, hz, hc)
+    assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
