@@ -69,8 +69,16 @@ const char* ffq_last_error(ffq_ctx_t ctx);
 int64_t ffq_ctx_kernel_launches(ffq_ctx_t ctx);
 /* The context's cudaStream_t, as an opaque pointer (for event timing). */
 int ffq_ctx_stream(ffq_ctx_t ctx, void** stream);
-/* Environment: FFQ_SMEM_MAX_QUBITS (default 13) caps the qubit count that
- * uses the shared-memory-resident evaluator; read at ffq_ctx_create. */
+/* Environment, read at ffq_ctx_create (tuning and diagnostics only; every
+ * setting gives the same energies to <= 1e-12):
+ *   FFQ_SECTOR (1)          support-closure evaluator first; 0 disables it
+ *   FFQ_SECTOR_CL (2)       CTAs per cluster for large closures: 2, 4 or 8
+ *   FFQ_SMEM_MAX_QUBITS (13) largest state held whole in one CTA's smem
+ *   FFQ_SUPPORT (1)         support-bitmap passes on the global-memory path
+ *   FFQ_TILE_BITS (12)      expectation tile width of the global path
+ *   FFQ_SLAB_MB (256)       state slab per chunk of the global path
+ *   FFQ_PERSIST, FFQ_PERSIST_MB, FFQ_PERSIST_NT  optional one-CTA-per-state kernel
+ *   FFQ_PHASE_CLOCKS        print per-phase cycle counts (read once per process) */
 
 /* ---- qubit Hamiltonian (PauliSum) ------------------------ */
 /* Flat Pauli sum, any order; duplicate strings are summed. The library groups

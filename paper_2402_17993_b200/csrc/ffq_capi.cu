@@ -93,6 +93,7 @@ struct ffq_ctx_s {
   int sector = 1;                                // env FFQ_SECTOR=0: no support-closure cluster evaluator
   int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
   int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
+  int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
@@ -386,14 +387,8 @@ constexpr uint32_t kSectorMaxSize = 32767;   // 15-bit pair indices
 
 // cluster size for a closure of `size` amplitudes: 1 when it fits a small CTA,
 // else env FFQ_SECTOR_CL (2, 4 or 8), default 2 (throughput-optimal at 18 qubits)
-int sector_parts(uint32_t size) {
-  if (size <= kSectorSingleMax) return 1;
-  static const int env_cl = [] {
-    const char* e = std::getenv("FFQ_SECTOR_CL");
-    const int v = e ? std::atoi(e) : 2;
-    return (v == 4 || v == 8) ? v : 2;
-  }();
-  return env_cl;
+int sector_parts(ffq_ctx_t ctx, uint32_t size) {
+  return size <= kSectorSingleMax ? 1 : ctx->sector_cl;
 }
 
 // compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
@@ -408,8 +403,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
     // closure size first (one part, no size limit on the part), then the real split
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1);
-    if (b->prog.ok && sector_parts(b->prog.size) > 1)
-      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(b->prog.size));
+    if (b->prog.ok && sector_parts(ctx, b->prog.size) > 1)
+      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size));
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
@@ -439,7 +434,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.seg_foff = b.seg_foff.p;
   sd.seg_fre = b.seg_fre.p;
   sd.seg_fim = b.seg_fim.p;
-  sd.hf_idx = b.prog.hf_idx;
+  sd.hf_slot = b.prog.hf_slot;
+  sd.f_real = b.prog.f_real ? 1 : 0;
   sd.n_ops = (int)pl->cp.op_kind.size();
   sd.gen_off = b.gen_off.p;
   sd.gen_pairs = b.gen_pairs.p;
@@ -706,6 +702,10 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_SECTOR")) c->sector = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
+    if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
+      const int v = std::atoi(e);
+      c->sector_cl = (v == 4 || v == 8) ? v : 2;
+    }
     return FFQ_OK;
   });
   if (rc != FFQ_OK) {

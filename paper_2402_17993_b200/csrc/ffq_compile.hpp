@@ -561,6 +561,49 @@ namespace ffq {
 //    precomputed per pair and deduplicated into a table.
 constexpr size_t kSegChunk = 512;
 
+// Shared-memory bank order for a list of pairs. A warp's 16-byte loads of
+// psi[i] (and of psi[j]) are served one quarter-warp per wavefront when the 8
+// lanes of each quarter hit distinct 16-byte bank groups, i.e. distinct
+// (slot & 7). ri[t], rj[t] are those residues for pair t; the returned order
+// packs the list into octets whose ri and rj are both all-distinct wherever the
+// residue histogram allows (largest bucket first), the rest fill in as they come.
+inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const std::vector<uint8_t>& rj) {
+  const size_t n = ri.size();
+  std::vector<uint32_t> bucket[64];
+  for (size_t t = n; t-- > 0;) bucket[ri[t] * 8 + rj[t]].push_back((uint32_t)t);  // pop_back -> ascending t
+  std::vector<uint32_t> out;
+  out.reserve(n);
+  size_t left = n;
+  while (left > 0) {
+    unsigned used_i = 0, used_j = 0;
+    int taken = 0;
+    for (; taken < 8 && left > 0; ++taken) {
+      int best = -1;
+      size_t best_n = 0;
+      for (int r = 0; r < 8; ++r) {
+        if ((used_i >> r) & 1u) continue;
+        for (int c = 0; c < 8; ++c)
+          if (!((used_j >> c) & 1u) && bucket[r * 8 + c].size() > best_n) { best = r * 8 + c; best_n = bucket[best].size(); }
+      }
+      if (best < 0) break;
+      out.push_back(bucket[best].back());
+      bucket[best].pop_back();
+      used_i |= 1u << (best >> 3);
+      used_j |= 1u << (best & 7);
+      --left;
+    }
+    for (; taken < 8 && left > 0; ++taken) {  // no conflict-free member left: largest bucket
+      int best = 0;
+      for (int b = 1; b < 64; ++b)
+        if (bucket[b].size() > bucket[best].size()) best = b;
+      out.push_back(bucket[best].back());
+      bucket[best].pop_back();
+      --left;
+    }
+  }
+  return out;
+}
+
 struct SectorProgram {
   bool ok = false;
   std::string why;  // reason when !ok
@@ -573,10 +616,15 @@ struct SectorProgram {
   uint64_t split_mask = 0;
   std::vector<uint32_t> part_start;  // [n_parts + 1]
   std::vector<uint32_t> basis;
+  // Amplitudes are addressed by 15-bit slots r << slot_bits | (i - part_start[r])
+  // (rank r of the owning CTA, offset in its part): the device turns a slot into
+  // a shared::cluster address with a shift, a mask and a select.
+  int slot_bits = 15;
+  uint32_t hf_slot = 0;
   std::vector<int64_t> gen_off;     // [n_ops * n_parts + 1]: op g, owner rank r -> gen_off[g * n_parts + r]
-  std::vector<uint32_t> gen_pairs;  // i | j << 16 (i: low-pattern member)
+  std::vector<uint32_t> gen_pairs;  // slot_i | slot_j << 15 | sgn(k & zout) < 0 << 30 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
-  // expectation pairs, i | j << 15 | sign << 30 (i: enumerated m, j: m ^ X),
+  // expectation pairs, slot_i | slot_j << 15 | sign << 30 (i: enumerated m, j: m ^ X),
   // in segments of one (group, pattern) and owner rank. A segment whose pairs
   // share |f| stores f once (seg_fre/fim) and a sign bit per pair; otherwise
   // f is stored per pair at seg_foff.
@@ -706,6 +754,16 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     while (i >= S.part_start[r + 1]) ++r;
     return r;
   };
+  S.slot_bits = 15 - __builtin_ctz((unsigned)n_parts);
+  for (int r = 0; r < n_parts; ++r)
+    if (S.part_start[r + 1] - S.part_start[r] > (1u << S.slot_bits)) { S.why = "part exceeds the slot range"; return S; }
+  auto slot = [&](uint32_t i) {
+    const int r = owner(i);
+    return ((uint32_t)r << S.slot_bits) | (i - S.part_start[r]);
+  };
+  S.hf_slot = slot(S.hf_idx);
+  // 16-byte bank group of S[i] within its CTA's amplitude array
+  auto bank_slot = [&](uint32_t i) { return (uint8_t)((i - S.part_start[owner(i)]) & 7u); };
   // a local pair stays with its CTA; a cross pair goes to the lighter of its two CTAs
   auto assign = [&](uint32_t i, uint32_t j, std::vector<int64_t>& load) {
     const int oi = owner(i), oj = owner(j);
@@ -723,12 +781,20 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       own[t] = (uint8_t)assign(i, j, load);
     }
     for (int r = 0; r < n_parts; ++r) {
+      std::vector<uint32_t> pi, pj;
+      std::vector<uint8_t> fl, ri, rj;
       for (size_t t = 0; t < gk[op].size(); ++t) {
         if (own[t] != r) continue;
         const auto& e = gk[op][t];
-        const uint32_t i = (uint32_t)idx[e.first], j = (uint32_t)idx[e.first ^ (uint32_t)d.x];
-        S.gen_pairs.push_back(i | (j << 16));
-        S.gen_flags.push_back(e.second);
+        pi.push_back((uint32_t)idx[e.first]);
+        pj.push_back((uint32_t)idx[e.first ^ (uint32_t)d.x]);
+        fl.push_back(e.second);
+        ri.push_back(bank_slot(pi.back()));
+        rj.push_back(bank_slot(pj.back()));
+      }
+      for (uint32_t t : bank_order(ri, rj)) {  // thread tid takes pair off + tid
+        S.gen_pairs.push_back(slot(pi[t]) | (slot(pj[t]) << 15) | ((uint32_t)(fl[t] & 1u) << 30));
+        S.gen_flags.push_back(fl[t]);
       }
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
     }
@@ -759,6 +825,17 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       for (size_t t = sg.first; t < sg.second; ++t)
         if (eown[t] == r) mine.push_back(t);
       if (mine.empty()) continue;
+      {  // lane l of a warp takes pair chunk_start + l (+ 32 u); chunks start at multiples of 8
+        std::vector<uint8_t> ri(mine.size()), rj(mine.size());
+        for (size_t u = 0; u < mine.size(); ++u) {
+          ri[u] = bank_slot((uint32_t)idx[ek[mine[u]].m]);
+          rj[u] = bank_slot((uint32_t)idx[ek[mine[u]].m ^ (uint32_t)H.groups[ek[mine[u]].g].x]);
+        }
+        std::vector<size_t> re;
+        re.reserve(mine.size());
+        for (uint32_t u : bank_order(ri, rj)) re.push_back(mine[u]);
+        mine.swap(re);
+      }
       const double fr0 = ek[mine[0]].fr, fi0 = ek[mine[0]].fi;
       bool shared = true;
       for (size_t t : mine)
@@ -774,7 +851,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         const auto& e = ek[t];
         const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
         const uint32_t neg = shared && (e.fr != fr0 || e.fi != fi0) ? 1u : 0u;
-        S.exp_pairs.push_back(i | (j << 15) | (neg << 30));
+        S.exp_pairs.push_back(slot(i) | (slot(j) << 15) | (neg << 30));
         if (!shared) {
           S.exp_fre.push_back(e.fr);
           S.exp_fim.push_back(e.fi);

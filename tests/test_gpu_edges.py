@@ -22,7 +22,7 @@ PATHS = {
 
 
 def _ctx(monkeypatch, env):
-    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST", "FFQ_SECTOR"):
+    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST", "FFQ_SECTOR", "FFQ_SECTOR_CL"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -148,21 +148,14 @@ def test_sector_single_cta_small_closure(monkeypatch, oracle):
 
 @pytest.mark.parametrize("cl", ["4", "8"])
 def test_sector_cluster_sizes_agree(monkeypatch, cl):
+    # FFQ_SECTOR_CL is read per context: 2-CTA (default) vs 4- or 8-CTA clusters
     P = problems.config_problem(3, batch=3)
-    c2 = _ctx(monkeypatch, {})
-    plan, ham = capi.Plan(c2, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c2, P.n_qubits, *P.ham_arrays())
-    e2 = capi.energy_batch(c2, plan, ham, P.hf, P.plan_thetas())
-    import subprocess
-    import sys
-    # FFQ_SECTOR_CL is read once per process: evaluate in a child process
-    code = ("import numpy as np;from paper_2402_17993_b200 import capi, problems;"
-            "P=problems.config_problem(3,batch=3);c=capi.Context(0);"
-            "pl=capi.Plan(c,P.n_qubits,*P.plan_arrays());h=capi.Hamiltonian(c,P.n_qubits,*P.ham_arrays());"
-            "print(repr(capi.energy_batch(c,pl,h,P.hf,P.plan_thetas()).tolist()))")
-    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FFQ_SECTOR_CL": cl},
-                         capture_output=True, text=True, check=True, cwd=os.path.dirname(os.path.dirname(__file__)))
-    e = np.array(eval(out.stdout.strip().splitlines()[-1]))
-    assert np.abs(e - e2).max() <= 1e-12
+    e = {}
+    for k in ("2", cl):
+        c = _ctx(monkeypatch, {"FFQ_SECTOR_CL": k})
+        plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        e[k] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    assert np.abs(e[cl] - e["2"]).max() <= 1e-12
 
 
 @pytest.mark.parametrize("env", [{}, {"FFQ_SECTOR": "0"}, {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SECTOR": "0"}])
