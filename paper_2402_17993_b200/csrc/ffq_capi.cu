@@ -131,10 +131,10 @@ struct ffq_plan_s {
   struct SectorDevBufs {
     SectorProgram prog;
     DevBuf<int64_t> gen_off;
-    DevBuf<uint32_t> gen_pairs, exp_pairs;
+    DevBuf<uint32_t> gen_pairs, row_pairs;
+    DevBuf<int32_t> secs;
     DevBuf<uint8_t> gen_flags;
-    DevBuf<double> exp_fre, exp_fim, seg_fre, seg_fim;
-    DevBuf<int64_t> seg_start, seg_foff;
+    DevBuf<double> row_fre, row_fim, pf_re, pf_im;
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
   PlanDev dev() const {
@@ -393,29 +393,42 @@ int sector_parts(ffq_ctx_t ctx, uint32_t size) {
 
 // compiled + uploaded support-closure program for (plan, Hamiltonian, hf), or
 // nullptr when the closure does not fit the cluster (then other paths run)
+// k_sector_eval's dynamic smem: Hmax + 1 amplitudes (zero slot), then either
+// the generator tables (cs and the two F per op, this rank's pair range and
+// flags per op) or, in the expectation, the peer-chunk buffer
+size_t sector_smem_bytes(size_t hmax, size_t n_ops, size_t buf_len = 0) {
+  const size_t tables = 3 * n_ops * sizeof(double2) + n_ops * (sizeof(uint2) + 1);
+  return (hmax + 1) * sizeof(double2) + std::max(tables, buf_len * sizeof(double2)) + 16;
+}
+
 const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
   auto key = std::make_pair(h->uid, hf);
   auto it = pl->sectors.find(key);
   if (it == pl->sectors.end()) {
     auto b = std::make_unique<ffq_plan_s::SectorDevBufs>();
-    const size_t tables = 3 * pl->cp.op_kind.size() * sizeof(double2) + pl->cp.op_kind.size() + 16;
+    const size_t tables = sector_smem_bytes(0, pl->cp.op_kind.size());
     const uint32_t max_part =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
     // closure size first (one part, no size limit on the part), then the real split
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1);
     if (b->prog.ok && sector_parts(ctx, b->prog.size) > 1)
-      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size));
+      b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
+                               (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)));
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
       b->gen_flags.upload(b->prog.gen_flags, ctx->stream);
-      b->exp_pairs.upload(b->prog.exp_pairs, ctx->stream);
-      b->exp_fre.upload(b->prog.exp_fre, ctx->stream);
-      if (!b->prog.f_real) b->exp_fim.upload(b->prog.exp_fim, ctx->stream);
-      b->seg_start.upload(b->prog.seg_start, ctx->stream);
-      b->seg_foff.upload(b->prog.seg_foff, ctx->stream);
-      b->seg_fre.upload(b->prog.seg_fre, ctx->stream);
-      b->seg_fim.upload(b->prog.seg_fim, ctx->stream);
+      b->row_pairs.upload(b->prog.row_pairs, ctx->stream);
+      std::vector<int32_t> secs;
+      for (const auto& es : b->prog.sections)
+        secs.insert(secs.end(), {es.src_rank, es.src_off, es.len, es.sh0, es.sh1, es.pp1, es.pf_base});
+      b->secs.upload(secs, ctx->stream);
+      b->row_fre.upload(b->prog.row_fre, ctx->stream);
+      b->pf_re.upload(b->prog.pf_re, ctx->stream);
+      if (!b->prog.f_real) {
+        b->row_fim.upload(b->prog.row_fim, ctx->stream);
+        b->pf_im.upload(b->prog.pf_im, ctx->stream);
+      }
       CK(cudaStreamSynchronize(ctx->stream));
     }
     it = pl->sectors.emplace(key, std::move(b)).first;
@@ -427,22 +440,23 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.size = b.prog.size;
   for (int r = 0; r <= b.prog.n_parts; ++r) {
     sd.part_start[r] = b.prog.part_start[r];
-    sd.seg_off[r] = b.prog.seg_off[r];
+    sd.sec_off[r] = b.prog.sec_off[r];
   }
   sd.split_mask = b.prog.split_mask;
-  sd.seg_start = b.seg_start.p;
-  sd.seg_foff = b.seg_foff.p;
-  sd.seg_fre = b.seg_fre.p;
-  sd.seg_fim = b.seg_fim.p;
   sd.hf_slot = b.prog.hf_slot;
   sd.f_real = b.prog.f_real ? 1 : 0;
   sd.n_ops = (int)pl->cp.op_kind.size();
   sd.gen_off = b.gen_off.p;
   sd.gen_pairs = b.gen_pairs.p;
   sd.gen_flags = b.gen_flags.p;
-  sd.exp_pairs = b.exp_pairs.p;
-  sd.exp_fre = b.exp_fre.p;
-  sd.exp_fim = b.prog.f_real ? nullptr : b.exp_fim.p;
+  sd.buf_off = b.prog.buf_off;
+  sd.buf_len = b.prog.buf_len;
+  sd.secs = b.secs.p;
+  sd.row_pairs = b.row_pairs.p;
+  sd.row_fre = b.row_fre.p;
+  sd.row_fim = b.prog.f_real ? nullptr : b.row_fim.p;
+  sd.pf_re = b.pf_re.p;
+  sd.pf_im = b.prog.f_real ? nullptr : b.pf_im.p;
   sd.n_parts = b.prog.n_parts;
   return &sd;
 }
@@ -452,7 +466,7 @@ void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, c
                      double* e, double* im, long long* clk) {
   size_t hmax = 0;
   for (int r = 0; r < CL; ++r) hmax = std::max<size_t>(hmax, sd.part_start[r + 1] - sd.part_start[r]);
-  const size_t sb = (hmax + 3 * pl->cp.op_kind.size()) * sizeof(double2) + pl->cp.op_kind.size() + 16;
+  const size_t sb = sector_smem_bytes(hmax, pl->cp.op_kind.size(), sd.buf_len);
   CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   if (CL > 1) CK(cudaFuncSetAttribute(k_sector_eval<CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};

@@ -624,21 +624,41 @@ struct SectorProgram {
   std::vector<int64_t> gen_off;     // [n_ops * n_parts + 1]: op g, owner rank r -> gen_off[g * n_parts + r]
   std::vector<uint32_t> gen_pairs;  // slot_i | slot_j << 15 | sgn(k & zout) < 0 << 30 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
-  // expectation pairs, slot_i | slot_j << 15 | sign << 30 (i: enumerated m, j: m ^ X),
-  // in segments of one (group, pattern) and owner rank. A segment whose pairs
-  // share |f| stores f once (seg_fre/fim) and a sign bit per pair; otherwise
-  // f is stored per pair at seg_foff.
-  std::vector<uint32_t> exp_pairs;
-  std::vector<double> exp_fre, exp_fim;  // per-pair f of per-pair segments (exp_fim empty if all real)
-  std::vector<int64_t> seg_start, seg_foff;  // seg_foff < 0: shared-f segment
-  std::vector<double> seg_fre, seg_fim;
-  std::vector<int32_t> seg_off;     // [n_parts + 1] segments per rank
+  // Expectation pairs, slot_i | slot_j << 15 | sign << 30 (i: enumerated m,
+  // j: m ^ X), in rows of 32 (one per warp lane). A row holds pairs of one
+  // (group, pattern) set owned by one CTA; sets are padded to whole rows with
+  // pairs of the owner's zero slot (an amplitude that stays 0). Rows whose
+  // pairs share |f| ("shared" rows, sign per pair) carry f once (row_fre/fim);
+  // the rest ("per-pair" rows) carry f per pair in pf_re/pf_im.
+  //
+  // Each rank's rows come in sections: first the pairs with both members in
+  // its own part, then, per chunk of a peer's part, the cross pairs whose peer
+  // member lies in that chunk. Before a chunk section the CTA copies the chunk
+  // (one coalesced DSMEM pass) into a buffer behind its own amplitudes (slots
+  // buf_off .. buf_off + buf_len - 1, overlaying the generator tables, dead by
+  // then) and the pairs address the copy, so cross pairs cost local smem reads.
+  struct ExpSection {
+    int32_t src_rank, src_off, len;  // chunk to copy (len 0: no copy)
+    int32_t sh0, sh1, pp1;           // shared rows [sh0, sh1), per-pair rows [sh1, pp1)
+    int32_t pf_base;                 // per-pair row ordinal of row sh1 (pf index (pf_base + row - sh1) * 32 + lane)
+  };
+  std::vector<ExpSection> sections;
+  std::vector<int32_t> sec_off;              // [n_parts + 1]
+  uint32_t hmax = 0, buf_off = 0, buf_len = 0;
+  std::vector<uint32_t> row_pairs;           // [n_rows * 32]
+  std::vector<double> row_fre, row_fim;      // [n_rows] (0 on per-pair rows; row_fim empty if all f real)
+  std::vector<double> pf_re, pf_im;          // [per-pair rows * 32] (pf_im empty if all f real)
+  std::vector<uint32_t> zero_slot;           // [n_parts]
   bool f_real = true;
   int64_t cross_pairs = 0;          // pairs whose members live in different CTAs
 };
 
+// cap_amps: shared-memory capacity of a CTA in amplitudes (own part, zero
+// slot and copy buffer); the buffer is used when at least kMinChunk fit.
+constexpr uint32_t kMinChunk = 256;
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
-                                    uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2) {
+                                    uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2,
+                                    uint32_t cap_amps = 0xFFFFFFFFu) {
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -756,7 +776,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   };
   S.slot_bits = 15 - __builtin_ctz((unsigned)n_parts);
   for (int r = 0; r < n_parts; ++r)
-    if (S.part_start[r + 1] - S.part_start[r] > (1u << S.slot_bits)) { S.why = "part exceeds the slot range"; return S; }
+    if (S.part_start[r + 1] - S.part_start[r] >= (1u << S.slot_bits)) { S.why = "part exceeds the slot range"; return S; }
   auto slot = [&](uint32_t i) {
     const int r = owner(i);
     return ((uint32_t)r << S.slot_bits) | (i - S.part_start[r]);
@@ -801,67 +821,134 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   }
   for (const auto& e : ek)
     if (e.fi != 0.0) S.f_real = false;
-  // ek is ordered by (group, pattern): segments of one (group, pattern) per owner
-  size_t a = 0;
-  std::vector<std::pair<size_t, size_t>> segs;
-  while (a < ek.size()) {
-    size_t b = a + 1;
-    while (b < ek.size() && ek[b].g == ek[a].g && ek[b].p == ek[a].p) ++b;
-    segs.push_back({a, b});
-    a = b;
-  }
-  std::vector<uint8_t> eown(ek.size());
+  S.zero_slot.resize((size_t)n_parts);
+  for (int r = 0; r < n_parts; ++r)
+    S.zero_slot[r] = ((uint32_t)r << S.slot_bits) | (S.part_start[r + 1] - S.part_start[r]);
+  for (int r = 0; r < n_parts; ++r) S.hmax = std::max(S.hmax, S.part_start[r + 1] - S.part_start[r]);
+  S.buf_off = S.hmax + 1;
   {
+    const uint64_t lim = std::min<uint64_t>(cap_amps, 1ull << S.slot_bits);
+    const uint64_t room = lim > S.buf_off ? lim - S.buf_off : 0;
+    uint32_t peer_max = 0;
+    for (int r = 0; r < n_parts; ++r) peer_max = std::max(peer_max, S.part_start[r + 1] - S.part_start[r]);
+    S.buf_len = n_parts > 1 && room >= kMinChunk ? (uint32_t)std::min<uint64_t>(room / 32 * 32, peer_max) : 0u;
+  }
+  const bool buffered = S.buf_len > 0;
+  std::vector<uint8_t> eown(ek.size());
+  {  // balance: with the chunk buffer a cross pair costs about what a local one does
     std::vector<int64_t> load((size_t)n_parts, 0);
     for (size_t t = 0; t < ek.size(); ++t) {
       const uint32_t i = (uint32_t)idx[ek[t].m], j = (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x];
-      eown[t] = (uint8_t)assign(i, j, load);
+      const int oi = owner(i), oj = owner(j);
+      const int o = oi == oj ? oi : (load[oi] <= load[oj] ? oi : oj);
+      load[o] += oi == oj || buffered ? 2 : 3;
+      eown[t] = (uint8_t)o;
     }
   }
-  S.seg_off.assign(1, 0);
+  S.sec_off.assign(1, 0);
+  std::vector<uint32_t> pp_words;  // staged per-pair rows of the current section
+  std::vector<double> pp_re, pp_im;
+  int32_t pf_rows = 0;
   for (int r = 0; r < n_parts; ++r) {
-    for (const auto& sg : segs) {
-      std::vector<size_t> mine;
-      for (size_t t = sg.first; t < sg.second; ++t)
-        if (eown[t] == r) mine.push_back(t);
-      if (mine.empty()) continue;
-      {  // lane l of a warp takes pair chunk_start + l (+ 32 u); chunks start at multiples of 8
-        std::vector<uint8_t> ri(mine.size()), rj(mine.size());
-        for (size_t u = 0; u < mine.size(); ++u) {
-          ri[u] = bank_slot((uint32_t)idx[ek[mine[u]].m]);
-          rj[u] = bank_slot((uint32_t)idx[ek[mine[u]].m ^ (uint32_t)H.groups[ek[mine[u]].g].x]);
-        }
-        std::vector<size_t> re;
-        re.reserve(mine.size());
-        for (uint32_t u : bank_order(ri, rj)) re.push_back(mine[u]);
-        mine.swap(re);
-      }
-      const double fr0 = ek[mine[0]].fr, fi0 = ek[mine[0]].fi;
-      bool shared = true;
-      for (size_t t : mine)
-        if (!((ek[t].fr == fr0 && ek[t].fi == fi0) || (ek[t].fr == -fr0 && ek[t].fi == -fi0))) { shared = false; break; }
-      // chunks of <= kSegChunk pairs, one warp each on the device
-      for (size_t c0 = 0; c0 < mine.size(); c0 += kSegChunk) {
-        S.seg_start.push_back((int64_t)S.exp_pairs.size() + (int64_t)c0);
-        S.seg_foff.push_back(shared ? -1 : (int64_t)S.exp_fre.size() + (int64_t)c0);
-        S.seg_fre.push_back(shared ? fr0 : 0.0);
-        S.seg_fim.push_back(shared ? fi0 : 0.0);
-      }
-      for (size_t t : mine) {
-        const auto& e = ek[t];
-        const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
-        const uint32_t neg = shared && (e.fr != fr0 || e.fi != fi0) ? 1u : 0u;
-        S.exp_pairs.push_back(slot(i) | (slot(j) << 15) | (neg << 30));
-        if (!shared) {
-          S.exp_fre.push_back(e.fr);
-          S.exp_fim.push_back(e.fi);
-        }
-      }
+    const uint32_t zpair = S.zero_slot[r] | (S.zero_slot[r] << 15);
+    // section key: 0 = local (and, unbuffered, every cross pair), else 1 + chunk id
+    auto key_of = [&](uint32_t i, uint32_t j) -> int64_t {
+      const int oi = owner(i), oj = owner(j);
+      if (oi == oj || !buffered) return 0;
+      const uint32_t peer = oi == r ? j : i;
+      const int rp = oi == r ? oj : oi;
+      return 1 + (int64_t)rp * 65536 + (peer - S.part_start[rp]) / S.buf_len;
+    };
+    auto enc = [&](uint32_t x, int64_t key) -> uint32_t {
+      if (owner(x) == r || key == 0) return slot(x);
+      const int rp = owner(x);
+      const uint32_t chunk0 = (uint32_t)(((key - 1) % 65536) * S.buf_len);
+      return ((uint32_t)r << S.slot_bits) | (S.buf_off + (x - S.part_start[rp] - chunk0));
+    };
+    std::map<int64_t, std::vector<size_t>> secs;  // ek indices in (group, pattern) order
+    for (size_t t = 0; t < ek.size(); ++t) {
+      if (eown[t] != r) continue;
+      const uint32_t i = (uint32_t)idx[ek[t].m], j = (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x];
+      secs[key_of(i, j)].push_back(t);
     }
-    S.seg_off.push_back((int32_t)S.seg_start.size());
+    if (secs.empty()) secs[0];
+    for (auto& [key, list] : secs) {
+      SectorProgram::ExpSection es{};
+      if (key > 0) {
+        es.src_rank = (int32_t)((key - 1) / 65536);
+        es.src_off = (int32_t)(((key - 1) % 65536) * S.buf_len);
+        es.len = (int32_t)std::min<uint32_t>(S.buf_len, S.part_start[es.src_rank + 1] - S.part_start[es.src_rank] - es.src_off);
+      }
+      es.sh0 = (int32_t)(S.row_pairs.size() / 32);
+      pp_words.clear();
+      pp_re.clear();
+      pp_im.clear();
+      size_t a0 = 0;
+      while (a0 < list.size()) {
+        size_t b0 = a0 + 1;
+        while (b0 < list.size() && ek[list[b0]].g == ek[list[a0]].g && ek[list[b0]].p == ek[list[a0]].p) ++b0;
+        // one (group, pattern) set: encode, bank-order, pad to rows
+        std::vector<uint32_t> si, sj;
+        std::vector<uint8_t> ri, rj;
+        for (size_t u = a0; u < b0; ++u) {
+          const auto& e = ek[list[u]];
+          const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
+          si.push_back(enc(i, key));
+          sj.push_back(enc(j, key));
+          ri.push_back((uint8_t)(si.back() & 7u));
+          rj.push_back((uint8_t)(sj.back() & 7u));
+        }
+        const std::vector<uint32_t> order = bank_order(ri, rj);
+        const double fr0 = ek[list[a0]].fr, fi0 = ek[list[a0]].fi;
+        bool shared = true;
+        for (size_t u = a0; u < b0; ++u) {
+          const auto& e = ek[list[u]];
+          if (!((e.fr == fr0 && e.fi == fi0) || (e.fr == -fr0 && e.fi == -fi0))) { shared = false; break; }
+        }
+        const size_t cnt = b0 - a0, padded = (cnt + 31) / 32 * 32;
+        for (size_t u = 0; u < padded; ++u) {
+          uint32_t word = zpair;
+          double fr = 0.0, fi = 0.0;
+          if (u < cnt) {
+            const uint32_t v = order[u];
+            const auto& e = ek[list[a0 + v]];
+            const uint32_t neg = shared && (e.fr != fr0 || e.fi != fi0) ? 1u : 0u;
+            word = si[v] | (sj[v] << 15) | (neg << 30);
+            fr = e.fr;
+            fi = e.fi;
+          }
+          if (shared) {
+            S.row_pairs.push_back(word);
+          } else {
+            pp_words.push_back(word);
+            pp_re.push_back(fr);
+            pp_im.push_back(fi);
+          }
+        }
+        if (shared)
+          for (size_t u = 0; u < padded / 32; ++u) {
+            S.row_fre.push_back(fr0);
+            S.row_fim.push_back(fi0);
+          }
+        a0 = b0;
+      }
+      es.sh1 = (int32_t)(S.row_pairs.size() / 32);
+      S.row_pairs.insert(S.row_pairs.end(), pp_words.begin(), pp_words.end());
+      S.row_fre.resize(S.row_pairs.size() / 32, 0.0);
+      S.row_fim.resize(S.row_pairs.size() / 32, 0.0);
+      S.pf_re.insert(S.pf_re.end(), pp_re.begin(), pp_re.end());
+      S.pf_im.insert(S.pf_im.end(), pp_im.begin(), pp_im.end());
+      es.pp1 = (int32_t)(S.row_pairs.size() / 32);
+      es.pf_base = pf_rows;
+      pf_rows += es.pp1 - es.sh1;
+      S.sections.push_back(es);
+    }
+    S.sec_off.push_back((int32_t)S.sections.size());
   }
-  S.seg_start.push_back((int64_t)S.exp_pairs.size());  // sentinel
-  if (S.f_real) S.exp_fim.clear();
+  if (S.f_real) {
+    S.row_fim.clear();
+    S.pf_im.clear();
+  }
   S.ok = true;
   return S;
 }

@@ -29,17 +29,18 @@ struct SectorDev {
   uint32_t part_start[kSectorMaxParts + 1];  // CTA r holds S[part_start[r], part_start[r + 1])
   int n_ops, n_parts, f_real;
   uint64_t split_mask;          // generators flipping any of these qubits need a cluster barrier
-  int32_t seg_off[kSectorMaxParts + 1];
-  const int64_t* seg_start;     // [n_seg + 1]
-  const int64_t* seg_foff;      // < 0: shared |f| (seg_fre/fim), else per-pair f offset
-  const double* seg_fre;
-  const double* seg_fim;
   const int64_t* gen_off;       // [CL * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;    // slot_i | slot_j << 15 | sign << 30
   const uint8_t* gen_flags;     // pattern pair index << 1 (read only for multi-pattern ops)
-  const uint32_t* exp_pairs;    // slot_i | slot_j << 15 | sign << 30
-  const double* exp_fre;
-  const double* exp_fim;  // nullptr when every f is real
+  // expectation rows in sections (SectorProgram::ExpSection): 32 pair words each
+  int32_t sec_off[kSectorMaxParts + 1];
+  uint32_t buf_off, buf_len;    // chunk copy buffer: amplitude indices [buf_off, buf_off + buf_len)
+  const int32_t* secs;          // [n_sec * 7]: src_rank, src_off, len, sh0, sh1, pp1, pf_base
+  const uint32_t* row_pairs;
+  const double* row_fre;        // [rows] (0 on per-pair rows)
+  const double* row_fim;        // nullptr when every f is real
+  const double* pf_re;          // [per-pair rows * 32]
+  const double* pf_im;          // nullptr when every f is real
 };
 
 // Amplitude slots (SectorProgram::slot_bits): 15 - log2(CL) offset bits, the
@@ -78,20 +79,69 @@ __device__ __forceinline__ void sst(uint32_t a, double2 v) {
     asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y));
 }
 
-// sum over one shared-|f| segment's pairs of sign * conj(psi[j]) psi[i]
-// (.x real part, .y imaginary part unless FR); lane takes pairs s0 + lane + 32 u
+// sum over shared-|f| rows [r0, r1) of f_row * sign * conj(psi[j]) psi[i]
+// (real part; with !FR also the imaginary one); lane takes word row * 32 + lane,
+// four rows per trip with the next trip's pair words already in flight
 template <int CL, bool FR>
-__device__ __forceinline__ double2 seg_signed_sum(const uint32_t* __restrict__ pairs, int s0, int s1, int lane,
-                                                  const SlotMap<CL>& sm) {
-  double sr = 0.0, si = 0.0;
-  for (int t = s0 + lane; t < s1; t += 128) {
-    uint32_t w[4];
-    double sg4[4];
+__device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r1, int lane, const SlotMap<CL>& sm) {
+  double acc = 0.0;
+  if (r0 >= r1) return acc;
+  const uint32_t* __restrict__ pairs = sd.row_pairs + lane;
+  uint32_t wn[4];
+  double fn[4], fin[4];
+  auto fetch = [&](int row) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int tu = t + 32 * u;
-      w[u] = __ldg(pairs + min(tu, s1 - 1));
-      sg4[u] = tu < s1 ? ((w[u] >> 30) ? -1.0 : 1.0) : 0.0;
+      const bool ok = row + u < r1;
+      const int q = ok ? row + u : r1 - 1;
+      wn[u] = __ldg(pairs + 32 * q);
+      fn[u] = ok ? __ldg(sd.row_fre + q) : 0.0;
+      if (!FR) fin[u] = ok ? __ldg(sd.row_fim + q) : 0.0;
+    }
+  };
+  fetch(r0);
+  for (int row = r0; row < r1; row += 4) {
+    uint32_t w[4];
+    double f[4], fi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      w[u] = wn[u];
+      f[u] = fn[u];
+      if (!FR) fi[u] = fin[u];
+    }
+    if (row + 4 < r1) fetch(row + 4);
+    double2 a[4], bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
+      bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double fs = (w[u] >> 30) & 1u ? -f[u] : f[u];
+      acc = fma(fs, fma(bb[u].x, a[u].x, bb[u].y * a[u].y), acc);
+      if (!FR) acc = fma((w[u] >> 30) & 1u ? fi[u] : -fi[u], fma(bb[u].x, a[u].y, -bb[u].y * a[u].x), acc);
+    }
+  }
+  return acc;
+}
+
+// per-pair-f rows [r0, r1) (f at pf[(row - pp0) * 32 + lane], pp0 = the row of pf ordinal 0)
+template <int CL>
+__device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int r1, int pp0, int lane,
+                                               const SlotMap<CL>& sm) {
+  double acc = 0.0;
+  for (int row = r0; row < r1; row += 4) {
+    uint32_t w[4];
+    double fr[4], fi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = row + u < r1;
+      const int q = ok ? row + u : r1 - 1;
+      w[u] = __ldg(sd.row_pairs + 32 * q + lane);
+      const int64_t fo = (int64_t)(q - pp0) * 32 + lane;
+      fr[u] = ok ? __ldg(sd.pf_re + fo) : 0.0;
+      fi[u] = (ok && sd.pf_im) ? __ldg(sd.pf_im + fo) : 0.0;
     }
     double2 a[4], bb[4];
 #pragma unroll
@@ -101,19 +151,21 @@ __device__ __forceinline__ double2 seg_signed_sum(const uint32_t* __restrict__ p
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      sr = fma(sg4[u], fma(bb[u].x, a[u].x, bb[u].y * a[u].y), sr);
-      if (!FR) si = fma(sg4[u], fma(bb[u].x, a[u].y, -bb[u].y * a[u].x), si);
+      const double prx = fma(bb[u].x, a[u].x, bb[u].y * a[u].y);
+      const double pry = fma(bb[u].x, a[u].y, -bb[u].y * a[u].x);
+      acc = fma(prx, fr[u], acc);
+      acc = fma(-pry, fi[u], acc);
     }
   }
-  return make_double2(sr, si);
+  return acc;
 }
 
 // one generator's pairs assigned to this CTA: exp(theta A) as the 2x2 rotation
 // a' = c a + g F_hi b, b' = c b + g F_lo a per pair (g = +-s by the pair's sign)
 template <int CL, int NT, bool MULTI>
-__device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl, int op, int64_t t0, int64_t t1,
+__device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl, int op, uint32_t t0, uint32_t t1,
                                          uint32_t w, double2 csv, double2 flo, double2 fhi, const SlotMap<CL>& sm) {
-  for (int64_t t = t0; t < t1; t += NT) {
+  for (uint32_t t = t0; t < t1; t += NT) {
     if (t != t0) w = __ldg(sd.gen_pairs + t);
     if (MULTI) {  // more than one active pattern pair (not UCCSD)
       const int po = pl.fused[pl.op_idx[op]].pair_off + (__ldg(sd.gen_flags + t) >> 1);
@@ -134,7 +186,9 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
                                                        int theta_stride, double* __restrict__ e_out,
                                                        double* __restrict__ im_out, int n_rows,
                                                        long long* __restrict__ phase_clk) {
-  // dynamic smem: [Hmax] amplitudes | [n_ops] (cos, sin*scale) | [n_ops] (F_lo, F_hi) of pattern pair 0 | [n_ops] flags
+  // dynamic smem: [Hmax + 1] amplitudes (the last ones of each part stay 0: the
+  // zero slot of padded rows) | [n_ops] (cos, sin*scale) | [n_ops] (F_lo, F_hi)
+  // of pattern pair 0 | [n_ops] this rank's pair range | [n_ops] flags
   extern __shared__ __align__(16) double2 sm_c[];
   __shared__ double2 red[NT / 32];
   __shared__ double cl_part[CL];
@@ -146,9 +200,10 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   uint32_t Hmax = 0;
 #pragma unroll
   for (int r = 0; r < CL; ++r) Hmax = max(Hmax, sd.part_start[r + 1] - sd.part_start[r]);
-  double2* cs = sm_c + Hmax;
+  double2* cs = sm_c + Hmax + 1;
   double2* fz = cs + pl.n_ops;  // [2 * n_ops]
-  uint8_t* opfl = reinterpret_cast<uint8_t*>(fz + 2 * pl.n_ops);  // [n_ops]: bit 0 crosses the split, bit 1 multi-pattern
+  uint2* gse = reinterpret_cast<uint2*>(fz + 2 * pl.n_ops);  // [n_ops]
+  uint8_t* opfl = reinterpret_cast<uint8_t*>(gse + pl.n_ops);  // [n_ops]: bit 0 crosses the split, bit 1 multi-pattern
   SlotMap<CL> sm;
   {
     const uint32_t local = (uint32_t)__cvta_generic_to_shared(sm_c);
@@ -163,7 +218,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
       }
     }
   }
-  for (uint32_t i = threadIdx.x; i < Hmax; i += NT) sm_c[i] = make_double2(0.0, 0.0);
+  for (uint32_t i = threadIdx.x; i <= Hmax; i += NT) sm_c[i] = make_double2(0.0, 0.0);
   for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
     const double phi = theta[(int64_t)row * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
     double sv, cv;
@@ -173,6 +228,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     fz[2 * op] = pl.pair_f[2 * d.pair_off];
     fz[2 * op + 1] = pl.pair_f[2 * d.pair_off + 1];
     opfl[op] = (uint8_t)(((d.x & sd.split_mask) != 0 ? 1 : 0) | (d.npair > 1 ? 2 : 0));
+    gse[op] = make_uint2((uint32_t)sd.gen_off[CL * op + rank], (uint32_t)sd.gen_off[CL * op + rank + 1]);
   }
   cluster.sync();
   if (threadIdx.x == 0 && (CL == 1 || (int)(sd.hf_slot >> SlotMap<CL>::kBits) == rank))
@@ -180,75 +236,66 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   cluster.sync();
   // generators: each CTA processes the pairs assigned to it (mostly local: S is
   // split on the qubits the fewest flip masks touch); one pair per thread per
-  // trip, the next op's first pair word prefetched across the barrier
-  const int tid = threadIdx.x;
-  int64_t nx0 = sd.gen_off[rank] + tid, nx1 = sd.gen_off[rank + 1];  // op 0
-  uint32_t nw = nx0 < nx1 ? __ldg(sd.gen_pairs + nx0) : 0u;
+  // trip; each thread's first pair word of the next two ops is in flight
+  // across the barriers
+  const uint32_t tid = threadIdx.x;
+  auto first_word = [&](int op) -> uint32_t {
+    const uint2 se = gse[op];
+    return se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u;
+  };
+  uint32_t w0 = sd.n_ops > 0 ? first_word(0) : 0u, w1 = sd.n_ops > 1 ? first_word(1) : 0u;
   for (int op = 0; op < sd.n_ops; ++op) {
-    const int64_t t0 = nx0, t1 = nx1;
-    uint32_t w = nw;
-    if (op + 1 < sd.n_ops) {
-      nx0 = sd.gen_off[CL * (op + 1) + rank] + tid;
-      nx1 = sd.gen_off[CL * (op + 1) + rank + 1];
-      nw = nx0 < nx1 ? __ldg(sd.gen_pairs + nx0) : 0u;
-    }
+    const uint32_t w = w0;
+    w0 = w1;
+    w1 = op + 2 < sd.n_ops ? first_word(op + 2) : 0u;
+    const uint2 se = gse[op];
     const int fl = opfl[op];
-    if (t0 < t1) {
+    if (se.x + tid < se.y) {
       if (fl & 2)
-        gen_pass<CL, NT, true>(sd, pl, op, t0, t1, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+        gen_pass<CL, NT, true>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
       else
-        gen_pass<CL, NT, false>(sd, pl, op, t0, t1, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+        gen_pass<CL, NT, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
     }
     // a generator whose flip mask avoids the split qubits only touches this
     // CTA's part: a CTA barrier suffices unless it or the next one crosses
     const bool cross = (fl & 1) != 0;
-    const bool next_cross = op + 1 < sd.n_ops && (opfl[op + 1] & 1) != 0;
+    // the last one also needs the cluster barrier: the expectation reads peer parts
+    const bool next_cross = op + 1 >= sd.n_ops || (opfl[op + 1] & 1) != 0;
     if (CL > 1 && (cross || next_cross)) cluster.sync(); else __syncthreads();
   }
   const long long clk1 = clock64();
-  // <H>: sum over (m, m ^ X) pairs of Re(conj(psi[j]) psi[i] f). Warp w takes
-  // this rank's segments w, w + NT/32, ... (<= 512 pairs each); lanes take four
-  // pairs per trip, every pair word and amplitude load issued before the
-  // arithmetic; tail lanes re-read the last pair with weight 0 (no branches)
+  // <H>: sum over (m, m ^ X) pairs of Re(conj(psi[j]) psi[i] f), section by
+  // section; a chunk section first copies the peer chunk into the buffer (the
+  // generator tables behind the amplitudes are dead by now). Warp w takes an
+  // equal contiguous share of each section's shared and per-pair rows.
   double acc = 0.0;
   {
+    constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int sg = sd.seg_off[rank] + warp; sg < sd.seg_off[rank + 1]; sg += NT / 32) {
-      const int s0 = (int)sd.seg_start[sg], s1 = (int)sd.seg_start[sg + 1];
-      const int64_t foff = sd.seg_foff[sg];
-      if (foff < 0) {  // shared |f|: per-pair sign, F applied once per segment
-        if (sd.f_real)
-          acc = fma(seg_signed_sum<CL, true>(sd.exp_pairs, s0, s1, lane, sm).x, sd.seg_fre[sg], acc);
-        else {
-          const double2 ss = seg_signed_sum<CL, false>(sd.exp_pairs, s0, s1, lane, sm);
-          acc = fma(ss.x, sd.seg_fre[sg], fma(-ss.y, sd.seg_fim[sg], acc));
+    for (int sc = sd.sec_off[rank]; sc < sd.sec_off[rank + 1]; ++sc) {
+      const int32_t* es = sd.secs + 7 * sc;
+      const int len = es[2];
+      if (CL > 1 && len > 0) {
+        const uint32_t src = ((uint32_t)es[0] << SlotMap<CL>::kBits) | (uint32_t)es[1];
+        __syncthreads();  // the previous chunk's readers are done
+        for (int i = threadIdx.x; i < len; i += 4 * NT) {
+          double2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u * NT < len) v[u] = sld<CL>(sm.addr(src + i + u * NT));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u * NT < len) sm_c[sd.buf_off + i + u * NT] = v[u];
         }
-      } else {  // per-pair f
-        for (int t = s0 + lane; t < s1; t += 128) {
-          uint32_t w[4];
-          double fr[4], fi[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int tu = t + 32 * u;
-            const int tc = min(tu, s1 - 1);
-            w[u] = __ldg(sd.exp_pairs + tc);
-            fr[u] = tu < s1 ? __ldg(sd.exp_fre + foff + (tc - s0)) : 0.0;
-            fi[u] = (tu < s1 && sd.exp_fim) ? __ldg(sd.exp_fim + foff + (tc - s0)) : 0.0;
-          }
-          double2 a[4], bb[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
-            bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double prx = fma(bb[u].x, a[u].x, bb[u].y * a[u].y);
-            const double pry = fma(bb[u].x, a[u].y, -bb[u].y * a[u].x);
-            acc = fma(prx, fr[u], acc);
-            acc = fma(-pry, fi[u], acc);
-          }
-        }
+        __syncthreads();
+      }
+      const int sh0 = es[3], shn = es[4] - es[3];
+      const int a0 = sh0 + (int)((int64_t)shn * warp / NW), a1 = sh0 + (int)((int64_t)shn * (warp + 1) / NW);
+      acc += sd.f_real ? shared_rows<CL, true>(sd, a0, a1, lane, sm) : shared_rows<CL, false>(sd, a0, a1, lane, sm);
+      const int pp0 = es[4], ppn = es[5] - es[4];
+      if (ppn > 0) {
+        const int b0 = pp0 + (int)((int64_t)ppn * warp / NW), b1 = pp0 + (int)((int64_t)ppn * (warp + 1) / NW);
+        acc += perpair_rows<CL>(sd, b0, b1, pp0 - es[6], lane, sm);
       }
     }
   }
