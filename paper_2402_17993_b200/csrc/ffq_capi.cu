@@ -133,7 +133,7 @@ struct ffq_plan_s {
     DevBuf<int64_t> gen_off;
     DevBuf<uint32_t> gen_pairs, row_pairs;
     DevBuf<int32_t> secs;
-    DevBuf<uint8_t> gen_flags;
+    DevBuf<uint8_t> gen_flags, op_cross;
     DevBuf<double> row_fre, row_fim, pf_re, pf_im;
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
@@ -418,6 +418,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
       b->gen_flags.upload(b->prog.gen_flags, ctx->stream);
+      b->op_cross.upload(b->prog.op_cross, ctx->stream);
       b->row_pairs.upload(b->prog.row_pairs, ctx->stream);
       std::vector<int32_t> secs;
       for (const auto& es : b->prog.sections)
@@ -442,7 +443,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     sd.part_start[r] = b.prog.part_start[r];
     sd.sec_off[r] = b.prog.sec_off[r];
   }
-  sd.split_mask = b.prog.split_mask;
+  sd.op_cross = b.op_cross.p;
   sd.hf_slot = b.prog.hf_slot;
   sd.f_real = b.prog.f_real ? 1 : 0;
   sd.n_ops = (int)pl->cp.op_kind.size();

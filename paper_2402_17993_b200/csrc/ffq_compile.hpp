@@ -609,11 +609,13 @@ struct SectorProgram {
   std::string why;  // reason when !ok
   int n = 0;
   uint32_t size = 0, hf_idx = 0;
-  // S is split over n_parts = 2^s CTAs by the values of the s qubits in
-  // split_mask (chosen to minimise pairs that cross CTAs); part r holds
-  // S[part_start[r], part_start[r + 1]), ordered by (part, k)
+  // S is split over n_parts = 2^s CTAs by the parities of the s masks in
+  // split_masks (see compile_sector); part r holds S[part_start[r],
+  // part_start[r + 1]), ordered by (part, k). op_cross[op] = 1 when generator
+  // op has pairs across CTAs (its step ends with a cluster barrier).
   int n_parts = 1;
-  uint64_t split_mask = 0;
+  std::vector<uint64_t> split_masks;
+  std::vector<uint8_t> op_cross;
   std::vector<uint32_t> part_start;  // [n_parts + 1]
   std::vector<uint32_t> basis;
   // Amplitudes are addressed by 15-bit slots r << slot_bits | (i - part_start[r])
@@ -650,7 +652,6 @@ struct SectorProgram {
   std::vector<double> pf_re, pf_im;          // [per-pair rows * 32] (pf_im empty if all f real)
   std::vector<uint32_t> zero_slot;           // [n_parts]
   bool f_real = true;
-  int64_t cross_pairs = 0;          // pairs whose members live in different CTAs
 };
 
 // cap_amps: shared-memory capacity of a CTA in amplitudes (own part, zero
@@ -722,50 +723,76 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   }
   S.size = (uint32_t)list.size();
   if (S.size > 32767) { S.why = "support closure exceeds 15-bit indices"; return S; }
-  // split qubits, greedily: each added bit minimises the pairs whose flip mask
-  // touches the split, with every part within max_part amplitudes
-  auto part_of = [&](uint32_t k, uint64_t mask) {
-    uint32_t r = 0, b = 0;
-    for (int q = 0; q < n; ++q)
-      if ((mask >> q) & 1ULL) r |= ((k >> q) & 1u) << b++;
+  // split S over 2^s CTAs by the parities of s qubit masks M_1..M_s (part bit
+  // b = parity(k & M_b)); a pair (k, k ^ X) crosses CTAs iff some parity(X & M_b)
+  // is odd. Masks are chosen greedily from single qubits and the occupied /
+  // virtual / spin classes of hf (and their intersections) by a cost in
+  // cycles measured on B200: ~2000 per generator step that needs a cluster
+  // barrier instead of a CTA barrier, ~1 per cross generator pair, ~0.02 per
+  // cross expectation pair (those read a local copy of the peer chunk); every
+  // part must fit a CTA.
+  auto part_of = [&](uint32_t k, const std::vector<uint64_t>& ms) {
+    uint32_t r = 0;
+    for (size_t b = 0; b < ms.size(); ++b) r |= (uint32_t)(__builtin_popcountll(k & ms[b]) & 1) << b;
     return r;
   };
-  uint64_t mask = 0;
-  int64_t cross = 0;
+  auto crosses = [](uint64_t x, const std::vector<uint64_t>& ms) {
+    for (uint64_t m : ms)
+      if (__builtin_popcountll(x & m) & 1) return true;
+    return false;
+  };
+  std::vector<uint64_t> cands;
+  {
+    const uint64_t all = n >= 64 ? ~0ULL : (1ULL << n) - 1, occ = hf & all, vir = all & ~hf;
+    uint64_t alpha = 0;
+    for (int q = 0; q < n; q += 2) alpha |= 1ULL << q;
+    const uint64_t beta = all & ~alpha;
+    for (int q = 0; q < n; ++q) cands.push_back(1ULL << q);
+    for (uint64_t m : {occ, vir, alpha, beta, occ & alpha, occ & beta, vir & alpha, vir & beta})
+      if (m != 0 && m != all && std::find(cands.begin(), cands.end(), m) == cands.end()) cands.push_back(m);
+  }
+  std::map<uint64_t, int64_t> exp_by_x;
+  for (const auto& e : ek) ++exp_by_x[H.groups[e.g].x];
+  std::vector<uint64_t> masks;
+  double best_cost = 0.0;
   for (int s = 0; (1 << s) < n_parts; ++s) {
     int best = -1;
-    int64_t best_cross = -1;
-    for (int b = 0; b < n; ++b) {
-      if ((mask >> b) & 1ULL) continue;
-      const uint64_t m2 = mask | (1ULL << b);
+    for (size_t c = 0; c < cands.size(); ++c) {
+      std::vector<uint64_t> m2 = masks;
+      m2.push_back(cands[c]);
       std::vector<uint32_t> cnt(size_t(1) << (s + 1), 0);
       for (uint32_t k : list) ++cnt[part_of(k, m2)];
       bool fits = true;
-      if (s + 1 == __builtin_ctz(n_parts))  // final level: every part non-empty and within a CTA
-        for (uint32_t c : cnt) fits &= c > 0 && c <= max_part;
+      for (uint32_t v : cnt) fits &= v > 0;  // independent of the earlier masks on S
+      if (s + 1 == __builtin_ctz(n_parts))  // final level: every part within a CTA
+        for (uint32_t v : cnt) fits &= v <= max_part;
       if (!fits) continue;
-      int64_t cr = 0;
-      for (int op = 0; op < n_ops; ++op)
-        if (P.fused[P.op_idx[op]].x & m2) cr += (int64_t)gk[op].size();
-      for (const auto& e : ek)
-        if (H.groups[e.g].x & m2) ++cr;
-      if (best < 0 || cr < best_cross) { best = b; best_cross = cr; }
+      double cost = 0.0;
+      for (int op = 0; op < n_ops; ++op) {
+        const bool cr = crosses(P.fused[P.op_idx[op]].x, m2);
+        const bool nx = op + 1 >= n_ops || crosses(P.fused[P.op_idx[op + 1]].x, m2);
+        if (cr || nx) cost += 2000.0;
+        if (cr) cost += (double)gk[op].size();
+      }
+      for (const auto& [x, c2] : exp_by_x)
+        if (crosses(x, m2)) cost += 0.02 * (double)c2;
+      if (best < 0 || cost < best_cost) { best = (int)c; best_cost = cost; }
     }
     if (best < 0) { S.why = "no split of the support closure fits the CTAs"; return S; }
-    mask |= 1ULL << best;
-    cross = best_cross;
+    masks.push_back(cands[best]);
   }
   if (n_parts == 1 && S.size > max_part) { S.why = "support closure does not fit one CTA"; return S; }
   S.n_parts = n_parts;
-  S.split_mask = mask;
-  S.cross_pairs = cross;
+  S.split_masks = masks;
+  S.op_cross.assign((size_t)n_ops, 0);
+  for (int op = 0; op < n_ops; ++op) S.op_cross[op] = crosses(P.fused[P.op_idx[op]].x, masks) ? 1 : 0;
   std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t c) {
-    const uint32_t pa = part_of(a, mask), pc = part_of(c, mask);
+    const uint32_t pa = part_of(a, masks), pc = part_of(c, masks);
     return pa != pc ? pa < pc : a < c;
   });
   S.basis = list;
   S.part_start.assign((size_t)n_parts + 1, 0);
-  for (uint32_t k : list) ++S.part_start[part_of(k, mask) + 1];
+  for (uint32_t k : list) ++S.part_start[part_of(k, masks) + 1];
   for (int r = 0; r < n_parts; ++r) S.part_start[r + 1] += S.part_start[r];
   for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
   S.hf_idx = (uint32_t)idx[hf];

@@ -28,7 +28,7 @@ struct SectorDev {
   uint32_t size, hf_slot;
   uint32_t part_start[kSectorMaxParts + 1];  // CTA r holds S[part_start[r], part_start[r + 1])
   int n_ops, n_parts, f_real;
-  uint64_t split_mask;          // generators flipping any of these qubits need a cluster barrier
+  const uint8_t* op_cross;      // [n_ops] 1: the generator has pairs across CTAs (cluster barrier)
   const int64_t* gen_off;       // [CL * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;    // slot_i | slot_j << 15 | sign << 30
   const uint8_t* gen_flags;     // pattern pair index << 1 (read only for multi-pattern ops)
@@ -50,6 +50,11 @@ template <int CL>
 struct SlotMap {
   static constexpr int kBits = CL == 1 ? 15 : (CL == 2 ? 14 : (CL == 4 ? 13 : 12));
   uint32_t base[CL];
+  uint32_t local;  // this CTA's amplitudes in the shared::cta window
+  // slot of this CTA's own part (or its chunk buffer): shared::cta address
+  __device__ __forceinline__ uint32_t laddr(uint32_t s) const {
+    return local + ((s & ((1u << kBits) - 1u)) << 4);
+  }
   __device__ __forceinline__ uint32_t addr(uint32_t s) const {
     const uint32_t off = (s & ((1u << kBits) - 1u)) << 4;
     if (CL == 1) return base[0] + off;
@@ -82,7 +87,8 @@ __device__ __forceinline__ void sst(uint32_t a, double2 v) {
 // sum over shared-|f| rows [r0, r1) of f_row * sign * conj(psi[j]) psi[i]
 // (real part; with !FR also the imaginary one); lane takes word row * 32 + lane,
 // four rows per trip with the next trip's pair words already in flight
-template <int CL, bool FR>
+// LOCAL: every slot is this CTA's (own part or chunk buffer): plain shared::cta loads
+template <int CL, bool FR, bool LOCAL>
 __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r1, int lane, const SlotMap<CL>& sm) {
   double acc = 0.0;
   if (r0 >= r1) return acc;
@@ -113,8 +119,13 @@ __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r
     double2 a[4], bb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
-      bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
+      if (LOCAL) {
+        a[u] = sld<1>(sm.laddr(w[u] & 0x7FFFu));
+        bb[u] = sld<1>(sm.laddr((w[u] >> 15) & 0x7FFFu));
+      } else {
+        a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
+        bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -127,7 +138,7 @@ __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r
 }
 
 // per-pair-f rows [r0, r1) (f at pf[(row - pp0) * 32 + lane], pp0 = the row of pf ordinal 0)
-template <int CL>
+template <int CL, bool LOCAL>
 __device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int r1, int pp0, int lane,
                                                const SlotMap<CL>& sm) {
   double acc = 0.0;
@@ -146,8 +157,13 @@ __device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int 
     double2 a[4], bb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
-      bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
+      if (LOCAL) {
+        a[u] = sld<1>(sm.laddr(w[u] & 0x7FFFu));
+        bb[u] = sld<1>(sm.laddr((w[u] >> 15) & 0x7FFFu));
+      } else {
+        a[u] = sld<CL>(sm.addr(w[u] & 0x7FFFu));
+        bb[u] = sld<CL>(sm.addr((w[u] >> 15) & 0x7FFFu));
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -162,7 +178,7 @@ __device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int 
 
 // one generator's pairs assigned to this CTA: exp(theta A) as the 2x2 rotation
 // a' = c a + g F_hi b, b' = c b + g F_lo a per pair (g = +-s by the pair's sign)
-template <int CL, int NT, bool MULTI>
+template <int CL, int NT, bool MULTI, bool LOCAL>
 __device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl, int op, uint32_t t0, uint32_t t1,
                                          uint32_t w, double2 csv, double2 flo, double2 fhi, const SlotMap<CL>& sm) {
   for (uint32_t t = t0; t < t1; t += NT) {
@@ -173,11 +189,13 @@ __device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl,
       fhi = pl.pair_f[2 * po + 1];
     }
     const double g = (w >> 30) & 1u ? -csv.y : csv.y;
-    const uint32_t pa = sm.addr(w & 0x7FFFu), pb = sm.addr((w >> 15) & 0x7FFFu);
-    const double2 a = sld<CL>(pa), bb = sld<CL>(pb);
+    constexpr int AS = LOCAL ? 1 : CL;  // address space: shared::cta or shared::cluster
+    const uint32_t pa = LOCAL ? sm.laddr(w & 0x7FFFu) : sm.addr(w & 0x7FFFu);
+    const uint32_t pb = LOCAL ? sm.laddr((w >> 15) & 0x7FFFu) : sm.addr((w >> 15) & 0x7FFFu);
+    const double2 a = sld<AS>(pa), bb = sld<AS>(pb);
     const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
-    sst<CL>(pa, make_double2(csv.x * a.x + g * hb.x, csv.x * a.y + g * hb.y));
-    sst<CL>(pb, make_double2(csv.x * bb.x + g * la.x, csv.x * bb.y + g * la.y));
+    sst<AS>(pa, make_double2(csv.x * a.x + g * hb.x, csv.x * a.y + g * hb.y));
+    sst<AS>(pb, make_double2(csv.x * bb.x + g * la.x, csv.x * bb.y + g * la.y));
   }
 }
 
@@ -207,6 +225,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
   SlotMap<CL> sm;
   {
     const uint32_t local = (uint32_t)__cvta_generic_to_shared(sm_c);
+    sm.local = local;
 #pragma unroll
     for (int r = 0; r < CL; ++r) {
       if (CL == 1) {
@@ -227,7 +246,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     const FusedDesc& d = pl.fused[pl.op_idx[op]];
     fz[2 * op] = pl.pair_f[2 * d.pair_off];
     fz[2 * op + 1] = pl.pair_f[2 * d.pair_off + 1];
-    opfl[op] = (uint8_t)(((d.x & sd.split_mask) != 0 ? 1 : 0) | (d.npair > 1 ? 2 : 0));
+    opfl[op] = (uint8_t)(sd.op_cross[op] | (d.npair > 1 ? 2 : 0));
     gse[op] = make_uint2((uint32_t)sd.gen_off[CL * op + rank], (uint32_t)sd.gen_off[CL * op + rank + 1]);
   }
   cluster.sync();
@@ -251,10 +270,13 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     const uint2 se = gse[op];
     const int fl = opfl[op];
     if (se.x + tid < se.y) {
+      // a CTA-local step (no pair across CTAs) addresses the shared::cta window
       if (fl & 2)
-        gen_pass<CL, NT, true>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+        gen_pass<CL, NT, true, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+      else if (CL == 1 || !(fl & 1))
+        gen_pass<CL, NT, false, true>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
       else
-        gen_pass<CL, NT, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+        gen_pass<CL, NT, false, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
     }
     // a generator whose flip mask avoids the split qubits only touches this
     // CTA's part: a CTA barrier suffices unless it or the next one crosses
@@ -291,11 +313,17 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
       }
       const int sh0 = es[3], shn = es[4] - es[3];
       const int a0 = sh0 + (int)((int64_t)shn * warp / NW), a1 = sh0 + (int)((int64_t)shn * (warp + 1) / NW);
-      acc += sd.f_real ? shared_rows<CL, true>(sd, a0, a1, lane, sm) : shared_rows<CL, false>(sd, a0, a1, lane, sm);
+      if (CL == 1 || sd.buf_len > 0)  // every slot is local: own part or chunk buffer
+        acc += sd.f_real ? shared_rows<CL, true, true>(sd, a0, a1, lane, sm)
+                         : shared_rows<CL, false, true>(sd, a0, a1, lane, sm);
+      else
+        acc += sd.f_real ? shared_rows<CL, true, false>(sd, a0, a1, lane, sm)
+                         : shared_rows<CL, false, false>(sd, a0, a1, lane, sm);
       const int pp0 = es[4], ppn = es[5] - es[4];
       if (ppn > 0) {
         const int b0 = pp0 + (int)((int64_t)ppn * warp / NW), b1 = pp0 + (int)((int64_t)ppn * (warp + 1) / NW);
-        acc += perpair_rows<CL>(sd, b0, b1, pp0 - es[6], lane, sm);
+        acc += CL == 1 || sd.buf_len > 0 ? perpair_rows<CL, true>(sd, b0, b1, pp0 - es[6], lane, sm)
+                                         : perpair_rows<CL, false>(sd, b0, b1, pp0 - es[6], lane, sm);
       }
     }
   }
