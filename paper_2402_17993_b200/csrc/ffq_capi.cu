@@ -380,7 +380,8 @@ bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
   return true;
 }
 
-constexpr int kSectorThreads = 1024;
+constexpr int kSectorThreads = 768;       // per CTA of a 2/4/8-CTA cluster (measured best at 18 qubits)
+constexpr int kSectorSingleThreads = 256;  // one-CTA evaluations (small closures, many CTAs per SM)
 // small closures run one CTA per evaluation (many per SM); large ones a 2^s-CTA cluster
 constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA
 constexpr uint32_t kSectorMaxSize = 32767;   // 15-bit pair indices
@@ -410,10 +411,11 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     const uint32_t max_part =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
     // closure size first (one part, no size limit on the part), then the real split
-    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1);
+    // (rows per section padded to multiples of 4)
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4);
     if (b->prog.ok && sector_parts(ctx, b->prog.size) > 1)
       b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
-                               (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)));
+                               (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)), 4);
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
@@ -493,7 +495,7 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
   if (clocks) clk.alloc(2 * (size_t)batch);
   long long* cp = clocks ? clk.p : nullptr;
   switch (sd.n_parts) {
-    case 1: launch_sector_t<1, 256>(ctx, pl, sd, theta, batch, e, im, cp); break;
+    case 1: launch_sector_t<1, kSectorSingleThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
     case 2: launch_sector_t<2, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
     case 4: launch_sector_t<4, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
     default: launch_sector_t<8, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;

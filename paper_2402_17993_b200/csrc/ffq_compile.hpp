@@ -659,7 +659,7 @@ struct SectorProgram {
 constexpr uint32_t kMinChunk = 256;
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
                                     uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2,
-                                    uint32_t cap_amps = 0xFFFFFFFFu) {
+                                    uint32_t cap_amps = 0xFFFFFFFFu, int row_quantum = 4) {
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -727,10 +727,11 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   // b = parity(k & M_b)); a pair (k, k ^ X) crosses CTAs iff some parity(X & M_b)
   // is odd. Masks are chosen greedily from single qubits and the occupied /
   // virtual / spin classes of hf (and their intersections) by a cost in
-  // cycles measured on B200: ~2000 per generator step that needs a cluster
-  // barrier instead of a CTA barrier, ~1 per cross generator pair, ~0.02 per
-  // cross expectation pair (those read a local copy of the peer chunk); every
-  // part must fit a CTA.
+  // cycles fitted to per-step clocks on B200 (18 qubits, 2 CTAs): ~600 per
+  // generator step that needs a cluster barrier instead of a CTA barrier,
+  // ~2.1 per cross generator pair (a DSMEM load and store: DSMEM moves ~20
+  // B/cycle), ~0.02 per cross expectation pair (those read a local copy of the
+  // peer chunk); every part must fit a CTA.
   auto part_of = [&](uint32_t k, const std::vector<uint64_t>& ms) {
     uint32_t r = 0;
     for (size_t b = 0; b < ms.size(); ++b) r |= (uint32_t)(__builtin_popcountll(k & ms[b]) & 1) << b;
@@ -771,8 +772,8 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       for (int op = 0; op < n_ops; ++op) {
         const bool cr = crosses(P.fused[P.op_idx[op]].x, m2);
         const bool nx = op + 1 >= n_ops || crosses(P.fused[P.op_idx[op + 1]].x, m2);
-        if (cr || nx) cost += 2000.0;
-        if (cr) cost += (double)gk[op].size();
+        if (cr || nx) cost += 600.0;
+        if (cr) cost += 2.1 * (double)gk[op].size();
       }
       for (const auto& [x, c2] : exp_by_x)
         if (crosses(x, m2)) cost += 0.02 * (double)c2;
@@ -959,6 +960,22 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
           }
         a0 = b0;
       }
+      // pad both row ranges to whole multiples of row_quantum (4 rows x warps
+      // per CTA on the device): every warp then owns whole groups of 4 rows
+      auto pad_rows = [&](std::vector<uint32_t>& words, int64_t first_row, std::vector<double>* re,
+                          std::vector<double>* im) {
+        int64_t rows = (int64_t)words.size() / 32 - first_row;
+        while (rows % row_quantum) {
+          words.insert(words.end(), 32, zpair);
+          if (re) re->insert(re->end(), 32, 0.0);
+          if (im) im->insert(im->end(), 32, 0.0);
+          ++rows;
+        }
+      };
+      pad_rows(S.row_pairs, es.sh0, nullptr, nullptr);
+      S.row_fre.resize(S.row_pairs.size() / 32, 0.0);
+      S.row_fim.resize(S.row_pairs.size() / 32, 0.0);
+      if (!pp_words.empty()) pad_rows(pp_words, 0, &pp_re, &pp_im);
       es.sh1 = (int32_t)(S.row_pairs.size() / 32);
       S.row_pairs.insert(S.row_pairs.end(), pp_words.begin(), pp_words.end());
       S.row_fre.resize(S.row_pairs.size() / 32, 0.0);

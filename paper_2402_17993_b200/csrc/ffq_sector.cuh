@@ -90,19 +90,18 @@ __device__ __forceinline__ void sst(uint32_t a, double2 v) {
 // LOCAL: every slot is this CTA's (own part or chunk buffer): plain shared::cta loads
 template <int CL, bool FR, bool LOCAL>
 __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r1, int lane, const SlotMap<CL>& sm) {
+  // r1 - r0 is a multiple of 4 (rows padded at compile time)
   double acc = 0.0;
   if (r0 >= r1) return acc;
-  const uint32_t* __restrict__ pairs = sd.row_pairs + lane;
   uint32_t wn[4];
   double fn[4], fin[4];
   auto fetch = [&](int row) {
+    const uint32_t* p = sd.row_pairs + (size_t)row * 32 + lane;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const bool ok = row + u < r1;
-      const int q = ok ? row + u : r1 - 1;
-      wn[u] = __ldg(pairs + 32 * q);
-      fn[u] = ok ? __ldg(sd.row_fre + q) : 0.0;
-      if (!FR) fin[u] = ok ? __ldg(sd.row_fim + q) : 0.0;
+      wn[u] = __ldg(p + 32 * u);
+      fn[u] = __ldg(sd.row_fre + row + u);
+      if (!FR) fin[u] = __ldg(sd.row_fim + row + u);
     }
   };
   fetch(r0);
@@ -129,9 +128,14 @@ __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double fs = (w[u] >> 30) & 1u ? -f[u] : f[u];
+      // sign bit 30 of the pair word flips f's sign bit
+      const long long sgn = (long long)((w[u] >> 30) & 1u) << 63;
+      const double fs = __longlong_as_double(__double_as_longlong(f[u]) ^ sgn);
       acc = fma(fs, fma(bb[u].x, a[u].x, bb[u].y * a[u].y), acc);
-      if (!FR) acc = fma((w[u] >> 30) & 1u ? fi[u] : -fi[u], fma(bb[u].x, a[u].y, -bb[u].y * a[u].x), acc);
+      if (!FR) {
+        const double fis = __longlong_as_double(__double_as_longlong(fi[u]) ^ sgn);
+        acc = fma(-fis, fma(bb[u].x, a[u].y, -bb[u].y * a[u].x), acc);
+      }
     }
   }
   return acc;
@@ -141,18 +145,18 @@ __device__ __forceinline__ double shared_rows(const SectorDev& sd, int r0, int r
 template <int CL, bool LOCAL>
 __device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int r1, int pp0, int lane,
                                                const SlotMap<CL>& sm) {
+  // r1 - r0 is a multiple of 4 (rows padded at compile time)
   double acc = 0.0;
   for (int row = r0; row < r1; row += 4) {
     uint32_t w[4];
     double fr[4], fi[4];
+    const uint32_t* p = sd.row_pairs + (size_t)row * 32 + lane;
+    const int64_t fo = (int64_t)(row - pp0) * 32 + lane;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const bool ok = row + u < r1;
-      const int q = ok ? row + u : r1 - 1;
-      w[u] = __ldg(sd.row_pairs + 32 * q + lane);
-      const int64_t fo = (int64_t)(q - pp0) * 32 + lane;
-      fr[u] = ok ? __ldg(sd.pf_re + fo) : 0.0;
-      fi[u] = (ok && sd.pf_im) ? __ldg(sd.pf_im + fo) : 0.0;
+      w[u] = __ldg(p + 32 * u);
+      fr[u] = __ldg(sd.pf_re + fo + 32 * u);
+      fi[u] = sd.pf_im ? __ldg(sd.pf_im + fo + 32 * u) : 0.0;
     }
     double2 a[4], bb[4];
 #pragma unroll
@@ -178,7 +182,7 @@ __device__ __forceinline__ double perpair_rows(const SectorDev& sd, int r0, int 
 
 // one generator's pairs assigned to this CTA: exp(theta A) as the 2x2 rotation
 // a' = c a + g F_hi b, b' = c b + g F_lo a per pair (g = +-s by the pair's sign)
-template <int CL, int NT, bool MULTI, bool LOCAL>
+template <int CL, int NT, bool MULTI, bool LOCAL, bool REALF = false>
 __device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl, int op, uint32_t t0, uint32_t t1,
                                          uint32_t w, double2 csv, double2 flo, double2 fhi, const SlotMap<CL>& sm) {
   for (uint32_t t = t0; t < t1; t += NT) {
@@ -188,14 +192,21 @@ __device__ __forceinline__ void gen_pass(const SectorDev& sd, const PlanDev& pl,
       flo = pl.pair_f[2 * po];
       fhi = pl.pair_f[2 * po + 1];
     }
-    const double g = (w >> 30) & 1u ? -csv.y : csv.y;
+    const bool neg = (w >> 30) & 1u;
     constexpr int AS = LOCAL ? 1 : CL;  // address space: shared::cta or shared::cluster
     const uint32_t pa = LOCAL ? sm.laddr(w & 0x7FFFu) : sm.addr(w & 0x7FFFu);
     const uint32_t pb = LOCAL ? sm.laddr((w >> 15) & 0x7FFFu) : sm.addr((w >> 15) & 0x7FFFu);
     const double2 a = sld<AS>(pa), bb = sld<AS>(pb);
-    const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
-    sst<AS>(pa, make_double2(csv.x * a.x + g * hb.x, csv.x * a.y + g * hb.y));
-    sst<AS>(pb, make_double2(csv.x * bb.x + g * la.x, csv.x * bb.y + g * la.y));
+    if (REALF) {  // F real: flo.x / fhi.x carry sin * F (sign applied here)
+      const double gh = neg ? -fhi.x : fhi.x, gl = neg ? -flo.x : flo.x;
+      sst<AS>(pa, make_double2(fma(gh, bb.x, csv.x * a.x), fma(gh, bb.y, csv.x * a.y)));
+      sst<AS>(pb, make_double2(fma(gl, a.x, csv.x * bb.x), fma(gl, a.y, csv.x * bb.y)));
+    } else {
+      const double g = neg ? -csv.y : csv.y;
+      const double2 hb = cmul(fhi, bb), la = cmul(flo, a);
+      sst<AS>(pa, make_double2(csv.x * a.x + g * hb.x, csv.x * a.y + g * hb.y));
+      sst<AS>(pb, make_double2(csv.x * bb.x + g * la.x, csv.x * bb.y + g * la.y));
+    }
   }
 }
 
@@ -246,7 +257,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     const FusedDesc& d = pl.fused[pl.op_idx[op]];
     fz[2 * op] = pl.pair_f[2 * d.pair_off];
     fz[2 * op + 1] = pl.pair_f[2 * d.pair_off + 1];
-    opfl[op] = (uint8_t)(sd.op_cross[op] | (d.npair > 1 ? 2 : 0));
+    const bool realf = d.npair == 1 && pl.pair_f[2 * d.pair_off].y == 0.0 && pl.pair_f[2 * d.pair_off + 1].y == 0.0;
+    opfl[op] = (uint8_t)(sd.op_cross[op] | (d.npair > 1 ? 2 : 0) | (realf ? 4 : 0));
     gse[op] = make_uint2((uint32_t)sd.gen_off[CL * op + rank], (uint32_t)sd.gen_off[CL * op + rank + 1]);
   }
   cluster.sync();
@@ -271,12 +283,20 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     const int fl = opfl[op];
     if (se.x + tid < se.y) {
       // a CTA-local step (no pair across CTAs) addresses the shared::cta window
-      if (fl & 2)
-        gen_pass<CL, NT, true, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
-      else if (CL == 1 || !(fl & 1))
-        gen_pass<CL, NT, false, true>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
-      else
-        gen_pass<CL, NT, false, false>(sd, pl, op, se.x + tid, se.y, w, cs[op], fz[2 * op], fz[2 * op + 1], sm);
+      const double2 csv = cs[op];
+      if (fl & 2) {
+        gen_pass<CL, NT, true, false>(sd, pl, op, se.x + tid, se.y, w, csv, fz[2 * op], fz[2 * op + 1], sm);
+      } else if (fl & 4) {  // real F (UCCSD): sin * F folded per step
+        const double2 slo = make_double2(csv.y * fz[2 * op].x, 0.0), shi = make_double2(csv.y * fz[2 * op + 1].x, 0.0);
+        if (CL == 1 || !(fl & 1))
+          gen_pass<CL, NT, false, true, true>(sd, pl, op, se.x + tid, se.y, w, csv, slo, shi, sm);
+        else
+          gen_pass<CL, NT, false, false, true>(sd, pl, op, se.x + tid, se.y, w, csv, slo, shi, sm);
+      } else if (CL == 1 || !(fl & 1)) {
+        gen_pass<CL, NT, false, true>(sd, pl, op, se.x + tid, se.y, w, csv, fz[2 * op], fz[2 * op + 1], sm);
+      } else {
+        gen_pass<CL, NT, false, false>(sd, pl, op, se.x + tid, se.y, w, csv, fz[2 * op], fz[2 * op + 1], sm);
+      }
     }
     // a generator whose flip mask avoids the split qubits only touches this
     // CTA's part: a CTA barrier suffices unless it or the next one crosses
@@ -311,17 +331,18 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
         }
         __syncthreads();
       }
-      const int sh0 = es[3], shn = es[4] - es[3];
-      const int a0 = sh0 + (int)((int64_t)shn * warp / NW), a1 = sh0 + (int)((int64_t)shn * (warp + 1) / NW);
+      // sections hold whole groups of 4 rows; warps take contiguous shares of groups
+      const int sh0 = es[3], shn = (es[4] - es[3]) / 4;
+      const int a0 = sh0 + 4 * (int)((int64_t)shn * warp / NW), a1 = sh0 + 4 * (int)((int64_t)shn * (warp + 1) / NW);
       if (CL == 1 || sd.buf_len > 0)  // every slot is local: own part or chunk buffer
         acc += sd.f_real ? shared_rows<CL, true, true>(sd, a0, a1, lane, sm)
                          : shared_rows<CL, false, true>(sd, a0, a1, lane, sm);
       else
         acc += sd.f_real ? shared_rows<CL, true, false>(sd, a0, a1, lane, sm)
                          : shared_rows<CL, false, false>(sd, a0, a1, lane, sm);
-      const int pp0 = es[4], ppn = es[5] - es[4];
+      const int pp0 = es[4], ppn = (es[5] - es[4]) / 4;
       if (ppn > 0) {
-        const int b0 = pp0 + (int)((int64_t)ppn * warp / NW), b1 = pp0 + (int)((int64_t)ppn * (warp + 1) / NW);
+        const int b0 = pp0 + 4 * (int)((int64_t)ppn * warp / NW), b1 = pp0 + 4 * (int)((int64_t)ppn * (warp + 1) / NW);
         acc += CL == 1 || sd.buf_len > 0 ? perpair_rows<CL, true>(sd, b0, b1, pp0 - es[6], lane, sm)
                                          : perpair_rows<CL, false>(sd, b0, b1, pp0 - es[6], lane, sm);
       }
