@@ -226,6 +226,8 @@ def main():
         tot_ms = float(t.item())
     e_first = e_dev.cpu().numpy().copy()
     value = world * B * args.steps / (tot_ms / 1e3)
+    # the kernel behind `value`: program statistics for its on-chip roofline
+    sector = capi.sector_info(ctx, plan, ham, P.hf)
 
     # e2e: host buffers through ffq_energy_batch (pinned staging + H2D + D2H inside)
     def step_host():
@@ -363,6 +365,22 @@ def main():
                           "config4_fmo": config4},
             "clocks": clk.summary(),
         }
+        # k_sector_eval moves no HBM data in the step (theta in, E out, pair tables
+        # L2-resident): its bound is shared memory. Algorithmic bytes per
+        # evaluation: 16 B per amplitude access, a generator pair = 2 loads + 2
+        # stores, an expectation pair = 2 loads; peak = 128 B/clk/SM x SMs x SM
+        # clock under load (the Blackwell L1/smem datapath).
+        cs = line["clocks"]
+        sm_hz = (cs.get("sm_mhz") or 1920) * 1e6
+        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        smem_bytes = 64 * sector["generator_pairs"] + 32 * sector["expectation_pairs"]
+        smem_ach = smem_bytes * value / world / 1e9
+        smem_peak = 128 * n_sm * sm_hz / 1e9
+        line["roofline_value_kernel"] = {
+            "kernel": "k_sector_eval", "bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+            "frac": smem_ach / smem_peak, "algorithmic_bytes_per_eval": smem_bytes,
+            "peak_source": "128 B/clk/SM x %d SMs x median SM clock under load" % n_sm,
+            "sector_program": sector}
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -116,6 +116,14 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
 int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
                             int batch, const double* theta_dev, double* e_dev,
                             double* imag_dev);
+/* Support-closure program that ffq_energy_batch(_device) runs for (plan, ham,
+ * hf_bits) (compiled on first use and cached): out[0] closure size |S|,
+ * out[1] CTAs per evaluation, out[2] generator pairs, out[3] expectation
+ * pairs, out[4] expectation rows of 32, out[5] generator steps ending in a
+ * cluster barrier, out[6] first split mask, out[7] peer-chunk buffer
+ * (amplitudes). FFQ_EINVAL when the closure does not fit the sector
+ * evaluator (the other paths then run) or FFQ_SECTOR=0. */
+int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
 
 /* ---- state-level operations (simulator) ------------------ */
 int ffq_state_alloc(ffq_ctx_t ctx, int n_qubits, int batch, ffq_state_t* out);

@@ -68,6 +68,7 @@ _SIGS = {
     "ffq_energy_exact": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, C.c_double, C.POINTER(C.c_double)]),
     "ffq_ham_compile_stats": (C.c_int, [C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, _i64p]),
     "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
+    "ffq_sector_info": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i64p]),
 }
 
 _lib = None
@@ -214,6 +215,17 @@ def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int
                         e_ptr, im_ptr=None):
     check(lib().ffq_energy_batch_device(ctx.h, plan.h, ham.h, hf_bits, batch, theta_ptr, e_ptr, im_ptr),
           ctx.h)
+
+
+SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expectation_pairs",
+                    "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes")
+
+
+def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:
+    """Statistics of the support-closure program energy_batch runs (ffq_sector_info)."""
+    out = np.zeros(8, np.int64)
+    check(lib().ffq_sector_info(ctx.h, plan.h, ham.h, hf_bits, out), ctx.h)
+    return dict(zip(SECTOR_INFO_KEYS, (int(v) for v in out)))
 
 
 class State:

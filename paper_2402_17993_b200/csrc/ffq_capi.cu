@@ -872,6 +872,31 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
   });
 }
 
+int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out) {
+  if (!ctx || !plan || !ham || !out) return fail(ctx, FFQ_EINVAL, "ffq_sector_info: invalid argument");
+  return guarded(ctx, [&] {
+    if (!ctx->sector) return fail(ctx, FFQ_EINVAL, "ffq_sector_info: support-closure evaluator disabled (FFQ_SECTOR=0)");
+    if (!sector_program(ctx, plan, ham, hf_bits)) {
+      const auto& b = *plan->sectors.at(std::make_pair(ham->uid, hf_bits));
+      return fail(ctx, FFQ_EINVAL, "ffq_sector_info: no support-closure program: " + b.prog.why);
+    }
+    const SectorProgram& S = plan->sectors.at(std::make_pair(ham->uid, hf_bits))->prog;
+    const int n_ops = (int)S.op_cross.size();
+    int64_t cluster_steps = 0;
+    for (int op = 0; op < n_ops; ++op)
+      cluster_steps += S.n_parts > 1 && (S.op_cross[op] || op + 1 >= n_ops || S.op_cross[op + 1]);
+    out[0] = S.size;
+    out[1] = S.n_parts;
+    out[2] = (int64_t)S.gen_pairs.size();
+    out[3] = S.exp_pair_count;
+    out[4] = (int64_t)(S.row_pairs.size() / 32);
+    out[5] = cluster_steps;
+    out[6] = S.split_masks.empty() ? 0 : (int64_t)S.split_masks[0];
+    out[7] = S.buf_len;
+    return FFQ_OK;
+  });
+}
+
 int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int batch,
                      const double* theta, double* e_out) {
   if (!ctx || !plan || !ham || batch < 0 || (batch > 0 && (!e_out || (!theta && plan->cp.n_gen > 0))))

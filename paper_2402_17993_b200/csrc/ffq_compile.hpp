@@ -647,6 +647,7 @@ struct SectorProgram {
   std::vector<ExpSection> sections;
   std::vector<int32_t> sec_off;              // [n_parts + 1]
   uint32_t hmax = 0, buf_off = 0, buf_len = 0;
+  int64_t exp_pair_count = 0;                // expectation pairs without the row padding
   std::vector<uint32_t> row_pairs;           // [n_rows * 32]
   std::vector<double> row_fre, row_fim;      // [n_rows] (0 on per-pair rows; row_fim empty if all f real)
   std::vector<double> pf_re, pf_im;          // [per-pair rows * 32] (pf_im empty if all f real)
@@ -862,6 +863,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     S.buf_len = n_parts > 1 && room >= kMinChunk ? (uint32_t)std::min<uint64_t>(room / 32 * 32, peer_max) : 0u;
   }
   const bool buffered = S.buf_len > 0;
+  S.exp_pair_count = (int64_t)ek.size();
   std::vector<uint8_t> eown(ek.size());
   {  // balance: with the chunk buffer a cross pair costs about what a local one does
     std::vector<int64_t> load((size_t)n_parts, 0);

@@ -191,3 +191,16 @@ def test_reuploaded_hamiltonian_never_hits_stale_cache(monkeypatch, oracle, env)
     plan2 = capi.Plan(c2, P.n_qubits, *P.plan_arrays())
     ham2 = capi.Hamiltonian(c2, P.n_qubits, hx, hz, hc)
     assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
+
+
+def test_sector_info_config3(ctx_default):
+    P = problems.config_problem(3, batch=1)
+    c = ctx_default
+    plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    info = capi.sector_info(c, plan, ham, P.hf)
+    # |S| = C(9,5)^2: the (5 alpha, 5 beta) sector of 9 spatial orbitals
+    assert info["closure_size"] == 15876
+    assert info["ctas_per_eval"] == 2
+    assert 0 < info["cluster_barrier_steps"] <= P.n_gen
+    assert info["expectation_rows"] * 32 >= info["expectation_pairs"] > 0
+    assert info["generator_pairs"] > 0
