@@ -342,13 +342,18 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if sector["real_amplitudes"] else "c128",
+            "dtype_note": ("complex128 semantics; psi(theta) is real for real F and real class sums, so the "
+                           "kernel holds the fp64 real parts (imaginary parts identically 0, energies equal to "
+                           "the c128 program to <= 1e-12)" if sector["real_amplitudes"] else "complex128"),
             "data": "synthetic (seeded h~N(0,1), g~N(0,0.1), theta~U(-0.1,0.1); BASELINE.json config 3)",
             "config": {"workload": "config3: 18 qubits, 10 electrons, 560 UCCSD generators, 9316-term JW "
                                    "Hamiltonian; one step = parameter-shift gradient set (1121 energy "
                                    "evaluations) per GPU",
-                       "path": "support-closure evaluator: the 15876 amplitudes reachable from |HF> in "
-                               "2-CTA cluster DSMEM (exact for every theta; see DESIGN.md)",
+                       "path": ("support-closure evaluator: the 15876 amplitudes reachable from |HF> "
+                                "(exact for every theta), " + ("real parts only, one CTA per evaluation "
+                                "(real F and class sums: psi is real; see DESIGN.md)" if sector["real_amplitudes"]
+                                else "complex, %d-CTA cluster" % sector["ctas_per_eval"])),
                        "evals_per_step_per_gpu": B, "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"replicas x{world} (independent gradient sets)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(th_host.nbytes),
@@ -365,19 +370,21 @@ def main():
                           "config4_fmo": config4},
             "clocks": clk.summary(),
         }
-        # k_sector_eval moves no HBM data in the step (theta in, E out, pair tables
-        # L2-resident): its bound is shared memory. Algorithmic bytes per
-        # evaluation: 16 B per amplitude access, a generator pair = 2 loads + 2
-        # stores, an expectation pair = 2 loads; peak = 128 B/clk/SM x SMs x SM
-        # clock under load (the Blackwell L1/smem datapath).
+        # the sector kernel moves no HBM data in the step (theta in, E out, pair
+        # tables L2-resident): its bound is shared memory. Algorithmic bytes per
+        # evaluation: one amplitude per access (16 B complex, 8 B on the
+        # real-amplitude program), a generator pair = 2 loads + 2 stores, an
+        # expectation pair = 2 loads; peak = 128 B/clk/SM x SMs x SM clock under
+        # load (the Blackwell L1/smem datapath).
         cs = line["clocks"]
         sm_hz = (cs.get("sm_mhz") or 1920) * 1e6
         n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-        smem_bytes = 64 * sector["generator_pairs"] + 32 * sector["expectation_pairs"]
+        amp_b = 8 if sector["real_amplitudes"] else 16
+        smem_bytes = amp_b * (4 * sector["generator_pairs"] + 2 * sector["expectation_pairs"])
         smem_ach = smem_bytes * value / world / 1e9
         smem_peak = 128 * n_sm * sm_hz / 1e9
         line["roofline_value_kernel"] = {
-            "kernel": "k_sector_eval", "bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+            "kernel": "k_sector_eval_real" if sector["real_amplitudes"] else "k_sector_eval", "bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
             "frac": smem_ach / smem_peak, "algorithmic_bytes_per_eval": smem_bytes,
             "peak_source": "128 B/clk/SM x %d SMs x median SM clock under load" % n_sm,
             "sector_program": sector}

@@ -72,7 +72,8 @@ int ffq_ctx_stream(ffq_ctx_t ctx, void** stream);
 /* Environment, read at ffq_ctx_create (tuning and diagnostics only; every
  * setting gives the same energies to <= 1e-12):
  *   FFQ_SECTOR (1)          support-closure evaluator first; 0 disables it
- *   FFQ_SECTOR_CL (2)       CTAs per cluster for large closures: 2, 4 or 8
+ *   FFQ_SECTOR_REAL (1)     real-amplitude one-CTA evaluator when psi is real; 0 off
+ *   FFQ_SECTOR_CL (2)       CTAs per cluster for large complex closures: 2, 4 or 8
  *   FFQ_SMEM_MAX_QUBITS (13) largest state held whole in one CTA's smem
  *   FFQ_SUPPORT (1)         support-bitmap passes on the global-memory path
  *   FFQ_TILE_BITS (12)      expectation tile width of the global path
@@ -121,8 +122,10 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
  * out[1] CTAs per evaluation, out[2] generator pairs, out[3] expectation
  * pairs, out[4] expectation rows of 32, out[5] generator steps ending in a
  * cluster barrier, out[6] first split mask, out[7] peer-chunk buffer
- * (amplitudes). FFQ_EINVAL when the closure does not fit the sector
- * evaluator (the other paths then run) or FFQ_SECTOR=0. */
+ * (amplitudes), out[8] 1 when the program stores real amplitudes only (real F
+ * on every generator and real class sums: psi(theta) is real for every theta).
+ * FFQ_EINVAL when the closure does not fit the sector evaluator (the other
+ * paths then run) or FFQ_SECTOR=0. */
 int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
 
 /* ---- state-level operations (simulator) ------------------ */

@@ -218,12 +218,13 @@ def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int
 
 
 SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expectation_pairs",
-                    "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes")
+                    "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
+                    "real_amplitudes")
 
 
 def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:
     """Statistics of the support-closure program energy_batch runs (ffq_sector_info)."""
-    out = np.zeros(8, np.int64)
+    out = np.zeros(9, np.int64)
     check(lib().ffq_sector_info(ctx.h, plan.h, ham.h, hf_bits, out), ctx.h)
     return dict(zip(SECTOR_INFO_KEYS, (int(v) for v in out)))
 

@@ -94,6 +94,7 @@ struct ffq_ctx_s {
   int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
   int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
+  int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
@@ -135,6 +136,7 @@ struct ffq_plan_s {
     DevBuf<int32_t> secs;
     DevBuf<uint8_t> gen_flags, op_cross;
     DevBuf<double> row_fre, row_fim, pf_re, pf_im;
+    bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
   PlanDev dev() const {
@@ -382,6 +384,7 @@ bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
 
 constexpr int kSectorThreads = 768;       // per CTA of a 2/4/8-CTA cluster (measured best at 18 qubits)
 constexpr int kSectorSingleThreads = 256;  // one-CTA evaluations (small closures, many CTAs per SM)
+constexpr int kSectorRealThreads = 1024;   // one-CTA real-amplitude evaluations of large closures
 // small closures run one CTA per evaluation (many per SM); large ones a 2^s-CTA cluster
 constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA
 constexpr uint32_t kSectorMaxSize = 32767;   // 15-bit pair indices
@@ -402,6 +405,29 @@ size_t sector_smem_bytes(size_t hmax, size_t n_ops, size_t buf_len = 0) {
   return (hmax + 1) * sizeof(double2) + std::max(tables, buf_len * sizeof(double2)) + 16;
 }
 
+// k_sector_eval_real's dynamic smem: size + 1 real amplitudes, then (cos, sin),
+// (sin F_lo, sin F_hi) and the pair range per op
+size_t sector_real_smem_bytes(size_t size, size_t n_ops) {
+  return (((size + 1) * sizeof(double) + 15) & ~(size_t)15) + n_ops * (2 * sizeof(double2) + sizeof(uint2)) + 16;
+}
+
+// every fused op with one pattern pair and real F (UCCSD: F = +-1)
+bool plan_is_real(const CompiledPlan& P) {
+  if (P.n_string_ops() > 0) return false;
+  for (size_t op = 0; op < P.op_kind.size(); ++op) {
+    const FusedDesc& d = P.fused[P.op_idx[op]];
+    if (d.npair != 1 || P.pair_f[4 * d.pair_off + 1] != 0.0 || P.pair_f[4 * d.pair_off + 3] != 0.0) return false;
+  }
+  return true;
+}
+
+// every class sum real, so every pair's f(m) is real
+bool ham_is_real(const CompiledHam& H) {
+  for (size_t i = 1; i < H.cls_f.size(); i += 2)
+    if (H.cls_f[i] != 0.0) return false;
+  return true;
+}
+
 const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
   auto key = std::make_pair(h->uid, hf);
   auto it = pl->sectors.find(key);
@@ -410,10 +436,15 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     const size_t tables = sector_smem_bytes(0, pl->cp.op_kind.size());
     const uint32_t max_part =
         ctx->smem_optin > tables ? (uint32_t)((ctx->smem_optin - tables) / sizeof(double2)) : 0u;
-    // closure size first (one part, no size limit on the part), then the real split
-    // (rows per section padded to multiples of 4)
-    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4);
-    if (b->prog.ok && sector_parts(ctx, b->prog.size) > 1)
+    // real amplitudes for every theta (see k_sector_eval_real): real F on every
+    // generator, real class sums, basis-state start
+    const bool real_ok = ctx->sector_real && plan_is_real(pl->cp) && ham_is_real(h->ch);
+    // closure size first (one part, no size limit on the part), then either the
+    // one-CTA real program or the cluster split (rows padded to multiples of 4)
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, real_ok ? 8 : 16);
+    b->real = b->prog.ok && real_ok &&
+              sector_real_smem_bytes(b->prog.size, pl->cp.op_kind.size()) <= ctx->smem_optin;
+    if (b->prog.ok && !b->real && sector_parts(ctx, b->prog.size) > 1)
       b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
                                (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)), 4);
     if (b->prog.ok) {
@@ -461,6 +492,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.pf_re = b.pf_re.p;
   sd.pf_im = b.prog.f_real ? nullptr : b.pf_im.p;
   sd.n_parts = b.prog.n_parts;
+  sd.real = b.real ? 1 : 0;
   return &sd;
 }
 
@@ -488,13 +520,28 @@ void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, c
   ctx->launches++;
 }
 
+template <int NT>
+void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
+                        double* e, double* im, long long* clk) {
+  const size_t sb = sector_real_smem_bytes(sd.size, pl->cp.op_kind.size());
+  CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  k_sector_eval_real<NT><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
 void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
                    double* e, double* im) {
   static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
   DevBuf<long long> clk;
   if (clocks) clk.alloc(2 * (size_t)batch);
   long long* cp = clocks ? clk.p : nullptr;
-  switch (sd.n_parts) {
+  if (sd.real) {
+    if (sd.size <= kSectorSingleMax)
+      launch_sector_real<kSectorSingleThreads>(ctx, pl, sd, theta, batch, e, im, cp);
+    else
+      launch_sector_real<kSectorRealThreads>(ctx, pl, sd, theta, batch, e, im, cp);
+  } else switch (sd.n_parts) {
     case 1: launch_sector_t<1, kSectorSingleThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
     case 2: launch_sector_t<2, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
     case 4: launch_sector_t<4, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
@@ -719,6 +766,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_SECTOR")) c->sector = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
+    if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);
       c->sector_cl = (v == 4 || v == 8) ? v : 2;
@@ -880,11 +928,13 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
       const auto& b = *plan->sectors.at(std::make_pair(ham->uid, hf_bits));
       return fail(ctx, FFQ_EINVAL, "ffq_sector_info: no support-closure program: " + b.prog.why);
     }
-    const SectorProgram& S = plan->sectors.at(std::make_pair(ham->uid, hf_bits))->prog;
+    const auto& bufs = *plan->sectors.at(std::make_pair(ham->uid, hf_bits));
+    const SectorProgram& S = bufs.prog;
     const int n_ops = (int)S.op_cross.size();
     int64_t cluster_steps = 0;
     for (int op = 0; op < n_ops; ++op)
       cluster_steps += S.n_parts > 1 && (S.op_cross[op] || op + 1 >= n_ops || S.op_cross[op + 1]);
+    if (S.n_parts == 1) cluster_steps = 0;
     out[0] = S.size;
     out[1] = S.n_parts;
     out[2] = (int64_t)S.gen_pairs.size();
@@ -893,6 +943,7 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
     out[5] = cluster_steps;
     out[6] = S.split_masks.empty() ? 0 : (int64_t)S.split_masks[0];
     out[7] = S.buf_len;
+    out[8] = bufs.real ? 1 : 0;
     return FFQ_OK;
   });
 }

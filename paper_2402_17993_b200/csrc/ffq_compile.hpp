@@ -561,44 +561,55 @@ namespace ffq {
 //    precomputed per pair and deduplicated into a table.
 constexpr size_t kSegChunk = 512;
 
-// Shared-memory bank order for a list of pairs. A warp's 16-byte loads of
-// psi[i] (and of psi[j]) are served one quarter-warp per wavefront when the 8
-// lanes of each quarter hit distinct 16-byte bank groups, i.e. distinct
-// (slot & 7). ri[t], rj[t] are those residues for pair t; the returned order
-// packs the list into octets whose ri and rj are both all-distinct wherever the
-// residue histogram allows (largest bucket first), the rest fill in as they come.
-inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const std::vector<uint8_t>& rj) {
+// Shared-memory bank order for a list of pairs. A warp's loads of psi[i] (and
+// of psi[j]) are served conflict-free when each group of G lanes served by one
+// wavefront hits G distinct bank slots: G = 8 lanes x 16 B (complex amplitudes)
+// or G = 16 lanes x 8 B (real amplitudes), slot = index mod G. ri[t], rj[t] are
+// those residues for pair t; the returned order packs the list into groups of G
+// whose ri and rj are both all-distinct wherever the residue histogram allows
+// (rows with most pairs left first, each taking the largest free column); the
+// rest fill in as they come.
+inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const std::vector<uint8_t>& rj,
+                                        int G = 8) {
   const size_t n = ri.size();
-  std::vector<uint32_t> bucket[64];
-  for (size_t t = n; t-- > 0;) bucket[ri[t] * 8 + rj[t]].push_back((uint32_t)t);  // pop_back -> ascending t
+  std::vector<std::vector<uint32_t>> bucket((size_t)G * G);
+  std::vector<int64_t> row_left((size_t)G, 0);
+  for (size_t t = n; t-- > 0;) {  // pop_back -> ascending t
+    bucket[(size_t)ri[t] * G + rj[t]].push_back((uint32_t)t);
+    ++row_left[ri[t]];
+  }
   std::vector<uint32_t> out;
   out.reserve(n);
   size_t left = n;
+  std::vector<int> rows((size_t)G);
+  auto take = [&](int b) {
+    out.push_back(bucket[b].back());
+    bucket[b].pop_back();
+    --row_left[b / G];
+    --left;
+  };
   while (left > 0) {
-    unsigned used_i = 0, used_j = 0;
+    for (int r = 0; r < G; ++r) rows[r] = r;
+    std::sort(rows.begin(), rows.end(), [&](int x, int y) { return row_left[x] > row_left[y]; });
+    uint32_t used_j = 0;
     int taken = 0;
-    for (; taken < 8 && left > 0; ++taken) {
+    for (int r : rows) {
+      if (row_left[r] == 0) continue;
       int best = -1;
-      size_t best_n = 0;
-      for (int r = 0; r < 8; ++r) {
-        if ((used_i >> r) & 1u) continue;
-        for (int c = 0; c < 8; ++c)
-          if (!((used_j >> c) & 1u) && bucket[r * 8 + c].size() > best_n) { best = r * 8 + c; best_n = bucket[best].size(); }
-      }
-      if (best < 0) break;
-      out.push_back(bucket[best].back());
-      bucket[best].pop_back();
-      used_i |= 1u << (best >> 3);
-      used_j |= 1u << (best & 7);
-      --left;
+      for (int c = 0; c < G; ++c)
+        if (!((used_j >> c) & 1u) && !bucket[(size_t)r * G + c].empty() &&
+            (best < 0 || bucket[(size_t)r * G + c].size() > bucket[(size_t)r * G + best].size()))
+          best = c;
+      if (best < 0) continue;
+      take(r * G + best);
+      used_j |= 1u << best;
+      ++taken;
     }
-    for (; taken < 8 && left > 0; ++taken) {  // no conflict-free member left: largest bucket
+    for (; taken < G && left > 0; ++taken) {  // no conflict-free member left: largest bucket
       int best = 0;
-      for (int b = 1; b < 64; ++b)
+      for (int b = 1; b < G * G; ++b)
         if (bucket[b].size() > bucket[best].size()) best = b;
-      out.push_back(bucket[best].back());
-      bucket[best].pop_back();
-      --left;
+      take(best);
     }
   }
   return out;
@@ -660,7 +671,10 @@ struct SectorProgram {
 constexpr uint32_t kMinChunk = 256;
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
                                     uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2,
-                                    uint32_t cap_amps = 0xFFFFFFFFu, int row_quantum = 4) {
+                                    uint32_t cap_amps = 0xFFFFFFFFu, int row_quantum = 4,
+                                    int elem_bytes = 16) {
+  // lanes per conflict-free shared-memory wavefront for this amplitude size
+  const int bank_group = elem_bytes == 8 ? 16 : 8;
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -812,7 +826,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   };
   S.hf_slot = slot(S.hf_idx);
   // 16-byte bank group of S[i] within its CTA's amplitude array
-  auto bank_slot = [&](uint32_t i) { return (uint8_t)((i - S.part_start[owner(i)]) & 7u); };
+  auto bank_slot = [&](uint32_t i) { return (uint8_t)((i - S.part_start[owner(i)]) & (uint32_t)(bank_group - 1)); };
   // a local pair stays with its CTA; a cross pair goes to the lighter of its two CTAs
   auto assign = [&](uint32_t i, uint32_t j, std::vector<int64_t>& load) {
     const int oi = owner(i), oj = owner(j);
@@ -841,7 +855,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         ri.push_back(bank_slot(pi.back()));
         rj.push_back(bank_slot(pj.back()));
       }
-      for (uint32_t t : bank_order(ri, rj)) {  // thread tid takes pair off + tid
+      for (uint32_t t : bank_order(ri, rj, bank_group)) {  // thread tid takes pair off + tid
         S.gen_pairs.push_back(slot(pi[t]) | (slot(pj[t]) << 15) | ((uint32_t)(fl[t] & 1u) << 30));
         S.gen_flags.push_back(fl[t]);
       }
@@ -925,10 +939,10 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
           const uint32_t i = (uint32_t)idx[e.m], j = (uint32_t)idx[e.m ^ (uint32_t)H.groups[e.g].x];
           si.push_back(enc(i, key));
           sj.push_back(enc(j, key));
-          ri.push_back((uint8_t)(si.back() & 7u));
-          rj.push_back((uint8_t)(sj.back() & 7u));
+          ri.push_back((uint8_t)(si.back() & (uint32_t)(bank_group - 1)));
+          rj.push_back((uint8_t)(sj.back() & (uint32_t)(bank_group - 1)));
         }
-        const std::vector<uint32_t> order = bank_order(ri, rj);
+        const std::vector<uint32_t> order = bank_order(ri, rj, bank_group);
         const double fr0 = ek[list[a0]].fr, fi0 = ek[list[a0]].fi;
         bool shared = true;
         for (size_t u = a0; u < b0; ++u) {

@@ -28,6 +28,7 @@ struct SectorDev {
   uint32_t size, hf_slot;
   uint32_t part_start[kSectorMaxParts + 1];  // CTA r holds S[part_start[r], part_start[r + 1])
   int n_ops, n_parts, f_real;
+  int real;                     // 1: real-amplitude program (k_sector_eval_real)
   const uint8_t* op_cross;      // [n_ops] 1: the generator has pairs across CTAs (cluster barrier)
   const int64_t* gen_off;       // [CL * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;    // slot_i | slot_j << 15 | sign << 30
@@ -363,6 +364,140 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
     e_out[row] = e;
     if (im_out) im_out[row] = 0.0;
     if (phase_clk) {  // diagnostics (FFQ_PHASE_CLOCKS): generator / expectation cycles
+      phase_clk[2 * row] = clk1 - clk0;
+      phase_clk[2 * row + 1] = clock64() - clk1;
+    }
+  }
+}
+
+
+// ---- real-amplitude evaluator ----------------------------------------------
+// When every fused generator has real F (UCCSD: F = +-1), every Hamiltonian
+// class sum is real and |hf> is a basis state, psi(theta) is real for every
+// theta: each step is a real 2x2 rotation and the start is real. The
+// imaginary parts are then identically zero, and the complex kernel's
+// arithmetic on the real parts is exactly the sequence below (fma(g, b, c a)
+// per member, fma(f, b a, acc) per pair), so this kernel stores the real parts
+// only: 8 B per amplitude, the 18-qubit closure (15 876 amplitudes, 127 KB)
+// in ONE CTA's shared memory -- no cluster, no DSMEM, CTA barriers only.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
+                                                            const double* __restrict__ theta, int theta_stride,
+                                                            double* __restrict__ e_out, double* __restrict__ im_out,
+                                                            int n_rows, long long* __restrict__ phase_clk) {
+  // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
+  // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  __shared__ double2 red[NT / 32];
+  const long long clk0 = clock64();
+  const int row = blockIdx.x;
+  if (row >= n_rows) return;
+  const uint32_t na = sd.size + 1;
+  double* amp = reinterpret_cast<double*>(sm_raw);
+  double2* cs = reinterpret_cast<double2*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
+  double2* fz = cs + pl.n_ops;
+  uint2* gse = reinterpret_cast<uint2*>(fz + pl.n_ops);
+  for (uint32_t i = threadIdx.x; i < na; i += NT) amp[i] = 0.0;
+  for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
+    const double phi = theta[(int64_t)row * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
+    double sv, cv;
+    sincos(phi, &sv, &cv);
+    const double sn = sv * pl.op_sscale[op];
+    const FusedDesc& d = pl.fused[pl.op_idx[op]];
+    cs[op] = make_double2(cv, sn);
+    fz[op] = make_double2(sn * pl.pair_f[2 * d.pair_off].x, sn * pl.pair_f[2 * d.pair_off + 1].x);
+    gse[op] = make_uint2((uint32_t)sd.gen_off[op], (uint32_t)sd.gen_off[op + 1]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) amp[sd.hf_slot] = 1.0;
+  __syncthreads();
+  const uint32_t tid = threadIdx.x;
+  auto first_word = [&](int op) -> uint32_t {
+    const uint2 se = gse[op];
+    return se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u;
+  };
+  uint32_t w0 = sd.n_ops > 0 ? first_word(0) : 0u, w1 = sd.n_ops > 1 ? first_word(1) : 0u;
+  for (int op = 0; op < sd.n_ops; ++op) {
+    uint32_t w = w0;
+    w0 = w1;
+    w1 = op + 2 < sd.n_ops ? first_word(op + 2) : 0u;
+    const uint2 se = gse[op];
+    if (se.x + tid < se.y) {
+      const double c = cs[op].x;
+      const double2 sf = fz[op];
+      for (uint32_t t = se.x + tid; t < se.y; t += NT) {
+        if (t != se.x + tid) w = __ldg(sd.gen_pairs + t);
+        const bool neg = (w >> 30) & 1u;
+        const uint32_t i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
+        const double a = amp[i], b = amp[j];
+        const double gh = neg ? -sf.y : sf.y, gl = neg ? -sf.x : sf.x;
+        amp[i] = fma(gh, b, c * a);
+        amp[j] = fma(gl, a, c * b);
+      }
+    }
+    __syncthreads();
+  }
+  const long long clk1 = clock64();
+  double acc = 0.0;
+  {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t* es = sd.secs;  // one section: every pair is local
+    const int sh0 = es[3], shn = (es[4] - es[3]) / 4;
+    const int r0 = sh0 + 4 * (int)((int64_t)shn * warp / NW), r1 = sh0 + 4 * (int)((int64_t)shn * (warp + 1) / NW);
+    if (r0 < r1) {
+      uint32_t wn[4];
+      double fn[4];
+      auto fetch = [&](int rw) {
+        const uint32_t* p = sd.row_pairs + (size_t)rw * 32 + lane;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wn[u] = __ldg(p + 32 * u);
+          fn[u] = __ldg(sd.row_fre + rw + u);
+        }
+      };
+      fetch(r0);
+      for (int rw = r0; rw < r1; rw += 4) {
+        uint32_t w[4];
+        double f[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          w[u] = wn[u];
+          f[u] = fn[u];
+        }
+        if (rw + 4 < r1) fetch(rw + 4);
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = amp[w[u] & 0x7FFFu];
+          b[u] = amp[(w[u] >> 15) & 0x7FFFu];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long sgn = (long long)((w[u] >> 30) & 1u) << 63;
+          const double fs = __longlong_as_double(__double_as_longlong(f[u]) ^ sgn);
+          acc = fma(fs, b[u] * a[u], acc);
+        }
+      }
+    }
+    const int pp0 = es[4], ppn = (es[5] - es[4]) / 4;
+    const int q0 = pp0 + 4 * (int)((int64_t)ppn * warp / NW), q1 = pp0 + 4 * (int)((int64_t)ppn * (warp + 1) / NW);
+    for (int rw = q0; rw < q1; rw += 4) {
+      const uint32_t* p = sd.row_pairs + (size_t)rw * 32 + lane;
+      const int64_t fo = (int64_t)(rw - pp0 + es[6]) * 32 + lane;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t w = __ldg(p + 32 * u);
+        const double fr = __ldg(sd.pf_re + fo + 32 * u);
+        acc = fma(amp[(w >> 15) & 0x7FFFu] * amp[w & 0x7FFFu], fr, acc);
+      }
+    }
+  }
+  const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
+  if (threadIdx.x == 0) {
+    e_out[row] = tot.x;
+    if (im_out) im_out[row] = 0.0;
+    if (phase_clk) {
       phase_clk[2 * row] = clk1 - clk0;
       phase_clk[2 * row + 1] = clock64() - clk1;
     }

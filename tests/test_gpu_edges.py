@@ -22,7 +22,7 @@ PATHS = {
 
 
 def _ctx(monkeypatch, env):
-    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST", "FFQ_SECTOR", "FFQ_SECTOR_CL"):
+    for k in ("FFQ_SMEM_MAX_QUBITS", "FFQ_SUPPORT", "FFQ_PERSIST", "FFQ_SECTOR", "FFQ_SECTOR_CL", "FFQ_SECTOR_REAL"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -152,7 +152,7 @@ def test_sector_cluster_sizes_agree(monkeypatch, cl):
     P = problems.config_problem(3, batch=3)
     e = {}
     for k in ("2", cl):
-        c = _ctx(monkeypatch, {"FFQ_SECTOR_CL": k})
+        c = _ctx(monkeypatch, {"FFQ_SECTOR_CL": k, "FFQ_SECTOR_REAL": "0"})
         plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
         e[k] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
     assert np.abs(e[cl] - e["2"]).max() <= 1e-12
@@ -193,14 +193,55 @@ def test_reuploaded_hamiltonian_never_hits_stale_cache(monkeypatch, oracle, env)
     assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
 
 
-def test_sector_info_config3(ctx_default):
+@pytest.mark.parametrize("real", ["1", "0"])
+def test_sector_info_config3(monkeypatch, real):
     P = problems.config_problem(3, batch=1)
-    c = ctx_default
+    c = _ctx(monkeypatch, {"FFQ_SECTOR_REAL": real})
     plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
     info = capi.sector_info(c, plan, ham, P.hf)
     # |S| = C(9,5)^2: the (5 alpha, 5 beta) sector of 9 spatial orbitals
     assert info["closure_size"] == 15876
-    assert info["ctas_per_eval"] == 2
-    assert 0 < info["cluster_barrier_steps"] <= P.n_gen
+    assert info["real_amplitudes"] == int(real)  # UCCSD F = +-1, real integrals
+    assert info["ctas_per_eval"] == (1 if real == "1" else 2)
+    assert (info["cluster_barrier_steps"] == 0) == (real == "1")
+    assert info["cluster_barrier_steps"] <= P.n_gen
     assert info["expectation_rows"] * 32 >= info["expectation_pairs"] > 0
     assert info["generator_pairs"] > 0
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_real_amplitude_kernel_matches_complex(monkeypatch, oracle, config):
+    # real F, real class sums, basis start: psi is real and the one-CTA
+    # real-amplitude program must agree with the complex cluster program
+    P = problems.config_problem(config, batch=6)
+    out = {}
+    for real in ("1", "0"):
+        c = _ctx(monkeypatch, {"FFQ_SECTOR_REAL": real})
+        plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        assert capi.sector_info(c, plan, ham, P.hf)["real_amplitudes"] == int(real)
+        out[real] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    assert np.abs(out["1"] - out["0"]).max() <= 1e-12
+    kind, idx = oracle.build_generators(P.n_qubits, P.n_elec)
+    x, z, co = P.ham_arrays()
+    hs = oracle.PauliSum.from_terms(P.n_qubits, x, z, co)
+    for b in range(2):
+        ref, _ = oracle.energy_trotter(P.n_qubits, P.n_elec, kind, idx, np.array(P.plan.order, np.int32),
+                                       P.thetas[b], hs)
+        assert abs(out["1"][b] - ref) <= 1e-10
+
+
+def test_complex_hamiltonian_takes_complex_program(monkeypatch):
+    # a Hamiltonian with a non-real class sum (an XY-type string with real
+    # coefficient gives an imaginary f) must not take the real-amplitude program
+    P = problems.config_problem(2, batch=2)
+    x, z, co = P.ham_arrays()
+    x2 = np.concatenate([x, np.array([0b11], np.uint64)])
+    z2 = np.concatenate([z, np.array([0b01], np.uint64)])  # Y0 X1
+    c2 = np.concatenate([co, np.array([0.05])])
+    c = _ctx(monkeypatch, {})
+    plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, x2, z2, c2)
+    assert capi.sector_info(c, plan, ham, P.hf)["real_amplitudes"] == 0
+    e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+    c0 = _ctx(monkeypatch, {"FFQ_SECTOR": "0"})
+    plan0, ham0 = capi.Plan(c0, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c0, P.n_qubits, x2, z2, c2)
+    assert np.abs(e - capi.energy_batch(c0, plan0, ham0, P.hf, P.plan_thetas())).max() <= 1e-12
