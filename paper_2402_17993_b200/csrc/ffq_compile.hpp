@@ -19,6 +19,7 @@
 #include <complex>
 #include <cstring>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -573,42 +574,65 @@ inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const st
                                         int G = 8) {
   const size_t n = ri.size();
   std::vector<std::vector<uint32_t>> bucket((size_t)G * G);
-  std::vector<int64_t> row_left((size_t)G, 0);
-  for (size_t t = n; t-- > 0;) {  // pop_back -> ascending t
-    bucket[(size_t)ri[t] * G + rj[t]].push_back((uint32_t)t);
-    ++row_left[ri[t]];
-  }
+  for (size_t t = n; t-- > 0;) bucket[(size_t)ri[t] * G + rj[t]].push_back((uint32_t)t);  // pop_back -> ascending t
   std::vector<uint32_t> out;
   out.reserve(n);
   size_t left = n;
-  std::vector<int> rows((size_t)G);
   auto take = [&](int b) {
     out.push_back(bucket[b].back());
     bucket[b].pop_back();
-    --row_left[b / G];
     --left;
   };
-  while (left > 0) {
-    for (int r = 0; r < G; ++r) rows[r] = r;
-    std::sort(rows.begin(), rows.end(), [&](int x, int y) { return row_left[x] > row_left[y]; });
-    uint32_t used_j = 0;
-    int taken = 0;
-    for (int r : rows) {
-      if (row_left[r] == 0) continue;
-      int best = -1;
-      for (int c = 0; c < G; ++c)
-        if (!((used_j >> c) & 1u) && !bucket[(size_t)r * G + c].empty() &&
-            (best < 0 || bucket[(size_t)r * G + c].size() > bucket[(size_t)r * G + best].size()))
-          best = c;
-      if (best < 0) continue;
-      take(r * G + best);
-      used_j |= 1u << best;
-      ++taken;
+  // each group: a maximum matching rows (ri) -> columns (rj) over non-empty
+  // buckets (Kuhn's augmenting paths, larger buckets tried first)
+  std::vector<int> match_col((size_t)G), match_row((size_t)G);
+  std::vector<int> order((size_t)G * G);
+  std::vector<char> seen((size_t)G);
+  std::function<bool(int)> augment = [&](int r) {
+    for (int k = 0; k < G; ++k) {
+      const int c = order[(size_t)r * G + k];
+      if (c < 0 || seen[c]) continue;
+      seen[c] = 1;
+      if (match_col[c] < 0 || augment(match_col[c])) {
+        match_col[c] = r;
+        match_row[r] = c;
+        return true;
+      }
     }
+    return false;
+  };
+  while (left > 0) {
+    for (int r = 0; r < G; ++r) {
+      std::vector<std::pair<size_t, int>> cs;
+      for (int c = 0; c < G; ++c)
+        if (!bucket[(size_t)r * G + c].empty()) cs.push_back({bucket[(size_t)r * G + c].size(), c});
+      std::sort(cs.begin(), cs.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (int k = 0; k < G; ++k) order[(size_t)r * G + k] = k < (int)cs.size() ? cs[k].second : -1;
+    }
+    std::fill(match_col.begin(), match_col.end(), -1);
+    std::fill(match_row.begin(), match_row.end(), -1);
+    // rows with the most pairs left first
+    std::vector<std::pair<size_t, int>> rows;
+    for (int r = 0; r < G; ++r) {
+      size_t tot = 0;
+      for (int c = 0; c < G; ++c) tot += bucket[(size_t)r * G + c].size();
+      if (tot) rows.push_back({tot, r});
+    }
+    std::sort(rows.begin(), rows.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (const auto& rr : rows) {
+      std::fill(seen.begin(), seen.end(), 0);
+      augment(rr.second);
+    }
+    int taken = 0;
+    for (int r = 0; r < G; ++r)
+      if (match_row[r] >= 0) {
+        take(r * G + match_row[r]);
+        ++taken;
+      }
     for (; taken < G && left > 0; ++taken) {  // no conflict-free member left: largest bucket
       int best = 0;
-      for (int b = 1; b < G * G; ++b)
-        if (bucket[b].size() > bucket[best].size()) best = b;
+      for (int b2 = 1; b2 < G * G; ++b2)
+        if (bucket[b2].size() > bucket[best].size()) best = b2;
       take(best);
     }
   }

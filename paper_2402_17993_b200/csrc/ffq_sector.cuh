@@ -412,21 +412,26 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   if (threadIdx.x == 0) amp[sd.hf_slot] = 1.0;
   __syncthreads();
   const uint32_t tid = threadIdx.x;
-  auto first_word = [&](int op) -> uint32_t {
+  // each thread's first two pair words of the next two ops are in flight
+  // across the barriers (steps have up to ~2 NT pairs)
+  auto first_words = [&](int op) -> uint2 {
     const uint2 se = gse[op];
-    return se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u;
+    return make_uint2(se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u,
+                      se.x + tid + NT < se.y ? __ldg(sd.gen_pairs + se.x + tid + NT) : 0u);
   };
-  uint32_t w0 = sd.n_ops > 0 ? first_word(0) : 0u, w1 = sd.n_ops > 1 ? first_word(1) : 0u;
+  const uint2 z2 = make_uint2(0u, 0u);
+  uint2 w0 = sd.n_ops > 0 ? first_words(0) : z2, w1 = sd.n_ops > 1 ? first_words(1) : z2;
   for (int op = 0; op < sd.n_ops; ++op) {
-    uint32_t w = w0;
+    const uint2 ww = w0;
     w0 = w1;
-    w1 = op + 2 < sd.n_ops ? first_word(op + 2) : 0u;
+    w1 = op + 2 < sd.n_ops ? first_words(op + 2) : z2;
     const uint2 se = gse[op];
     if (se.x + tid < se.y) {
       const double c = cs[op].x;
       const double2 sf = fz[op];
       for (uint32_t t = se.x + tid; t < se.y; t += NT) {
-        if (t != se.x + tid) w = __ldg(sd.gen_pairs + t);
+        const uint32_t k = (t - se.x - tid) / NT;
+        const uint32_t w = k == 0 ? ww.x : (k == 1 ? ww.y : __ldg(sd.gen_pairs + t));
         const bool neg = (w >> 30) & 1u;
         const uint32_t i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
         const double a = amp[i], b = amp[j];
