@@ -456,10 +456,14 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       auto fetch = [&](int rw) {
         const uint32_t* p = sd.row_pairs + (size_t)rw * 32 + lane;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          wn[u] = __ldg(p + 32 * u);
-          fn[u] = __ldg(sd.row_fre + rw + u);
-        }
+        for (int u = 0; u < 4; ++u) wn[u] = __ldg(p + 32 * u);
+        // rw is a multiple of 4: the four f of a trip are two aligned 16-B loads
+        const double2 f01 = __ldg(reinterpret_cast<const double2*>(sd.row_fre + rw));
+        const double2 f23 = __ldg(reinterpret_cast<const double2*>(sd.row_fre + rw) + 1);
+        fn[0] = f01.x;
+        fn[1] = f01.y;
+        fn[2] = f23.x;
+        fn[3] = f23.y;
       };
       fetch(r0);
       for (int rw = r0; rw < r1; rw += 4) {
