@@ -429,15 +429,21 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     if (se.x + tid < se.y) {
       const double c = cs[op].x;
       const double2 sf = fz[op];
-      for (uint32_t t = se.x + tid; t < se.y; t += NT) {
-        const uint32_t k = (t - se.x - tid) / NT;
-        const uint32_t w = k == 0 ? ww.x : (k == 1 ? ww.y : __ldg(sd.gen_pairs + t));
-        const bool neg = (w >> 30) & 1u;
+      // one pair: sign bit 30 of the word flips sin F (an XOR on the high word)
+      auto rot = [&](uint32_t w) {
+        const unsigned sg = ((w >> 30) & 1u) << 31;
+        const double gh = __hiloint2double((int)((unsigned)__double2hiint(sf.y) ^ sg), __double2loint(sf.y));
+        const double gl = __hiloint2double((int)((unsigned)__double2hiint(sf.x) ^ sg), __double2loint(sf.x));
         const uint32_t i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
         const double a = amp[i], b = amp[j];
-        const double gh = neg ? -sf.y : sf.y, gl = neg ? -sf.x : sf.x;
         amp[i] = fma(gh, b, c * a);
         amp[j] = fma(gl, a, c * b);
+      };
+      rot(ww.x);
+      const uint32_t t1 = se.x + tid + NT;
+      if (t1 < se.y) {
+        rot(ww.y);
+        for (uint32_t t = t1 + NT; t < se.y; t += NT) rot(__ldg(sd.gen_pairs + t));
       }
     }
     __syncthreads();
