@@ -412,19 +412,17 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   if (threadIdx.x == 0) amp[sd.hf_slot] = 1.0;
   __syncthreads();
   const uint32_t tid = threadIdx.x;
-  // each thread's first two pair words of the next two ops are in flight
-  // across the barriers (steps have up to ~2 NT pairs)
+  // each thread's first two pair words of the next three steps are in flight
+  // across the barriers (steps have up to ~2 NT pairs). The step loop is
+  // unrolled by three so the in-flight registers are never copied (a copy
+  // would wait for the load).
   auto first_words = [&](int op) -> uint2 {
+    if (op >= sd.n_ops) return make_uint2(0u, 0u);
     const uint2 se = gse[op];
     return make_uint2(se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u,
                       se.x + tid + NT < se.y ? __ldg(sd.gen_pairs + se.x + tid + NT) : 0u);
   };
-  const uint2 z2 = make_uint2(0u, 0u);
-  uint2 w0 = sd.n_ops > 0 ? first_words(0) : z2, w1 = sd.n_ops > 1 ? first_words(1) : z2;
-  for (int op = 0; op < sd.n_ops; ++op) {
-    const uint2 ww = w0;
-    w0 = w1;
-    w1 = op + 2 < sd.n_ops ? first_words(op + 2) : z2;
+  auto step = [&](int op, uint2 ww) {
     const uint2 se = gse[op];
     if (se.x + tid < se.y) {
       const double c = cs[op].x;
@@ -447,7 +445,19 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       }
     }
     __syncthreads();
+  };
+  uint2 wa = first_words(0), wb = first_words(1), wc = first_words(2);
+  int op = 0;
+  for (; op + 3 <= sd.n_ops; op += 3) {
+    step(op, wa);
+    wa = first_words(op + 3);
+    step(op + 1, wb);
+    wb = first_words(op + 4);
+    step(op + 2, wc);
+    wc = first_words(op + 5);
   }
+  if (op < sd.n_ops) step(op, wa);
+  if (op + 1 < sd.n_ops) step(op + 1, wb);
   const long long clk1 = clock64();
   double acc = 0.0;
   {
