@@ -573,56 +573,84 @@ constexpr size_t kSegChunk = 512;
 inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const std::vector<uint8_t>& rj,
                                         int G = 8) {
   const size_t n = ri.size();
-  std::vector<std::vector<uint32_t>> bucket((size_t)G * G);
-  for (size_t t = n; t-- > 0;) bucket[(size_t)ri[t] * G + rj[t]].push_back((uint32_t)t);  // pop_back -> ascending t
   std::vector<uint32_t> out;
   out.reserve(n);
+  if (n <= 1) {
+    for (size_t t = 0; t < n; ++t) out.push_back((uint32_t)t);
+    return out;
+  }
+  // buckets (ri, rj) as one flat array, each taken front to back (ascending t)
+  const int NB = G * G;
+  std::vector<uint32_t> head((size_t)NB + 1, 0), items(n);
+  for (size_t t = 0; t < n; ++t) ++head[(size_t)ri[t] * G + rj[t] + 1];
+  for (int b = 0; b < NB; ++b) head[b + 1] += head[b];
+  std::vector<uint32_t> tail(head.begin(), head.end() - 1);
+  for (size_t t = 0; t < n; ++t) items[tail[(size_t)ri[t] * G + rj[t]]++] = (uint32_t)t;
+  auto size_of = [&](int b) { return tail[b] - head[b]; };
+  int64_t row_left[16] = {0};
+  for (size_t t = 0; t < n; ++t) ++row_left[ri[t]];
   size_t left = n;
   auto take = [&](int b) {
-    out.push_back(bucket[b].back());
-    bucket[b].pop_back();
+    out.push_back(items[head[b]++]);
+    --row_left[b / G];
     --left;
   };
-  // each group: a maximum matching rows (ri) -> columns (rj) over non-empty
-  // buckets (Kuhn's augmenting paths, larger buckets tried first)
-  std::vector<int> match_col((size_t)G), match_row((size_t)G);
-  std::vector<int> order((size_t)G * G);
-  std::vector<char> seen((size_t)G);
-  std::function<bool(int)> augment = [&](int r) {
-    for (int k = 0; k < G; ++k) {
-      const int c = order[(size_t)r * G + k];
-      if (c < 0 || seen[c]) continue;
-      seen[c] = 1;
-      if (match_col[c] < 0 || augment(match_col[c])) {
-        match_col[c] = r;
-        match_row[r] = c;
-        return true;
+  // per group: a maximum matching rows (ri) -> columns (rj) over non-empty
+  // buckets: greedy (rows with most pairs left first, largest free bucket),
+  // then Kuhn's augmenting paths for the rows left unmatched
+  int match_col[16], match_row[16], rows[16], order[16][16], n_order[16];
+  bool seen[16];
+  struct Aug {
+    int G;
+    int (*order)[16];
+    int* n_order;
+    int* match_col;
+    int* match_row;
+    bool* seen;
+    bool run(int r) {
+      for (int k = 0; k < n_order[r]; ++k) {
+        const int c = order[r][k];
+        if (seen[c]) continue;
+        seen[c] = true;
+        if (match_col[c] < 0 || run(match_col[c])) {
+          match_col[c] = r;
+          match_row[r] = c;
+          return true;
+        }
       }
+      return false;
     }
-    return false;
-  };
+  } aug{G, order, n_order, match_col, match_row, seen};
   while (left > 0) {
+    int nr = 0;
     for (int r = 0; r < G; ++r) {
-      std::vector<std::pair<size_t, int>> cs;
+      match_row[r] = -1;
+      match_col[r] = -1;
+      if (row_left[r] > 0) rows[nr++] = r;
+    }
+    std::sort(rows, rows + nr, [&](int x, int y) { return row_left[x] > row_left[y]; });
+    for (int k = 0; k < nr; ++k) {  // columns of row r by bucket size, largest first
+      const int r = rows[k];
+      int m = 0;
       for (int c = 0; c < G; ++c)
-        if (!bucket[(size_t)r * G + c].empty()) cs.push_back({bucket[(size_t)r * G + c].size(), c});
-      std::sort(cs.begin(), cs.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-      for (int k = 0; k < G; ++k) order[(size_t)r * G + k] = k < (int)cs.size() ? cs[k].second : -1;
+        if (size_of(r * G + c)) order[r][m++] = c;
+      std::sort(order[r], order[r] + m, [&](int x, int y) { return size_of(r * G + x) > size_of(r * G + y); });
+      n_order[r] = m;
     }
-    std::fill(match_col.begin(), match_col.end(), -1);
-    std::fill(match_row.begin(), match_row.end(), -1);
-    // rows with the most pairs left first
-    std::vector<std::pair<size_t, int>> rows;
-    for (int r = 0; r < G; ++r) {
-      size_t tot = 0;
-      for (int c = 0; c < G; ++c) tot += bucket[(size_t)r * G + c].size();
-      if (tot) rows.push_back({tot, r});
+    for (int k = 0; k < nr; ++k) {  // greedy pass
+      const int r = rows[k];
+      for (int q = 0; q < n_order[r]; ++q)
+        if (match_col[order[r][q]] < 0) {
+          match_col[order[r][q]] = r;
+          match_row[r] = order[r][q];
+          break;
+        }
     }
-    std::sort(rows.begin(), rows.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-    for (const auto& rr : rows) {
-      std::fill(seen.begin(), seen.end(), 0);
-      augment(rr.second);
-    }
+    for (int k = 0; k < nr; ++k)
+      if (match_row[rows[k]] < 0) {
+        for (int c = 0; c < G; ++c) seen[c] = false;
+        aug.run(rows[k]);
+      }
     int taken = 0;
     for (int r = 0; r < G; ++r)
       if (match_row[r] >= 0) {
@@ -631,8 +659,8 @@ inline std::vector<uint32_t> bank_order(const std::vector<uint8_t>& ri, const st
       }
     for (; taken < G && left > 0; ++taken) {  // no conflict-free member left: largest bucket
       int best = 0;
-      for (int b2 = 1; b2 < G * G; ++b2)
-        if (bucket[b2].size() > bucket[best].size()) best = b2;
+      for (int b2 = 1; b2 < NB; ++b2)
+        if (size_of(b2) > size_of(best)) best = b2;
       take(best);
     }
   }
