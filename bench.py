@@ -229,6 +229,30 @@ def main():
     # the kernel behind `value`: program statistics for its on-chip roofline
     sector = capi.sector_info(ctx, plan, ham, P.hf)
 
+    # B = 1 latency and B = 64 throughput at 18 qubits (device
+    # buffers, CUDA events, L2 flushed before each timed call)
+    def batch_call(nb):
+        return lambda: capi.energy_batch_device(ctx, plan, ham, P.hf, nb, th_dev.data_ptr(), e_dev.data_ptr())
+    b1 = batch_call(1)
+    b1()
+    ms_b1 = timed(b1, 20)
+    b64 = batch_call(64)
+    b64()
+    ms_b64 = timed(b64, 10)
+    # unfused HBM roofline of one evaluation: every generator string
+    # a full rotation pass (32 B/amplitude) and every x-group a read pass (16 B)
+    n_strings = int(P.plan_arrays()[0][-1])
+    n_groups = ham.info()[0]
+    unfused_bytes = (32 * n_strings + 16 * n_groups) * 2 ** P.n_qubits
+    peak_gbs, _ = peaks()
+    unfused_evals = peak_gbs * 1e9 / unfused_bytes
+    latency = {"b1_ms": statistics.median(ms_b1), "b64_evals_per_s": 64 / (statistics.median(ms_b64) / 1e3),
+               "unfused_roofline_evals_per_s": unfused_evals,
+               "x_unfused_roofline": value / world / unfused_evals,
+               "unfused_bytes_per_eval": unfused_bytes,
+               "note": "unfused roofline = measured HBM peak / (32 B x 2^n per generator string + 16 B x 2^n "
+                       "per x-group); label, not a fraction (fusion and on-chip residency pass it)"}
+
     # e2e: host buffers through ffq_energy_batch (pinned staging + H2D + D2H inside)
     def step_host():
         step_host.out = capi.energy_batch(ctx, plan, ham, P.hf, th_host)
@@ -336,9 +360,11 @@ def main():
         n_cpu = 2
         rate, es, cores = cpu_oracle_rate(P, rows, n_cpu, os.cpu_count())
         parity = max(abs(es[i] - e_first[i]) for i in range(n_cpu))
+        rate1, es1, _ = cpu_oracle_rate(P, rows, 1, 1)  # single-threaded too
+        parity = max(parity, abs(es1[0] - e_first[0]))
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{n_cpu} energy evaluations of the config-3 parameter-shift set (C oracle, OpenMP)",
-               "parity_max_abs_hartree": parity}
+               "parity_max_abs_hartree": parity, "single_thread_value": rate1}
 
     if rank == 0:
         line = {
@@ -368,7 +394,8 @@ def main():
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
             "gpu_launches": int(launches),
-            "secondary": {"config3_dense_slab_path": dense_path, "config2_12q": config2,
+            "secondary": {"config3_latency_and_b64": latency, "config3_dense_slab_path": dense_path,
+                          "config2_12q": config2,
                           "config4_fmo": config4},
             "clocks": clk.summary(),
         }
