@@ -1,0 +1,58 @@
+"""Golden fixtures (tests/golden/energies.json, made by tools/make_golden.py):
+the seeded synthetic inputs and the C oracle must reproduce them. The reference
+has no golden vectors for this path; these pin the oracle and the
+input generators against drift. The CUDA path is checked against the same file
+in tests/test_gpu_parity.py."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2402_17993_b200 import problems
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "energies.json")
+
+
+def load():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3"])
+def test_inputs_reproduce_golden(cfg):
+    g = load()["configs"][cfg]
+    P = problems.config_problem(int(cfg), batch=len(g["rows"]))
+    x, z, c = P.ham_arrays()
+    assert (P.n_qubits, P.n_elec, P.hf, P.n_gen, len(x)) == (g["n_qubits"], g["n_elec"], g["hf"], g["n_gen"],
+                                                             g["n_terms"])
+    assert digest(x, z, c) == g["ham_sha256"]
+    assert digest(np.array(P.plan.order, np.int32)) == g["plan_order_sha256"]
+    for b, row in enumerate(g["rows"]):
+        assert [float(t).hex() for t in P.thetas[b]] == row["theta_canonical"]
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3"])
+def test_oracle_reproduces_golden(oracle, cfg):
+    g = load()["configs"][cfg]
+    P = problems.config_problem(int(cfg), batch=len(g["rows"]))
+    x, z, c = P.ham_arrays()
+    H = oracle.PauliSum.from_terms(P.n_qubits, x, z, c)
+    kind, idx = oracle.build_generators(P.n_qubits, P.n_elec)
+    order = np.array(P.plan.order, np.int32)
+    for b, row in enumerate(g["rows"]):
+        want = "state_re" in row
+        r = oracle.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, P.thetas[b], H, want_state=want)
+        assert abs(r[0] - float.fromhex(row["energy"])) <= 1e-12
+        if want:
+            ref = np.array([float.fromhex(v) for v in row["state_re"]]) + 1j * np.array(
+                [float.fromhex(v) for v in row["state_im"]])
+            assert np.abs(r[2] - ref).max() <= 1e-13

@@ -245,3 +245,27 @@ def test_sector_path_18q_vs_oracle_and_dense(monkeypatch, oracle):
     c2 = capi.Context(0)
     plan2, ham2 = upload(c2, P)
     assert np.abs(e - capi.energy_batch(c2, plan2, ham2, P.hf, P.plan_thetas())).max() <= 1e-12
+
+
+def test_cuda_path_matches_golden_fixtures(ctx):
+    # tests/golden/energies.json (tools/make_golden.py): energies <= 1e-10,
+    # the config-1 state <= 1e-12, through the default execution paths
+    import json
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "energies.json")) as f:
+        golden = json.load(f)["configs"]
+    for cfg, g in golden.items():
+        P = problems.config_problem(int(cfg), batch=len(g["rows"]))
+        plan, ham = upload(ctx, P)
+        e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())
+        ref = np.array([float.fromhex(r["energy"]) for r in g["rows"]])
+        assert np.abs(e - ref).max() <= E_TOL, cfg
+        for b, row in enumerate(g["rows"]):
+            if "state_re" not in row:
+                continue
+            st = capi.State(ctx, P.n_qubits, 1)
+            st.set_basis(P.hf)
+            st.apply_plan(plan, P.plan_thetas()[b:b + 1])
+            want = np.array([float.fromhex(v) for v in row["state_re"]]) + 1j * np.array(
+                [float.fromhex(v) for v in row["state_im"]])
+            assert np.abs(st.download()[0] - want).max() <= A_TOL
