@@ -123,7 +123,10 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
  * pairs, out[4] expectation rows of 32, out[5] generator steps ending in a
  * cluster barrier, out[6] first split mask, out[7] peer-chunk buffer
  * (amplitudes), out[8] 1 when the program stores real amplitudes only (real F
- * on every generator and real class sums: psi(theta) is real for every theta).
+ * on every generator and real class sums: psi(theta) is real for every theta),
+ * out[9] expectation pairs held by anchored string blocks (product layout),
+ * out[10] amplitude slots (padded product layout; = out[0] otherwise).
+ * out must hold 11 values.
  * FFQ_EINVAL when the closure does not fit the sector evaluator (the other
  * paths then run) or FFQ_SECTOR=0. */
 int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
@@ -199,6 +202,16 @@ int ffq_ham_compile_stats(int n_qubits, int64_t n_terms, const uint64_t* x, cons
 int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* x,
                            const uint64_t* z, const double* c_re, const double* c_im,
                            int64_t* stats);
+/* Test hook (host only, no GPU): compiles the one-CTA real-amplitude sector
+ * program (product layout, anchored string blocks) for plan + Hamiltonian +
+ * hf and evaluates its expectation tables on the real state psi[2^n] exactly
+ * as k_sector_eval_real would. out[8]: energy, closure size, amplitude slots,
+ * product layout (0/1), pairs held by blocks, expectation pairs, generic rows,
+ * block units. FFQ_EINVAL when the program is complex or has no sector. */
+int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
+                       const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
+                       const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
+                       const double* psi, double* out);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,8 @@ _SIGS = {
     "ffq_energy_exact": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, C.c_double, C.POINTER(C.c_double)]),
     "ffq_ham_compile_stats": (C.c_int, [C.c_int, C.c_int64, _u64p, _u64p, _f64p, _f64p, _i64p]),
     "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
+    "ffq_sector_emulate": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.c_int64, _u64p, _u64p,
+                                     _f64p, _f64p, C.c_uint64, _f64p, _f64p]),
     "ffq_sector_info": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i64p]),
 }
 
@@ -125,6 +127,21 @@ def plan_compile_stats(n, off, x, z, c):
     check(lib().ffq_plan_compile_stats(n, len(off) - 1, off, x, z, re_, im, st))
     keys = ["fused", "string_ops", "pattern_pairs", "pair_updates", "bytes", "ops"]
     return dict(zip(keys, st.tolist()))
+
+
+def sector_emulate(n, plan_arrays, ham_arrays, hf_bits, psi):
+    """Host emulation of the real one-CTA sector program's expectation on the
+    real state psi (no GPU); returns the energy and the layout statistics."""
+    off, px, pz, pc = plan_arrays
+    px, pz, pre, pim = _terms(px, pz, pc)
+    hx, hz, hre, him = _terms(*ham_arrays)
+    off = np.ascontiguousarray(off, np.int64)
+    psi = np.ascontiguousarray(psi, np.float64)
+    out = np.zeros(8)
+    check(lib().ffq_sector_emulate(n, len(off) - 1, off, px, pz, pre, pim, len(hx), hx, hz, hre, him, hf_bits, psi,
+                                   out))
+    keys = ["energy", "closure_size", "slots", "product", "block_pairs", "exp_pairs", "generic_rows", "units"]
+    return dict(zip(keys, out.tolist()))
 
 
 class Context:
@@ -219,12 +236,12 @@ def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int
 
 SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expectation_pairs",
                     "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
-                    "real_amplitudes")
+                    "real_amplitudes", "block_pairs", "slots")
 
 
 def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:
     """Statistics of the support-closure program energy_batch runs (ffq_sector_info)."""
-    out = np.zeros(9, np.int64)
+    out = np.zeros(11, np.int64)
     check(lib().ffq_sector_info(ctx.h, plan.h, ham.h, hf_bits, out), ctx.h)
     return dict(zip(SECTOR_INFO_KEYS, (int(v) for v in out)))
 

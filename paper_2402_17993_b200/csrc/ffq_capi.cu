@@ -95,6 +95,8 @@ struct ffq_ctx_s {
   int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
+  int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
+  int blk_fmode = 1;                             // env FFQ_BLK_F: shared-row f from 0 params / 1 smem (default) / 2 shfl
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
@@ -136,6 +138,9 @@ struct ffq_plan_s {
     DevBuf<int32_t> secs;
     DevBuf<uint8_t> gen_flags, op_cross;
     DevBuf<double> row_fre, row_fim, pf_re, pf_im;
+    DevBuf<int32_t> blk_warp_off, blk_units;
+    DevBuf<uint32_t> blk_lanes, blk_sh, blk_plo;
+    DevBuf<double> blk_plf, blk_shf;
     bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
@@ -441,9 +446,11 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     const bool real_ok = ctx->sector_real && plan_is_real(pl->cp) && ham_is_real(h->ch);
     // closure size first (one part, no size limit on the part), then either the
     // one-CTA real program or the cluster split (rows padded to multiples of 4)
-    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, real_ok ? 8 : 16);
+    // (anchored string blocks for the 1024-thread real program: FFQ_BLOCKS=0 disables them)
+    b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, real_ok ? 8 : 16,
+                             real_ok && ctx->sector_blocks ? kSectorRealThreads / 32 : 0, kSectorSingleMax);
     b->real = b->prog.ok && real_ok &&
-              sector_real_smem_bytes(b->prog.size, pl->cp.op_kind.size()) <= ctx->smem_optin;
+              sector_real_smem_bytes(b->prog.n_slots, pl->cp.op_kind.size()) <= ctx->smem_optin;
     if (b->prog.ok && !b->real && sector_parts(ctx, b->prog.size) > 1)
       b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
                                (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)), 4);
@@ -459,6 +466,15 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
       b->secs.upload(secs, ctx->stream);
       b->row_fre.upload(b->prog.row_fre, ctx->stream);
       b->pf_re.upload(b->prog.pf_re, ctx->stream);
+      if (b->prog.product) {
+        b->blk_warp_off.upload(b->prog.blk_warp_off, ctx->stream);
+        b->blk_units.upload(b->prog.blk_units, ctx->stream);
+        b->blk_lanes.upload(b->prog.blk_lanes, ctx->stream);
+        b->blk_sh.upload(b->prog.blk_sh, ctx->stream);
+        b->blk_plo.upload(b->prog.blk_plo, ctx->stream);
+        b->blk_plf.upload(b->prog.blk_plf, ctx->stream);
+        b->blk_shf.upload(b->prog.blk_shf, ctx->stream);
+      }
       if (!b->prog.f_real) {
         b->row_fim.upload(b->prog.row_fim, ctx->stream);
         b->pf_im.upload(b->prog.pf_im, ctx->stream);
@@ -493,6 +509,17 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.pf_im = b.prog.f_real ? nullptr : b.pf_im.p;
   sd.n_parts = b.prog.n_parts;
   sd.real = b.real ? 1 : 0;
+  sd.n_slots = b.prog.n_slots;
+  const bool blk = b.prog.product && !b.prog.blk_warp_off.empty();
+  sd.blk_warp_off = blk ? b.blk_warp_off.p : nullptr;
+  sd.blk_units = blk ? reinterpret_cast<const int4*>(b.blk_units.p) : nullptr;
+  sd.blk_lanes = blk ? b.blk_lanes.p : nullptr;
+  sd.blk_sh = blk ? b.blk_sh.p : nullptr;
+  sd.ftab_host = b.prog.ftab.data();
+  sd.n_ftab = (int)b.prog.ftab.size();
+  sd.blk_plo = blk ? b.blk_plo.p : nullptr;
+  sd.blk_plf = blk ? b.blk_plf.p : nullptr;
+  sd.blk_shf = blk ? b.blk_shf.p : nullptr;
   return &sd;
 }
 
@@ -520,14 +547,27 @@ void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, c
   ctx->launches++;
 }
 
+template <int NT, int FM>
+void launch_sector_real_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
+                          double* e, double* im, long long* clk) {
+  // FM 1 keeps a copy of the shared-row f table behind the per-op tables
+  const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) +
+                    (FM == 1 ? (size_t)sd.n_ftab * sizeof(double) : 0);
+  CK(cudaFuncSetAttribute(k_sector_eval_real<NT, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  static thread_local FTab ft;
+  std::memset(&ft, 0, sizeof(ft));
+  if (sd.n_ftab > 0) std::memcpy(ft.f, sd.ftab_host, (size_t)std::min(sd.n_ftab, kFTabMax) * sizeof(double));
+  k_sector_eval_real<NT, FM><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, ft);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
 template <int NT>
 void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
                         double* e, double* im, long long* clk) {
-  const size_t sb = sector_real_smem_bytes(sd.size, pl->cp.op_kind.size());
-  CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  k_sector_eval_real<NT><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk);
-  CK(cudaGetLastError());
-  ctx->launches++;
+  if (!sd.blk_warp_off || ctx->blk_fmode == 0) launch_sector_real_t<NT, 0>(ctx, pl, sd, theta, batch, e, im, clk);
+  else if (ctx->blk_fmode == 1) launch_sector_real_t<NT, 1>(ctx, pl, sd, theta, batch, e, im, clk);
+  else launch_sector_real_t<NT, 2>(ctx, pl, sd, theta, batch, e, im, clk);
 }
 
 void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
@@ -767,6 +807,8 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_BLK_F")) c->blk_fmode = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);
       c->sector_cl = (v == 4 || v == 8) ? v : 2;
@@ -939,11 +981,13 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
     out[1] = S.n_parts;
     out[2] = (int64_t)S.gen_pairs.size();
     out[3] = S.exp_pair_count;
-    out[4] = (int64_t)(S.row_pairs.size() / 32);
+    out[4] = (int64_t)(S.row_pairs.size() / 32 + S.blk_sh.size() / 32 + S.blk_plo.size());
     out[5] = cluster_steps;
     out[6] = S.split_masks.empty() ? 0 : (int64_t)S.split_masks[0];
     out[7] = S.buf_len;
     out[8] = bufs.real ? 1 : 0;
+    out[9] = S.blk_pairs;
+    out[10] = S.n_slots;
     return FFQ_OK;
   });
 }
@@ -1154,6 +1198,64 @@ int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, con
     stats[3] = upd + (int64_t)P.n_string_ops() * (1LL << (n_qubits - 1));
     stats[4] = bytes + string_bytes;
     stats[5] = (int64_t)P.op_kind.size();
+    return FFQ_OK;
+  });
+}
+
+// Host emulation of the one-CTA real program's expectation (generic rows +
+// anchored blocks) on a real state psi[2^n]: checks the product layout and
+// the block compilation without a GPU. out[8]: energy, closure size, slots,
+// product layout, block pairs, expectation pairs, generic rows, block units.
+int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
+                       const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
+                       const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
+                       const double* psi, double* out) {
+  if (!out || !psi || !term_off || n_qubits < 1 || n_qubits > 26) return fail(nullptr, FFQ_EINVAL, "invalid argument");
+  return guarded(nullptr, [&] {
+    const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, px, pz, pc_re, pc_im);
+    const CompiledHam H = compile_ham(n_qubits, n_terms, hx, hz, hc_re, hc_im);
+    if (!plan_is_real(P) || !ham_is_real(H)) return fail(nullptr, FFQ_EINVAL, "ffq_sector_emulate: complex program");
+    const SectorProgram S = compile_sector(P, H, hf_bits, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, 8,
+                                           kSectorRealThreads / 32, kSectorSingleMax);
+    if (!S.ok) return fail(nullptr, FFQ_EINVAL, "ffq_sector_emulate: " + S.why);
+    std::vector<double> amp((size_t)S.n_slots + 1, 0.0);
+    for (uint32_t i = 0; i < S.size; ++i) amp[S.slot_of[i]] = psi[S.basis[i]];
+    double e = 0.0;
+    const auto& es = S.sections[0];
+    for (int r = es.sh0; r < es.pp1; ++r)
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t w = S.row_pairs[(size_t)r * 32 + l];
+        double f = r < es.sh1 ? S.row_fre[r] : S.pf_re[((size_t)(es.pf_base + r - es.sh1)) * 32 + l];
+        if (r < es.sh1 && ((w >> 30) & 1u)) f = -f;
+        e += f * amp[w & 0x7FFFu] * amp[(w >> 15) & 0x7FFFu];
+      }
+    const size_t nu = S.blk_units.size() / 8;
+    for (size_t u = 0; u < nu; ++u) {
+      const int32_t* h = &S.blk_units[8 * u];
+      const int nsh = h[5], npl = h[6];
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t w = S.blk_lanes[(size_t)h[0] * 32 + l];
+        const double a = amp[w & 0x7FFFu];
+        const uint32_t bs = (w >> 15) & 0x7FFFu;
+        double t = 0.0;
+        for (int r = 0; r < nsh; ++r) {
+          const uint32_t d = S.blk_sh[((size_t)h[1] + r) * 32 + l];
+          const double f = S.ftab.at(d >> 16);
+          t += ((d >> 15) & 1u ? -f : f) * amp.at(bs + (d & 0x7FFFu));
+        }
+        for (int r = 0; r < npl; ++r)
+          t += S.blk_plf[((size_t)h[3] + r) * 32 + l] * amp.at(bs + S.blk_plo[h[2] + r] / 8);
+        e += a * t;
+      }
+    }
+    out[0] = e;
+    out[1] = S.size;
+    out[2] = S.n_slots;
+    out[3] = S.product ? 1 : 0;
+    out[4] = (double)S.blk_pairs;
+    out[5] = (double)S.exp_pair_count;
+    out[6] = (double)(es.pp1 - es.sh0);
+    out[7] = (double)nu;
     return FFQ_OK;
   });
 }

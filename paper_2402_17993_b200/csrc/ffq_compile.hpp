@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cstdint>
 #include <functional>
@@ -716,7 +718,322 @@ struct SectorProgram {
   std::vector<double> pf_re, pf_im;          // [per-pair rows * 32] (pf_im empty if all f real)
   std::vector<uint32_t> zero_slot;           // [n_parts]
   bool f_real = true;
+  // Product layout (one-CTA real program, see compile_blocks): S is the set
+  // product of its alpha strings (even qubits) and beta strings (odd qubits),
+  // and amplitude k lives at slot idx_a(k) * stride_b + idx_b(k) (stride_b odd,
+  // so consecutive alpha or beta strings hit distinct banks). n_slots counts
+  // the padded slots; the zero slot is n_slots. Without it, n_slots = size.
+  bool product = false;
+  uint32_t n_slots = 0, stride_b = 0, n_alpha = 0, n_beta = 0;
+  std::vector<uint32_t> slot_of;  // one-CTA programs: slot of basis[i]
+  // Anchored string blocks: expectation pairs that share one member ("anchor")
+  // per lane and one partner offset per row. A unit is one chunk of <= 32
+  // lanes run by one warp: lane word = anchor slot | B slot << 15; row r's
+  // partner of lane l is slot B_l + O_r. Shared rows (one |f| per row) carry a
+  // word per lane, O_r | sign << 15 | ftab index << 16, with f in ftab (kernel
+  // parameter space: read through the constant cache, not the LSU); per-lane
+  // rows carry O_r and f per lane. Units are assigned to warps at compile time
+  // (blk_warp_off), balanced with the generic rows.
+  std::vector<int32_t> blk_warp_off;   // [n_warps + 1]
+  std::vector<int32_t> blk_units;      // [units * 8]: lw_off, sh_off (rows), pl_off, pf_off, 1, nsh, npl, 0
+  std::vector<uint32_t> blk_lanes;     // [units * 32]
+  std::vector<uint32_t> blk_sh;        // [shared rows * 32] lane words
+  std::vector<uint32_t> blk_plo;       // per-lane rows: O*8
+  std::vector<double> blk_plf;         // per-lane rows: [row][32] f
+  std::vector<double> ftab;            // distinct shared-row f values
+  std::vector<double> blk_shf;         // [shared rows] f per row
+  int64_t blk_pairs = 0;               // expectation pairs held by the blocks
 };
+
+constexpr int kBlockMaxNC = 1;        // lane chunks per unit (the device runs one)
+constexpr int kFTabMax = 3968;        // shared-row f values (kernel parameter space, 31 KiB)
+constexpr int kBlockMinLanes = 16;    // smaller chunks go to the generic rows
+constexpr int kBlockRowQuantum = 4;   // shared rows per unit padded to a multiple of this
+
+// Anchored string blocks for the expectation pairs of a product-layout sector
+// (see SectorProgram). For pair (i, j = i ^ X) with X = Xa | Xb (alpha / beta
+// parts of the flip mask):
+//   Xb = 0 (alpha type, also the diagonal X = 0): anchor = member with the lower
+//     alpha index, block = its alpha string, lane = beta index, row = partner
+//     alpha string: B_l = anchor slot, O_r = (ja - ia) * stride_b;
+//   Xa = 0 (beta type): the same with the roles of the strings swapped;
+//   both (alpha-beta): anchor = member holding Xa's lowest qubit, block = (Xa,
+//     anchor beta string), lane = anchor alpha index, row = partner beta string:
+//     B_l = idx_a(partner) * stride_b, O_r = idx_b(partner).
+// In every case the partner slot is B_l + O_r, so a row costs one uniform
+// descriptor load and one shared load per lane chunk, and the anchor is read
+// once per unit. Pairs of chunks with fewer than kBlockMinLanes lanes stay in
+// the generic rows (in_block[t] = 0).
+struct BlockPair { uint32_t key_hi, key_lo, lane, row, anchor, partner; int64_t t; };
+inline void compile_blocks(SectorProgram& S, const std::vector<uint32_t>& list,
+                           const std::vector<std::pair<uint32_t, uint32_t>>& ij,  // closure indices per pair
+                           const std::vector<double>& f, const std::vector<uint32_t>& slot_of,
+                           const std::vector<uint32_t>& ia_of, const std::vector<uint32_t>& ib_of,
+                           uint64_t amask, std::vector<uint8_t>& in_block) {
+  const uint32_t sb = S.stride_b;
+  std::vector<BlockPair> bp;
+  bp.reserve(ij.size());
+  for (size_t t = 0; t < ij.size(); ++t) {
+    uint32_t i = ij[t].first, j = ij[t].second;
+    const uint64_t X = (uint64_t)(list[i] ^ list[j]);
+    const uint64_t xa = X & amask, xb = X & ~amask;
+    BlockPair p{};
+    p.t = (int64_t)t;
+    if (xb == 0) {
+      if (ia_of[j] < ia_of[i]) std::swap(i, j);
+      p.key_hi = 0; p.key_lo = ia_of[i]; p.lane = ib_of[i]; p.row = (ia_of[j] - ia_of[i]) * sb;
+    } else if (xa == 0) {
+      if (ib_of[j] < ib_of[i]) std::swap(i, j);
+      p.key_hi = 1; p.key_lo = ib_of[i]; p.lane = ia_of[i]; p.row = ib_of[j] - ib_of[i];
+    } else {
+      // alpha-beta blocks are keyed by the alpha flip mask (n <= 26: <= 13 alpha qubits)
+      // and the anchor's beta string; the anchor holds Xa's lowest qubit
+      if (!(list[i] & (xa & (~xa + 1)))) std::swap(i, j);
+      p.key_hi = 2u + (uint32_t)xa; p.key_lo = ib_of[i]; p.lane = ia_of[i]; p.row = ib_of[j];
+    }
+    p.anchor = i;
+    p.partner = j;
+    bp.push_back(p);
+  }
+  std::sort(bp.begin(), bp.end(), [](const BlockPair& a, const BlockPair& b) {
+    if (a.key_hi != b.key_hi) return a.key_hi < b.key_hi;
+    if (a.key_lo != b.key_lo) return a.key_lo < b.key_lo;
+    if (a.lane != b.lane) return a.lane < b.lane;
+    return a.row < b.row;
+  });
+  const uint32_t zero = S.n_slots;
+  std::map<double, uint32_t> ftab_index{{0.0, 0u}};  // ftab[0] = 0: padding rows
+  S.ftab.assign(1, 0.0);
+  size_t b0 = 0;
+  while (b0 < bp.size()) {
+    size_t b1 = b0;
+    while (b1 < bp.size() && bp[b1].key_hi == bp[b0].key_hi && bp[b1].key_lo == bp[b0].key_lo) ++b1;
+    // lanes of the block in ascending order, chunked by 32
+    std::vector<size_t> lane_start;  // first entry of each distinct lane
+    for (size_t u = b0; u < b1; ++u)
+      if (u == b0 || bp[u].lane != bp[u - 1].lane) lane_start.push_back(u);
+    lane_start.push_back(b1);
+    const size_t nl = lane_start.size() - 1;
+    std::vector<std::vector<size_t>> chunks;  // lane positions of the good chunks
+    if (bp[b0].key_hi >= 2 && nl > 32 && nl < 32 + (size_t)kBlockMinLanes) {
+      // alpha-beta block a little over one warp: keep the 32 lanes whose
+      // partner loads spread best over the 16 eight-byte bank pairs (partner
+      // slot = idx_a(partner) * stride_b + O_r, stride_b odd), the rest stay generic
+      std::vector<size_t> keep(nl);
+      for (size_t l = 0; l < nl; ++l) keep[l] = l;
+      auto color = [&](size_t l) { return (ia_of[bp[lane_start[l]].partner] * sb) & 15u; };
+      while (keep.size() > 32) {
+        int cnt[16] = {0};
+        for (size_t l : keep) ++cnt[color(l)];
+        const int cmax = (int)(std::max_element(cnt, cnt + 16) - cnt);
+        for (size_t q = keep.size(); q-- > 0;)
+          if ((int)color(keep[q]) == cmax) { keep.erase(keep.begin() + (long)q); break; }
+      }
+      // 8-byte loads are served per half warp: lanes 0-15 and 16-31 each want 16
+      // distinct bank pairs, so the first member of every color goes to the first half
+      std::stable_sort(keep.begin(), keep.end(), [&](size_t x, size_t y) { return color(x) < color(y); });
+      std::vector<size_t> h0, h1;
+      for (size_t q = 0; q < keep.size(); ++q)
+        ((q == 0 || color(keep[q]) != color(keep[q - 1])) && h0.size() < 16 ? h0 : h1).push_back(keep[q]);
+      while (h0.size() < 16 && !h1.empty()) { h0.push_back(h1.back()); h1.pop_back(); }
+      h0.insert(h0.end(), h1.begin(), h1.end());
+      chunks.push_back(h0);
+    } else {
+      for (size_t c0 = 0; c0 < nl; c0 += 32) {
+        const size_t c1 = std::min(nl, c0 + 32);
+        if (c1 - c0 < (size_t)kBlockMinLanes) continue;
+        chunks.emplace_back();
+        for (size_t l = c0; l < c1; ++l) chunks.back().push_back(l);
+      }
+    }
+    for (size_t g0 = 0; g0 < chunks.size(); g0 += kBlockMaxNC) {
+      const int nc = (int)std::min<size_t>(kBlockMaxNC, chunks.size() - g0);
+      // rows of the unit: cell (chunk, lane in chunk, row) -> pair entry
+      std::map<uint32_t, std::vector<int64_t>> rows;  // row -> [nc * 32] bp index or -1
+      for (int c = 0; c < nc; ++c) {
+        const auto& lanes = chunks[g0 + c];
+        for (size_t q = 0; q < lanes.size(); ++q)
+          for (size_t u = lane_start[lanes[q]]; u < lane_start[lanes[q] + 1]; ++u) {
+            auto& v = rows[bp[u].row];
+            if (v.empty()) v.assign((size_t)nc * 32, -1);
+            v[(size_t)c * 32 + q] = (int64_t)u;
+          }
+      }
+      int32_t hdr[8] = {0, 0, 0, 0, nc, 0, 0, 0};
+      hdr[0] = (int32_t)(S.blk_lanes.size() / 32);
+      for (int c = 0; c < nc; ++c) {
+        const auto& lanes = chunks[g0 + c];
+        for (size_t q = 0; q < 32; ++q) {
+          uint32_t w = zero;  // idle lane: anchor = zero slot, B = 0
+          if (q < lanes.size()) {
+            const BlockPair& p = bp[lane_start[lanes[q]]];
+            const uint32_t B = p.key_hi >= 2 ? ia_of[p.partner] * sb : slot_of[p.anchor];
+            w = slot_of[p.anchor] | (B << 15);
+          }
+          S.blk_lanes.push_back(w);
+        }
+      }
+      // shared rows: every active lane present with one |f|; the rest per lane
+      std::vector<std::pair<uint32_t, const std::vector<int64_t>*>> sh, pl;
+      for (const auto& [r, cells] : rows) {
+        bool shared = true;
+        double f0 = 0.0;
+        bool have = false;
+        for (int c = 0; c < nc && shared; ++c) {
+          const size_t act = chunks[g0 + c].size();
+          for (size_t l = 0; l < act; ++l) {
+            const int64_t u = cells[(size_t)c * 32 + l];
+            if (u < 0) { shared = false; break; }
+            const double fv = f[bp[u].t];
+            if (!have) { f0 = fv; have = true; }
+            else if (!(fv == f0 || fv == -f0)) { shared = false; break; }
+          }
+        }
+        (shared ? sh : pl).push_back({r, &cells});
+      }
+      // shared rows whose f fits the table; the rest go to the per-lane rows
+      std::vector<std::pair<uint32_t, const std::vector<int64_t>*>> sh2;
+      std::vector<uint32_t> fidx;
+      for (const auto& e : sh) {
+        double fv = 0.0;
+        for (int l = 0; l < 32; ++l)
+          if ((*e.second)[l] >= 0) { fv = f[bp[(*e.second)[l]].t]; break; }
+        auto it = ftab_index.find(fv);
+        if (it == ftab_index.end()) {
+          if (S.ftab.size() >= (size_t)kFTabMax) { pl.push_back(e); continue; }
+          it = ftab_index.emplace(fv, (uint32_t)S.ftab.size()).first;
+          S.ftab.push_back(fv);
+        }
+        sh2.push_back(e);
+        fidx.push_back(it->second);
+      }
+      hdr[1] = (int32_t)(S.blk_sh.size() / 32);
+      hdr[5] = (int32_t)((sh2.size() + kBlockRowQuantum - 1) / kBlockRowQuantum * kBlockRowQuantum);
+      for (size_t k = 0; k < (size_t)hdr[5]; ++k) {
+        if (k >= sh2.size()) {  // padding row: O = 0, f = ftab[0] = 0
+          S.blk_sh.insert(S.blk_sh.end(), 32, 0u);
+          S.blk_shf.push_back(0.0);
+          continue;
+        }
+        S.blk_shf.push_back(S.ftab[fidx[k]]);
+        const auto& cells = *sh2[k].second;
+        const double fv = S.ftab[fidx[k]];
+        for (int l = 0; l < 32; ++l) {
+          const int64_t u = cells[l];
+          const uint32_t neg = (u >= 0 && f[bp[u].t] != fv) ? 1u : 0u;
+          S.blk_sh.push_back(sh2[k].first | (neg << 15) | (fidx[k] << 16));
+        }
+      }
+      hdr[2] = (int32_t)S.blk_plo.size();
+      hdr[3] = (int32_t)(S.blk_plf.size() / 32);
+      hdr[6] = (int32_t)pl.size();
+      std::sort(pl.begin(), pl.end());
+      for (const auto& [r, cp] : pl) {
+        S.blk_plo.push_back(r * 8);
+        for (int l = 0; l < 32; ++l) {
+          const int64_t u = (*cp)[l];
+          S.blk_plf.push_back(u >= 0 ? f[bp[u].t] : 0.0);
+        }
+      }
+      for (const auto& [r, cells] : rows)
+        for (int64_t u : cells)
+          if (u >= 0) {
+            in_block[bp[u].t] = 1;
+            ++S.blk_pairs;
+          }
+      S.blk_units.insert(S.blk_units.end(), hdr, hdr + 8);
+    }
+    b0 = b1;
+  }
+}
+
+// L1 wavefronts of a block unit (a lane word and a shared load per row;
+// per-lane rows add a coalesced f load), used to balance warps
+inline double block_unit_cost(const int32_t* hdr) {
+  return 4.0 + hdr[5] * 3.2 + hdr[6] * 5.2;
+}
+
+// Order of the alpha strings for the product layout. An alpha-beta block with
+// alpha flip mask Xa reads, per row, psi[idx_a(J) * stride + O] for the partner
+// strings J of its lanes, so its shared-load wavefronts are the largest number
+// of lanes on one 8-byte bank pair, color(J) = idx_a(J) * stride mod 16. The
+// order is a local search over colors (capacities fixed by the string count)
+// minimising the sum over masks of that maximum, after the block drops its
+// lanes beyond 32 from the fullest colors (as compile_blocks does).
+inline std::vector<uint32_t> alpha_order(const std::vector<uint32_t>& sa, const std::vector<uint64_t>& xas,
+                                         uint32_t stride) {
+  const size_t na = sa.size();
+  if (na < 32 || xas.empty()) return sa;
+  std::map<uint32_t, uint32_t> pos;
+  for (uint32_t q = 0; q < (uint32_t)na; ++q) pos[sa[q]] = q;
+  // partner sets (positions in sa) of each mask with 32 < size < 48
+  std::vector<std::vector<uint32_t>> sets;
+  for (uint64_t xa : xas) {
+    const uint32_t low = (uint32_t)(xa & (~xa + 1));
+    std::vector<uint32_t> P;
+    for (uint32_t J : sa)
+      if (!(J & low) && pos.count(J ^ (uint32_t)xa)) P.push_back(pos[J]);
+    if (P.size() > 32 && P.size() < 48) sets.push_back(P);
+    else if (P.size() >= 16 && P.size() <= 32) sets.push_back(P);
+  }
+  if (sets.empty()) return sa;
+  const bool dbg = std::getenv("FFQ_DEBUG") != nullptr;
+  std::vector<std::vector<uint32_t>> member(na);  // sets containing each string
+  for (uint32_t k = 0; k < (uint32_t)sets.size(); ++k)
+    for (uint32_t q : sets[k]) member[q].push_back(k);
+  // initial colors: the natural order's (color of position q = q * stride mod 16)
+  std::vector<uint8_t> col(na);
+  for (size_t q = 0; q < na; ++q) col[q] = (uint8_t)((q * stride) & 15u);
+  // cost: lanes beyond two per color after the block's drops (0 = every row's
+  // partner loads conflict-free), squared per color so the search has a slope
+  auto set_cost = [&](uint32_t k) {
+    int cnt[16] = {0};
+    for (uint32_t q : sets[k]) ++cnt[col[q]];
+    for (size_t d = sets[k].size(); d > 32; --d) --*std::max_element(cnt, cnt + 16);
+    int c2 = 0;
+    for (int c = 0; c < 16; ++c)
+      if (cnt[c] > 2) c2 += (cnt[c] - 2) * (cnt[c] - 2);
+    return c2;
+  };
+  std::vector<int> cost(sets.size());
+  long total = 0;
+  for (uint32_t k = 0; k < (uint32_t)sets.size(); ++k) total += cost[k] = set_cost(k);
+  uint64_t rng = 0x9E3779B97F4A7C15ull;
+  auto next = [&]() {
+    rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+    return rng;
+  };
+  if (dbg) std::fprintf(stderr, "[ffq] alpha_order: %zu sets, cost %ld before\n", sets.size(), total);
+  for (int it = 0; it < 400000 && total > 0; ++it) {
+    const size_t a = next() % na, b = next() % na;
+    if (col[a] == col[b]) continue;
+    std::swap(col[a], col[b]);
+    std::vector<uint32_t> aff(member[a]);
+    aff.insert(aff.end(), member[b].begin(), member[b].end());
+    std::sort(aff.begin(), aff.end());
+    aff.erase(std::unique(aff.begin(), aff.end()), aff.end());
+    long delta = 0;
+    std::vector<int> nc(aff.size());
+    for (size_t t = 0; t < aff.size(); ++t) delta += (nc[t] = set_cost(aff[t])) - cost[aff[t]];
+    if (delta <= 0) {
+      for (size_t t = 0; t < aff.size(); ++t) cost[aff[t]] = nc[t];
+      total += delta;
+    } else {
+      std::swap(col[a], col[b]);
+    }
+  }
+  if (dbg) std::fprintf(stderr, "[ffq] alpha_order: cost %ld after (0 = conflict-free)\n", total);
+  // positions with color c (q * stride mod 16 == c) take the strings of color c
+  std::vector<std::vector<uint32_t>> by_col(16), slots(16);
+  for (size_t q = 0; q < na; ++q) {
+    by_col[col[q]].push_back(sa[q]);
+    slots[(q * stride) & 15u].push_back((uint32_t)q);
+  }
+  std::vector<uint32_t> out(na);
+  for (int c = 0; c < 16; ++c)
+    for (size_t t = 0; t < by_col[c].size(); ++t) out[slots[c][t]] = by_col[c][t];
+  return out;
+}
 
 // cap_amps: shared-memory capacity of a CTA in amplitudes (own part, zero
 // slot and copy buffer); the buffer is used when at least kMinChunk fit.
@@ -724,7 +1041,7 @@ constexpr uint32_t kMinChunk = 256;
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
                                     uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2,
                                     uint32_t cap_amps = 0xFFFFFFFFu, int row_quantum = 4,
-                                    int elem_bytes = 16) {
+                                    int elem_bytes = 16, int block_warps = 0, uint32_t block_min_size = 0) {
   // lanes per conflict-free shared-memory wavefront for this amplitude size
   const int bank_group = elem_bytes == 8 ? 16 : 8;
   SectorProgram S;
@@ -864,6 +1181,51 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   for (int r = 0; r < n_parts; ++r) S.part_start[r + 1] += S.part_start[r];
   for (uint32_t i = 0; i < S.size; ++i) idx[list[i]] = (int32_t)i;
   S.hf_idx = (uint32_t)idx[hf];
+  // product layout for the one-CTA real program with anchored blocks: S must be
+  // exactly (alpha strings) x (beta strings) and fit 15-bit slots when padded
+  uint64_t amask = 0;
+  for (int q = 0; q < n; q += 2) amask |= 1ULL << q;
+  std::vector<uint32_t> slot_of, ia_of, ib_of;
+  if (block_warps > 0 && n_parts == 1 && elem_bytes == 8 && S.size > block_min_size) {
+    std::vector<uint32_t> sa, sbv;
+    for (uint32_t k : list) {
+      sa.push_back(k & (uint32_t)amask);
+      sbv.push_back(k & ~(uint32_t)amask);
+    }
+    std::sort(sa.begin(), sa.end());
+    sa.erase(std::unique(sa.begin(), sa.end()), sa.end());
+    std::sort(sbv.begin(), sbv.end());
+    sbv.erase(std::unique(sbv.begin(), sbv.end()), sbv.end());
+    const uint32_t stride = (uint32_t)sbv.size() | 1u;
+    if ((uint64_t)sa.size() * sbv.size() == S.size && (uint64_t)sa.size() * stride + 1 <= 32768) {
+      // order the alpha strings so that the partner strings of every alpha flip
+      // mask of the alpha-beta pairs spread over the bank pairs (see alpha_order)
+      std::vector<uint64_t> xas;
+      for (const auto& e : ek) {
+        const uint64_t X = H.groups[e.g].x;
+        if ((X & amask) && (X & ~amask)) xas.push_back(X & amask);
+      }
+      std::sort(xas.begin(), xas.end());
+      xas.erase(std::unique(xas.begin(), xas.end()), xas.end());
+      sa = alpha_order(sa, xas, stride);
+      S.product = true;
+      S.n_alpha = (uint32_t)sa.size();
+      S.n_beta = (uint32_t)sbv.size();
+      S.stride_b = stride;
+      S.n_slots = S.n_alpha * stride;
+      std::map<uint32_t, uint32_t> apos;
+      for (uint32_t q = 0; q < (uint32_t)sa.size(); ++q) apos[sa[q]] = q;
+      slot_of.resize(S.size);
+      ia_of.resize(S.size);
+      ib_of.resize(S.size);
+      for (uint32_t i = 0; i < S.size; ++i) {
+        ia_of[i] = apos.at(list[i] & (uint32_t)amask);
+        ib_of[i] = (uint32_t)(std::lower_bound(sbv.begin(), sbv.end(), list[i] & ~(uint32_t)amask) - sbv.begin());
+        slot_of[i] = ia_of[i] * stride + ib_of[i];
+      }
+    }
+  }
+  if (!S.product) S.n_slots = S.size;
   auto owner = [&](uint32_t i) {
     int r = 0;
     while (i >= S.part_start[r + 1]) ++r;
@@ -873,12 +1235,17 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   for (int r = 0; r < n_parts; ++r)
     if (S.part_start[r + 1] - S.part_start[r] >= (1u << S.slot_bits)) { S.why = "part exceeds the slot range"; return S; }
   auto slot = [&](uint32_t i) {
+    if (S.product) return slot_of[i];
     const int r = owner(i);
     return ((uint32_t)r << S.slot_bits) | (i - S.part_start[r]);
   };
   S.hf_slot = slot(S.hf_idx);
+  if (n_parts == 1) {
+    S.slot_of.resize(S.size);
+    for (uint32_t i = 0; i < S.size; ++i) S.slot_of[i] = slot(i);
+  }
   // 16-byte bank group of S[i] within its CTA's amplitude array
-  auto bank_slot = [&](uint32_t i) { return (uint8_t)((i - S.part_start[owner(i)]) & (uint32_t)(bank_group - 1)); };
+  auto bank_slot = [&](uint32_t i) { return (uint8_t)(slot(i) & (uint32_t)(bank_group - 1)); };
   // a local pair stays with its CTA; a cross pair goes to the lighter of its two CTAs
   auto assign = [&](uint32_t i, uint32_t j, std::vector<int64_t>& load) {
     const int oi = owner(i), oj = owner(j);
@@ -919,7 +1286,9 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   S.zero_slot.resize((size_t)n_parts);
   for (int r = 0; r < n_parts; ++r)
     S.zero_slot[r] = ((uint32_t)r << S.slot_bits) | (S.part_start[r + 1] - S.part_start[r]);
+  if (S.product) S.zero_slot[0] = S.n_slots;
   for (int r = 0; r < n_parts; ++r) S.hmax = std::max(S.hmax, S.part_start[r + 1] - S.part_start[r]);
+  if (S.product) S.hmax = S.n_slots;
   S.buf_off = S.hmax + 1;
   {
     const uint64_t lim = std::min<uint64_t>(cap_amps, 1ull << S.slot_bits);
@@ -930,6 +1299,16 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   }
   const bool buffered = S.buf_len > 0;
   S.exp_pair_count = (int64_t)ek.size();
+  std::vector<uint8_t> in_block(ek.size(), 0);
+  if (S.product) {
+    std::vector<std::pair<uint32_t, uint32_t>> ij(ek.size());
+    std::vector<double> fv(ek.size());
+    for (size_t t = 0; t < ek.size(); ++t) {
+      ij[t] = {(uint32_t)idx[ek[t].m], (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x]};
+      fv[t] = ek[t].fr;
+    }
+    compile_blocks(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_block);
+  }
   std::vector<uint8_t> eown(ek.size());
   {  // balance: with the chunk buffer a cross pair costs about what a local one does
     std::vector<int64_t> load((size_t)n_parts, 0);
@@ -963,7 +1342,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     };
     std::map<int64_t, std::vector<size_t>> secs;  // ek indices in (group, pattern) order
     for (size_t t = 0; t < ek.size(); ++t) {
-      if (eown[t] != r) continue;
+      if (eown[t] != r || in_block[t]) continue;
       const uint32_t i = (uint32_t)idx[ek[t].m], j = (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x];
       secs[key_of(i, j)].push_back(t);
     }
@@ -1060,6 +1439,34 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   if (S.f_real) {
     S.row_fim.clear();
     S.pf_im.clear();
+  }
+  if (S.product) {
+    // warps take equal shares of the generic rows (the kernel splits them
+    // evenly); block units go to the least-loaded warp, largest first, and
+    // are stored warp by warp
+    const int nw = block_warps;
+    const auto& es = S.sections[0];
+    const double generic = (es.sh1 - es.sh0) * 7.5 + (es.pp1 - es.sh1) * 9.0;
+    const size_t nu = S.blk_units.size() / 8;
+    std::vector<size_t> ord(nu);
+    for (size_t u = 0; u < nu; ++u) ord[u] = u;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+      return block_unit_cost(&S.blk_units[8 * a]) > block_unit_cost(&S.blk_units[8 * b]);
+    });
+    (void)generic;
+    // round robin in block order (units of one alpha flip mask run on all warps
+    // at about the same time, so the shared-row f values they read through the
+    // constant cache stay few)
+    std::vector<std::vector<size_t>> mine((size_t)nw);
+    for (size_t u = 0; u < nu; ++u) mine[u % (size_t)nw].push_back(u);
+    std::vector<int32_t> units;
+    S.blk_warp_off.assign(1, 0);
+    for (int w = 0; w < nw; ++w) {
+      std::sort(mine[w].begin(), mine[w].end());
+      for (size_t u : mine[w]) units.insert(units.end(), &S.blk_units[8 * u], &S.blk_units[8 * u] + 8);
+      S.blk_warp_off.push_back((int32_t)(units.size() / 8));
+    }
+    S.blk_units.swap(units);
   }
   S.ok = true;
   return S;

@@ -42,6 +42,24 @@ struct SectorDev {
   const double* row_fim;        // nullptr when every f is real
   const double* pf_re;          // [per-pair rows * 32]
   const double* pf_im;          // nullptr when every f is real
+  // product layout + anchored string blocks (real one-CTA program; SectorProgram::blk_*)
+  uint32_t n_slots;             // amplitude slots (zero slot = n_slots)
+  const int32_t* blk_warp_off;  // nullptr: no blocks
+  const int4* blk_units;        // [units * 2]: {lw_off, sh_off, pl_off, pf_off}, {nc, nsh, npl, 0}
+  const uint32_t* blk_lanes;
+  const uint32_t* blk_sh;
+  const uint32_t* blk_plo;
+  const double* blk_plf;
+  const double* blk_shf;        // [shared rows] f per row (FM 2)
+  const double* ftab_host;      // host copy of the shared-row f table (launch parameter), n_ftab values
+  int n_ftab;
+};
+
+// shared-row f values of the anchored blocks, passed by value as a
+// __grid_constant__ kernel parameter: rows read them through the constant
+// cache, keeping the LSU for the amplitude loads
+struct FTab {
+  double f[kFTabMax];
 };
 
 // Amplitude slots (SectorProgram::slot_bits): 15 - log2(CL) offset bits, the
@@ -380,11 +398,81 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
 // per member, fma(f, b a, acc) per pair), so this kernel stores the real parts
 // only: 8 B per amplitude, the 18-qubit closure (15 876 amplitudes, 127 KB)
 // in ONE CTA's shared memory -- no cluster, no DSMEM, CTA barriers only.
-template <int NT>
+// One anchored block unit (SectorProgram::blk_*, one lane chunk) on one warp:
+// lane l holds its anchor a = psi[anchor slot] and partner base B; row r adds
+// (-1)^sign * f * psi[B + O_r] to the lane's partner sum t, and the unit
+// contributes a * t. A shared row is one 4-B word per lane (O_r | sign << 15 |
+// f index << 16, f from the parameter-space table), streamed four rows per
+// trip through two register buffers (no copies of loads in flight); per-lane
+// rows carry O_r plus f per lane.
+// FM: where a shared row's f comes from -- 0: the parameter-space table
+// (constant cache, LDC), 1: a copy of the table in shared memory (broadcast
+// LDS), 2: per-row f preloaded one per lane, 32 rows at a time (SHFL)
+template <int FM>
+__device__ __forceinline__ double blk_f(uint32_t w, const FTab& ft, const double* sft, double fl, int r) {
+  if (FM == 0) return ft.f[w >> 16];
+  if (FM == 1) return sft[w >> 16];
+  return __shfl_sync(0xFFFFFFFFu, fl, r & 31);
+}
+
+template <int FM>
+__device__ __forceinline__ double blk_trip(const uint32_t (&d)[4], const char* ab, uint32_t bb, const FTab& ft,
+                                           const double* sft, double fl, int r, double t) {
+  double b[4], f[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    b[u] = *reinterpret_cast<const double*>(ab + bb + (d[u] & 0x7FFFu) * 8u);
+    f[u] = blk_f<FM>(d[u], ft, sft, fl, r + u);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    // sign bit 15 of the word -> bit 31 of f's high word
+    const uint32_t hi = (uint32_t)__double2hiint(f[u]) ^ ((d[u] << 16) & 0x80000000u);
+    t = fma(__hiloint2double((int)hi, __double2loint(f[u])), b[u], t);
+  }
+  return t;
+}
+
+template <int FM>
+__device__ __forceinline__ double blk_unit(const SectorDev& sd, int4 h0, int4 h1, int lane, const double* amp,
+                                           const FTab& ft, const double* sft) {
+  const char* ab = reinterpret_cast<const char*>(amp);
+  const uint32_t w = __ldg(sd.blk_lanes + (size_t)h0.x * 32 + lane);
+  const double a = amp[w & 0x7FFFu];
+  const uint32_t bb = ((w >> 15) & 0x7FFFu) * 8u;
+  double t = 0.0;
+  const int nsh = h1.y, npl = h1.z;  // nsh: a multiple of 4
+  const uint32_t* rw = sd.blk_sh + (size_t)h0.y * 32 + lane;
+  uint32_t A[4], B[4];
+  auto fetch = [&](uint32_t (&d)[4], int r) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[u] = r < nsh ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
+  };
+  double fl = 0.0;
+  if (FM == 2 && lane < nsh) fl = __ldg(sd.blk_shf + h0.y + lane);
+  fetch(A, 0);
+  fetch(B, 4);
+  for (int r = 0; r < nsh; r += 8) {
+    if (FM == 2 && r > 0 && (r & 31) == 0) fl = r + lane < nsh ? __ldg(sd.blk_shf + h0.y + r + lane) : 0.0;
+    t = blk_trip<FM>(A, ab, bb, ft, sft, fl, r, t);
+    fetch(A, r + 8);
+    if (r + 4 < nsh) t = blk_trip<FM>(B, ab, bb, ft, sft, fl, r + 4, t);
+    fetch(B, r + 12);
+  }
+  for (int r = 0; r < npl; ++r) {
+    const uint32_t o = __ldg(sd.blk_plo + h0.z + r);
+    const double fv = __ldg(sd.blk_plf + ((size_t)h0.w + r) * 32 + lane);
+    t = fma(fv, *reinterpret_cast<const double*>(ab + bb + o), t);
+  }
+  return a * t;
+}
+
+template <int NT, int FM>
 __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
-                                                            int n_rows, long long* __restrict__ phase_clk) {
+                                                            int n_rows, long long* __restrict__ phase_clk,
+                                                            const __grid_constant__ FTab ftab) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
   extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -392,12 +480,15 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   const long long clk0 = clock64();
   const int row = blockIdx.x;
   if (row >= n_rows) return;
-  const uint32_t na = sd.size + 1;
+  const uint32_t na = sd.n_slots + 1;
   double* amp = reinterpret_cast<double*>(sm_raw);
   double2* cs = reinterpret_cast<double2*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
   double2* fz = cs + pl.n_ops;
   uint2* gse = reinterpret_cast<uint2*>(fz + pl.n_ops);
+  double* sft = reinterpret_cast<double*>(gse + pl.n_ops);  // FM 1: f table
   for (uint32_t i = threadIdx.x; i < na; i += NT) amp[i] = 0.0;
+  if (FM == 1)
+    for (int i = threadIdx.x; i < sd.n_ftab; i += NT) sft[i] = ftab.f[i];
   for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
     const double phi = theta[(int64_t)row * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
     double sv, cv;
@@ -515,6 +606,12 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
         const uint32_t w = __ldg(p + 32 * u);
         const double fr = __ldg(sd.pf_re + fo + 32 * u);
         acc = fma(amp[(w >> 15) & 0x7FFFu] * amp[w & 0x7FFFu], fr, acc);
+      }
+    }
+    if (sd.blk_warp_off) {  // this warp's anchored block units
+      for (int u = __ldg(sd.blk_warp_off + warp); u < __ldg(sd.blk_warp_off + warp + 1); ++u) {
+        const int4 h0 = __ldg(sd.blk_units + 2 * u), h1 = __ldg(sd.blk_units + 2 * u + 1);
+        acc += blk_unit<FM>(sd, h0, h1, lane, amp, ftab, sft);
       }
     }
   }

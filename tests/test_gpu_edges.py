@@ -207,6 +207,10 @@ def test_sector_info_config3(monkeypatch, real):
     assert info["cluster_barrier_steps"] <= P.n_gen
     assert info["expectation_rows"] * 32 >= info["expectation_pairs"] > 0
     assert info["generator_pairs"] > 0
+    # the real program lays S out as 126 alpha x 127 (odd stride) beta slots and
+    # holds most expectation pairs in anchored string blocks
+    assert info["slots"] == (126 * 127 if real == "1" else 15876)
+    assert (info["block_pairs"] >= 0.9 * info["expectation_pairs"]) == (real == "1")
 
 
 @pytest.mark.parametrize("config", [2, 3])

@@ -183,3 +183,31 @@ def test_shard_schedule_is_a_valid_swap_sequence(g):
     assert all(uses[q] <= min(uses[[r for r in range(18) if r not in glob]]) for q in glob)
     if g == 0:
         assert ns == 0 and ip.tolist() == list(range(18))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_sector_program_emulation_matches_oracle(oracle, cfg):
+    """The real one-CTA sector program's expectation tables (product slot
+    layout + anchored string blocks at 18 qubits, generic rows below), run on
+    the host exactly as k_sector_eval_real reads them, against the oracle's
+    term-by-term <psi|H|psi> on a random real sector state."""
+    P = problems.config_problem(cfg)
+    n = P.n_qubits
+    k = np.arange(1 << n, dtype=np.int64)
+    am = sum(1 << q for q in range(0, n, 2))
+    pop = np.vectorize(lambda v: bin(v).count("1"))
+    pa, pb = pop(k & am), pop(k & ~am & ((1 << n) - 1))
+    na, nb = bin(P.hf & am).count("1"), bin(P.hf & ~am).count("1")
+    rng = np.random.default_rng(cfg)
+    psi = np.where((pa == na) & (pb == nb), rng.standard_normal(1 << n), 0.0)
+    psi /= np.linalg.norm(psi)
+    r = capi.sector_emulate(n, P.plan_arrays(), P.ham_arrays(), P.hf, psi)
+    H = oracle.PauliSum.from_terms(n, *P.ham_arrays())
+    ref = oracle.expectation(n, psi.astype(np.complex128), H)
+    assert abs(r["energy"] - ref.real) <= 1e-12
+    assert r["closure_size"] == int(((pa == na) & (pb == nb)).sum())
+    if cfg == 3:  # 18 qubits: (5a, 5b) sector = 126 x 126 strings, stride 127
+        assert r["product"] == 1 and r["slots"] == 126 * 127
+        assert r["block_pairs"] >= 0.9 * r["exp_pairs"] and r["units"] > 0
+    else:  # small closures keep the natural layout (256-thread program)
+        assert r["product"] == 0 and r["block_pairs"] == 0
