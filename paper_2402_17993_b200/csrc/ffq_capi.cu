@@ -96,7 +96,6 @@ struct ffq_ctx_s {
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
-  int blk_fmode = 1;                             // env FFQ_BLK_F: shared-row f from 0 params / 1 smem (default) / 2 shfl
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
@@ -138,9 +137,9 @@ struct ffq_plan_s {
     DevBuf<int32_t> secs;
     DevBuf<uint8_t> gen_flags, op_cross;
     DevBuf<double> row_fre, row_fim, pf_re, pf_im;
-    DevBuf<int32_t> blk_warp_off, blk_units;
-    DevBuf<uint32_t> blk_lanes, blk_sh, blk_plo;
-    DevBuf<double> blk_plf, blk_shf;
+    DevBuf<int32_t> blk_warp;
+    DevBuf<uint32_t> blk_stream;
+    DevBuf<double> ftab;
     bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
@@ -450,7 +449,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, real_ok ? 8 : 16,
                              real_ok && ctx->sector_blocks ? kSectorRealThreads / 32 : 0, kSectorSingleMax);
     b->real = b->prog.ok && real_ok &&
-              sector_real_smem_bytes(b->prog.n_slots, pl->cp.op_kind.size()) <= ctx->smem_optin;
+              sector_real_smem_bytes(b->prog.n_slots, pl->cp.op_kind.size()) +
+                      b->prog.ftab.size() * sizeof(double) <= ctx->smem_optin;
     if (b->prog.ok && !b->real && sector_parts(ctx, b->prog.size) > 1)
       b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
                                (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)), 4);
@@ -466,14 +466,10 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
       b->secs.upload(secs, ctx->stream);
       b->row_fre.upload(b->prog.row_fre, ctx->stream);
       b->pf_re.upload(b->prog.pf_re, ctx->stream);
-      if (b->prog.product) {
-        b->blk_warp_off.upload(b->prog.blk_warp_off, ctx->stream);
-        b->blk_units.upload(b->prog.blk_units, ctx->stream);
-        b->blk_lanes.upload(b->prog.blk_lanes, ctx->stream);
-        b->blk_sh.upload(b->prog.blk_sh, ctx->stream);
-        b->blk_plo.upload(b->prog.blk_plo, ctx->stream);
-        b->blk_plf.upload(b->prog.blk_plf, ctx->stream);
-        b->blk_shf.upload(b->prog.blk_shf, ctx->stream);
+      if (b->prog.product && !b->prog.blk_warp.empty()) {
+        b->blk_warp.upload(b->prog.blk_warp, ctx->stream);
+        b->blk_stream.upload(b->prog.blk_stream, ctx->stream);
+        b->ftab.upload(b->prog.ftab, ctx->stream);
       }
       if (!b->prog.f_real) {
         b->row_fim.upload(b->prog.row_fim, ctx->stream);
@@ -510,16 +506,11 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.n_parts = b.prog.n_parts;
   sd.real = b.real ? 1 : 0;
   sd.n_slots = b.prog.n_slots;
-  const bool blk = b.prog.product && !b.prog.blk_warp_off.empty();
-  sd.blk_warp_off = blk ? b.blk_warp_off.p : nullptr;
-  sd.blk_units = blk ? reinterpret_cast<const int4*>(b.blk_units.p) : nullptr;
-  sd.blk_lanes = blk ? b.blk_lanes.p : nullptr;
-  sd.blk_sh = blk ? b.blk_sh.p : nullptr;
-  sd.ftab_host = b.prog.ftab.data();
-  sd.n_ftab = (int)b.prog.ftab.size();
-  sd.blk_plo = blk ? b.blk_plo.p : nullptr;
-  sd.blk_plf = blk ? b.blk_plf.p : nullptr;
-  sd.blk_shf = blk ? b.blk_shf.p : nullptr;
+  const bool blk = b.prog.product && !b.prog.blk_warp.empty();
+  sd.blk_warp = blk ? reinterpret_cast<const int4*>(b.blk_warp.p) : nullptr;
+  sd.blk_stream = blk ? b.blk_stream.p : nullptr;
+  sd.ftab = blk ? b.ftab.p : nullptr;
+  sd.n_ftab = blk ? (int)b.prog.ftab.size() : 0;
   return &sd;
 }
 
@@ -547,27 +538,15 @@ void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, c
   ctx->launches++;
 }
 
-template <int NT, int FM>
-void launch_sector_real_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
-                          double* e, double* im, long long* clk) {
-  // FM 1 keeps a copy of the shared-row f table behind the per-op tables
-  const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) +
-                    (FM == 1 ? (size_t)sd.n_ftab * sizeof(double) : 0);
-  CK(cudaFuncSetAttribute(k_sector_eval_real<NT, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  static thread_local FTab ft;
-  std::memset(&ft, 0, sizeof(ft));
-  if (sd.n_ftab > 0) std::memcpy(ft.f, sd.ftab_host, (size_t)std::min(sd.n_ftab, kFTabMax) * sizeof(double));
-  k_sector_eval_real<NT, FM><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, ft);
-  CK(cudaGetLastError());
-  ctx->launches++;
-}
-
 template <int NT>
 void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
                         double* e, double* im, long long* clk) {
-  if (!sd.blk_warp_off || ctx->blk_fmode == 0) launch_sector_real_t<NT, 0>(ctx, pl, sd, theta, batch, e, im, clk);
-  else if (ctx->blk_fmode == 1) launch_sector_real_t<NT, 1>(ctx, pl, sd, theta, batch, e, im, clk);
-  else launch_sector_real_t<NT, 2>(ctx, pl, sd, theta, batch, e, im, clk);
+  // anchored blocks keep the shared-row f table behind the per-op tables
+  const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) + (size_t)sd.n_ftab * sizeof(double);
+  CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  k_sector_eval_real<NT><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk);
+  CK(cudaGetLastError());
+  ctx->launches++;
 }
 
 void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
@@ -808,7 +787,6 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
-    if (const char* e = std::getenv("FFQ_BLK_F")) c->blk_fmode = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);
       c->sector_cl = (v == 4 || v == 8) ? v : 2;
@@ -981,7 +959,7 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
     out[1] = S.n_parts;
     out[2] = (int64_t)S.gen_pairs.size();
     out[3] = S.exp_pair_count;
-    out[4] = (int64_t)(S.row_pairs.size() / 32 + S.blk_sh.size() / 32 + S.blk_plo.size());
+    out[4] = (int64_t)(S.row_pairs.size() / 32 + S.blk_stream.size() / 32);
     out[5] = cluster_steps;
     out[6] = S.split_masks.empty() ? 0 : (int64_t)S.split_masks[0];
     out[7] = S.buf_len;
@@ -1000,24 +978,36 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
   return guarded(ctx, [&] {
     const int ng = plan->cp.n_gen;
     const size_t nth = (size_t)batch * ng;
-    // host -> pinned staging -> device (one H2D), energies + residues back (one D2H)
-    ctx->ensure_pinned(std::max<size_t>(nth, 2 * (size_t)batch));
+    // host -> pinned staging -> device, energies + residues back (one D2H). A
+    // large batch goes in chunks of whole SM waves: the host copies chunk c + 1
+    // into the staging buffer and its H2D is queued while chunk c computes
+    // (energies are bitwise independent of the split).
+    ctx->ensure_pinned(nth + 2 * (size_t)batch);
+    double* stage_e = ctx->pinned + nth;
     DevBuf<double>& th = ctx->io_theta;
     DevBuf<double>& eo = ctx->io_e;
     th.alloc(std::max<size_t>(1, nth));
     eo.alloc(2 * (size_t)batch);
-    if (nth) {
-      std::memcpy(ctx->pinned, theta, nth * sizeof(double));
-      CK(cudaMemcpyAsync(th.p, ctx->pinned, nth * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    int chunk = batch;
+    if (nth * sizeof(double) >= (size_t)(1 << 20)) {
+      const int wave = std::max(1, ctx->n_sm);
+      chunk = std::max(wave, (batch / 4 + wave - 1) / wave * wave);
     }
-    energy_device(ctx, plan, ham, hf_bits, batch, th.p, eo.p, eo.p + batch);
-    CK(cudaMemcpyAsync(ctx->pinned, eo.p, 2 * sizeof(double) * batch, cudaMemcpyDeviceToHost,
-                       ctx->stream));
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+      const int nb = std::min(chunk, batch - b0);
+      const size_t o = (size_t)b0 * ng, n = (size_t)nb * ng;
+      if (n) {
+        std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
+        CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      }
+      energy_device(ctx, plan, ham, hf_bits, nb, th.p + o, eo.p + b0, eo.p + batch + b0);
+    }
+    CK(cudaMemcpyAsync(stage_e, eo.p, 2 * sizeof(double) * batch, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(e_out, ctx->pinned, sizeof(double) * batch);
+    std::memcpy(e_out, stage_e, sizeof(double) * batch);
     for (int b = 0; b < batch; ++b)
-      if (std::abs(ctx->pinned[batch + b]) > 1e-10)
-        throw BadInput("energy has imaginary residue " + std::to_string(ctx->pinned[batch + b]) +
+      if (std::abs(stage_e[batch + b]) > 1e-10)
+        throw BadInput("energy has imaginary residue " + std::to_string(stage_e[batch + b]) +
                            " > 1e-10 (non-Hermitian Hamiltonian?)",
                        FFQ_ENONHERMITIAN);
     return FFQ_OK;
@@ -1230,21 +1220,23 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
         e += f * amp[w & 0x7FFFu] * amp[(w >> 15) & 0x7FFFu];
       }
     const size_t nu = S.blk_units.size() / 8;
-    for (size_t u = 0; u < nu; ++u) {
-      const int32_t* h = &S.blk_units[8 * u];
-      const int nsh = h[5], npl = h[6];
+    for (size_t w = 0; w < S.blk_warp.size() / 4; ++w) {  // the device's per-warp row streams
+      const int32_t* h = &S.blk_warp[4 * w];
       for (int l = 0; l < 32; ++l) {
-        const uint32_t w = S.blk_lanes[(size_t)h[0] * 32 + l];
-        const double a = amp[w & 0x7FFFu];
-        const uint32_t bs = (w >> 15) & 0x7FFFu;
-        double t = 0.0;
-        for (int r = 0; r < nsh; ++r) {
-          const uint32_t d = S.blk_sh[((size_t)h[1] + r) * 32 + l];
-          const double f = S.ftab.at(d >> 16);
-          t += ((d >> 15) & 1u ? -f : f) * amp.at(bs + (d & 0x7FFFu));
+        double a = 0.0, t = 0.0;
+        uint32_t bs = 0;
+        for (int r = h[0]; r < h[1]; ++r) {
+          const uint32_t d = S.blk_stream[(size_t)r * 32 + l];
+          if (d >> 30) {
+            e += a * t;
+            a = amp.at(d & 0x7FFFu);
+            bs = (d >> 15) & 0x7FFFu;
+            t = 0.0;
+          } else {
+            const double f = S.ftab.at(d >> 16);
+            t += ((d >> 15) & 1u ? -f : f) * amp.at(bs + (d & 0x7FFFu));
+          }
         }
-        for (int r = 0; r < npl; ++r)
-          t += S.blk_plf[((size_t)h[3] + r) * 32 + l] * amp.at(bs + S.blk_plo[h[2] + r] / 8);
         e += a * t;
       }
     }

@@ -742,13 +742,21 @@ struct SectorProgram {
   std::vector<double> blk_plf;         // per-lane rows: [row][32] f
   std::vector<double> ftab;            // distinct shared-row f values
   std::vector<double> blk_shf;         // [shared rows] f per row
+  // Per-warp row streams (what the device runs): the units of warp w back to
+  // back, rows [blk_warp[4w], blk_warp[4w+1]) of 32 lane words each:
+  //   bit 30 clear: shared row  O | sign << 15 | ftab index << 16
+  //   bit 30 set:   anchor row  anchor slot | B slot << 15 | 1 << 30 (closes the previous unit)
+  std::vector<uint32_t> blk_stream;
+  std::vector<double> blk_fs;
+  std::vector<int32_t> blk_warp;
   int64_t blk_pairs = 0;               // expectation pairs held by the blocks
 };
 
 constexpr int kBlockMaxNC = 1;        // lane chunks per unit (the device runs one)
 constexpr int kFTabMax = 3968;        // shared-row f values (kernel parameter space, 31 KiB)
 constexpr int kBlockMinLanes = 16;    // smaller chunks go to the generic rows
-constexpr int kBlockRowQuantum = 4;   // shared rows per unit padded to a multiple of this
+constexpr int kBlockRowQuantum = 1;   // shared rows per unit padded to a multiple of this
+constexpr int kStreamQuantum = 16;    // rows per warp stream padded to a multiple of this
 
 // Anchored string blocks for the expectation pairs of a product-layout sector
 // (see SectorProgram). For pair (i, j = i ^ X) with X = Xa | Xb (alpha / beta
@@ -924,19 +932,13 @@ inline void compile_blocks(SectorProgram& S, const std::vector<uint32_t>& list,
           S.blk_sh.push_back(sh2[k].first | (neg << 15) | (fidx[k] << 16));
         }
       }
+      // rows without one shared |f| (singles: f depends on the other
+      // occupations) stay in the generic per-pair rows
       hdr[2] = (int32_t)S.blk_plo.size();
       hdr[3] = (int32_t)(S.blk_plf.size() / 32);
-      hdr[6] = (int32_t)pl.size();
-      std::sort(pl.begin(), pl.end());
-      for (const auto& [r, cp] : pl) {
-        S.blk_plo.push_back(r * 8);
-        for (int l = 0; l < 32; ++l) {
-          const int64_t u = (*cp)[l];
-          S.blk_plf.push_back(u >= 0 ? f[bp[u].t] : 0.0);
-        }
-      }
-      for (const auto& [r, cells] : rows)
-        for (int64_t u : cells)
+      hdr[6] = 0;
+      for (const auto& e : sh2)
+        for (int64_t u : *e.second)
           if (u >= 0) {
             in_block[bp[u].t] = 1;
             ++S.blk_pairs;
@@ -1443,30 +1445,36 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   if (S.product) {
     // warps take equal shares of the generic rows (the kernel splits them
     // evenly); block units go to the least-loaded warp, largest first, and
-    // are stored warp by warp
+    // each warp's units become one row stream
     const int nw = block_warps;
     const auto& es = S.sections[0];
     const double generic = (es.sh1 - es.sh0) * 7.5 + (es.pp1 - es.sh1) * 9.0;
     const size_t nu = S.blk_units.size() / 8;
     std::vector<size_t> ord(nu);
     for (size_t u = 0; u < nu; ++u) ord[u] = u;
-    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-      return block_unit_cost(&S.blk_units[8 * a]) > block_unit_cost(&S.blk_units[8 * b]);
-    });
-    (void)generic;
-    // round robin in block order (units of one alpha flip mask run on all warps
-    // at about the same time, so the shared-row f values they read through the
-    // constant cache stay few)
+    auto ucost = [&](size_t u) { const int32_t* h = &S.blk_units[8 * u]; return 4.0 * (1 + h[5]) + 6.0 * h[6]; };
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ucost(a) > ucost(b); });
+    std::vector<double> load((size_t)nw, generic / nw);
     std::vector<std::vector<size_t>> mine((size_t)nw);
-    for (size_t u = 0; u < nu; ++u) mine[u % (size_t)nw].push_back(u);
-    std::vector<int32_t> units;
-    S.blk_warp_off.assign(1, 0);
+    for (size_t u : ord) {
+      const size_t w = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[w] += ucost(u);
+      mine[w].push_back(u);
+    }
+    S.blk_warp.clear();
     for (int w = 0; w < nw; ++w) {
       std::sort(mine[w].begin(), mine[w].end());
-      for (size_t u : mine[w]) units.insert(units.end(), &S.blk_units[8 * u], &S.blk_units[8 * u] + 8);
-      S.blk_warp_off.push_back((int32_t)(units.size() / 8));
+      const int32_t r0 = (int32_t)(S.blk_stream.size() / 32), f0 = (int32_t)(S.blk_fs.size() / 32);
+      for (size_t u : mine[w]) {
+        const int32_t* h = &S.blk_units[8 * u];
+        for (int l = 0; l < 32; ++l) S.blk_stream.push_back(S.blk_lanes[(size_t)h[0] * 32 + l] | (1u << 30));
+        for (int r = 0; r < h[5]; ++r)
+          S.blk_stream.insert(S.blk_stream.end(), &S.blk_sh[((size_t)h[1] + r) * 32],
+                              &S.blk_sh[((size_t)h[1] + r) * 32] + 32);
+      }
+      while ((S.blk_stream.size() / 32 - r0) % kStreamQuantum) S.blk_stream.insert(S.blk_stream.end(), 32, 0u);
+      S.blk_warp.insert(S.blk_warp.end(), {r0, (int32_t)(S.blk_stream.size() / 32), f0, 0});
     }
-    S.blk_units.swap(units);
   }
   S.ok = true;
   return S;

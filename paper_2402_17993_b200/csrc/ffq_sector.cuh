@@ -44,22 +44,10 @@ struct SectorDev {
   const double* pf_im;          // nullptr when every f is real
   // product layout + anchored string blocks (real one-CTA program; SectorProgram::blk_*)
   uint32_t n_slots;             // amplitude slots (zero slot = n_slots)
-  const int32_t* blk_warp_off;  // nullptr: no blocks
-  const int4* blk_units;        // [units * 2]: {lw_off, sh_off, pl_off, pf_off}, {nc, nsh, npl, 0}
-  const uint32_t* blk_lanes;
-  const uint32_t* blk_sh;
-  const uint32_t* blk_plo;
-  const double* blk_plf;
-  const double* blk_shf;        // [shared rows] f per row (FM 2)
-  const double* ftab_host;      // host copy of the shared-row f table (launch parameter), n_ftab values
+  const int4* blk_warp;         // [warps]: row stream [x, y); nullptr: no blocks
+  const uint32_t* blk_stream;   // [rows * 32] lane words
+  const double* ftab;           // [n_ftab] shared-row f values (copied to shared memory)
   int n_ftab;
-};
-
-// shared-row f values of the anchored blocks, passed by value as a
-// __grid_constant__ kernel parameter: rows read them through the constant
-// cache, keeping the LSU for the amplitude loads
-struct FTab {
-  double f[kFTabMax];
 };
 
 // Amplitude slots (SectorProgram::slot_bits): 15 - log2(CL) offset bits, the
@@ -405,74 +393,80 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
 // f index << 16, f from the parameter-space table), streamed four rows per
 // trip through two register buffers (no copies of loads in flight); per-lane
 // rows carry O_r plus f per lane.
-// FM: where a shared row's f comes from -- 0: the parameter-space table
-// (constant cache, LDC), 1: a copy of the table in shared memory (broadcast
-// LDS), 2: per-row f preloaded one per lane, 32 rows at a time (SHFL)
-template <int FM>
-__device__ __forceinline__ double blk_f(uint32_t w, const FTab& ft, const double* sft, double fl, int r) {
-  if (FM == 0) return ft.f[w >> 16];
-  if (FM == 1) return sft[w >> 16];
-  return __shfl_sync(0xFFFFFFFFu, fl, r & 31);
-}
-
-template <int FM>
-__device__ __forceinline__ double blk_trip(const uint32_t (&d)[4], const char* ab, uint32_t bb, const FTab& ft,
-                                           const double* sft, double fl, int r, double t) {
-  double b[4], f[4];
+// A warp's anchored-block row stream (SectorProgram::blk_stream): its units
+// back to back, four rows per trip through two register buffers of prefetched
+// lane words (no copies of loads in flight), so loads run ahead across unit
+// boundaries. Per lane: an anchor row loads a = psi[anchor] and the partner
+// base B (closing the previous unit: acc += a * t); a shared row adds
+// (-1)^sign * ftab[i] * psi[B + O] to t, f by broadcast from shared memory.
+// Trips without an anchor row (the common case) take the short path.
+__device__ __forceinline__ void blk_trip(const uint32_t (&d)[4], const double* amp, const double* sft, uint32_t& bs,
+                                         double& a, double& t, double& acc) {
+  if (((d[0] | d[1] | d[2] | d[3]) >> 30) == 0u) {
+    double v[4], f[4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    b[u] = *reinterpret_cast<const double*>(ab + bb + (d[u] & 0x7FFFu) * 8u);
-    f[u] = blk_f<FM>(d[u], ft, sft, fl, r + u);
+    for (int u = 0; u < 4; ++u) {
+      v[u] = amp[bs + (d[u] & 0x7FFFu)];
+      f[u] = sft[d[u] >> 16];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // sign bit 15 of the word -> bit 31 of f's high word
+      const uint32_t hi = (uint32_t)__double2hiint(f[u]) ^ ((d[u] << 16) & 0x80000000u);
+      t = fma(__hiloint2double((int)hi, __double2loint(f[u])), v[u], t);
+    }
+    return;
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    // sign bit 15 of the word -> bit 31 of f's high word
-    const uint32_t hi = (uint32_t)__double2hiint(f[u]) ^ ((d[u] << 16) & 0x80000000u);
-    t = fma(__hiloint2double((int)hi, __double2loint(f[u])), b[u], t);
+    const uint32_t w = d[u];
+    if (w >> 30) {
+      acc = fma(a, t, acc);
+      a = amp[w & 0x7FFFu];
+      bs = (w >> 15) & 0x7FFFu;
+      t = 0.0;
+    } else {
+      const double f = sft[w >> 16];
+      const uint32_t hi = (uint32_t)__double2hiint(f) ^ ((w << 16) & 0x80000000u);
+      t = fma(__hiloint2double((int)hi, __double2loint(f)), amp[bs + (w & 0x7FFFu)], t);
+    }
   }
-  return t;
 }
 
-template <int FM>
-__device__ __forceinline__ double blk_unit(const SectorDev& sd, int4 h0, int4 h1, int lane, const double* amp,
-                                           const FTab& ft, const double* sft) {
-  const char* ab = reinterpret_cast<const char*>(amp);
-  const uint32_t w = __ldg(sd.blk_lanes + (size_t)h0.x * 32 + lane);
-  const double a = amp[w & 0x7FFFu];
-  const uint32_t bb = ((w >> 15) & 0x7FFFu) * 8u;
-  double t = 0.0;
-  const int nsh = h1.y, npl = h1.z;  // nsh: a multiple of 4
-  const uint32_t* rw = sd.blk_sh + (size_t)h0.y * 32 + lane;
+__device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int lane, const double* amp,
+                                             const double* sft) {
+  const int4 h = __ldg(sd.blk_warp + warp);
+  const uint32_t* rw = sd.blk_stream + lane;
   uint32_t A[4], B[4];
   auto fetch = [&](uint32_t (&d)[4], int r) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) d[u] = r < nsh ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
+    for (int u = 0; u < 4; ++u) d[u] = r < h.y ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
   };
-  double fl = 0.0;
-  if (FM == 2 && lane < nsh) fl = __ldg(sd.blk_shf + h0.y + lane);
-  fetch(A, 0);
-  fetch(B, 4);
-  for (int r = 0; r < nsh; r += 8) {
-    if (FM == 2 && r > 0 && (r & 31) == 0) fl = r + lane < nsh ? __ldg(sd.blk_shf + h0.y + r + lane) : 0.0;
-    t = blk_trip<FM>(A, ab, bb, ft, sft, fl, r, t);
-    fetch(A, r + 8);
-    if (r + 4 < nsh) t = blk_trip<FM>(B, ab, bb, ft, sft, fl, r + 4, t);
-    fetch(B, r + 12);
+  uint32_t bs = 0;
+  double a = 0.0, t = 0.0, acc = 0.0;
+  uint32_t C[4], D[4];
+  fetch(A, h.x);
+  fetch(B, h.x + 4);
+  fetch(C, h.x + 8);
+  fetch(D, h.x + 12);
+  for (int r = h.x; r < h.y; r += 16) {  // the stream is padded to whole 16-row rounds
+    blk_trip(A, amp, sft, bs, a, t, acc);
+    fetch(A, r + 16);
+    blk_trip(B, amp, sft, bs, a, t, acc);
+    fetch(B, r + 20);
+    blk_trip(C, amp, sft, bs, a, t, acc);
+    fetch(C, r + 24);
+    blk_trip(D, amp, sft, bs, a, t, acc);
+    fetch(D, r + 28);
   }
-  for (int r = 0; r < npl; ++r) {
-    const uint32_t o = __ldg(sd.blk_plo + h0.z + r);
-    const double fv = __ldg(sd.blk_plf + ((size_t)h0.w + r) * 32 + lane);
-    t = fma(fv, *reinterpret_cast<const double*>(ab + bb + o), t);
-  }
-  return a * t;
+  return fma(a, t, acc);
 }
 
-template <int NT, int FM>
+template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
-                                                            int n_rows, long long* __restrict__ phase_clk,
-                                                            const __grid_constant__ FTab ftab) {
+                                                            int n_rows, long long* __restrict__ phase_clk) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
   extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -485,10 +479,10 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   double2* cs = reinterpret_cast<double2*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
   double2* fz = cs + pl.n_ops;
   uint2* gse = reinterpret_cast<uint2*>(fz + pl.n_ops);
-  double* sft = reinterpret_cast<double*>(gse + pl.n_ops);  // FM 1: f table
+  double* sft = reinterpret_cast<double*>(gse + pl.n_ops);  // anchored blocks: shared-row f table
   for (uint32_t i = threadIdx.x; i < na; i += NT) amp[i] = 0.0;
-  if (FM == 1)
-    for (int i = threadIdx.x; i < sd.n_ftab; i += NT) sft[i] = ftab.f[i];
+  if (sd.blk_warp)
+    for (int i = threadIdx.x; i < sd.n_ftab; i += NT) sft[i] = __ldg(sd.ftab + i);
   for (int op = threadIdx.x; op < pl.n_ops; op += NT) {
     const double phi = theta[(int64_t)row * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
     double sv, cv;
@@ -503,9 +497,9 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   if (threadIdx.x == 0) amp[sd.hf_slot] = 1.0;
   __syncthreads();
   const uint32_t tid = threadIdx.x;
-  // each thread's first two pair words of the next three steps are in flight
+  // each thread's first two pair words of the next four steps are in flight
   // across the barriers (steps have up to ~2 NT pairs). The step loop is
-  // unrolled by three so the in-flight registers are never copied (a copy
+  // unrolled by four so the in-flight registers are never copied (a copy
   // would wait for the load).
   auto first_words = [&](int op) -> uint2 {
     if (op >= sd.n_ops) return make_uint2(0u, 0u);
@@ -537,18 +531,21 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     }
     __syncthreads();
   };
-  uint2 wa = first_words(0), wb = first_words(1), wc = first_words(2);
+  uint2 wa = first_words(0), wb = first_words(1), wc = first_words(2), wd = first_words(3);
   int op = 0;
-  for (; op + 3 <= sd.n_ops; op += 3) {
+  for (; op + 4 <= sd.n_ops; op += 4) {
     step(op, wa);
-    wa = first_words(op + 3);
+    wa = first_words(op + 4);
     step(op + 1, wb);
-    wb = first_words(op + 4);
+    wb = first_words(op + 5);
     step(op + 2, wc);
-    wc = first_words(op + 5);
+    wc = first_words(op + 6);
+    step(op + 3, wd);
+    wd = first_words(op + 7);
   }
   if (op < sd.n_ops) step(op, wa);
   if (op + 1 < sd.n_ops) step(op + 1, wb);
+  if (op + 2 < sd.n_ops) step(op + 2, wc);
   const long long clk1 = clock64();
   double acc = 0.0;
   {
@@ -608,12 +605,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
         acc = fma(amp[(w >> 15) & 0x7FFFu] * amp[w & 0x7FFFu], fr, acc);
       }
     }
-    if (sd.blk_warp_off) {  // this warp's anchored block units
-      for (int u = __ldg(sd.blk_warp_off + warp); u < __ldg(sd.blk_warp_off + warp + 1); ++u) {
-        const int4 h0 = __ldg(sd.blk_units + 2 * u), h1 = __ldg(sd.blk_units + 2 * u + 1);
-        acc += blk_unit<FM>(sd, h0, h1, lane, amp, ftab, sft);
-      }
-    }
+    if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
   }
   const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
   if (threadIdx.x == 0) {

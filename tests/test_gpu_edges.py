@@ -210,7 +210,7 @@ def test_sector_info_config3(monkeypatch, real):
     # the real program lays S out as 126 alpha x 127 (odd stride) beta slots and
     # holds most expectation pairs in anchored string blocks
     assert info["slots"] == (126 * 127 if real == "1" else 15876)
-    assert (info["block_pairs"] >= 0.9 * info["expectation_pairs"]) == (real == "1")
+    assert (info["block_pairs"] >= 0.8 * info["expectation_pairs"]) == (real == "1")
 
 
 @pytest.mark.parametrize("config", [2, 3])

@@ -208,6 +208,6 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
     assert r["closure_size"] == int(((pa == na) & (pb == nb)).sum())
     if cfg == 3:  # 18 qubits: (5a, 5b) sector = 126 x 126 strings, stride 127
         assert r["product"] == 1 and r["slots"] == 126 * 127
-        assert r["block_pairs"] >= 0.9 * r["exp_pairs"] and r["units"] > 0
+        assert r["block_pairs"] >= 0.8 * r["exp_pairs"] and r["units"] > 0
     else:  # small closures keep the natural layout (256-thread program)
         assert r["product"] == 0 and r["block_pairs"] == 0
