@@ -293,30 +293,46 @@ def main():
     rot_avg = statistics.mean(rot_ms[2:])
     achieved = rot_bytes / (rot_avg / 1e3) / 1e9
 
-    # secondary: the same step through the support-tracked dense-slab path
-    # (FFQ_SECTOR=0): every generator a [chunk][2^n] pass restricted to set
-    # support bits, i.e. no support-closure compilation
-    os.environ["FFQ_SECTOR"] = "0"
-    ctx_d = capi.Context(local)
-    os.environ.pop("FFQ_SECTOR")
-    stream_d = torch.cuda.ExternalStream(ctx_d.stream_ptr(), device=torch.device("cuda", local))
-    plan_d = capi.Plan(ctx_d, P.n_qubits, *P.plan_arrays())
-    ham_d = capi.Hamiltonian(ctx_d, P.n_qubits, *P.ham_arrays())
-    e_d = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
-    f_d = lambda: capi.energy_batch_device(ctx_d, plan_d, ham_d, P.hf, B, th_dev.data_ptr(), e_d.data_ptr())  # noqa: E731
-    f_d()
-    ctx_d.synchronize()
-    with torch.cuda.stream(stream_d):
-        a_ev = torch.cuda.Event(enable_timing=True)
-        b_ev = torch.cuda.Event(enable_timing=True)
-        a_ev.record(stream_d)
+    def other_path(env):
+        """The same step (same theta rows, device-resident) through another
+        execution path selected by FFQ_* knobs read at context creation."""
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        ctx_d = capi.Context(local)
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
+        stream_d = torch.cuda.ExternalStream(ctx_d.stream_ptr(), device=torch.device("cuda", local))
+        plan_d = capi.Plan(ctx_d, P.n_qubits, *P.plan_arrays())
+        ham_d = capi.Hamiltonian(ctx_d, P.n_qubits, *P.ham_arrays())
+        e_d = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
+        f_d = lambda: capi.energy_batch_device(ctx_d, plan_d, ham_d, P.hf, B, th_dev.data_ptr(), e_d.data_ptr())  # noqa: E731
         f_d()
-        b_ev.record(stream_d)
-        b_ev.synchronize()
-    dense_path = {"evals_per_s": B / (a_ev.elapsed_time(b_ev) / 1e3),
-                  "max_abs_diff_vs_value_path": float((e_d - e_dev).abs().max().item()),
-                  "path": "support-tracked [chunk][2^n] slab, CUDA graph of per-generator passes"}
-    del plan_d, ham_d, ctx_d
+        ctx_d.synchronize()
+        with torch.cuda.stream(stream_d):
+            a_ev = torch.cuda.Event(enable_timing=True)
+            b_ev = torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream_d)
+            f_d()
+            b_ev.record(stream_d)
+            b_ev.synchronize()
+        out = {"evals_per_s": B / (a_ev.elapsed_time(b_ev) / 1e3),
+               "max_abs_diff_vs_value_path": float((e_d - e_dev).abs().max().item())}
+        del plan_d, ham_d, ctx_d
+        return out
+
+    # secondary: the same step through the complex128 support-closure program
+    # (FFQ_SECTOR_REAL=0: full (re, im) amplitudes, 2-CTA clusters), i.e. the
+    # c128 arithmetic without the real-amplitude specialisation
+    complex_path = other_path({"FFQ_SECTOR_REAL": "0"})
+    complex_path["path"] = "k_sector_eval<2,768>: complex128 amplitudes over 2-CTA clusters (DSMEM)"
+    # secondary: the support-tracked dense-slab path (FFQ_SECTOR=0): every
+    # generator a [chunk][2^n] pass restricted to set support bits, i.e. no
+    # support-closure compilation
+    dense_path = other_path({"FFQ_SECTOR": "0"})
+    dense_path["path"] = "support-tracked [chunk][2^n] slab, CUDA graph of per-generator passes"
 
     # secondary: BASELINE.json config 2 -- 64 theta vectors x (1 + 2*117) shifts
     # = 15040 evaluations at 12 qubits in one batched call (smem-resident path)
@@ -394,7 +410,8 @@ def main():
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
             "gpu_launches": int(launches),
-            "secondary": {"config3_latency_and_b64": latency, "config3_dense_slab_path": dense_path,
+            "secondary": {"config3_latency_and_b64": latency, "config3_complex128_program": complex_path,
+                          "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
                           "config4_fmo": config4},
             "clocks": clk.summary(),
