@@ -75,4 +75,19 @@ using FermionOperator = std::vector<FermionTerm>;
 PauliSum jordan_wigner(const FermionOperator& op, int n_so);
 PauliSum jordan_wigner_ladder(const LadderOp& op, int n_so);
 
+/// reduce_two_qubits: the symmetry-conserving two-qubit
+/// reduction of a JW-mapped (interleaved alpha/beta) operator.
+/// Modes are re-ordered alpha first (spin orbital 2P -> P, 2P+1 -> m + P,
+/// m = n_so / 2) and parity-encoded: qubit j holds the parity of modes
+/// 0..j. This is the GF(2)-linear basis change y = A x of occupation bits x,
+/// so X^a Z^b -> X^(A a) Z^(A^-T b) (phases from Y = iXZ carried exactly).
+/// Qubit m - 1 then holds the N_alpha parity and qubit n_so - 1 the N parity;
+/// both are replaced by their eigenvalues for (n_alpha, n_beta) and removed,
+/// leaving n_so - 2 qubits (pinned layout; SPEC leaves the ordering open).
+/// Throws ContractViolation when a term acts with X or Y on a tapered qubit
+/// (the operator does not conserve the two parities).
+PauliSum reduce_two_qubits(const PauliSum& op, int n_so, int n_alpha, int n_beta);
+/// The same reduction of a JW occupation bitstring (e.g. |HF>).
+uint64_t reduce_two_qubits_basis(uint64_t jw_bits, int n_so);
+
 }  // namespace fragfield

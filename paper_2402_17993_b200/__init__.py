@@ -58,6 +58,8 @@ from .lib._fragfield import (  # noqa: E402,F401
     jordan_wigner,
     magnitude_order,
     neldermead_minimize,
+    reduce_two_qubits,
+    reduce_two_qubits_basis,
     parameter_shift_set,
     pauli_mul,
     powell_minimize,

@@ -191,6 +191,74 @@ PauliSum jordan_wigner(const FermionOperator& op, int n_so) {
   return total;
 }
 
+// ---- two-qubit reduction -----------------------------------
+namespace {
+// blocked index of JW qubit q (alpha first) and its inverse
+int blocked_of(int q, int m) { return (q & 1) ? m + q / 2 : q / 2; }
+int jw_of(int k, int m) { return k < m ? 2 * k : 2 * (k - m) + 1; }
+// y = A x: y_j = parity of the modes with blocked index <= j
+uint64_t parity_encode(uint64_t x, int n) {
+  const int m = n / 2;
+  uint64_t y = 0;
+  int acc = 0;
+  for (int k = 0; k < n; ++k) {
+    acc ^= (int)((x >> jw_of(k, m)) & 1u);
+    y |= (uint64_t)acc << k;
+  }
+  return y;
+}
+// z' = A^-T z: z'_k = z_(jw of k) xor z_(jw of k+1)
+uint64_t parity_encode_z(uint64_t z, int n) {
+  const int m = n / 2;
+  uint64_t out = 0;
+  for (int k = 0; k < n; ++k) {
+    int v = (int)((z >> jw_of(k, m)) & 1u);
+    if (k + 1 < n) v ^= (int)((z >> jw_of(k + 1, m)) & 1u);
+    out |= (uint64_t)v << k;
+  }
+  return out;
+}
+// drop bits t1 < t2 of v
+uint64_t drop_two(uint64_t v, int t1, int t2) {
+  const uint64_t lo = v & ((1ULL << t1) - 1);
+  const uint64_t mid = (v >> (t1 + 1)) & ((1ULL << (t2 - t1 - 1)) - 1);
+  const uint64_t hi = t2 + 1 < 64 ? v >> (t2 + 1) : 0;
+  return lo | (mid << t1) | (hi << (t2 - 1));
+}
+}  // namespace
+
+PauliSum reduce_two_qubits(const PauliSum& op, int n_so, int n_alpha, int n_beta) {
+  if (n_so < 4 || n_so % 2 || n_so > 64 || op.n_qubits() != n_so)
+    throw ContractViolation("reduce_two_qubits: need an even n_so in [4, 64] matching the operator");
+  if (n_alpha < 0 || n_beta < 0 || n_alpha > n_so / 2 || n_beta > n_so / 2)
+    throw ContractViolation("reduce_two_qubits: electron counts out of range");
+  const int m = n_so / 2, t1 = m - 1, t2 = n_so - 1;
+  const int y1 = n_alpha & 1, y2 = (n_alpha + n_beta) & 1;  // parity-qubit eigenvalues (-1)^y
+  (void)blocked_of;
+  PauliSum out(n_so - 2);
+  for (const auto& kv : op.terms()) {
+    const uint64_t a = kv.first.first, b = kv.first.second;
+    const uint64_t a2 = parity_encode(a, n_so), b2 = parity_encode_z(b, n_so);
+    if (((a2 >> t1) & 1u) || ((a2 >> t2) & 1u))
+      throw ContractViolation("reduce_two_qubits: a term flips a conserved parity qubit (operator does not "
+                              "commute with the N_alpha / N parities)");
+    // c i^{|a&b|} X^a Z^b -> c i^{|a&b|} X^a2 Z^b2 = c i^{|a&b| - |a2&b2|} P(a2, b2)
+    const int k = (__builtin_popcountll(a & b) - __builtin_popcountll(a2 & b2)) & 3;
+    Complex c = kv.second;
+    static const Complex ik[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    c *= ik[k];
+    if ((((b2 >> t1) & 1u) && y1) ^ (((b2 >> t2) & 1u) && y2)) c = -c;  // Z on a parity qubit -> eigenvalue
+    out.add(drop_two(a2, t1, t2), drop_two(b2, t1, t2), c);
+  }
+  out.simplify();
+  return out;
+}
+
+uint64_t reduce_two_qubits_basis(uint64_t jw_bits, int n_so) {
+  if (n_so < 4 || n_so % 2 || n_so > 64) throw ContractViolation("reduce_two_qubits_basis: need an even n_so in [4, 64]");
+  return drop_two(parity_encode(jw_bits, n_so), n_so / 2 - 1, n_so - 1);
+}
+
 // ---- Hamiltonians --------------------------------------------------------------
 SpatialIntegrals synthetic_integrals(int m, uint64_t seed, double sigma_h, double sigma_g) {
   if (m < 1 || m > 32) throw ContractViolation("synthetic_integrals: m out of range");

@@ -73,6 +73,7 @@ PYBIND11_MODULE(_fragfield, m) {
       .def(py::init<int>(), py::arg("n_qubits"))
       .def_static("from_arrays", &psum_from_arrays)
       .def_static("from_text", &PauliSum::from_text)
+      .def_property_readonly("n_qubits", &PauliSum::n_qubits)
       .def("add", [](PauliSum& s, const PauliString& p, Complex c) { s.add(p, c); })
       .def("simplify", &PauliSum::simplify, py::arg("tol") = 1e-14)
       .def("arrays", &psum_arrays)
@@ -125,6 +126,9 @@ PYBIND11_MODULE(_fragfield, m) {
   m.def("random_pauli_hamiltonian", &random_pauli_hamiltonian, py::arg("n_qubits"),
         py::arg("n_terms"), py::arg("seed"), py::arg("sigma") = 0.1);
   m.def("uniform_vector", &uniform_vector);
+  m.def("reduce_two_qubits", &reduce_two_qubits, py::arg("op"), py::arg("n_so"), py::arg("n_alpha"),
+        py::arg("n_beta"));
+  m.def("reduce_two_qubits_basis", &reduce_two_qubits_basis, py::arg("jw_bits"), py::arg("n_so"));
 
   // ---- uccsd ----
   py::class_<Excitation>(m, "Excitation")

@@ -10,7 +10,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import build_generators, hf_bits, magnitude_order, qubit_hamiltonian, synthetic_integrals, uniform_vector
+from . import (build_generators, hf_bits, magnitude_order, qubit_hamiltonian, reduce_two_qubits,
+               reduce_two_qubits_basis, synthetic_integrals, uniform_vector)
 
 SEED_BASE = 2402179930
 
@@ -35,10 +36,12 @@ class Problem:
     thetas: np.ndarray  # [batch][n_gen], canonical generator order
     seed: int
     extra: dict = field(default_factory=dict)
+    mapping: str = "jw"  # "jw" or "scbkt" (two-qubit reduction)
+    images: list = None  # scbkt: reduced generator images by canonical id
 
     @property
     def n_qubits(self):
-        return 2 * self.m
+        return 2 * self.m - (2 if self.mapping == "scbkt" else 0)
 
     @property
     def n_gen(self):
@@ -46,6 +49,8 @@ class Problem:
 
     @property
     def hf(self):
+        if self.mapping == "scbkt":
+            return reduce_two_qubits_basis(hf_bits(self.n_elec), 2 * self.m)
         return hf_bits(self.n_elec)
 
     def plan_thetas(self, thetas=None):
@@ -57,7 +62,7 @@ class Problem:
         """Flat C-ABI arrays of the plan: term_off, x, z, c (execution order)."""
         off = [0]; xs = []; zs = []; cs = []
         for gid in self.plan.order:
-            x, z, c = self.gens[gid].image.arrays()
+            x, z, c = (self.images[gid] if self.images is not None else self.gens[gid].image).arrays()
             xs.append(x); zs.append(z); cs.append(c)
             off.append(off[-1] + len(x))
         return (np.array(off, np.int64), np.concatenate(xs).astype(np.uint64),
@@ -68,18 +73,29 @@ class Problem:
 
 
 def make_problem(m: int, n_elec: int, seed: int, batch: int = 1, theta_hw: float = 0.1,
-                 name: str = "") -> Problem:
+                 name: str = "", mapping: str = "jw") -> Problem:
+    """mapping "scbkt": the Hamiltonian and every generator image go through
+    reduce_two_qubits (2m - 2 qubits); the Trotter energy is mapping
+    independent (each generator's strings commute, so its exponential is exact)."""
     h, g = synthetic_integrals(m, seed)
     H = qubit_hamiltonian(h, g, n_elec)
     gens = build_generators(2 * m, n_elec)
     th = np.array(uniform_vector(seed + 1, batch * len(gens), -theta_hw, theta_hw)).reshape(batch, len(gens))
     plan = magnitude_order(gens, list(th[0]), 2 * m)
-    return Problem(name or f"m{m}e{n_elec}", m, n_elec, h, g, H, gens, plan, th, seed)
+    images = None
+    if mapping == "scbkt":
+        na, nb = (n_elec + 1) // 2, n_elec // 2  # |HF>: lowest spin orbitals, interleaved
+        H = reduce_two_qubits(H, 2 * m, na, nb)
+        images = [reduce_two_qubits(gn.image, 2 * m, na, nb) for gn in gens]
+    elif mapping != "jw":
+        raise ValueError(f"unknown mapping {mapping!r}")
+    return Problem(name or f"m{m}e{n_elec}", m, n_elec, h, g, H, gens, plan, th, seed, mapping=mapping,
+                   images=images)
 
 
-def config_problem(config: int, batch: int = 1, fragment: int = 0) -> Problem:
+def config_problem(config: int, batch: int = 1, fragment: int = 0, mapping: str = "jw") -> Problem:
     m, ne, hw = CONFIGS[config]
-    return make_problem(m, ne, ham_seed(config, fragment), batch, hw, name=f"config{config}")
+    return make_problem(m, ne, ham_seed(config, fragment), batch, hw, name=f"config{config}", mapping=mapping)
 
 
 def fmo_fragments():

@@ -269,3 +269,21 @@ def test_cuda_path_matches_golden_fixtures(ctx):
             want = np.array([float.fromhex(v) for v in row["state_re"]]) + 1j * np.array(
                 [float.fromhex(v) for v in row["state_im"]])
             assert np.abs(st.download()[0] - want).max() <= A_TOL
+
+
+@pytest.mark.parametrize("config,rows", [(1, 4), (2, 4), (3, 2)])
+def test_scbkt_energies_match_jw(ctx, oracle, config, rows):
+    """SPEC.md:361-370 two-qubit reduction on the device: the reduced plan
+    (n - 2 qubits; its generators run as per-string rotation passes) gives the
+    JW energies of the same theta rows (the Trotter energy is mapping
+    independent), and at config 1 the oracle's."""
+    J = problems.config_problem(config, batch=rows)
+    R = problems.config_problem(config, batch=rows, mapping="scbkt")
+    assert R.n_qubits == J.n_qubits - 2
+    ej = capi.energy_batch(ctx, *upload(ctx, J), J.hf, J.plan_thetas())
+    er = capi.energy_batch(ctx, *upload(ctx, R), R.hf, R.plan_thetas())
+    assert np.abs(ej - er).max() <= E_TOL
+    if config == 1:
+        for b in range(rows):
+            ref, _ = oracle_energy(oracle, J, J.thetas[b])
+            assert abs(er[b] - ref) <= E_TOL
