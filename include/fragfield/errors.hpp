@@ -23,6 +23,13 @@ struct ContractViolation : std::logic_error {
 };
 #endif
 
+/// Malformed input file (FCIDUMP, state dump); mirrors the reference's
+/// ParseError{line_number} (proj/core/include/fragfield/errors.hpp:8-13).
+struct ParseError : std::runtime_error {
+  ParseError(const std::string& what, int line) : std::runtime_error(what), line_number(line) {}
+  int line_number;
+};
+
 struct DeviceError : std::runtime_error {
   DeviceError(const std::string& what, int code) : std::runtime_error(what), code(code) {}
   int code;

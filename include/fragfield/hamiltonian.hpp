@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "fragfield/pauli.hpp"
@@ -39,6 +40,19 @@ SpinOrbitalHamiltonian to_spin_orbitals(const SpatialIntegrals& ints, int n_elec
 PauliSum qubit_hamiltonian(const SpinOrbitalHamiltonian& H);
 /// Config 5: n_terms seeded random {I,X,Y,Z}^n strings, real c ~ N(0, sigma).
 PauliSum random_pauli_hamiltonian(int n_qubits, int n_terms, uint64_t seed, double sigma = 0.1);
+
+/// FCIDUMP interchange: spatial orbitals, chemists' (ij|kl)
+/// with 8-fold symmetry written once (i >= j, k >= l, ij >= kl, 1-based),
+/// then h_ij (i >= j) as "v i j 0 0", then E_const as "v 0 0 0 0"; zero
+/// values are omitted; values at 17 significant digits (lossless round trip).
+struct Fcidump {
+  SpatialIntegrals ints;
+  int n_elec = 0;
+  int ms2 = 0;
+};
+void write_fcidump(const std::string& path, const SpatialIntegrals& ints, int n_elec, int ms2 = 0);
+/// Throws ParseError (with the line number) on a malformed file.
+Fcidump read_fcidump(const std::string& path);
 
 /// Uniform draws U(lo, hi) from mt19937_64(seed), same value mapping.
 std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double hi);

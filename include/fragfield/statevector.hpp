@@ -4,8 +4,10 @@
 // fallback (a missing device raises DeviceError).
 #pragma once
 
+#include <complex>
 #include <cstdint>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "fragfield/errors.hpp"
@@ -14,6 +16,11 @@
 #include "fragfield_cuda.h"
 
 namespace fragfield {
+
+/// State dump: little-endian int64 n_qubits, then 2^n complex
+/// doubles (re, im) in natural binary order, qubit 0 = least significant bit.
+void write_state_dump(const std::string& path, int n_qubits, const std::vector<std::complex<double>>& amps);
+std::vector<std::complex<double>> read_state_dump(const std::string& path, int* n_qubits);
 
 /// Throws ContractViolation (FFQ_EINVAL, FFQ_ENONHERMITIAN) or DeviceError.
 void check_ffq(int rc, ffq_ctx_t ctx);

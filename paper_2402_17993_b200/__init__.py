@@ -26,6 +26,7 @@ except ImportError as e:  # pragma: no cover - exercised only on a broken instal
 
 from .lib._fragfield import (  # noqa: E402,F401
     ContractViolation,
+    ParseError,
     ConvergenceError,
     Device,
     DeviceError,
@@ -60,6 +61,10 @@ from .lib._fragfield import (  # noqa: E402,F401
     neldermead_minimize,
     reduce_two_qubits,
     reduce_two_qubits_basis,
+    read_fcidump,
+    read_state_dump,
+    write_fcidump,
+    write_state_dump,
     parameter_shift_set,
     pauli_mul,
     powell_minimize,

@@ -5,7 +5,11 @@
 // optimizers and the FMO two-body assembly
 // (reference proj/core/src/fmo.cpp:28-48).
 #include <algorithm>
+#include <cctype>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <limits>
 #include <numeric>
 #include <random>
@@ -287,6 +291,116 @@ SpatialIntegrals synthetic_integrals(int m, uint64_t seed, double sigma_h, doubl
         }
       }
   return I;
+}
+
+void write_fcidump(const std::string& path, const SpatialIntegrals& I, int n_elec, int ms2) {
+  const int m = I.m;
+  if (m < 1 || I.h.size() != (size_t)m * m || I.g.size() != (size_t)m * m * m * m)
+    throw ContractViolation("write_fcidump: integral shapes");
+  std::FILE* f = std::fopen(path.c_str(), "w");
+  if (!f) throw std::runtime_error("write_fcidump: cannot open " + path);
+  std::fprintf(f, " &FCI NORB=%d,NELEC=%d,MS2=%d,\n  ORBSYM=", m, n_elec, ms2);
+  for (int i = 0; i < m; ++i) std::fprintf(f, "1,");
+  std::fprintf(f, "\n  ISYM=1,\n &END\n");
+  auto G = [&](int a, int b, int c, int d) { return I.g[(((size_t)a * m + b) * m + c) * m + d]; };
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j)
+      for (int k = 0; k < m; ++k)
+        for (int l = 0; l <= k; ++l) {
+          if (i * (i + 1) / 2 + j < k * (k + 1) / 2 + l) continue;  // ij >= kl
+          const double v = G(i, j, k, l);
+          if (v != 0.0) std::fprintf(f, "%.17g %d %d %d %d\n", v, i + 1, j + 1, k + 1, l + 1);
+        }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j)
+      if (I.h[(size_t)i * m + j] != 0.0) std::fprintf(f, "%.17g %d %d 0 0\n", I.h[(size_t)i * m + j], i + 1, j + 1);
+  std::fprintf(f, "%.17g 0 0 0 0\n", I.e_const);
+  std::fclose(f);
+}
+
+Fcidump read_fcidump(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("read_fcidump: cannot open " + path);
+  std::string line, header;
+  int ln = 0;
+  bool done = false;
+  while (!done && std::getline(in, line)) {
+    ++ln;
+    header += line + " ";
+    std::string up = line;
+    for (auto& ch : up) ch = (char)std::toupper((unsigned char)ch);
+    if (up.find("&END") != std::string::npos || up.find("/") != std::string::npos) done = true;
+  }
+  if (!done) throw ParseError("read_fcidump: header without &END", ln);
+  auto key = [&](const char* k, int dflt, bool required) {
+    std::string up = header;
+    for (auto& ch : up) ch = (char)std::toupper((unsigned char)ch);
+    const size_t p = up.find(k);
+    if (p == std::string::npos) {
+      if (required) throw ParseError(std::string("read_fcidump: header lacks ") + k, ln);
+      return dflt;
+    }
+    size_t q = up.find('=', p);
+    if (q == std::string::npos) throw ParseError(std::string("read_fcidump: malformed ") + k, ln);
+    return std::atoi(header.c_str() + q + 1);
+  };
+  Fcidump F;
+  const int m = key("NORB", 0, true);
+  F.n_elec = key("NELEC", 0, true);
+  F.ms2 = key("MS2", 0, false);
+  if (m < 1 || m > 64) throw ParseError("read_fcidump: NORB out of range", ln);
+  F.ints.m = m;
+  F.ints.h.assign((size_t)m * m, 0.0);
+  F.ints.g.assign((size_t)m * m * m * m, 0.0);
+  auto G = [&](int a, int b, int c, int d) -> double& { return F.ints.g[(((size_t)a * m + b) * m + c) * m + d]; };
+  while (std::getline(in, line)) {
+    ++ln;
+    if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
+    std::istringstream ss(line);
+    double v;
+    int i, j, k, l;
+    if (!(ss >> v >> i >> j >> k >> l)) throw ParseError("read_fcidump: malformed integral line", ln);
+    if (i < 0 || j < 0 || k < 0 || l < 0 || i > m || j > m || k > m || l > m)
+      throw ParseError("read_fcidump: orbital index out of range", ln);
+    if (i == 0 && j == 0 && k == 0 && l == 0) {
+      F.ints.e_const = v;
+    } else if (k == 0 && l == 0) {
+      if (i == 0 || j == 0) throw ParseError("read_fcidump: malformed one-electron line", ln);
+      F.ints.h[(size_t)(i - 1) * m + (j - 1)] = v;
+      F.ints.h[(size_t)(j - 1) * m + (i - 1)] = v;
+    } else {
+      if (i == 0 || j == 0 || k == 0 || l == 0) throw ParseError("read_fcidump: malformed two-electron line", ln);
+      const int a = i - 1, b = j - 1, c = k - 1, d = l - 1;
+      G(a, b, c, d) = v; G(b, a, c, d) = v; G(a, b, d, c) = v; G(b, a, d, c) = v;
+      G(c, d, a, b) = v; G(d, c, a, b) = v; G(c, d, b, a) = v; G(d, c, b, a) = v;
+    }
+  }
+  return F;
+}
+
+void write_state_dump(const std::string& path, int n_qubits, const std::vector<std::complex<double>>& amps) {
+  if (n_qubits < 0 || n_qubits > 40 || amps.size() != (size_t)1 << n_qubits)
+    throw ContractViolation("write_state_dump: need 2^n_qubits amplitudes");
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("write_state_dump: cannot open " + path);
+  const int64_t n = n_qubits;  // x86-64 and aarch64 hosts are little-endian
+  out.write(reinterpret_cast<const char*>(&n), sizeof(n));
+  out.write(reinterpret_cast<const char*>(amps.data()), (std::streamsize)(amps.size() * sizeof(amps[0])));
+  if (!out) throw std::runtime_error("write_state_dump: write failed");
+}
+
+std::vector<std::complex<double>> read_state_dump(const std::string& path, int* n_qubits) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("read_state_dump: cannot open " + path);
+  int64_t n = -1;
+  in.read(reinterpret_cast<char*>(&n), sizeof(n));
+  if (!in || n < 0 || n > 40) throw ParseError("read_state_dump: bad header", 0);
+  std::vector<std::complex<double>> a((size_t)1 << n);
+  in.read(reinterpret_cast<char*>(a.data()), (std::streamsize)(a.size() * sizeof(a[0])));
+  if (!in) throw ParseError("read_state_dump: truncated amplitude array", 0);
+  if (in.peek() != std::char_traits<char>::eof()) throw ParseError("read_state_dump: trailing bytes", 0);
+  if (n_qubits) *n_qubits = (int)n;
+  return a;
 }
 
 std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double hi) {

@@ -56,6 +56,7 @@ PYBIND11_MODULE(_fragfield, m) {
   py::register_exception<ContractViolation>(m, "ContractViolation", PyExc_ValueError);
   py::register_exception<DeviceError>(m, "DeviceError", PyExc_RuntimeError);
   py::register_exception<ConvergenceError>(m, "ConvergenceError", PyExc_RuntimeError);
+  py::register_exception<ParseError>(m, "ParseError", PyExc_ValueError);
 
   // ---- qubit-map ----
   py::class_<PauliString>(m, "PauliString")
@@ -126,6 +127,38 @@ PYBIND11_MODULE(_fragfield, m) {
   m.def("random_pauli_hamiltonian", &random_pauli_hamiltonian, py::arg("n_qubits"),
         py::arg("n_terms"), py::arg("seed"), py::arg("sigma") = 0.1);
   m.def("uniform_vector", &uniform_vector);
+  m.def(
+      "write_fcidump",
+      [](const std::string& path, arr_f64 h, arr_f64 g, int n_elec, double e_const, int ms2) {
+        SpatialIntegrals I;
+        I.m = (int)h.shape(0);
+        I.h = to_vec(h);
+        I.g = to_vec(g);
+        I.e_const = e_const;
+        write_fcidump(path, I, n_elec, ms2);
+      },
+      py::arg("path"), py::arg("h"), py::arg("g"), py::arg("n_elec"), py::arg("e_const") = 0.0,
+      py::arg("ms2") = 0);
+  m.def(
+      "read_fcidump",
+      [](const std::string& path) {
+        Fcidump F = read_fcidump(path);
+        const int mo = F.ints.m;
+        arr_f64 h({mo, mo}), g({mo, mo, mo, mo});
+        std::copy(F.ints.h.begin(), F.ints.h.end(), h.mutable_data());
+        std::copy(F.ints.g.begin(), F.ints.g.end(), g.mutable_data());
+        return py::make_tuple(h, g, F.ints.e_const, F.n_elec, F.ms2);
+      },
+      py::arg("path"), "-> (h, g, e_const, n_elec, ms2)");
+  m.def("write_state_dump", &write_state_dump, py::arg("path"), py::arg("n_qubits"), py::arg("amplitudes"));
+  m.def(
+      "read_state_dump",
+      [](const std::string& path) {
+        int n = 0;
+        auto a = read_state_dump(path, &n);
+        return py::make_tuple(n, a);
+      },
+      py::arg("path"), "-> (n_qubits, amplitudes)");
   m.def("reduce_two_qubits", &reduce_two_qubits, py::arg("op"), py::arg("n_so"), py::arg("n_alpha"),
         py::arg("n_beta"));
   m.def("reduce_two_qubits_basis", &reduce_two_qubits_basis, py::arg("jw_bits"), py::arg("n_so"));

@@ -78,7 +78,18 @@ def make_problem(m: int, n_elec: int, seed: int, batch: int = 1, theta_hw: float
     reduce_two_qubits (2m - 2 qubits); the Trotter energy is mapping
     independent (each generator's strings commute, so its exponential is exact)."""
     h, g = synthetic_integrals(m, seed)
-    H = qubit_hamiltonian(h, g, n_elec)
+    return problem_from_integrals(h, g, n_elec, seed=seed, batch=batch, theta_hw=theta_hw,
+                                  name=name or f"m{m}e{n_elec}", mapping=mapping)
+
+
+def problem_from_integrals(h, g, n_elec: int, e_const: float = 0.0, seed: int = SEED_BASE, batch: int = 1,
+                           theta_hw: float = 0.1, name: str = "", mapping: str = "jw") -> Problem:
+    """A problem from spatial integrals (e.g. read_fcidump); theta rows seeded
+    from `seed` + 1 as for the synthetic configs."""
+    h = np.ascontiguousarray(h, np.float64)
+    g = np.ascontiguousarray(g, np.float64)
+    m = h.shape[0]
+    H = qubit_hamiltonian(h, g, n_elec, e_const)
     gens = build_generators(2 * m, n_elec)
     th = np.array(uniform_vector(seed + 1, batch * len(gens), -theta_hw, theta_hw)).reshape(batch, len(gens))
     plan = magnitude_order(gens, list(th[0]), 2 * m)
@@ -90,7 +101,7 @@ def make_problem(m: int, n_elec: int, seed: int, batch: int = 1, theta_hw: float
     elif mapping != "jw":
         raise ValueError(f"unknown mapping {mapping!r}")
     return Problem(name or f"m{m}e{n_elec}", m, n_elec, h, g, H, gens, plan, th, seed, mapping=mapping,
-                   images=images)
+                   images=images, extra={"e_const": e_const})
 
 
 def config_problem(config: int, batch: int = 1, fragment: int = 0, mapping: str = "jw") -> Problem:

@@ -249,3 +249,26 @@ def test_complex_hamiltonian_takes_complex_program(monkeypatch):
     c0 = _ctx(monkeypatch, {"FFQ_SECTOR": "0"})
     plan0, ham0 = capi.Plan(c0, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c0, P.n_qubits, x2, z2, c2)
     assert np.abs(e - capi.energy_batch(c0, plan0, ham0, P.hf, P.plan_thetas())).max() <= 1e-12
+
+
+def test_cli_energy_from_fcidump_and_vqe(tmp_path, capsys):
+    """SPEC.md:578-629 CLI on the device: energies of a config read back from
+    its FCIDUMP equal the config's own; the config-1 VQE converges below HF."""
+    import json
+
+    from paper_2402_17993_b200 import cli
+
+    f = str(tmp_path / "c2.fcidump")
+    assert cli.main(["ham", "--config", "2", "--out", f]) == 0
+    capsys.readouterr()
+    seed = problems.ham_seed(2)
+    assert cli.main(["energy", "--fcidump", f, "--batch", "3", "--seed", str(seed)]) == 0
+    rep = json.loads(capsys.readouterr().out)
+    P = problems.config_problem(2, batch=3)
+    c = capi.Context(0)
+    ref = capi.energy_batch(c, capi.Plan(c, P.n_qubits, *P.plan_arrays()),
+                            capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays()), P.hf, P.plan_thetas())
+    assert np.abs(np.array([r["total"] for r in rep["records"]]) - ref).max() <= 1e-10
+    assert cli.main(["vqe", "--config", "1", "--optimizer", "bfgs"]) == 0
+    r = json.loads(capsys.readouterr().out)["records"][0]
+    assert r["converged"] and r["total"] < r["hf_energy"]
