@@ -988,19 +988,18 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
     DevBuf<double>& eo = ctx->io_e;
     th.alloc(std::max<size_t>(1, nth));
     eo.alloc(2 * (size_t)batch);
-    int chunk = batch;
-    if (nth * sizeof(double) >= (size_t)(1 << 20)) {
-      const int wave = std::max(1, ctx->n_sm);
-      chunk = std::max(wave, (batch / 4 + wave - 1) / wave * wave);
-    }
-    for (int b0 = 0; b0 < batch; b0 += chunk) {
-      const int nb = std::min(chunk, batch - b0);
+    // first chunk one wave (its staging is the exposed part), then two waves
+    const bool piped = nth * sizeof(double) >= (size_t)(1 << 20);
+    const int wave = std::max(1, ctx->n_sm);
+    for (int b0 = 0, k = 0; b0 < batch; ++k) {
+      const int nb = piped ? std::min((k == 0 ? 1 : 2) * wave, batch - b0) : batch;
       const size_t o = (size_t)b0 * ng, n = (size_t)nb * ng;
       if (n) {
         std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
         CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
       }
       energy_device(ctx, plan, ham, hf_bits, nb, th.p + o, eo.p + b0, eo.p + batch + b0);
+      b0 += nb;
     }
     CK(cudaMemcpyAsync(stage_e, eo.p, 2 * sizeof(double) * batch, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
