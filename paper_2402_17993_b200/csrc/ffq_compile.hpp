@@ -756,7 +756,8 @@ constexpr int kBlockMaxNC = 1;        // lane chunks per unit (the device runs o
 constexpr int kFTabMax = 3968;        // shared-row f values (kernel parameter space, 31 KiB)
 constexpr int kBlockMinLanes = 16;    // smaller chunks go to the generic rows
 constexpr int kBlockRowQuantum = 1;   // shared rows per unit padded to a multiple of this
-constexpr int kStreamQuantum = 16;    // rows per warp stream padded to a multiple of this
+constexpr int kBlkTrips = 6;          // k_sector_eval_real: four-row trips of block words in flight per warp (4: 877k, 6: 869k, 8: 906k expectation cycles, config 3)
+constexpr int kStreamQuantum = 4 * kBlkTrips;  // rows per warp stream padded to a multiple of this
 
 // Anchored string blocks for the expectation pairs of a product-layout sector
 // (see SectorProgram). For pair (i, j = i ^ X) with X = Xa | Xb (alpha / beta

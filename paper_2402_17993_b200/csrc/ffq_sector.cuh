@@ -437,27 +437,23 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
                                              const double* sft) {
   const int4 h = __ldg(sd.blk_warp + warp);
   const uint32_t* rw = sd.blk_stream + lane;
-  uint32_t A[4], B[4];
   auto fetch = [&](uint32_t (&d)[4], int r) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) d[u] = r < h.y ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
   };
   uint32_t bs = 0;
   double a = 0.0, t = 0.0, acc = 0.0;
-  uint32_t C[4], D[4];
-  fetch(A, h.x);
-  fetch(B, h.x + 4);
-  fetch(C, h.x + 8);
-  fetch(D, h.x + 12);
-  for (int r = h.x; r < h.y; r += 16) {  // the stream is padded to whole 16-row rounds
-    blk_trip(A, amp, sft, bs, a, t, acc);
-    fetch(A, r + 16);
-    blk_trip(B, amp, sft, bs, a, t, acc);
-    fetch(B, r + 20);
-    blk_trip(C, amp, sft, bs, a, t, acc);
-    fetch(C, r + 24);
-    blk_trip(D, amp, sft, bs, a, t, acc);
-    fetch(D, r + 28);
+  // kBlkTrips trips of four rows in flight; the stream is padded to whole
+  // rounds of kStreamQuantum = 4 * kBlkTrips rows
+  uint32_t W[kBlkTrips][4];
+#pragma unroll
+  for (int k = 0; k < kBlkTrips; ++k) fetch(W[k], h.x + 4 * k);
+  for (int r = h.x; r < h.y; r += 4 * kBlkTrips) {
+#pragma unroll
+    for (int k = 0; k < kBlkTrips; ++k) {
+      blk_trip(W[k], amp, sft, bs, a, t, acc);
+      fetch(W[k], r + 4 * (k + kBlkTrips));
+    }
   }
   return fma(a, t, acc);
 }
