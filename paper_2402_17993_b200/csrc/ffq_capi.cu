@@ -96,11 +96,13 @@ struct ffq_ctx_s {
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
+  int sector_split = 8;                          // env FFQ_SPLIT: most CTAs per evaluation of the 1024-thread real program
   std::string err = "no error";
   int64_t launches = 0;
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
+  DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
   DevBuf<uint32_t> slab_sup;
   bool slab_clean = false;      // support path: slab all-zero between graph replays
   DevBuf<double2> pslab;        // persistent-path slab, all-zero between evaluations
@@ -544,9 +546,22 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   // anchored blocks keep the shared-row f table behind the per-op tables
   const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) + (size_t)sd.n_ftab * sizeof(double);
   CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  k_sector_eval_real<NT><<<batch, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk);
+  // Batches smaller than the SM count: up to sector_split CTAs per evaluation
+  // (1024-thread program only). Each runs the generator phase and 32 / split
+  // of the warp shares of the expectation; the energies are bit-identical.
+  int split = 1;
+  if (NT == 32 * 32)
+    while (split * 2 <= ctx->sector_split && (int64_t)batch * split * 2 <= ctx->n_sm) split *= 2;
+  if (split > 1) ctx->warp_sums.alloc((size_t)batch * 32);
+  k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
+                                                                 clk, split, ctx->warp_sums.p);
   CK(cudaGetLastError());
   ctx->launches++;
+  if (split > 1) {
+    k_sum_warps<<<batch, 32, 0, ctx->stream>>>(ctx->warp_sums.p, e, im);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
 }
 
 void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
@@ -787,6 +802,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);
       c->sector_cl = (v == 4 || v == 8) ? v : 2;
@@ -1231,7 +1247,7 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
             a = amp.at(d & 0x7FFFu);
             bs = (d >> 15) & 0x7FFFu;
             t = 0.0;
-          } else {
+          } else {  // (the device keeps t as two chains, even and odd rows)
             const double f = S.ftab.at(d >> 16);
             t += ((d >> 15) & 1u ? -f : f) * amp.at(bs + (d & 0x7FFFu));
           }

@@ -400,8 +400,11 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval(SectorDev sd, PlanDev pl,
 // base B (closing the previous unit: acc += a * t); a shared row adds
 // (-1)^sign * ftab[i] * psi[B + O] to t, f by broadcast from shared memory.
 // Trips without an anchor row (the common case) take the short path.
+// The lane's partner sum of a unit is kept as two chains (even and odd rows of
+// the stream), added when the unit closes: two FMA chains per lane, so a warp
+// running alone (split evaluations) is not bound by one chain's latency.
 __device__ __forceinline__ void blk_trip(const uint32_t (&d)[4], const double* amp, const double* sft, uint32_t& bs,
-                                         double& a, double& t, double& acc) {
+                                         double& a, double (&t)[2], double& acc) {
   if (((d[0] | d[1] | d[2] | d[3]) >> 30) == 0u) {
     double v[4], f[4];
 #pragma unroll
@@ -413,7 +416,7 @@ __device__ __forceinline__ void blk_trip(const uint32_t (&d)[4], const double* a
     for (int u = 0; u < 4; ++u) {
       // sign bit 15 of the word -> bit 31 of f's high word
       const uint32_t hi = (uint32_t)__double2hiint(f[u]) ^ ((d[u] << 16) & 0x80000000u);
-      t = fma(__hiloint2double((int)hi, __double2loint(f[u])), v[u], t);
+      t[u & 1] = fma(__hiloint2double((int)hi, __double2loint(f[u])), v[u], t[u & 1]);
     }
     return;
   }
@@ -421,14 +424,14 @@ __device__ __forceinline__ void blk_trip(const uint32_t (&d)[4], const double* a
   for (int u = 0; u < 4; ++u) {
     const uint32_t w = d[u];
     if (w >> 30) {
-      acc = fma(a, t, acc);
+      acc = fma(a, t[0] + t[1], acc);
       a = amp[w & 0x7FFFu];
       bs = (w >> 15) & 0x7FFFu;
-      t = 0.0;
+      t[0] = t[1] = 0.0;
     } else {
       const double f = sft[w >> 16];
       const uint32_t hi = (uint32_t)__double2hiint(f) ^ ((w << 16) & 0x80000000u);
-      t = fma(__hiloint2double((int)hi, __double2loint(f)), amp[bs + (w & 0x7FFFu)], t);
+      t[u & 1] = fma(__hiloint2double((int)hi, __double2loint(f)), amp[bs + (w & 0x7FFFu)], t[u & 1]);
     }
   }
 }
@@ -442,7 +445,7 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
     for (int u = 0; u < 4; ++u) d[u] = r < h.y ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
   };
   uint32_t bs = 0;
-  double a = 0.0, t = 0.0, acc = 0.0;
+  double a = 0.0, t[2] = {0.0, 0.0}, acc = 0.0;
   // kBlkTrips trips of four rows in flight; the stream is padded to whole
   // rounds of kStreamQuantum = 4 * kBlkTrips rows
   uint32_t W[kBlkTrips][4];
@@ -455,20 +458,26 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
       fetch(W[k], r + 4 * (k + kBlkTrips));
     }
   }
-  return fma(a, t, acc);
+  return fma(a, t[0] + t[1], acc);
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
-                                                            int n_rows, long long* __restrict__ phase_clk) {
+                                                            int n_rows, long long* __restrict__ phase_clk,
+                                                            int split, double* __restrict__ warp_sums) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
+  // split > 1 (small batches): `split` CTAs run one evaluation; each runs the
+  // generator phase, then the warp shares w = part (mod split) of the
+  // expectation, whose warp sums go to warp_sums[row][w]; k_sum_warps then
+  // adds them with block_sum's second-stage tree, so the energy bits equal
+  // the one-CTA kernel's.
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ double2 red[NT / 32];
   const long long clk0 = clock64();
-  const int row = blockIdx.x;
+  const int row = blockIdx.x / split, part = blockIdx.x % split;
   if (row >= n_rows) return;
   const uint32_t na = sd.n_slots + 1;
   double* amp = reinterpret_cast<double*>(sm_raw);
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     if (op + k < sd.n_ops) step(op + k, w[k]);
   const long long clk1 = clock64();
   double acc = 0.0;
-  {
+  if (split == 1 || (threadIdx.x >> 5) % split == part) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t* es = sd.secs;  // one section: every pair is local
@@ -605,6 +614,17 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     }
     if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
   }
+  if (split > 1) {
+    if ((threadIdx.x >> 5) % split != part) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);  // block_sum's first stage
+    if ((threadIdx.x & 31) == 0) warp_sums[(int64_t)row * (NT / 32) + (threadIdx.x >> 5)] = acc;
+    if (threadIdx.x == 0 && phase_clk) {
+      phase_clk[2 * row] = clk1 - clk0;
+      phase_clk[2 * row + 1] = clock64() - clk1;
+    }
+    return;
+  }
   const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
   if (threadIdx.x == 0) {
     e_out[row] = tot.x;
@@ -613,6 +633,23 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       phase_clk[2 * row] = clk1 - clk0;
       phase_clk[2 * row + 1] = clock64() - clk1;
     }
+  }
+}
+
+// One warp per evaluation: block_sum's second stage over the 32 warp sums
+// of a split k_sector_eval_real launch.
+__global__ void k_sum_warps(const double* __restrict__ warp_sums, double* __restrict__ e_out,
+                            double* __restrict__ im_out) {
+  double v = warp_sums[(int64_t)blockIdx.x * 32 + threadIdx.x];
+  double z = 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_down_sync(0xffffffffu, v, o);
+    z += __shfl_down_sync(0xffffffffu, z, o);
+  }
+  if (threadIdx.x == 0) {
+    e_out[blockIdx.x] = v;
+    if (im_out) im_out[blockIdx.x] = z;
   }
 }
 
