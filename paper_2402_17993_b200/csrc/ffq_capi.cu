@@ -102,6 +102,11 @@ struct ffq_ctx_s {
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
+  DevBuf<double> compact_psi, compact_coef;  // compact real sector path (ffq_compact.inl)
+  DevBuf<double2> compact_part;
+  int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
+  int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
+                                             // support path is faster below: grouped Hamiltonian)
   DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
   DevBuf<uint32_t> slab_sup;
   bool slab_clean = false;      // support path: slab all-zero between graph replays
@@ -145,6 +150,7 @@ struct ffq_plan_s {
     bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
+  std::map<std::string, std::shared_ptr<void>> compacts;  // CompactProg per (ham, hf) (ffq_compact.inl)
   PlanDev dev() const {
     PlanDev d;
     d.n_ops = (int)cp.op_kind.size();
@@ -597,6 +603,8 @@ bool use_smem_path(ffq_ctx_t ctx, const ffq_plan_s* pl) {
 }
 
 // energies of `batch` rows of theta (device) into e/im (device), async
+#include "ffq_compact.inl"
+
 void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int batch,
                    const double* theta_dev, double* e_dev, double* im_dev) {
   const int n = pl->cp.n_qubits;
@@ -604,13 +612,19 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
   if (n < 64 && (hf >> n) != 0) throw BadInput("hf_bits exceeds n_qubits", FFQ_EINVAL);
   if (batch <= 0) return;
   // support-closure evaluator first (FFQ_SECTOR=0 disables it); plans it cannot
-  // take (non-fused generators, closures beyond 32768 amplitudes) fall through
+  // take (non-fused generators, closures beyond 32768 amplitudes) fall through,
+  // real spin-conserving ones to the compact sector layout (FFQ_COMPACT=0 disables it)
   if (ctx->sector) {
     if (const SectorDev* sd = sector_program(ctx, pl, h, hf)) {
       launch_sector(ctx, pl, *sd, theta_dev, batch, e_dev, im_dev);
       return;
     }
   }
+  if (ctx->compact && n >= ctx->compact_min_qubits)
+    if (CompactProg* cpg = compact_program(ctx, pl, h, hf)) {
+      compact_energy(ctx, pl, *cpg, theta_dev, batch, e_dev, im_dev);
+      return;
+    }
   if (use_smem_path(ctx, pl)) {
     const size_t sb = smem_bytes(pl);
     CK(cudaFuncSetAttribute(k_smem_eval<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -802,6 +816,8 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_COMPACT")) c->compact = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);

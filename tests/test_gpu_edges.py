@@ -272,3 +272,60 @@ def test_cli_energy_from_fcidump_and_vqe(tmp_path, capsys):
     assert cli.main(["vqe", "--config", "1", "--optimizer", "bfgs"]) == 0
     r = json.loads(capsys.readouterr().out)["records"][0]
     assert r["converged"] and r["total"] < r["hf_energy"]
+
+
+def test_split_knob_bit_identical(monkeypatch):
+    # FFQ_SPLIT caps the CTAs per 18-qubit evaluation (1 = one CTA each); the
+    # energies do not depend on it
+    P = problems.config_problem(3, batch=3)
+    out = {}
+    for split in ("1", "2", "8"):
+        c = _ctx(monkeypatch, {"FFQ_SPLIT": split})
+        plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+        ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        out[split] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        del plan, ham, c
+    assert np.array_equal(out["1"], out["2"]) and np.array_equal(out["1"], out["8"])
+
+
+@pytest.mark.parametrize("case", ["config5_20q", "uccsd_20q"])
+def test_compact_sector_path_matches_dense(monkeypatch, case):
+    # the compact real [alpha][beta] sector layout (ffq_compact.inl; the default
+    # above 26 qubits) against the dense support-tracked path on the same inputs
+    if case == "config5_20q":
+        P = problems.config5_problem(n_doubles=300, n_terms=200, n_qubits=20, n_elec=10)
+    else:
+        P = problems.make_problem(10, 10, problems.ham_seed(9, 1), batch=2)
+    out = {}
+    for mode, env in (("compact", {"FFQ_COMPACT_MIN": "20"}), ("dense", {"FFQ_COMPACT": "0"})):
+        for k in ("FFQ_COMPACT", "FFQ_COMPACT_MIN"):
+            monkeypatch.delenv(k, raising=False)
+        c = _ctx(monkeypatch, env)
+        plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+        ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        out[mode] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        out[mode + "2"] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        del plan, ham, c
+    assert np.max(np.abs(out["compact"] - out["dense"])) <= 1e-10
+    assert np.array_equal(out["compact"], out["compact2"])  # deterministic
+
+
+def test_compact_sector_path_golden(monkeypatch):
+    # the compact layout forced at configs 1-3 (FFQ_SECTOR=0 skips the closure
+    # programs, FFQ_COMPACT_MIN=0 lets the compact path take every size) against
+    # the committed oracle energies (tests/golden/energies.json)
+    import json
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "energies.json")) as f:
+        golden = json.load(f)["configs"]
+    monkeypatch.delenv("FFQ_COMPACT", raising=False)
+    c = _ctx(monkeypatch, {"FFQ_SECTOR": "0", "FFQ_COMPACT_MIN": "0"})
+    for cfg, g in golden.items():
+        P = problems.config_problem(int(cfg), batch=len(g["rows"]))
+        plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+        ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        n0 = c.launches()
+        e = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        assert c.launches() - n0 > P.n_gen  # one pass per generator: the compact path ran
+        ref = np.array([float.fromhex(r["energy"]) for r in g["rows"]])
+        assert np.abs(e - ref).max() <= 1e-10, cfg
