@@ -395,6 +395,27 @@ def main():
                                 "note": "all six fragments' parameter-shift sets, compiled once, device-resident theta"}
     del fsets
 
+    # secondary: BASELINE.json config 5 (32 qubits, 16 electrons, all singles + the
+    # first 2000 doubles, 5000 random Pauli terms) on this GPU: one energy
+    # evaluation through the compact real sector layout (1.3 GB instead of 64 GiB)
+    config5 = None
+    if rank == 0:
+        P5 = _pb.config5_problem()
+        t5 = time.perf_counter()
+        plan5 = capi.Plan(ctx, P5.n_qubits, *P5.plan_arrays())
+        ham5 = capi.Hamiltonian(ctx, P5.n_qubits, *P5.ham_arrays())
+        th5 = torch.from_numpy(P5.plan_thetas()).to(f"cuda:{local}")
+        e5 = torch.zeros(1, dtype=torch.float64, device=f"cuda:{local}")
+        f5 = lambda: capi.energy_batch_device(ctx, plan5, ham5, P5.hf, 1, th5.data_ptr(), e5.data_ptr())  # noqa: E731
+        f5()
+        ctx.synchronize()
+        t5 = time.perf_counter() - t5
+        ms5 = timed(f5, 2)
+        config5 = {"qubits": P5.n_qubits, "generators": P5.n_gen, "terms": len(P5.H), "energy": float(e5.item()),
+                   "ms_per_eval": statistics.mean(ms5), "first_call_s_incl_compile": t5,
+                   "path": "compact real [C(16,8)][C(16,8)] sector layout, one GPU (no global qubits)"}
+        del plan5, ham5
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = 2
@@ -437,7 +458,7 @@ def main():
             "secondary": {"config3_latency_and_b64": latency, "config3_complex128_program": complex_path,
                           "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
-                          "config4_fmo": config4},
+                          "config4_fmo": config4, "config5_32q": config5},
             "clocks": clk.summary(),
         }
         # the sector kernel moves no HBM data in the step (theta in, E out, pair

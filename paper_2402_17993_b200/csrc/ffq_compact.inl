@@ -227,7 +227,7 @@ void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double
   const size_t dim = (size_t)cp.na * cp.nb;
   ctx->compact_psi.alloc(dim);
   ctx->compact_coef.alloc(3 * pl->cp.op_kind.size());
-  const int g = 8 * ctx->n_sm;  // term kernels: fixed grid (fixed partial slots)
+  const int g = 32 * ctx->n_sm;  // term kernels: fixed grid (fixed partial slots)
   const size_t nterm = cp.terms.size();
   ctx->compact_part.alloc(std::max<size_t>(1, nterm * g));
   const PlanDev pd = pl->dev();

@@ -28,5 +28,6 @@ for rep in range(2):
     b.synchronize()
     out[f"rep{rep}"] = {"energy": e, "ms": a.elapsed_time(b)}
 print(json.dumps({"config": 5, "n_qubits": nq, "generators": P.n_gen, "terms": len(P.H),
-                  "host_build_s": host_s, "path": "support-tracked graph, 1 GPU, 0 global qubits", **out}),
+                  "host_build_s": host_s, "path": ("compact real sector layout (ffq_compact.inl), 1 GPU" if nq >= 27 else
+                          "support-tracked graph, 1 GPU, 0 global qubits"), **out}),
       flush=True)
