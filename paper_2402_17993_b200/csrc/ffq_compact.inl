@@ -16,8 +16,9 @@
 //  - A Hamiltonian term (x, z, c) adds Re(c i^ny) * S with
 //    S = sum_k psi_k psi_{k^x} (-1)^popc((k^x) & z) over k with both members
 //    in the sector (ffo_oracle.c pauli_expect restricted to the sector; psi is
-//    real, so a term with Re(c i^ny) = 0 contributes nothing). Each term's CTA
-//    partials land in fixed slots; one fixed-order reduction gives the energy.
+//    real, so a term with Re(c i^ny) = 0 contributes nothing). Terms sharing a
+//    flip mask are one pass (the pair weight sums their signed w). Each pass's
+//    CTA partials land in fixed slots; one fixed-order reduction gives the energy.
 //
 // Eligibility (compact_program): n even, m = n / 2 <= 16, every op a fused
 // generator with one real pattern pair that keeps both spin counts.
@@ -28,9 +29,13 @@ constexpr int kCompactThreads = 256;
 struct CompactOp {  // one fused op over compressed alpha / beta strings
   uint32_t xa, la, za, xb, lb, zb;
 };
-struct CompactTerm {
-  uint32_t xa, za, xb, zb;
+struct CompactTerm {  // one Hamiltonian term of a flip-mask group
+  uint32_t za, zb;
   double w;  // Re(c i^ny)
+};
+struct CompactGroup {  // terms sharing the flip mask (xa, xb): one pass
+  uint32_t xa, xb;
+  int32_t t0, nt;
 };
 
 // per-op rotation coefficients for one theta row: (cos phi, sin phi * F_hi, sin phi * F_lo)
@@ -97,22 +102,26 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_gen(double* __restr
   }
 }
 
-// S of one term, CTA partial (times the term weight) into part[blockIdx.x]
+// One flip-mask group: sum over its pairs of psi_k psi_{k^x} * sum_t w_t
+// (-1)^popc((k^x) & z_t); the CTA partial goes to part[blockIdx.x]. MULTI =
+// false: a one-term group (random strings), its term t1 passed by value.
+template <bool MULTI>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_term(const double* __restrict__ psi, int na, int nb,
                                                                   const uint32_t* __restrict__ stra,
                                                                   const uint32_t* __restrict__ strb,
                                                                   const uint16_t* __restrict__ ranka,
-                                                                  const uint16_t* __restrict__ rankb, CompactTerm t,
-                                                                  double2* __restrict__ part) {
+                                                                  const uint16_t* __restrict__ rankb, CompactGroup gr,
+                                                                  const CompactTerm* __restrict__ terms,
+                                                                  CompactTerm t1, double2* __restrict__ part) {
   __shared__ double2 red[kCompactThreads / 32];
-  const int ha = __popc(t.xa) / 2, hb = __popc(t.xb) / 2;
+  const int ha = __popc(gr.xa) / 2, hb = __popc(gr.xb) / 2;
+  const CompactTerm* tt = terms + gr.t0;
   double acc = 0.0;
   for (int r = blockIdx.x; r < na; r += gridDim.x) {
     const uint32_t a = __ldg(stra + r);
-    if (__popc(a & t.xa) != ha) continue;
-    const uint32_t ap = a ^ t.xa;
+    if (__popc(a & gr.xa) != ha) continue;
+    const uint32_t ap = a ^ gr.xa;
     const int64_t ri = (int64_t)r * nb, rj = (int64_t)__ldg(ranka + ap) * nb;
-    const uint32_t sa = (uint32_t)__popc(ap & t.za) & 1u;
     double racc = 0.0;
     constexpr int U = 4;
     for (int c0 = threadIdx.x; c0 < nb; c0 += U * kCompactThreads) {
@@ -123,11 +132,21 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_term(const double* 
         v[u] = 0.0;
         if (col < nb) {
           const uint32_t b = __ldg(strb + col);
-          if (__popc(b & t.xb) == hb) {
-            const uint32_t bp = b ^ t.xb;
-            const int cj = t.xb ? __ldg(rankb + bp) : col;
+          if (__popc(b & gr.xb) == hb) {
+            const uint32_t bp = b ^ gr.xb;
+            const int cj = gr.xb ? __ldg(rankb + bp) : col;
             const double p = psi[ri + col] * psi[rj + cj];
-            v[u] = (sa ^ ((uint32_t)__popc(bp & t.zb) & 1u)) ? -p : p;
+            if (!MULTI) {
+              const uint32_t s = ((uint32_t)__popc(ap & t1.za) ^ (uint32_t)__popc(bp & t1.zb)) & 1u;
+              v[u] = s ? -t1.w * p : t1.w * p;
+            } else {
+              double f = 0.0;
+              for (int t = 0; t < gr.nt; ++t) {
+                const uint32_t s = ((uint32_t)__popc(ap & tt[t].za) ^ (uint32_t)__popc(bp & tt[t].zb)) & 1u;
+                f += s ? -tt[t].w : tt[t].w;
+              }
+              v[u] = f * p;
+            }
           }
         }
       }
@@ -137,7 +156,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_term(const double* 
     acc += racc;
   }
   const double2 tot = block_sum<kCompactThreads>(make_double2(acc, 0.0), red);
-  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t.w * tot.x, 0.0);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
 struct CompactProg {
@@ -145,7 +164,9 @@ struct CompactProg {
   int m = 0, na = 0, nb = 0;
   int64_t hf_at = 0;
   std::vector<CompactOp> ops;
-  std::vector<CompactTerm> terms;  // the terms that can contribute
+  std::vector<CompactGroup> groups;  // flip-mask groups of the terms that can contribute
+  std::vector<CompactTerm> host_terms;
+  DevBuf<CompactTerm> terms;
   DevBuf<uint32_t> stra, strb;
   DevBuf<uint16_t> ranka, rankb;
 };
@@ -198,17 +219,25 @@ CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64
     cp->na = (int)sa.size();
     cp->nb = (int)sb.size();
     cp->hf_at = (int64_t)ra[compact_pext(hf, ev)] * cp->nb + rb[compact_pext(hf, od)];
+    std::map<uint64_t, std::vector<CompactTerm>> by_x;  // (xa, xb) -> terms, in upload order
     for (size_t t = 0; t < h->raw_x.size(); ++t) {
       const uint64_t x = h->raw_x[t], z = h->raw_z[t];
       const int ny = __builtin_popcountll(x & z) & 3;
       // Re(c i^ny)
       const double w = ny == 0 ? h->raw_re[t] : ny == 1 ? -h->raw_im[t] : ny == 2 ? -h->raw_re[t] : h->raw_im[t];
-      CompactTerm ct{compact_pext(x, ev), compact_pext(z, ev), compact_pext(x, od), compact_pext(z, od), w};
-      if (w == 0.0 || __builtin_popcount(ct.xa) % 2 || __builtin_popcount(ct.xb) % 2) continue;
-      if (__builtin_popcount(ct.xa) / 2 > std::min(ka, m - ka) || __builtin_popcount(ct.xb) / 2 > std::min(kb, m - kb))
+      const uint32_t xa = compact_pext(x, ev), xb = compact_pext(x, od);
+      if (w == 0.0 || __builtin_popcount(xa) % 2 || __builtin_popcount(xb) % 2) continue;
+      if (__builtin_popcount(xa) / 2 > std::min(ka, m - ka) || __builtin_popcount(xb) / 2 > std::min(kb, m - kb))
         continue;  // no sector member can pair with a sector member
-      cp->terms.push_back(ct);
+      by_x[((uint64_t)xa << 32) | xb].push_back({compact_pext(z, ev), compact_pext(z, od), w});
     }
+    std::vector<CompactTerm>& tl = cp->host_terms;
+    for (const auto& kv : by_x) {
+      cp->groups.push_back({(uint32_t)(kv.first >> 32), (uint32_t)kv.first, (int32_t)tl.size(),
+                            (int32_t)kv.second.size()});
+      tl.insert(tl.end(), kv.second.begin(), kv.second.end());
+    }
+    cp->terms.upload(tl, ctx->stream);
     cp->stra.upload(sa, ctx->stream);
     cp->strb.upload(sb, ctx->stream);
     cp->ranka.upload(ra, ctx->stream);
@@ -228,7 +257,7 @@ void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double
   ctx->compact_psi.alloc(dim);
   ctx->compact_coef.alloc(3 * pl->cp.op_kind.size());
   const int g = 32 * ctx->n_sm;  // term kernels: fixed grid (fixed partial slots)
-  const size_t nterm = cp.terms.size();
+  const size_t nterm = cp.groups.size();
   ctx->compact_part.alloc(std::max<size_t>(1, nterm * g));
   const PlanDev pd = pl->dev();
   const int nops = (int)pl->cp.op_kind.size();
@@ -242,9 +271,9 @@ void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double
                                                              cp.ranka.p, cp.rankb.p, cp.ops[op],
                                                              ctx->compact_coef.p + 3 * op);
     for (size_t t = 0; t < nterm; ++t)
-      k_compact_term<<<g, kCompactThreads, 0, ctx->stream>>>(ctx->compact_psi.p, cp.na, cp.nb, cp.stra.p, cp.strb.p,
-                                                              cp.ranka.p, cp.rankb.p, cp.terms[t],
-                                                              ctx->compact_part.p + t * g);
+      (cp.groups[t].nt == 1 ? k_compact_term<false> : k_compact_term<true>)<<<g, kCompactThreads, 0, ctx->stream>>>(
+          ctx->compact_psi.p, cp.na, cp.nb, cp.stra.p, cp.strb.p, cp.ranka.p, cp.rankb.p, cp.groups[t], cp.terms.p,
+          cp.host_terms[cp.groups[t].t0], ctx->compact_part.p + t * g);
     if (nterm == 0) CK(cudaMemsetAsync(ctx->compact_part.p, 0, sizeof(double2), ctx->stream));
     k_reduce_partials<kThreads><<<1, kThreads, 0, ctx->stream>>>(ctx->compact_part.p,
                                                                   (int64_t)std::max<size_t>(1, nterm * g), e + b,
