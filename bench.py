@@ -288,6 +288,33 @@ def main():
             b.record(stream)
             b.synchronize()
             rot_ms.append(a.elapsed_time(b))
+    # fused run: 16 rotations with flip masks in the low 12 qubits (z anywhere),
+    # one TMA-staged tile pass (k_rotation_run), then its inverse
+    rr = np.random.default_rng(11)
+    run_x = rr.integers(1, 1 << 12, size=16, dtype=np.uint64)
+    run_z = rr.integers(0, 1 << nq, size=16, dtype=np.uint64)
+    run_th = rr.uniform(-1, 1, size=16)
+    run_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(12):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            fwd = k % 2 == 0
+            xs, zs, ts = (run_x, run_z, run_th) if fwd else (run_x[::-1].copy(), run_z[::-1].copy(), -run_th[::-1])
+            a.record(stream)
+            st.rotate_many(xs, zs, ts)  # includes the 16-descriptor upload (1 KiB) and the sync
+            b.record(stream)
+            b.synchronize()
+            run_ms.append(a.elapsed_time(b))
+    run_avg = statistics.mean(run_ms[2:])
+    rotation_run = {
+        "kernel": "k_rotation_run (16 low-qubit rotations per tile pass, 2^12-amplitude TMA tiles)",
+        "state_qubits": nq, "rotations_per_run": 16, "ms_per_run": run_avg,
+        "hbm_gbs": 32 * (1 << nq) / (run_avg / 1e3) / 1e9,
+        "hbm_frac": 32 * (1 << nq) / (run_avg / 1e3) / 1e9 / peak,
+        "ms_per_rotation": run_avg / 16,
+        "speedup_vs_unfused_passes": 16 * statistics.mean(rot_ms[2:]) / run_avg,
+    }
     del st
     rot_bytes = 32 * (1 << nq)
     rot_avg = statistics.mean(rot_ms[2:])
@@ -458,7 +485,7 @@ def main():
             "secondary": {"config3_latency_and_b64": latency, "config3_complex128_program": complex_path,
                           "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
-                          "config4_fmo": config4, "config5_32q": config5},
+                          "config4_fmo": config4, "config5_32q": config5, "rotation_run_28q": rotation_run},
             "clocks": clk.summary(),
         }
         # the sector kernel moves no HBM data in the step (theta in, E out, pair

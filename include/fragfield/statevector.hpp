@@ -91,6 +91,9 @@ class Statevector {
   void set_basis(uint64_t bits);
   /// e^{i theta P} on every row.
   void apply_pauli_rotation(const PauliString& p, double theta);
+  /// e^{i theta_r P_r} for r = 0, 1, ... in order; runs of low-qubit flip
+  /// masks are applied per shared-memory tile (ffq_state_apply_pauli_rotations).
+  void apply_pauli_rotations(const std::vector<PauliString>& ps, const std::vector<double>& theta);
   /// theta [batch][n_gen] in plan order.
   void apply_plan(const DevicePlan& plan, const std::vector<double>& theta);
   /// <psi|H|psi> per row; throws ContractViolation if |Im| > 1e-10.

@@ -9,6 +9,8 @@
  *
  *   ffq_state_set_basis            hf_state
  *   ffq_state_apply_pauli_rotation apply_pauli_rotation
+ *   ffq_state_apply_pauli_rotations apply_pauli_rotation over a string list
+ *                                  (Trotter step)
  *   ffq_state_expectation          expectation
  *   ffq_plan_upload                TrotterPlan
  *   ffq_state_apply_plan           energy_trotter (state) SPEC.md:508-516
@@ -139,6 +141,12 @@ int ffq_state_upload(ffq_state_t st, const double* psi);   /* [batch][2^n][2] */
 int ffq_state_download(ffq_state_t st, double* psi);       /* [batch][2^n][2] */
 /* psi <- cos(theta) psi + i sin(theta) P psi  (e^{i theta P}), every batch row */
 int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, double theta);
+/* The sequence e^{i theta[n_rot-1] P_{n_rot-1}} ... e^{i theta[0] P_0}, in order
+ * (apply_pauli_rotation over a Trotter string list).
+ * Runs of consecutive rotations whose flip masks lie in the low 12 qubits go
+ * through one shared-memory tile pass each (TMA-staged; FFQ_ROT_TILE). */
+int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x, const uint64_t* z,
+                                    const double* theta);
 /* Apply the plan with theta [batch][n_gen] (host pointer). */
 int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta);
 /* re_out/im_out [batch] (host) */

@@ -44,6 +44,7 @@ _SIGS = {
     "ffq_state_upload": (C.c_int, [_vp, _f64p]),
     "ffq_state_download": (C.c_int, [_vp, _f64p]),
     "ffq_state_apply_pauli_rotation": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_double]),
+    "ffq_state_apply_pauli_rotations": (C.c_int, [_vp, C.c_int, _u64p, _u64p, _f64p]),
     "ffq_state_apply_plan": (C.c_int, [_vp, _vp, _f64p]),
     "ffq_state_expectation": (C.c_int, [_vp, _vp, _f64p, _f64p]),
     "ffq_state_device_ptr": (C.c_int, [_vp, C.POINTER(_vp)]),
@@ -277,6 +278,14 @@ class State:
 
     def rotate(self, x, z, theta):
         check(lib().ffq_state_apply_pauli_rotation(self.h, x, z, theta), self.ctx.h)
+
+    def rotate_many(self, x, z, theta):
+        """e^{i theta_r P_r} for r = 0, 1, ... in order (low-qubit runs fused in tiles)."""
+        x = np.ascontiguousarray(x, np.uint64); z = np.ascontiguousarray(z, np.uint64)
+        th = np.ascontiguousarray(theta, np.float64)
+        if not (x.shape == z.shape == th.shape) or x.ndim != 1:
+            raise ContractViolation("x, z, theta must be 1-D arrays of one length")
+        check(lib().ffq_state_apply_pauli_rotations(self.h, len(x), x, z, th), self.ctx.h)
 
     def apply_plan(self, plan: Plan, theta):
         check(lib().ffq_state_apply_plan(self.h, plan.h, np.ascontiguousarray(theta, np.float64).ravel()),

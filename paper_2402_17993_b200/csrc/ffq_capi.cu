@@ -108,6 +108,8 @@ struct ffq_ctx_s {
   int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
                                              // support path is faster below: grouped Hamiltonian)
   DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
+  DevBuf<RotDesc> rot;       // ffq_state_apply_pauli_rotations: fused low-qubit runs
+  int rot_tile_bits = 12;    // env FFQ_ROT_TILE: tile of a fused run (0: one pass per rotation)
   DevBuf<uint32_t> slab_sup;
   bool slab_clean = false;      // support path: slab all-zero between graph replays
   DevBuf<double2> pslab;        // persistent-path slab, all-zero between evaluations
@@ -267,6 +269,19 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
   dim3 grid(grid_for(nvec, ctx->n_sm), batch);
   k_pauli_rotation<<<grid, kThreads, 0, ctx->stream>>>(psi, n, x, z, ny, cs, cs_stride, op, mode,
                                                         hbit);
+  CK(cudaGetLastError());
+  ctx->launches++;
+}
+
+// a run of rotations with flip masks below 2^t: one TMA-staged tile per CTA
+void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotDesc* rd, int n_rot) {
+  constexpr int NT = 512;
+  const size_t sb = sizeof(double2) << t;
+  CK(cudaFuncSetAttribute(k_rotation_run<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  CK(cudaFuncSetAttribute(k_rotation_run<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                          (int)cudaSharedmemCarveoutMaxShared));
+  dim3 grid((unsigned)(1u << (n - t)), batch);
+  k_rotation_run<NT><<<grid, NT, sb, ctx->stream>>>(psi, n, t, rd, n_rot);
   CK(cudaGetLastError());
   ctx->launches++;
 }
@@ -808,6 +823,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     c->smem_optin = (size_t)optin - 2048;  // static smem of the reduction scratch
     if (const char* e = std::getenv("FFQ_SMEM_MAX_QUBITS")) c->smem_max_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_ROT_TILE")) c->rot_tile_bits = std::min(12, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
@@ -1123,6 +1139,45 @@ int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, doubl
     launch_string(ctx, st->psi.p, st->n, st->batch, x, z, __builtin_popcountll(x & z) & 3, ctx->cs.p,
                   1, 0);
     st->sup_valid = false;  // dense pass: the support is rebuilt lazily
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FFQ_OK;
+  });
+}
+
+int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x, const uint64_t* z,
+                                    const double* theta) {
+  if (!st || n_rot < 0 || (n_rot > 0 && (!x || !z || !theta))) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
+  ffq_ctx_t ctx = st->ctx;
+  for (int r = 0; r < n_rot; ++r)
+    if (st->n < 64 && ((x[r] | z[r]) >> st->n)) return fail(ctx, FFQ_EINVAL, "Pauli string exceeds n_qubits");
+  return guarded(ctx, [&] {
+    if (n_rot == 0) return FFQ_OK;
+    if (st->n < 2) throw BadInput("rotation kernels need n_qubits >= 2", FFQ_EINVAL);
+    // maximal runs of >= 2 consecutive rotations with flip masks below 2^t
+    // are one tiled launch each; every other rotation is one pass
+    const int t = ctx->rot_tile_bits > 0 ? std::min(st->n, ctx->rot_tile_bits) : 0;
+    std::vector<RotDesc> rd(n_rot);
+    std::vector<double2> cs(n_rot);
+    for (int r = 0; r < n_rot; ++r) {
+      rd[r] = RotDesc{x[r], z[r], std::cos(theta[r]), std::sin(theta[r]), __builtin_popcountll(x[r] & z[r]) & 3,
+                      x[r] ? 63 - __builtin_clzll(x[r]) : 0};
+      cs[r] = make_double2(rd[r].c, rd[r].s);
+    }
+    ctx->rot.upload(rd, ctx->stream);
+    ctx->cs.upload(cs, ctx->stream);
+    for (int r = 0; r < n_rot;) {
+      int e = r;
+      if (t > 0)
+        while (e < n_rot && (x[e] >> t) == 0) ++e;
+      if (e - r >= 2) {
+        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot.p + r, e - r);
+        r = e;
+      } else {
+        launch_string(ctx, st->psi.p, st->n, st->batch, x[r], z[r], rd[r].ny, ctx->cs.p, 0, r);
+        ++r;
+      }
+    }
+    st->sup_valid = false;
     CK(cudaStreamSynchronize(ctx->stream));
     return FFQ_OK;
   });

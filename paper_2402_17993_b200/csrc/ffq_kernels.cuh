@@ -435,6 +435,71 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// ---- fused run of low-qubit rotations on TMA-staged tiles ------------------------
+// A run of consecutive rotations e^{i phi_r P_r} whose flip masks all lie in
+// the low t qubits maps every 2^t-amplitude tile (contiguous: the high bits of
+// the index are fixed) onto itself. One CTA stages its tile with bulk copies
+// (cp.async.bulk + mbarrier), applies the whole run in shared memory with a CTA
+// barrier between rotations, and writes the tile back with 32-byte stores: the
+// state crosses HBM once per run (32 B per amplitude) instead of once per
+// rotation. z is unrestricted: the parity of the tile's high bits is folded
+// into sin once per rotation. Per pair the arithmetic is k_pauli_rotation's.
+struct RotDesc {
+  uint64_t x, z;  // x < 2^t
+  double c, s;    // cos phi, sin phi
+  int ny;         // popc(x & z) & 3
+  int h;          // highest set bit of x (x != 0): the pair is (k, k ^ x) with bit h of k
+                  // clear, so for h >= 3 each 8-lane phase of a 16-byte shared access
+                  // covers one aligned 128-byte line (k) or a permutation of one (k ^ x)
+                  // and the pair loads and stores are bank-conflict-free
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_rotation_run(double2* __restrict__ psi, int n, int t,
+                                                     const RotDesc* __restrict__ rd, int n_rot) {
+  extern __shared__ __align__(128) double2 tl[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tsize = 1u << t, tmask = tsize - 1u;
+  const uint64_t base = (uint64_t)blockIdx.x << t;
+  double2* s = psi + ((int64_t)blockIdx.y << n) + base;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    const uint32_t bytes = tsize * (uint32_t)sizeof(double2);
+    mbar_expect_tx(&bar, bytes);
+    const uint32_t piece = 32768;
+    for (uint32_t off = 0; off < bytes; off += piece)
+      bulk_g2s((char*)tl + off, (const char*)s + off, min(piece, bytes - off), &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int r = 0; r < n_rot; ++r) {
+    const uint64_t x = __ldg(&rd[r].x), z = __ldg(&rd[r].z);
+    const double c = __ldg(&rd[r].c);
+    const double sn = __ldg(&rd[r].s) * sgn_par(base & z);
+    const uint32_t xl = (uint32_t)x, zl = (uint32_t)z & tmask;
+    if (xl == 0u) {
+      for (uint32_t k = threadIdx.x; k < tsize; k += NT) {
+        const double2 a = tl[k];
+        const double s0 = sn * sgn_par(k & zl);
+        tl[k] = make_double2(c * a.x - s0 * a.y, c * a.y + s0 * a.x);
+      }
+    } else {
+      const double2 w = ipow_d(__ldg(&rd[r].ny) + 1);
+      const int h = __ldg(&rd[r].h);
+      for (uint32_t u = threadIdx.x; u < (tsize >> 1); u += NT) {
+        const uint32_t k = insert_zero<uint32_t>(u, h), kp = k ^ xl;
+        const double2 a = tl[k], b = tl[kp];
+        const double sk = sn * sgn_par(k & zl), sp = sn * sgn_par(kp & zl);
+        const double2 wb = cmul(w, b), wa = cmul(w, a);
+        tl[k] = make_double2(c * a.x + sp * wb.x, c * a.y + sp * wb.y);
+        tl[kp] = make_double2(c * b.x + sk * wa.x, c * b.y + sk * wa.y);
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t k = 2 * threadIdx.x; k < tsize; k += 2 * NT) st256(s + k, tl[k], tl[k + 1]);
+}
+
 // ---- tiled expectation ---------------------------------------------------------
 // Work item = (bucket of groups sharing h = X >> t, tile pair {u, u ^ h}); the
 // low t qubits of the index form a contiguous 2^t-amplitude tile, so each tile

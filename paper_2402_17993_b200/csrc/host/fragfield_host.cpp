@@ -621,6 +621,16 @@ void Statevector::apply_pauli_rotation(const PauliString& p, double theta) {
   if (p.n_qubits != n_) throw ContractViolation("apply_pauli_rotation: qubit count mismatch");
   check_ffq(ffq_state_apply_pauli_rotation(s_, p.x, p.z, theta), dev_.handle());
 }
+void Statevector::apply_pauli_rotations(const std::vector<PauliString>& ps, const std::vector<double>& theta) {
+  if (ps.size() != theta.size()) throw ContractViolation("apply_pauli_rotations: one angle per string");
+  std::vector<uint64_t> x(ps.size()), z(ps.size());
+  for (size_t r = 0; r < ps.size(); ++r) {
+    if (ps[r].n_qubits != n_) throw ContractViolation("apply_pauli_rotations: qubit count mismatch");
+    x[r] = ps[r].x;
+    z[r] = ps[r].z;
+  }
+  check_ffq(ffq_state_apply_pauli_rotations(s_, (int)ps.size(), x.data(), z.data(), theta.data()), dev_.handle());
+}
 void Statevector::apply_plan(const DevicePlan& plan, const std::vector<double>& theta) {
   if (theta.size() != plan.plan().order.size() * (size_t)batch_)
     throw ContractViolation("apply_plan: theta must be [batch][n_gen]");

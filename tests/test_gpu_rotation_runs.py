@@ -1,0 +1,107 @@
+"""GPU parity of ffq_state_apply_pauli_rotations: runs of rotations whose flip
+masks lie in the low 12 qubits are applied per TMA-staged shared-memory tile
+(k_rotation_run, one HBM round trip per run), the others one pass each
+(k_pauli_rotation). Checked through the C-ABI against the oracle's
+apply_pauli_rotation string by string, against the unfused
+path (FFQ_ROT_TILE=0), and at 26 qubits through run-then-inverse-run.
+
+Tolerance: amplitudes <= 1e-12 max-abs (north_star)."""
+import numpy as np
+import pytest
+
+from paper_2402_17993_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+A_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return capi.Context(0)
+
+
+def random_state(rng, n, batch):
+    psi = rng.normal(size=(batch, 1 << n)) + 1j * rng.normal(size=(batch, 1 << n))
+    return psi / np.linalg.norm(psi, axis=1, keepdims=True)
+
+
+def random_strings(rng, n, count, low_frac=0.7):
+    """Mixed list: low flip masks (x < 2^min(n,12), incl. x = 0 and x odd),
+    high flip masks, z anywhere."""
+    lo = min(n, 12)
+    x = np.zeros(count, np.uint64)
+    z = rng.integers(0, 1 << n, size=count, dtype=np.uint64)
+    for r in range(count):
+        u = rng.random()
+        if u < 0.1:
+            x[r] = 0
+        elif u < low_frac:
+            x[r] = rng.integers(1, 1 << lo)
+        else:
+            x[r] = rng.integers(1, 1 << n)
+    th = rng.uniform(-np.pi, np.pi, size=count)
+    return x, z, th
+
+
+@pytest.mark.parametrize("n", [2, 5, 11, 12, 13, 16])
+def test_rotation_runs_vs_oracle(ctx, oracle, n):
+    rng = np.random.default_rng(100 + n)
+    psi = random_state(rng, n, 2)
+    x, z, th = random_strings(rng, n, 48)
+    st = capi.State(ctx, n, 2)
+    st.upload(psi)
+    st.rotate_many(x, z, th)
+    ref = psi.copy()
+    for b in range(2):
+        for r in range(len(x)):
+            ref[b] = oracle.apply_pauli_rotation(n, ref[b], int(x[r]), int(z[r]), float(th[r]))
+    assert np.abs(st.download() - ref).max() <= A_TOL
+
+
+def test_fused_runs_equal_unfused_and_launch_count(monkeypatch):
+    n = 20
+    rng = np.random.default_rng(7)
+    psi = random_state(rng, n, 1)
+    x = rng.integers(1, 1 << 12, size=32, dtype=np.uint64)  # one run of 32 low-qubit rotations
+    z = rng.integers(0, 1 << n, size=32, dtype=np.uint64)
+    th = rng.uniform(-1, 1, size=32)
+    out = {}
+    for tile in ("12", "0"):
+        monkeypatch.setenv("FFQ_ROT_TILE", tile)
+        c = capi.Context(0)
+        st = capi.State(c, n, 1)
+        st.upload(psi)
+        l0 = c.launches()
+        st.rotate_many(x, z, th)
+        out[tile] = (st.download()[0], c.launches() - l0)
+        del st  # the state before its context
+        c.close()
+    assert out["12"][1] == 1 and out["0"][1] == 32
+    assert np.abs(out["12"][0] - out["0"][0]).max() <= 1e-14
+
+
+def test_rotation_run_inverse_roundtrip_26q(ctx):
+    # 26 qubits (1 GiB): a mixed run, then the inverse run (reverse order, -theta) = I
+    n = 26
+    rng = np.random.default_rng(3)
+    psi = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)) / np.sqrt(2 << n)
+    x, z, th = random_strings(rng, n, 24)
+    st = capi.State(ctx, n, 1)
+    st.upload(psi)
+    st.rotate_many(x, z, th)
+    mid = st.download()[0]
+    assert abs(np.linalg.norm(mid) - np.linalg.norm(psi)) <= 1e-12
+    st.rotate_many(x[::-1].copy(), z[::-1].copy(), -th[::-1])
+    assert np.abs(st.download()[0] - psi).max() <= A_TOL
+
+
+def test_rotation_runs_edges(ctx):
+    st = capi.State(ctx, 6, 1)
+    st.set_basis(5)
+    st.rotate_many(np.zeros(0, np.uint64), np.zeros(0, np.uint64), np.zeros(0))  # empty list: no-op
+    assert st.download()[0][5] == 1.0
+    with pytest.raises(Exception):
+        st.rotate_many(np.array([1 << 6], np.uint64), np.array([0], np.uint64), np.array([0.1]))
+    with pytest.raises(capi.ContractViolation):
+        st.rotate_many(np.array([1, 2], np.uint64), np.array([0], np.uint64), np.array([0.1]))
