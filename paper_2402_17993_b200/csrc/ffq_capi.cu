@@ -137,6 +137,7 @@ struct ffq_plan_s {
   DevBuf<uint64_t> pair_bits, str_x, str_z;
   DevBuf<uint32_t> pair_low;
   DevBuf<double2> pair_f;
+  DevBuf<RotDesc> rot;  // per op: the string's (x, z, ny, pair bit) for fused runs of string ops
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int64_t> graph_nodes;
   struct SectorDevBufs {
@@ -274,14 +275,14 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
 }
 
 // a run of rotations with flip masks below 2^t: one TMA-staged tile per CTA
-void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotDesc* rd, int n_rot) {
-  constexpr int NT = 512;
+// (the 64 KiB dynamic-smem and carveout attributes are set at context creation,
+// so the launch can sit inside a captured graph)
+constexpr int kRotRunThreads = 512;
+void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotDesc* rd,
+                         const double2* cs, int cs_stride, int n_rot) {
   const size_t sb = sizeof(double2) << t;
-  CK(cudaFuncSetAttribute(k_rotation_run<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  CK(cudaFuncSetAttribute(k_rotation_run<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                          (int)cudaSharedmemCarveoutMaxShared));
   dim3 grid((unsigned)(1u << (n - t)), batch);
-  k_rotation_run<NT><<<grid, NT, sb, ctx->stream>>>(psi, n, t, rd, n_rot);
+  k_rotation_run<kRotRunThreads><<<grid, kRotRunThreads, sb, ctx->stream>>>(psi, n, t, rd, cs, cs_stride, n_rot);
   CK(cudaGetLastError());
   ctx->launches++;
 }
@@ -328,8 +329,18 @@ void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
       launch_fused(ctx, pl, psi, sup, n, batch, cp.fused[cp.op_idx[op]], cs, n_ops, op,
                    rstride ? rstride : (1LL << n));
     } else {
-      const int si = cp.op_idx[op];
-      launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
+      // a run of >= 2 string ops with flip masks below 2^t: one tiled pass
+      const int t = ctx->rot_tile_bits > 0 ? std::min(n, ctx->rot_tile_bits) : 0;
+      int e = op;
+      if (t > 0)
+        while (e < n_ops && cp.op_kind[e] != 0 && (cp.str_x[cp.op_idx[e]] >> t) == 0) ++e;
+      if (e - op >= 2) {
+        launch_rotation_run(ctx, psi, n, batch, t, pl->rot.p + op, cs + op, n_ops, e - op);
+        op = e - 1;
+      } else {
+        const int si = cp.op_idx[op];
+        launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
+      }
       stale = true;
     }
   }
@@ -824,6 +835,10 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_SMEM_MAX_QUBITS")) c->smem_max_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_ROT_TILE")) c->rot_tile_bits = std::min(12, std::max(0, std::atoi(e)));
+    CK(cudaFuncSetAttribute(k_rotation_run<kRotRunThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double2) << 12)));
+    CK(cudaFuncSetAttribute(k_rotation_run<kRotRunThreads>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            (int)cudaSharedmemCarveoutMaxShared));
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
     if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
@@ -954,6 +969,14 @@ int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_
     std::vector<double2> pf(cp.pair_f.size() / 2);
     for (size_t i = 0; i < pf.size(); ++i) pf[i] = make_double2(cp.pair_f[2 * i], cp.pair_f[2 * i + 1]);
     p->pair_f.upload(pf, ctx->stream);
+    std::vector<RotDesc> rd(cp.op_kind.size(), RotDesc{0, 0, 0, 0});
+    for (size_t op = 0; op < cp.op_kind.size(); ++op)
+      if (cp.op_kind[op] != 0) {
+        const int si = cp.op_idx[op];
+        const uint64_t x = cp.str_x[si];
+        rd[op] = RotDesc{x, cp.str_z[si], cp.str_ny[si], x ? 63 - __builtin_clzll(x) : 0};
+      }
+    p->rot.upload(rd, ctx->stream);
     p->str_x.upload(cp.str_x, ctx->stream);
     p->str_z.upload(cp.str_z, ctx->stream);
     p->str_ny.upload(cp.str_ny, ctx->stream);
@@ -1159,9 +1182,8 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
     std::vector<RotDesc> rd(n_rot);
     std::vector<double2> cs(n_rot);
     for (int r = 0; r < n_rot; ++r) {
-      rd[r] = RotDesc{x[r], z[r], std::cos(theta[r]), std::sin(theta[r]), __builtin_popcountll(x[r] & z[r]) & 3,
-                      x[r] ? 63 - __builtin_clzll(x[r]) : 0};
-      cs[r] = make_double2(rd[r].c, rd[r].s);
+      rd[r] = RotDesc{x[r], z[r], __builtin_popcountll(x[r] & z[r]) & 3, x[r] ? 63 - __builtin_clzll(x[r]) : 0};
+      cs[r] = make_double2(std::cos(theta[r]), std::sin(theta[r]));
     }
     ctx->rot.upload(rd, ctx->stream);
     ctx->cs.upload(cs, ctx->stream);
@@ -1170,7 +1192,7 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
       if (t > 0)
         while (e < n_rot && (x[e] >> t) == 0) ++e;
       if (e - r >= 2) {
-        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot.p + r, e - r);
+        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot.p + r, ctx->cs.p + r, 0, e - r);
         r = e;
       } else {
         launch_string(ctx, st->psi.p, st->n, st->batch, x[r], z[r], rd[r].ny, ctx->cs.p, 0, r);

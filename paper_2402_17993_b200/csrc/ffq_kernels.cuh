@@ -446,7 +446,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // into sin once per rotation. Per pair the arithmetic is k_pauli_rotation's.
 struct RotDesc {
   uint64_t x, z;  // x < 2^t
-  double c, s;    // cos phi, sin phi
   int ny;         // popc(x & z) & 3
   int h;          // highest set bit of x (x != 0): the pair is (k, k ^ x) with bit h of k
                   // clear, so for h >= 3 each 8-lane phase of a 16-byte shared access
@@ -456,7 +455,10 @@ struct RotDesc {
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_rotation_run(double2* __restrict__ psi, int n, int t,
-                                                     const RotDesc* __restrict__ rd, int n_rot) {
+                                                     const RotDesc* __restrict__ rd,
+                                                     const double2* __restrict__ cs, int cs_stride,
+                                                     int n_rot) {
+  // rotation r of row b: (cos phi, sin phi) = cs[b * cs_stride + r]
   extern __shared__ __align__(128) double2 tl[];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t tsize = 1u << t, tmask = tsize - 1u;
@@ -474,8 +476,9 @@ __global__ void __launch_bounds__(NT) k_rotation_run(double2* __restrict__ psi, 
   mbar_wait(&bar, 0);
   for (int r = 0; r < n_rot; ++r) {
     const uint64_t x = __ldg(&rd[r].x), z = __ldg(&rd[r].z);
-    const double c = __ldg(&rd[r].c);
-    const double sn = __ldg(&rd[r].s) * sgn_par(base & z);
+    const double2 csv = __ldg(&cs[(int64_t)blockIdx.y * cs_stride + r]);
+    const double c = csv.x;
+    const double sn = csv.y * sgn_par(base & z);
     const uint32_t xl = (uint32_t)x, zl = (uint32_t)z & tmask;
     if (xl == 0u) {
       for (uint32_t k = threadIdx.x; k < tsize; k += NT) {

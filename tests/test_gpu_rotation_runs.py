@@ -105,3 +105,35 @@ def test_rotation_runs_edges(ctx):
         st.rotate_many(np.array([1 << 6], np.uint64), np.array([0], np.uint64), np.array([0.1]))
     with pytest.raises(capi.ContractViolation):
         st.rotate_many(np.array([1, 2], np.uint64), np.array([0], np.uint64), np.array([0.1]))
+
+
+def test_plan_string_runs_fused_equal_unfused(monkeypatch):
+    """Plan path (run_plan_ops): consecutive string ops with low flip masks run
+    as one k_rotation_run inside the captured graph. SCBKT config 3 (16 qubits,
+    every generator as per-string rotations): energies equal the unfused
+    passes' to 1e-12 with fewer launches; the JW energies are the anchor
+    (test_scbkt_energies_match_jw)."""
+    from paper_2402_17993_b200 import problems
+
+    R = problems.config_problem(3, batch=2, mapping="scbkt")
+    J = problems.config_problem(3, batch=2)
+    res = {}
+    for tile in ("12", "0"):
+        monkeypatch.setenv("FFQ_ROT_TILE", tile)
+        c = capi.Context(0)
+        plan = capi.Plan(c, R.n_qubits, *R.plan_arrays())
+        ham = capi.Hamiltonian(c, R.n_qubits, *R.ham_arrays())
+        l0 = c.launches()
+        e = capi.energy_batch(c, plan, ham, R.hf, R.plan_thetas())
+        res[tile] = (e, c.launches() - l0)
+        del plan, ham
+        c.close()
+    assert np.abs(res["12"][0] - res["0"][0]).max() <= 1e-12
+    assert res["12"][1] < res["0"][1]
+    c = capi.Context(0)
+    plan = capi.Plan(c, J.n_qubits, *J.plan_arrays())
+    ham = capi.Hamiltonian(c, J.n_qubits, *J.ham_arrays())
+    ej = capi.energy_batch(c, plan, ham, J.hf, J.plan_thetas())
+    del plan, ham
+    c.close()
+    assert np.abs(res["12"][0] - ej).max() <= 1e-10
