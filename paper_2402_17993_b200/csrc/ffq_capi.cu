@@ -116,6 +116,19 @@ struct ffq_ctx_s {
   bool pslab_clean = false;
   double* pinned = nullptr;
   size_t pinned_n = 0;
+  // ffq_energy_batch: chunk H2D copies on their own stream, so a copy overlaps
+  // the previous chunk's kernels instead of sitting between them
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_done;
+  cudaEvent_t copy_event(size_t k) {
+    if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    while (copy_done.size() <= k) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      copy_done.push_back(e);
+    }
+    return copy_done[k];
+  }
   void ensure_pinned(size_t n) {
     if (n <= pinned_n) return;
     if (pinned) cudaFreeHost(pinned);
@@ -870,6 +883,8 @@ int ffq_ctx_destroy(ffq_ctx_t ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (cudaEvent_t e : ctx->copy_done) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
   return FFQ_OK;
 }
@@ -1062,10 +1077,24 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
     // first chunk one wave (its staging is the exposed part), then two waves
     const bool piped = nth * sizeof(double) >= (size_t)(1 << 20);
     const int wave = std::max(1, ctx->n_sm);
+    if (piped) {
+      // the copies start after everything already queued on the context stream
+      const cudaEvent_t start = ctx->copy_event(0);
+      CK(cudaEventRecord(start, ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
+    }
     for (int b0 = 0, k = 0; b0 < batch; ++k) {
       const int nb = piped ? std::min((k == 0 ? 1 : 2) * wave, batch - b0) : batch;
       const size_t o = (size_t)b0 * ng, n = (size_t)nb * ng;
-      if (n) {
+      if (n && piped) {
+        // chunk k's copy runs on the copy stream while chunk k - 1 computes
+        std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
+        const cudaEvent_t ev = ctx->copy_event((size_t)k + 1);
+        CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->copy_stream));
+        CK(cudaEventRecord(ev, ctx->copy_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
+      } else if (n) {
         std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
         CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
       }
