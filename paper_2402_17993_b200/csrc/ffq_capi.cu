@@ -78,6 +78,76 @@ struct DevBuf {
   }
 };
 
+// Runs of >= 2 consecutive eligible rotations (flip mask below 2^t), each cut
+// into groups of consecutive rotations whose flip masks span <= 3 dimensions
+// (k_rotation_run). Fills RotDesc::cx; group ranges are relative to the run.
+struct RotRuns {
+  std::vector<int> run_at;  // per rotation: index of the run starting there, else -1
+  std::vector<int> len, g0, ng;
+  std::vector<RotGroup> groups;
+};
+
+RotRuns build_rot_runs(std::vector<RotDesc>& rd, const std::vector<char>& ok, int t) {
+  RotRuns R;
+  const int N = (int)rd.size();
+  R.run_at.assign(N, -1);
+  if (t < 3) return R;
+  for (int i = 0; i < N;) {
+    if (!ok[i]) { ++i; continue; }
+    int e = i;
+    while (e < N && ok[e]) ++e;
+    if (e - i < 2) { i = e; continue; }
+    R.run_at[i] = (int)R.len.size();
+    R.len.push_back(e - i);
+    R.g0.push_back((int)R.groups.size());
+    for (int r = i; r < e;) {
+      uint32_t b[3];
+      int piv[3], d = 0, q = r;
+      for (; q < e; ++q) {
+        uint32_t v = (uint32_t)rd[q].x;
+        for (int j = 0; j < d; ++j)
+          if ((v >> piv[j]) & 1u) v ^= b[j];
+        if (!v) continue;  // in the span: joins the group
+        if (d == 3) break;
+        const int p = 31 - __builtin_clz(v);
+        for (int j = 0; j < d; ++j)
+          if ((b[j] >> p) & 1u) b[j] ^= v;
+        b[d] = v;
+        piv[d++] = p;
+      }
+      for (int bit = t - 1; d < 3; --bit) {  // pad with unit vectors at the highest free bits
+        bool used = false;
+        for (int j = 0; j < d; ++j) used |= piv[j] == bit;
+        if (used) continue;
+        for (int j = 0; j < d; ++j)
+          if ((b[j] >> bit) & 1u) b[j] ^= 1u << bit;
+        b[d] = 1u << bit;
+        piv[d++] = bit;
+      }
+      RotGroup G;
+      int ord[3] = {0, 1, 2};
+      std::sort(ord, ord + 3, [&](int a2, int b2) { return piv[a2] < piv[b2]; });
+      for (int j = 0; j < 3; ++j) {
+        G.b[j] = b[ord[j]];
+        G.piv[j] = piv[ord[j]];
+      }
+      G.r0 = r - i;
+      G.r1 = q - i;
+      for (int j = r; j < q; ++j) {
+        int cx = 0;
+        for (int k = 0; k < 3; ++k)
+          if ((rd[j].x >> G.piv[k]) & 1u) cx |= 1 << k;
+        rd[j].cx = cx;
+      }
+      R.groups.push_back(G);
+      r = q;
+    }
+    R.ng.push_back((int)R.groups.size() - R.g0.back());
+    i = e;
+  }
+  return R;
+}
+
 }  // namespace
 
 struct ffq_ctx_s {
@@ -109,6 +179,7 @@ struct ffq_ctx_s {
                                              // support path is faster below: grouped Hamiltonian)
   DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
   DevBuf<RotDesc> rot;       // ffq_state_apply_pauli_rotations: fused low-qubit runs
+  DevBuf<RotGroup> rot_groups;
   int rot_tile_bits = 12;    // env FFQ_ROT_TILE: tile of a fused run (0: one pass per rotation)
   DevBuf<uint32_t> slab_sup;
   bool slab_clean = false;      // support path: slab all-zero between graph replays
@@ -150,7 +221,10 @@ struct ffq_plan_s {
   DevBuf<uint64_t> pair_bits, str_x, str_z;
   DevBuf<uint32_t> pair_low;
   DevBuf<double2> pair_f;
-  DevBuf<RotDesc> rot;  // per op: the string's (x, z, ny, pair bit) for fused runs of string ops
+  DevBuf<RotDesc> rot;  // per op: the string's (x, z, ny, coset coordinate) for fused runs of string ops
+  RotRuns runs;         // runs of string ops with low flip masks (context's FFQ_ROT_TILE)
+  int runs_t = 0;
+  DevBuf<RotGroup> rot_groups;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int64_t> graph_nodes;
   struct SectorDevBufs {
@@ -290,12 +364,12 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
 // a run of rotations with flip masks below 2^t: one TMA-staged tile per CTA
 // (the 64 KiB dynamic-smem and carveout attributes are set at context creation,
 // so the launch can sit inside a captured graph)
-constexpr int kRotRunThreads = 512;
-void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotDesc* rd,
-                         const double2* cs, int cs_stride, int n_rot) {
+constexpr int kRotRunThreads = 256;  // 3 CTAs (64 KiB tiles) per SM
+void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotGroup* g, int n_grp,
+                         const RotDesc* rd, const double2* cs, int cs_stride) {
   const size_t sb = sizeof(double2) << t;
   dim3 grid((unsigned)(1u << (n - t)), batch);
-  k_rotation_run<kRotRunThreads><<<grid, kRotRunThreads, sb, ctx->stream>>>(psi, n, t, rd, cs, cs_stride, n_rot);
+  k_rotation_run<kRotRunThreads><<<grid, kRotRunThreads, sb, ctx->stream>>>(psi, n, t, g, n_grp, rd, cs, cs_stride);
   CK(cudaGetLastError());
   ctx->launches++;
 }
@@ -343,13 +417,11 @@ void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
                    rstride ? rstride : (1LL << n));
     } else {
       // a run of >= 2 string ops with flip masks below 2^t: one tiled pass
-      const int t = ctx->rot_tile_bits > 0 ? std::min(n, ctx->rot_tile_bits) : 0;
-      int e = op;
-      if (t > 0)
-        while (e < n_ops && cp.op_kind[e] != 0 && (cp.str_x[cp.op_idx[e]] >> t) == 0) ++e;
-      if (e - op >= 2) {
-        launch_rotation_run(ctx, psi, n, batch, t, pl->rot.p + op, cs + op, n_ops, e - op);
-        op = e - 1;
+      const int ri = pl->runs.run_at[op];
+      if (ri >= 0) {
+        launch_rotation_run(ctx, psi, n, batch, pl->runs_t, pl->rot_groups.p + pl->runs.g0[ri], pl->runs.ng[ri],
+                            pl->rot.p + op, cs + op, n_ops);
+        op += pl->runs.len[ri] - 1;
       } else {
         const int si = cp.op_idx[op];
         launch_string(ctx, psi, n, batch, cp.str_x[si], cp.str_z[si], cp.str_ny[si], cs, n_ops, op);
@@ -989,8 +1061,14 @@ int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_
       if (cp.op_kind[op] != 0) {
         const int si = cp.op_idx[op];
         const uint64_t x = cp.str_x[si];
-        rd[op] = RotDesc{x, cp.str_z[si], cp.str_ny[si], x ? 63 - __builtin_clzll(x) : 0};
+        rd[op] = RotDesc{x, cp.str_z[si], cp.str_ny[si], 0};
       }
+    p->runs_t = ctx->rot_tile_bits > 0 ? std::min(n_qubits, ctx->rot_tile_bits) : 0;
+    std::vector<char> ok(rd.size(), 0);
+    for (size_t op = 0; op < rd.size(); ++op)
+      ok[op] = cp.op_kind[op] != 0 && p->runs_t >= 3 && (rd[op].x >> p->runs_t) == 0;
+    p->runs = build_rot_runs(rd, ok, p->runs_t);
+    p->rot_groups.upload(p->runs.groups, ctx->stream);
     p->rot.upload(rd, ctx->stream);
     p->str_x.upload(cp.str_x, ctx->stream);
     p->str_z.upload(cp.str_z, ctx->stream);
@@ -1210,19 +1288,22 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
     const int t = ctx->rot_tile_bits > 0 ? std::min(st->n, ctx->rot_tile_bits) : 0;
     std::vector<RotDesc> rd(n_rot);
     std::vector<double2> cs(n_rot);
+    std::vector<char> ok(n_rot);
     for (int r = 0; r < n_rot; ++r) {
-      rd[r] = RotDesc{x[r], z[r], __builtin_popcountll(x[r] & z[r]) & 3, x[r] ? 63 - __builtin_clzll(x[r]) : 0};
+      rd[r] = RotDesc{x[r], z[r], __builtin_popcountll(x[r] & z[r]) & 3, 0};
       cs[r] = make_double2(std::cos(theta[r]), std::sin(theta[r]));
+      ok[r] = t >= 3 && (x[r] >> t) == 0;
     }
+    const RotRuns runs = build_rot_runs(rd, ok, t);
     ctx->rot.upload(rd, ctx->stream);
+    ctx->rot_groups.upload(runs.groups, ctx->stream);
     ctx->cs.upload(cs, ctx->stream);
     for (int r = 0; r < n_rot;) {
-      int e = r;
-      if (t > 0)
-        while (e < n_rot && (x[e] >> t) == 0) ++e;
-      if (e - r >= 2) {
-        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot.p + r, ctx->cs.p + r, 0, e - r);
-        r = e;
+      const int ri = runs.run_at[r];
+      if (ri >= 0) {
+        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot_groups.p + runs.g0[ri], runs.ng[ri],
+                            ctx->rot.p + r, ctx->cs.p + r, 0);
+        r += runs.len[ri];
       } else {
         launch_string(ctx, st->psi.p, st->n, st->batch, x[r], z[r], rd[r].ny, ctx->cs.p, 0, r);
         ++r;

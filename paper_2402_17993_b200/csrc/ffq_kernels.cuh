@@ -439,31 +439,78 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // A run of consecutive rotations e^{i phi_r P_r} whose flip masks all lie in
 // the low t qubits maps every 2^t-amplitude tile (contiguous: the high bits of
 // the index are fixed) onto itself. One CTA stages its tile with bulk copies
-// (cp.async.bulk + mbarrier), applies the whole run in shared memory with a CTA
-// barrier between rotations, and writes the tile back with 32-byte stores: the
-// state crosses HBM once per run (32 B per amplitude) instead of once per
-// rotation. z is unrestricted: the parity of the tile's high bits is folded
-// into sin once per rotation. Per pair the arithmetic is k_pauli_rotation's.
+// (cp.async.bulk + mbarrier), applies the whole run in shared memory, and
+// writes the tile back with 32-byte stores: the state crosses HBM once per run
+// (32 B per amplitude) instead of once per rotation.
+// Inside the tile the run is cut (on the host) into groups of consecutive
+// rotations whose flip masks span at most 3 dimensions over GF(2). A group has
+// a reduced-echelon basis {b_0, b_1, b_2} with pivot bits p_i (b_i has bit p_i,
+// no other b_j does); the cosets k ^ span{b} with the pivot bits of k clear
+// partition the tile into 2^(t-3) sets of 8, and every pair (k', k' ^ x) of
+// every rotation of the group lies inside one coset. Each thread loads one
+// coset into registers, applies the group's rotations in order there, and
+// stores it: one shared-memory round trip per group instead of per rotation,
+// one CTA barrier per group. The pivot bits are the highest available, so
+// lanes of a quarter warp differ in low bits (conflict-free 16-byte accesses).
+// z is unrestricted: the tile's high-bit parity is folded into sin once per
+// rotation. Per pair the arithmetic is k_pauli_rotation's.
 struct RotDesc {
   uint64_t x, z;  // x < 2^t
   int ny;         // popc(x & z) & 3
-  int h;          // highest set bit of x (x != 0): the pair is (k, k ^ x) with bit h of k
-                  // clear, so for h >= 3 each 8-lane phase of a 16-byte shared access
-                  // covers one aligned 128-byte line (k) or a permutation of one (k ^ x)
-                  // and the pair loads and stores are bank-conflict-free
+  int cx;         // x in its group's basis: bit i set <=> b_i in x (x = 0: diagonal)
+};
+struct RotGroup {
+  int r0, r1;        // rotations [r0, r1) of the run
+  uint32_t b[3];     // reduced-echelon basis (padded with unit vectors to 3)
+  int piv[3];        // pivot bits, ascending
 };
 
+// rotation of the coset registers v[0..7] on the pairs (e, e ^ CX), e < e ^ CX.
+// w = i^(ny+1) is +-1 (IM = false, ws = w) or +-i (IM = true, ws = Im w), so
+// w b is a sign and (for +-i) a swap: no complex multiply. sg[e] = +-sin phi.
+// sg[e] already carries the sign of w (ws * sin phi * parity sign, exact).
+template <int CX, bool IM>
+__device__ __forceinline__ void coset_pairs(double2 (&v)[8], double c, const double (&sg)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < (e ^ CX)) {
+      const int f = e ^ CX;
+      const double2 a = v[e], b = v[f];
+      if (IM) {
+        v[e] = make_double2(c * a.x - sg[f] * b.y, c * a.y + sg[f] * b.x);
+        v[f] = make_double2(c * b.x - sg[e] * a.y, c * b.y + sg[e] * a.x);
+      } else {
+        v[e] = make_double2(c * a.x + sg[f] * b.x, c * a.y + sg[f] * b.y);
+        v[f] = make_double2(c * b.x + sg[e] * a.x, c * b.y + sg[e] * a.y);
+      }
+    }
+  }
+}
+template <bool IM>
+__device__ __forceinline__ void coset_rot(int cx, double2 (&v)[8], double c, const double (&sg)[8]) {
+  switch (cx) {
+    case 1: coset_pairs<1, IM>(v, c, sg); break;
+    case 2: coset_pairs<2, IM>(v, c, sg); break;
+    case 3: coset_pairs<3, IM>(v, c, sg); break;
+    case 4: coset_pairs<4, IM>(v, c, sg); break;
+    case 5: coset_pairs<5, IM>(v, c, sg); break;
+    case 6: coset_pairs<6, IM>(v, c, sg); break;
+    default: coset_pairs<7, IM>(v, c, sg); break;
+  }
+}
+
 template <int NT>
-__global__ void __launch_bounds__(NT) k_rotation_run(double2* __restrict__ psi, int n, int t,
+__global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ psi, int n, int t,
+                                                     const RotGroup* __restrict__ grp, int n_grp,
                                                      const RotDesc* __restrict__ rd,
-                                                     const double2* __restrict__ cs, int cs_stride,
-                                                     int n_rot) {
+                                                     const double2* __restrict__ cs, int cs_stride) {
   // rotation r of row b: (cos phi, sin phi) = cs[b * cs_stride + r]
   extern __shared__ __align__(128) double2 tl[];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t tsize = 1u << t, tmask = tsize - 1u;
   const uint64_t base = (uint64_t)blockIdx.x << t;
   double2* s = psi + ((int64_t)blockIdx.y << n) + base;
+  const double2* csb = cs + (int64_t)blockIdx.y * cs_stride;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     const uint32_t bytes = tsize * (uint32_t)sizeof(double2);
@@ -474,29 +521,52 @@ __global__ void __launch_bounds__(NT) k_rotation_run(double2* __restrict__ psi, 
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  for (int r = 0; r < n_rot; ++r) {
-    const uint64_t x = __ldg(&rd[r].x), z = __ldg(&rd[r].z);
-    const double2 csv = __ldg(&cs[(int64_t)blockIdx.y * cs_stride + r]);
-    const double c = csv.x;
-    const double sn = csv.y * sgn_par(base & z);
-    const uint32_t xl = (uint32_t)x, zl = (uint32_t)z & tmask;
-    if (xl == 0u) {
-      for (uint32_t k = threadIdx.x; k < tsize; k += NT) {
-        const double2 a = tl[k];
-        const double s0 = sn * sgn_par(k & zl);
-        tl[k] = make_double2(c * a.x - s0 * a.y, c * a.y + s0 * a.x);
+  for (int g = 0; g < n_grp; ++g) {
+    const RotGroup G = grp[g];
+    uint32_t off[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      off[c] = ((c & 1) ? G.b[0] : 0u) ^ ((c & 2) ? G.b[1] : 0u) ^ ((c & 4) ? G.b[2] : 0u);
+    for (uint32_t u = threadIdx.x; u < (tsize >> 3); u += NT) {
+      const uint32_t k = insert_zero<uint32_t>(insert_zero<uint32_t>(insert_zero<uint32_t>(u, G.piv[0]), G.piv[1]),
+                                               G.piv[2]);
+      double2 v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = tl[k ^ off[c]];
+      for (int r = G.r0; r < G.r1; ++r) {
+        const uint64_t z = __ldg(&rd[r].z);
+        const int cx = __ldg(&rd[r].cx);
+        const double2 csv = __ldg(&csb[r]);
+        const double c = csv.x, sn = csv.y * sgn_par(base & z);
+        const uint32_t zl = (uint32_t)z & tmask;
+        // parity of (k ^ off[e]) & z = parity(k & z) ^ parity(off[e] & z), the
+        // second a XOR of the basis parities: one sign flip of sin per member
+        const uint32_t pb = (__popc(G.b[0] & zl) & 1u) | ((__popc(G.b[1] & zl) & 1u) << 1) |
+                            ((__popc(G.b[2] & zl) & 1u) << 2);
+        const int wk = cx ? (__ldg(&rd[r].ny) + 1) & 3 : 0;  // w = i^wk (pairs only)
+        const double snw = (wk == 2 || wk == 3) ? -sn : sn;   // sign of w folded into sin
+        const double snk = (__popc(k & zl) & 1u) ? -snw : snw;
+        double sg[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t flip = (uint32_t)(__popc(pb & (uint32_t)e) & 1) << 31;
+          sg[e] = __hiloint2double((int)((uint32_t)__double2hiint(snk) ^ flip), __double2loint(snk));
+        }
+        if (cx == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const double2 a = v[e];
+            v[e] = make_double2(c * a.x - sg[e] * a.y, c * a.y + sg[e] * a.x);
+          }
+        } else {
+          if (wk & 1)
+            coset_rot<true>(cx, v, c, sg);
+          else
+            coset_rot<false>(cx, v, c, sg);
+        }
       }
-    } else {
-      const double2 w = ipow_d(__ldg(&rd[r].ny) + 1);
-      const int h = __ldg(&rd[r].h);
-      for (uint32_t u = threadIdx.x; u < (tsize >> 1); u += NT) {
-        const uint32_t k = insert_zero<uint32_t>(u, h), kp = k ^ xl;
-        const double2 a = tl[k], b = tl[kp];
-        const double sk = sn * sgn_par(k & zl), sp = sn * sgn_par(kp & zl);
-        const double2 wb = cmul(w, b), wa = cmul(w, a);
-        tl[k] = make_double2(c * a.x + sp * wb.x, c * a.y + sp * wb.y);
-        tl[kp] = make_double2(c * b.x + sk * wa.x, c * b.y + sk * wa.y);
-      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tl[k ^ off[c]] = v[c];
     }
     __syncthreads();
   }
