@@ -541,17 +541,22 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
         const uint32_t zl = (uint32_t)z & tmask;
         // parity of (k ^ off[e]) & z = parity(k & z) ^ parity(off[e] & z), the
         // second a XOR of the basis parities: one sign flip of sin per member
-        const uint32_t pb = (__popc(G.b[0] & zl) & 1u) | ((__popc(G.b[1] & zl) & 1u) << 1) |
-                            ((__popc(G.b[2] & zl) & 1u) << 2);
+        const uint32_t p0 = (uint32_t)__popc(G.b[0] & zl) << 31, p1 = (uint32_t)__popc(G.b[1] & zl) << 31,
+                       p2 = (uint32_t)__popc(G.b[2] & zl) << 31;  // basis parities in bit 31
         const int wk = cx ? (__ldg(&rd[r].ny) + 1) & 3 : 0;  // w = i^wk (pairs only)
         const double snw = (wk == 2 || wk == 3) ? -sn : sn;   // sign of w folded into sin
         const double snk = (__popc(k & zl) & 1u) ? -snw : snw;
+        uint32_t hi[8];
+        hi[0] = (uint32_t)__double2hiint(snk);
+        hi[1] = hi[0] ^ p0;
+        hi[2] = hi[0] ^ p1;
+        hi[3] = hi[1] ^ p1;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hi[4 + e] = hi[e] ^ p2;
+        const int lo = __double2loint(snk);
         double sg[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t flip = (uint32_t)(__popc(pb & (uint32_t)e) & 1) << 31;
-          sg[e] = __hiloint2double((int)((uint32_t)__double2hiint(snk) ^ flip), __double2loint(snk));
-        }
+        for (int e = 0; e < 8; ++e) sg[e] = __hiloint2double((int)hi[e], lo);
         if (cx == 0) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
