@@ -147,6 +147,12 @@ int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, doubl
  * through one shared-memory tile pass each (TMA-staged; FFQ_ROT_TILE). */
 int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x, const uint64_t* z,
                                     const double* theta);
+/* Host only (no device work): how ffq_state_apply_pauli_rotations cuts a list
+ * of flip masks for tile bits t. run_of/group_of/cx [n_rot]: run and group of
+ * each rotation (-1 when it is a single pass) and x's coordinates in its
+ * group's basis; basis/piv [n_rot * 3] (first 3 * n_groups used). */
+int ffq_rotation_groups(int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
+                        uint32_t* basis, int32_t* piv, int32_t* n_groups);
 /* Apply the plan with theta [batch][n_gen] (host pointer). */
 int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta);
 /* re_out/im_out [batch] (host) */

@@ -19,6 +19,7 @@ FFQ_OK, FFQ_EINVAL, FFQ_ENONHERMITIAN, FFQ_ECUDA, FFQ_ENOMEM, FFQ_ENCCL, FFQ_ENO
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 
 _SIGS = {
@@ -45,6 +46,9 @@ _SIGS = {
     "ffq_state_download": (C.c_int, [_vp, _f64p]),
     "ffq_state_apply_pauli_rotation": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_double]),
     "ffq_state_apply_pauli_rotations": (C.c_int, [_vp, C.c_int, _u64p, _u64p, _f64p]),
+    "ffq_rotation_groups": (C.c_int, [C.c_int, C.c_int, _u64p, _i32p, _i32p, _i32p,
+                                      np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS"), _i32p,
+                                      C.POINTER(C.c_int32)]),
     "ffq_state_apply_plan": (C.c_int, [_vp, _vp, _f64p]),
     "ffq_state_expectation": (C.c_int, [_vp, _vp, _f64p, _f64p]),
     "ffq_state_device_ptr": (C.c_int, [_vp, C.POINTER(_vp)]),
@@ -300,6 +304,19 @@ class State:
         p = _vp()
         check(lib().ffq_state_device_ptr(self.h, C.byref(p)))
         return p.value
+
+
+def rotation_groups(t, x):
+    """Host-only: how ffq_state_apply_pauli_rotations cuts flip masks x for tile
+    bits t -> (run_of, group_of, cx, basis [G][3], piv [G][3])."""
+    x = np.ascontiguousarray(x, np.uint64)
+    n = len(x)
+    run_of = np.zeros(n, np.int32); group_of = np.zeros(n, np.int32); cx = np.zeros(n, np.int32)
+    basis = np.zeros(3 * max(n, 1), np.uint32); piv = np.zeros(3 * max(n, 1), np.int32)
+    ng = C.c_int32(0)
+    check(lib().ffq_rotation_groups(t, n, x, run_of, group_of, cx, basis, piv, C.byref(ng)))
+    g = ng.value
+    return run_of, group_of, cx, basis[:3 * g].reshape(g, 3), piv[:3 * g].reshape(g, 3)
 
 
 def shard_schedule(n, n_global, off, x, z, c):

@@ -1315,6 +1315,37 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
   });
 }
 
+int ffq_rotation_groups(int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
+                        uint32_t* basis, int32_t* piv, int32_t* n_groups) {
+  if (n_rot < 0 || t < 0 || t > 31 || (n_rot > 0 && (!x || !run_of || !group_of || !cx || !basis || !piv)) || !n_groups)
+    return fail(nullptr, FFQ_EINVAL, "ffq_rotation_groups: invalid argument");
+  std::vector<RotDesc> rd(n_rot);
+  std::vector<char> ok(n_rot);
+  for (int r = 0; r < n_rot; ++r) {
+    rd[r] = RotDesc{x[r], 0, 0, 0};
+    ok[r] = t >= 3 && (x[r] >> t) == 0;
+  }
+  const RotRuns R = build_rot_runs(rd, ok, t);
+  for (int r = 0; r < n_rot; ++r) run_of[r] = group_of[r] = -1;
+  for (int r = 0; r < n_rot; ++r) {
+    const int ri = R.run_at[r];
+    if (ri < 0) continue;
+    for (int g = R.g0[ri]; g < R.g0[ri] + R.ng[ri]; ++g)
+      for (int q = R.groups[g].r0; q < R.groups[g].r1; ++q) {
+        run_of[r + q] = ri;
+        group_of[r + q] = g;
+      }
+  }
+  for (int r = 0; r < n_rot; ++r) cx[r] = group_of[r] >= 0 ? rd[r].cx : 0;
+  for (size_t g = 0; g < R.groups.size(); ++g)
+    for (int i = 0; i < 3; ++i) {
+      basis[3 * g + i] = R.groups[g].b[i];
+      piv[3 * g + i] = R.groups[g].piv[i];
+    }
+  *n_groups = (int32_t)R.groups.size();
+  return FFQ_OK;
+}
+
 int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta) {
   if (!st || !plan || (!theta && plan->cp.n_gen > 0)) return fail(st ? st->ctx : nullptr, FFQ_EINVAL, "null argument");
   ffq_ctx_t ctx = st->ctx;

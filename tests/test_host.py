@@ -211,3 +211,58 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
         assert r["block_pairs"] >= 0.8 * r["exp_pairs"] and r["units"] > 0
     else:  # small closures keep the natural layout (256-thread program)
         assert r["product"] == 0 and r["block_pairs"] == 0
+
+
+@pytest.mark.parametrize("t,seed", [(12, 0), (12, 1), (5, 2), (3, 3), (2, 4)])
+def test_rotation_groups_cover_and_partition(t, seed):
+    """Host logic of the fused rotation runs (build_rot_runs behind
+    ffq_state_apply_pauli_rotations): runs are the maximal >= 2 sequences of
+    flip masks below 2^t; each group's masks lie in the span of a reduced-echelon
+    basis of 3 vectors (cx = coordinates), pivots ascending below t, and the
+    cosets k ^ span{b} (pivot bits of k clear) partition the tile."""
+    rng = np.random.default_rng(seed)
+    n = 16
+    x = np.where(rng.random(60) < 0.75, rng.integers(0, 1 << min(t, n), size=60),
+                 rng.integers(1, 1 << n, size=60)).astype(np.uint64)
+    x[10:14] = 0  # diagonal rotations join any group
+    run_of, group_of, cx, basis, piv = capi.rotation_groups(t, x)
+    ok = (x >> np.uint64(t)) == 0 if t >= 3 else np.zeros(len(x), bool)
+    # runs: maximal stretches of ok of length >= 2
+    want = np.full(len(x), -1)
+    r, nrun = 0, 0
+    while r < len(x):
+        if not ok[r]:
+            r += 1
+            continue
+        e = r
+        while e < len(x) and ok[e]:
+            e += 1
+        if e - r >= 2:
+            want[r:e] = nrun
+            nrun += 1
+        r = e
+    assert np.array_equal(run_of, want)
+    assert np.all((group_of >= 0) == (run_of >= 0))
+    assert np.all(np.diff(group_of[group_of >= 0]) >= 0)  # groups are consecutive
+    for g in range(len(basis)):
+        b, p = [int(v) for v in basis[g]], [int(v) for v in piv[g]]
+        assert p == sorted(p) and len(set(p)) == 3 and max(p) < t
+        for i in range(3):
+            assert (b[i] >> p[i]) & 1
+            assert all(not ((b[j] >> p[i]) & 1) for j in range(3) if j != i)
+        for r in np.nonzero(group_of == g)[0]:
+            span = 0
+            for i in range(3):
+                if (cx[r] >> i) & 1:
+                    span ^= b[i]
+            assert span == int(x[r])
+        if t <= 6:
+            seen = np.zeros(1 << t, int)
+            pm = sum(1 << q for q in p)
+            for k in range(1 << t):
+                if k & pm:
+                    continue
+                for c in range(8):
+                    off = (b[0] if c & 1 else 0) ^ (b[1] if c & 2 else 0) ^ (b[2] if c & 4 else 0)
+                    seen[k ^ off] += 1
+            assert np.all(seen == 1)
