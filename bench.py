@@ -288,6 +288,28 @@ def main():
             b.record(stream)
             b.synchronize()
             rot_ms.append(a.elapsed_time(b))
+    # the same pass at 18 qubits (north_star's size): 256 rows of 4 MiB = 1 GiB (> L2)
+    st18 = capi.State(ctx, 18, 256)
+    st18.set_basis(0)
+    for _ in range(3):
+        st18.rotate(x, z, 0.1)
+    ctx.synchronize()
+    r18 = []
+    with torch.cuda.stream(stream):
+        for k in range(10):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st18.rotate(x, z, 0.1 * (k % 2 * 2 - 1))
+            b.record(stream)
+            b.synchronize()
+            r18.append(a.elapsed_time(b))
+    del st18
+    r18_avg = statistics.mean(r18[2:])
+    rot18 = {"kernel": "k_pauli_rotation", "state_qubits": 18, "rows": 256, "ms_per_pass": r18_avg,
+             "achieved_gbs": 256 * 32 * (1 << 18) / (r18_avg / 1e3) / 1e9,
+             "frac": 256 * 32 * (1 << 18) / (r18_avg / 1e3) / 1e9 / peak,
+             "note": "one rotation pass over 256 batched 18-qubit states (1 GiB, > L2), incl. the API call's cos/sin upload and sync"}
     # fused run: 16 rotations with flip masks in the low 12 qubits (z anywhere),
     # one TMA-staged tile pass (k_rotation_run), then its inverse
     rr = np.random.default_rng(11)
@@ -485,7 +507,8 @@ def main():
             "secondary": {"config3_latency_and_b64": latency, "config3_complex128_program": complex_path,
                           "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
-                          "config4_fmo": config4, "config5_32q": config5, "rotation_run_28q": rotation_run},
+                          "config4_fmo": config4, "config5_32q": config5, "rotation_run_28q": rotation_run,
+                          "rotation_pass_18q_b256": rot18},
             "clocks": clk.summary(),
         }
         # the sector kernel moves no HBM data in the step (theta in, E out, pair
