@@ -143,16 +143,19 @@ int ffq_state_download(ffq_state_t st, double* psi);       /* [batch][2^n][2] */
 int ffq_state_apply_pauli_rotation(ffq_state_t st, uint64_t x, uint64_t z, double theta);
 /* The sequence e^{i theta[n_rot-1] P_{n_rot-1}} ... e^{i theta[0] P_0}, in order
  * (apply_pauli_rotation over a Trotter string list).
- * Runs of consecutive rotations whose flip masks lie in the low 12 qubits go
- * through one shared-memory tile pass each (TMA-staged; FFQ_ROT_TILE). */
+ * Runs of consecutive rotations whose flip masks, with the low 5 qubits, lie in
+ * 12 qubits go through one shared-memory tile pass each (TMA-staged when those
+ * are the low 12; FFQ_ROT_TILE). */
 int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x, const uint64_t* z,
                                     const double* theta);
 /* Host only (no device work): how ffq_state_apply_pauli_rotations cuts a list
- * of flip masks for tile bits t. run_of/group_of/cx [n_rot]: run and group of
- * each rotation (-1 when it is a single pass) and x's coordinates in its
- * group's basis; basis/piv [n_rot * 3] (first 3 * n_groups used). */
-int ffq_rotation_groups(int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
-                        uint32_t* basis, int32_t* piv, int32_t* n_groups);
+ * of flip masks on n qubits for tile bits t (min(n, t) used). run_of/group_of/
+ * cx [n_rot]: run and group of each rotation (-1 when it is a single pass) and
+ * its flip mask's coordinates in its group's basis (tile coordinates = pext by
+ * the run's qubit set run_q [n_rot]); basis/piv [n_rot * 3] (first 3 * n_groups
+ * used). */
+int ffq_rotation_groups(int n, int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
+                        uint64_t* run_q, uint32_t* basis, int32_t* piv, int32_t* n_groups);
 /* Apply the plan with theta [batch][n_gen] (host pointer). */
 int ffq_state_apply_plan(ffq_state_t st, ffq_plan_t plan, const double* theta);
 /* re_out/im_out [batch] (host) */

@@ -46,7 +46,7 @@ _SIGS = {
     "ffq_state_download": (C.c_int, [_vp, _f64p]),
     "ffq_state_apply_pauli_rotation": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_double]),
     "ffq_state_apply_pauli_rotations": (C.c_int, [_vp, C.c_int, _u64p, _u64p, _f64p]),
-    "ffq_rotation_groups": (C.c_int, [C.c_int, C.c_int, _u64p, _i32p, _i32p, _i32p,
+    "ffq_rotation_groups": (C.c_int, [C.c_int, C.c_int, C.c_int, _u64p, _i32p, _i32p, _i32p, _u64p,
                                       np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS"), _i32p,
                                       C.POINTER(C.c_int32)]),
     "ffq_state_apply_plan": (C.c_int, [_vp, _vp, _f64p]),
@@ -306,17 +306,18 @@ class State:
         return p.value
 
 
-def rotation_groups(t, x):
-    """Host-only: how ffq_state_apply_pauli_rotations cuts flip masks x for tile
-    bits t -> (run_of, group_of, cx, basis [G][3], piv [G][3])."""
+def rotation_groups(n, t, x):
+    """Host-only: how ffq_state_apply_pauli_rotations cuts flip masks x on n
+    qubits for tile bits t -> (run_of, group_of, cx, run_q, basis [G][3], piv [G][3])."""
     x = np.ascontiguousarray(x, np.uint64)
-    n = len(x)
-    run_of = np.zeros(n, np.int32); group_of = np.zeros(n, np.int32); cx = np.zeros(n, np.int32)
-    basis = np.zeros(3 * max(n, 1), np.uint32); piv = np.zeros(3 * max(n, 1), np.int32)
+    m = len(x)
+    run_of = np.zeros(m, np.int32); group_of = np.zeros(m, np.int32); cx = np.zeros(m, np.int32)
+    run_q = np.zeros(m, np.uint64)
+    basis = np.zeros(3 * max(m, 1), np.uint32); piv = np.zeros(3 * max(m, 1), np.int32)
     ng = C.c_int32(0)
-    check(lib().ffq_rotation_groups(t, n, x, run_of, group_of, cx, basis, piv, C.byref(ng)))
+    check(lib().ffq_rotation_groups(n, t, m, x, run_of, group_of, cx, run_q, basis, piv, C.byref(ng)))
     g = ng.value
-    return run_of, group_of, cx, basis[:3 * g].reshape(g, 3), piv[:3 * g].reshape(g, 3)
+    return run_of, group_of, cx, run_q, basis[:3 * g].reshape(g, 3), piv[:3 * g].reshape(g, 3)
 
 
 def shard_schedule(n, n_global, off, x, z, c):

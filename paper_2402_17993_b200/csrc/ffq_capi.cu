@@ -78,33 +78,55 @@ struct DevBuf {
   }
 };
 
-// Runs of >= 2 consecutive eligible rotations (flip mask below 2^t), each cut
-// into groups of consecutive rotations whose flip masks span <= 3 dimensions
-// (k_rotation_run). Fills RotDesc::cx; group ranges are relative to the run.
+// Runs of >= 2 consecutive eligible rotations whose flip masks, together with
+// the low 5 qubits, lie in a set Q of t qubits (the run's tile: Q = the union
+// filled up with the lowest free qubits; Q = the low t qubits is the TMA case),
+// each cut into groups of consecutive rotations whose flip masks span <= 3
+// dimensions (k_rotation_run). rd gets the masks in tile coordinates (pext by
+// Q) and the group coordinates; group ranges are relative to the run.
 struct RotRuns {
   std::vector<int> run_at;  // per rotation: index of the run starting there, else -1
   std::vector<int> len, g0, ng;
+  std::vector<uint64_t> q;  // per run: its qubit set
   std::vector<RotGroup> groups;
 };
 
-RotRuns build_rot_runs(std::vector<RotDesc>& rd, const std::vector<char>& ok, int t) {
+inline uint64_t pext64(uint64_t v, uint64_t mask) {
+  uint64_t r = 0;
+  for (int o = 0; mask; mask &= mask - 1, ++o)
+    if (v & mask & (~mask + 1)) r |= 1ULL << o;
+  return r;
+}
+
+// x, z: original strings; rd[r].ny must be set by the caller
+RotRuns build_rot_runs(std::vector<RotDesc>& rd, const uint64_t* x, const uint64_t* z,
+                       const std::vector<char>& ok, int n, int t) {
   RotRuns R;
   const int N = (int)rd.size();
   R.run_at.assign(N, -1);
-  if (t < 3) return R;
+  if (t < 3 || t > 12 || n < t) return R;
+  const uint64_t low = (1ULL << std::min(5, t)) - 1ULL;
   for (int i = 0; i < N;) {
-    if (!ok[i]) { ++i; continue; }
+    uint64_t U = low;
     int e = i;
-    while (e < N && ok[e]) ++e;
-    if (e - i < 2) { i = e; continue; }
+    while (e < N && ok[e] && __builtin_popcountll(U | x[e]) <= t) U |= x[e++];
+    if (e - i < 2) { i = std::max(i + 1, e); continue; }
+    uint64_t Q = U;
+    for (int bit = 0; __builtin_popcountll(Q) < t; ++bit) Q |= 1ULL << bit;
     R.run_at[i] = (int)R.len.size();
     R.len.push_back(e - i);
+    R.q.push_back(Q);
     R.g0.push_back((int)R.groups.size());
+    for (int r = i; r < e; ++r) {
+      rd[r].x = pext64(x[r], Q);
+      rd[r].z = pext64(z[r], Q);
+      rd[r].zo = z[r] & ~Q;
+    }
     for (int r = i; r < e;) {
       uint32_t b[3];
-      int piv[3], d = 0, q = r;
-      for (; q < e; ++q) {
-        uint32_t v = (uint32_t)rd[q].x;
+      int piv[3], d = 0, qq = r;
+      for (; qq < e; ++qq) {
+        uint32_t v = (uint32_t)rd[qq].x;
         for (int j = 0; j < d; ++j)
           if ((v >> piv[j]) & 1u) v ^= b[j];
         if (!v) continue;  // in the span: joins the group
@@ -132,15 +154,15 @@ RotRuns build_rot_runs(std::vector<RotDesc>& rd, const std::vector<char>& ok, in
         G.piv[j] = piv[ord[j]];
       }
       G.r0 = r - i;
-      G.r1 = q - i;
-      for (int j = r; j < q; ++j) {
+      G.r1 = qq - i;
+      for (int j = r; j < qq; ++j) {
         int cx = 0;
         for (int k = 0; k < 3; ++k)
           if ((rd[j].x >> G.piv[k]) & 1u) cx |= 1 << k;
         rd[j].cx = cx;
       }
       R.groups.push_back(G);
-      r = q;
+      r = qq;
     }
     R.ng.push_back((int)R.groups.size() - R.g0.back());
     i = e;
@@ -365,11 +387,12 @@ void launch_string(ffq_ctx_t ctx, double2* psi, int n, int batch, uint64_t x, ui
 // (the 64 KiB dynamic-smem and carveout attributes are set at context creation,
 // so the launch can sit inside a captured graph)
 constexpr int kRotRunThreads = 256;  // 3 CTAs (64 KiB tiles) per SM
-void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, const RotGroup* g, int n_grp,
-                         const RotDesc* rd, const double2* cs, int cs_stride) {
+void launch_rotation_run(ffq_ctx_t ctx, double2* psi, int n, int batch, int t, uint64_t q, const RotGroup* g,
+                         int n_grp, const RotDesc* rd, const double2* cs, int cs_stride) {
   const size_t sb = sizeof(double2) << t;
   dim3 grid((unsigned)(1u << (n - t)), batch);
-  k_rotation_run<kRotRunThreads><<<grid, kRotRunThreads, sb, ctx->stream>>>(psi, n, t, g, n_grp, rd, cs, cs_stride);
+  k_rotation_run<kRotRunThreads><<<grid, kRotRunThreads, sb, ctx->stream>>>(psi, n, t, q, g, n_grp, rd, cs,
+                                                                           cs_stride);
   CK(cudaGetLastError());
   ctx->launches++;
 }
@@ -419,8 +442,8 @@ void run_plan_ops(ffq_ctx_t ctx, const ffq_plan_s* pl, double2* psi, uint32_t* s
       // a run of >= 2 string ops with flip masks below 2^t: one tiled pass
       const int ri = pl->runs.run_at[op];
       if (ri >= 0) {
-        launch_rotation_run(ctx, psi, n, batch, pl->runs_t, pl->rot_groups.p + pl->runs.g0[ri], pl->runs.ng[ri],
-                            pl->rot.p + op, cs + op, n_ops);
+        launch_rotation_run(ctx, psi, n, batch, pl->runs_t, pl->runs.q[ri], pl->rot_groups.p + pl->runs.g0[ri],
+                            pl->runs.ng[ri], pl->rot.p + op, cs + op, n_ops);
         op += pl->runs.len[ri] - 1;
       } else {
         const int si = cp.op_idx[op];
@@ -1056,18 +1079,20 @@ int ffq_plan_upload(ffq_ctx_t ctx, int n_qubits, int n_gen, const int64_t* term_
     std::vector<double2> pf(cp.pair_f.size() / 2);
     for (size_t i = 0; i < pf.size(); ++i) pf[i] = make_double2(cp.pair_f[2 * i], cp.pair_f[2 * i + 1]);
     p->pair_f.upload(pf, ctx->stream);
-    std::vector<RotDesc> rd(cp.op_kind.size(), RotDesc{0, 0, 0, 0});
-    for (size_t op = 0; op < cp.op_kind.size(); ++op)
+    const size_t nop = cp.op_kind.size();
+    std::vector<RotDesc> rd(nop, RotDesc{0, 0, 0, 0, 0});
+    std::vector<uint64_t> ox(nop, 0), oz(nop, 0);
+    std::vector<char> ok(nop, 0);
+    for (size_t op = 0; op < nop; ++op)
       if (cp.op_kind[op] != 0) {
         const int si = cp.op_idx[op];
-        const uint64_t x = cp.str_x[si];
-        rd[op] = RotDesc{x, cp.str_z[si], cp.str_ny[si], 0};
+        ox[op] = cp.str_x[si];
+        oz[op] = cp.str_z[si];
+        rd[op].ny = cp.str_ny[si];
+        ok[op] = 1;
       }
     p->runs_t = ctx->rot_tile_bits > 0 ? std::min(n_qubits, ctx->rot_tile_bits) : 0;
-    std::vector<char> ok(rd.size(), 0);
-    for (size_t op = 0; op < rd.size(); ++op)
-      ok[op] = cp.op_kind[op] != 0 && p->runs_t >= 3 && (rd[op].x >> p->runs_t) == 0;
-    p->runs = build_rot_runs(rd, ok, p->runs_t);
+    p->runs = build_rot_runs(rd, ox.data(), oz.data(), ok, n_qubits, p->runs_t);
     p->rot_groups.upload(p->runs.groups, ctx->stream);
     p->rot.upload(rd, ctx->stream);
     p->str_x.upload(cp.str_x, ctx->stream);
@@ -1290,19 +1315,19 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
     std::vector<double2> cs(n_rot);
     std::vector<char> ok(n_rot);
     for (int r = 0; r < n_rot; ++r) {
-      rd[r] = RotDesc{x[r], z[r], __builtin_popcountll(x[r] & z[r]) & 3, 0};
+      rd[r] = RotDesc{0, 0, 0, __builtin_popcountll(x[r] & z[r]) & 3, 0};
       cs[r] = make_double2(std::cos(theta[r]), std::sin(theta[r]));
-      ok[r] = t >= 3 && (x[r] >> t) == 0;
+      ok[r] = 1;
     }
-    const RotRuns runs = build_rot_runs(rd, ok, t);
+    const RotRuns runs = build_rot_runs(rd, x, z, ok, st->n, t);
     ctx->rot.upload(rd, ctx->stream);
     ctx->rot_groups.upload(runs.groups, ctx->stream);
     ctx->cs.upload(cs, ctx->stream);
     for (int r = 0; r < n_rot;) {
       const int ri = runs.run_at[r];
       if (ri >= 0) {
-        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, ctx->rot_groups.p + runs.g0[ri], runs.ng[ri],
-                            ctx->rot.p + r, ctx->cs.p + r, 0);
+        launch_rotation_run(ctx, st->psi.p, st->n, st->batch, t, runs.q[ri], ctx->rot_groups.p + runs.g0[ri],
+                            runs.ng[ri], ctx->rot.p + r, ctx->cs.p + r, 0);
         r += runs.len[ri];
       } else {
         launch_string(ctx, st->psi.p, st->n, st->batch, x[r], z[r], rd[r].ny, ctx->cs.p, 0, r);
@@ -1315,18 +1340,22 @@ int ffq_state_apply_pauli_rotations(ffq_state_t st, int n_rot, const uint64_t* x
   });
 }
 
-int ffq_rotation_groups(int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
-                        uint32_t* basis, int32_t* piv, int32_t* n_groups) {
-  if (n_rot < 0 || t < 0 || t > 31 || (n_rot > 0 && (!x || !run_of || !group_of || !cx || !basis || !piv)) || !n_groups)
+int ffq_rotation_groups(int n, int t, int n_rot, const uint64_t* x, int32_t* run_of, int32_t* group_of, int32_t* cx,
+                        uint64_t* run_q, uint32_t* basis, int32_t* piv, int32_t* n_groups) {
+  if (n_rot < 0 || n < 1 || n > 63 || t < 0 || t > 31 ||
+      (n_rot > 0 && (!x || !run_of || !group_of || !cx || !run_q || !basis || !piv)) || !n_groups)
     return fail(nullptr, FFQ_EINVAL, "ffq_rotation_groups: invalid argument");
-  std::vector<RotDesc> rd(n_rot);
-  std::vector<char> ok(n_rot);
+  std::vector<RotDesc> rd(n_rot, RotDesc{0, 0, 0, 0, 0});
+  std::vector<char> ok(n_rot, 1);
+  std::vector<uint64_t> z(n_rot, 0);
+  const RotRuns R = build_rot_runs(rd, x, z.data(), ok, n, std::min(n, t));
   for (int r = 0; r < n_rot; ++r) {
-    rd[r] = RotDesc{x[r], 0, 0, 0};
-    ok[r] = t >= 3 && (x[r] >> t) == 0;
+    run_of[r] = group_of[r] = -1;
+    run_q[r] = 0;
   }
-  const RotRuns R = build_rot_runs(rd, ok, t);
-  for (int r = 0; r < n_rot; ++r) run_of[r] = group_of[r] = -1;
+  for (int r = 0; r < n_rot; ++r)
+    if (R.run_at[r] >= 0)
+      for (int q = 0; q < R.len[R.run_at[r]]; ++q) run_q[r + q] = R.q[R.run_at[r]];
   for (int r = 0; r < n_rot; ++r) {
     const int ri = R.run_at[r];
     if (ri < 0) continue;

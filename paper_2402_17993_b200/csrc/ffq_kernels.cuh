@@ -455,8 +455,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // z is unrestricted: the tile's high-bit parity is folded into sin once per
 // rotation. Per pair the arithmetic is k_pauli_rotation's.
 struct RotDesc {
-  uint64_t x, z;  // x < 2^t
-  int ny;         // popc(x & z) & 3
+  uint64_t x, z;  // in tile coordinates (pext by the run's qubit set Q): x, z < 2^t
+  uint64_t zo;    // z & ~Q (full index bits): the tile's part of the parity
+  int ny;         // popc(x & z) & 3 of the original string
   int cx;         // x in its group's basis: bit i set <=> b_i in x (x = 0: diagonal)
 };
 struct RotGroup {
@@ -500,27 +501,66 @@ __device__ __forceinline__ void coset_rot(int cx, double2 (&v)[8], double c, con
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ psi, int n, int t,
+__global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ psi, int n, int t, uint64_t q,
                                                      const RotGroup* __restrict__ grp, int n_grp,
                                                      const RotDesc* __restrict__ rd,
                                                      const double2* __restrict__ cs, int cs_stride) {
-  // rotation r of row b: (cos phi, sin phi) = cs[b * cs_stride + r]
+  // rotation r of row b: (cos phi, sin phi) = cs[b * cs_stride + r].
+  // The tile is the 2^t amplitudes whose bits outside the qubit set q are
+  // those of blockIdx.x; tile coordinate m <-> index base | pdep(m, q).
+  // q = the low t bits: one contiguous block, staged by bulk copies. Otherwise
+  // q holds the low 5 bits, so 32 consecutive m are 512 contiguous bytes
+  // (coalesced 32-byte vector gathers through a 2^(t-5)-entry offset table).
   extern __shared__ __align__(128) double2 tl[];
   __shared__ __align__(8) uint64_t bar;
-  const uint32_t tsize = 1u << t, tmask = tsize - 1u;
-  const uint64_t base = (uint64_t)blockIdx.x << t;
+  __shared__ uint64_t hi_off[128];
+  const uint32_t tsize = 1u << t;
+  const uint64_t nmask = (n >= 64) ? ~0ULL : ((1ULL << n) - 1ULL);
+  const bool low = q == (uint64_t)(tsize - 1u);
+  uint64_t base = 0;
+  {
+    uint64_t rest = ~q & nmask, bx = blockIdx.x;
+    while (rest) {
+      const uint64_t lsb = rest & (~rest + 1ULL);
+      if (bx & 1ULL) base |= lsb;
+      bx >>= 1;
+      rest ^= lsb;
+    }
+  }
   double2* s = psi + ((int64_t)blockIdx.y << n) + base;
   const double2* csb = cs + (int64_t)blockIdx.y * cs_stride;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    const uint32_t bytes = tsize * (uint32_t)sizeof(double2);
-    mbar_expect_tx(&bar, bytes);
-    const uint32_t piece = 32768;
-    for (uint32_t off = 0; off < bytes; off += piece)
-      bulk_g2s((char*)tl + off, (const char*)s + off, min(piece, bytes - off), &bar);
+  if (low) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      const uint32_t bytes = tsize * (uint32_t)sizeof(double2);
+      mbar_expect_tx(&bar, bytes);
+      const uint32_t piece = 32768;
+      for (uint32_t off = 0; off < bytes; off += piece)
+        bulk_g2s((char*)tl + off, (const char*)s + off, min(piece, bytes - off), &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  } else {
+    const uint64_t qh = q & ~31ULL;
+    for (uint32_t j = threadIdx.x; j < (tsize >> 5); j += NT) {
+      uint64_t o = 0, rest = qh, bj = j;
+      while (rest) {
+        const uint64_t lsb = rest & (~rest + 1ULL);
+        if (bj & 1ULL) o |= lsb;
+        bj >>= 1;
+        rest ^= lsb;
+      }
+      hi_off[j] = o;
+    }
+    __syncthreads();
+    for (uint32_t m = 2 * threadIdx.x; m < tsize; m += 2 * NT) {
+      double2 a, b;
+      ld256(s + (hi_off[m >> 5] | (m & 31u)), a, b);
+      tl[m] = a;
+      tl[m + 1] = b;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  mbar_wait(&bar, 0);
   for (int g = 0; g < n_grp; ++g) {
     const RotGroup G = grp[g];
     uint32_t off[8];
@@ -534,11 +574,10 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
 #pragma unroll
       for (int c = 0; c < 8; ++c) v[c] = tl[k ^ off[c]];
       for (int r = G.r0; r < G.r1; ++r) {
-        const uint64_t z = __ldg(&rd[r].z);
+        const uint32_t zl = (uint32_t)__ldg(&rd[r].z);
         const int cx = __ldg(&rd[r].cx);
         const double2 csv = __ldg(&csb[r]);
-        const double c = csv.x, sn = csv.y * sgn_par(base & z);
-        const uint32_t zl = (uint32_t)z & tmask;
+        const double c = csv.x, sn = csv.y * sgn_par(base & __ldg(&rd[r].zo));
         // parity of (k ^ off[e]) & z = parity(k & z) ^ parity(off[e] & z), the
         // second a XOR of the basis parities: one sign flip of sin per member
         const uint32_t p0 = (uint32_t)__popc(G.b[0] & zl) << 31, p1 = (uint32_t)__popc(G.b[1] & zl) << 31,
@@ -575,7 +614,10 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
     }
     __syncthreads();
   }
-  for (uint32_t k = 2 * threadIdx.x; k < tsize; k += 2 * NT) st256(s + k, tl[k], tl[k + 1]);
+  if (low)
+    for (uint32_t k = 2 * threadIdx.x; k < tsize; k += 2 * NT) st256(s + k, tl[k], tl[k + 1]);
+  else
+    for (uint32_t m = 2 * threadIdx.x; m < tsize; m += 2 * NT) st256(s + (hi_off[m >> 5] | (m & 31u)), tl[m], tl[m + 1]);
 }
 
 // ---- tiled expectation ---------------------------------------------------------

@@ -213,53 +213,74 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
         assert r["product"] == 0 and r["block_pairs"] == 0
 
 
-@pytest.mark.parametrize("t,seed", [(12, 0), (12, 1), (5, 2), (3, 3), (2, 4)])
-def test_rotation_groups_cover_and_partition(t, seed):
+@pytest.mark.parametrize("n,t,seed", [(16, 12, 0), (16, 12, 1), (20, 12, 5), (16, 5, 2), (16, 3, 3), (16, 2, 4),
+                                      (8, 12, 6)])
+def test_rotation_groups_cover_and_partition(n, t, seed):
     """Host logic of the fused rotation runs (build_rot_runs behind
-    ffq_state_apply_pauli_rotations): runs are the maximal >= 2 sequences of
-    flip masks below 2^t; each group's masks lie in the span of a reduced-echelon
+    ffq_state_apply_pauli_rotations): a run is a greedy stretch of >= 2
+    rotations whose flip masks, with the low 5 qubits, fit in min(n, t) qubits
+    (run_q = that union filled with the lowest free qubits); each group's masks
+    (in tile coordinates, pext by run_q) lie in the span of a reduced-echelon
     basis of 3 vectors (cx = coordinates), pivots ascending below t, and the
     cosets k ^ span{b} (pivot bits of k clear) partition the tile."""
     rng = np.random.default_rng(seed)
-    n = 16
-    x = np.where(rng.random(60) < 0.75, rng.integers(0, 1 << min(t, n), size=60),
+    tt = min(n, t)
+    x = np.where(rng.random(60) < 0.6, rng.integers(0, 1 << min(tt, n), size=60),
                  rng.integers(1, 1 << n, size=60)).astype(np.uint64)
     x[10:14] = 0  # diagonal rotations join any group
-    run_of, group_of, cx, basis, piv = capi.rotation_groups(t, x)
-    ok = (x >> np.uint64(t)) == 0 if t >= 3 else np.zeros(len(x), bool)
-    # runs: maximal stretches of ok of length >= 2
+    x[20:26] = [1 << (n - 1), 1 << (n - 2), (1 << (n - 1)) | 1, 3 << (n - 3), 1 << (n - 1), 2]  # high qubits
+    run_of, group_of, cx, run_q, basis, piv = capi.rotation_groups(n, t, x)
+    low = (1 << min(5, tt)) - 1
     want = np.full(len(x), -1)
-    r, nrun = 0, 0
-    while r < len(x):
-        if not ok[r]:
-            r += 1
-            continue
-        e = r
-        while e < len(x) and ok[e]:
+    want_q = np.zeros(len(x), np.uint64)
+    i, nrun = 0, 0
+    while i < len(x) and tt >= 3:
+        U, e = low, i
+        while e < len(x) and bin(U | int(x[e])).count("1") <= tt:
+            U |= int(x[e])
             e += 1
-        if e - r >= 2:
-            want[r:e] = nrun
-            nrun += 1
-        r = e
+        if e - i < 2:
+            i = max(i + 1, e)
+            continue
+        q, bit = U, 0
+        while bin(q).count("1") < tt:
+            q |= 1 << bit
+            bit += 1
+        want[i:e] = nrun
+        want_q[i:e] = q
+        nrun += 1
+        i = e
     assert np.array_equal(run_of, want)
+    assert np.array_equal(run_q, want_q)
     assert np.all((group_of >= 0) == (run_of >= 0))
     assert np.all(np.diff(group_of[group_of >= 0]) >= 0)  # groups are consecutive
+
+    def pext(v, m):
+        r, o = 0, 0
+        while m:
+            lsb = m & -m
+            if v & lsb:
+                r |= 1 << o
+            m ^= lsb
+            o += 1
+        return r
+
     for g in range(len(basis)):
         b, p = [int(v) for v in basis[g]], [int(v) for v in piv[g]]
-        assert p == sorted(p) and len(set(p)) == 3 and max(p) < t
-        for i in range(3):
-            assert (b[i] >> p[i]) & 1
-            assert all(not ((b[j] >> p[i]) & 1) for j in range(3) if j != i)
+        assert p == sorted(p) and len(set(p)) == 3 and max(p) < tt
+        for k in range(3):
+            assert (b[k] >> p[k]) & 1
+            assert all(not ((b[j] >> p[k]) & 1) for j in range(3) if j != k)
         for r in np.nonzero(group_of == g)[0]:
             span = 0
-            for i in range(3):
-                if (cx[r] >> i) & 1:
-                    span ^= b[i]
-            assert span == int(x[r])
-        if t <= 6:
-            seen = np.zeros(1 << t, int)
-            pm = sum(1 << q for q in p)
-            for k in range(1 << t):
+            for k in range(3):
+                if (cx[r] >> k) & 1:
+                    span ^= b[k]
+            assert span == pext(int(x[r]), int(run_q[r]))
+        if tt <= 6:
+            seen = np.zeros(1 << tt, int)
+            pm = sum(1 << v for v in p)
+            for k in range(1 << tt):
                 if k & pm:
                     continue
                 for c in range(8):

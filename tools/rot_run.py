@@ -17,6 +17,8 @@ st = capi.State(ctx, n, 1)
 st.set_basis(0)
 rr = np.random.default_rng(11)
 x = rr.integers(1, 1 << 12, size=R, dtype=np.uint64)
+if os.environ.get("ROT_HIGH"):  # flip masks on qubits 0-4 and n-7..n-1: gather tiles (not the low 12)
+    x = np.array([(int(v) & 31) | ((int(v) >> 5) << (n - 7)) for v in x], np.uint64)
 z = rr.integers(0, 1 << n, size=R, dtype=np.uint64)
 th = rr.uniform(-1, 1, size=R)
 reps = int(os.environ.get("ROT_REPS", "6"))
@@ -33,5 +35,5 @@ for r in range(R):
     st.rotate(int(x[r]), int(z[r]), float(th[r]))
 ctx.synchronize()
 du = time.perf_counter() - t
-print(f"n={n} R={R}: fused {dt*1e3:.3f} ms/run ({32*(1<<n)/dt/1e9:.0f} GB/s), unfused {du*1e3:.3f} ms "
+print(f"n={n} R={R}{' high-qubit masks' if os.environ.get('ROT_HIGH') else ''}: fused {dt*1e3:.3f} ms/run ({32*(1<<n)/dt/1e9:.0f} GB/s), unfused {du*1e3:.3f} ms "
       f"({du/dt:.2f}x)")
