@@ -517,15 +517,21 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
   const uint32_t tsize = 1u << t;
   const uint64_t nmask = (n >= 64) ? ~0ULL : ((1ULL << n) - 1ULL);
   const bool low = q == (uint64_t)(tsize - 1u);
-  uint64_t base = 0;
-  {
-    uint64_t rest = ~q & nmask, bx = blockIdx.x;
-    while (rest) {
-      const uint64_t lsb = rest & (~rest + 1ULL);
-      if (bx & 1ULL) base |= lsb;
-      bx >>= 1;
-      rest ^= lsb;
+  __shared__ uint64_t base_sh;
+  uint64_t base = (uint64_t)blockIdx.x << t;
+  if (!low) {  // pdep(blockIdx.x, ~q): one thread, broadcast
+    if (threadIdx.x == 0) {
+      uint64_t rest = ~q & nmask, bx = blockIdx.x, bs = 0;
+      while (rest) {
+        const uint64_t lsb = rest & (~rest + 1ULL);
+        if (bx & 1ULL) bs |= lsb;
+        bx >>= 1;
+        rest ^= lsb;
+      }
+      base_sh = bs;
     }
+    __syncthreads();
+    base = base_sh;
   }
   double2* s = psi + ((int64_t)blockIdx.y << n) + base;
   const double2* csb = cs + (int64_t)blockIdx.y * cs_stride;
