@@ -59,22 +59,27 @@ def test_rotation_runs_vs_oracle(ctx, oracle, n):
     assert np.abs(st.download() - ref).max() <= A_TOL
 
 
-def test_fused_runs_equal_unfused_and_launch_count(monkeypatch):
+@pytest.mark.parametrize("high", [False, True])
+def test_fused_runs_equal_unfused_and_launch_count(monkeypatch, high):
+    """One run of 32 rotations: flip masks in the low 12 qubits (TMA tile) or on
+    qubits 0-4 and 13-19 (gathered tile), batch of 3 rows."""
     n = 20
-    rng = np.random.default_rng(7)
-    psi = random_state(rng, n, 1)
-    x = rng.integers(1, 1 << 12, size=32, dtype=np.uint64)  # one run of 32 low-qubit rotations
+    rng = np.random.default_rng(7 + high)
+    psi = random_state(rng, n, 3)
+    x = rng.integers(1, 1 << 12, size=32, dtype=np.uint64)
+    if high:
+        x = np.array([(int(v) & 31) | ((int(v) >> 5) << (n - 7)) for v in x], np.uint64)
     z = rng.integers(0, 1 << n, size=32, dtype=np.uint64)
     th = rng.uniform(-1, 1, size=32)
     out = {}
     for tile in ("12", "0"):
         monkeypatch.setenv("FFQ_ROT_TILE", tile)
         c = capi.Context(0)
-        st = capi.State(c, n, 1)
+        st = capi.State(c, n, 3)
         st.upload(psi)
         l0 = c.launches()
         st.rotate_many(x, z, th)
-        out[tile] = (st.download()[0], c.launches() - l0)
+        out[tile] = (st.download(), c.launches() - l0)
         del st  # the state before its context
         c.close()
     assert out["12"][1] == 1 and out["0"][1] == 32
