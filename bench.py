@@ -102,19 +102,31 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
 
 
+def bench_config(world):
+    """The `config` dict of both arms (identical, so the driver compares like with like)."""
+    return {"workload": "config3: 18 qubits, 10 electrons, 560 UCCSD generators, 9316-term JW "
+                        "Hamiltonian; one step = parameter-shift gradient set (1121 energy "
+                        "evaluations) per GPU",
+            "evals_per_step_per_gpu": 1121, "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"replicas x{world} (independent gradient sets)"}
+
+
+def oracle_workload():
+    """Config 3 and its parameter-shift set built by the CPU oracle alone
+    (oracle/workload.py): no product import on the reference arm."""
+    from oracle import workload as ow
+
+    P = ow.config_problem(3)
+    return P, ow.parameter_shift_set(P.thetas[0])
+
+
 def cpu_oracle_rate(P, rows, n_evals, threads=None):
     from oracle import ffo
 
     if threads:
         ffo.set_threads(threads)
-    x, z, c = P.ham_arrays()
-    H = ffo.PauliSum.from_terms(P.n_qubits, x, z, c)
-    kind, idx = ffo.build_generators(P.n_qubits, P.n_elec)
-    order = np.array(P.plan.order, np.int32)
     t = time.perf_counter()
-    es = []
-    for r in range(n_evals):
-        es.append(ffo.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, rows[r], H)[0])
+    es = [P.energy(rows[r]) for r in range(n_evals)]
     dt = time.perf_counter() - t
     return n_evals / dt, es, ffo.get_threads()
 
@@ -122,7 +134,7 @@ def cpu_oracle_rate(P, rows, n_evals, threads=None):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    P, rows = workload(0)
+    P, rows = oracle_workload()
     cores = os.cpu_count() or 1
     evals_per_step = 1
     for _ in range(args.warmup):
@@ -136,11 +148,13 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic (seeded, BASELINE.json config 3)",
-        "config": {"workload": "config3 18q/10e/560 generators; CPU oracle (SPEC restatement, C+OpenMP), "
-                               f"{evals_per_step} energy evaluation of the parameter-shift set per step"},
+        "data": "synthetic (seeded h~N(0,1), g~N(0,0.1), theta~U(-0.1,0.1); BASELINE.json config 3)",
+        "config": bench_config(args.gpus),
+        "path": "CPU oracle (oracle/ffo_oracle.c: SPEC.md restatement, C+OpenMP), dense 2^18 complex128 "
+                "state, per-string rotations and term-by-term expectation; inputs from oracle/workload.py",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} x {evals_per_step} evaluation(s) of config 3"},
+                         "sample": f"{args.steps} x {evals_per_step} evaluation(s) of the config-3 "
+                                   "parameter-shift set (rows 0..steps-1)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -468,9 +482,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = 2
-        rate, es, cores = cpu_oracle_rate(P, rows, n_cpu, os.cpu_count())
+        OP, orows = oracle_workload()
+        assert np.array_equal(orows, rows), "oracle and product parameter-shift sets differ"
+        rate, es, cores = cpu_oracle_rate(OP, orows, n_cpu, os.cpu_count())
         parity = max(abs(es[i] - e_first[i]) for i in range(n_cpu))
-        rate1, es1, _ = cpu_oracle_rate(P, rows, 1, 1)  # single-threaded too
+        rate1, es1, _ = cpu_oracle_rate(OP, orows, 1, 1)  # single-threaded too
         parity = max(parity, abs(es1[0] - e_first[0]))
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{n_cpu} energy evaluations of the config-3 parameter-shift set (C oracle, OpenMP)",
@@ -485,15 +501,11 @@ def main():
                            "kernel holds the fp64 real parts (imaginary parts identically 0, energies equal to "
                            "the c128 program to <= 1e-12)" if sector["real_amplitudes"] else "complex128"),
             "data": "synthetic (seeded h~N(0,1), g~N(0,0.1), theta~U(-0.1,0.1); BASELINE.json config 3)",
-            "config": {"workload": "config3: 18 qubits, 10 electrons, 560 UCCSD generators, 9316-term JW "
-                                   "Hamiltonian; one step = parameter-shift gradient set (1121 energy "
-                                   "evaluations) per GPU",
-                       "path": ("support-closure evaluator: the 15876 amplitudes reachable from |HF> "
-                                "(exact for every theta), " + ("real parts only, one CTA per evaluation "
-                                "(real F and class sums: psi is real; see DESIGN.md)" if sector["real_amplitudes"]
-                                else "complex, %d-CTA cluster" % sector["ctas_per_eval"])),
-                       "evals_per_step_per_gpu": B, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"replicas x{world} (independent gradient sets)"},
+            "config": bench_config(world),
+            "path": ("support-closure evaluator: the 15876 amplitudes reachable from |HF> "
+                     "(exact for every theta), " + ("real parts only, one CTA per evaluation "
+                     "(real F and class sums: psi is real; see DESIGN.md)" if sector["real_amplitudes"]
+                     else "complex, %d-CTA cluster" % sector["ctas_per_eval"])),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(th_host.nbytes),
                     "d2h_bytes_per_step": int(16 * B)},
             "roofline": {"bound": "hbm", "kernel": "k_pauli_rotation (generic rotation pass)",

@@ -107,11 +107,41 @@ def cmd_vqe(args):
     return rep
 
 
-def cmd_selftest(args):
-    import __graft_entry__ as ge  # repo root: smoke() checks the CUDA path against the oracle
+GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                      "energies.json")
 
-    ge.smoke()
-    return _report("selftest", args, [{"unit": "config1", "method": "smoke", "ok": True}])
+
+def cmd_selftest(args):
+    """The CUDA path against the committed golden fixtures (tests/golden/energies.json,
+    tools/make_golden.py): config-1 energies of every fixture row (<= 1e-10 Ha) and
+    the config-1 state after the plan (<= 1e-12 max-abs)."""
+    from . import capi, problems
+
+    if not os.path.exists(GOLDEN):
+        raise OSError(f"selftest: golden fixtures not found at {GOLDEN}")
+    with open(GOLDEN) as f:
+        g = json.load(f)["configs"]["1"]
+    rows = g["rows"]
+    th = np.array([[float.fromhex(t) for t in r["theta_canonical"]] for r in rows])
+    P = problems.config_problem(1, batch=len(rows))
+    if not np.array_equal(th, P.thetas):
+        raise ValueError("selftest: seeded config-1 theta rows differ from the golden fixtures")
+    ctx, plan, ham = _device(P)
+    e = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())
+    de = max(abs(float(e[b]) - float.fromhex(r["energy"])) for b, r in enumerate(rows))
+    st = capi.State(ctx, P.n_qubits, 1)
+    st.set_basis(P.hf)
+    st.apply_plan(plan, P.plan_thetas()[:1])
+    psi = st.download()[0]
+    ref = np.array([float.fromhex(v) for v in rows[0]["state_re"]]) + 1j * np.array(
+        [float.fromhex(v) for v in rows[0]["state_im"]])
+    ds = float(np.abs(psi - ref).max())
+    ok = de <= 1e-10 and ds <= 1e-12
+    rep = _report("selftest", args, [{"unit": "config1", "method": "golden fixtures", "rows": len(rows),
+                                      "max_energy_err": de, "max_state_err": ds, "ok": ok}], [GOLDEN])
+    if not ok:
+        raise ValueError(f"selftest: CUDA path differs from the golden fixtures (energy {de:.3g}, state {ds:.3g})")
+    return rep
 
 
 def main(argv=None) -> int:
@@ -139,7 +169,6 @@ def main(argv=None) -> int:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 1 if e.code else 0
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     try:
         rep = {"ham": cmd_ham, "energy": cmd_energy, "vqe": cmd_vqe, "selftest": cmd_selftest}[args.cmd](args)
     except (ValueError, OSError) as e:  # ContractViolation / ParseError are ValueErrors

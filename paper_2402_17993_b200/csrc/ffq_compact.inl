@@ -15,7 +15,7 @@
 //    The 2x2 rotation is k_sector_eval_real's (same F, same fma order).
 //  - A Hamiltonian term (x, z, c) adds Re(c i^ny) * S with
 //    S = sum_k psi_k psi_{k^x} (-1)^popc((k^x) & z) over k with both members
-//    in the sector (ffo_oracle.c pauli_expect restricted to the sector; psi is
+//    in the sector (SPEC.md:419-427 expectation restricted to the sector; psi is
 //    real, so a term with Re(c i^ny) = 0 contributes nothing). Terms sharing a
 //    flip mask are one pass (the pair weight sums their signed w). Each pass's
 //    CTA partials land in fixed slots; one fixed-order reduction gives the energy.

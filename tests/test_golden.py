@@ -56,3 +56,28 @@ def test_oracle_reproduces_golden(oracle, cfg):
             ref = np.array([float.fromhex(v) for v in row["state_re"]]) + 1j * np.array(
                 [float.fromhex(v) for v in row["state_im"]])
             assert np.abs(r[2] - ref).max() <= 1e-13
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3"])
+def test_oracle_workload_matches_product_and_golden(cfg):
+    """bench.py --impl reference builds config 3 with the oracle alone
+    (oracle/workload.py). Its inputs equal the product's: theta rows and plan
+    order bit-identical (and equal to the golden fixtures' theta and plan hash),
+    Hamiltonian strings identical with coefficients within 1e-13 (the two JW
+    expansions sum the same products in different orders), shift sets identical."""
+    from oracle import workload as ow
+    from paper_2402_17993_b200 import parameter_shift_set
+
+    g = load()["configs"][cfg]
+    OP = ow.config_problem(int(cfg), batch=len(g["rows"]))
+    P = problems.config_problem(int(cfg), batch=len(g["rows"]))
+    assert np.array_equal(OP.thetas, P.thetas)
+    for b, row in enumerate(g["rows"]):
+        assert [float(t).hex() for t in OP.thetas[b]] == row["theta_canonical"]
+    assert digest(np.asarray(OP.order, np.int32)) == g["plan_order_sha256"]
+    ox, oz, oc = OP.H.terms()
+    x, z, c = P.ham_arrays()
+    assert np.array_equal(ox, x) and np.array_equal(oz, z)
+    assert np.abs(oc - c).max() <= 1e-13
+    assert np.array_equal(ow.parameter_shift_set(OP.thetas[0]),
+                          np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen))

@@ -272,6 +272,10 @@ def test_cli_energy_from_fcidump_and_vqe(tmp_path, capsys):
     assert cli.main(["vqe", "--config", "1", "--optimizer", "bfgs"]) == 0
     r = json.loads(capsys.readouterr().out)["records"][0]
     assert r["converged"] and r["total"] < r["hf_energy"]
+    # selftest: the CUDA path against the committed golden fixtures (no oracle import)
+    assert cli.main(["selftest"]) == 0
+    r = json.loads(capsys.readouterr().out)["records"][0]
+    assert r["ok"] and r["max_energy_err"] <= 1e-10 and r["max_state_err"] <= 1e-12
 
 
 def test_split_knob_bit_identical(monkeypatch):
