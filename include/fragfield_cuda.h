@@ -127,8 +127,11 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
  * (amplitudes), out[8] 1 when the program stores real amplitudes only (real F
  * on every generator and real class sums: psi(theta) is real for every theta),
  * out[9] expectation pairs held by anchored string blocks (product layout),
- * out[10] amplitude slots (padded product layout; = out[0] otherwise).
- * out must hold 11 values.
+ * out[10] amplitude slots (padded product layout; = out[0] otherwise),
+ * out[11] expectation pairs held by alpha-beta cliques, out[12] clique warp
+ * tasks, out[13] modelled extra shared wavefronts per clique row (bank
+ * conflicts summed over half-warp tasks; 0 = conflict-free).
+ * out must hold 14 values.
  * FFQ_EINVAL when the closure does not fit the sector evaluator (the other
  * paths then run) or FFQ_SECTOR=0. */
 int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
@@ -222,9 +225,12 @@ int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, con
 /* Test hook (host only, no GPU): compiles the one-CTA real-amplitude sector
  * program (product layout, anchored string blocks) for plan + Hamiltonian +
  * hf and evaluates its expectation tables on the real state psi[2^n] exactly
- * as k_sector_eval_real would. out[8]: energy, closure size, amplitude slots,
- * product layout (0/1), pairs held by blocks, expectation pairs, generic rows,
- * block units. FFQ_EINVAL when the program is complex or has no sector. */
+ * as k_sector_eval_real would (generic rows, blocks, then the alpha-beta
+ * cliques in the alpha-first gauge). out[10]: energy, closure size, amplitude
+ * slots, product layout (0/1), pairs held by blocks, expectation pairs,
+ * generic rows, block units, pairs held by cliques, modelled clique bank
+ * conflicts. FFQ_CLIQUES=0 compiles without cliques. FFQ_EINVAL when the
+ * program is complex or has no sector. */
 int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
                        const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,

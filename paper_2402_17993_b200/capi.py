@@ -142,10 +142,11 @@ def sector_emulate(n, plan_arrays, ham_arrays, hf_bits, psi):
     hx, hz, hre, him = _terms(*ham_arrays)
     off = np.ascontiguousarray(off, np.int64)
     psi = np.ascontiguousarray(psi, np.float64)
-    out = np.zeros(8)
+    out = np.zeros(10)
     check(lib().ffq_sector_emulate(n, len(off) - 1, off, px, pz, pre, pim, len(hx), hx, hz, hre, him, hf_bits, psi,
                                    out))
-    keys = ["energy", "closure_size", "slots", "product", "block_pairs", "exp_pairs", "generic_rows", "units"]
+    keys = ["energy", "closure_size", "slots", "product", "block_pairs", "exp_pairs", "generic_rows", "units",
+            "clique_pairs", "clique_conflicts"]
     return dict(zip(keys, out.tolist()))
 
 
@@ -241,12 +242,13 @@ def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int
 
 SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expectation_pairs",
                     "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
-                    "real_amplitudes", "block_pairs", "slots")
+                    "real_amplitudes", "block_pairs", "slots", "clique_pairs", "clique_warp_tasks",
+                    "clique_conflicts")
 
 
 def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:
     """Statistics of the support-closure program energy_batch runs (ffq_sector_info)."""
-    out = np.zeros(11, np.int64)
+    out = np.zeros(14, np.int64)
     check(lib().ffq_sector_info(ctx.h, plan.h, ham.h, hf_bits, out), ctx.h)
     return dict(zip(SECTOR_INFO_KEYS, (int(v) for v in out)))
 

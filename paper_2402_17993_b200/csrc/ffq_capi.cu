@@ -188,6 +188,7 @@ struct ffq_ctx_s {
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
+  int sector_cliques = 1;                        // env FFQ_CLIQUES=0: alpha-beta pairs in the blocks, not the cliques
   int sector_split = 8;                          // env FFQ_SPLIT: most CTAs per evaluation of the 1024-thread real program
   std::string err = "no error";
   int64_t launches = 0;
@@ -259,6 +260,9 @@ struct ffq_plan_s {
     DevBuf<int32_t> blk_warp;
     DevBuf<uint32_t> blk_stream;
     DevBuf<double> ftab;
+    DevBuf<uint32_t> eps_flip, cq_rows;
+    DevBuf<int32_t> cq_desc, cq_warp;
+    DevBuf<double> cq_coef;
     bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
@@ -589,7 +593,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     // one-CTA real program or the cluster split (rows padded to multiples of 4)
     // (anchored string blocks for the 1024-thread real program: FFQ_BLOCKS=0 disables them)
     b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, real_ok ? 8 : 16,
-                             real_ok && ctx->sector_blocks ? kSectorRealThreads / 32 : 0, kSectorSingleMax);
+                             real_ok && ctx->sector_blocks ? kSectorRealThreads / 32 : 0, kSectorSingleMax,
+                             real_ok && ctx->sector_blocks && ctx->sector_cliques);
     b->real = b->prog.ok && real_ok &&
               sector_real_smem_bytes(b->prog.n_slots, pl->cp.op_kind.size()) +
                       b->prog.ftab.size() * sizeof(double) <= ctx->smem_optin;
@@ -612,6 +617,13 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
         b->blk_warp.upload(b->prog.blk_warp, ctx->stream);
         b->blk_stream.upload(b->prog.blk_stream, ctx->stream);
         b->ftab.upload(b->prog.ftab, ctx->stream);
+      }
+      if (!b->prog.eps_flip.empty()) b->eps_flip.upload(b->prog.eps_flip, ctx->stream);
+      if (b->prog.product && !b->prog.cq_warp.empty()) {
+        b->cq_rows.upload(b->prog.cq_rows, ctx->stream);
+        b->cq_desc.upload(b->prog.cq_desc, ctx->stream);
+        b->cq_warp.upload(b->prog.cq_warp, ctx->stream);
+        b->cq_coef.upload(b->prog.cq_coef, ctx->stream);
       }
       if (!b->prog.f_real) {
         b->row_fim.upload(b->prog.row_fim, ctx->stream);
@@ -653,6 +665,12 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.blk_stream = blk ? b.blk_stream.p : nullptr;
   sd.ftab = blk ? b.ftab.p : nullptr;
   sd.n_ftab = blk ? (int)b.prog.ftab.size() : 0;
+  const bool cq = blk && !b.prog.cq_warp.empty();
+  sd.eps_flip = blk && !b.prog.eps_flip.empty() ? b.eps_flip.p : nullptr;
+  sd.cq_rows = cq ? b.cq_rows.p : nullptr;
+  sd.cq_desc = cq ? reinterpret_cast<const int4*>(b.cq_desc.p) : nullptr;
+  sd.cq_warp = cq ? reinterpret_cast<const int2*>(b.cq_warp.p) : nullptr;
+  sd.cq_coef = cq ? b.cq_coef.p : nullptr;
   return &sd;
 }
 
@@ -955,6 +973,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_CLIQUES")) c->sector_cliques = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT")) c->compact = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
@@ -1155,6 +1174,9 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
     out[8] = bufs.real ? 1 : 0;
     out[9] = S.blk_pairs;
     out[10] = S.n_slots;
+    out[11] = S.cq_pairs;
+    out[12] = (int64_t)(S.cq_desc.size() / 128);
+    out[13] = S.cq_conflicts;
     return FFQ_OK;
   });
 }
@@ -1483,11 +1505,15 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
     const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, px, pz, pc_re, pc_im);
     const CompiledHam H = compile_ham(n_qubits, n_terms, hx, hz, hc_re, hc_im);
     if (!plan_is_real(P) || !ham_is_real(H)) return fail(nullptr, FFQ_EINVAL, "ffq_sector_emulate: complex program");
+    const char* cqe = std::getenv("FFQ_CLIQUES");
     const SectorProgram S = compile_sector(P, H, hf_bits, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, 8,
-                                           kSectorRealThreads / 32, kSectorSingleMax);
+                                           kSectorRealThreads / 32, kSectorSingleMax, !cqe || std::atoi(cqe) != 0);
     if (!S.ok) return fail(nullptr, FFQ_EINVAL, "ffq_sector_emulate: " + S.why);
     std::vector<double> amp((size_t)S.n_slots + 1, 0.0);
     for (uint32_t i = 0; i < S.size; ++i) amp[S.slot_of[i]] = psi[S.basis[i]];
+    if (!S.eps_flip.empty())  // the expectation tables are in the alpha-first gauge
+      for (uint32_t i = 0; i < S.n_slots; ++i)
+        if ((S.eps_flip[i / 32] >> (i % 32)) & 1u) amp[i] = -amp[i];
     double e = 0.0;
     const auto& es = S.sections[0];
     for (int r = es.sh0; r < es.pp1; ++r)
@@ -1518,6 +1544,34 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
         e += a * t;
       }
     }
+    if (!S.cq_warp.empty()) {  // the device's clique phase, same arithmetic
+      for (size_t w = 0; w < S.cq_warp.size() / 2; ++w)
+        for (int32_t wt = S.cq_warp[2 * w]; wt < S.cq_warp[2 * w + 1]; ++wt)
+          for (int l = 0; l < 32; ++l) {
+            const int32_t* d = &S.cq_desc[((size_t)wt * 32 + l) * 4];
+            uint32_t c[kCliqueMax];
+            for (int i = 0; i < 4; ++i) c[i] = ((uint32_t)d[0] >> (8 * i)) & 0xFFu;
+            c[4] = (uint32_t)d[1] & 0xFFu;
+            c[5] = ((uint32_t)d[1] >> 8) & 0xFFu;
+            double acc[kCliquePairs] = {0.0};
+            for (int k = d[2]; k < d[3]; ++k) {
+              const uint32_t rw = S.cq_rows[k];
+              double u[kCliqueMax], v[kCliqueMax];
+              for (int i = 0; i < kCliqueMax; ++i) {
+                u[i] = amp.at((rw & 0x7FFFu) + c[i]) * ((rw >> 31) ? -1.0 : 1.0);
+                v[i] = amp.at(((rw >> 15) & 0x7FFFu) + c[i]);
+              }
+              for (int jj = 0; jj < kCliqueMax; ++jj)
+                for (int i = 0; i < kCliqueMax; ++i)
+                  if (i != jj) {
+                    const int a = std::min(i, jj), b = std::max(i, jj);
+                    const int p = a * (2 * kCliqueMax - a - 1) / 2 + (b - a - 1);
+                    acc[p] = std::fma(u[i], v[jj], acc[p]);
+                  }
+            }
+            for (int p = 0; p < kCliquePairs; ++p) e += S.cq_coef[((size_t)wt * kCliquePairs + p) * 32 + l] * acc[p];
+          }
+    }
     out[0] = e;
     out[1] = S.size;
     out[2] = S.n_slots;
@@ -1526,6 +1580,8 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
     out[5] = (double)S.exp_pair_count;
     out[6] = (double)(es.pp1 - es.sh0);
     out[7] = (double)nu;
+    out[8] = (double)S.cq_pairs;
+    out[9] = (double)S.cq_conflicts;
     return FFQ_OK;
   });
 }

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -23,6 +24,7 @@
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -750,6 +752,19 @@ struct SectorProgram {
   std::vector<double> blk_fs;
   std::vector<int32_t> blk_warp;
   int64_t blk_pairs = 0;               // expectation pairs held by the blocks
+  // Alpha-beta cliques (compile_cliques): the expectation pairs whose flip
+  // mask is one alpha and one beta single excitation, evaluated as
+  // sum_k s_k u_k^T C v_k over beta cliques (see compile_cliques), in the
+  // alpha-first sign gauge: before the clique phase the device negates the
+  // slots set in eps_flip.
+  std::vector<uint32_t> alpha_strings, beta_strings;  // product layout: string of each alpha / beta index
+  std::vector<uint32_t> eps_flip;      // [n_slots / 32 + 1] bitset over slots
+  std::vector<uint32_t> cq_rows;       // ia * stride | ia' * stride << 15 | neg << 31
+  std::vector<int32_t> cq_desc;        // [warp tasks][32][4]: columns 0-3 (bytes), columns 4-5, row begin, row end
+  std::vector<double> cq_coef;         // [warp tasks][15][32]: C_ij of the lane's clique, pairs (i < j) in order
+  std::vector<int32_t> cq_warp;        // [warps][2]: warp-task range of each warp
+  int64_t cq_pairs = 0;                // expectation pairs held by the cliques
+  int64_t cq_conflicts = 0;            // extra shared wavefronts per row over all half-warp tasks (bank model)
 };
 
 constexpr int kBlockMaxNC = 1;        // lane chunks per unit (the device runs one)
@@ -950,6 +965,243 @@ inline void compile_blocks(SectorProgram& S, const std::vector<uint32_t>& list,
   }
 }
 
+// ---- alpha-beta cliques -------------------------------------------------------------
+// A pair (m, m ^ X) whose flip mask is one alpha single excitation Xa and one
+// beta single excitation Xb has weight f(m) = c(X) (-1)^popc(m & zout): one
+// outside-Z class (two-body H). Reordered to the alpha-first gauge (amplitude
+// psi'(k) = eps(k) psi(k), eps = sign of moving every alpha creator in front
+// of the beta ones), the weight factorises as
+//     f'(m) = eps(m) eps(m ^ X) f(m) = s_Xa(a) * C_Xa(b, b')
+// (a, b: alpha / beta strings of the member m that holds Xa's lowest qubit;
+// b' = b ^ Xb). This is checked pair by pair below, never assumed. Writing
+// u_k = psi'[a_k][.], v_k = psi'[a_k ^ Xa][.] for the rows k of Xa,
+//     E_ab = sum_Xa sum_k s_k sum_(b, b') C_Xa(b, b') u_k[b] v_k[b'].
+// Every beta pair (b, b') lies in exactly one clique T = b | b' (the N_b + 1
+// strings that are N_b-subsets of T, pairwise single excitations), so a lane
+// owning (Xa, T) loads the 6 + 6 amplitudes of T in rows a_k and a_k ^ Xa and
+// accumulates acc_ij += s_k (u_i v_j + u_j v_i) over the 15 member pairs (C is
+// symmetric, checked), 30 FMAs per 12 shared loads; C_ij is applied once per
+// task. The lanes of a half warp share Xa (so a row's base slot is uniform) and
+// their member order is chosen so each of the 6 loads hits 16 distinct bank
+// pairs where the columns allow.
+constexpr int kCliqueMax = 6;
+constexpr int kCliquePairs = kCliqueMax * (kCliqueMax - 1) / 2;
+
+// parity of the reorder interleaved -> alpha-first for basis state k (alpha =
+// even qubits): each occupied beta qubit passes the occupied alpha qubits above it
+inline int alpha_first_parity(uint64_t k, int n) {
+  uint64_t am = 0;
+  for (int q = 0; q < n; q += 2) am |= 1ULL << q;
+  int s = 0;
+  for (int r = 1; r < n; r += 2)
+    if ((k >> r) & 1ULL) s += popc64(k & am & ~((2ULL << r) - 1ULL));
+  return s & 1;
+}
+
+// member order of each lane of a half warp (lanes: <= 16 column lists of
+// kCliqueMax entries) so that load c of every lane hits distinct 8-byte bank
+// pairs (column mod 16; equal columns broadcast). Returns the extra
+// wavefronts per row over the 6 loads (0 = conflict-free).
+inline int clique_color(std::vector<std::array<uint32_t, kCliqueMax>>& lanes) {
+  const size_t L = lanes.size();
+  auto cost_of = [&](int c) {
+    int cnt[16] = {0};
+    uint32_t seen[16][16];
+    int ns[16] = {0};
+    for (size_t l = 0; l < L; ++l) {
+      const uint32_t col = lanes[l][c], r = col & 15u;
+      bool dup = false;
+      for (int q = 0; q < ns[r]; ++q) dup |= seen[r][q] == col;
+      if (!dup) { seen[r][ns[r]++] = col; ++cnt[r]; }
+    }
+    return *std::max_element(cnt, cnt + 16) - 1;
+  };
+  // greedy: per load slot a maximum matching lanes -> residues (Kuhn)
+  std::vector<std::array<uint32_t, kCliqueMax>> rem = lanes;
+  std::vector<int> nrem(L, kCliqueMax);
+  for (int c = 0; c < kCliqueMax; ++c) {
+    int match_res[16], match_lane[16];
+    for (int r = 0; r < 16; ++r) match_res[r] = -1;
+    for (size_t l = 0; l < L; ++l) match_lane[l] = -1;
+    std::function<bool(int, std::vector<bool>&)> aug = [&](int l, std::vector<bool>& vis) {
+      for (int q = 0; q < nrem[l]; ++q) {
+        const int r = (int)(rem[l][q] & 15u);
+        if (vis[r]) continue;
+        vis[r] = true;
+        if (match_res[r] < 0 || aug(match_res[r], vis)) { match_res[r] = l; match_lane[l] = q; return true; }
+      }
+      return false;
+    };
+    // lanes with the fewest choices first
+    std::vector<int> ord(L);
+    for (size_t l = 0; l < L; ++l) ord[l] = (int)l;
+    for (int l : ord) { std::vector<bool> vis(16, false); aug(l, vis); }
+    for (int r = 0; r < 16; ++r)
+      if (match_res[r] >= 0) {  // Kuhn may have re-pointed lanes: recover each lane's member by residue
+        const int l = match_res[r];
+        for (int q = 0; q < nrem[l]; ++q)
+          if ((int)(rem[l][q] & 15u) == r) { match_lane[l] = q; break; }
+      }
+    for (size_t l = 0; l < L; ++l) {
+      const int q = match_lane[l] >= 0 ? match_lane[l] : 0;
+      lanes[l][c] = rem[l][q];
+      rem[l][q] = rem[l][nrem[l] - 1];
+      --nrem[l];
+    }
+  }
+  int total = 0;
+  for (int c = 0; c < kCliqueMax; ++c) total += cost_of(c);
+  // local search: swap two load slots of one lane when the total does not grow
+  uint64_t rng = 0x2545F4914F6CDD1Dull;
+  for (int it = 0; it < 4000 && total > 0; ++it) {
+    rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+    const size_t l = rng % L;
+    const int c1 = (int)((rng >> 20) % kCliqueMax), c2 = (int)((rng >> 40) % kCliqueMax);
+    if (c1 == c2) continue;
+    const int before = cost_of(c1) + cost_of(c2);
+    std::swap(lanes[l][c1], lanes[l][c2]);
+    const int after = cost_of(c1) + cost_of(c2);
+    if (after <= before) total += after - before;
+    else std::swap(lanes[l][c1], lanes[l][c2]);
+  }
+  return total;
+}
+
+// f: pair weights already in the alpha-first gauge (compile_sector multiplies
+// every expectation weight by eps(m) eps(m ^ X) when cliques are on)
+inline void compile_cliques(SectorProgram& S, const std::vector<uint32_t>& list,
+                            const std::vector<std::pair<uint32_t, uint32_t>>& ij, const std::vector<double>& f,
+                            const std::vector<uint32_t>& slot_of, const std::vector<uint32_t>& ia_of,
+                            const std::vector<uint32_t>& ib_of, uint64_t amask, std::vector<uint8_t>& in_clique) {
+  const uint32_t NB = S.n_beta, stride = S.stride_b;
+  if (NB >= 256) return;  // 8-bit columns
+  const uint32_t zero_col = NB;  // slot a * stride + NB is padding (zero) in every row when stride > NB
+  std::map<uint32_t, uint32_t> bpos;
+  for (uint32_t q = 0; q < NB; ++q) bpos[S.beta_strings[q]] = q;
+  struct Cand { uint32_t a, a2, b, b2; double w; size_t t; };
+  std::map<uint64_t, std::vector<Cand>> by_xa;
+  for (size_t t = 0; t < ij.size(); ++t) {
+    uint32_t i = ij[t].first, j = ij[t].second;
+    const uint64_t X = (uint64_t)(list[i] ^ list[j]), xa = X & amask, xb = X & ~amask;
+    if (popc64(xa) != 2 || popc64(xb) != 2) continue;
+    if (!(list[i] & (xa & (~xa + 1)))) std::swap(i, j);
+    by_xa[xa].push_back({ia_of[i], ia_of[j], ib_of[i], ib_of[j], f[t], t});
+  }
+  struct Group { uint64_t xa; std::vector<uint32_t> rows; std::vector<int8_t> sgn; std::map<std::pair<uint32_t, uint32_t>, double> C; std::vector<uint64_t> cliques; };
+  std::vector<Group> groups;
+  for (auto& [xa, cs] : by_xa) {
+    Group g;
+    g.xa = xa;
+    std::map<uint32_t, uint32_t> rix;
+    std::map<std::pair<uint32_t, uint32_t>, uint32_t> kix;
+    std::vector<std::pair<uint32_t, uint32_t>> keys;
+    for (const Cand& c : cs) {
+      if (!rix.count(c.a)) { rix[c.a] = (uint32_t)g.rows.size(); g.rows.push_back(c.a); }
+      const auto key = std::make_pair(c.b, c.b2);
+      if (!kix.count(key)) { kix[key] = (uint32_t)keys.size(); keys.push_back(key); }
+    }
+    const size_t R = g.rows.size(), K = keys.size();
+    if (R * K != cs.size()) continue;  // not every (row, key): some weights vanish
+    std::vector<double> W(R * K, 0.0);
+    std::vector<uint8_t> have(R * K, 0);
+    for (const Cand& c : cs) {
+      const size_t s = (size_t)rix[c.a] * K + kix[{c.b, c.b2}];
+      if (have[s]) goto reject;
+      have[s] = 1;
+      W[s] = c.w;
+    }
+    {
+      // gauge: row 0 positive; C from row 0; every row's sign from key 0
+      std::vector<double> C(W.begin(), W.begin() + (long)K);
+      g.sgn.assign(R, 1);
+      for (size_t r = 0; r < R; ++r) {
+        g.sgn[r] = (W[r * K] > 0) == (C[0] > 0) ? 1 : -1;
+        for (size_t k = 0; k < K; ++k) {
+          const double want = g.sgn[r] * C[k];
+          if (std::fabs(want - W[r * K + k]) > 1e-13 * std::fabs(W[r * K + k])) goto reject;
+        }
+      }
+      for (size_t k = 0; k < K; ++k) {
+        auto it = kix.find({keys[k].second, keys[k].first});
+        if (it == kix.end() || std::fabs(C[it->second] - C[k]) > 1e-13 * std::fabs(C[k])) goto reject;
+        g.C[keys[k]] = C[k];
+      }
+      std::set<uint64_t> ts;
+      for (const auto& key : keys) ts.insert((uint64_t)S.beta_strings[key.first] | S.beta_strings[key.second]);
+      for (uint64_t T : ts) {
+        if (popc64(T) > kCliqueMax) goto reject;
+        uint32_t nm = 0;
+        for (int q = 0; q < S.n; ++q)
+          if (((T >> q) & 1ULL) && bpos.count((uint32_t)(T ^ (1ULL << q)))) ++nm;
+        if (nm < (uint32_t)kCliqueMax && stride <= NB) goto reject;  // no zero column to pad with
+      }
+      g.cliques.assign(ts.begin(), ts.end());
+      for (const Cand& c : cs) in_clique[c.t] = 1;
+      S.cq_pairs += (int64_t)cs.size();
+      groups.push_back(std::move(g));
+      continue;
+    }
+  reject:;
+  }
+  if (groups.empty()) return;
+  // half-warp tasks: per group, its cliques in chunks of <= 16 lanes, member
+  // orders colored per chunk (cached by clique list)
+  struct Half { uint32_t row0, row1; std::vector<std::array<uint32_t, kCliqueMax>> cols; const Group* g; };
+  std::vector<Half> halves;
+  std::map<std::vector<uint64_t>, std::vector<std::vector<std::array<uint32_t, kCliqueMax>>>> cache;
+  for (const Group& g : groups) {
+    const uint32_t row0 = (uint32_t)S.cq_rows.size();
+    for (size_t r = 0; r < g.rows.size(); ++r) {
+      const uint32_t a = g.rows[r], a2 = (uint32_t)std::distance(
+          S.alpha_strings.begin(), std::find(S.alpha_strings.begin(), S.alpha_strings.end(),
+                                             S.alpha_strings[a] ^ (uint32_t)g.xa));
+      S.cq_rows.push_back(a * stride | (a2 * stride) << 15 | (g.sgn[r] < 0 ? 1u << 31 : 0u));
+    }
+    auto it = cache.find(g.cliques);
+    if (it == cache.end()) {
+      const size_t nT = g.cliques.size(), nh = (nT + 15) / 16;
+      std::vector<std::vector<std::array<uint32_t, kCliqueMax>>> hs(nh);
+      for (size_t q = 0; q < nT; ++q) {
+        const uint64_t T = g.cliques[q];
+        std::array<uint32_t, kCliqueMax> m;
+        m.fill(zero_col);
+        int nm = 0;
+        for (int b = 0; b < S.n; ++b)
+          if ((T >> b) & 1ULL) {
+            auto p = bpos.find((uint32_t)(T ^ (1ULL << b)));
+            if (p != bpos.end()) m[nm++] = p->second;
+          }
+        hs[q * nh / nT].push_back(m);  // balanced chunks
+      }
+      for (auto& h : hs) S.cq_conflicts += clique_color(h);
+      it = cache.emplace(g.cliques, std::move(hs)).first;
+    }
+    for (const auto& h : it->second) halves.push_back({row0, (uint32_t)S.cq_rows.size(), h, &g});
+  }
+  // warp tasks = two half-warp tasks; lanes beyond a half's cliques are idle
+  const size_t nwt = (halves.size() + 1) / 2;
+  S.cq_desc.assign(nwt * 32 * 4, 0);
+  S.cq_coef.assign(nwt * kCliquePairs * 32, 0.0);
+  for (size_t h = 0; h < halves.size(); ++h) {
+    const Half& H = halves[h];
+    const size_t wt = h / 2, l0 = (h % 2) * 16;
+    for (size_t l = 0; l < H.cols.size(); ++l) {
+      const auto& m = H.cols[l];
+      int32_t* d = &S.cq_desc[(wt * 32 + l0 + l) * 4];
+      d[0] = (int32_t)(m[0] | m[1] << 8 | m[2] << 16 | m[3] << 24);
+      d[1] = (int32_t)(m[4] | m[5] << 8);
+      d[2] = (int32_t)H.row0;
+      d[3] = (int32_t)H.row1;
+      int p = 0;
+      for (int i = 0; i < kCliqueMax; ++i)
+        for (int j = i + 1; j < kCliqueMax; ++j, ++p) {
+          auto c = H.g->C.find({m[i], m[j]});
+          S.cq_coef[(wt * kCliquePairs + p) * 32 + l0 + l] = c == H.g->C.end() ? 0.0 : c->second;
+        }
+    }
+  }
+}
+
 // L1 wavefronts of a block unit (a lane word and a shared load per row;
 // per-lane rows add a coalesced f load), used to balance warps
 inline double block_unit_cost(const int32_t* hdr) {
@@ -1044,7 +1296,8 @@ constexpr uint32_t kMinChunk = 256;
 inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H, uint64_t hf,
                                     uint32_t max_size, uint32_t max_part = 0xFFFFFFFFu, int n_parts = 2,
                                     uint32_t cap_amps = 0xFFFFFFFFu, int row_quantum = 4,
-                                    int elem_bytes = 16, int block_warps = 0, uint32_t block_min_size = 0) {
+                                    int elem_bytes = 16, int block_warps = 0, uint32_t block_min_size = 0,
+                                    bool cliques = false) {
   // lanes per conflict-free shared-memory wavefront for this amplitude size
   const int bank_group = elem_bytes == 8 ? 16 : 8;
   SectorProgram S;
@@ -1210,8 +1463,11 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       }
       std::sort(xas.begin(), xas.end());
       xas.erase(std::unique(xas.begin(), xas.end()), xas.end());
-      sa = alpha_order(sa, xas, stride);
+      // (with the alpha-beta cliques those blocks are gone: natural order)
+      if (!cliques) sa = alpha_order(sa, xas, stride);
       S.product = true;
+      S.alpha_strings = sa;
+      S.beta_strings = sbv;
       S.n_alpha = (uint32_t)sa.size();
       S.n_beta = (uint32_t)sbv.size();
       S.stride_b = stride;
@@ -1303,6 +1559,18 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   const bool buffered = S.buf_len > 0;
   S.exp_pair_count = (int64_t)ek.size();
   std::vector<uint8_t> in_block(ek.size(), 0);
+  if (S.product && cliques) {
+    // the whole expectation runs in the alpha-first gauge (see compile_cliques):
+    // psi'(k) = eps(k) psi(k) (the device negates the eps_flip slots after the
+    // generator phase), so every pair weight takes the factor eps(m) eps(m ^ X)
+    std::vector<uint8_t> eps(list.size());
+    for (size_t i = 0; i < list.size(); ++i) eps[i] = (uint8_t)alpha_first_parity(list[i], n);
+    for (auto& e : ek)
+      if (eps[idx[e.m]] ^ eps[idx[e.m ^ (uint32_t)H.groups[e.g].x]]) { e.fr = -e.fr; e.fi = -e.fi; }
+    S.eps_flip.assign(S.n_slots / 32 + 1, 0u);
+    for (size_t i = 0; i < list.size(); ++i)
+      if (eps[i]) S.eps_flip[slot_of[i] / 32] |= 1u << (slot_of[i] % 32);
+  }
   if (S.product) {
     std::vector<std::pair<uint32_t, uint32_t>> ij(ek.size());
     std::vector<double> fv(ek.size());
@@ -1310,7 +1578,22 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       ij[t] = {(uint32_t)idx[ek[t].m], (uint32_t)idx[ek[t].m ^ (uint32_t)H.groups[ek[t].g].x]};
       fv[t] = ek[t].fr;
     }
-    compile_blocks(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_block);
+    if (cliques) {
+      // alpha-beta pairs that factorise go to the cliques, the rest to the blocks
+      std::vector<uint8_t> in_clique(ek.size(), 0);
+      compile_cliques(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_clique);
+      std::vector<std::pair<uint32_t, uint32_t>> ij2;
+      std::vector<double> fv2;
+      std::vector<size_t> back;
+      for (size_t t = 0; t < ek.size(); ++t)
+        if (!in_clique[t]) { ij2.push_back(ij[t]); fv2.push_back(fv[t]); back.push_back(t); }
+      std::vector<uint8_t> in2(ij2.size(), 0);
+      compile_blocks(S, list, ij2, fv2, slot_of, ia_of, ib_of, amask, in2);
+      for (size_t u = 0; u < back.size(); ++u) in_block[back[u]] = in2[u];
+      for (size_t t = 0; t < ek.size(); ++t) in_block[t] |= in_clique[t];
+    } else {
+      compile_blocks(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_block);
+    }
   }
   std::vector<uint8_t> eown(ek.size());
   {  // balance: with the chunk buffer a cross pair costs about what a local one does
@@ -1457,10 +1740,35 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ucost(a) > ucost(b); });
     std::vector<double> load((size_t)nw, generic / nw);
     std::vector<std::vector<size_t>> mine((size_t)nw);
+    // clique warp tasks first (the largest items), then the block units
+    const size_t nwt = S.cq_desc.size() / 128;
+    std::vector<std::vector<size_t>> cq_mine((size_t)nw);
+    for (size_t t = 0; t < nwt; ++t) {
+      int rows = 0;
+      for (int l = 0; l < 32; ++l) rows = std::max(rows, S.cq_desc[(t * 32 + l) * 4 + 3] - S.cq_desc[(t * 32 + l) * 4 + 2]);
+      const size_t w = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[w] += 25.0 * rows + 30.0;
+      cq_mine[w].push_back(t);
+    }
     for (size_t u : ord) {
       const size_t w = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
       load[w] += ucost(u);
       mine[w].push_back(u);
+    }
+    if (nwt) {  // each warp's clique tasks contiguous
+      std::vector<int32_t> desc;
+      std::vector<double> coef;
+      S.cq_warp.clear();
+      for (int w = 0; w < nw; ++w) {
+        S.cq_warp.push_back((int32_t)(desc.size() / 128));
+        for (size_t t : cq_mine[w]) {
+          desc.insert(desc.end(), &S.cq_desc[t * 128], &S.cq_desc[t * 128] + 128);
+          coef.insert(coef.end(), &S.cq_coef[t * kCliquePairs * 32], &S.cq_coef[t * kCliquePairs * 32] + kCliquePairs * 32);
+        }
+        S.cq_warp.push_back((int32_t)(desc.size() / 128));
+      }
+      S.cq_desc.swap(desc);
+      S.cq_coef.swap(coef);
     }
     S.blk_warp.clear();
     for (int w = 0; w < nw; ++w) {

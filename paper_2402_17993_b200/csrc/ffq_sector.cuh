@@ -48,6 +48,12 @@ struct SectorDev {
   const uint32_t* blk_stream;   // [rows * 32] lane words
   const double* ftab;           // [n_ftab] shared-row f values (copied to shared memory)
   int n_ftab;
+  // alpha-beta cliques (SectorProgram::cq_*); nullptr: none
+  const uint32_t* eps_flip;     // slots negated into the alpha-first gauge before the expectation (nullptr: none)
+  const uint32_t* cq_rows;      // ia * stride | ia' * stride << 15 | neg << 31
+  const int4* cq_desc;          // [warp tasks][32]: columns 0-3, columns 4-5, row begin, row end
+  const int2* cq_warp;          // [warps]: warp-task range
+  const double* cq_coef;        // [warp tasks][15][32]
 };
 
 // Amplitude slots (SectorProgram::slot_bits): 15 - log2(CL) offset bits, the
@@ -461,6 +467,54 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
   return fma(a, t[0] + t[1], acc);
 }
 
+// One warp's alpha-beta clique tasks (SectorProgram::cq_*, compile_cliques):
+// lane = (Xa, clique T), rows k of Xa: u = psi'[a_k][T], v = psi'[a_k ^ Xa][T]
+// (psi' in the alpha-first gauge), acc_ij += s_k (u_i v_j + u_j v_i), then
+// sum_ij C_ij acc_ij. The row word of the next row is in flight.
+__device__ __forceinline__ double clique_tasks(const SectorDev& sd, int warp, int lane, const double* amp) {
+  const int2 wr = __ldg(sd.cq_warp + warp);
+  double tot = 0.0;
+  for (int wt = wr.x; wt < wr.y; ++wt) {
+    const int4 d = __ldg(sd.cq_desc + (size_t)wt * 32 + lane);
+    double acc[kCliquePairs];
+#pragma unroll
+    for (int p = 0; p < kCliquePairs; ++p) acc[p] = 0.0;
+    uint32_t rn = d.z < d.w ? __ldg(sd.cq_rows + d.z) : 0u;
+    for (int k = d.z; k < d.w; ++k) {
+      const uint32_t rw = rn;
+      if (k + 1 < d.w) rn = __ldg(sd.cq_rows + k + 1);
+      const double* ra = amp + (rw & 0x7FFFu);
+      const double* rb = amp + ((rw >> 15) & 0x7FFFu);
+      const int sg = (int)(rw & 0x80000000u);
+      // columns stay packed (bytes of d.x, d.y): extracted per row, not held
+      auto col = [&](int i) { return ((uint32_t)(i < 4 ? d.x : d.y) >> (8 * (i & 3))) & 0xFFu; };
+      double u[kCliqueMax];
+#pragma unroll
+      for (int i = 0; i < kCliqueMax; ++i) {
+        const double x = ra[col(i)];
+        u[i] = __hiloint2double(__double2hiint(x) ^ sg, __double2loint(x));
+      }
+      // v one column at a time (register budget of the 1024-thread CTA):
+      // acc_ij += u_i v_j for every i != j, pair index of (min, max)
+#pragma unroll
+      for (int j = 0; j < kCliqueMax; ++j) {
+        const double v = rb[col(j)];
+#pragma unroll
+        for (int i = 0; i < kCliqueMax; ++i)
+          if (i != j) {
+            const int a = i < j ? i : j, b = i < j ? j : i;
+            const int p = a * (2 * kCliqueMax - a - 1) / 2 + (b - a - 1);
+            acc[p] = fma(u[i], v, acc[p]);
+          }
+      }
+    }
+    const double* cf = sd.cq_coef + (size_t)wt * kCliquePairs * 32 + lane;
+#pragma unroll
+    for (int p = 0; p < kCliquePairs; ++p) tot = fma(__ldg(cf + p * 32), acc[p], tot);
+  }
+  return tot;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
@@ -554,8 +608,14 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   for (int k = 0; k < D - 1; ++k)
     if (op + k < sd.n_ops) step(op + k, w[k]);
   const long long clk1 = clock64();
+  if (sd.eps_flip) {  // the expectation tables are in the alpha-first gauge (compile_sector)
+    for (uint32_t i = threadIdx.x; i < sd.n_slots; i += NT)
+      if ((__ldg(sd.eps_flip + (i >> 5)) >> (i & 31u)) & 1u) amp[i] = -amp[i];
+    __syncthreads();
+  }
   double acc = 0.0;
-  if (split == 1 || (threadIdx.x >> 5) % split == part) {
+  const bool mine = split == 1 || (threadIdx.x >> 5) % split == part;
+  if (mine) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t* es = sd.secs;  // one section: every pair is local
@@ -613,6 +673,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       }
     }
     if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
+    if (sd.cq_warp) acc += clique_tasks(sd, warp, lane, amp);      // this warp's alpha-beta cliques
   }
   if (split > 1) {
     if ((threadIdx.x >> 5) % split != part) return;

@@ -205,12 +205,36 @@ def test_sector_info_config3(monkeypatch, real):
     assert info["ctas_per_eval"] == (1 if real == "1" else 2)
     assert (info["cluster_barrier_steps"] == 0) == (real == "1")
     assert info["cluster_barrier_steps"] <= P.n_gen
-    assert info["expectation_rows"] * 32 >= info["expectation_pairs"] > 0
+    assert info["expectation_rows"] * 32 + info["clique_pairs"] >= info["expectation_pairs"] > 0
     assert info["generator_pairs"] > 0
     # the real program lays S out as 126 alpha x 127 (odd stride) beta slots and
-    # holds most expectation pairs in anchored string blocks
+    # holds most expectation pairs in alpha-beta cliques (every alpha-beta pair:
+    # 36 x 36 excitation masks x 35 x 70 pairs) and anchored string blocks
     assert info["slots"] == (126 * 127 if real == "1" else 15876)
-    assert (info["block_pairs"] >= 0.8 * info["expectation_pairs"]) == (real == "1")
+    held = info["block_pairs"] + info["clique_pairs"]
+    assert (held >= 0.8 * info["expectation_pairs"]) == (real == "1")
+    assert info["clique_pairs"] == (36 * 36 * 35 * 70 if real == "1" else 0)
+    if real == "1":  # the member order of the clique loads is bank-conflict free (model)
+        assert info["clique_conflicts"] <= 4
+
+
+def test_clique_expectation_matches_blocks(monkeypatch):
+    """The alpha-beta cliques (alpha-first gauge, FFQ_CLIQUES=1, the default)
+    against the anchored-block program without them (FFQ_CLIQUES=0) on config-3
+    parameter-shift rows, including +-pi/2 shifts (oracle parity of the default
+    program: tests/test_gpu_parity.py)."""
+    from paper_2402_17993_b200 import parameter_shift_set
+
+    P = problems.config_problem(3, batch=1)
+    rows = np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)[::37]
+    out = {}
+    for cq in ("1", "0"):
+        c = _ctx(monkeypatch, {"FFQ_CLIQUES": cq})
+        plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        assert (capi.sector_info(c, plan, ham, P.hf)["clique_pairs"] > 0) == (cq == "1")
+        out[cq] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas(rows))
+        del plan, ham, c
+    assert np.abs(out["1"] - out["0"]).max() <= 1e-12
 
 
 @pytest.mark.parametrize("config", [2, 3])

@@ -208,7 +208,9 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
     assert r["closure_size"] == int(((pa == na) & (pb == nb)).sum())
     if cfg == 3:  # 18 qubits: (5a, 5b) sector = 126 x 126 strings, stride 127
         assert r["product"] == 1 and r["slots"] == 126 * 127
-        assert r["block_pairs"] >= 0.8 * r["exp_pairs"] and r["units"] > 0
+        assert r["block_pairs"] + r["clique_pairs"] >= 0.8 * r["exp_pairs"] and r["units"] > 0
+        # the alpha-beta pairs (36 alpha x 36 beta single excitations, 35 x 70 pairs each) all factorise
+        assert r["clique_pairs"] == 36 * 36 * 35 * 70
     else:  # small closures keep the natural layout (256-thread program)
         assert r["product"] == 0 and r["block_pairs"] == 0
 
