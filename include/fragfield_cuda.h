@@ -135,6 +135,16 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
  * FFQ_EINVAL when the closure does not fit the sector evaluator (the other
  * paths then run) or FFQ_SECTOR=0. */
 int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
+/* Amplitude-level view of the 1024-thread real-amplitude sector program (the
+ * 18-qubit default): runs one evaluation of theta[n_gen] (plan order) and
+ * returns the state after the plan, scattered from its product-layout slots to
+ * natural order, in psi[2^n][2] (re, im; im = 0: the program holds psi's real
+ * parts, which is all of psi), plus the energy of the same launch in *energy
+ * (may be NULL). Replaces the state-dump side of energy_trotter (SPEC.md:459,
+ * 508-516) for the sector program. FFQ_EINVAL when that program does not run
+ * for these inputs. */
+int ffq_sector_state(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, const double* theta,
+                     double* psi, double* energy);
 
 /* ---- state-level operations (simulator) ------------------ */
 int ffq_state_alloc(ffq_ctx_t ctx, int n_qubits, int batch, ffq_state_t* out);

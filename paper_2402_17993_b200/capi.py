@@ -76,6 +76,7 @@ _SIGS = {
     "ffq_sector_emulate": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.c_int64, _u64p, _u64p,
                                      _f64p, _f64p, C.c_uint64, _f64p, _f64p]),
     "ffq_sector_info": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i64p]),
+    "ffq_sector_state": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, _f64p, C.POINTER(C.c_double)]),
 }
 
 _lib = None
@@ -244,6 +245,16 @@ SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expecta
                     "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
                     "real_amplitudes", "block_pairs", "slots", "clique_pairs", "clique_warp_tasks",
                     "clique_conflicts")
+
+
+def sector_state(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, theta, n_qubits: int):
+    """(psi[2^n] complex128 in natural order, energy) of one evaluation of the
+    real-amplitude sector program (ffq_sector_state); theta in plan order."""
+    th = np.ascontiguousarray(theta, np.float64).ravel()
+    psi = np.zeros(2 << n_qubits)
+    e = C.c_double()
+    check(lib().ffq_sector_state(ctx.h, plan.h, ham.h, hf_bits, th, psi, C.byref(e)), ctx.h)
+    return psi.view(np.complex128), e.value
 
 
 def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:

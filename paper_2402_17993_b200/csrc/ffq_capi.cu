@@ -700,7 +700,7 @@ void launch_sector_t(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, c
 
 template <int NT>
 void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, const double* theta, int batch,
-                        double* e, double* im, long long* clk) {
+                        double* e, double* im, long long* clk, double* state_out = nullptr) {
   // anchored blocks keep the shared-row f table behind the per-op tables
   const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) + (size_t)sd.n_ftab * sizeof(double);
   CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
@@ -708,11 +708,11 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   // (1024-thread program only). Each runs the generator phase and 32 / split
   // of the warp shares of the expectation; the energies are bit-identical.
   int split = 1;
-  if (NT == 32 * 32)
+  if (NT == 32 * 32 && !state_out)
     while (split * 2 <= ctx->sector_split && (int64_t)batch * split * 2 <= ctx->n_sm) split *= 2;
   if (split > 1) ctx->warp_sums.alloc((size_t)batch * 32);
   k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
-                                                                 clk, split, ctx->warp_sums.p);
+                                                                 clk, split, ctx->warp_sums.p, state_out);
   CK(cudaGetLastError());
   ctx->launches++;
   if (split > 1) {
@@ -1144,6 +1144,35 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
     return fail(ctx, FFQ_EINVAL, "ffq_energy_batch_device: invalid argument");
   return guarded(ctx, [&] {
     energy_device(ctx, plan, ham, hf_bits, batch, theta_dev, e_dev, imag_dev);
+    return FFQ_OK;
+  });
+}
+
+int ffq_sector_state(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, const double* theta,
+                     double* psi, double* energy) {
+  if (!ctx || !plan || !ham || !theta || !psi) return fail(ctx, FFQ_EINVAL, "ffq_sector_state: invalid argument");
+  return guarded(ctx, [&] {
+    if (!ctx->sector) return fail(ctx, FFQ_EINVAL, "ffq_sector_state: support-closure evaluator disabled (FFQ_SECTOR=0)");
+    const SectorDev* sd = sector_program(ctx, plan, ham, hf_bits);
+    if (!sd || !sd->real || sd->size <= kSectorSingleMax)
+      return fail(ctx, FFQ_EINVAL, "ffq_sector_state: no 1024-thread real-amplitude sector program for these inputs");
+    const SectorProgram& S = plan->sectors.at(std::make_pair(ham->uid, hf_bits))->prog;
+    const int ng = plan->cp.n_gen;
+    DevBuf<double> th, e, st;
+    th.alloc((size_t)ng);
+    e.alloc(1);
+    st.alloc((size_t)S.n_slots);
+    CK(cudaMemcpyAsync(th.p, theta, (size_t)ng * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    launch_sector_real<kSectorRealThreads>(ctx, plan, *sd, th.p, 1, e.p, nullptr, nullptr, st.p);
+    std::vector<double> slots(S.n_slots);
+    double eh = 0.0;
+    CK(cudaMemcpyAsync(slots.data(), st.p, slots.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&eh, e.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const size_t dim = size_t(1) << plan->cp.n_qubits;
+    std::memset(psi, 0, 2 * dim * sizeof(double));
+    for (uint32_t i = 0; i < S.size; ++i) psi[2 * (size_t)S.basis[i]] = slots[S.slot_of[i]];
+    if (energy) *energy = eh;
     return FFQ_OK;
   });
 }

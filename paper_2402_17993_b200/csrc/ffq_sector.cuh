@@ -520,7 +520,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
                                                             int n_rows, long long* __restrict__ phase_clk,
-                                                            int split, double* __restrict__ warp_sums) {
+                                                            int split, double* __restrict__ warp_sums,
+                                                            double* __restrict__ state_out) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
   // split > 1 (small batches): `split` CTAs run one evaluation; each runs the
@@ -608,6 +609,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   for (int k = 0; k < D - 1; ++k)
     if (op + k < sd.n_ops) step(op + k, w[k]);
   const long long clk1 = clock64();
+  if (state_out && part == 0)  // ffq_sector_state: the slots after the plan (natural gauge)
+    for (uint32_t i = threadIdx.x; i < sd.n_slots; i += NT) state_out[(int64_t)row * sd.n_slots + i] = amp[i];
   if (sd.eps_flip) {  // the expectation tables are in the alpha-first gauge (compile_sector)
     for (uint32_t i = threadIdx.x; i < sd.n_slots; i += NT)
       if ((__ldg(sd.eps_flip + (i >> 5)) >> (i & 31u)) & 1u) amp[i] = -amp[i];

@@ -81,3 +81,18 @@ def test_oracle_workload_matches_product_and_golden(cfg):
     assert np.abs(oc - c).max() <= 1e-13
     assert np.array_equal(ow.parameter_shift_set(OP.thetas[0]),
                           np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen))
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3"])
+def test_golden_energies_match_jw_free_oracle(cfg):
+    """Every golden row against the oracle's JW-free evaluator
+    (ffo.energy_fermionic: fermionic Givens rotations on determinants, <H>
+    from the second-quantised integrals; no Pauli strings, no JW), with inputs
+    from oracle/workload.py: an independent pin of the golden energies."""
+    from oracle import ffo, workload as ow
+
+    g = load()["configs"][cfg]
+    OP = ow.config_problem(int(cfg), batch=len(g["rows"]))
+    for b, row in enumerate(g["rows"]):
+        ef = ffo.energy_fermionic(OP.h, OP.g, OP.n_elec, OP.kind, OP.idx, OP.order, OP.thetas[b])
+        assert abs(ef - float.fromhex(row["energy"])) <= 1e-12

@@ -3,12 +3,15 @@ for BASELINE.json configs 1-3 on their seeded synthetic inputs.
 
 The reference has no implementation or golden vectors for this path (SURVEY.md
 8c), so the values come from the C oracle (oracle/ffo_oracle.c, the SPEC.md
-restatement), cross-checked here against an independent dense-matrix
-computation for config 1. The fixtures pin the oracle (tests/test_golden.py)
+restatement), cross-checked here against two independent computations: a
+dense-matrix <psi|H|psi> for config 1, and, for EVERY row of configs 1-3, the
+oracle's JW-free evaluator (ffo.energy_fermionic: Givens rotations on
+determinants and <H> from the second-quantised h, g; no Pauli strings), which
+must agree to <= 1e-12 Hartree. The fixtures pin the oracle (tests/test_golden.py)
 and the CUDA path (tests/test_gpu_parity.py) against drift. Floats are stored
 as hex strings (exact round trip).
 
-Usage: python tools/make_golden.py   (CPU only; ~10 s)
+Usage: python tools/make_golden.py   (CPU only; ~20 s)
 """
 import hashlib
 import json
@@ -22,6 +25,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from oracle import ffo  # noqa: E402
+from oracle import workload as ow  # noqa: E402
 from paper_2402_17993_b200 import problems  # noqa: E402
 
 import dense  # noqa: E402
@@ -47,11 +51,17 @@ def main():
         kind, idx = ffo.build_generators(P.n_qubits, P.n_elec)
         order = np.array(P.plan.order, np.int32)
         rows = []
+        OP = ow.config_problem(cfg, batch=nrows)  # integrals from the oracle alone
+        assert np.array_equal(OP.thetas, P.thetas) and np.array_equal(OP.order, order)
+        ferm_dev = 0.0
         for b in range(nrows):
             want_state = cfg == 1 and b == 0
             r = ffo.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, P.thetas[b], H, want_state=want_state)
             e, im = r[0], r[1]
             assert abs(im) <= 1e-12
+            ef = ffo.energy_fermionic(OP.h, OP.g, OP.n_elec, OP.kind, OP.idx, OP.order, P.thetas[b])
+            assert abs(ef - e) <= 1e-12, (cfg, b, ef, e)
+            ferm_dev = max(ferm_dev, abs(ef - e))
             row = {"theta_canonical": [float(t).hex() for t in P.thetas[b]], "energy": float(e).hex()}
             if want_state:
                 psi = r[2]
@@ -65,7 +75,8 @@ def main():
             rows.append(row)
         out["configs"][str(cfg)] = {
             "n_qubits": P.n_qubits, "n_elec": P.n_elec, "hf": P.hf, "n_gen": P.n_gen, "n_terms": int(len(x)),
-            "ham_sha256": digest(x, z, c), "plan_order_sha256": digest(order), "rows": rows}
+            "ham_sha256": digest(x, z, c), "plan_order_sha256": digest(order),
+            "jw_free_max_abs_dev": ferm_dev, "rows": rows}
         print(f"config {cfg}: {nrows} rows, E0 = {float.fromhex(rows[0]['energy']):.12f}", flush=True)
     path = os.path.join(ROOT, "tests", "golden", "energies.json")
     with open(path, "w") as f:
