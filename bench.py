@@ -179,26 +179,43 @@ def main():
 
     import torch
 
+    # one process per GPU; BENCH_BACKEND=gloo (tests only) lets ranks share a
+    # device (no kernel of one rank waits on another's: the legs have no
+    # data-path collective) and keeps the scalar collectives on the host
+    gpu = local % max(1, torch.cuda.device_count())
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(gpu)
+    cdev = torch.device("cuda", gpu)
+
+    def max_ranks(v):
+        """max over ranks of a host float (device time of the slowest rank)"""
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=cdev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     from paper_2402_17993_b200 import capi
 
-    ctx = capi.Context(local)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    ctx = capi.Context(gpu)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=cdev)
     P, rows = workload(rank)
     B = rows.shape[0]
     plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
     ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
     th_host = P.plan_thetas(rows)
-    th_dev = torch.from_numpy(th_host).to(f"cuda:{local}")
-    e_dev = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # 2x L2
+    th_dev = torch.from_numpy(th_host).to(cdev)
+    e_dev = torch.zeros(B, dtype=torch.float64, device=cdev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=cdev)  # 2x L2
     torch.cuda.synchronize()
 
     def barrier():
@@ -228,16 +245,13 @@ def main():
         step_device()
     barrier()
     l0 = ctx.launches()
-    with Clocks(local) as clk:
+    with Clocks(gpu) as clk:
         barrier()
         ms = timed(step_device, args.steps)
         barrier()
     launches = ctx.launches() - l0
     tot_ms = sum(ms)
-    if dist:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = max_ranks(tot_ms)
     e_first = e_dev.cpu().numpy().copy()
     value = world * B * args.steps / (tot_ms / 1e3)
     # the kernel behind `value`: program statistics for its on-chip roofline
@@ -276,10 +290,7 @@ def main():
     ms_e2e = timed(step_host, args.steps)
     barrier()
     tot_e2e = sum(ms_e2e)
-    if dist:
-        t = torch.tensor([tot_e2e], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_e2e = float(t.item())
+    tot_e2e = max_ranks(tot_e2e)
     e2e = world * B * args.steps / (tot_e2e / 1e3)
     assert np.array_equal(step_host.out, e_first), "device and host paths disagree"
 
@@ -361,16 +372,16 @@ def main():
         execution path selected by FFQ_* knobs read at context creation."""
         saved = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
-        ctx_d = capi.Context(local)
+        ctx_d = capi.Context(gpu)
         for k, v in saved.items():
             if v is None:
                 os.environ.pop(k)
             else:
                 os.environ[k] = v
-        stream_d = torch.cuda.ExternalStream(ctx_d.stream_ptr(), device=torch.device("cuda", local))
+        stream_d = torch.cuda.ExternalStream(ctx_d.stream_ptr(), device=cdev)
         plan_d = capi.Plan(ctx_d, P.n_qubits, *P.plan_arrays())
         ham_d = capi.Hamiltonian(ctx_d, P.n_qubits, *P.ham_arrays())
-        e_d = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
+        e_d = torch.zeros(B, dtype=torch.float64, device=cdev)
         f_d = lambda: capi.energy_batch_device(ctx_d, plan_d, ham_d, P.hf, B, th_dev.data_ptr(), e_d.data_ptr())  # noqa: E731
         f_d()
         ctx_d.synchronize()
@@ -405,8 +416,8 @@ def main():
     rows2 = np.concatenate([np.array(parameter_shift_set(list(t))).reshape(-1, P2.n_gen) for t in P2.thetas])
     plan2 = capi.Plan(ctx, P2.n_qubits, *P2.plan_arrays())
     ham2 = capi.Hamiltonian(ctx, P2.n_qubits, *P2.ham_arrays())
-    th2 = torch.from_numpy(P2.plan_thetas(rows2)).to(f"cuda:{local}")
-    e2 = torch.zeros(rows2.shape[0], dtype=torch.float64, device=f"cuda:{local}")
+    th2 = torch.from_numpy(P2.plan_thetas(rows2)).to(cdev)
+    e2 = torch.zeros(rows2.shape[0], dtype=torch.float64, device=cdev)
     f2 = lambda: capi.energy_batch_device(ctx, plan2, ham2, P2.hf, rows2.shape[0], th2.data_ptr(),  # noqa: E731
                                          e2.data_ptr())
     for _ in range(2):
@@ -419,44 +430,76 @@ def main():
                    "k_sector_eval_real" if si2["real_amplitudes"] else "k_sector_eval", si2["closure_size"])}
 
     # secondary: BASELINE.json config 4 -- FMO batch of 3 monomers (12 q) + 3 dimers
-    # (18 q), one evaluation each through the C++ fragment API, assembled with the
-    # reference's two-body formula; plan/Hamiltonian uploads and closure compiles are
-    # timed separately from the evaluations (first call vs second call)
+    # (18 q). (a) one evaluation each through the C++ fragment API, fragments
+    # sharded over the ranks by cost (shard_by_cost), energies gathered in rank
+    # order and assembled with the reference's two-body formula; (b) one FMO
+    # gradient step = every fragment's parameter-shift set (3 x 235 + 3 x 1121
+    # rows), each fragment's rows split over the ranks (dist.row_range), device-
+    # resident theta, max over ranks.
     import paper_2402_17993_b200 as _ff
+    from paper_2402_17993_b200 import dist as fdist
 
     frags = _pb.fmo_fragment_problems()
-    dev = _ff.Device(local)
+    dev = _ff.Device(gpu)
     t_first = time.perf_counter()
-    en = _ff.evaluate_fragments(dev, frags, 0, 1)
+    e_fmo2, en = fdist.fmo_energy(frags, 3, lambda fr, r, w: _ff.evaluate_fragments(dev, fr, r, w))
     t_first = time.perf_counter() - t_first
-    config4 = {"fragments": len(frags), "e_fmo2": _ff.assemble_fragments(3, en),
-               "first_call_s_incl_compile": t_first,
-               "note": "per-fragment evaluation, sharded by cost over ranks with --gpus N"}
+    owners = fdist.fragment_owners(frags, world)
+    config4 = {"fragments": len(frags), "e_fmo2": e_fmo2, "first_call_s_incl_compile": t_first,
+               "owners": {f.label: int(o) for f, o in zip(frags, owners)},
+               "note": "one evaluation per fragment, fragments sharded by cost over the ranks (shard_by_cost)"}
     del dev
-    # steady state: one FMO gradient step = every fragment's parameter-shift set
-    # (3 x 235 monomer + 3 x 1121 dimer evaluations), programs compiled once,
-    # theta resident on the device, fragments back to back on the context stream
     fsets = []
     for lab, Pf in _pb.fmo_fragments().items():
         rf = np.array(parameter_shift_set(list(Pf.thetas[0]))).reshape(-1, Pf.n_gen)
+        lo4, hi4 = fdist.row_range(rf.shape[0], rank, world)
         plf = capi.Plan(ctx, Pf.n_qubits, *Pf.plan_arrays())
         hmf = capi.Hamiltonian(ctx, Pf.n_qubits, *Pf.ham_arrays())
-        thf = torch.from_numpy(Pf.plan_thetas(rf)).to(f"cuda:{local}")
-        ef = torch.zeros(rf.shape[0], dtype=torch.float64, device=f"cuda:{local}")
-        fsets.append((plf, hmf, Pf.hf, rf.shape[0], thf, ef))
+        thf = torch.from_numpy(Pf.plan_thetas(rf[lo4:hi4])).to(cdev)
+        ef = torch.zeros(max(1, hi4 - lo4), dtype=torch.float64, device=cdev)
+        fsets.append((lab, plf, hmf, Pf.hf, hi4 - lo4, thf, ef, rf.shape[0]))
 
     def fmo_step():
-        for plf, hmf, hf, nb, thf, ef in fsets:
-            capi.energy_batch_device(ctx, plf, hmf, hf, nb, thf.data_ptr(), ef.data_ptr())
+        for _, plf, hmf, hf, nb, thf, ef, _ in fsets:
+            if nb:
+                capi.energy_batch_device(ctx, plf, hmf, hf, nb, thf.data_ptr(), ef.data_ptr())
 
     for _ in range(2):
         fmo_step()
+    barrier()
     ms4 = timed(fmo_step, 3)
-    n4 = sum(f[3] for f in fsets)
-    config4["gradient_step"] = {"evals": n4, "ms_per_step": statistics.mean(ms4),
-                                "evals_per_s": n4 / (statistics.mean(ms4) / 1e3),
-                                "note": "all six fragments' parameter-shift sets, compiled once, device-resident theta"}
+    t4 = statistics.mean(ms4)
+    t4 = max_ranks(t4)
+    grad = {lab: fdist.gather_rows(ef.cpu().numpy()[:nb], ntot) if dist else ef.cpu().numpy()[:nb]
+            for lab, _, _, _, nb, _, ef, ntot in fsets}
+    n4 = sum(f[7] for f in fsets)
+    config4["gradient_step"] = {
+        "evals": n4, "ms_per_step": t4, "evals_per_s": n4 / (t4 / 1e3),
+        "e_fmo2_from_step": float(_ff.assemble_fragments(3, {k: float(v[0]) for k, v in grad.items()})),
+        "note": "all six fragments' parameter-shift sets, each split over the ranks by rows (dist.row_range), "
+                "compiled once, device-resident theta, max over ranks"}
     del fsets
+
+    # strong scaling: ONE config-3 gradient set (rank 0's 1121 rows)
+    # split over the ranks by dist.row_range, no data-path collective, energies
+    # gathered in rank order; must equal the one-GPU energies bit for bit
+    P0, rows0 = workload(0)
+    lo_s, hi_s = fdist.row_range(rows0.shape[0], rank, world)
+    th_s = torch.from_numpy(P0.plan_thetas(rows0[lo_s:hi_s])).to(cdev)
+    e_s = torch.zeros(max(1, hi_s - lo_s), dtype=torch.float64, device=cdev)
+    f_s = lambda: capi.energy_batch_device(ctx, plan, ham, P0.hf, hi_s - lo_s, th_s.data_ptr(),  # noqa: E731
+                                           e_s.data_ptr())
+    f_s()
+    barrier()
+    ms_s = timed(f_s, args.steps)
+    t_s = statistics.mean(ms_s)
+    t_s = max_ranks(t_s)
+    e_all = fdist.gather_rows(e_s.cpu().numpy()[:hi_s - lo_s], rows0.shape[0]) if dist else e_s.cpu().numpy()
+    strong = {"evals": int(rows0.shape[0]), "ms_per_step": t_s, "evals_per_s": rows0.shape[0] / (t_s / 1e3),
+              "rows_per_rank": hi_s - lo_s,
+              "bitwise_equal_to_unsplit": bool(np.array_equal(e_all, e_first)) if rank == 0 else None,
+              "note": "scaling strong: one 1121-row gradient set split over the ranks (dist.row_range), "
+                      "max over ranks; compare ms_per_step across --gpus N"}
 
     # secondary: BASELINE.json config 5 (32 qubits, 16 electrons, all singles + the
     # first 2000 doubles, 5000 random Pauli terms) on this GPU: one energy
@@ -467,8 +510,8 @@ def main():
         t5 = time.perf_counter()
         plan5 = capi.Plan(ctx, P5.n_qubits, *P5.plan_arrays())
         ham5 = capi.Hamiltonian(ctx, P5.n_qubits, *P5.ham_arrays())
-        th5 = torch.from_numpy(P5.plan_thetas()).to(f"cuda:{local}")
-        e5 = torch.zeros(1, dtype=torch.float64, device=f"cuda:{local}")
+        th5 = torch.from_numpy(P5.plan_thetas()).to(cdev)
+        e5 = torch.zeros(1, dtype=torch.float64, device=cdev)
         f5 = lambda: capi.energy_batch_device(ctx, plan5, ham5, P5.hf, 1, th5.data_ptr(), e5.data_ptr())  # noqa: E731
         f5()
         ctx.synchronize()
@@ -519,7 +562,8 @@ def main():
             "secondary": {"config3_latency_and_b64": latency, "config3_complex128_program": complex_path,
                           "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
-                          "config4_fmo": config4, "config5_32q": config5, "rotation_run_28q": rotation_run,
+                          "config4_fmo": config4, "config3_strong_scaling": strong,
+                          "config5_32q": config5, "rotation_run_28q": rotation_run,
                           "rotation_pass_18q_b256": rot18},
             "clocks": clk.summary(),
         }
@@ -531,9 +575,15 @@ def main():
         # load (the Blackwell L1/smem datapath).
         cs = line["clocks"]
         sm_hz = (cs.get("sm_mhz") or 1920) * 1e6
-        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        n_sm = torch.cuda.get_device_properties(gpu).multi_processor_count
         amp_b = 8 if sector["real_amplitudes"] else 16
-        smem_bytes = amp_b * (4 * sector["generator_pairs"] + 2 * sector["expectation_pairs"])
+        # amplitude bytes the program moves through the L1/shared datapath per
+        # evaluation: a generator pair 2 loads + 2 stores; a generic expectation
+        # pair 2 loads; a block pair 1 load (the anchor is held); a clique
+        # lane-row 12 loads (6 + 6 amplitudes for up to 30 pairs)
+        generic = sector["expectation_pairs"] - sector["block_pairs"] - sector["clique_pairs"]
+        smem_bytes = amp_b * (4 * sector["generator_pairs"] + 2 * generic + sector["block_pairs"]
+                              + 12 * sector["clique_lane_rows"])
         smem_ach = smem_bytes * value / world / 1e9
         smem_peak = 128 * n_sm * sm_hz / 1e9
         line["roofline_value_kernel"] = {

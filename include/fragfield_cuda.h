@@ -57,6 +57,7 @@ typedef struct ffq_ctx_s* ffq_ctx_t;
 typedef struct ffq_ham_s* ffq_ham_t;
 typedef struct ffq_plan_s* ffq_plan_t;
 typedef struct ffq_state_s* ffq_state_t;
+typedef struct ffq_multi_s* ffq_multi_t;
 
 /* ---- library / context ---------------------------------------------------- */
 int ffq_version(void);
@@ -130,8 +131,9 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
  * out[10] amplitude slots (padded product layout; = out[0] otherwise),
  * out[11] expectation pairs held by alpha-beta cliques, out[12] clique warp
  * tasks, out[13] modelled extra shared wavefronts per clique row (bank
- * conflicts summed over half-warp tasks; 0 = conflict-free).
- * out must hold 14 values.
+ * conflicts summed over half-warp tasks; 0 = conflict-free), out[14] clique
+ * lane-rows (12 amplitude loads each).
+ * out must hold 15 values.
  * FFQ_EINVAL when the closure does not fit the sector evaluator (the other
  * paths then run) or FFQ_SECTOR=0. */
 int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, int64_t* out);
@@ -245,6 +247,37 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
                        const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
                        const double* psi, double* out);
+
+/* ---- multi-GPU, independent units (BASELINE configs 2-4) ---- */
+/* One context per device of `devices` (one node); every call runs one host
+ * thread per device, with no data-path collective: the units (theta rows,
+ * fragments) are independent, and a row's energy is bitwise the same on any
+ * device and in any batch, so results equal the one-device call bit for bit
+ * (SPEC.md:455-457 worker-count independence). Replaces the fragment driver's
+ * concurrent per-fragment VQE evaluations (`--jobs` :621) that
+ * feed FMOEnergyLedger (proj/core/src/fmo.cpp:46-48). */
+int ffq_multi_create(const int* devices, int n_dev, ffq_multi_t* out);
+int ffq_multi_destroy(ffq_multi_t m);
+int ffq_multi_device_count(ffq_multi_t m, int* n_dev);
+const char* ffq_multi_last_error(ffq_multi_t m);
+/* Plan (as ffq_plan_upload) + Hamiltonian (as ffq_ham_upload) uploaded to
+ * every device; *problem_out = its id for the calls below. */
+int ffq_multi_problem_upload(ffq_multi_t m, int n_qubits, int n_gen, const int64_t* term_off,
+                             const uint64_t* px, const uint64_t* pz, const double* pc_re,
+                             const double* pc_im, int64_t n_terms, const uint64_t* hx,
+                             const uint64_t* hz, const double* hc_re, const double* hc_im,
+                             int* problem_out);
+/* ffq_energy_batch over all devices: rows split into contiguous blocks
+ * (sizes differ by at most one), written back in row order. */
+int ffq_multi_energy_batch(ffq_multi_t m, int problem, uint64_t hf_bits, int batch,
+                           const double* theta, double* e_out);
+/* n_units independent units (problem[u], hf_bits[u], batch[u] rows of
+ * theta[u] -> e_out[u]), e.g. FMO monomers and dimers with their gradient
+ * sets, assigned to devices longest-first by cost 2^n x (generators + flip-
+ * mask groups) x rows; device_out[u] (optional) receives the assignment. */
+int ffq_multi_energy_units(ffq_multi_t m, int n_units, const int* problem, const uint64_t* hf_bits,
+                           const int* batch, const double* const* theta, double* const* e_out,
+                           int* device_out);
 
 #ifdef __cplusplus
 }

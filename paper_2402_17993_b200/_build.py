@@ -39,7 +39,7 @@ CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-I" + INC, "-I/usr/local/cud
 CUDA_SOURCES = [os.path.join(CSRC, "ffq_capi.cu")]
 CUDA_DEPS = [os.path.join(CSRC, f) for f in ("ffq_compile.hpp", "ffq_kernels.cuh", "ffq_sparse.cuh",
                                                "ffq_shard.inl", "ffq_sector.cuh", "ffq_krylov.inl",
-                                               "ffq_compact.inl")] + [
+                                               "ffq_compact.inl", "ffq_multi.inl")] + [
     os.path.join(INC, "fragfield_cuda.h")]
 HOST_SOURCES = [os.path.join(CSRC, "host", "fragfield_host.cpp")]
 HOST_DEPS = [os.path.join(INC, "fragfield", f) for f in os.listdir(os.path.join(INC, "fragfield"))]

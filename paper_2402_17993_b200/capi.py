@@ -77,6 +77,18 @@ _SIGS = {
                                      _f64p, _f64p, C.c_uint64, _f64p, _f64p]),
     "ffq_sector_info": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i64p]),
     "ffq_sector_state": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, _f64p, C.POINTER(C.c_double)]),
+    "ffq_multi_create": (C.c_int, [np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), C.c_int,
+                                   C.POINTER(_vp)]),
+    "ffq_multi_destroy": (C.c_int, [_vp]),
+    "ffq_multi_device_count": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "ffq_multi_last_error": (C.c_char_p, [_vp]),
+    "ffq_multi_problem_upload": (C.c_int, [_vp, C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.c_int64,
+                                           _u64p, _u64p, _f64p, _f64p, C.POINTER(C.c_int)]),
+    "ffq_multi_energy_batch": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_int, _f64p, _f64p]),
+    "ffq_multi_energy_units": (C.c_int, [_vp, C.c_int, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                         _u64p, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                         np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]),
 }
 
 _lib = None
@@ -244,7 +256,7 @@ def energy_batch_device(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int
 SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expectation_pairs",
                     "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
                     "real_amplitudes", "block_pairs", "slots", "clique_pairs", "clique_warp_tasks",
-                    "clique_conflicts")
+                    "clique_conflicts", "clique_lane_rows")
 
 
 def sector_state(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, theta, n_qubits: int):
@@ -259,7 +271,7 @@ def sector_state(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, theta
 
 def sector_info(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int) -> dict:
     """Statistics of the support-closure program energy_batch runs (ffq_sector_info)."""
-    out = np.zeros(14, np.int64)
+    out = np.zeros(15, np.int64)
     check(lib().ffq_sector_info(ctx.h, plan.h, ham.h, hf_bits, out), ctx.h)
     return dict(zip(SECTOR_INFO_KEYS, (int(v) for v in out)))
 
@@ -415,3 +427,63 @@ def energy_exact(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits, theta, tol
     check(lib().ffq_energy_exact(ctx.h, plan.h, ham.h, hf_bits, np.ascontiguousarray(theta, np.float64).ravel(),
                                  tol, C.byref(e)), ctx.h)
     return e.value
+
+
+class Multi:
+    """One context per device (ffq_multi_*): independent units sharded over the
+    devices of one node by host threads, no collective; results equal the
+    one-device call bit for bit."""
+
+    def __init__(self, devices):
+        devs = np.ascontiguousarray(devices, np.int32)
+        h = _vp()
+        self._lib = lib()
+        rc = self._lib.ffq_multi_create(devs, len(devs), C.byref(h))
+        if rc != 0:
+            check(rc)
+        self.h = h
+
+    def _check(self, rc):
+        if rc == FFQ_OK:
+            return
+        msg = self._lib.ffq_multi_last_error(self.h).decode()
+        if rc in (FFQ_EINVAL, FFQ_ENONHERMITIAN):
+            raise ContractViolation(msg)
+        raise DeviceError(f"[{rc}] {msg}")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.ffq_multi_destroy(self.h)
+            self.h = None
+
+    def device_count(self):
+        n = C.c_int()
+        self._check(self._lib.ffq_multi_device_count(self.h, C.byref(n)))
+        return n.value
+
+    def upload(self, n, plan_arrays, ham_arrays):
+        off, px, pz, pc = plan_arrays
+        px, pz, pre, pim = _terms(px, pz, pc)
+        hx, hz, hre, him = _terms(*ham_arrays)
+        pid = C.c_int()
+        self._check(self._lib.ffq_multi_problem_upload(self.h, n, len(off) - 1, np.ascontiguousarray(off, np.int64),
+                                                       px, pz, pre, pim, len(hx), hx, hz, hre, him, C.byref(pid)))
+        return pid.value
+
+    def energy_batch(self, problem, hf_bits, theta):
+        th = np.ascontiguousarray(np.atleast_2d(theta), np.float64)
+        e = np.zeros(th.shape[0])
+        self._check(self._lib.ffq_multi_energy_batch(self.h, problem, hf_bits, th.shape[0], th, e))
+        return e
+
+    def energy_units(self, problems_, hf_bits, thetas):
+        ths = [np.ascontiguousarray(np.atleast_2d(t), np.float64) for t in thetas]
+        es = [np.zeros(t.shape[0]) for t in ths]
+        n = len(ths)
+        tp = (C.c_void_p * n)(*[t.ctypes.data for t in ths])
+        ep = (C.c_void_p * n)(*[e.ctypes.data for e in es])
+        dev = np.zeros(n, np.int32)
+        self._check(self._lib.ffq_multi_energy_units(
+            self.h, n, np.ascontiguousarray(problems_, np.int32), np.ascontiguousarray(hf_bits, np.uint64),
+            np.array([t.shape[0] for t in ths], np.int32), tp, ep, dev))
+        return es, dev.tolist()

@@ -1206,6 +1206,9 @@ int ffq_sector_info(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_b
     out[11] = S.cq_pairs;
     out[12] = (int64_t)(S.cq_desc.size() / 128);
     out[13] = S.cq_conflicts;
+    int64_t lane_rows = 0;  // sum over clique lanes of their rows (12 amplitude loads each)
+    for (size_t l = 0; l < S.cq_desc.size() / 4; ++l) lane_rows += S.cq_desc[4 * l + 3] - S.cq_desc[4 * l + 2];
+    out[14] = lane_rows;
     return FFQ_OK;
   });
 }
@@ -1619,3 +1622,4 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
 
 #include "ffq_shard.inl"
 #include "ffq_krylov.inl"
+#include "ffq_multi.inl"

@@ -45,3 +45,35 @@ def test_fmo_sharded_equals_single_and_assembles(fmo):
     assert abs(e - (dim - mono)) <= 1e-12  # N_f = 3: E = sum E_IJ - sum E_I
     fmo2 = mono + sum(energies[a + b] - energies[a] - energies[b] for a, b in (("2", "1"), ("3", "1"), ("3", "2")))
     assert abs(e - fmo2) <= 1e-10  # FMO2 form (BASELINE.json config 4)
+
+
+def test_multi_capi_equals_one_context_bitwise():
+    """ffq_multi_* (one host thread per device, rows / units sharded, no
+    collective) on the devices of this box against one context: the config-3
+    gradient rows (ffq_multi_energy_batch) and the config-4 fragments' shift
+    sets (ffq_multi_energy_units, assigned by cost) are bit-identical."""
+    import paper_2402_17993_b200 as ff
+    from paper_2402_17993_b200 import capi, problems
+
+    n_dev = ff.Device.count()
+    m = capi.Multi(list(range(n_dev)))
+    assert m.device_count() == n_dev
+    P = problems.config_problem(3)
+    rows = np.array(ff.parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)[:300]
+    pid = m.upload(P.n_qubits, P.plan_arrays(), P.ham_arrays())
+    e_multi = m.energy_batch(pid, P.hf, P.plan_thetas(rows))
+    ctx = capi.Context(0)
+    plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
+    assert np.array_equal(e_multi, capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas(rows)))
+    frs = list(problems.fmo_fragments().values())
+    pids = [m.upload(F.n_qubits, F.plan_arrays(), F.ham_arrays()) for F in frs]
+    ths = [F.plan_thetas(np.array(ff.parameter_shift_set(list(F.thetas[0]))).reshape(-1, F.n_gen)[:40]) for F in frs]
+    es, devs = m.energy_units(pids, [F.hf for F in frs], ths)
+    assert all(0 <= d < n_dev for d in devs)
+    for F, th, e in zip(frs, ths, es):
+        pl = capi.Plan(ctx, F.n_qubits, *F.plan_arrays())
+        hm = capi.Hamiltonian(ctx, F.n_qubits, *F.ham_arrays())
+        assert np.array_equal(e, capi.energy_batch(ctx, pl, hm, F.hf, th))
+    with pytest.raises(ff.ContractViolation):
+        capi.Multi([0, 0])

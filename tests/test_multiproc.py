@@ -84,6 +84,52 @@ def test_fmo_and_rows_sharded_over_two_ranks():
         assert rows == [0.5 * i for i in range(10)]
 
 
+def _rows_worker(rank, world, port, q):
+    """One config-1 parameter-shift set split over the ranks by the product's
+    dist.row_range; each rank evaluates its block (oracle compute: no device
+    here), dist.gather_rows reassembles it in rank order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ffo
+
+        ffo.set_threads(1)  # ranks share the host cores (OpenMP would oversubscribe)
+        P = problems.config_problem(1)
+        rows = np.array(ff.parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)
+        lo, hi = fdist.row_range(rows.shape[0], rank, world)
+        H = ffo.PauliSum.from_terms(P.n_qubits, *P.ham_arrays())
+        kind, idx = ffo.build_generators(P.n_qubits, P.n_elec)
+        order = np.array(P.plan.order, np.int32)
+        mine = [ffo.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, rows[r], H)[0] for r in range(lo, hi)]
+        q.put((rank, fdist.gather_rows(np.array(mine), rows.shape[0]).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gradient_rows_split_over_ranks_bitwise(world):
+    from oracle import ffo
+
+    P = problems.config_problem(1)
+    rows = np.array(ff.parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)
+    H = ffo.PauliSum.from_terms(P.n_qubits, *P.ham_arrays())
+    kind, idx = ffo.build_generators(P.n_qubits, P.n_elec)
+    order = np.array(P.plan.order, np.int32)
+    full = [ffo.energy_trotter(P.n_qubits, P.n_elec, kind, idx, order, r, H)[0] for r in rows]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, got in res:
+        assert got == full  # bitwise, in row order, on every rank
+
+
 def test_shard_by_cost_is_balanced_and_deterministic():
     costs = [1.0, 1.0, 1.0, 300.0, 300.0, 300.0]
     assert ff.shard_by_cost(costs, 1) == [0] * 6
