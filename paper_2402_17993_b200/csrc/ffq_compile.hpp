@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -27,6 +28,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace ffq {
@@ -1092,20 +1094,20 @@ inline void compile_cliques(SectorProgram& S, const std::vector<uint32_t>& list,
   for (auto& [xa, cs] : by_xa) {
     Group g;
     g.xa = xa;
-    std::map<uint32_t, uint32_t> rix;
-    std::map<std::pair<uint32_t, uint32_t>, uint32_t> kix;
+    // dense index tables (alpha index -> row, (beta, beta') -> key): no maps on the 3 M pairs
+    std::vector<int32_t> rix(S.n_alpha, -1), kix((size_t)NB * NB, -1);
     std::vector<std::pair<uint32_t, uint32_t>> keys;
     for (const Cand& c : cs) {
-      if (!rix.count(c.a)) { rix[c.a] = (uint32_t)g.rows.size(); g.rows.push_back(c.a); }
-      const auto key = std::make_pair(c.b, c.b2);
-      if (!kix.count(key)) { kix[key] = (uint32_t)keys.size(); keys.push_back(key); }
+      if (rix[c.a] < 0) { rix[c.a] = (int32_t)g.rows.size(); g.rows.push_back(c.a); }
+      int32_t& kk = kix[(size_t)c.b * NB + c.b2];
+      if (kk < 0) { kk = (int32_t)keys.size(); keys.push_back({c.b, c.b2}); }
     }
     const size_t R = g.rows.size(), K = keys.size();
     if (R * K != cs.size()) continue;  // not every (row, key): some weights vanish
     std::vector<double> W(R * K, 0.0);
     std::vector<uint8_t> have(R * K, 0);
     for (const Cand& c : cs) {
-      const size_t s = (size_t)rix[c.a] * K + kix[{c.b, c.b2}];
+      const size_t s = (size_t)rix[c.a] * K + (size_t)kix[(size_t)c.b * NB + c.b2];
       if (have[s]) goto reject;
       have[s] = 1;
       W[s] = c.w;
@@ -1122,8 +1124,8 @@ inline void compile_cliques(SectorProgram& S, const std::vector<uint32_t>& list,
         }
       }
       for (size_t k = 0; k < K; ++k) {
-        auto it = kix.find({keys[k].second, keys[k].first});
-        if (it == kix.end() || std::fabs(C[it->second] - C[k]) > 1e-13 * std::fabs(C[k])) goto reject;
+        const int32_t kt = kix[(size_t)keys[k].second * NB + keys[k].first];
+        if (kt < 0 || std::fabs(C[kt] - C[k]) > 1e-13 * std::fabs(C[k])) goto reject;
         g.C[keys[k]] = C[k];
       }
       std::set<uint64_t> ts;
@@ -1307,6 +1309,15 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
   if (P.n_string_ops() > 0) { S.why = "plan has non-fused generators"; return S; }
   if (n_parts != 1 && n_parts != 2 && n_parts != 4 && n_parts != 8) { S.why = "parts must be 1, 2, 4 or 8"; return S; }
   const size_t dim = size_t(1) << n;
+  const bool dbg_t = std::getenv("FFQ_DEBUG") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!dbg_t) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ffq] compile_sector %-22s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   std::vector<int32_t> idx(dim, -1);
   std::vector<uint32_t> list{(uint32_t)hf};
   idx[hf] = 0;
@@ -1338,29 +1349,48 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       if (list.size() > max_size) { S.why = "support closure too large"; return S; }
     }
   }
+  stage("closure");
   // expectation pairs in k space with their class sums f(m)
   struct EP { uint32_t m; int g, p; double fr, fi; };
   std::vector<EP> ek;
-  for (size_t gi = 0; gi < H.groups.size(); ++gi) {
-    const auto& d = H.groups[gi];
-    uint64_t Q = 0;
-    for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
-    for (int p = 0; p < d.nact; ++p) {
-      const uint64_t pb = H.act_bits[d.act_off + p];
-      for (uint32_t m : list) {
-        if ((m & Q) != pb) continue;
-        if (pos[m ^ (uint32_t)d.x] < 0) continue;
-        double fr = 0.0, fi = 0.0;
-        for (int o = 0; o < d.ncls; ++o) {
-          const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
-          fr += sg * H.cls_f[2 * (d.val_off + o * d.nact + p)];
-          fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
+  {
+    // groups in contiguous chunks over host threads, concatenated in group order
+    const size_t ng = H.groups.size();
+    const int nth = (int)std::max<size_t>(1, std::min<size_t>({(size_t)std::thread::hardware_concurrency(), 16,
+                                                               (ng + 63) / 64}));
+    std::vector<std::vector<EP>> part((size_t)nth);
+    auto work = [&](int t) {
+      for (size_t gi = ng * t / nth; gi < ng * (t + 1) / nth; ++gi) {
+        const auto& d = H.groups[gi];
+        uint64_t Q = 0;
+        for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
+        for (int p = 0; p < d.nact; ++p) {
+          const uint64_t pb = H.act_bits[d.act_off + p];
+          for (uint32_t m : list) {
+            if ((m & Q) != pb) continue;
+            if (pos[m ^ (uint32_t)d.x] < 0) continue;
+            double fr = 0.0, fi = 0.0;
+            for (int o = 0; o < d.ncls; ++o) {
+              const double sg = (__builtin_popcountll(m & H.cls_z[d.cls_off + o]) & 1) ? -1.0 : 1.0;
+              fr += sg * H.cls_f[2 * (d.val_off + o * d.nact + p)];
+              fi += sg * H.cls_f[2 * (d.val_off + o * d.nact + p) + 1];
+            }
+            if (fr == 0.0 && fi == 0.0) continue;
+            part[t].push_back({m, (int)gi, p, fr, fi});
+          }
         }
-        if (fr == 0.0 && fi == 0.0) continue;
-        ek.push_back({m, (int)gi, p, fr, fi});
       }
-    }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    size_t tot = 0;
+    for (auto& v : part) tot += v.size();
+    ek.reserve(tot);
+    for (auto& v : part) ek.insert(ek.end(), v.begin(), v.end());
   }
+  stage("expectation pairs");
   S.size = (uint32_t)list.size();
   if (S.size > 32767) { S.why = "support closure exceeds 15-bit indices"; return S; }
   // split S over 2^s CTAs by the parities of s qubit masks M_1..M_s (part bit
@@ -1422,6 +1452,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     if (best < 0) { S.why = "no split of the support closure fits the CTAs"; return S; }
     masks.push_back(cands[best]);
   }
+  stage("split");
   if (n_parts == 1 && S.size > max_part) { S.why = "support closure does not fit one CTA"; return S; }
   S.n_parts = n_parts;
   S.split_masks = masks;
@@ -1512,6 +1543,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     load[o] += oi == oj ? 2 : 3;  // a cross pair costs one slow DSMEM access
     return o;
   };
+  stage("layout");
   S.gen_off.assign(1, 0);
   for (int op = 0; op < n_ops; ++op) {
     const FusedDesc& d = P.fused[P.op_idx[op]];
@@ -1540,6 +1572,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
     }
   }
+  stage("generator pairs");
   for (const auto& e : ek)
     if (e.fi != 0.0) S.f_real = false;
   S.zero_slot.resize((size_t)n_parts);
@@ -1581,7 +1614,9 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     if (cliques) {
       // alpha-beta pairs that factorise go to the cliques, the rest to the blocks
       std::vector<uint8_t> in_clique(ek.size(), 0);
+      stage("pair lists");
       compile_cliques(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_clique);
+      stage("cliques");
       std::vector<std::pair<uint32_t, uint32_t>> ij2;
       std::vector<double> fv2;
       std::vector<size_t> back;
@@ -1595,6 +1630,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       compile_blocks(S, list, ij, fv, slot_of, ia_of, ib_of, amask, in_block);
     }
   }
+  stage("cliques+blocks");
   std::vector<uint8_t> eown(ek.size());
   {  // balance: with the chunk buffer a cross pair costs about what a local one does
     std::vector<int64_t> load((size_t)n_parts, 0);
@@ -1722,6 +1758,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
     }
     S.sec_off.push_back((int32_t)S.sections.size());
   }
+  stage("generic rows");
   if (S.f_real) {
     S.row_fim.clear();
     S.pf_im.clear();
@@ -1785,6 +1822,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       S.blk_warp.insert(S.blk_warp.end(), {r0, (int32_t)(S.blk_stream.size() / 32), f0, 0});
     }
   }
+  stage("warp streams");
   S.ok = true;
   return S;
 }

@@ -939,6 +939,12 @@ OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, con
   for (int i = 0; i < P; ++i) Hinv[(size_t)i * P + i] = 1.0;
   double fx = energy(x);
   std::vector<double> g = grad(x);
+  auto gmax = [&]() {
+    double v = 0.0;
+    for (double gi : g) v = std::max(v, std::abs(gi));
+    return v;
+  };
+  bool reset_tried = false;  // a failed line search first retries steepest descent
   while (R.n_evals < opts.max_evals) {
     ++R.n_iterations;
     std::vector<double> d(P, 0.0);
@@ -961,14 +967,24 @@ OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, con
       if (fn <= fx + 1e-4 * t * slope) break;
       t *= 0.5;
     }
-    if (!(fn < fx)) { R.converged = true; break; }
+    if (!(fn < fx)) {
+      // no decrease along d after 40 halvings: a stationary point within the
+      // objective's resolution only if the gradient vanishes there; otherwise
+      // restart from steepest descent once, then stop UNconverged
+      if (gmax() <= 1e-6) { R.converged = true; break; }
+      if (reset_tried) break;
+      reset_tried = true;
+      std::fill(Hinv.begin(), Hinv.end(), 0.0);
+      for (int i = 0; i < P; ++i) Hinv[(size_t)i * P + i] = 1.0;
+      continue;
+    }
+    reset_tried = false;
     std::vector<double> gn = grad(xn), s(P), y(P);
     for (int i = 0; i < P; ++i) { s[i] = xn[i] - x[i]; y[i] = gn[i] - g[i]; }
     const double df = fx - fn;
     x = xn; fx = fn; g = gn;
-    double gnorm = 0.0;
-    for (double v : g) gnorm = std::max(gnorm, std::abs(v));
-    if (df <= opts.ftol || gnorm <= 1e-6) { R.converged = true; break; }
+    // |dE| <= ftol on an accepted step, or a vanishing gradient
+    if (df <= opts.ftol || gmax() <= 1e-6) { R.converged = true; break; }
     double sy = 0.0;
     for (int i = 0; i < P; ++i) sy += s[i] * y[i];
     if (sy > 1e-14) {

@@ -102,3 +102,29 @@ def test_cpp_facade_exact_references():
     e_tr = ff.energy_trotter(dev, list(P.thetas[0]), plan, H, P.hf)
     e_ex = ff.energy_exact(dev, list(P.thetas[0]), plan, H, P.hf)
     assert g.dimension == 36 and e_tr >= g.energy - 1e-10 and e_ex >= g.energy - 1e-10
+
+
+def test_config2_vqe_converges_to_ftol_and_is_variational():
+    """BASELINE config 2 (12 qubits): BFGS on batched exact gradients through
+    the C-ABI converges to ftol 1e-8 (|dE| of an accepted step)
+    below the HF energy and above E_CASCI - 1e-10."""
+    import paper_2402_17993_b200 as ff
+
+    P = problems.config_problem(2)
+    ctx = capi.Context(0)
+    plan = capi.Plan(ctx, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, P.n_qubits, *P.ham_arrays())
+    order = np.asarray(P.plan.order)
+
+    def fb(X, B):
+        X = np.asarray(X).reshape(B, P.n_gen)
+        return list(capi.energy_batch(ctx, plan, ham, P.hf, np.ascontiguousarray(X[:, order])))
+
+    opts = ff.OptimizerOptions()
+    opts.ftol = 1e-8
+    opts.max_evals = 5_000_000
+    r = ff.bfgs_minimize(fb, list(P.thetas[0]), opts)
+    e_hf = fb(np.zeros(P.n_gen), 1)[0]
+    e_cas = capi.lanczos_ground(ctx, ham, P.hf)[0]
+    assert r.converged
+    assert e_cas - 1e-10 <= r.energy < e_hf

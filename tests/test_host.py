@@ -289,3 +289,20 @@ def test_rotation_groups_cover_and_partition(n, t, seed):
                     off = (b[0] if c & 1 else 0) ^ (b[1] if c & 2 else 0) ^ (b[2] if c & 4 else 0)
                     seen[k ^ off] += 1
             assert np.all(seen == 1)
+
+
+def test_bfgs_line_search_failure_is_not_convergence():
+    """A line search that finds no decrease while the gradient is not small
+    (here: the objective lies about its own gradient, so BFGS walks uphill)
+    must come back UNconverged (best-so-far flagged
+    unconverged), after one steepest-descent restart -- not as converged."""
+    def fb(X, B):
+        X = np.asarray(X).reshape(B, 2)
+        if B == 1:  # energies: a bowl at 0
+            return list(np.sum(X ** 2, axis=1))
+        # gradient rows (4 per parameter): make the four-term rule return -grad
+        return list(-np.sum(np.sin(X) ** 2, axis=1))
+
+    r = ff.bfgs_minimize(fb, [0.5, -0.3])
+    assert not r.converged
+    assert r.energy <= 0.5 ** 2 + 0.3 ** 2  # best-so-far, never worse than the start
