@@ -54,6 +54,28 @@ void write_fcidump(const std::string& path, const SpatialIntegrals& ints, int n_
 /// Throws ParseError (with the line number) on a malformed file.
 Fcidump read_fcidump(const std::string& path);
 
+/// AO -> MO transformation: h_mo = C^T (h_ao + V_esp) C and
+/// (pq|rs)_mo = sum C_mp C_nq C_lr C_ss' (mn|ls')_ao as four quarter
+/// transformations, O(N^5). ao: n AO functions (h n x n, g n^4 chemists'
+/// order, v_esp n x n or empty: the embedding operator folded into the
+/// one-electron part); C: n x m row-major, column j = MO j. e_const is kept.
+SpatialIntegrals ao_to_mo(const SpatialIntegrals& ao, const std::vector<double>& C, int m,
+                          const std::vector<double>& v_esp = {});
+
+/// Frozen-core contraction of the n_frozen lowest MOs (the
+/// first n_frozen, orbitals in energy order):
+///   h_eff_pq = h_pq + sum_c [2 (pq|cc) - (pc|cq)],
+///   E_frozen = sum_c 2 h_cc + sum_cd [2 (cc|dd) - (cd|dc)],
+/// active integrals over MOs n_frozen .. m-1, e_const += E_frozen, and the
+/// active electron count n_elec - 2 n_frozen. ContractViolation when
+/// n_frozen exceeds the occupied orbitals (n_elec / 2) or is negative.
+struct FrozenCore {
+  SpatialIntegrals active;  // e_const includes E_frozen
+  double e_frozen = 0.0;
+  int n_elec_active = 0;
+};
+FrozenCore freeze_core(const SpatialIntegrals& mo, int n_frozen, int n_elec);
+
 /// Uniform draws U(lo, hi) from mt19937_64(seed), same value mapping.
 std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double hi);
 

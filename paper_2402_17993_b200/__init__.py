@@ -42,6 +42,7 @@ from .lib._fragfield import (  # noqa: E402,F401
     Statevector,
     TrotterPlan,
     assemble_fragments,
+    ao_to_mo,
     assemble_two_body,
     bfgs_minimize,
     build_generators,
@@ -53,6 +54,7 @@ from .lib._fragfield import (  # noqa: E402,F401
     GroundState,
     lanczos_ground,
     exact_gradient_from_energies,
+    freeze_core,
     fragment_cost,
     exact_gradient_set,
     hf_bits,

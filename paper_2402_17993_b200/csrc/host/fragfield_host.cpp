@@ -410,6 +410,100 @@ std::vector<double> uniform_vector(uint64_t seed, int count, double lo, double h
   return v;
 }
 
+SpatialIntegrals ao_to_mo(const SpatialIntegrals& ao, const std::vector<double>& C, int m,
+                          const std::vector<double>& v_esp) {
+  const int n = ao.m;
+  const size_t N = (size_t)n;
+  if (n < 1 || m < 1 || m > n) throw ContractViolation("ao_to_mo: need 1 <= m <= n AO functions");
+  if (ao.h.size() != N * N || ao.g.size() != N * N * N * N || C.size() != N * (size_t)m)
+    throw ContractViolation("ao_to_mo: integral or coefficient shapes");
+  if (!v_esp.empty() && v_esp.size() != N * N) throw ContractViolation("ao_to_mo: v_esp shape");
+  const size_t M = (size_t)m;
+  SpatialIntegrals mo;
+  mo.m = m;
+  mo.e_const = ao.e_const;
+  // one-electron: C^T (h + V) C
+  std::vector<double> hv(ao.h);
+  if (!v_esp.empty())
+    for (size_t k = 0; k < N * N; ++k) hv[k] += v_esp[k];
+  std::vector<double> t1(N * M, 0.0);
+  for (size_t a = 0; a < N; ++a)
+    for (size_t b = 0; b < N; ++b)
+      for (size_t q = 0; q < M; ++q) t1[a * M + q] += hv[a * N + b] * C[b * M + q];
+  mo.h.assign(M * M, 0.0);
+  for (size_t p = 0; p < M; ++p)
+    for (size_t a = 0; a < N; ++a)
+      for (size_t q = 0; q < M; ++q) mo.h[p * M + q] += C[a * M + p] * t1[a * M + q];
+  // two-electron: four quarter transformations, one index at a time
+  // g1[a][b][c][s] = sum_d g[a][b][c][d] C[d][s], then c -> r, b -> q, a -> p
+  std::vector<double> g1(N * N * N * M, 0.0);
+  for (size_t abc = 0; abc < N * N * N; ++abc)
+    for (size_t d = 0; d < N; ++d) {
+      const double v = ao.g[abc * N + d];
+      if (v == 0.0) continue;
+      for (size_t s2 = 0; s2 < M; ++s2) g1[abc * M + s2] += v * C[d * M + s2];
+    }
+  std::vector<double> g2(N * N * M * M, 0.0);  // [a][b][r][s]
+  for (size_t ab = 0; ab < N * N; ++ab)
+    for (size_t c = 0; c < N; ++c)
+      for (size_t r = 0; r < M; ++r) {
+        const double cr = C[c * M + r];
+        if (cr == 0.0) continue;
+        for (size_t s2 = 0; s2 < M; ++s2) g2[(ab * M + r) * M + s2] += cr * g1[(ab * N + c) * M + s2];
+      }
+  std::vector<double> g3(N * M * M * M, 0.0);  // [a][q][r][s]
+  for (size_t a = 0; a < N; ++a)
+    for (size_t b = 0; b < N; ++b)
+      for (size_t q = 0; q < M; ++q) {
+        const double bq = C[b * M + q];
+        if (bq == 0.0) continue;
+        for (size_t rs = 0; rs < M * M; ++rs) g3[(a * M + q) * M * M + rs] += bq * g2[(a * N + b) * M * M + rs];
+      }
+  mo.g.assign(M * M * M * M, 0.0);
+  for (size_t a = 0; a < N; ++a)
+    for (size_t p = 0; p < M; ++p) {
+      const double ap = C[a * M + p];
+      if (ap == 0.0) continue;
+      for (size_t qrs = 0; qrs < M * M * M; ++qrs) mo.g[p * M * M * M + qrs] += ap * g3[a * M * M * M + qrs];
+    }
+  return mo;
+}
+
+FrozenCore freeze_core(const SpatialIntegrals& mo, int n_frozen, int n_elec) {
+  const int m = mo.m;
+  if (n_frozen < 0 || 2 * n_frozen > n_elec || n_frozen > m)
+    throw ContractViolation("freeze_core: n_frozen exceeds the occupied orbitals");
+  const size_t M = (size_t)m;
+  auto G = [&](int p, int q, int r, int s2) { return mo.g[((p * M + q) * M + r) * M + s2]; };
+  FrozenCore F;
+  double ef = 0.0;
+  for (int c = 0; c < n_frozen; ++c) {
+    ef += 2.0 * mo.h[c * M + c];
+    for (int d = 0; d < n_frozen; ++d) ef += 2.0 * G(c, c, d, d) - G(c, d, d, c);
+  }
+  const int ma = m - n_frozen;
+  const size_t A = (size_t)ma;
+  F.active.m = ma;
+  F.active.h.assign(A * A, 0.0);
+  F.active.g.assign(A * A * A * A, 0.0);
+  for (int p = 0; p < ma; ++p)
+    for (int q = 0; q < ma; ++q) {
+      double v = mo.h[(p + n_frozen) * M + (q + n_frozen)];
+      for (int c = 0; c < n_frozen; ++c)
+        v += 2.0 * G(p + n_frozen, q + n_frozen, c, c) - G(p + n_frozen, c, c, q + n_frozen);
+      F.active.h[p * A + q] = v;
+    }
+  for (int p = 0; p < ma; ++p)
+    for (int q = 0; q < ma; ++q)
+      for (int r = 0; r < ma; ++r)
+        for (int s2 = 0; s2 < ma; ++s2)
+          F.active.g[((p * A + q) * A + r) * A + s2] = G(p + n_frozen, q + n_frozen, r + n_frozen, s2 + n_frozen);
+  F.e_frozen = ef;
+  F.active.e_const = mo.e_const + ef;
+  F.n_elec_active = n_elec - 2 * n_frozen;
+  return F;
+}
+
 SpinOrbitalHamiltonian to_spin_orbitals(const SpatialIntegrals& I, int n_elec) {
   const int m = I.m, n = 2 * m;
   if (n_elec < 0 || n_elec > n) throw ContractViolation("to_spin_orbitals: bad electron count");

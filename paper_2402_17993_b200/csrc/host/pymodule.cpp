@@ -124,6 +124,44 @@ PYBIND11_MODULE(_fragfield, m) {
         return qubit_hamiltonian(to_spin_orbitals(I, n_elec));
       },
       py::arg("h"), py::arg("g"), py::arg("n_elec"), py::arg("e_const") = 0.0);
+  m.def(
+      "ao_to_mo",
+      [](arr_f64 h, arr_f64 g, arr_f64 C, double e_const, py::object v_esp) {
+        SpatialIntegrals I;
+        I.m = (int)h.shape(0);
+        I.h = to_vec(h);
+        I.g = to_vec(g);
+        I.e_const = e_const;
+        const int mo = C.ndim() == 2 ? (int)C.shape(1) : 0;
+        std::vector<double> v;
+        if (!v_esp.is_none()) v = to_vec(v_esp.cast<arr_f64>());
+        SpatialIntegrals R = ao_to_mo(I, to_vec(C), mo, v);
+        arr_f64 ho({mo, mo}), go({mo, mo, mo, mo});
+        std::copy(R.h.begin(), R.h.end(), ho.mutable_data());
+        std::copy(R.g.begin(), R.g.end(), go.mutable_data());
+        return py::make_tuple(ho, go, R.e_const);
+      },
+      py::arg("h"), py::arg("g"), py::arg("C"), py::arg("e_const") = 0.0, py::arg("v_esp") = py::none(),
+      "SPEC.md:272-279 -> (h_mo, g_mo, e_const)");
+  m.def(
+      "freeze_core",
+      [](arr_f64 h, arr_f64 g, double e_const, int n_frozen, int n_elec) {
+        SpatialIntegrals I;
+        I.m = (int)h.shape(0);
+        I.h = to_vec(h);
+        I.g = to_vec(g);
+        I.e_const = e_const;
+        if (I.h.size() != (size_t)I.m * I.m || I.g.size() != (size_t)I.m * I.m * I.m * I.m)
+          throw ContractViolation("freeze_core: integral shapes");
+        FrozenCore F = freeze_core(I, n_frozen, n_elec);
+        const int ma = F.active.m;
+        arr_f64 ho({ma, ma}), go({ma, ma, ma, ma});
+        std::copy(F.active.h.begin(), F.active.h.end(), ho.mutable_data());
+        std::copy(F.active.g.begin(), F.active.g.end(), go.mutable_data());
+        return py::make_tuple(ho, go, F.active.e_const, F.e_frozen, F.n_elec_active);
+      },
+      py::arg("h"), py::arg("g"), py::arg("e_const"), py::arg("n_frozen"), py::arg("n_elec"),
+      "SPEC.md:280-289 -> (h_eff, g_active, e_const incl. E_frozen, E_frozen, active electrons)");
   m.def("random_pauli_hamiltonian", &random_pauli_hamiltonian, py::arg("n_qubits"),
         py::arg("n_terms"), py::arg("seed"), py::arg("sigma") = 0.1);
   m.def("uniform_vector", &uniform_vector);
