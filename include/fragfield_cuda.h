@@ -79,9 +79,12 @@ int ffq_ctx_stream(ffq_ctx_t ctx, void** stream);
  *   FFQ_SECTOR_CL (2)       CTAs per cluster for large complex closures: 2, 4 or 8
  *   FFQ_SMEM_MAX_QUBITS (13) largest state held whole in one CTA's smem
  *   FFQ_SUPPORT (1)         support-bitmap passes on the global-memory path
- *   FFQ_TILE_BITS (12)      expectation tile width of the global path
  *   FFQ_SLAB_MB (256)       state slab per chunk of the global path
- *   FFQ_PERSIST, FFQ_PERSIST_MB, FFQ_PERSIST_NT  optional one-CTA-per-state kernel
+ *   FFQ_BLOCKS (1)          anchored string blocks of the real sector program; 0 off
+ *   FFQ_CLIQUES (1)         alpha-beta cliques of the real sector program; 0 off
+ *   FFQ_SPLIT (8)           most CTAs per evaluation of small real-program batches
+ *   FFQ_COMPACT (1), FFQ_COMPACT_MIN (27)  compact real sector layout, from n qubits
+ *   FFQ_ROT_TILE (12)       tile bits of fused rotation runs; 0: one pass per rotation
  *   FFQ_PHASE_CLOCKS        print per-phase cycle counts (read once per process) */
 
 /* ---- qubit Hamiltonian (PauliSum) ------------------------ */

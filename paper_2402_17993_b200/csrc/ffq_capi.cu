@@ -178,13 +178,9 @@ struct ffq_ctx_s {
   int n_sm = 148;
   size_t smem_optin = 0;
   int smem_max_qubits = kSmemMaxQubitsDefault;  // env FFQ_SMEM_MAX_QUBITS overrides
-  int tile_bits = kDefaultTileBits;              // env FFQ_TILE_BITS (0 disables tiling)
   int64_t slab_bytes = 256LL << 20;              // env FFQ_SLAB_MB: batch chunk of the graph path
   int support = 1;                               // env FFQ_SUPPORT=0: dense passes only
-  int persist = 0;                               // env FFQ_PERSIST=1: k_eval_persistent instead of the graph path
   int sector = 1;                                // env FFQ_SECTOR=0: no support-closure cluster evaluator
-  int64_t persist_bytes = 4096LL << 20;          // env FFQ_PERSIST_MB: zeroed slab of the persistent path
-  int persist_nt = 512;                          // env FFQ_PERSIST_NT: 512 or 1024 threads per state
   int sector_cl = 2;                             // env FFQ_SECTOR_CL: 2, 4 or 8 CTAs per large closure
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
@@ -206,8 +202,6 @@ struct ffq_ctx_s {
   int rot_tile_bits = 12;    // env FFQ_ROT_TILE: tile of a fused run (0: one pass per rotation)
   DevBuf<uint32_t> slab_sup;
   bool slab_clean = false;      // support path: slab all-zero between graph replays
-  DevBuf<double2> pslab;        // persistent-path slab, all-zero between evaluations
-  bool pslab_clean = false;
   double* pinned = nullptr;
   size_t pinned_n = 0;
   // ffq_energy_batch: chunk H2D copies on their own stream, so a copy overlaps
@@ -296,12 +290,12 @@ struct ffq_ham_s {
   DevBuf<double2> cls_f;
   DevBuf<int32_t> item_g, item_p;
   DevBuf<int64_t> item_u0;
-  DevBuf<uint32_t> bucket_h, titem_u, act_low;
-  DevBuf<int32_t> bucket_goff, bucket_groups, titem_bucket, sitem_g, sitem_p;
+  DevBuf<uint32_t> act_low;
+  DevBuf<int32_t> sitem_g, sitem_p;
   DevBuf<int64_t> sitem_w0;
   int64_t n_partials(bool support) const {
     if (support) return (int64_t)ch.sitem_g.size();
-    return ch.tile_bits ? (int64_t)ch.titem_u.size() : (int64_t)ch.item_g.size();
+    return (int64_t)ch.item_g.size();
   }
   HamDev dev() const {
     HamDev d;
@@ -311,9 +305,6 @@ struct ffq_ham_s {
     d.item_g = item_g.p; d.item_p = item_p.p; d.item_u0 = item_u0.p;
     d.item_chunk = ch.item_chunk;
     d.sitem_words = ch.sitem_words;
-    d.tile_bits = ch.tile_bits;
-    d.bucket_h = bucket_h.p; d.bucket_goff = bucket_goff.p; d.bucket_groups = bucket_groups.p;
-    d.titem_bucket = titem_bucket.p; d.titem_u = titem_u.p;
     return d;
   }
 };
@@ -483,23 +474,6 @@ void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, const 
         rstride ? rstride : (1LL << n));
     CK(cudaGetLastError());
     ctx->launches++;
-  } else if (h->ch.tile_bits) {
-    constexpr int NT = 512;
-    const size_t tile = sizeof(double2) << h->ch.tile_bits;
-    CK(cudaFuncSetAttribute(k_expect_tiles<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * tile)));
-    const int64_t n0 = h->ch.n_titems_h0, n1 = items - n0;
-    if (n0 > 0) {
-      k_expect_tiles<NT><<<dim3((unsigned)n0, batch), NT, tile, ctx->stream>>>(psi, n, h->dev(), 0, 0,
-                                                                               partial, items);
-      CK(cudaGetLastError());
-      ctx->launches++;
-    }
-    if (n1 > 0) {
-      k_expect_tiles<NT><<<dim3((unsigned)n1, batch), NT, 2 * tile, ctx->stream>>>(psi, n, h->dev(), n0, 1,
-                                                                                   partial, items);
-      CK(cudaGetLastError());
-      ctx->launches++;
-    }
   } else {
     dim3 grid((unsigned)items, batch);
     k_expect_items<kThreads><<<grid, kThreads, 0, ctx->stream>>>(psi, n, h->dev(), partial);
@@ -513,23 +487,6 @@ void launch_expect(ffq_ctx_t ctx, const ffq_ham_s* h, const double2* psi, const 
 
 size_t smem_bytes(const ffq_plan_s* pl) {
   return ((size_t(1) << pl->cp.n_qubits) + pl->cp.op_kind.size()) * sizeof(double2);
-}
-
-constexpr int kPersistThreadsMax = 1024;
-
-size_t persistent_smem(const ffq_plan_s* pl) {
-  const int n = pl->cp.n_qubits;
-  return (size_t(1) << (n - 5)) * sizeof(uint32_t) + pl->cp.op_kind.size() * sizeof(double2) +
-         (kPersistThreadsMax / 32) * kQ * sizeof(uint64_t);
-}
-
-bool use_persistent(ffq_ctx_t ctx, const ffq_plan_s* pl, const ffq_ham_s* h) {
-  const int n = pl->cp.n_qubits;
-  if (!ctx->persist || !use_support(ctx, n) || n > kPersistMaxQubits) return false;
-  if (persistent_smem(pl) > ctx->smem_optin) return false;
-  for (const auto& g : h->ch.groups)
-    if (g.w != __builtin_popcountll(g.x)) return false;  // generic-mode groups: graph path
-  return true;
 }
 
 constexpr int kSectorThreads = 768;       // per CTA of a 2/4/8-CTA cluster (measured best at 18 qubits)
@@ -788,49 +745,6 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
     ctx->launches++;
     return;
   }
-  if (use_persistent(ctx, pl, h)) {
-    const int64_t dim = 1LL << n;
-    const int64_t cap = std::max<int64_t>(1, ctx->persist_bytes / (dim * (int64_t)sizeof(double2)));
-    const int64_t n_chunks = (batch + cap - 1) / cap;
-    const int chunk = (int)((batch + n_chunks - 1) / n_chunks);
-    if (ctx->pslab.n < (size_t)chunk * dim) {
-      ctx->pslab.alloc((size_t)chunk * dim);
-      ctx->pslab_clean = false;
-    }
-    if (!ctx->pslab_clean) {
-      CK(cudaMemsetAsync(ctx->pslab.p, 0, ctx->pslab.n * sizeof(double2), ctx->stream));
-      ctx->pslab_clean = true;
-    }
-    const size_t sb = persistent_smem(pl);
-    auto kern = ctx->persist_nt == 1024 ? k_eval_persistent<1024> : k_eval_persistent<512>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-    static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
-    DevBuf<long long> clk;
-    if (clocks) clk.alloc(2 * (size_t)chunk);
-    for (int b0 = 0; b0 < batch; b0 += chunk) {
-      const int nb = std::min(chunk, batch - b0);
-      kern<<<nb, ctx->persist_nt, sb, ctx->stream>>>(
-          n, pl->dev(), h->dev(), hf, pl->pair_low.p, h->act_low.p, theta_dev + (int64_t)b0 * pl->cp.n_gen,
-          pl->cp.n_gen, ctx->pslab.p, e_dev + b0, im_dev ? im_dev + b0 : nullptr, nb,
-          clocks ? clk.p : nullptr);
-      if (clocks) {
-        std::vector<long long> hc(2 * (size_t)nb);
-        CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        double g = 0, e = 0;
-        for (int r = 0; r < nb; ++r) { g += (double)hc[2 * r]; e += (double)hc[2 * r + 1]; }
-        std::fprintf(stderr, "[ffq] persistent rows=%d avg cycles: generators %.0f expectation %.0f\n", nb,
-                     g / nb, e / nb);
-      }
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) {
-        ctx->pslab_clean = false;
-        throw CudaError(std::string("k_eval_persistent: ") + cudaGetErrorString(e));
-      }
-      ctx->launches++;
-    }
-    return;
-  }
   // global path: chunk the batch so the slab stays L2-resident (<= 64 MiB)
   const int64_t dim = 1LL << n;
   const int64_t slab_cap = ctx->slab_bytes / (dim * (int64_t)sizeof(double2));
@@ -959,7 +873,6 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     c->smem_optin = (size_t)optin - 2048;  // static smem of the reduction scratch
     if (const char* e = std::getenv("FFQ_SMEM_MAX_QUBITS")) c->smem_max_qubits = std::atoi(e);
-    if (const char* e = std::getenv("FFQ_TILE_BITS")) c->tile_bits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_ROT_TILE")) c->rot_tile_bits = std::min(12, std::max(0, std::atoi(e)));
     CK(cudaFuncSetAttribute(k_rotation_run<kRotRunThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) << 12)));
@@ -967,10 +880,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
                             (int)cudaSharedmemCarveoutMaxShared));
     if (const char* e = std::getenv("FFQ_SLAB_MB")) c->slab_bytes = std::max(1LL, std::atoll(e)) << 20;
     if (const char* e = std::getenv("FFQ_SUPPORT")) c->support = std::atoi(e);
-    if (const char* e = std::getenv("FFQ_PERSIST")) c->persist = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SECTOR")) c->sector = std::atoi(e);
-    if (const char* e = std::getenv("FFQ_PERSIST_MB")) c->persist_bytes = std::max(1LL, std::atoll(e)) << 20;
-    if (const char* e = std::getenv("FFQ_PERSIST_NT")) c->persist_nt = std::atoi(e) >= 1024 ? 1024 : 512;
     if (const char* e = std::getenv("FFQ_SECTOR_REAL")) c->sector_real = std::atoi(e);
     if (const char* e = std::getenv("FFQ_BLOCKS")) c->sector_blocks = std::atoi(e);
     if (const char* e = std::getenv("FFQ_CLIQUES")) c->sector_cliques = std::atoi(e);
@@ -1029,7 +939,7 @@ int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t*
   return guarded(ctx, [&] {
     auto h = std::make_unique<ffq_ham_s>();
     h->ctx = ctx;
-    h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im, ctx->tile_bits);
+    h->ch = compile_ham(n_qubits, n_terms, x, z, c_re, c_im);
     h->raw_x.assign(x, x + n_terms);
     h->raw_z.assign(z, z + n_terms);
     h->raw_re.assign(c_re, c_re + n_terms);
@@ -1044,11 +954,6 @@ int ffq_ham_upload(ffq_ctx_t ctx, int n_qubits, int64_t n_terms, const uint64_t*
     h->item_g.upload(ch.item_g, ctx->stream);
     h->item_p.upload(ch.item_p, ctx->stream);
     h->item_u0.upload(ch.item_u0, ctx->stream);
-    h->bucket_h.upload(ch.bucket_h, ctx->stream);
-    h->bucket_goff.upload(ch.bucket_goff, ctx->stream);
-    h->bucket_groups.upload(ch.bucket_groups, ctx->stream);
-    h->titem_bucket.upload(ch.titem_bucket, ctx->stream);
-    h->titem_u.upload(ch.titem_u, ctx->stream);
     h->act_low.upload(ch.act_low, ctx->stream);
     h->sitem_g.upload(ch.sitem_g, ctx->stream);
     h->sitem_p.upload(ch.sitem_p, ctx->stream);
@@ -1399,6 +1304,8 @@ int ffq_rotation_groups(int n, int t, int n_rot, const uint64_t* x, int32_t* run
   if (n_rot < 0 || n < 1 || n > 63 || t < 0 || t > 31 ||
       (n_rot > 0 && (!x || !run_of || !group_of || !cx || !run_q || !basis || !piv)) || !n_groups)
     return fail(nullptr, FFQ_EINVAL, "ffq_rotation_groups: invalid argument");
+  for (int r = 0; r < n_rot; ++r)  // the same check as ffq_state_apply_pauli_rotations
+    if (x[r] >> n) return fail(nullptr, FFQ_EINVAL, "ffq_rotation_groups: flip mask beyond n_qubits");
   std::vector<RotDesc> rd(n_rot, RotDesc{0, 0, 0, 0, 0});
   std::vector<char> ok(n_rot, 1);
   std::vector<uint64_t> z(n_rot, 0);

@@ -250,17 +250,7 @@ struct CompiledHam {
   int64_t item_chunk = 0;
   std::vector<int32_t> item_g, item_p;
   std::vector<int64_t> item_u0;
-  // tiled path: low `tile_bits` qubits form a contiguous tile; groups are
-  // bucketed by their out-of-tile flip pattern h = X >> tile_bits and every
-  // (bucket, tile pair {u, u^h}) is one work item (0 = tiling disabled)
-  int tile_bits = 0;
   bool has_generic = false;  // some group has |X| > kMaxTableBits (random Pauli strings)
-  std::vector<uint32_t> bucket_h;
-  std::vector<int32_t> bucket_goff;  // [n_buckets + 1] into bucket_groups
-  std::vector<int32_t> bucket_groups;
-  std::vector<int32_t> titem_bucket;  // items with h == 0 first, then h != 0
-  std::vector<uint32_t> titem_u;
-  int64_t n_titems_h0 = 0;
   // support-tracked path: items (group, pattern, first support word)
   std::vector<int32_t> sitem_g, sitem_p;
   std::vector<int64_t> sitem_w0;
@@ -268,14 +258,11 @@ struct CompiledHam {
   int64_t n_classes() const { return (int64_t)cls_z.size(); }
 };
 
-constexpr int kDefaultTileBits = 12;
-
 constexpr int64_t kItemChunk = 4096;
 constexpr int64_t kSupportWordsPerItem = 2048;
 
 inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint64_t* z,
-                               const double* cr, const double* ci,
-                               int tile_bits = kDefaultTileBits) {
+                               const double* cr, const double* ci) {
   if (n < 1 || n > 40) throw BadInput("hamiltonian: n_qubits out of range [1, 40]", -1);
   const uint64_t full = (1ULL << n) - 1ULL;
   std::map<uint64_t, std::map<uint64_t, double>> byx;  // x -> z -> real coefficient
@@ -412,34 +399,6 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
           H.sitem_w0.push_back(w0);
         }
     }
-  }
-  // tiled decomposition (table-mode groups only, n <= 32, at least one out bit)
-  bool tileable = tile_bits > 0 && n > tile_bits && n <= 32;
-  for (const auto& d : H.groups)
-    if (popc64(d.x) > kMaxTableBits) tileable = false;
-  if (tileable) {
-    H.tile_bits = tile_bits;
-    std::map<uint32_t, std::vector<int32_t>> buckets;
-    for (size_t g = 0; g < H.groups.size(); ++g)
-      buckets[(uint32_t)(H.groups[g].x >> tile_bits)].push_back((int32_t)g);
-    H.bucket_goff.push_back(0);
-    for (auto& b : buckets) {
-      H.bucket_h.push_back(b.first);
-      H.bucket_groups.insert(H.bucket_groups.end(), b.second.begin(), b.second.end());
-      H.bucket_goff.push_back((int32_t)H.bucket_groups.size());
-    }
-    const uint32_t n_out = 1u << (n - tile_bits);
-    for (int pass = 0; pass < 2; ++pass)
-      for (size_t b = 0; b < H.bucket_h.size(); ++b) {
-        const uint32_t h = H.bucket_h[b];
-        if ((pass == 0) != (h == 0)) continue;
-        for (uint32_t u = 0; u < n_out; ++u)
-          if (h == 0 || u < (u ^ h)) {
-            H.titem_bucket.push_back((int32_t)b);
-            H.titem_u.push_back(u);
-          }
-        if (pass == 0) H.n_titems_h0 = (int64_t)H.titem_u.size();
-      }
   }
   return H;
 }

@@ -51,13 +51,6 @@ struct HamDev {
   const int64_t* item_u0;
   int64_t item_chunk;
   int64_t sitem_words;  // support words per support-path item
-  // tiled path
-  int tile_bits;
-  const uint32_t* bucket_h;
-  const int32_t* bucket_goff;
-  const int32_t* bucket_groups;
-  const int32_t* titem_bucket;
-  const uint32_t* titem_u;
 };
 
 // ---- small helpers -----------------------------------------------------------
@@ -450,8 +443,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // every rotation of the group lies inside one coset. Each thread loads one
 // coset into registers, applies the group's rotations in order there, and
 // stores it: one shared-memory round trip per group instead of per rotation,
-// one CTA barrier per group. The pivot bits are the highest available, so
-// lanes of a quarter warp differ in low bits (conflict-free 16-byte accesses).
+// one CTA barrier per group. A pivot is the highest set bit of its reduced
+// flip mask (padding vectors take the highest free bits), so it can be a low
+// bit (x = 1 gives pivot 0): then consecutive coset indices u spread to
+// non-adjacent k and a quarter warp's 16-byte accesses can conflict. This
+// costs bandwidth only; the result does not depend on the pivot choice.
 // z is unrestricted: the tile's high-bit parity is folded into sin once per
 // rotation. Per pair the arithmetic is k_pauli_rotation's.
 struct RotDesc {
@@ -624,130 +620,6 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
     for (uint32_t k = 2 * threadIdx.x; k < tsize; k += 2 * NT) st256(s + k, tl[k], tl[k + 1]);
   else
     for (uint32_t m = 2 * threadIdx.x; m < tsize; m += 2 * NT) st256(s + (hi_off[m >> 5] | (m & 31u)), tl[m], tl[m + 1]);
-}
-
-// ---- tiled expectation ---------------------------------------------------------
-// Work item = (bucket of groups sharing h = X >> t, tile pair {u, u ^ h}); the
-// low t qubits of the index form a contiguous 2^t-amplitude tile, so each tile
-// is ONE bulk copy. Every group of the bucket is evaluated from shared memory:
-// the state is read once per distinct h instead of once per group.
-// Warps take groups round-robin; lanes stride the group's (pattern, u) space.
-template <int NT>
-__global__ void __launch_bounds__(NT) k_expect_tiles(const double2* __restrict__ psi, int n, HamDev h,
-                                                     int64_t item0, int two_tiles,
-                                                     double2* __restrict__ partial,
-                                                     int64_t partial_stride) {
-  extern __shared__ __align__(128) double2 tl[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ double2 red[NT / 32];
-  const int t = h.tile_bits;
-  const uint32_t tsize = 1u << t, tmask = tsize - 1u;
-  const int64_t item = item0 + blockIdx.x;
-  const int b = blockIdx.y;
-  const int bk = h.titem_bucket[item];
-  const uint32_t uA = h.titem_u[item], hh = h.bucket_h[bk], uB = uA ^ hh;
-  const double2* s = psi + ((int64_t)b << n);
-  double2* tA = tl;
-  double2* tB = two_tiles ? tl + tsize : tl;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    const uint32_t bytes = tsize * (uint32_t)sizeof(double2);
-    mbar_expect_tx(&bar, two_tiles ? 2 * bytes : bytes);
-    const uint32_t piece = 32768;  // 32 KiB per bulk copy
-    for (uint32_t off = 0; off < bytes; off += piece) {
-      const uint32_t len = min(piece, bytes - off);
-      bulk_g2s((char*)tA + off, (const char*)(s + ((uint64_t)uA << t)) + off, len, &bar);
-      if (two_tiles) bulk_g2s((char*)tB + off, (const char*)(s + ((uint64_t)uB << t)) + off, len, &bar);
-    }
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g0 = h.bucket_goff[bk], g1 = h.bucket_goff[bk + 1];
-  // per-warp queue of non-zero pair products: the class loop (the expensive
-  // part) runs only on pairs whose product conj(psi[m^X]) psi[m] is non-zero
-  __shared__ uint32_t q_m[NT];
-  __shared__ double2 q_pr[NT];
-  uint32_t* wq_m = q_m + warp * 32;
-  double2* wq_pr = q_pr + warp * 32;
-  double acc = 0.0;
-  for (int gi = g0 + warp; gi < g1; gi += NT / 32) {
-    const GroupDesc d = h.groups[h.bucket_groups[gi]];
-    const uint32_t XT = (uint32_t)d.x & tmask;
-    const int wT = __popc(XT);
-    const int ub = t - wT;
-    const uint32_t U = 1u << ub;
-    for (int p = 0; p < d.nact; ++p) {
-      // the enumerated member m has pattern p; its out-of-tile bits must be
-      // one of this item's two tiles, otherwise the pair belongs to another item
-      const uint64_t pb = h.act_bits[d.act_off + p];
-      const uint32_t pO = (uint32_t)(pb >> t);
-      const bool inA = ((uA & hh) == pO);
-      if (!inA && ((uB & hh) != pO)) continue;
-      const uint32_t mO = inA ? uA : uB;
-      const double2* src = inA ? tA : tB;
-      const double2* dst = inA ? tB : tA;
-      const uint32_t pT = (uint32_t)pb & tmask;
-      // class loop over `count` queued pairs, one per lane
-      auto drain = [&](int count) {
-        if (lane < count) {
-          const uint32_t mm = wq_m[lane];
-          const double2 pr = wq_pr[lane];
-          double fx = 0.0, fy = 0.0;
-          for (int o = 0; o < d.ncls; ++o) {
-            const double sg = sgn_par((uint64_t)(mm & (uint32_t)h.cls_z[d.cls_off + o]));
-            const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
-            fx = fma(sg, fo.x, fx);
-            fy = fma(sg, fo.y, fy);
-          }
-          acc = fma(pr.x, fx, acc);
-          acc = fma(-pr.y, fy, acc);
-        }
-        __syncwarp();
-      };
-      int qn = 0;
-      for (uint32_t u0 = 0; u0 < U; u0 += 32) {
-        const uint32_t u = u0 + lane;
-        double prx = 0.0, pry = 0.0;
-        uint32_t m = 0;
-        bool nz = false;
-        if (u < U) {
-          const uint32_t mT = insert_bits<uint32_t>(u, d.qpack, wT) | pT;
-          m = (mO << t) | mT;
-          const double2 a = src[mT];
-          if (a.x != 0.0 || a.y != 0.0) {
-            const double2 bb = dst[mT ^ XT];
-            prx = bb.x * a.x + bb.y * a.y;
-            pry = bb.x * a.y - bb.y * a.x;
-            nz = (prx != 0.0 || pry != 0.0);
-          }
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-        const int rank = __popc(bal & ((1u << lane) - 1u));
-        const int cnt = __popc(bal);
-        const int room = 32 - qn;
-        if (nz && rank < room) {
-          wq_m[qn + rank] = m;
-          wq_pr[qn + rank] = make_double2(prx, pry);
-        }
-        __syncwarp();
-        if (cnt >= room) {
-          drain(32);
-          if (nz && rank >= room) {
-            wq_m[rank - room] = m;
-            wq_pr[rank - room] = make_double2(prx, pry);
-          }
-          __syncwarp();
-          qn = cnt - room;
-        } else {
-          qn += cnt;
-        }
-      }
-      if (qn > 0) drain(qn);
-    }
-  }
-  const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);
-  if (threadIdx.x == 0) partial[(int64_t)b * partial_stride + item] = tot;
 }
 
 // ---- shared-memory-resident evaluator (n <= 13) ------------------------------

@@ -209,7 +209,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     }
     auto hp = std::make_unique<ffq_ham_s>();
     hp->ctx = ctx;
-    hp->ch = compile_ham(sh->n, (int64_t)x.size(), x.data(), z.data(), h->raw_re.data(), h->raw_im.data(), 0);
+    hp->ch = compile_ham(sh->n, (int64_t)x.size(), x.data(), z.data(), h->raw_re.data(), h->raw_im.data());
     hp->ch.item_chunk = std::max<int64_t>(kItemChunk, (1LL << (l - 1)) / 256);
     const auto& ch = hp->ch;
     hp->groups.upload(ch.groups, ctx->stream);

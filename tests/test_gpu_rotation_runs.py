@@ -142,3 +142,36 @@ def test_plan_string_runs_fused_equal_unfused(monkeypatch):
     del plan, ham
     c.close()
     assert np.abs(res["12"][0] - ej).max() <= 1e-10
+
+
+@pytest.mark.parametrize("n", [14, 17])
+def test_gathered_tile_runs_vs_oracle_deterministic(ctx, oracle, n):
+    """The gathered-tile path of k_rotation_run (a run's qubit set is not the
+    low 12: flip masks on qubits 0-4 plus high qubits) against the oracle,
+    deterministically: every run here needs gathered tiles, z spans all qubits,
+    batch of 3."""
+    rng = np.random.default_rng(1000 + n)
+    psi = random_state(rng, n, 3)
+    hi = [n - 1, n - 3, n - 6]
+    xs = []
+    for r in range(24):
+        low = int(rng.integers(0, 32))
+        high = sum(1 << q for q in hi if rng.random() < 0.6) or (1 << hi[r % 3])
+        xs.append(low | high)
+    x = np.array(xs, np.uint64)
+    z = rng.integers(0, 1 << n, size=len(x), dtype=np.uint64)
+    th = rng.uniform(-np.pi, np.pi, size=len(x))
+    run_of, _, _, run_q, _, _ = capi.rotation_groups(n, 12, x)
+    assert (run_of >= 0).all()  # every rotation runs fused
+    low12 = (1 << 12) - 1
+    assert all(int(q) & ~low12 for q in run_q)  # and every run gathers (its qubit set is not the low 12)
+    st = capi.State(ctx, n, 3)
+    st.upload(psi)
+    l0 = ctx.launches()
+    st.rotate_many(x, z, th)
+    assert ctx.launches() - l0 < len(x)
+    ref = psi.copy()
+    for b in range(3):
+        for r in range(len(x)):
+            ref[b] = oracle.apply_pauli_rotation(n, ref[b], int(x[r]), int(z[r]), float(th[r]))
+    assert np.abs(st.download() - ref).max() <= A_TOL
