@@ -8,7 +8,7 @@ import numpy as np  # noqa: E402
 from paper_2402_17993_b200 import capi, problems  # noqa: E402
 
 for env in ({}, {"FFQ_SMEM_MAX_QUBITS": "0"}, {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_SUPPORT": "0"},
-            {"FFQ_SMEM_MAX_QUBITS": "0", "FFQ_PERSIST": "1"}):
+            ):
     os.environ.update(env)
     ctx = capi.Context(0)
     P = problems.make_problem(7, 6, problems.ham_seed(9), batch=3)
