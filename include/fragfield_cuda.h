@@ -241,11 +241,13 @@ int ffq_plan_compile_stats(int n_qubits, int n_gen, const int64_t* term_off, con
  * program (product layout, anchored string blocks) for plan + Hamiltonian +
  * hf and evaluates its expectation tables on the real state psi[2^n] exactly
  * as k_sector_eval_real would (generic rows, blocks, then the alpha-beta
- * cliques in the alpha-first gauge). out[10]: energy, closure size, amplitude
+ * cliques in the alpha-first gauge). out[11]: energy, closure size, amplitude
  * slots, product layout (0/1), pairs held by blocks, expectation pairs,
  * generic rows, block units, pairs held by cliques, modelled clique bank
- * conflicts. FFQ_CLIQUES=0 compiles without cliques. FFQ_EINVAL when the
- * program is complex or has no sector. */
+ * conflicts, and table violations: generator steps whose pairs share a slot
+ * (a race) or any table slot outside [0, n_slots] (0 = race-free and in
+ * bounds by construction). FFQ_CLIQUES=0 compiles without cliques.
+ * FFQ_EINVAL when the program is complex or has no sector. */
 int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
                        const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,

@@ -155,11 +155,11 @@ def sector_emulate(n, plan_arrays, ham_arrays, hf_bits, psi):
     hx, hz, hre, him = _terms(*ham_arrays)
     off = np.ascontiguousarray(off, np.int64)
     psi = np.ascontiguousarray(psi, np.float64)
-    out = np.zeros(10)
+    out = np.zeros(11)
     check(lib().ffq_sector_emulate(n, len(off) - 1, off, px, pz, pre, pim, len(hx), hx, hz, hre, him, hf_bits, psi,
                                    out))
     keys = ["energy", "closure_size", "slots", "product", "block_pairs", "exp_pairs", "generic_rows", "units",
-            "clique_pairs", "clique_conflicts"]
+            "clique_pairs", "clique_conflicts", "table_violations"]
     return dict(zip(keys, out.tolist()))
 
 

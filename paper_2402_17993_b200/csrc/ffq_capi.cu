@@ -1448,6 +1448,49 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
     const SectorProgram S = compile_sector(P, H, hf_bits, kSectorMaxSize, 0xFFFFFFFFu, 1, 0xFFFFFFFFu, 4, 8,
                                            kSectorRealThreads / 32, kSectorSingleMax, !cqe || std::atoi(cqe) != 0);
     if (!S.ok) return fail(nullptr, FFQ_EINVAL, "ffq_sector_emulate: " + S.why);
+    // race freedom and bounds by construction (compute-sanitizer is not available
+    // on the GPU pool): every generator step's pairs touch distinct amplitude
+    // slots (the step's threads then never race; steps are barrier-separated),
+    // and every slot a table can address lies in [0, n_slots] (n_slots = zero slot)
+    int64_t bad = 0;
+    {
+      std::vector<int32_t> seen((size_t)S.n_slots + 1, -1);
+      const int n_ops = (int)S.op_cross.size();
+      for (int op = 0; op < n_ops; ++op)
+        for (int64_t t = S.gen_off[op]; t < S.gen_off[op + 1]; ++t) {
+          const uint32_t w = S.gen_pairs[t], i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
+          if (i >= S.n_slots || j >= S.n_slots || i == j) { ++bad; continue; }
+          for (uint32_t k : {i, j}) {
+            if (seen[k] == op) ++bad;
+            seen[k] = op;
+          }
+        }
+      for (uint32_t w : S.row_pairs)
+        if ((w & 0x7FFFu) > S.n_slots || ((w >> 15) & 0x7FFFu) > S.n_slots) ++bad;
+      for (size_t w = 0; w < S.blk_warp.size() / 4; ++w) {
+        uint32_t bs = 0;
+        for (int r = S.blk_warp[4 * w]; r < S.blk_warp[4 * w + 1]; ++r)
+          for (int l = 0; l < 32; ++l) {
+            const uint32_t d = S.blk_stream[(size_t)r * 32 + l];
+            if (d >> 30) {
+              bs = (d >> 15) & 0x7FFFu;
+              if ((d & 0x7FFFu) > S.n_slots) ++bad;
+            } else if (bs + (d & 0x7FFFu) > S.n_slots || (d >> 16) >= S.ftab.size()) {
+              ++bad;
+            }
+          }
+      }
+      for (size_t l = 0; l < S.cq_desc.size() / 4; ++l) {
+        const int32_t* d = &S.cq_desc[4 * l];
+        for (int32_t k = d[2]; k < d[3]; ++k)
+          for (int i = 0; i < kCliqueMax; ++i) {
+            const uint32_t c = ((uint32_t)(i < 4 ? d[0] : d[1]) >> (8 * (i & 3))) & 0xFFu;
+            if (c >= S.stride_b || (S.cq_rows[k] & 0x7FFFu) + c >= S.n_slots ||
+                ((S.cq_rows[k] >> 15) & 0x7FFFu) + c >= S.n_slots)
+              ++bad;
+          }
+      }
+    }
     std::vector<double> amp((size_t)S.n_slots + 1, 0.0);
     for (uint32_t i = 0; i < S.size; ++i) amp[S.slot_of[i]] = psi[S.basis[i]];
     if (!S.eps_flip.empty())  // the expectation tables are in the alpha-first gauge
@@ -1521,6 +1564,7 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
     out[7] = (double)nu;
     out[8] = (double)S.cq_pairs;
     out[9] = (double)S.cq_conflicts;
+    out[10] = (double)bad;
     return FFQ_OK;
   });
 }

@@ -357,3 +357,23 @@ def test_compact_sector_path_golden(monkeypatch):
         assert c.launches() - n0 > P.n_gen  # one pass per generator: the compact path ran
         ref = np.array([float.fromhex(r["energy"]) for r in g["rows"]])
         assert np.abs(e - ref).max() <= 1e-10, cfg
+
+
+def test_sector_program_repeatable_under_load():
+    """Evidence against shared-memory races in the barrier-pipelined real
+    program (compute-sanitizer is closed on the GPU pool; the host check
+    ffq_sector_emulate proves every generator step race-free by construction):
+    ten launches of 300 config-3 rows, plus small batches that take the split
+    path, give bit-identical energies."""
+    P = problems.config_problem(3, batch=1)
+    from paper_2402_17993_b200 import parameter_shift_set
+
+    rows = np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)[:300]
+    c = capi.Context(0)
+    plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    th = P.plan_thetas(rows)
+    ref = capi.energy_batch(c, plan, ham, P.hf, th)
+    for _ in range(10):
+        assert np.array_equal(capi.energy_batch(c, plan, ham, P.hf, th), ref)
+    for nb in (1, 3, 17):
+        assert np.array_equal(capi.energy_batch(c, plan, ham, P.hf, th[:nb]), ref[:nb])

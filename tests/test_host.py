@@ -205,6 +205,7 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
     H = oracle.PauliSum.from_terms(n, *P.ham_arrays())
     ref = oracle.expectation(n, psi.astype(np.complex128), H)
     assert abs(r["energy"] - ref.real) <= 1e-12
+    assert r["table_violations"] == 0  # steps race-free, every slot in bounds
     assert r["closure_size"] == int(((pa == na) & (pb == nb)).sum())
     if cfg == 3:  # 18 qubits: (5a, 5b) sector = 126 x 126 strings, stride 127
         assert r["product"] == 1 and r["slots"] == 126 * 127
