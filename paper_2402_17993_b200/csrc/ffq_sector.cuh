@@ -563,12 +563,20 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   // would wait for the load).
   auto first_words = [&](int op) -> uint2 {
     if (op >= sd.n_ops) return make_uint2(0u, 0u);
+#if defined(FFQ_EXP_NOPREF)
+    return make_uint2(0u, 0u);
+#endif
     const uint2 se = gse[op];
     return make_uint2(se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u,
                       se.x + tid + NT < se.y ? __ldg(sd.gen_pairs + se.x + tid + NT) : 0u);
   };
   auto step = [&](int op, uint2 ww) {
     const uint2 se = gse[op];
+#if defined(FFQ_EXP_NOROT)  // timing experiment: barrier + parameters + word prefetch only
+    if (se.x + tid < se.y && ww.x == 0xFFFFFFFFu) amp[0] = cs[op].x + fz[op].x;
+    __syncthreads();
+    return;
+#endif
     if (se.x + tid < se.y) {
       const double c = cs[op].x;
       const double2 sf = fz[op];
@@ -586,6 +594,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       const uint32_t t1 = se.x + tid + NT;
       if (t1 < se.y) {
         rot(ww.y);
+        // (the compiler unrolls this loop and issues its word loads together)
         for (uint32_t t = t1 + NT; t < se.y; t += NT) rot(__ldg(sd.gen_pairs + t));
       }
     }
