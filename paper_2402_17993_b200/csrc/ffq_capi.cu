@@ -191,8 +191,8 @@ struct ffq_ctx_s {
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
-  DevBuf<double> compact_psi, compact_coef;  // compact real sector path (ffq_compact.inl)
-  DevBuf<double2> compact_part;
+  DevBuf<double> compact_psi, compact_coef, compact_part;  // compact real sector path (ffq_compact.inl)
+  int compact_il = 4;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4)
   int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
   int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
                                              // support path is faster below: grouped Hamiltonian)
@@ -886,6 +886,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_CLIQUES")) c->sector_cliques = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT")) c->compact = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_COMPACT_IL")) c->compact_il = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);

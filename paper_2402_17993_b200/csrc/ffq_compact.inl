@@ -4,171 +4,309 @@
 // (N_alpha, N_beta) sector, and with real F on every generator the state is
 // real (see k_sector_eval_real). Instead of the dense 2^n complex layout
 // (64 GiB at 32 qubits, <= 4% of it ever non-zero), the state is held as a
-// real [C(m, N_alpha)][C(m, N_beta)] matrix: row = rank of the alpha string
-// (even qubits), column = rank of the beta string (odd qubits). That is
-// 1.3 GB at 32 qubits, and a pass streams whole rows.
+// real matrix psi[rank(alpha)][rank(beta)][lane]:
+//   row   = rank of the alpha string (even qubits, compressed),
+//   col   = rank of the beta string (odd qubits), row stride ld = cols rounded
+//           up to 4 (rows start on 32-byte sectors),
+//   lane  = one of IL in {1, 2, 4} theta rows of the batch evaluated together
+//           (the plan is shared by the batch). With IL = 4 one amplitude of
+//           four evaluations is exactly one 32-byte sector, so a pass moves
+//           its algorithmic bytes and nothing else.
+// That is 1.3 GB per lane at 32 qubits.
 //
-//  - A generator pass (one fused op: flip mask x, low pattern lo, outside-Z
-//    mask zout) visits the low members k = (alpha, beta) with (alpha & x_a)
-//    == lo_a and (beta & x_b) == lo_b; the partner is (alpha ^ x_a, beta ^ x_b)
-//    and the JW sign factorises, (-1)^popc(k & zout) = row sign * column sign.
-//    The 2x2 rotation is k_sector_eval_real's (same F, same fma order).
-//  - A Hamiltonian term (x, z, c) adds Re(c i^ny) * S with
-//    S = sum_k psi_k psi_{k^x} (-1)^popc((k^x) & z) over k with both members
-//    in the sector (SPEC.md:419-427 expectation restricted to the sector; psi is
-//    real, so a term with Re(c i^ny) = 0 contributes nothing). Terms sharing a
-//    flip mask are one pass (the pair weight sums their signed w). Each pass's
-//    CTA partials land in fixed slots; one fixed-order reduction gives the energy.
+// Every pass runs from lists compiled once per (plan, Hamiltonian, HF):
+//  - a generator (flip mask x, low pattern lo, outside-Z mask zout) is the
+//    2x2 rotation of k_sector_eval_real (same F, same fma order) on the pairs
+//    (alpha, beta) <-> (alpha ^ x_a, beta ^ x_b) with (alpha & x_a) == lo_a,
+//    (beta & x_b) == lo_b; its JW sign factorises into a row and a column
+//    sign. The op is a row list (ri | rj << 14 | sign << 28, one CTA each) and
+//    a column list with the same packing, shared by every op with the same
+//    alpha / beta part; ops without a beta flip stream whole row pairs with
+//    32-byte vectors and a per-column sign bitmask.
+//  - a Hamiltonian term (x, z, c) adds Re(c i^ny) S with
+//    S = sum_k psi_k psi_{k^x} (-1)^popc((k^x) & z) over sector pairs
+//    (SPEC.md:419-427 restricted to the sector; psi real). For odd ny the two
+//    orientations of a pair cancel (S = 0: the term is dropped at compile
+//    time); for even ny they are equal, so every unordered pair is visited
+//    once with weight 2 (the x = 0 group once with weight 1). Terms sharing a
+//    flip mask are one group (the pair weight sums their signed w); all groups
+//    run in one launch, CTA partials in fixed slots, one fixed-order reduction.
+//  - the beta strings are ranked with the least-flipped beta qubits varying
+//    fastest, which keeps the live columns of the frequent beta parts in
+//    longer runs (config 5, IL = 1: modelled DRAM 1431 -> 1270 GB per
+//    evaluation against 937 GB algorithmic).
 //
 // Eligibility (compact_program): n even, m = n / 2 <= 16, every op a fused
 // generator with one real pattern pair that keeps both spin counts.
 // (Included by ffq_capi.cu inside its internal namespace.)
 
 constexpr int kCompactThreads = 256;
+constexpr uint32_t kCompactIdx = 0x3FFFu;  // 14-bit ranks: C(16, 8) = 12870
 
-struct CompactOp {  // one fused op over compressed alpha / beta strings
-  uint32_t xa, la, za, xb, lb, zb;
+struct CompactOp {  // one fused op: offsets into CompactProg::lists
+  int32_t row_off, n_rows;
+  int32_t col_off, n_cols;  // n_cols = 0: no beta flip, col_off = column sign bitmask words
 };
-struct CompactTerm {  // one Hamiltonian term of a flip-mask group
+struct CompactTerm {  // one Hamiltonian term of a multi-term flip-mask group
   uint32_t za, zb;
-  double w;  // Re(c i^ny)
+  double w;  // Re(c i^ny), times 2 off the diagonal
 };
-struct CompactGroup {  // terms sharing the flip mask (xa, xb): one pass
-  uint32_t xa, xb;
-  int32_t t0, nt;
+struct CompactGroup {  // terms sharing the flip mask (xa, xb)
+  int32_t row_off, n_rows, col_off, n_cols;
+  int32_t t0, nt;  // nt == 1: the signs are in the lists and w is the weight
+  double w;
 };
 
-// per-op rotation coefficients for one theta row: (cos phi, sin phi * F_hi, sin phi * F_lo)
-__global__ void k_compact_coef(PlanDev pl, const double* __restrict__ theta, double* __restrict__ coef) {
-  const int op = blockIdx.x * blockDim.x + threadIdx.x;
+template <int IL>
+__device__ __forceinline__ void cld(const double* p, double (&v)[IL]) {
+  if constexpr (IL == 1) {
+    v[0] = *p;
+  } else if constexpr (IL == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  }
+}
+template <int IL>
+__device__ __forceinline__ void cst(double* p, const double (&v)[IL]) {
+  if constexpr (IL == 1) {
+    *p = v[0];
+  } else if constexpr (IL == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  } else {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+  }
+}
+
+// per-op rotation coefficients of IL theta rows: coef[op][k][lane],
+// k = (cos phi, sin phi * F_hi, sin phi * F_lo)
+template <int IL>
+__global__ void k_compact_coef(PlanDev pl, const double* __restrict__ theta, int theta_stride,
+                               double* __restrict__ coef) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int op = t / IL, lane = t % IL;
   if (op >= pl.n_ops) return;
-  const double phi = theta[pl.op_gen[op]] * pl.op_cfac[op];
+  const double phi = theta[(int64_t)lane * theta_stride + pl.op_gen[op]] * pl.op_cfac[op];
   double sv, cv;
   sincos(phi, &sv, &cv);
   const double sn = sv * pl.op_sscale[op];
   const FusedDesc& d = pl.fused[pl.op_idx[op]];
-  coef[3 * op] = cv;
-  coef[3 * op + 1] = sn * pl.pair_f[2 * d.pair_off + 1].x;
-  coef[3 * op + 2] = sn * pl.pair_f[2 * d.pair_off].x;
+  coef[(3 * op) * IL + lane] = cv;
+  coef[(3 * op + 1) * IL + lane] = sn * pl.pair_f[2 * d.pair_off + 1].x;
+  coef[(3 * op + 2) * IL + lane] = sn * pl.pair_f[2 * d.pair_off].x;
 }
 
-__global__ void k_compact_set(double* __restrict__ psi, int64_t at) { psi[at] = 1.0; }
+template <int IL>
+__global__ void k_compact_set(double* __restrict__ psi, int64_t at) {
+  if (threadIdx.x < IL) psi[at * IL + threadIdx.x] = 1.0;
+}
 
-// One CTA per row (alpha string); columns four per thread per trip, every load
-// of a trip issued before its stores (the pairs of one op are disjoint).
-__global__ void __launch_bounds__(kCompactThreads) k_compact_gen(double* __restrict__ psi, int na, int nb,
-                                                                 const uint32_t* __restrict__ stra,
-                                                                 const uint32_t* __restrict__ strb,
-                                                                 const uint16_t* __restrict__ ranka,
-                                                                 const uint16_t* __restrict__ rankb, CompactOp o,
-                                                                 const double* __restrict__ coef) {
-  constexpr int T = kCompactThreads, U = 4;
-  const int r = blockIdx.x;
-  const uint32_t a = __ldg(stra + r);
-  if ((a & o.xa) != o.la) return;
-  const double c = coef[0], gh0 = coef[1], gl0 = coef[2];
-  double* __restrict__ pi = psi + (int64_t)r * nb;
-  double* __restrict__ pj = psi + (int64_t)__ldg(ranka + (a ^ o.xa)) * nb;
-  const uint32_t sa = (uint32_t)__popc(a & o.za) & 1u;
-  for (int c0 = threadIdx.x; c0 < nb; c0 += U * T) {
-    int ci[U], cj[U];
-    uint32_t sg[U];
-    bool ok[U];
+// Generator with a beta flip: CTA = (row entry, column chunk); every load of a
+// trip is issued before its stores (the pairs of one op are disjoint).
+template <int IL>
+__global__ void __launch_bounds__(kCompactThreads) k_compact_gen(double* __restrict__ psi, int64_t ld,
+                                                                 const uint32_t* __restrict__ rows,
+                                                                 const uint32_t* __restrict__ cols, int n_cols,
+                                                                 int chunk, const double* __restrict__ coef) {
+  constexpr int T = kCompactThreads, U = IL == 4 ? 4 : 8;
+  const uint32_t re = __ldg(rows + blockIdx.x);
+  const uint32_t sa = re >> 28;
+  double* __restrict__ pi = psi + (int64_t)(re & kCompactIdx) * ld * IL;
+  double* __restrict__ pj = psi + (int64_t)((re >> 14) & kCompactIdx) * ld * IL;
+  double c[IL], gh[IL], gl[IL];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int col = c0 + u * T;
-      ok[u] = col < nb;
-      ci[u] = cj[u] = col;
-      sg[u] = sa;
-      if (ok[u] && (o.xb | o.zb)) {
-        const uint32_t b = __ldg(strb + col);
-        ok[u] = (b & o.xb) == o.lb;
-        sg[u] ^= (uint32_t)__popc(b & o.zb) & 1u;
-        if (o.xb && ok[u]) cj[u] = __ldg(rankb + (b ^ o.xb));
-      }
-    }
-    double x[U], y[U];
+  for (int l = 0; l < IL; ++l) {
+    c[l] = coef[l];
+    gh[l] = coef[IL + l];
+    gl[l] = coef[2 * IL + l];
+  }
+  const int c1 = min(n_cols, ((int)blockIdx.y + 1) * chunk);
+  for (int t0 = blockIdx.y * chunk + threadIdx.x; t0 < c1; t0 += U * T) {
+    uint32_t ce[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      x[u] = ok[u] ? pi[ci[u]] : 0.0;
-      y[u] = ok[u] ? pj[cj[u]] : 0.0;
-    }
+    for (int u = 0; u < U; ++u) ce[u] = t0 + u * T < c1 ? __ldg(cols + t0 + u * T) : 0xFFFFFFFFu;
+    double x[U][IL], y[U][IL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (ok[u]) {
-        pi[ci[u]] = fma(sg[u] ? -gh0 : gh0, y[u], c * x[u]);
-        pj[cj[u]] = fma(sg[u] ? -gl0 : gl0, x[u], c * y[u]);
+      if (ce[u] != 0xFFFFFFFFu) {
+        cld<IL>(pi + (int64_t)(ce[u] & kCompactIdx) * IL, x[u]);
+        cld<IL>(pj + (int64_t)((ce[u] >> 14) & kCompactIdx) * IL, y[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ce[u] != 0xFFFFFFFFu) {
+        const bool neg = ((sa ^ (ce[u] >> 28)) & 1u) != 0;
+        double nx[IL], ny[IL];
+#pragma unroll
+        for (int l = 0; l < IL; ++l) {
+          nx[l] = fma(neg ? -gh[l] : gh[l], y[u][l], c[l] * x[u][l]);
+          ny[l] = fma(neg ? -gl[l] : gl[l], x[u][l], c[l] * y[u][l]);
+        }
+        cst<IL>(pi + (int64_t)(ce[u] & kCompactIdx) * IL, nx);
+        cst<IL>(pj + (int64_t)((ce[u] >> 14) & kCompactIdx) * IL, ny);
       }
   }
 }
 
-// One flip-mask group: sum over its pairs of psi_k psi_{k^x} * sum_t w_t
-// (-1)^popc((k^x) & z_t); the CTA partial goes to part[blockIdx.x]. MULTI =
-// false: a one-term group (random strings), its term t1 passed by value.
-template <bool MULTI>
-__global__ void __launch_bounds__(kCompactThreads) k_compact_term(const double* __restrict__ psi, int na, int nb,
-                                                                  const uint32_t* __restrict__ stra,
-                                                                  const uint32_t* __restrict__ strb,
-                                                                  const uint16_t* __restrict__ ranka,
-                                                                  const uint16_t* __restrict__ rankb, CompactGroup gr,
-                                                                  const CompactTerm* __restrict__ terms,
-                                                                  CompactTerm t1, double2* __restrict__ part) {
-  __shared__ double2 red[kCompactThreads / 32];
-  const int ha = __popc(gr.xa) / 2, hb = __popc(gr.xb) / 2;
-  const CompactTerm* tt = terms + gr.t0;
-  double acc = 0.0;
-  for (int r = blockIdx.x; r < na; r += gridDim.x) {
-    const uint32_t a = __ldg(stra + r);
-    if (__popc(a & gr.xa) != ha) continue;
-    const uint32_t ap = a ^ gr.xa;
-    const int64_t ri = (int64_t)r * nb, rj = (int64_t)__ldg(ranka + ap) * nb;
-    double racc = 0.0;
-    constexpr int U = 4;
-    for (int c0 = threadIdx.x; c0 < nb; c0 += U * kCompactThreads) {
-      double v[U];
+// Generator without a beta flip: whole row pairs, 32-byte vectors (4 / IL
+// columns each), column signs from a bitmask (bit c of word c / 32).
+template <int IL>
+__global__ void __launch_bounds__(kCompactThreads) k_compact_gen_rows(double* __restrict__ psi, int64_t ld,
+                                                                      const uint32_t* __restrict__ rows,
+                                                                      const uint32_t* __restrict__ smask, int n_vec,
+                                                                      int chunk, const double* __restrict__ coef) {
+  constexpr int T = kCompactThreads, U = 4, V = 4 / IL;
+  const uint32_t re = __ldg(rows + blockIdx.x);
+  const uint32_t sa = re >> 28;
+  double* __restrict__ pi = psi + (int64_t)(re & kCompactIdx) * ld * IL;
+  double* __restrict__ pj = psi + (int64_t)((re >> 14) & kCompactIdx) * ld * IL;
+  double c[IL], gh[IL], gl[IL];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int col = c0 + u * kCompactThreads;
-        v[u] = 0.0;
-        if (col < nb) {
-          const uint32_t b = __ldg(strb + col);
-          if (__popc(b & gr.xb) == hb) {
-            const uint32_t bp = b ^ gr.xb;
-            const int cj = gr.xb ? __ldg(rankb + bp) : col;
-            const double p = psi[ri + col] * psi[rj + cj];
-            if (!MULTI) {
-              const uint32_t s = ((uint32_t)__popc(ap & t1.za) ^ (uint32_t)__popc(bp & t1.zb)) & 1u;
-              v[u] = s ? -t1.w * p : t1.w * p;
-            } else {
-              double f = 0.0;
-              for (int t = 0; t < gr.nt; ++t) {
-                const uint32_t s = ((uint32_t)__popc(ap & tt[t].za) ^ (uint32_t)__popc(bp & tt[t].zb)) & 1u;
-                f += s ? -tt[t].w : tt[t].w;
-              }
-              v[u] = f * p;
+  for (int l = 0; l < IL; ++l) {
+    c[l] = coef[l];
+    gh[l] = coef[IL + l];
+    gl[l] = coef[2 * IL + l];
+  }
+  const int v1 = min(n_vec, ((int)blockIdx.y + 1) * chunk);
+  for (int t0 = blockIdx.y * chunk + threadIdx.x; t0 < v1; t0 += U * T) {
+    double x[U][4], y[U][4];
+    uint32_t sg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = t0 + u * T;
+      if (v < v1) {
+        cld<4>(pi + 4 * (int64_t)v, x[u]);
+        cld<4>(pj + 4 * (int64_t)v, y[u]);
+        const int col = v * V;
+        sg[u] = __ldg(smask + (col >> 5)) >> (col & 31);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = t0 + u * T;
+      if (v < v1) {
+        double nx[4], ny[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int l = e % IL;
+          const bool neg = ((sa ^ (sg[u] >> (e / IL))) & 1u) != 0;
+          nx[e] = fma(neg ? -gh[l] : gh[l], y[u][e], c[l] * x[u][e]);
+          ny[e] = fma(neg ? -gl[l] : gl[l], x[u][e], c[l] * y[u][e]);
+        }
+        cst<4>(pi + 4 * (int64_t)v, nx);
+        cst<4>(pj + 4 * (int64_t)v, ny);
+      }
+    }
+  }
+}
+
+// All flip-mask groups of one kind in one launch: blockIdx.y = group, the CTAs
+// of a group stride over its row entries; thread partials in a fixed order,
+// CTA partial lane l to part[(group * gridDim.x + blockIdx.x) * IL + l].
+template <int IL, bool MULTI>
+__global__ void __launch_bounds__(kCompactThreads) k_compact_terms(const double* __restrict__ psi, int64_t ld,
+                                                                   const uint32_t* __restrict__ lists,
+                                                                   const CompactGroup* __restrict__ groups,
+                                                                   const CompactTerm* __restrict__ terms,
+                                                                   const uint32_t* __restrict__ stra,
+                                                                   const uint32_t* __restrict__ strb,
+                                                                   double* __restrict__ part) {
+  constexpr int T = kCompactThreads, U = IL == 4 ? 4 : 8;
+  __shared__ double2 red[T / 32];
+  const CompactGroup g = groups[blockIdx.y];
+  const uint32_t* __restrict__ cols = lists + g.col_off;
+  const CompactTerm* __restrict__ tt = terms + g.t0;
+  double acc[IL];
+#pragma unroll
+  for (int l = 0; l < IL; ++l) acc[l] = 0.0;
+  for (int r = blockIdx.x; r < g.n_rows; r += gridDim.x) {
+    const uint32_t re = __ldg(lists + g.row_off + r);
+    const uint32_t sa = re >> 28;
+    const double* __restrict__ pi = psi + (int64_t)(re & kCompactIdx) * ld * IL;
+    const double* __restrict__ pj = psi + (int64_t)((re >> 14) & kCompactIdx) * ld * IL;
+    const uint32_t a = MULTI ? __ldg(stra + (re & kCompactIdx)) : 0u;
+    double racc[IL];
+#pragma unroll
+    for (int l = 0; l < IL; ++l) racc[l] = 0.0;
+    for (int t0 = threadIdx.x; t0 < g.n_cols; t0 += U * T) {
+      uint32_t ce[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) ce[u] = t0 + u * T < g.n_cols ? __ldg(cols + t0 + u * T) : 0xFFFFFFFFu;
+      double x[U][IL], y[U][IL];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ce[u] != 0xFFFFFFFFu) {
+          cld<IL>(pi + (int64_t)(ce[u] & kCompactIdx) * IL, x[u]);
+          cld<IL>(pj + (int64_t)((ce[u] >> 14) & kCompactIdx) * IL, y[u]);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ce[u] != 0xFFFFFFFFu) {
+          if (!MULTI) {
+            const bool neg = ((sa ^ (ce[u] >> 28)) & 1u) != 0;
+#pragma unroll
+            for (int l = 0; l < IL; ++l) {
+              const double p = x[u][l] * y[u][l];
+              racc[l] += neg ? -p : p;
             }
+          } else {
+            const uint32_t b = __ldg(strb + (ce[u] & kCompactIdx));
+            double f = 0.0;
+            for (int t = 0; t < g.nt; ++t) {
+              const uint32_t s = ((uint32_t)__popc(a & tt[t].za) ^ (uint32_t)__popc(b & tt[t].zb)) & 1u;
+              f += s ? -tt[t].w : tt[t].w;
+            }
+#pragma unroll
+            for (int l = 0; l < IL; ++l) racc[l] = fma(f, x[u][l] * y[u][l], racc[l]);
           }
         }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) racc += v[u];
     }
-    acc += racc;
+#pragma unroll
+    for (int l = 0; l < IL; ++l) acc[l] += racc[l];
   }
+  double* out = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * IL;
+#pragma unroll
+  for (int l = 0; l < IL; l += 2) {
+    const double w = MULTI ? 1.0 : g.w;
+    const double2 tot = block_sum<T>(make_double2(acc[l] * w, l + 1 < IL ? acc[l + 1] * w : 0.0), red);
+    if (threadIdx.x == 0) {
+      out[l] = tot.x;
+      if (l + 1 < IL) out[l + 1] = tot.y;
+    }
+    __syncthreads();
+  }
+}
+
+// e[lane] = sum of part[slot][lane] over the slots in a fixed order
+template <int IL>
+__global__ void __launch_bounds__(kCompactThreads) k_compact_reduce(const double* __restrict__ part, int64_t n_slots,
+                                                                    double* __restrict__ e, double* __restrict__ im) {
+  __shared__ double2 red[kCompactThreads / 32];
+  const int lane = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n_slots; i += kCompactThreads) acc += part[i * IL + lane];
   const double2 tot = block_sum<kCompactThreads>(make_double2(acc, 0.0), red);
-  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+  if (threadIdx.x == 0) {
+    e[lane] = tot.x;
+    if (im) im[lane] = 0.0;
+  }
 }
 
 struct CompactProg {
   bool ok = false;
-  int m = 0, na = 0, nb = 0;
+  int m = 0, na = 0, nb = 0, ld = 0;
   int64_t hf_at = 0;
   std::vector<CompactOp> ops;
-  std::vector<CompactGroup> groups;  // flip-mask groups of the terms that can contribute
-  std::vector<CompactTerm> host_terms;
+  std::vector<CompactGroup> single, multi;  // one-term / multi-term flip-mask groups that can contribute
+  std::vector<uint32_t> host_lists;
+  int64_t gen_pairs = 0, term_pairs = 0;  // amplitude pairs per evaluation (statistics)
+  DevBuf<uint32_t> lists;
+  DevBuf<CompactGroup> groups_single, groups_multi;
   DevBuf<CompactTerm> terms;
-  DevBuf<uint32_t> stra, strb;
-  DevBuf<uint16_t> ranka, rankb;
+  DevBuf<uint32_t> stra, strb;  // string of a row / column rank
 };
 
 // bits of x selected by mask, packed low
@@ -180,10 +318,19 @@ inline uint32_t compact_pext(uint64_t x, uint64_t mask) {
   return out;
 }
 
-inline std::vector<uint32_t> strings_with(int m, int k) {
-  std::vector<uint32_t> out;
+// the m-bit strings of weight k, ordered by the key whose bit i is the
+// string's bit sig[i] (sig[0] varies fastest)
+inline std::vector<uint32_t> strings_with(int m, int k, const std::vector<int>& sig) {
+  std::vector<std::pair<uint32_t, uint32_t>> ks;
   for (uint32_t s = 0; s < (1u << m); ++s)
-    if (__builtin_popcount(s) == k) out.push_back(s);
+    if (__builtin_popcount(s) == k) {
+      uint32_t key = 0;
+      for (int i = 0; i < m; ++i) key |= ((s >> sig[i]) & 1u) << i;
+      ks.push_back({key, s});
+    }
+  std::sort(ks.begin(), ks.end());
+  std::vector<uint32_t> out;
+  for (const auto& p : ks) out.push_back(p.second);
   return out;
 }
 
@@ -199,49 +346,122 @@ CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64
   auto cp = std::make_shared<CompactProg>();
   const CompiledPlan& P = pl->cp;
   const uint64_t ev = 0x5555555555555555ull & ((n >= 64) ? ~0ull : ((1ull << n) - 1ull)), od = ev << 1;
+  struct Part {
+    uint32_t x, lo, z;
+    bool operator<(const Part& o) const { return std::tie(x, lo, z) < std::tie(o.x, o.lo, o.z); }
+  };
+  std::vector<std::pair<Part, Part>> parts;  // per op: alpha part, beta part
   bool ok = n % 2 == 0 && n / 2 <= 16 && plan_is_real(P) && !P.op_kind.empty();
   for (size_t op = 0; ok && op < P.op_kind.size(); ++op) {
     const FusedDesc& d = P.fused[P.op_idx[op]];
     const uint64_t lo = P.pair_bits[d.pair_off];
-    CompactOp o{compact_pext(d.x, ev), compact_pext(lo, ev), compact_pext(d.zout, ev),
-                compact_pext(d.x, od), compact_pext(lo, od), compact_pext(d.zout, od)};
-    ok = 2 * __builtin_popcount(o.la) == __builtin_popcount(o.xa) &&
-         2 * __builtin_popcount(o.lb) == __builtin_popcount(o.xb);
-    cp->ops.push_back(o);
+    const Part pa{compact_pext(d.x, ev), compact_pext(lo, ev), compact_pext(d.zout, ev)};
+    const Part pb{compact_pext(d.x, od), compact_pext(lo, od), compact_pext(d.zout, od)};
+    ok = 2 * __builtin_popcount(pa.lo) == __builtin_popcount(pa.x) &&
+         2 * __builtin_popcount(pb.lo) == __builtin_popcount(pb.x);
+    parts.push_back({pa, pb});
   }
   if (ok) {
     const int m = n / 2, ka = __builtin_popcountll(hf & ev), kb = __builtin_popcountll(hf & od);
-    const std::vector<uint32_t> sa = strings_with(m, ka), sb = strings_with(m, kb);
+    // beta significance: the least-flipped beta qubits vary fastest
+    std::vector<int> use(m, 0), sig_a(m), sig_b(m);
+    for (const auto& p : parts)
+      for (int q = 0; q < m; ++q) use[q] += (p.second.x >> q) & 1u;
+    for (int q = 0; q < m; ++q) sig_a[q] = sig_b[q] = q;
+    std::stable_sort(sig_b.begin(), sig_b.end(), [&](int p, int q) { return use[p] < use[q]; });
+    const std::vector<uint32_t> sa = strings_with(m, ka, sig_a), sb = strings_with(m, kb, sig_b);
     std::vector<uint16_t> ra(1u << m, 0), rb(1u << m, 0);
     for (size_t i = 0; i < sa.size(); ++i) ra[sa[i]] = (uint16_t)i;
     for (size_t i = 0; i < sb.size(); ++i) rb[sb[i]] = (uint16_t)i;
     cp->m = m;
     cp->na = (int)sa.size();
     cp->nb = (int)sb.size();
-    cp->hf_at = (int64_t)ra[compact_pext(hf, ev)] * cp->nb + rb[compact_pext(hf, od)];
-    std::map<uint64_t, std::vector<CompactTerm>> by_x;  // (xa, xb) -> terms, in upload order
+    cp->ld = (cp->nb + 3) & ~3;
+    cp->hf_at = (int64_t)ra[compact_pext(hf, ev)] * cp->ld + rb[compact_pext(hf, od)];
+    std::vector<uint32_t>& L = cp->host_lists;
+    auto par = [](uint32_t v) { return (uint32_t)__builtin_popcount(v) & 1u; };
+    // generator lists, shared by the ops with the same alpha / beta part
+    std::map<Part, std::pair<int32_t, int32_t>> rows_of, cols_of;
+    auto pair_list = [&](const Part& p, const std::vector<uint32_t>& str, const std::vector<uint16_t>& rk,
+                         std::map<Part, std::pair<int32_t, int32_t>>& memo) {
+      auto f = memo.find(p);
+      if (f != memo.end()) return f->second;
+      const int32_t off = (int32_t)L.size();
+      for (size_t i = 0; i < str.size(); ++i)
+        if ((str[i] & p.x) == p.lo) L.push_back((uint32_t)i | (uint32_t)rk[str[i] ^ p.x] << 14 | par(str[i] & p.z) << 28);
+      return memo[p] = {off, (int32_t)L.size() - off};
+    };
+    std::map<uint32_t, int32_t> mask_of;  // zb -> column sign bitmask
+    for (const auto& p : parts) {
+      CompactOp o{};
+      std::tie(o.row_off, o.n_rows) = pair_list(p.first, sa, ra, rows_of);
+      if (p.second.x) {
+        std::tie(o.col_off, o.n_cols) = pair_list(p.second, sb, rb, cols_of);
+      } else {
+        auto f = mask_of.find(p.second.z);
+        if (f == mask_of.end()) {
+          const int32_t off = (int32_t)L.size();
+          L.resize(L.size() + (size_t)(cp->ld + 31) / 32 + 1, 0u);
+          for (size_t i = 0; i < sb.size(); ++i) L[off + i / 32] |= par(sb[i] & p.second.z) << (i % 32);
+          f = mask_of.emplace(p.second.z, off).first;
+        }
+        o.col_off = f->second;
+        o.n_cols = 0;
+      }
+      cp->gen_pairs += (int64_t)o.n_rows * (o.n_cols ? o.n_cols : cp->nb);
+      cp->ops.push_back(o);
+    }
+    // Hamiltonian: flip-mask groups of the terms that can contribute
+    struct RawTerm {
+      uint32_t za, zb;
+      double w;
+    };
+    std::map<uint64_t, std::vector<RawTerm>> by_x;  // (xa, xb) -> terms, in upload order
     for (size_t t = 0; t < h->raw_x.size(); ++t) {
       const uint64_t x = h->raw_x[t], z = h->raw_z[t];
       const int ny = __builtin_popcountll(x & z) & 3;
-      // Re(c i^ny)
-      const double w = ny == 0 ? h->raw_re[t] : ny == 1 ? -h->raw_im[t] : ny == 2 ? -h->raw_re[t] : h->raw_im[t];
+      if (ny & 1) continue;  // the two orientations of every pair cancel (psi real)
+      const double w = ny == 0 ? h->raw_re[t] : -h->raw_re[t];  // Re(c i^ny)
       const uint32_t xa = compact_pext(x, ev), xb = compact_pext(x, od);
       if (w == 0.0 || __builtin_popcount(xa) % 2 || __builtin_popcount(xb) % 2) continue;
       if (__builtin_popcount(xa) / 2 > std::min(ka, m - ka) || __builtin_popcount(xb) / 2 > std::min(kb, m - kb))
         continue;  // no sector member can pair with a sector member
       by_x[((uint64_t)xa << 32) | xb].push_back({compact_pext(z, ev), compact_pext(z, od), w});
     }
-    std::vector<CompactTerm>& tl = cp->host_terms;
+    std::vector<CompactTerm> tl;
+    // members of one string set: every string whose flipped bits are half
+    // filled, or (once = true) only those with the lowest flipped bit clear
+    auto member_list = [&](uint32_t x, uint32_t z, bool once, const std::vector<uint32_t>& str,
+                           const std::vector<uint16_t>& rk, int32_t& off, int32_t& cnt) {
+      off = (int32_t)L.size();
+      const int half = __builtin_popcount(x) / 2;
+      const uint32_t low = x & (0u - x);
+      for (size_t i = 0; i < str.size(); ++i) {
+        if (__builtin_popcount(str[i] & x) != half || (once && (str[i] & low))) continue;
+        L.push_back((uint32_t)i | (uint32_t)rk[str[i] ^ x] << 14 | par(str[i] & z) << 28);
+      }
+      cnt = (int32_t)L.size() - off;
+    };
     for (const auto& kv : by_x) {
-      cp->groups.push_back({(uint32_t)(kv.first >> 32), (uint32_t)kv.first, (int32_t)tl.size(),
-                            (int32_t)kv.second.size()});
-      tl.insert(tl.end(), kv.second.begin(), kv.second.end());
+      const uint32_t xa = (uint32_t)(kv.first >> 32), xb = (uint32_t)kv.first;
+      const bool one = kv.second.size() == 1;
+      const double pw = (xa | xb) ? 2.0 : 1.0;  // unordered pairs once
+      CompactGroup g{};
+      member_list(xa, one ? kv.second[0].za : 0u, xa != 0, sa, ra, g.row_off, g.n_rows);
+      member_list(xb, one ? kv.second[0].zb : 0u, xa == 0 && xb != 0, sb, rb, g.col_off, g.n_cols);
+      g.t0 = (int32_t)tl.size();
+      g.nt = (int32_t)kv.second.size();
+      g.w = pw * kv.second[0].w;
+      for (const RawTerm& t : kv.second) tl.push_back({t.za, t.zb, pw * t.w});
+      cp->term_pairs += (int64_t)g.n_rows * g.n_cols;
+      (one ? cp->single : cp->multi).push_back(g);
     }
+    cp->lists.upload(L, ctx->stream);
+    cp->groups_single.upload(cp->single, ctx->stream);
+    cp->groups_multi.upload(cp->multi, ctx->stream);
     cp->terms.upload(tl, ctx->stream);
     cp->stra.upload(sa, ctx->stream);
     cp->strb.upload(sb, ctx->stream);
-    cp->ranka.upload(ra, ctx->stream);
-    cp->rankb.upload(rb, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
   }
   cp->ok = ok;
@@ -250,35 +470,69 @@ CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64
   return ok ? raw : nullptr;
 }
 
-// energies of `batch` theta rows (device) into e/im (device), one state at a time
-void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double* theta, int batch, double* e,
-                    double* im) {
-  const size_t dim = (size_t)cp.na * cp.nb;
-  ctx->compact_psi.alloc(dim);
-  ctx->compact_coef.alloc(3 * pl->cp.op_kind.size());
-  const int g = 32 * ctx->n_sm;  // term kernels: fixed grid (fixed partial slots)
-  const size_t nterm = cp.groups.size();
-  ctx->compact_part.alloc(std::max<size_t>(1, nterm * g));
+// IL theta rows (device, stride n_gen) -> e[0..IL) (device), the lanes interleaved in one matrix
+template <int IL>
+void compact_energy_lanes(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double* theta, double* e, double* im) {
+  constexpr int T = kCompactThreads;
+  const int64_t ld = cp.ld;
+  const size_t dim = (size_t)cp.na * ld * IL;
+  const int g = 4 * ctx->n_sm;  // CTAs per flip-mask group (fixed partial slots)
+  const size_t n_slots = std::max<size_t>(1, (cp.single.size() + cp.multi.size()) * g);
   const PlanDev pd = pl->dev();
   const int nops = (int)pl->cp.op_kind.size();
-  for (int b = 0; b < batch; ++b) {
-    CK(cudaMemsetAsync(ctx->compact_psi.p, 0, dim * sizeof(double), ctx->stream));
-    k_compact_set<<<1, 1, 0, ctx->stream>>>(ctx->compact_psi.p, cp.hf_at);
-    k_compact_coef<<<(nops + 127) / 128, 128, 0, ctx->stream>>>(pd, theta + (size_t)b * pl->cp.n_gen,
-                                                               ctx->compact_coef.p);
-    for (int op = 0; op < nops; ++op)
-      k_compact_gen<<<cp.na, kCompactThreads, 0, ctx->stream>>>(ctx->compact_psi.p, cp.na, cp.nb, cp.stra.p, cp.strb.p,
-                                                             cp.ranka.p, cp.rankb.p, cp.ops[op],
-                                                             ctx->compact_coef.p + 3 * op);
-    for (size_t t = 0; t < nterm; ++t)
-      (cp.groups[t].nt == 1 ? k_compact_term<false> : k_compact_term<true>)<<<g, kCompactThreads, 0, ctx->stream>>>(
-          ctx->compact_psi.p, cp.na, cp.nb, cp.stra.p, cp.strb.p, cp.ranka.p, cp.rankb.p, cp.groups[t], cp.terms.p,
-          cp.host_terms[cp.groups[t].t0], ctx->compact_part.p + t * g);
-    if (nterm == 0) CK(cudaMemsetAsync(ctx->compact_part.p, 0, sizeof(double2), ctx->stream));
-    k_reduce_partials<kThreads><<<1, kThreads, 0, ctx->stream>>>(ctx->compact_part.p,
-                                                                  (int64_t)std::max<size_t>(1, nterm * g), e + b,
-                                                                  im ? im + b : nullptr);
-    CK(cudaGetLastError());
-    ctx->launches += 4 + nops + (int64_t)nterm;
+  double* psi = ctx->compact_psi.p;
+  double* part = ctx->compact_part.p;
+  CK(cudaMemsetAsync(psi, 0, dim * sizeof(double), ctx->stream));
+  k_compact_set<IL><<<1, 32, 0, ctx->stream>>>(psi, cp.hf_at);
+  k_compact_coef<IL><<<(nops * IL + 127) / 128, 128, 0, ctx->stream>>>(pd, theta, pl->cp.n_gen, ctx->compact_coef.p);
+  const uint32_t* L = cp.lists.p;
+  for (int op = 0; op < nops; ++op) {
+    const CompactOp& o = cp.ops[op];
+    const double* coef = ctx->compact_coef.p + (size_t)3 * op * IL;
+    if (o.n_rows == 0) continue;
+    if (o.n_cols) {
+      constexpr int per = (IL == 4 ? 4 : 8) * T;
+      const int chunks = (o.n_cols + per - 1) / per, chunk = (o.n_cols + chunks - 1) / chunks;
+      k_compact_gen<IL><<<dim3(o.n_rows, chunks), T, 0, ctx->stream>>>(psi, ld, L + o.row_off, L + o.col_off, o.n_cols,
+                                                                      chunk, coef);
+    } else {
+      const int n_vec = (int)(ld * IL / 4), per = 4 * T;
+      const int chunks = (n_vec + per - 1) / per, chunk = (n_vec + chunks - 1) / chunks;
+      k_compact_gen_rows<IL><<<dim3(o.n_rows, chunks), T, 0, ctx->stream>>>(psi, ld, L + o.row_off, L + o.col_off,
+                                                                           n_vec, chunk, coef);
+    }
+  }
+  if (!cp.single.empty())
+    k_compact_terms<IL, false><<<dim3(g, (unsigned)cp.single.size()), T, 0, ctx->stream>>>(
+        psi, ld, L, cp.groups_single.p, cp.terms.p, cp.stra.p, cp.strb.p, part);
+  if (!cp.multi.empty())
+    k_compact_terms<IL, true><<<dim3(g, (unsigned)cp.multi.size()), T, 0, ctx->stream>>>(
+        psi, ld, L, cp.groups_multi.p, cp.terms.p, cp.stra.p, cp.strb.p, part + cp.single.size() * (size_t)g * IL);
+  if (cp.single.empty() && cp.multi.empty()) CK(cudaMemsetAsync(part, 0, IL * sizeof(double), ctx->stream));
+  k_compact_reduce<IL><<<IL, T, 0, ctx->stream>>>(part, (int64_t)n_slots, e, im);
+  CK(cudaGetLastError());
+  ctx->launches += 4 + nops + (cp.single.empty() ? 0 : 1) + (cp.multi.empty() ? 0 : 1);
+}
+
+// energies of `batch` theta rows (device) into e/im (device): the rows run in
+// groups of 4, 2 or 1 interleaved lanes (FFQ_COMPACT_IL caps the group size)
+void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double* theta, int batch, double* e,
+                    double* im) {
+  const int cap = ctx->compact_il >= 4 ? 4 : ctx->compact_il >= 2 ? 2 : 1;
+  const int il0 = std::min(cap, batch >= 4 ? 4 : batch >= 2 ? 2 : 1);
+  ctx->compact_psi.alloc((size_t)cp.na * cp.ld * il0);
+  ctx->compact_coef.alloc(3 * pl->cp.op_kind.size() * il0);
+  ctx->compact_part.alloc(std::max<size_t>(1, (cp.single.size() + cp.multi.size()) * 4 * ctx->n_sm) * il0);
+  const int ng = pl->cp.n_gen;
+  for (int b = 0; b < batch;) {
+    const int left = batch - b, il = std::min(cap, left >= 4 ? 4 : left >= 2 ? 2 : 1);
+    const double* th = theta + (size_t)b * ng;
+    if (il == 4)
+      compact_energy_lanes<4>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+    else if (il == 2)
+      compact_energy_lanes<2>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+    else
+      compact_energy_lanes<1>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+    b += il;
   }
 }

@@ -338,6 +338,38 @@ def test_compact_sector_path_matches_dense(monkeypatch, case):
     assert np.array_equal(out["compact"], out["compact2"])  # deterministic
 
 
+@pytest.mark.parametrize("case", ["config5_20q", "uccsd_16q"])
+def test_compact_interleaved_lanes_bit_identical(monkeypatch, case):
+    # the compact layout evaluates 4, 2 or 1 theta rows per matrix (lanes
+    # interleaved per amplitude); a batch of 7 runs as 4 + 2 + 1 and must equal
+    # the one-row-at-a-time energies bit for bit (same pair order per lane), and
+    # the dense support path to 1e-10
+    if case == "config5_20q":
+        P = problems.config5_problem(n_doubles=300, n_terms=200, n_qubits=20, n_elec=10)
+        rng = np.random.default_rng(3)
+        rows = np.concatenate([P.thetas, rng.uniform(-0.05, 0.05, size=(6, P.n_gen))])
+    else:
+        P = problems.make_problem(8, 8, problems.ham_seed(9, 2), batch=7)
+        rows = P.thetas
+    th = P.plan_thetas(rows)
+    out = {}
+    for mode, env in (("il4", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0"}),
+                      ("il1", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0", "FFQ_COMPACT_IL": "1"}),
+                      ("dense", {"FFQ_COMPACT": "0", "FFQ_SECTOR": "0"})):
+        for k in ("FFQ_COMPACT", "FFQ_COMPACT_MIN", "FFQ_COMPACT_IL", "FFQ_SECTOR"):
+            monkeypatch.delenv(k, raising=False)
+        c = _ctx(monkeypatch, env)
+        plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+        ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+        n0 = c.launches()
+        out[mode] = capi.energy_batch(c, plan, ham, P.hf, th)
+        out[mode + "_launches"] = c.launches() - n0
+        del plan, ham, c
+    assert np.array_equal(out["il4"], out["il1"])
+    assert out["il4_launches"] < out["il1_launches"] // 2  # 3 matrix passes instead of 7
+    assert np.max(np.abs(out["il4"] - out["dense"])) <= 1e-10
+
+
 def test_compact_sector_path_golden(monkeypatch):
     # the compact layout forced at configs 1-3 (FFQ_SECTOR=0 skips the closure
     # programs, FFQ_COMPACT_MIN=0 lets the compact path take every size) against
