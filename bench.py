@@ -517,9 +517,20 @@ def main():
         ctx.synchronize()
         t5 = time.perf_counter() - t5
         ms5 = timed(f5, 2)
+        # the same evaluation as 8 theta rows interleaved per matrix (one amplitude of
+        # 8 evaluations = one 64-byte DRAM atom: passes move algorithmic bytes only)
+        rows5 = np.concatenate([P5.thetas, np.random.default_rng(5).uniform(-0.05, 0.05, size=(7, P5.n_gen))])
+        th5b = torch.from_numpy(P5.plan_thetas(rows5)).to(cdev)
+        e5b = torch.zeros(8, dtype=torch.float64, device=cdev)
+        f5b = lambda: capi.energy_batch_device(ctx, plan5, ham5, P5.hf, 8, th5b.data_ptr(), e5b.data_ptr())  # noqa: E731
+        f5b()
+        ms5b = timed(f5b, 2)
         config5 = {"qubits": P5.n_qubits, "generators": P5.n_gen, "terms": len(P5.H), "energy": float(e5.item()),
                    "ms_per_eval": statistics.mean(ms5), "first_call_s_incl_compile": t5,
-                   "path": "compact real [C(16,8)][C(16,8)] sector layout, one GPU (no global qubits)"}
+                   "batch8_ms_per_eval": statistics.mean(ms5b) / 8,
+                   "batch8_row0_equals_single": bool(e5b[0].item() == e5.item()),
+                   "path": "compact real [C(16,8)][C(16,8)][lanes] sector layout, list-driven passes, one GPU "
+                           "(no global qubits)"}
         del plan5, ham5
 
     cpu = None

@@ -192,7 +192,7 @@ struct ffq_ctx_s {
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
   DevBuf<double> compact_psi, compact_coef, compact_part;  // compact real sector path (ffq_compact.inl)
-  int compact_il = 4;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4)
+  int compact_il = 8;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4, 8)
   int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
   int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
                                              // support path is faster below: grouped Hamiltonian)

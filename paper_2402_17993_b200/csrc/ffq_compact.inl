@@ -8,7 +8,7 @@
 //   row   = rank of the alpha string (even qubits, compressed),
 //   col   = rank of the beta string (odd qubits), row stride ld = cols rounded
 //           up to 4 (rows start on 32-byte sectors),
-//   lane  = one of IL in {1, 2, 4} theta rows of the batch evaluated together
+//   lane  = one of IL in {1, 2, 4, 8} theta rows of the batch evaluated together
 //           (the plan is shared by the batch). With IL = 4 one amplitude of
 //           four evaluations is exactly one 32-byte sector, so a pass moves
 //           its algorithmic bytes and nothing else.
@@ -66,7 +66,11 @@ __device__ __forceinline__ void cld(const double* p, double (&v)[IL]) {
     v[0] = t.x;
     v[1] = t.y;
   } else {
-    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+#pragma unroll
+    for (int q = 0; q < IL; q += 4)
+      asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(v[q]), "=d"(v[q + 1]), "=d"(v[q + 2]), "=d"(v[q + 3])
+                   : "l"(p + q));
   }
 }
 template <int IL>
@@ -76,8 +80,11 @@ __device__ __forceinline__ void cst(double* p, const double (&v)[IL]) {
   } else if constexpr (IL == 2) {
     *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
   } else {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-                 : "memory");
+#pragma unroll
+    for (int q = 0; q < IL; q += 4)
+      asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + q), "d"(v[q]), "d"(v[q + 1]), "d"(v[q + 2]),
+                   "d"(v[q + 3])
+                   : "memory");
   }
 }
 
@@ -107,11 +114,11 @@ __global__ void k_compact_set(double* __restrict__ psi, int64_t at) {
 // Generator with a beta flip: CTA = (row entry, column chunk); every load of a
 // trip is issued before its stores (the pairs of one op are disjoint).
 template <int IL>
-__global__ void __launch_bounds__(kCompactThreads) k_compact_gen(double* __restrict__ psi, int64_t ld,
+__global__ void __launch_bounds__(kCompactThreads, IL == 8 ? 2 : 1) k_compact_gen(double* __restrict__ psi, int64_t ld,
                                                                  const uint32_t* __restrict__ rows,
                                                                  const uint32_t* __restrict__ cols, int n_cols,
                                                                  int chunk, const double* __restrict__ coef) {
-  constexpr int T = kCompactThreads, U = IL == 4 ? 4 : 8;
+  constexpr int T = kCompactThreads, U = IL <= 2 ? 8 : 16 / IL;
   const uint32_t re = __ldg(rows + blockIdx.x);
   const uint32_t sa = re >> 28;
   double* __restrict__ pi = psi + (int64_t)(re & kCompactIdx) * ld * IL;
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_gen_rows(double* __
                                                                       const uint32_t* __restrict__ rows,
                                                                       const uint32_t* __restrict__ smask, int n_vec,
                                                                       int chunk, const double* __restrict__ coef) {
-  constexpr int T = kCompactThreads, U = 4, V = 4 / IL;
+  constexpr int T = kCompactThreads, U = 4;
   const uint32_t re = __ldg(rows + blockIdx.x);
   const uint32_t sa = re >> 28;
   double* __restrict__ pi = psi + (int64_t)(re & kCompactIdx) * ld * IL;
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_gen_rows(double* __
       if (v < v1) {
         cld<4>(pi + 4 * (int64_t)v, x[u]);
         cld<4>(pj + 4 * (int64_t)v, y[u]);
-        const int col = v * V;
+        const int col = (int)((int64_t)v * 4 / IL);
         sg[u] = __ldg(smask + (col >> 5)) >> (col & 31);
       }
     }
@@ -191,10 +198,21 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_gen_rows(double* __
         double nx[4], ny[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int l = e % IL;
-          const bool neg = ((sa ^ (sg[u] >> (e / IL))) & 1u) != 0;
-          nx[e] = fma(neg ? -gh[l] : gh[l], y[u][e], c[l] * x[u][e]);
-          ny[e] = fma(neg ? -gl[l] : gl[l], x[u][e], c[l] * y[u][e]);
+          // element e of vector v: lane (4 v + e) % IL of column (4 v + e) / IL
+          const bool neg = ((sa ^ (sg[u] >> (IL >= 4 ? 0 : e / IL))) & 1u) != 0;
+          double cc, hh, gg;
+          if constexpr (IL == 8) {  // the vector's parity picks the lane half (no dynamic indexing)
+            const bool hi = (v & 1) != 0;
+            cc = hi ? c[(4 + e) % IL] : c[e];
+            hh = hi ? gh[(4 + e) % IL] : gh[e];
+            gg = hi ? gl[(4 + e) % IL] : gl[e];
+          } else {
+            cc = c[e % IL];
+            hh = gh[e % IL];
+            gg = gl[e % IL];
+          }
+          nx[e] = fma(neg ? -hh : hh, y[u][e], cc * x[u][e]);
+          ny[e] = fma(neg ? -gg : gg, x[u][e], cc * y[u][e]);
         }
         cst<4>(pi + 4 * (int64_t)v, nx);
         cst<4>(pj + 4 * (int64_t)v, ny);
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_terms(const double*
                                                                    const uint32_t* __restrict__ stra,
                                                                    const uint32_t* __restrict__ strb,
                                                                    double* __restrict__ part) {
-  constexpr int T = kCompactThreads, U = IL == 4 ? 4 : 8;
+  constexpr int T = kCompactThreads, U = IL <= 2 ? 8 : 16 / IL;
   __shared__ double2 red[T / 32];
   const CompactGroup g = groups[blockIdx.y];
   const uint32_t* __restrict__ cols = lists + g.col_off;
@@ -491,7 +509,7 @@ void compact_energy_lanes(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const 
     const double* coef = ctx->compact_coef.p + (size_t)3 * op * IL;
     if (o.n_rows == 0) continue;
     if (o.n_cols) {
-      constexpr int per = (IL == 4 ? 4 : 8) * T;
+      constexpr int per = (IL <= 2 ? 8 : 16 / IL) * T;
       const int chunks = (o.n_cols + per - 1) / per, chunk = (o.n_cols + chunks - 1) / chunks;
       k_compact_gen<IL><<<dim3(o.n_rows, chunks), T, 0, ctx->stream>>>(psi, ld, L + o.row_off, L + o.col_off, o.n_cols,
                                                                       chunk, coef);
@@ -515,24 +533,30 @@ void compact_energy_lanes(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const 
 }
 
 // energies of `batch` theta rows (device) into e/im (device): the rows run in
-// groups of 4, 2 or 1 interleaved lanes (FFQ_COMPACT_IL caps the group size)
+// groups of 8, 4, 2 or 1 interleaved lanes (FFQ_COMPACT_IL caps the group size)
 void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double* theta, int batch, double* e,
                     double* im) {
-  const int cap = ctx->compact_il >= 4 ? 4 : ctx->compact_il >= 2 ? 2 : 1;
-  const int il0 = std::min(cap, batch >= 4 ? 4 : batch >= 2 ? 2 : 1);
+  auto lanes = [&](int left) {
+    const int cap = ctx->compact_il >= 8 ? 8 : ctx->compact_il >= 4 ? 4 : ctx->compact_il >= 2 ? 2 : 1;
+    return std::min(cap, left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1);
+  };
+  const int il0 = lanes(batch);
   ctx->compact_psi.alloc((size_t)cp.na * cp.ld * il0);
   ctx->compact_coef.alloc(3 * pl->cp.op_kind.size() * il0);
   ctx->compact_part.alloc(std::max<size_t>(1, (cp.single.size() + cp.multi.size()) * 4 * ctx->n_sm) * il0);
   const int ng = pl->cp.n_gen;
   for (int b = 0; b < batch;) {
-    const int left = batch - b, il = std::min(cap, left >= 4 ? 4 : left >= 2 ? 2 : 1);
+    const int il = lanes(batch - b);
     const double* th = theta + (size_t)b * ng;
-    if (il == 4)
-      compact_energy_lanes<4>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+    double* imb = im ? im + b : nullptr;
+    if (il == 8)
+      compact_energy_lanes<8>(ctx, pl, cp, th, e + b, imb);
+    else if (il == 4)
+      compact_energy_lanes<4>(ctx, pl, cp, th, e + b, imb);
     else if (il == 2)
-      compact_energy_lanes<2>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+      compact_energy_lanes<2>(ctx, pl, cp, th, e + b, imb);
     else
-      compact_energy_lanes<1>(ctx, pl, cp, th, e + b, im ? im + b : nullptr);
+      compact_energy_lanes<1>(ctx, pl, cp, th, e + b, imb);
     b += il;
   }
 }

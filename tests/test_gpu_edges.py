@@ -340,20 +340,21 @@ def test_compact_sector_path_matches_dense(monkeypatch, case):
 
 @pytest.mark.parametrize("case", ["config5_20q", "uccsd_16q"])
 def test_compact_interleaved_lanes_bit_identical(monkeypatch, case):
-    # the compact layout evaluates 4, 2 or 1 theta rows per matrix (lanes
-    # interleaved per amplitude); a batch of 7 runs as 4 + 2 + 1 and must equal
-    # the one-row-at-a-time energies bit for bit (same pair order per lane), and
-    # the dense support path to 1e-10
+    # the compact layout evaluates 8, 4, 2 or 1 theta rows per matrix (lanes
+    # interleaved per amplitude); a batch of 15 runs as 8 + 4 + 2 + 1 (9 as 8 + 1)
+    # and must equal the one-row-at-a-time energies bit for bit (same pair order
+    # per lane), and the dense support path to 1e-10
     if case == "config5_20q":
         P = problems.config5_problem(n_doubles=300, n_terms=200, n_qubits=20, n_elec=10)
         rng = np.random.default_rng(3)
-        rows = np.concatenate([P.thetas, rng.uniform(-0.05, 0.05, size=(6, P.n_gen))])
+        rows = np.concatenate([P.thetas, rng.uniform(-0.05, 0.05, size=(8, P.n_gen))])
     else:
-        P = problems.make_problem(8, 8, problems.ham_seed(9, 2), batch=7)
+        P = problems.make_problem(8, 8, problems.ham_seed(9, 2), batch=15)
         rows = P.thetas
     th = P.plan_thetas(rows)
     out = {}
-    for mode, env in (("il4", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0"}),
+    for mode, env in (("il8", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0"}),
+                      ("il4", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0", "FFQ_COMPACT_IL": "4"}),
                       ("il1", {"FFQ_COMPACT_MIN": "0", "FFQ_SECTOR": "0", "FFQ_COMPACT_IL": "1"}),
                       ("dense", {"FFQ_COMPACT": "0", "FFQ_SECTOR": "0"})):
         for k in ("FFQ_COMPACT", "FFQ_COMPACT_MIN", "FFQ_COMPACT_IL", "FFQ_SECTOR"):
@@ -365,9 +366,9 @@ def test_compact_interleaved_lanes_bit_identical(monkeypatch, case):
         out[mode] = capi.energy_batch(c, plan, ham, P.hf, th)
         out[mode + "_launches"] = c.launches() - n0
         del plan, ham, c
-    assert np.array_equal(out["il4"], out["il1"])
-    assert out["il4_launches"] < out["il1_launches"] // 2  # 3 matrix passes instead of 7
-    assert np.max(np.abs(out["il4"] - out["dense"])) <= 1e-10
+    assert np.array_equal(out["il8"], out["il1"]) and np.array_equal(out["il4"], out["il1"])
+    assert out["il8_launches"] < out["il4_launches"] < out["il1_launches"] // 2  # fewer matrix passes
+    assert np.max(np.abs(out["il8"] - out["dense"])) <= 1e-10
 
 
 def test_compact_sector_path_golden(monkeypatch):
