@@ -278,7 +278,9 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
   // {m, m^X} once as 2 Re(conj(psi[m^X]) psi[m] b(m)) (X != 0) and the
   // diagonal group as |psi[m]|^2 b(m). m runs over the inserted bits Q:
   //   table mode (|X| <= 6): Q = X, b(m) = sum_o sgn(m & zout_o) F_o[pattern]
-  //   generic mode:          Q = {lowest bit of X}, one class per term.
+  //   generic mode:          Q = {highest bit of X}, one class per term (members and
+  //                          partners then run over contiguous index ranges: whole
+  //                          32-byte sectors for any X).
   CompiledHam H;
   H.n_qubits = n;
   H.n_terms = 0;
@@ -354,7 +356,7 @@ inline CompiledHam compile_ham(int n, int64_t nt, const uint64_t* x, const uint6
     } else {
       H.has_generic = true;
       d.w = 1;
-      d.q[0] = __builtin_ctzll(X);
+      d.q[0] = 63 - __builtin_clzll(X);
       d.qpack = pack_q(d.q, 1);
       d.nact = 1;
       H.act_bits.push_back(0);

@@ -280,8 +280,14 @@ __global__ void __launch_bounds__(NT) k_expect_items(const double2* __restrict__
   const int64_t u1 = min(U, u0 + h.item_chunk);
   const uint64_t pb = h.act_bits[d.act_off + p];
   double2 acc = make_double2(0, 0);
-  for (int64_t u = u0 + threadIdx.x; u < u1; u += NT) {
-    const uint64_t m = insert_bits<uint64_t>((uint64_t)u, d.qpack, d.w) | pb;
+  // members with the X bits clear, stepped by NT with a masked add (the carries
+  // run through the X positions): no per-member bit insertion
+  uint64_t Q = 0;  // inserted positions: all of X in table mode, X's highest bit in generic mode
+  for (int i = 0; i < d.w; ++i) Q |= 1ULL << ((d.qpack >> (6 * i)) & 63u);
+  const uint64_t step = insert_bits<uint64_t>((uint64_t)NT, d.qpack, d.w);
+  uint64_t mz = insert_bits<uint64_t>((uint64_t)(u0 + threadIdx.x), d.qpack, d.w);
+  for (int64_t u = u0 + threadIdx.x; u < u1; u += NT, mz = ((mz | Q) + step) & ~Q) {
+    const uint64_t m = mz | pb;
     const double2 a = s[m];
     if (a.x == 0.0 && a.y == 0.0) continue;  // zero product: skip partner load and classes
     const double2 bb = s[m ^ d.x];
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(NT) k_expect_shard(const double2* __restrict__
   const GroupDesc d = h.groups[g];
   const uint64_t lmask = (1ULL << l) - 1ULL;
   const uint64_t XL = d.x & lmask;
-  // inserted (pattern-fixed) positions: all of X in table mode, X's lowest bit in generic mode
+  // inserted (pattern-fixed) positions: all of X in table mode, X's highest bit in generic mode
   uint64_t Q = 0;
   for (int i = 0; i < d.w; ++i) Q |= 1ULL << ((d.qpack >> (6 * i)) & 63u);
   const uint32_t QG = (uint32_t)(Q >> l);
