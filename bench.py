@@ -362,6 +362,24 @@ def main():
         "ms_per_rotation": run_avg / 16,
         "speedup_vs_unfused_passes": 16 * statistics.mean(rot_ms[2:]) / run_avg,
     }
+    # gathered tiles: 2 rotations whose flip masks sit on qubits 0-4 and the top 7
+    # qubits (the tile is 128 strided 512-byte pieces, one bulk copy each)
+    gx = np.array([(int(v) & 31) | ((int(v) >> 5) << (nq - 7)) for v in run_x[:2]], np.uint64)
+    gather_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(12):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st.rotate_many(gx, run_z[:2], run_th[:2] * (1 if k % 2 == 0 else -1))
+            b.record(stream)
+            b.synchronize()
+            gather_ms.append(a.elapsed_time(b))
+    g_avg = statistics.mean(gather_ms[2:])
+    rotation_run["gathered_tiles_2_rotations"] = {
+        "ms_per_run": g_avg, "hbm_gbs": 32 * (1 << nq) / (g_avg / 1e3) / 1e9,
+        "hbm_frac": 32 * (1 << nq) / (g_avg / 1e3) / 1e9 / peak,
+        "note": "flip masks on qubits 0-4 and the top 7: tiles of 128 x 512-byte pieces, cp.async.bulk each way"}
     del st
     rot_bytes = 32 * (1 << nq)
     rot_avg = statistics.mean(rot_ms[2:])

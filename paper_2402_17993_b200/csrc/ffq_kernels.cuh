@@ -426,6 +426,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// shared -> global bulk copy of this thread's bulk group; the generic-proxy
+// writes to the tile must be fenced (fence_async_smem) before it is issued
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -512,7 +523,7 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
   // those of blockIdx.x; tile coordinate m <-> index base | pdep(m, q).
   // q = the low t bits: one contiguous block, staged by bulk copies. Otherwise
   // q holds the low 5 bits, so 32 consecutive m are 512 contiguous bytes
-  // (coalesced 32-byte vector gathers through a 2^(t-5)-entry offset table).
+  // (one 512-byte bulk copy per entry of a 2^(t-5)-entry offset table).
   extern __shared__ __align__(128) double2 tl[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint64_t hi_off[128];
@@ -537,6 +548,8 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
   }
   double2* s = psi + ((int64_t)blockIdx.y << n) + base;
   const double2* csb = cs + (int64_t)blockIdx.y * cs_stride;
+  // the tile arrives by bulk copies (TMA) on one mbarrier: two 32 KiB pieces when
+  // q is the low t bits, else one 512-byte piece per offset-table entry
   if (low) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
@@ -560,14 +573,13 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
       }
       hi_off[j] = o;
     }
-    __syncthreads();
-    for (uint32_t m = 2 * threadIdx.x; m < tsize; m += 2 * NT) {
-      double2 a, b;
-      ld256(s + (hi_off[m >> 5] | (m & 31u)), a, b);
-      tl[m] = a;
-      tl[m + 1] = b;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, tsize * (uint32_t)sizeof(double2));
     }
     __syncthreads();
+    for (uint32_t j = threadIdx.x; j < (tsize >> 5); j += NT) bulk_g2s(tl + 32 * j, s + hi_off[j], 512, &bar);
+    mbar_wait(&bar, 0);
   }
   for (int g = 0; g < n_grp; ++g) {
     const RotGroup G = grp[g];
@@ -622,10 +634,20 @@ __global__ void __launch_bounds__(NT, 3) k_rotation_run(double2* __restrict__ ps
     }
     __syncthreads();
   }
-  if (low)
-    for (uint32_t k = 2 * threadIdx.x; k < tsize; k += 2 * NT) st256(s + k, tl[k], tl[k + 1]);
-  else
-    for (uint32_t m = 2 * threadIdx.x; m < tsize; m += 2 * NT) st256(s + (hi_off[m >> 5] | (m & 31u)), tl[m], tl[m + 1]);
+  // write-back by bulk copies from the tile (the last group's barrier precedes)
+  fence_async_smem();
+  __syncthreads();
+  if (low) {
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = tsize * (uint32_t)sizeof(double2), piece = 32768;
+      for (uint32_t off = 0; off < bytes; off += piece)
+        bulk_s2g((char*)s + off, (const char*)tl + off, min(piece, bytes - off));
+      bulk_commit_wait_read();
+    }
+  } else if (threadIdx.x < (tsize >> 5)) {
+    for (uint32_t j = threadIdx.x; j < (tsize >> 5); j += NT) bulk_s2g(s + hi_off[j], tl + 32 * j, 512);
+    bulk_commit_wait_read();
+  }
 }
 
 // ---- shared-memory-resident evaluator (n <= 13) ------------------------------
