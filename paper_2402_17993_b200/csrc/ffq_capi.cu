@@ -193,6 +193,7 @@ struct ffq_ctx_s {
   DevBuf<double2> cs, partial, slab;
   DevBuf<double> compact_psi, compact_coef, compact_part;  // compact real sector path (ffq_compact.inl)
   int compact_il = 8;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4, 8)
+  int sector_warm = 1;                       // env FFQ_WARM=0: no L2 warm-up pass before small sector batches
   int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
   int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
                                              // support path is faster below: grouped Hamiltonian)
@@ -257,6 +258,8 @@ struct ffq_plan_s {
     DevBuf<uint32_t> eps_flip, cq_rows;
     DevBuf<int32_t> cq_desc, cq_warp;
     DevBuf<double> cq_coef;
+    DevBuf<ulonglong2> warm;  // (address, bytes) of every table (k_l2_warm)
+    int n_warm = 0;
     bool real = false;  // real-amplitude program (k_sector_eval_real)
   };
   std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SectorDevBufs>> sectors;  // (ham uid, hf)
@@ -586,6 +589,22 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
         b->row_fim.upload(b->prog.row_fim, ctx->stream);
         b->pf_im.upload(b->prog.pf_im, ctx->stream);
       }
+      std::vector<ulonglong2> warm;
+      auto range = [&](const void* p, size_t bytes) {
+        if (p && bytes) warm.push_back(make_ulonglong2((unsigned long long)(uintptr_t)p, (unsigned long long)bytes));
+      };
+      range(b->gen_off.p, b->prog.gen_off.size() * sizeof(int64_t));
+      range(b->gen_pairs.p, b->prog.gen_pairs.size() * sizeof(uint32_t));
+      range(b->row_pairs.p, b->prog.row_pairs.size() * sizeof(uint32_t));
+      range(b->row_fre.p, b->prog.row_fre.size() * sizeof(double));
+      range(b->pf_re.p, b->prog.pf_re.size() * sizeof(double));
+      range(b->blk_warp.p, b->blk_warp.p ? b->prog.blk_warp.size() * sizeof(int32_t) : 0);
+      range(b->blk_stream.p, b->blk_stream.p ? b->prog.blk_stream.size() * sizeof(uint32_t) : 0);
+      range(b->cq_rows.p, b->cq_rows.p ? b->prog.cq_rows.size() * sizeof(uint32_t) : 0);
+      range(b->cq_desc.p, b->cq_desc.p ? b->prog.cq_desc.size() * sizeof(int32_t) : 0);
+      range(b->cq_coef.p, b->cq_coef.p ? b->prog.cq_coef.size() * sizeof(double) : 0);
+      b->n_warm = (int)warm.size();
+      b->warm.upload(warm, ctx->stream);
       CK(cudaStreamSynchronize(ctx->stream));
     }
     it = pl->sectors.emplace(key, std::move(b)).first;
@@ -628,6 +647,8 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.cq_desc = cq ? reinterpret_cast<const int4*>(b.cq_desc.p) : nullptr;
   sd.cq_warp = cq ? reinterpret_cast<const int2*>(b.cq_warp.p) : nullptr;
   sd.cq_coef = cq ? b.cq_coef.p : nullptr;
+  sd.warm = b.warm.p;
+  sd.n_warm = b.n_warm;
   return &sd;
 }
 
@@ -668,6 +689,11 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   if (NT == 32 * 32 && !state_out)
     while (split * 2 <= ctx->sector_split && (int64_t)batch * split * 2 <= ctx->n_sm) split *= 2;
   if (split > 1) ctx->warp_sums.alloc((size_t)batch * 32);
+  // a batch on less than half of the SMs: all SMs pull the tables into L2 first
+  if (2 * batch * split <= ctx->n_sm && sd.n_warm > 0 && ctx->sector_warm) {
+    k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
+    ctx->launches++;
+  }
   k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
                                                                  clk, split, ctx->warp_sums.p, state_out);
   CK(cudaGetLastError());
@@ -887,6 +913,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_COMPACT")) c->compact = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_IL")) c->compact_il = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_WARM")) c->sector_warm = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);

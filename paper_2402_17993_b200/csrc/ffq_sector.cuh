@@ -54,7 +54,22 @@ struct SectorDev {
   const int4* cq_desc;          // [warp tasks][32]: columns 0-3, columns 4-5, row begin, row end
   const int2* cq_warp;          // [warps]: warp-task range
   const double* cq_coef;        // [warp tasks][15][32]
+  // host side only: the (address, bytes) ranges of the tables above, for k_l2_warm
+  const ulonglong2* warm;
+  int n_warm;
 };
+
+// Pull table ranges into L2 with every SM: a batch far below the SM count would
+// otherwise stream its ~13 MB of tables through the few SMs that compute, at
+// single-SM HBM bandwidth, whenever the tables are not L2-resident.
+__global__ void k_l2_warm(const ulonglong2* __restrict__ ranges, int n) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < n; ++r) {
+    const ulonglong2 rg = ranges[r];
+    for (uint64_t off = t * 128; off < rg.y; off += stride * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rg.x + off));
+  }
+}
 
 // Amplitude slots (SectorProgram::slot_bits): 15 - log2(CL) offset bits, the
 // owning rank above them. Addresses are 32-bit shared::cluster addresses (the
