@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rot-qubits", type=int, default=28)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the sharded-state NCCL leg (child processes)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -551,6 +552,41 @@ def main():
                            "(no global qubits)"}
         del plan5, ham5
 
+    # sharded state over NCCL: BASELINE config 5's recipe at 26
+    # qubits (1 GiB of complex128) split on log2(N) global qubits, one CHILD
+    # process per rank (tools/shard_nccl_leg.py: a transport failure cannot take
+    # this line with it), half-shard swaps by ncclSend/ncclRecv, max over ranks
+    sharded = None
+    if world & (world - 1) == 0 and (world == 1 or backend == "nccl") and not args.no_sharded:
+        g_sh = world.bit_length() - 1
+        ids = [capi.nccl_unique_id().hex() if (rank == 0 and world > 1) else "self"]
+        if dist:
+            dist.broadcast_object_list(ids, src=0)
+        leg = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools", "shard_nccl_leg.py")
+        try:
+            r = subprocess.run([sys.executable, leg, "26", str(g_sh), str(rank), ids[0], str(gpu)],
+                               capture_output=True, text=True, timeout=420)
+            mine = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {
+                "error": (r.stderr or r.stdout)[-300:]}
+        except Exception as ex:  # timeout, no output
+            mine = {"error": repr(ex)[:300]}
+        legs = [mine]
+        if dist:
+            legs = [None] * world
+            dist.all_gather_object(legs, mine)
+        if rank == 0:
+            bad = [x for x in legs if "error" in x]
+            if bad:
+                sharded = {"unavailable": bad[0]["error"], "n_gpus": world}
+            else:
+                sharded = {"n_qubits": 26, "global_qubits": g_sh, "n_gpus": world,
+                           "shard_gib": legs[0]["shard_gib"], "swaps_per_eval": legs[0]["swaps_per_eval"],
+                           "ms_per_eval": max(x["ms_per_eval"] for x in legs), "energy": legs[0]["energy"],
+                           "ranks_agree": all(x["energy"] == legs[0]["energy"] for x in legs),
+                           "repeatable": all(x["repeatable"] for x in legs),
+                           "note": "dense sharded path (k_fused_gen / k_expect_shard per shard); scaling strong: "
+                                   "compare ms_per_eval across --gpus N"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = 2
@@ -592,7 +628,8 @@ def main():
                           "config3_dense_slab_path": dense_path,
                           "config2_12q": config2,
                           "config4_fmo": config4, "config3_strong_scaling": strong,
-                          "config5_32q": config5, "rotation_run_28q": rotation_run,
+                          "config5_32q": config5, "sharded_state_nccl_26q": sharded,
+                          "rotation_run_28q": rotation_run,
                           "rotation_pass_18q_b256": rot18},
             "clocks": clk.summary(),
         }
