@@ -193,6 +193,7 @@ struct ffq_ctx_s {
   DevBuf<double2> cs, partial, slab;
   DevBuf<double> compact_psi, compact_coef, compact_part;  // compact real sector path (ffq_compact.inl)
   int compact_il = 8;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4, 8)
+  int sector_roles = 1;                      // env FFQ_ROLES=0: split evaluations without role warps
   int sector_warm = 1;                       // env FFQ_WARM=0: no L2 warm-up pass before small sector batches
   int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
   int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
@@ -648,6 +649,9 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.cq_warp = cq ? reinterpret_cast<const int2*>(b.cq_warp.p) : nullptr;
   sd.cq_coef = cq ? b.cq_coef.p : nullptr;
   sd.warm = b.warm.p;
+  sd.max_warp_tasks = 0;
+  for (size_t w2 = 0; w2 + 1 < b.prog.cq_warp.size(); w2 += 2)
+    sd.max_warp_tasks = std::max(sd.max_warp_tasks, b.prog.cq_warp[w2 + 1] - b.prog.cq_warp[w2]);
   sd.n_warm = b.n_warm;
   return &sd;
 }
@@ -694,8 +698,18 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
     k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
     ctx->launches++;
   }
+  // role warps (split evaluations of the 1024-thread program): each of the
+  // 32 / split warp shares of a CTA gets `roles` warps (generic rows, block
+  // stream, clique tasks); needs >= 3 warps per share and the exchange buffer
+  // ([share][1 + tasks][32] doubles) inside the per-op tables
+  int roles = 0;
+  if (split > 1 && ctx->sector_roles) {
+    const int r = 32 / (32 / split);
+    const size_t need = (size_t)(32 / split) * (1 + sd.max_warp_tasks) * 32 * sizeof(double);
+    if (r >= 3 && need <= pl->cp.op_kind.size() * 2 * sizeof(double2)) roles = r;
+  }
   k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
-                                                                 clk, split, ctx->warp_sums.p, state_out);
+                                                                 clk, split, ctx->warp_sums.p, state_out, roles);
   CK(cudaGetLastError());
   ctx->launches++;
   if (split > 1) {
@@ -914,6 +928,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_IL")) c->compact_il = std::atoi(e);
     if (const char* e = std::getenv("FFQ_WARM")) c->sector_warm = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_ROLES")) c->sector_roles = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FFQ_SECTOR_CL")) {
       const int v = std::atoi(e);

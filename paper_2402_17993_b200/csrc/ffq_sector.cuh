@@ -57,6 +57,7 @@ struct SectorDev {
   // host side only: the (address, bytes) ranges of the tables above, for k_l2_warm
   const ulonglong2* warm;
   int n_warm;
+  int max_warp_tasks;  // most clique tasks of one warp share
 };
 
 // Pull table ranges into L2 with every SM: a batch far below the SM count would
@@ -486,47 +487,54 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
 // lane = (Xa, clique T), rows k of Xa: u = psi'[a_k][T], v = psi'[a_k ^ Xa][T]
 // (psi' in the alpha-first gauge), acc_ij += s_k (u_i v_j + u_j v_i), then
 // sum_ij C_ij acc_ij. The row word of the next row is in flight.
+// One warp task: lane = (Xa, clique T); returns sum_ij C_ij acc_ij (a chain from 0).
+__device__ __forceinline__ double clique_task(const SectorDev& sd, int wt, int lane, const double* amp) {
+  const int4 d = __ldg(sd.cq_desc + (size_t)wt * 32 + lane);
+  double acc[kCliquePairs];
+#pragma unroll
+  for (int p = 0; p < kCliquePairs; ++p) acc[p] = 0.0;
+  uint32_t rn = d.z < d.w ? __ldg(sd.cq_rows + d.z) : 0u;
+  for (int k = d.z; k < d.w; ++k) {
+    const uint32_t rw = rn;
+    if (k + 1 < d.w) rn = __ldg(sd.cq_rows + k + 1);
+    const double* ra = amp + (rw & 0x7FFFu);
+    const double* rb = amp + ((rw >> 15) & 0x7FFFu);
+    const int sg = (int)(rw & 0x80000000u);
+    // columns stay packed (bytes of d.x, d.y): extracted per row, not held
+    auto col = [&](int i) { return ((uint32_t)(i < 4 ? d.x : d.y) >> (8 * (i & 3))) & 0xFFu; };
+    double u[kCliqueMax];
+#pragma unroll
+    for (int i = 0; i < kCliqueMax; ++i) {
+      const double x = ra[col(i)];
+      u[i] = __hiloint2double(__double2hiint(x) ^ sg, __double2loint(x));
+    }
+    // v one column at a time (register budget of the 1024-thread CTA):
+    // acc_ij += u_i v_j for every i != j, pair index of (min, max)
+#pragma unroll
+    for (int j = 0; j < kCliqueMax; ++j) {
+      const double v = rb[col(j)];
+#pragma unroll
+      for (int i = 0; i < kCliqueMax; ++i)
+        if (i != j) {
+          const int a = i < j ? i : j, b = i < j ? j : i;
+          const int p = a * (2 * kCliqueMax - a - 1) / 2 + (b - a - 1);
+          acc[p] = fma(u[i], v, acc[p]);
+        }
+    }
+  }
+  const double* cf = sd.cq_coef + (size_t)wt * kCliquePairs * 32 + lane;
+  double tot = 0.0;
+#pragma unroll
+  for (int p = 0; p < kCliquePairs; ++p) tot = fma(__ldg(cf + p * 32), acc[p], tot);
+  return tot;
+}
+
+// A warp share's clique tasks: the task totals added in task order (the order
+// the role warps of a split evaluation reproduce from shared memory).
 __device__ __forceinline__ double clique_tasks(const SectorDev& sd, int warp, int lane, const double* amp) {
   const int2 wr = __ldg(sd.cq_warp + warp);
   double tot = 0.0;
-  for (int wt = wr.x; wt < wr.y; ++wt) {
-    const int4 d = __ldg(sd.cq_desc + (size_t)wt * 32 + lane);
-    double acc[kCliquePairs];
-#pragma unroll
-    for (int p = 0; p < kCliquePairs; ++p) acc[p] = 0.0;
-    uint32_t rn = d.z < d.w ? __ldg(sd.cq_rows + d.z) : 0u;
-    for (int k = d.z; k < d.w; ++k) {
-      const uint32_t rw = rn;
-      if (k + 1 < d.w) rn = __ldg(sd.cq_rows + k + 1);
-      const double* ra = amp + (rw & 0x7FFFu);
-      const double* rb = amp + ((rw >> 15) & 0x7FFFu);
-      const int sg = (int)(rw & 0x80000000u);
-      // columns stay packed (bytes of d.x, d.y): extracted per row, not held
-      auto col = [&](int i) { return ((uint32_t)(i < 4 ? d.x : d.y) >> (8 * (i & 3))) & 0xFFu; };
-      double u[kCliqueMax];
-#pragma unroll
-      for (int i = 0; i < kCliqueMax; ++i) {
-        const double x = ra[col(i)];
-        u[i] = __hiloint2double(__double2hiint(x) ^ sg, __double2loint(x));
-      }
-      // v one column at a time (register budget of the 1024-thread CTA):
-      // acc_ij += u_i v_j for every i != j, pair index of (min, max)
-#pragma unroll
-      for (int j = 0; j < kCliqueMax; ++j) {
-        const double v = rb[col(j)];
-#pragma unroll
-        for (int i = 0; i < kCliqueMax; ++i)
-          if (i != j) {
-            const int a = i < j ? i : j, b = i < j ? j : i;
-            const int p = a * (2 * kCliqueMax - a - 1) / 2 + (b - a - 1);
-            acc[p] = fma(u[i], v, acc[p]);
-          }
-      }
-    }
-    const double* cf = sd.cq_coef + (size_t)wt * kCliquePairs * 32 + lane;
-#pragma unroll
-    for (int p = 0; p < kCliquePairs; ++p) tot = fma(__ldg(cf + p * 32), acc[p], tot);
-  }
+  for (int wt = wr.x; wt < wr.y; ++wt) tot += clique_task(sd, wt, lane, amp);
   return tot;
 }
 
@@ -536,7 +544,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
                                                             int n_rows, long long* __restrict__ phase_clk,
                                                             int split, double* __restrict__ warp_sums,
-                                                            double* __restrict__ state_out) {
+                                                            double* __restrict__ state_out, int roles) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
   // split > 1 (small batches): `split` CTAs run one evaluation; each runs the
@@ -640,11 +648,11 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
       if ((__ldg(sd.eps_flip + (i >> 5)) >> (i & 31u)) & 1u) amp[i] = -amp[i];
     __syncthreads();
   }
-  double acc = 0.0;
-  const bool mine = split == 1 || (threadIdx.x >> 5) % split == part;
-  if (mine) {
-    constexpr int NW = NT / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31;
+  // warp share `warp`: its generic rows (shared-f rows, then per-pair-f rows), one chain
+  auto generic_rows = [&](int warp) -> double {
+    double acc = 0.0;
     const int32_t* es = sd.secs;  // one section: every pair is local
     const int sh0 = es[3], shn = (es[4] - es[3]) / 4;
     const int r0 = sh0 + 4 * (int)((int64_t)shn * warp / NW), r1 = sh0 + 4 * (int)((int64_t)shn * (warp + 1) / NW);
@@ -699,6 +707,50 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
         acc = fma(amp[(w >> 15) & 0x7FFFu] * amp[w & 0x7FFFu], fr, acc);
       }
     }
+    return acc;
+  };
+  double acc = 0.0;
+  if (split > 1 && roles >= 3) {
+    // Split evaluation with role warps: this CTA serves the shares w = part + split * si;
+    // each share gets `roles` physical warps: 0 its generic rows, 1 its anchored
+    // block stream, 2.. its clique tasks (task k on role 2 + k % (roles - 2)). Every
+    // piece is the value the one-CTA kernel computes for it; role 0 adds them in the
+    // one-CTA kernel's order (generic + blocks, then the clique task totals in task
+    // order), so the energy bits are the same. The exchange buffer overlays the
+    // per-op tables (dead after the generator phase).
+    double* xch = reinterpret_cast<double*>(cs);  // [share][1 + max_warp_tasks][32]
+    const int pw = threadIdx.x >> 5, si = pw / roles, role = pw % roles;
+    const int w = part + split * si;
+    const int2 wr = sd.cq_warp ? __ldg(sd.cq_warp + w) : make_int2(0, 0);
+    double* xs = xch + (size_t)si * (1 + sd.max_warp_tasks) * 32 + lane;
+    if (role == 0) {
+      acc = generic_rows(w);
+    } else if (role == 1) {
+      xs[0] = sd.blk_warp ? blk_stream(sd, w, lane, amp, sft) : 0.0;
+    } else {
+      for (int wt = wr.x + role - 2; wt < wr.y; wt += roles - 2) xs[(1 + wt - wr.x) * 32] = clique_task(sd, wt, lane, amp);
+    }
+    __syncthreads();
+    if (role != 0) return;
+    if (sd.blk_warp) acc += xs[0];
+    if (sd.cq_warp) {
+      double tot = 0.0;
+      for (int k = 0; k < wr.y - wr.x; ++k) tot += xs[(1 + k) * 32];
+      acc += tot;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);  // block_sum's first stage
+    if (lane == 0) warp_sums[(int64_t)row * NW + w] = acc;
+    if (threadIdx.x == 0 && phase_clk) {
+      phase_clk[2 * row] = clk1 - clk0;
+      phase_clk[2 * row + 1] = clock64() - clk1;
+    }
+    return;
+  }
+  const bool mine = split == 1 || (threadIdx.x >> 5) % split == part;
+  if (mine) {
+    const int warp = threadIdx.x >> 5;
+    acc = generic_rows(warp);
     if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
     if (sd.cq_warp) acc += clique_tasks(sd, warp, lane, amp);      // this warp's alpha-beta cliques
   }

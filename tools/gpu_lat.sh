@@ -1,4 +1,5 @@
-mkdir -p gpurun_out/r02c
-timeout 1200 python bench.py > gpurun_out/r02c/bench.log 2>&1; echo "bench rc=$?"
-tail -c 600 gpurun_out/r02c/bench.log
-BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02c/bench2.log 2>&1; echo "rc=$?"; tail -c 300 gpurun_out/r02c/bench2.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -q -x -k "split or identical or sector or golden" 2>&1 | tail -3
+LAT_ENV="FFQ_ROLES=1;FFQ_ROLES=0;FFQ_ROLES=1,FFQ_SPLIT=4" python tools/latency_cold.py
+LAT_ENV="FFQ_ROLES=1;FFQ_ROLES=0" python tools/latency.py
+PT_BATCH=1 python tools/phase_real.py 2>&1 | tail -2
+SWEEP_BATCH=1121 SWEEP_SLAB=256 python tools/sweep.py 2>&1 | tail -2
