@@ -723,7 +723,10 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
                    double* e, double* im) {
   static const bool clocks = std::getenv("FFQ_PHASE_CLOCKS") != nullptr;
   DevBuf<long long> clk;
-  if (clocks) clk.alloc(2 * (size_t)batch);
+  if (clocks) {
+    clk.alloc(2 * (size_t)batch + 32);
+    CK(cudaMemsetAsync(clk.p, 0, (2 * (size_t)batch + 32) * sizeof(long long), ctx->stream));
+  }
   long long* cp = clocks ? clk.p : nullptr;
   if (sd.real) {
     if (sd.size <= kSectorSingleMax)
@@ -737,13 +740,18 @@ void launch_sector(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd, con
     default: launch_sector_t<8, kSectorThreads>(ctx, pl, sd, theta, batch, e, im, cp); break;
   }
   if (clocks) {
-    std::vector<long long> hc(2 * (size_t)batch);
+    std::vector<long long> hc(2 * (size_t)batch + 32);
     CK(cudaMemcpyAsync(hc.data(), clk.p, hc.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     double g = 0, x = 0;
     for (int r = 0; r < batch; ++r) { g += (double)hc[2 * r]; x += (double)hc[2 * r + 1]; }
     std::fprintf(stderr, "[ffq] sector rows=%d avg cycles: generators %.0f expectation %.0f\n", batch,
                  g / batch, x / batch);
+    if (hc[2 * (size_t)batch]) {  // per-warp expectation cycles of row 0 (one-CTA real program)
+      std::fprintf(stderr, "[ffq] row 0 expectation cycles per warp:");
+      for (int w = 0; w < 32; ++w) std::fprintf(stderr, " %lld", hc[2 * (size_t)batch + w]);
+      std::fprintf(stderr, "\n");
+    }
   }
 }
 

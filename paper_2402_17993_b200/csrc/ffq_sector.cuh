@@ -753,6 +753,8 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     acc = generic_rows(warp);
     if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
     if (sd.cq_warp) acc += clique_tasks(sd, warp, lane, amp);      // this warp's alpha-beta cliques
+    // diagnostics: per-warp expectation cycles of row 0 behind the per-row pairs
+    if (phase_clk && split == 1 && row == 0 && lane == 0) phase_clk[2 * n_rows + warp] = clock64() - clk1;
   }
   if (split > 1) {
     if ((threadIdx.x >> 5) % split != part) return;
