@@ -565,7 +565,7 @@ def main():
         leg = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools", "shard_nccl_leg.py")
         try:
             r = subprocess.run([sys.executable, leg, "26", str(g_sh), str(rank), ids[0], str(gpu)],
-                               capture_output=True, text=True, timeout=420)
+                               capture_output=True, text=True, timeout=300)
             mine = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {
                 "error": (r.stderr or r.stdout)[-300:]}
         except Exception as ex:  # timeout, no output
@@ -618,6 +618,7 @@ def main():
                     "d2h_bytes_per_step": int(16 * B)},
             "roofline": {"bound": "hbm", "kernel": "k_pauli_rotation (generic rotation pass)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "traffic": ROT_TRAFFIC_BYTES if nq == 28 else None,
                          "traffic_source": "profiles/r01/ncu_full_summaries.txt (dram read+write per launch)",
                          "peak_source": peak_src,
