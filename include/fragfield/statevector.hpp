@@ -107,6 +107,11 @@ class Statevector {
   int n_, batch_;
 };
 
+/// Compile and cache the device program of (plan, H, hf) ahead of the first
+/// energy call (ffq_energy_prepare); safe to call from several host threads for
+/// distinct plans of one device.
+void prepare(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf);
+
 /// energy_trotter for a batch of amplitude vectors given in
 /// plan order: e[b] = <HF| U(theta_b)^dag H U(theta_b) |HF>.
 std::vector<double> energy_batch(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H,

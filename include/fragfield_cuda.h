@@ -123,6 +123,14 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
 int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits,
                             int batch, const double* theta_dev, double* e_dev,
                             double* imag_dev);
+/* Compile and cache the program ffq_energy_batch(_device) runs for (plan, ham,
+ * hf_bits) -- the support-closure program, or the compact sector lists from 27
+ * qubits up -- without evaluating anything (otherwise compiled on the first
+ * energy call: ~1-2 s of host work at 18 qubits). The one entry point that is
+ * re-entrant per context: host threads may call it concurrently for DISTINCT
+ * plans of one context (the VQE driver of SPEC.md:566 compiles its fragments in
+ * parallel before the serial optimiser loops). */
+int ffq_energy_prepare(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits);
 /* Support-closure program that ffq_energy_batch(_device) runs for (plan, ham,
  * hf_bits) (compiled on first use and cached): out[0] closure size |S|,
  * out[1] CTAs per evaluation, out[2] generator pairs, out[3] expectation

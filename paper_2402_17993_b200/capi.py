@@ -39,6 +39,7 @@ _SIGS = {
     "ffq_plan_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ffq_energy_batch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, _f64p, _f64p]),
     "ffq_energy_batch_device": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, _vp, _vp, _vp]),
+    "ffq_energy_prepare": (C.c_int, [_vp, _vp, _vp, C.c_uint64]),
     "ffq_state_alloc": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "ffq_state_free": (C.c_int, [_vp]),
     "ffq_state_set_basis": (C.c_int, [_vp, C.c_uint64]),
@@ -257,6 +258,11 @@ SECTOR_INFO_KEYS = ("closure_size", "ctas_per_eval", "generator_pairs", "expecta
                     "expectation_rows", "cluster_barrier_steps", "split_mask", "chunk_buffer_amplitudes",
                     "real_amplitudes", "block_pairs", "slots", "clique_pairs", "clique_warp_tasks",
                     "clique_conflicts", "clique_lane_rows")
+
+
+def energy_prepare(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int):
+    """Compile and cache the program energy_batch runs for these handles (thread-safe for distinct plans)."""
+    check(lib().ffq_energy_prepare(ctx.h, plan.h, ham.h, hf_bits), ctx.h)
 
 
 def sector_state(ctx: Context, plan: Plan, ham: Hamiltonian, hf_bits: int, theta, n_qubits: int):

@@ -1104,6 +1104,19 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
   });
 }
 
+int ffq_energy_prepare(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits) {
+  if (!ctx || !plan || !ham) return fail(ctx, FFQ_EINVAL, "ffq_energy_prepare: invalid argument");
+  return guarded(ctx, [&] {
+    const int n = plan->cp.n_qubits;
+    if (ham->ch.n_qubits != n) throw BadInput("plan and Hamiltonian qubit counts differ", FFQ_EINVAL);
+    if (n < 64 && (hf_bits >> n) != 0) throw BadInput("hf_bits exceeds n_qubits", FFQ_EINVAL);
+    // the same order as energy_device: sector program first, then the compact layout
+    if (ctx->sector && sector_program(ctx, plan, ham, hf_bits)) return FFQ_OK;
+    if (ctx->compact && n >= ctx->compact_min_qubits) compact_program(ctx, plan, ham, hf_bits);
+    return FFQ_OK;
+  });
+}
+
 int ffq_sector_state(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, const double* theta,
                      double* psi, double* energy) {
   if (!ctx || !plan || !ham || !theta || !psi) return fail(ctx, FFQ_EINVAL, "ffq_sector_state: invalid argument");

@@ -6,6 +6,7 @@
 // (reference proj/core/src/fmo.cpp:28-48).
 #include <algorithm>
 #include <cctype>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,7 +15,9 @@
 #include <numeric>
 #include <random>
 #include <sstream>
+#include <memory>
 #include <string>
+#include <thread>
 
 #include "fragfield/errors.hpp"
 #include "fragfield/fmo_batch.hpp"
@@ -757,6 +760,10 @@ std::vector<double> energy_batch(Device& dev, const DevicePlan& plan, const Devi
   return e;
 }
 
+void prepare(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf) {
+  check_ffq(ffq_energy_prepare(dev.handle(), plan.handle(), H.handle(), hf), dev.handle());
+}
+
 double energy_trotter(Device& dev, const std::vector<double>& amps, const DevicePlan& plan,
                       const DeviceHamiltonian& H, uint64_t hf) {
   return energy_batch(dev, plan, H, hf, plan.plan().plan_theta(amps), 1)[0];
@@ -1142,14 +1149,44 @@ std::map<std::string, double> evaluate_fragments(Device& dev, const std::vector<
   std::vector<double> costs;
   for (auto& f : frags) costs.push_back(fragment_cost(f));
   const std::vector<int> owner = shard_by_cost(costs, world);
-  std::map<std::string, double> out;
-  for (size_t i = 0; i < frags.size(); ++i) {
-    if (owner[i] != rank) continue;
-    const FragmentProblem& f = frags[i];
-    DeviceHamiltonian H(dev, f.hamiltonian);
-    DevicePlan P(dev, f.plan);
-    out[f.label] = energy_trotter(dev, f.amplitudes, P, H, f.hf) - f.e_reference;
+  // this rank's fragments: upload, compile every device program on its own host
+  // thread (ffq_energy_prepare is re-entrant for distinct plans), then evaluate
+  std::vector<const FragmentProblem*> mine;
+  for (size_t i = 0; i < frags.size(); ++i)
+    if (owner[i] == rank) mine.push_back(&frags[i]);
+  const bool dbg = std::getenv("FFQ_DEBUG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ffq] evaluate_fragments %-10s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  std::vector<std::unique_ptr<DeviceHamiltonian>> Hs;
+  std::vector<std::unique_ptr<DevicePlan>> Ps;
+  for (const FragmentProblem* f : mine) {
+    Hs.emplace_back(new DeviceHamiltonian(dev, f->hamiltonian));
+    Ps.emplace_back(new DevicePlan(dev, f->plan));
   }
+  lap("uploads");
+  std::vector<std::thread> workers;
+  std::vector<std::exception_ptr> errs(mine.size());
+  for (size_t i = 0; i < mine.size(); ++i)
+    workers.emplace_back([&, i] {
+      try {
+        prepare(dev, *Ps[i], *Hs[i], mine[i]->hf);
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& w : workers) w.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  lap("compile");
+  std::map<std::string, double> out;
+  for (size_t i = 0; i < mine.size(); ++i)
+    out[mine[i]->label] = energy_trotter(dev, mine[i]->amplitudes, *Ps[i], *Hs[i], mine[i]->hf) - mine[i]->e_reference;
+  lap("energies");
   return out;
 }
 

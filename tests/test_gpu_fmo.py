@@ -77,3 +77,48 @@ def test_multi_capi_equals_one_context_bitwise():
         assert np.array_equal(e, capi.energy_batch(ctx, pl, hm, F.hf, th))
     with pytest.raises(ff.ContractViolation):
         capi.Multi([0, 0])
+
+
+def test_energy_prepare_concurrent_compile_equals_lazy_compile():
+    """ffq_energy_prepare compiles the device program ahead of the first energy
+    call and is re-entrant for distinct plans of one context: three fragments
+    prepared from three host threads give the energies of the lazily compiled
+    programs bit for bit, and the first energy call no longer pays the compile."""
+    import threading
+    import time
+
+    import numpy as np
+
+    from paper_2402_17993_b200 import capi, problems
+
+    frs = [problems.make_problem(9, 10, problems.ham_seed(4, 10 + k)) for k in range(2)]
+    frs.append(problems.make_problem(6, 6, problems.ham_seed(4, 1)))
+    lazy = []
+    c0 = capi.Context(0)
+    for P in frs:
+        plan = capi.Plan(c0, P.n_qubits, *P.plan_arrays())
+        ham = capi.Hamiltonian(c0, P.n_qubits, *P.ham_arrays())
+        lazy.append(capi.energy_batch(c0, plan, ham, P.hf, P.plan_thetas()))
+        del plan, ham
+    c1 = capi.Context(0)
+    hs = [(capi.Plan(c1, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c1, P.n_qubits, *P.ham_arrays())) for P in frs]
+    errs = []
+
+    def work(k):
+        try:
+            capi.energy_prepare(c1, hs[k][0], hs[k][1], frs[k].hf)
+        except Exception as ex:  # surfaced below
+            errs.append(ex)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(len(frs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    t0 = time.perf_counter()
+    eager = [capi.energy_batch(c1, hs[k][0], hs[k][1], frs[k].hf, frs[k].plan_thetas()) for k in range(len(frs))]
+    first_calls_s = time.perf_counter() - t0
+    for a, b in zip(lazy, eager):
+        assert np.array_equal(a, b)
+    assert first_calls_s < 0.5  # three evaluations without a compile
