@@ -34,7 +34,7 @@ NCCL_INC = os.path.join(NCCL_DIR, "include")
 NCCL_LIB = os.path.join(NCCL_DIR, "lib")
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INC,
                   "-I" + NCCL_INC, "-ccbin", CXX]
-# experiments only (tools/*.sh): extra nvcc defines, e.g. FFQ_NVCC_EXTRA="-DFFQ_EXP_NOROT"
+# experiments only: extra nvcc flags (e.g. FFQ_NVCC_EXTRA="-DSOME_EXPERIMENT")
 NVFLAGS += os.environ.get("FFQ_NVCC_EXTRA", "").split()
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-I" + INC, "-I/usr/local/cuda/include"]
 

@@ -249,7 +249,7 @@ struct ffq_plan_s {
   struct SectorDevBufs {
     SectorProgram prog;
     DevBuf<int64_t> gen_off;
-    DevBuf<uint32_t> gen_pairs, row_pairs;
+    DevBuf<uint32_t> gen_pairs, gen_head, row_pairs;
     DevBuf<int32_t> secs;
     DevBuf<uint8_t> gen_flags, op_cross;
     DevBuf<double> row_fre, row_fim, pf_re, pf_im;
@@ -498,6 +498,8 @@ constexpr int kSectorSingleThreads = 256;  // one-CTA evaluations (small closure
 constexpr int kSectorRealThreads = 1024;   // one-CTA real-amplitude evaluations of large closures
 // small closures run one CTA per evaluation (many per SM); large ones a 2^s-CTA cluster
 constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA
+static_assert(kSectorHeadSmall == kSectorSingleThreads && kSectorHeadLarge == kSectorRealThreads,
+              "gen_head is compiled for the real program's thread counts");
 constexpr uint32_t kSectorMaxSize = 32767;   // 15-bit pair indices
 
 // cluster size for a closure of `size` amplitudes: 1 when it fits a small CTA,
@@ -522,12 +524,15 @@ size_t sector_real_smem_bytes(size_t size, size_t n_ops) {
   return (((size + 1) * sizeof(double) + 15) & ~(size_t)15) + n_ops * (2 * sizeof(double2) + sizeof(uint2)) + 16;
 }
 
-// every fused op with one pattern pair and real F (UCCSD: F = +-1)
+// every fused op with one pattern pair and real antisymmetric F (UCCSD: F = +-1)
 bool plan_is_real(const CompiledPlan& P) {
   if (P.n_string_ops() > 0) return false;
   for (size_t op = 0; op < P.op_kind.size(); ++op) {
     const FusedDesc& d = P.fused[P.op_idx[op]];
     if (d.npair != 1 || P.pair_f[4 * d.pair_off + 1] != 0.0 || P.pair_f[4 * d.pair_off + 3] != 0.0) return false;
+    // a real unitary 2x2 block with equal diagonal is a rotation: F_hi = -F_lo
+    // (the real programs turn a pair's sign into a swap of its members)
+    if (P.pair_f[4 * d.pair_off + 2] != -P.pair_f[4 * d.pair_off]) return false;
   }
   return true;
 }
@@ -565,6 +570,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     if (b->prog.ok) {
       b->gen_off.upload(b->prog.gen_off, ctx->stream);
       b->gen_pairs.upload(b->prog.gen_pairs, ctx->stream);
+      if (!b->prog.gen_head.empty()) b->gen_head.upload(b->prog.gen_head, ctx->stream);
       b->gen_flags.upload(b->prog.gen_flags, ctx->stream);
       b->op_cross.upload(b->prog.op_cross, ctx->stream);
       b->row_pairs.upload(b->prog.row_pairs, ctx->stream);
@@ -596,6 +602,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
       };
       range(b->gen_off.p, b->prog.gen_off.size() * sizeof(int64_t));
       range(b->gen_pairs.p, b->prog.gen_pairs.size() * sizeof(uint32_t));
+      range(b->gen_head.p, b->prog.gen_head.size() * sizeof(uint32_t));
       range(b->row_pairs.p, b->prog.row_pairs.size() * sizeof(uint32_t));
       range(b->row_fre.p, b->prog.row_fre.size() * sizeof(double));
       range(b->pf_re.p, b->prog.pf_re.size() * sizeof(double));
@@ -625,6 +632,7 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
   sd.n_ops = (int)pl->cp.op_kind.size();
   sd.gen_off = b.gen_off.p;
   sd.gen_pairs = b.gen_pairs.p;
+  sd.gen_head = b.gen_head.p;
   sd.gen_flags = b.gen_flags.p;
   sd.buf_off = b.prog.buf_off;
   sd.buf_len = b.prog.buf_len;
@@ -1529,6 +1537,18 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
             seen[k] = op;
           }
         }
+      // the head table repeats the first 2 head_threads words of every op (bit 30: more follow)
+      const int NT = S.head_threads;
+      if (NT <= 0 || S.gen_head.size() != (size_t)(n_ops + kSectorHeadPad) * 2 * NT) ++bad;
+      for (int op = 0; NT > 0 && op < n_ops + kSectorHeadPad; ++op)
+        for (int t = 0; t < 2 * NT; ++t) {
+          const uint32_t hw = S.gen_head[(size_t)2 * op * NT + t];
+          const int64_t at = op < n_ops ? S.gen_off[op] + t : -1;
+          const bool have = op < n_ops && at < S.gen_off[op + 1];
+          const bool more = have && t >= NT && at + NT < S.gen_off[op + 1];
+          if (!have ? hw != 0xFFFFFFFFu : hw != (S.gen_pairs[at] | (more ? 1u << 30 : 0u))) ++bad;
+        }
+      for (uint32_t w : S.gen_pairs) bad += (w >> 30) != 0;  // signs are swaps in the real program
       for (uint32_t w : S.row_pairs)
         if ((w & 0x7FFFu) > S.n_slots || ((w >> 15) & 0x7FFFu) > S.n_slots) ++bad;
       for (size_t w = 0; w < S.blk_warp.size() / 4; ++w) {

@@ -34,6 +34,8 @@
 namespace ffq {
 
 using cplx = std::complex<double>;
+constexpr int kSectorHeadPad = 8;   // empty ops behind gen_head (>= the kernel's prefetch depth)
+constexpr int kSectorHeadSmall = 256, kSectorHeadLarge = 1024;  // threads of the real one-CTA program
 constexpr int kMaxTableBits = 6;  // |X| up to 6 -> pattern tables of <= 64 entries
 
 struct BadInput : std::invalid_argument {
@@ -656,6 +658,15 @@ struct SectorProgram {
   std::vector<int64_t> gen_off;     // [n_ops * n_parts + 1]: op g, owner rank r -> gen_off[g * n_parts + r]
   std::vector<uint32_t> gen_pairs;  // slot_i | slot_j << 15 | sgn(k & zout) < 0 << 30 (i: low-pattern member)
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
+  // Real one-CTA program (elem_bytes 8, one part): a negative sign swaps the
+  // pair's members instead (F_hi = -F_lo: the 2x2 block is a rotation, so the
+  // swapped pair is the same arithmetic bit for bit) and bit 30 stays clear in
+  // gen_pairs. gen_head[(2 op + h) * head_threads + tid] is thread tid's h-th
+  // pair word of op (0xFFFFFFFF: none), bit 30 of the second word set when the
+  // thread has further words in gen_pairs (ops with more than 2 head_threads
+  // pairs); kSectorHeadPad all-empty ops follow (prefetch never leaves the table).
+  std::vector<uint32_t> gen_head;
+  int head_threads = 0;
   // Expectation pairs, slot_i | slot_j << 15 | sign << 30 (i: enumerated m,
   // j: m ^ X), in rows of 32 (one per warp lane). A row holds pairs of one
   // (group, pattern) set owned by one CTA; sets are padded to whole rows with
@@ -1263,6 +1274,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
                                     bool cliques = false) {
   // lanes per conflict-free shared-memory wavefront for this amplitude size
   const int bank_group = elem_bytes == 8 ? 16 : 8;
+  const bool real_prog = elem_bytes == 8 && n_parts == 1;  // k_sector_eval_real's tables
   SectorProgram S;
   const int n = P.n_qubits;
   S.n = n;
@@ -1523,6 +1535,10 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         pi.push_back((uint32_t)idx[e.first]);
         pj.push_back((uint32_t)idx[e.first ^ (uint32_t)d.x]);
         fl.push_back(e.second);
+        if (real_prog && (fl.back() & 1u)) {  // the sign as a swap of the members
+          std::swap(pi.back(), pj.back());
+          fl.back() &= (uint8_t)~1u;
+        }
         ri.push_back(bank_slot(pi.back()));
         rj.push_back(bank_slot(pj.back()));
       }
@@ -1531,6 +1547,18 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         S.gen_flags.push_back(fl[t]);
       }
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
+    }
+  }
+  if (real_prog) {
+    const int NT = S.size <= block_min_size ? kSectorHeadSmall : kSectorHeadLarge;
+    S.head_threads = NT;
+    S.gen_head.assign((size_t)(n_ops + kSectorHeadPad) * 2 * NT, 0xFFFFFFFFu);
+    for (int op = 0; op < n_ops; ++op) {
+      const int64_t b0 = S.gen_off[op], b1 = S.gen_off[op + 1];
+      for (int64_t t = b0; t < std::min<int64_t>(b1, b0 + 2 * NT); ++t)
+        S.gen_head[((size_t)2 * op + (size_t)((t - b0) / NT)) * NT + (size_t)((t - b0) % NT)] = S.gen_pairs[t];
+      for (int64_t t = b0 + 2 * NT; t < std::min<int64_t>(b1, b0 + 3 * NT); ++t)
+        S.gen_head[((size_t)2 * op + 1) * NT + (size_t)(t - b0 - 2 * NT)] |= 1u << 30;  // more words follow
     }
   }
   stage("generator pairs");

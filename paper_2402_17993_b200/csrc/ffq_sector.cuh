@@ -32,6 +32,7 @@ struct SectorDev {
   const uint8_t* op_cross;      // [n_ops] 1: the generator has pairs across CTAs (cluster barrier)
   const int64_t* gen_off;       // [CL * n_ops + 1], per op and owner rank
   const uint32_t* gen_pairs;    // slot_i | slot_j << 15 | sign << 30
+  const uint32_t* gen_head;     // real one-CTA program: per-thread head words (SectorProgram::gen_head)
   const uint8_t* gen_flags;     // pattern pair index << 1 (read only for multi-pattern ops)
   // expectation rows in sections (SectorProgram::ExpSection): 32 pair words each
   int32_t sec_off[kSectorMaxParts + 1];
@@ -581,44 +582,35 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   __syncthreads();
   const uint32_t tid = threadIdx.x;
   // each thread's first two pair words of the next D steps are in flight
-  // across the barriers (steps have up to ~2 NT pairs). The step loop is
-  // unrolled by D so the in-flight registers are never copied (a copy
+  // across the barriers (steps have up to ~2 NT pairs), read from the head
+  // table at a fixed per-thread stride (no range lookup; 0xFFFFFFFF = none;
+  // the table ends with empty ops, so the prefetch needs no bound). The step
+  // loop is unrolled by D so the in-flight registers are never copied (a copy
   // would wait for the load).
+  const uint32_t* hp = sd.gen_head + tid;
   auto first_words = [&](int op) -> uint2 {
-    if (op >= sd.n_ops) return make_uint2(0u, 0u);
-#if defined(FFQ_EXP_NOPREF)
-    return make_uint2(0u, 0u);
-#endif
-    const uint2 se = gse[op];
-    return make_uint2(se.x + tid < se.y ? __ldg(sd.gen_pairs + se.x + tid) : 0u,
-                      se.x + tid + NT < se.y ? __ldg(sd.gen_pairs + se.x + tid + NT) : 0u);
+    const uint32_t* p = hp + (size_t)op * (2 * NT);
+    return make_uint2(__ldg(p), __ldg(p + NT));
   };
   auto step = [&](int op, uint2 ww) {
-    const uint2 se = gse[op];
-#if defined(FFQ_EXP_NOROT)  // timing experiment: barrier + parameters + word prefetch only
-    if (se.x + tid < se.y && ww.x == 0xFFFFFFFFu) amp[0] = cs[op].x + fz[op].x;
-    __syncthreads();
-    return;
-#endif
-    if (se.x + tid < se.y) {
+    if (ww.x != 0xFFFFFFFFu) {
       const double c = cs[op].x;
       const double2 sf = fz[op];
-      // one pair: sign bit 30 of the word flips sin F (an XOR on the high word)
+      // one pair (a negative sign is a swap of the members, done by the compiler)
       auto rot = [&](uint32_t w) {
-        const unsigned sg = ((w >> 30) & 1u) << 31;
-        const double gh = __hiloint2double((int)((unsigned)__double2hiint(sf.y) ^ sg), __double2loint(sf.y));
-        const double gl = __hiloint2double((int)((unsigned)__double2hiint(sf.x) ^ sg), __double2loint(sf.x));
         const uint32_t i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
         const double a = amp[i], b = amp[j];
-        amp[i] = fma(gh, b, c * a);
-        amp[j] = fma(gl, a, c * b);
+        amp[i] = fma(sf.y, b, c * a);
+        amp[j] = fma(sf.x, a, c * b);
       };
       rot(ww.x);
-      const uint32_t t1 = se.x + tid + NT;
-      if (t1 < se.y) {
+      if (ww.y != 0xFFFFFFFFu) {
         rot(ww.y);
-        // (the compiler unrolls this loop and issues its word loads together)
-        for (uint32_t t = t1 + NT; t < se.y; t += NT) rot(__ldg(sd.gen_pairs + t));
+        if (ww.y & (1u << 30)) {  // long steps (single excitations): the rest from gen_pairs
+          const uint2 se = gse[op];
+          // (the compiler unrolls this loop and issues its word loads together)
+          for (uint32_t t = se.x + tid + 2 * NT; t < se.y; t += NT) rot(__ldg(sd.gen_pairs + t));
+        }
       }
     }
     __syncthreads();
