@@ -564,7 +564,9 @@ const SectorDev* sector_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uin
     b->real = b->prog.ok && real_ok &&
               sector_real_smem_bytes(b->prog.n_slots, pl->cp.op_kind.size()) +
                       b->prog.ftab.size() * sizeof(double) <= ctx->smem_optin;
-    if (b->prog.ok && !b->real && sector_parts(ctx, b->prog.size) > 1)
+    // (a real-format compile that does not become the real program is redone: its
+    // generator words are in the real program's format)
+    if (b->prog.ok && !b->real && (real_ok || sector_parts(ctx, b->prog.size) > 1))
       b->prog = compile_sector(pl->cp, h->ch, hf, kSectorMaxSize, max_part, sector_parts(ctx, b->prog.size),
                                (uint32_t)((ctx->smem_optin - 16) / sizeof(double2)), 4);
     if (b->prog.ok) {
@@ -1530,14 +1532,14 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
       const int n_ops = (int)S.op_cross.size();
       for (int op = 0; op < n_ops; ++op)
         for (int64_t t = S.gen_off[op]; t < S.gen_off[op + 1]; ++t) {
-          const uint32_t w = S.gen_pairs[t], i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
-          if (i >= S.n_slots || j >= S.n_slots || i == j) { ++bad; continue; }
+          const uint32_t w = S.gen_pairs[t], i = w & 0x7FFFu, j = w >> 16;  // real program: i | j << 16
+          if (i >= S.n_slots || j >= S.n_slots || i == j || (w & 0x8000u)) { ++bad; continue; }
           for (uint32_t k : {i, j}) {
             if (seen[k] == op) ++bad;
             seen[k] = op;
           }
         }
-      // the head table repeats the first 2 head_threads words of every op (bit 30: more follow)
+      // the head table repeats the first 2 head_threads words of every op (bit 15: more follow)
       const int NT = S.head_threads;
       if (NT <= 0 || S.gen_head.size() != (size_t)(n_ops + kSectorHeadPad) * 2 * NT) ++bad;
       for (int op = 0; NT > 0 && op < n_ops + kSectorHeadPad; ++op)
@@ -1546,9 +1548,8 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
           const int64_t at = op < n_ops ? S.gen_off[op] + t : -1;
           const bool have = op < n_ops && at < S.gen_off[op + 1];
           const bool more = have && t >= NT && at + NT < S.gen_off[op + 1];
-          if (!have ? hw != 0xFFFFFFFFu : hw != (S.gen_pairs[at] | (more ? 1u << 30 : 0u))) ++bad;
+          if (!have ? hw != 0xFFFFFFFFu : hw != (S.gen_pairs[at] | (more ? 1u << 15 : 0u))) ++bad;
         }
-      for (uint32_t w : S.gen_pairs) bad += (w >> 30) != 0;  // signs are swaps in the real program
       for (uint32_t w : S.row_pairs)
         if ((w & 0x7FFFu) > S.n_slots || ((w >> 15) & 0x7FFFu) > S.n_slots) ++bad;
       for (size_t w = 0; w < S.blk_warp.size() / 4; ++w) {

@@ -660,9 +660,10 @@ struct SectorProgram {
   std::vector<uint8_t> gen_flags;   // bit 0: sgn(k & zout) < 0; bits 1..5: pattern pair index
   // Real one-CTA program (elem_bytes 8, one part): a negative sign swaps the
   // pair's members instead (F_hi = -F_lo: the 2x2 block is a rotation, so the
-  // swapped pair is the same arithmetic bit for bit) and bit 30 stays clear in
-  // gen_pairs. gen_head[(2 op + h) * head_threads + tid] is thread tid's h-th
-  // pair word of op (0xFFFFFFFF: none), bit 30 of the second word set when the
+  // swapped pair is the same arithmetic bit for bit) and a word is
+  // slot_i | slot_j << 16 (one mask and one shift to decode; bits 15, 31 clear).
+  // gen_head[(2 op + h) * head_threads + tid] is thread tid's h-th
+  // pair word of op (0xFFFFFFFF: none), bit 15 of the second word set when the
   // thread has further words in gen_pairs (ops with more than 2 head_threads
   // pairs); kSectorHeadPad all-empty ops follow (prefetch never leaves the table).
   std::vector<uint32_t> gen_head;
@@ -1543,7 +1544,8 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
         rj.push_back(bank_slot(pj.back()));
       }
       for (uint32_t t : bank_order(ri, rj, bank_group)) {  // thread tid takes pair off + tid
-        S.gen_pairs.push_back(slot(pi[t]) | (slot(pj[t]) << 15) | ((uint32_t)(fl[t] & 1u) << 30));
+        S.gen_pairs.push_back(real_prog ? slot(pi[t]) | (slot(pj[t]) << 16)
+                                        : slot(pi[t]) | (slot(pj[t]) << 15) | ((uint32_t)(fl[t] & 1u) << 30));
         S.gen_flags.push_back(fl[t]);
       }
       S.gen_off.push_back((int64_t)S.gen_pairs.size());
@@ -1558,7 +1560,7 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       for (int64_t t = b0; t < std::min<int64_t>(b1, b0 + 2 * NT); ++t)
         S.gen_head[((size_t)2 * op + (size_t)((t - b0) / NT)) * NT + (size_t)((t - b0) % NT)] = S.gen_pairs[t];
       for (int64_t t = b0 + 2 * NT; t < std::min<int64_t>(b1, b0 + 3 * NT); ++t)
-        S.gen_head[((size_t)2 * op + 1) * NT + (size_t)(t - b0 - 2 * NT)] |= 1u << 30;  // more words follow
+        S.gen_head[((size_t)2 * op + 1) * NT + (size_t)(t - b0 - 2 * NT)] |= 1u << 15;  // more words follow
     }
   }
   stage("generator pairs");

@@ -560,10 +560,15 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   if (row >= n_rows) return;
   const uint32_t na = sd.n_slots + 1;
   double* amp = reinterpret_cast<double*>(sm_raw);
-  double2* cs = reinterpret_cast<double2*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
-  double2* fz = cs + pl.n_ops;
-  uint2* gse = reinterpret_cast<uint2*>(fz + pl.n_ops);
-  double* sft = reinterpret_cast<double*>(gse + pl.n_ops);  // anchored blocks: shared-row f table
+  // per-op record (32 B): cos phi, sin phi F_lo, sin phi F_hi, pair range in gen_pairs
+  struct __align__(16) OpRec {
+    double c, gl, gh;
+    uint32_t s0, s1;
+  };
+  OpRec* opt = reinterpret_cast<OpRec*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
+  double2* cs = reinterpret_cast<double2*>(opt);  // the records' bytes, reused after the generator phase
+  double* sft = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(opt) +
+                                          (size_t)pl.n_ops * (2 * sizeof(double2) + sizeof(uint2)));  // shared-row f table
   for (uint32_t i = threadIdx.x; i < na; i += NT) amp[i] = 0.0;
   if (sd.blk_warp)
     for (int i = threadIdx.x; i < sd.n_ftab; i += NT) sft[i] = __ldg(sd.ftab + i);
@@ -573,9 +578,13 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     sincos(phi, &sv, &cv);
     const double sn = sv * pl.op_sscale[op];
     const FusedDesc& d = pl.fused[pl.op_idx[op]];
-    cs[op] = make_double2(cv, sn);
-    fz[op] = make_double2(sn * pl.pair_f[2 * d.pair_off].x, sn * pl.pair_f[2 * d.pair_off + 1].x);
-    gse[op] = make_uint2((uint32_t)sd.gen_off[op], (uint32_t)sd.gen_off[op + 1]);
+    OpRec r;
+    r.c = cv;
+    r.gl = sn * pl.pair_f[2 * d.pair_off].x;
+    r.gh = sn * pl.pair_f[2 * d.pair_off + 1].x;
+    r.s0 = (uint32_t)sd.gen_off[op];
+    r.s1 = (uint32_t)sd.gen_off[op + 1];
+    opt[op] = r;
   }
   __syncthreads();
   if (threadIdx.x == 0) amp[sd.hf_slot] = 1.0;
@@ -594,22 +603,21 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   };
   auto step = [&](int op, uint2 ww) {
     if (ww.x != 0xFFFFFFFFu) {
-      const double c = cs[op].x;
-      const double2 sf = fz[op];
-      // one pair (a negative sign is a swap of the members, done by the compiler)
+      const double c = opt[op].c, gl = opt[op].gl, gh = opt[op].gh;
+      // one pair, slot_i | slot_j << 16 (a negative sign is a swap of the members, done by the compiler)
       auto rot = [&](uint32_t w) {
-        const uint32_t i = w & 0x7FFFu, j = (w >> 15) & 0x7FFFu;
+        const uint32_t i = w & 0x7FFFu, j = w >> 16;
         const double a = amp[i], b = amp[j];
-        amp[i] = fma(sf.y, b, c * a);
-        amp[j] = fma(sf.x, a, c * b);
+        amp[i] = fma(gh, b, c * a);
+        amp[j] = fma(gl, a, c * b);
       };
       rot(ww.x);
       if (ww.y != 0xFFFFFFFFu) {
         rot(ww.y);
-        if (ww.y & (1u << 30)) {  // long steps (single excitations): the rest from gen_pairs
-          const uint2 se = gse[op];
+        if (ww.y & (1u << 15)) {  // long steps (single excitations): the rest from gen_pairs
+          const uint32_t s1 = opt[op].s1;
           // (the compiler unrolls this loop and issues its word loads together)
-          for (uint32_t t = se.x + tid + 2 * NT; t < se.y; t += NT) rot(__ldg(sd.gen_pairs + t));
+          for (uint32_t t = opt[op].s0 + tid + 2 * NT; t < s1; t += NT) rot(__ldg(sd.gen_pairs + t));
         }
       }
     }
