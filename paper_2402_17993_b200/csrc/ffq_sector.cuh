@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   double* amp = reinterpret_cast<double*>(sm_raw);
   // per-op record (32 B): cos phi, sin phi F_lo, sin phi F_hi, pair range in gen_pairs
   struct __align__(16) OpRec {
-    double c, gl, gh;
+    double c, gh, gl;
     uint32_t s0, s1;
   };
   OpRec* opt = reinterpret_cast<OpRec*>(sm_raw + ((na * sizeof(double) + 15) & ~(size_t)15));
@@ -603,7 +603,9 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
   };
   auto step = [&](int op, uint2 ww) {
     if (ww.x != 0xFFFFFFFFu) {
-      const double c = opt[op].c, gl = opt[op].gl, gh = opt[op].gh;
+      // (c, gh) in one 16-byte load; gl = -gh exactly (rotation block), a free operand negation
+      const double2 cg = *reinterpret_cast<const double2*>(&opt[op].c);
+      const double c = cg.x, gh = cg.y, gl = -cg.y;
       // one pair, slot_i | slot_j << 16 (a negative sign is a swap of the members, done by the compiler)
       auto rot = [&](uint32_t w) {
         const uint32_t i = w & 0x7FFFu, j = w >> 16;
