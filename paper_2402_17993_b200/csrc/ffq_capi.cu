@@ -710,13 +710,13 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   }
   // role warps (split evaluations of the 1024-thread program): each of the
   // 32 / split warp shares of a CTA gets `roles` warps (generic rows, block
-  // stream, clique tasks); needs >= 3 warps per share and the exchange buffer
+  // stream, clique tasks); needs >= 2 warps per share and the exchange buffer
   // ([share][1 + tasks][32] doubles) inside the per-op tables
   int roles = 0;
   if (split > 1 && ctx->sector_roles) {
     const int r = 32 / (32 / split);
-    const size_t need = (size_t)(32 / split) * (1 + sd.max_warp_tasks) * 32 * sizeof(double);
-    if (r >= 3 && need <= pl->cp.op_kind.size() * 2 * sizeof(double2)) roles = r;
+    const size_t need = (size_t)(32 / split) * ((r >= 3 ? 1 : 0) + sd.max_warp_tasks) * 32 * sizeof(double);
+    if (r >= 2 && need <= pl->cp.op_kind.size() * 2 * sizeof(double2)) roles = r;
   }
   k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
                                                                  clk, split, ctx->warp_sums.p, state_out, roles);

@@ -712,32 +712,39 @@ __global__ void __launch_bounds__(NT, 1) k_sector_eval_real(SectorDev sd, PlanDe
     return acc;
   };
   double acc = 0.0;
-  if (split > 1 && roles >= 3) {
+  if (split > 1 && roles >= 2) {
     // Split evaluation with role warps: this CTA serves the shares w = part + split * si;
-    // each share gets `roles` physical warps: 0 its generic rows, 1 its anchored
-    // block stream, 2.. its clique tasks (task k on role 2 + k % (roles - 2)). Every
-    // piece is the value the one-CTA kernel computes for it; role 0 adds them in the
-    // one-CTA kernel's order (generic + blocks, then the clique task totals in task
-    // order), so the energy bits are the same. The exchange buffer overlays the
-    // per-op tables (dead after the generator phase).
-    double* xch = reinterpret_cast<double*>(cs);  // [share][1 + max_warp_tasks][32]
+    // each share gets `roles` physical warps: role 0 its generic rows, role 1 its
+    // anchored block stream, roles 2.. its clique tasks (round robin); with two
+    // roles, role 0 takes the generic rows and the block stream, role 1 the clique
+    // tasks. Every piece is the value the one-CTA kernel computes for it; role 0
+    // adds them in the one-CTA kernel's order (generic + blocks, then the clique
+    // task totals in task order), so the energy bits are the same. The exchange
+    // buffer overlays the per-op records (dead after the generator phase).
+    double* xch = reinterpret_cast<double*>(cs);
     const int pw = threadIdx.x >> 5, si = pw / roles, role = pw % roles;
     const int w = part + split * si;
     const int2 wr = sd.cq_warp ? __ldg(sd.cq_warp + w) : make_int2(0, 0);
-    double* xs = xch + (size_t)si * (1 + sd.max_warp_tasks) * 32 + lane;
-    if (role == 0) {
-      acc = generic_rows(w);
-    } else if (role == 1) {
-      xs[0] = sd.blk_warp ? blk_stream(sd, w, lane, amp, sft) : 0.0;
-    } else {
-      for (int wt = wr.x + role - 2; wt < wr.y; wt += roles - 2) xs[(1 + wt - wr.x) * 32] = clique_task(sd, wt, lane, amp);
+    const int blk_role = roles >= 3 ? 1 : 0, cq0 = roles >= 3 ? 2 : 1, ncq = roles - cq0;
+    // per share: [block stream value (three or more roles)] [clique task totals]
+    double* xs = xch + (size_t)si * (blk_role + sd.max_warp_tasks) * 32 + lane;
+    double* xt = xs + blk_role * 32;
+    if (role == 0) acc = generic_rows(w);
+    if (role == blk_role) {
+      const double b = sd.blk_warp ? blk_stream(sd, w, lane, amp, sft) : 0.0;
+      if (role == 0)
+        acc += b;
+      else
+        xs[0] = b;
     }
+    if (role >= cq0)
+      for (int wt = wr.x + role - cq0; wt < wr.y; wt += ncq) xt[(wt - wr.x) * 32] = clique_task(sd, wt, lane, amp);
     __syncthreads();
     if (role != 0) return;
-    if (sd.blk_warp) acc += xs[0];
+    if (sd.blk_warp && blk_role != 0) acc += xs[0];
     if (sd.cq_warp) {
       double tot = 0.0;
-      for (int k = 0; k < wr.y - wr.x; ++k) tot += xs[(1 + k) * 32];
+      for (int k = 0; k < wr.y - wr.x; ++k) tot += xt[k * 32];
       acc += tot;
     }
 #pragma unroll
