@@ -1210,7 +1210,9 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
     DevBuf<double>& eo = ctx->io_e;
     th.alloc(std::max<size_t>(1, nth));
     eo.alloc(2 * (size_t)batch);
-    // first chunk one wave (its staging is the exposed part), then two waves
+    // first chunk one wave (its staging is the exposed part), then 2, 4, ... waves
+    // (a chunk boundary drains the SMs: few boundaries), a tail below one wave
+    // joining the last chunk
     const bool piped = nth * sizeof(double) >= (size_t)(1 << 20);
     const int wave = std::max(1, ctx->n_sm);
     if (piped) {
@@ -1220,7 +1222,8 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
       CK(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
     }
     for (int b0 = 0, k = 0; b0 < batch; ++k) {
-      const int nb = piped ? std::min((k == 0 ? 1 : 2) * wave, batch - b0) : batch;
+      int nb = piped ? std::min((1 << std::min(k, 20)) * wave, batch - b0) : batch;
+      if (piped && batch - b0 - nb < wave) nb = batch - b0;
       const size_t o = (size_t)b0 * ng, n = (size_t)nb * ng;
       if (n && piped) {
         // chunk k's copy runs on the copy stream while chunk k - 1 computes
