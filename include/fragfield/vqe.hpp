@@ -48,4 +48,18 @@ std::vector<double> exact_gradient_from_energies(const std::vector<double>& e, i
 OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x0,
                              const OptimizerOptions& opts = {});
 
+class Device;
+class DevicePlan;
+class DeviceHamiltonian;
+
+/// The VQE loop of SPEC.md:525-541 with the device objective built in: amplitudes
+/// in generator order, every energy through energy_batch on `dev` (no
+/// host-language callback inside the loop). vqe_bfgs runs bfgs_minimize with one
+/// batched 4P-row gradient call per iteration; vqe_device runs the serial
+/// Powell / Nelder-Mead optimizers on the B = 1 path.
+OptimizeResult vqe_bfgs(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
+                        std::vector<double> amps0, const OptimizerOptions& opts = {});
+OptimizeResult vqe_device(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
+                          std::vector<double> amps0, Optimizer method, const OptimizerOptions& opts = {});
+
 }  // namespace fragfield

@@ -75,6 +75,8 @@ from .lib._fragfield import (  # noqa: E402,F401
     shard_by_cost,
     synthetic_integrals,
     uniform_vector,
+    vqe_bfgs,
+    vqe_device,
 )
 
 

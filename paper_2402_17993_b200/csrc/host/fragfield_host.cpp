@@ -1104,6 +1104,35 @@ OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, con
   return R;
 }
 
+// ---- VQE loops on the device objective -------------------------------------------------
+namespace {
+// rows of amplitudes (generator order) -> energies, through the plan-order batch call
+BatchObjective device_objective(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf) {
+  return [&dev, &plan, &H, hf](const std::vector<double>& rows, int batch) {
+    const std::vector<int>& order = plan.plan().order;
+    const size_t P = order.size();
+    if (rows.size() != P * (size_t)batch) throw ContractViolation("vqe: rows must be [batch][n_generators]");
+    std::vector<double> th(rows.size());
+    for (int b = 0; b < batch; ++b)
+      for (size_t s = 0; s < P; ++s) th[(size_t)b * P + s] = rows[(size_t)b * P + (size_t)order[s]];
+    return energy_batch(dev, plan, H, hf, th, batch);
+  };
+}
+}  // namespace
+
+OptimizeResult vqe_bfgs(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
+                        std::vector<double> amps0, const OptimizerOptions& opts) {
+  if (amps0.size() != plan.plan().order.size()) throw ContractViolation("vqe_bfgs: amplitude count mismatch");
+  return bfgs_minimize(device_objective(dev, plan, H, hf), std::move(amps0), opts);
+}
+
+OptimizeResult vqe_device(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
+                          std::vector<double> amps0, Optimizer method, const OptimizerOptions& opts) {
+  if (amps0.size() != plan.plan().order.size()) throw ContractViolation("vqe_device: amplitude count mismatch");
+  const BatchObjective f = device_objective(dev, plan, H, hf);
+  return vqe_minimize([&f](const std::vector<double>& x) { return f(x, 1)[0]; }, std::move(amps0), method, opts);
+}
+
 // ---- FMO two-body assembly -----------------------------------------------------------
 double assemble_two_body(int n_fragments, const std::map<std::string, double>& monomers,
                          const std::map<std::string, double>& dimers) {

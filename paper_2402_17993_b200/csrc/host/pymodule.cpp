@@ -294,6 +294,19 @@ PYBIND11_MODULE(_fragfield, m) {
   m.def("neldermead_minimize", &neldermead_minimize, py::arg("f"), py::arg("x0"),
         py::arg("opts") = OptimizerOptions{});
   m.def("bfgs_minimize", &bfgs_minimize, py::arg("f"), py::arg("x0"), py::arg("opts") = OptimizerOptions{});
+  m.def("vqe_bfgs", &vqe_bfgs, py::arg("device"), py::arg("plan"), py::arg("hamiltonian"), py::arg("hf_bits"),
+        py::arg("amplitudes"), py::arg("opts") = OptimizerOptions{}, py::call_guard<py::gil_scoped_release>());
+  m.def(
+      "vqe_device",
+      [](Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf, std::vector<double> x0,
+         const std::string& method, const OptimizerOptions& opts) {
+        if (method != "powell" && method != "neldermead") throw ContractViolation("vqe_device: unknown optimizer");
+        py::gil_scoped_release nogil;
+        return vqe_device(dev, plan, H, hf, std::move(x0),
+                          method == "powell" ? Optimizer::powell : Optimizer::neldermead, opts);
+      },
+      py::arg("device"), py::arg("plan"), py::arg("hamiltonian"), py::arg("hf_bits"), py::arg("amplitudes"),
+      py::arg("method") = "powell", py::arg("opts") = OptimizerOptions{});
   m.def("parameter_shift_set", &parameter_shift_set);
   m.def("exact_gradient_set", &exact_gradient_set);
   m.def("exact_gradient_from_energies", &exact_gradient_from_energies);

@@ -128,3 +128,37 @@ def test_config2_vqe_converges_to_ftol_and_is_variational():
     e_cas = capi.lanczos_ground(ctx, ham, P.hf)[0]
     assert r.converged
     assert e_cas - 1e-10 <= r.energy < e_hf
+
+
+def test_native_vqe_drivers_equal_callback_loops():
+    """fragfield::vqe_bfgs / vqe_device build the device objective in C++ (no
+    host-language callback inside the loop): at config 2 they follow the
+    callback-driven optimizers step for step (same evaluations, same energy and
+    amplitudes bit for bit), converge to ftol 1e-8 and stay variational."""
+    import paper_2402_17993_b200 as ff
+
+    P = problems.config_problem(2)
+    dev = ff.Device(0)
+    H = ff.DeviceHamiltonian(dev, P.H)
+    plan = ff.DevicePlan(dev, P.plan)
+    x0 = list(P.thetas[0])
+
+    def fb(X, B):
+        X = np.asarray(X).reshape(B, P.n_gen)
+        th = np.ascontiguousarray(X[:, np.asarray(P.plan.order)])
+        return list(ff.energy_batch(dev, plan, H, P.hf, th))
+
+    opts = ff.OptimizerOptions()
+    opts.ftol = 1e-8
+    opts.max_evals = 5_000_000
+    a = ff.vqe_bfgs(dev, plan, H, P.hf, x0, opts)
+    b = ff.bfgs_minimize(fb, x0, opts)
+    assert a.converged and b.converged
+    assert (a.n_evals, a.n_iterations, a.energy) == (b.n_evals, b.n_iterations, b.energy)
+    assert np.array_equal(np.array(a.x), np.array(b.x))
+    e_cas = ff.lanczos_ground(dev, H, P.hf).energy
+    assert e_cas - 1e-10 <= a.energy < ff.energy_trotter(dev, [0.0] * P.n_gen, plan, H, P.hf)
+    opts.max_evals = 3000
+    c = ff.vqe_device(dev, plan, H, P.hf, x0, "powell", opts)
+    d = ff.vqe_minimize(lambda x: fb(x, 1)[0], x0, "powell", opts)
+    assert (c.n_evals, c.energy) == (d.n_evals, d.energy) and c.energy <= ff.energy_trotter(dev, x0, plan, H, P.hf)
