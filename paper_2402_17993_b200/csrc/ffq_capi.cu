@@ -196,8 +196,9 @@ struct ffq_ctx_s {
   int sector_roles = 1;                      // env FFQ_ROLES=0: split evaluations without role warps
   int sector_warm = 1;                       // env FFQ_WARM=0: no L2 warm-up pass before small sector batches
   int compact = 1;                           // env FFQ_COMPACT=0: no compact sector path
-  int compact_min_qubits = 27;               // env FFQ_COMPACT_MIN: smallest n it takes (the dense
-                                             // support path is faster below: grouped Hamiltonian)
+  int compact_min_qubits = 24;               // env FFQ_COMPACT_MIN: smallest n it takes at any batch
+                                             // (batches >= 8 from two qubits lower): measured
+                                             // crossover against the dense support path
   DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
   DevBuf<RotDesc> rot;       // ffq_state_apply_pauli_rotations: fused low-qubit runs
   DevBuf<RotGroup> rot_groups;
@@ -787,7 +788,7 @@ void energy_device(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, int
       return;
     }
   }
-  if (ctx->compact && n >= ctx->compact_min_qubits)
+  if (ctx->compact && (n >= ctx->compact_min_qubits || (n >= ctx->compact_min_qubits - 2 && batch >= 8)))
     if (CompactProg* cpg = compact_program(ctx, pl, h, hf)) {
       compact_energy(ctx, pl, *cpg, theta_dev, batch, e_dev, im_dev);
       return;
@@ -1122,7 +1123,7 @@ int ffq_energy_prepare(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t h
     if (n < 64 && (hf_bits >> n) != 0) throw BadInput("hf_bits exceeds n_qubits", FFQ_EINVAL);
     // the same order as energy_device: sector program first, then the compact layout
     if (ctx->sector && sector_program(ctx, plan, ham, hf_bits)) return FFQ_OK;
-    if (ctx->compact && n >= ctx->compact_min_qubits) compact_program(ctx, plan, ham, hf_bits);
+    if (ctx->compact && n >= ctx->compact_min_qubits - 2) compact_program(ctx, plan, ham, hf_bits);
     return FFQ_OK;
   });
 }
