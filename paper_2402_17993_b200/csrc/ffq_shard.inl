@@ -32,6 +32,16 @@ struct ffq_shard_s {
   uint64_t ham_key = 0;  // ffq_ham_s::uid of the cached physical Hamiltonian
   std::vector<int> ham_perm;
   std::unique_ptr<ffq_ham_s> hphys;
+  // one-term groups with |X| > 6 (random Pauli strings), batched per out-of-shard
+  // flip pattern (k_expect_shard_multi): terms, batches of <= 16, buckets
+  DevBuf<ShardTerm> mterms;
+  DevBuf<int2> mbatches;
+  struct MultiBucket {
+    uint32_t hG;
+    int batch0, n_batches;
+  };
+  std::vector<MultiBucket> mbuckets;
+  int64_t mchunk = 0, mchunks = 0;  // members per CTA, CTAs per batch
   ~ffq_shard_s() {
     if (comm) ncclCommDestroy(comm);
   }
@@ -218,11 +228,51 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     std::vector<double2> f(ch.cls_f.size() / 2);
     for (size_t i = 0; i < f.size(); ++i) f[i] = make_double2(ch.cls_f[2 * i], ch.cls_f[2 * i + 1]);
     hp->cls_f.upload(f, ctx->stream);
+    // one-term groups in generic mode (|X| > 6) leave the item list: they run
+    // batched per out-of-shard flip pattern, every local member enumerated
+    // (weight 1, full z: the folded pair-once weight 2 and the cleared pairing
+    // bit of the generic class are undone from the raw term)
+    std::map<uint64_t, std::map<uint64_t, double>> byx;
+    for (size_t t = 0; t < x.size(); ++t) byx[x[t]][z[t]] += h->raw_re[t];
+    std::map<uint32_t, std::vector<ShardTerm>> multi;  // hG -> terms, ascending X
+    std::set<uint64_t> multi_x;
+    for (const auto& gx : byx) {
+      if (__builtin_popcountll(gx.first) <= kMaxTableBits) continue;
+      int live = 0;
+      uint64_t zz = 0;
+      double cc = 0.0;
+      for (const auto& kv : gx.second)
+        if (kv.second != 0.0) { ++live; zz = kv.first; cc = kv.second; }
+      if (live != 1) continue;
+      const int ny = __builtin_popcountll(gx.first & zz) & 3;
+      const double2 f = make_double2(ny == 0 ? cc : ny == 2 ? -cc : 0.0, ny == 1 ? cc : ny == 3 ? -cc : 0.0);
+      multi[(uint32_t)(gx.first >> l)].push_back({gx.first & ((1ULL << l) - 1ULL), zz, f});
+      multi_x.insert(gx.first);
+    }
+    {
+      std::vector<ShardTerm> mt;
+      std::vector<int2> mb;
+      sh->mbuckets.clear();
+      for (const auto& kv : multi) {
+        ffq_shard_s::MultiBucket bk{kv.first, (int)mb.size(), 0};
+        for (size_t t0 = 0; t0 < kv.second.size(); t0 += 16) {
+          mb.push_back(make_int2((int)(mt.size() + t0), (int)std::min<size_t>(16, kv.second.size() - t0)));
+          ++bk.n_batches;
+        }
+        mt.insert(mt.end(), kv.second.begin(), kv.second.end());
+        sh->mbuckets.push_back(bk);
+      }
+      sh->mterms.upload(mt, ctx->stream);
+      sh->mbatches.upload(mb, ctx->stream);
+      sh->mchunk = std::max<int64_t>(4 * kItemChunk, (1LL << l) / 512);
+      sh->mchunks = ((1LL << l) + sh->mchunk - 1) / sh->mchunk;
+    }
     // items over the local index space (the global part of X picks the partner)
     std::vector<int32_t> ig, ip;
     std::vector<int64_t> iu;
     for (size_t gi = 0; gi < ch.groups.size(); ++gi) {
       const auto& d = ch.groups[gi];
+      if (multi_x.count(d.x)) continue;
       uint64_t Q = 0;  // inserted positions (see k_expect_shard)
       for (int i = 0; i < d.w; ++i) Q |= 1ULL << d.q[i];
       const int wl = __builtin_popcountll(Q & ((1ULL << l) - 1ULL));
@@ -245,16 +295,23 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     sh->ham_perm = S.final_perm;
   }
   const ffq_ham_s* hp = sh->hphys.get();
-  const int64_t items = (int64_t)hp->ch.item_g.size();
+  const int64_t items_old = (int64_t)hp->ch.item_g.size();
+  int64_t n_mbatches = 0;
+  for (const auto& bk : sh->mbuckets) n_mbatches += bk.n_batches;
+  const int64_t items = items_old + n_mbatches * sh->mchunks;  // partial slots per local shard
   sh->partial.alloc((size_t)std::max<int64_t>(1, items) * sh->n_local());
   sh->eloc.alloc(std::max<size_t>(2 * (size_t)sh->n_local(), (size_t)sh->R + 1));
   if (items > 0) CK(cudaMemsetAsync(sh->partial.p, 0, sizeof(double2) * items * sh->n_local(), ctx->stream));
-  // buckets of items sharing hG are contiguous (groups sorted by X)
+  // buckets of one out-of-shard flip pattern hG, ascending: the items sharing hG
+  // are contiguous (groups sorted by X), the batched one-term groups per bucket
   int64_t i0 = 0;
-  while (i0 < items) {
-    const uint32_t hG = (uint32_t)(hp->ch.groups[hp->ch.item_g[i0]].x >> l);
+  size_t mb = 0;
+  while (i0 < items_old || mb < sh->mbuckets.size()) {
+    const uint32_t h_old = i0 < items_old ? (uint32_t)(hp->ch.groups[hp->ch.item_g[i0]].x >> l) : 0xFFFFFFFFu;
+    const uint32_t h_multi = mb < sh->mbuckets.size() ? sh->mbuckets[mb].hG : 0xFFFFFFFFu;
+    const uint32_t hG = std::min(h_old, h_multi);
     int64_t i1 = i0;
-    while (i1 < items && (uint32_t)(hp->ch.groups[hp->ch.item_g[i1]].x >> l) == hG) ++i1;
+    while (i1 < items_old && (uint32_t)(hp->ch.groups[hp->ch.item_g[i1]].x >> l) == hG) ++i1;
     const double2* partner_nccl = nullptr;
     if (!sh->group() && hG != 0) {
       const int partner = sh->rank ^ (int)hG;
@@ -269,12 +326,24 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
       const double2* partner = hG == 0 ? sh->shards[i]->p
                                : sh->group() ? sh->shards[r ^ (int)hG]->p
                                              : partner_nccl;
-      k_expect_shard<kThreads><<<(unsigned)(i1 - i0), kThreads, 0, ctx->stream>>>(
-          sh->shards[i]->p, partner, l, (uint32_t)r, hp->dev(), i0, sh->partial.p + (size_t)i * items);
-      CK(cudaGetLastError());
-      ctx->launches++;
+      if (i1 > i0) {
+        k_expect_shard<kThreads><<<(unsigned)(i1 - i0), kThreads, 0, ctx->stream>>>(
+            sh->shards[i]->p, partner, l, (uint32_t)r, hp->dev(), i0, sh->partial.p + (size_t)i * items);
+        CK(cudaGetLastError());
+        ctx->launches++;
+      }
+      if (h_multi == hG) {
+        const auto& bk = sh->mbuckets[mb];
+        const int64_t slot0 = items_old + (int64_t)bk.batch0 * sh->mchunks;
+        k_expect_shard_multi<kThreads><<<dim3((unsigned)sh->mchunks, (unsigned)bk.n_batches), kThreads, 0, ctx->stream>>>(
+            sh->shards[i]->p, partner, l, (uint32_t)r, sh->mterms.p, sh->mbatches.p, bk.batch0, sh->mchunk, slot0,
+            sh->partial.p + (size_t)i * items);
+        CK(cudaGetLastError());
+        ctx->launches++;
+      }
     }
     i0 = i1;
+    if (h_multi == hG) ++mb;
   }
   for (int i = 0; i < sh->n_local(); ++i) {
     k_reduce_partials<kThreads><<<1, kThreads, 0, ctx->stream>>>(sh->partial.p + (size_t)i * std::max<int64_t>(1, items),
