@@ -462,11 +462,14 @@ inline ShardSchedule schedule_shards(const CompiledPlan& P, int g) {
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return uses[a] != uses[b] ? uses[a] < uses[b] : a > b;
   });
+  // local positions by ascending use: the least-flipped local qubits take the
+  // lowest positions, so a generator's flip mask sits high and its active
+  // patterns are long contiguous runs (a flip mask holding positions 0 and 1
+  // leaves one live amplitude per 64-byte DRAM atom: k_fused_gen at 26% of HBM
+  // against 88%)
   std::vector<int> perm(n, -1);
-  std::vector<bool> is_global(n, false);
-  for (int i = 0; i < g; ++i) is_global[order[i]] = true;
-  int nl = 0, ng = 0;
-  for (int q = 0; q < n; ++q) perm[q] = is_global[q] ? l + ng++ : nl++;
+  for (int i = 0; i < g; ++i) perm[order[i]] = l + i;
+  for (int i = g; i < n; ++i) perm[order[i]] = i - g;
   S.init_perm = perm;
   std::vector<int> inv(n);
   for (int q = 0; q < n; ++q) inv[perm[q]] = q;
