@@ -378,22 +378,26 @@ __global__ void __launch_bounds__(NT) k_expect_shard(const double2* __restrict__
 }
 
 // Several one-term x-groups of one out-of-shard flip pattern hG in one pass over
-// the shard: every local member m is enumerated (both orientations of a pair:
-// sum_m Re(conj(psi[m ^ X]) psi[m] c i^ny (-1)^popc(m & z)) equals the
-// pair-once sum with weight 2 for a Hermitian term), so all groups share the
-// m stream: own[m] is read once per batch and the partner gather happens only
-// where own[m] != 0 (a UCCSD state fills a few percent of the shard). CTA =
-// (chunk of m, batch); partial[item0 + batch * chunks + chunk].
+// the shard's support bitmap: every non-zero local member m is enumerated (both
+// orientations of a pair: sum_m Re(conj(psi[m ^ X]) psi[m] c i^ny (-1)^popc(m & z))
+// equals the pair-once sum with weight 2 for a Hermitian term), so all groups
+// share the m stream, and a partner amplitude is gathered only where the
+// partner's bitmap has its bit set (for a random X a few percent of the
+// partners of a UCCSD state are non-zero). Bitmaps: bit k % 32 of word k / 32,
+// conservative supersets are fine (a zero amplitude contributes zero). CTA =
+// (chunk of bitmap words, batch); partial[item0 + batch * chunks + chunk].
 struct ShardTerm {
   uint64_t xl, z;  // flip mask inside the shard; full z (physical positions, rank bits included)
   double2 f;       // c i^ny
 };
 template <int NT>
 __global__ void __launch_bounds__(NT) k_expect_shard_multi(const double2* __restrict__ own,
-                                                           const double2* __restrict__ partner, int l,
+                                                           const double2* __restrict__ partner,
+                                                           const uint32_t* __restrict__ own_sup,
+                                                           const uint32_t* __restrict__ partner_sup, int l,
                                                            uint32_t rank, const ShardTerm* __restrict__ terms,
                                                            const int2* __restrict__ batches, int batch0,
-                                                           int64_t chunk, int64_t item0,
+                                                           int64_t chunk_words, int64_t item0,
                                                            double2* __restrict__ partial) {
   __shared__ double2 red[NT / 32];
   __shared__ ShardTerm st[16];
@@ -401,18 +405,24 @@ __global__ void __launch_bounds__(NT) k_expect_shard_multi(const double2* __rest
   if (threadIdx.x < bt.y) st[threadIdx.x] = terms[bt.x + threadIdx.x];
   __syncthreads();
   const uint64_t base = (uint64_t)rank << l;
-  const int64_t m1 = min((int64_t)1 << l, ((int64_t)blockIdx.x + 1) * chunk);
+  const int64_t w1 = min((int64_t)1 << (l - 5), ((int64_t)blockIdx.x + 1) * chunk_words);
   double acc = 0.0;
-  for (int64_t m = (int64_t)blockIdx.x * chunk + threadIdx.x; m < m1; m += NT) {
-    const double2 a = own[m];
-    if (a.x == 0.0 && a.y == 0.0) continue;
-    const uint64_t M = base | (uint64_t)m;
-    for (int t = 0; t < bt.y; ++t) {
-      const double2 bb = partner[(uint64_t)m ^ st[t].xl];
-      const double sg = sgn_par(M & st[t].z);
-      const double prx = bb.x * a.x + bb.y * a.y, pry = bb.x * a.y - bb.y * a.x;
-      acc = fma(sg * prx, st[t].f.x, acc);
-      acc = fma(-sg * pry, st[t].f.y, acc);
+  for (int64_t w = (int64_t)blockIdx.x * chunk_words + threadIdx.x; w < w1; w += NT) {
+    uint32_t bits = own_sup[w];
+    while (bits) {
+      const uint64_t m = ((uint64_t)w << 5) | (uint32_t)(__ffs((int)bits) - 1);
+      bits &= bits - 1u;
+      const double2 a = own[m];
+      const uint64_t M = base | m;
+      for (int t = 0; t < bt.y; ++t) {
+        const uint64_t pm = m ^ st[t].xl;
+        if (!((__ldg(partner_sup + (pm >> 5)) >> (pm & 31u)) & 1u)) continue;
+        const double2 bb = partner[pm];
+        const double sg = sgn_par(M & st[t].z);
+        const double prx = bb.x * a.x + bb.y * a.y, pry = bb.x * a.y - bb.y * a.x;
+        acc = fma(sg * prx, st[t].f.x, acc);
+        acc = fma(-sg * pry, st[t].f.y, acc);
+      }
     }
   }
   const double2 tot = block_sum<NT>(make_double2(acc, 0.0), red);

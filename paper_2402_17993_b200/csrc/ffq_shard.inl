@@ -36,12 +36,13 @@ struct ffq_shard_s {
   // flip pattern (k_expect_shard_multi): terms, batches of <= 16, buckets
   DevBuf<ShardTerm> mterms;
   DevBuf<int2> mbatches;
+  DevBuf<uint32_t> sup_own, sup_partner;  // support bitmaps of the local shards / of a received partner shard
   struct MultiBucket {
     uint32_t hG;
     int batch0, n_batches;
   };
   std::vector<MultiBucket> mbuckets;
-  int64_t mchunk = 0, mchunks = 0;  // members per CTA, CTAs per batch
+  int64_t mchunk = 0, mchunks = 0;  // bitmap words per CTA, CTAs per batch
   ~ffq_shard_s() {
     if (comm) ncclCommDestroy(comm);
   }
@@ -237,7 +238,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
     std::map<uint32_t, std::vector<ShardTerm>> multi;  // hG -> terms, ascending X
     std::set<uint64_t> multi_x;
     for (const auto& gx : byx) {
-      if (__builtin_popcountll(gx.first) <= kMaxTableBits) continue;
+      if (l < 5 || __builtin_popcountll(gx.first) <= kMaxTableBits) continue;  // (bitmap words need 32 amplitudes)
       int live = 0;
       uint64_t zz = 0;
       double cc = 0.0;
@@ -264,8 +265,9 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
       }
       sh->mterms.upload(mt, ctx->stream);
       sh->mbatches.upload(mb, ctx->stream);
-      sh->mchunk = std::max<int64_t>(4 * kItemChunk, (1LL << l) / 512);
-      sh->mchunks = ((1LL << l) + sh->mchunk - 1) / sh->mchunk;
+      const int64_t words = l >= 5 ? 1LL << (l - 5) : 1;
+      sh->mchunk = std::max<int64_t>(kItemChunk, words / 512);
+      sh->mchunks = (words + sh->mchunk - 1) / sh->mchunk;
     }
     // items over the local index space (the global part of X picks the partner)
     std::vector<int32_t> ig, ip;
@@ -302,6 +304,14 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   sh->partial.alloc((size_t)std::max<int64_t>(1, items) * sh->n_local());
   sh->eloc.alloc(std::max<size_t>(2 * (size_t)sh->n_local(), (size_t)sh->R + 1));
   if (items > 0) CK(cudaMemsetAsync(sh->partial.p, 0, sizeof(double2) * items * sh->n_local(), ctx->stream));
+  // support bitmaps of the local shards for the batched one-term groups
+  const int64_t sup_words = l >= 5 ? 1LL << (l - 5) : 0;
+  if (!sh->mbuckets.empty()) {
+    sh->sup_own.alloc((size_t)sup_words * sh->n_local());
+    if (!sh->group()) sh->sup_partner.alloc((size_t)sup_words);
+    for (int i = 0; i < sh->n_local(); ++i)
+      launch_support_from_state(ctx, sh->shards[i]->p, sh->sup_own.p + (size_t)i * sup_words, l, 1);
+  }
   // buckets of one out-of-shard flip pattern hG, ascending: the items sharing hG
   // are contiguous (groups sorted by X), the batched one-term groups per bucket
   int64_t i0 = 0;
@@ -320,12 +330,16 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
       NCK(ncclRecv(sh->recvbuf.p, (size_t)2 << l, ncclDouble, partner, sh->comm, ctx->stream));
       NCK(ncclGroupEnd());
       partner_nccl = sh->recvbuf.p;
+      if (h_multi == hG) launch_support_from_state(ctx, sh->recvbuf.p, sh->sup_partner.p, l, 1);
     }
     for (int i = 0; i < sh->n_local(); ++i) {
       const int r = sh->rank_of(i);
       const double2* partner = hG == 0 ? sh->shards[i]->p
                                : sh->group() ? sh->shards[r ^ (int)hG]->p
                                              : partner_nccl;
+      const uint32_t* partner_sup = hG == 0 ? sh->sup_own.p + (size_t)i * sup_words
+                                    : sh->group() ? sh->sup_own.p + (size_t)(r ^ (int)hG) * sup_words
+                                                  : sh->sup_partner.p;
       if (i1 > i0) {
         k_expect_shard<kThreads><<<(unsigned)(i1 - i0), kThreads, 0, ctx->stream>>>(
             sh->shards[i]->p, partner, l, (uint32_t)r, hp->dev(), i0, sh->partial.p + (size_t)i * items);
@@ -336,7 +350,8 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
         const auto& bk = sh->mbuckets[mb];
         const int64_t slot0 = items_old + (int64_t)bk.batch0 * sh->mchunks;
         k_expect_shard_multi<kThreads><<<dim3((unsigned)sh->mchunks, (unsigned)bk.n_batches), kThreads, 0, ctx->stream>>>(
-            sh->shards[i]->p, partner, l, (uint32_t)r, sh->mterms.p, sh->mbatches.p, bk.batch0, sh->mchunk, slot0,
+            sh->shards[i]->p, partner, sh->sup_own.p + (size_t)i * sup_words, partner_sup, l, (uint32_t)r,
+            sh->mterms.p, sh->mbatches.p, bk.batch0, sh->mchunk, slot0,
             sh->partial.p + (size_t)i * items);
         CK(cudaGetLastError());
         ctx->launches++;
