@@ -6,7 +6,8 @@
 // index is (r << l) | k. Plan ops whose flip mask reaches a global position
 // are preceded by a qubit swap with a free local position (schedule_shards):
 // ranks r and r ^ (1 << j) exchange the half shard whose local bit differs
-// from their rank bit. Z on global qubits is a per-rank sign (sign_base).
+// from their rank bit. Z on global qubits is a per-rank sign folded into sin.
+// Generator passes are support-tracked per shard (bitmaps rebuilt after a swap).
 // The expectation exchanges whole shards once per distinct out-of-shard flip
 // pattern hG and evaluates that bucket of x-groups locally.
 //
@@ -25,6 +26,7 @@ struct ffq_shard_s {
   DevBuf<double2> cs, partial;
   DevBuf<double> eloc;
   DevBuf<uint64_t> pbits;
+  DevBuf<uint32_t> plow;  // low_pattern_mask of every pattern pair at its op's physical positions
   ncclComm_t comm = nullptr;
   std::vector<int> perm;
   int last_swaps = 0;
@@ -134,6 +136,7 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   // per-rank rotation coefficients; string ops fold the global Z sign into sin
   std::vector<double2> cs((size_t)sh->n_local() * std::max(1, n_ops));
   std::vector<uint64_t> pbits(cp.pair_bits.size());
+  std::vector<uint32_t> plow(cp.pair_bits.size(), 0u);
   std::vector<FusedDesc> phys(cp.fused.size());
   std::vector<int> perm = S.init_perm;
   std::vector<std::vector<int>> op_perm(n_ops);
@@ -151,23 +154,26 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   }
   for (int op = 0; op < n_ops; ++op) {
     const double phi = theta[cp.op_gen[op]] * cp.op_cfac[op];
-    for (int i = 0; i < sh->n_local(); ++i) {
-      double sg = 1.0;
-      if (cp.op_kind[op] == 1) {
-        const uint64_t zp = permute_mask(cp.str_z[cp.op_idx[op]], op_perm[op]);
-        sg = (__builtin_popcountll(((uint64_t)sh->rank_of(i) << l) & zp) & 1) ? -1.0 : 1.0;
-      }
-      cs[(size_t)i * n_ops + op] = make_double2(std::cos(phi), std::sin(phi) * cp.op_sscale[op] * sg);
-    }
     if (cp.op_kind[op] == 0) {
       const FusedDesc& d = cp.fused[cp.op_idx[op]];
       phys[cp.op_idx[op]] = physical_fused(d, op_perm[op]);
-      for (int p = 0; p < d.npair; ++p)
+      for (int p = 0; p < d.npair; ++p) {
         pbits[d.pair_off + p] = permute_mask(cp.pair_bits[d.pair_off + p], op_perm[op]);
+        plow[d.pair_off + p] = low_pattern_mask(phys[cp.op_idx[op]].x, pbits[d.pair_off + p]);
+      }
+    }
+    for (int i = 0; i < sh->n_local(); ++i) {
+      // Z on global qubits is a per-rank sign, folded into sin (string ops: the
+      // string's z; fused ops: the outside-Z mask of the generator)
+      const uint64_t zp = cp.op_kind[op] == 1 ? permute_mask(cp.str_z[cp.op_idx[op]], op_perm[op])
+                                              : phys[cp.op_idx[op]].zout;
+      const double sg = (__builtin_popcountll(((uint64_t)sh->rank_of(i) << l) & zp) & 1) ? -1.0 : 1.0;
+      cs[(size_t)i * n_ops + op] = make_double2(std::cos(phi), std::sin(phi) * cp.op_sscale[op] * sg);
     }
   }
   sh->cs.upload(cs, ctx->stream);
   sh->pbits.upload(pbits, ctx->stream);
+  sh->plow.upload(plow, ctx->stream);
   // |HF> on its owner rank
   const uint64_t hf_phys = permute_mask(hf, S.init_perm);
   for (int i = 0; i < sh->n_local(); ++i) {
@@ -178,11 +184,27 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
                          cudaMemcpyHostToDevice, ctx->stream));
     }
   }
+  // support bitmaps of the local shards (bit k % 32 of word k / 32: amplitude k may be
+  // non-zero), kept by the support-tracked generator passes and rebuilt from the
+  // data after a swap or a dense string pass
+  const bool track = use_support(ctx, l);
+  const int64_t sup_words = l >= 5 ? 1LL << (l - 5) : 0;
+  bool stale = false;
+  auto rebuild = [&] {
+    for (int i = 0; i < sh->n_local(); ++i)
+      launch_support_from_state(ctx, sh->shards[i]->p, sh->sup_own.p + (size_t)i * sup_words, l, 1);
+    stale = false;
+  };
+  if (track) {
+    sh->sup_own.alloc((size_t)sup_words * sh->n_local());
+    rebuild();  // |HF> only
+  }
   sh->last_swaps = 0;
   for (const auto& st : S.steps) {
     if (st.kind == 0) {
       shard_swap(sh, st.gpos, st.lpos);
       ++sh->last_swaps;
+      stale = true;
       continue;
     }
     const int op = st.op;
@@ -190,18 +212,28 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
       const double2* csr = sh->cs.p + (size_t)i * n_ops;
       if (cp.op_kind[op] == 0) {
         const FusedDesc& d = phys[cp.op_idx[op]];
+        if (track) {  // support-tracked pass (the global Z sign is in csr)
+          if (stale && i == 0) rebuild();
+          const int64_t work = (int64_t)d.npair << (l - 5 - d.whi);
+          k_fused_gen_support<<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
+              sh->shards[i]->p, sh->sup_own.p + (size_t)i * sup_words, l, d, sh->pbits.p, sh->plow.p, pl->pair_f.p,
+              csr, n_ops, op, 1LL << l);
+          CK(cudaGetLastError());
+          ctx->launches++;
+          continue;
+        }
         const bool vec = !(d.x & 1ULL) && (l - d.w) >= 1;
         const int64_t work = ((int64_t)d.npair << (l - d.w)) >> (vec ? 1 : 0);
-        const uint64_t base = (uint64_t)sh->rank_of(i) << l;
         if (vec)
           k_fused_gen<true><<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
-              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, base);
+              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, 0);
         else
           k_fused_gen<false><<<grid_for(work, ctx->n_sm), kThreads, 0, ctx->stream>>>(
-              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, base);
+              sh->shards[i]->p, l, d, sh->pbits.p, pl->pair_f.p, csr, n_ops, op, 0);
         CK(cudaGetLastError());
         ctx->launches++;
       } else {
+        stale = true;
         const int si = cp.op_idx[op];
         const uint64_t lm = (1ULL << l) - 1ULL;
         const uint64_t xp = permute_mask(cp.str_x[si], op_perm[op]);
@@ -305,12 +337,10 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   sh->eloc.alloc(std::max<size_t>(2 * (size_t)sh->n_local(), (size_t)sh->R + 1));
   if (items > 0) CK(cudaMemsetAsync(sh->partial.p, 0, sizeof(double2) * items * sh->n_local(), ctx->stream));
   // support bitmaps of the local shards for the batched one-term groups
-  const int64_t sup_words = l >= 5 ? 1LL << (l - 5) : 0;
   if (!sh->mbuckets.empty()) {
     sh->sup_own.alloc((size_t)sup_words * sh->n_local());
     if (!sh->group()) sh->sup_partner.alloc((size_t)sup_words);
-    for (int i = 0; i < sh->n_local(); ++i)
-      launch_support_from_state(ctx, sh->shards[i]->p, sh->sup_own.p + (size_t)i * sup_words, l, 1);
+    if (!track || stale) rebuild();  // (tracked bitmaps are conservative supersets: fine)
   }
   // buckets of one out-of-shard flip pattern hG, ascending: the items sharing hG
   // are contiguous (groups sorted by X), the batched one-term groups per bucket
