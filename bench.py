@@ -585,7 +585,8 @@ def main():
                            "ms_per_eval": max(x["ms_per_eval"] for x in legs), "energy": legs[0]["energy"],
                            "ranks_agree": all(x["energy"] == legs[0]["energy"] for x in legs),
                            "repeatable": all(x["repeatable"] for x in legs),
-                           "note": "dense sharded path (k_fused_gen / k_expect_shard per shard); scaling strong: "
+                           "note": "sharded path: support-tracked generator passes per shard, expectation batched over "
+                                   "support bitmaps, half-shard swaps by ncclSend/ncclRecv; scaling strong: "
                                    "compare ms_per_eval across --gpus N"}
 
     cpu = None
