@@ -446,6 +446,74 @@ __global__ void k_swap_unpack(double2* __restrict__ s, const double2* __restrict
        u += (int64_t)gridDim.x * blockDim.x)
     s[insert_zero<uint64_t>((uint64_t)u, lpos) | ((uint64_t)val << lpos)] = buf[u];
 }
+// Support-compacted swap: only the amplitudes whose support bit is set move.
+// bits of word w that belong to the half with local bit lpos == val
+__device__ __forceinline__ uint32_t swap_half_bits(uint32_t word, int64_t w, int lpos, int val) {
+  if (lpos >= 5) return (((uint64_t)w >> (lpos - 5)) & 1ULL) == (uint64_t)val ? word : 0u;
+  uint32_t m = 0;  // offsets o in the word with bit lpos of o equal to val
+#pragma unroll
+  for (uint32_t o = 0; o < 32; ++o) m |= (((o >> lpos) & 1u) == (uint32_t)val ? 1u : 0u) << o;
+  return word & m;
+}
+__global__ void k_swap_count(const uint32_t* __restrict__ sup, int l, int lpos, int val,
+                             unsigned long long* __restrict__ count) {
+  const int64_t words = 1LL << (l - 5);
+  unsigned long long n = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+    n += (unsigned)__popc(swap_half_bits(sup[w], w, lpos, val));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(count, n);
+}
+// move the supported amplitudes of the half out: (index within the half, value)
+// pairs in any order (the unpack scatters by index), slots and bits cleared
+__global__ void k_swap_pack_sparse(double2* __restrict__ s, uint32_t* __restrict__ sup, int l, int lpos, int val,
+                                   double2* __restrict__ vals, uint32_t* __restrict__ idx,
+                                   unsigned long long* __restrict__ cursor) {
+  const int64_t words = 1LL << (l - 5);
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate together (words is a multiple of 32 for l >= 10; the
+  // guard keeps short shards correct): one cursor atomic per warp
+  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; w0 < words;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = w0 + lane;
+    const uint32_t word = w < words ? sup[w] : 0u;
+    uint32_t bits = w < words ? swap_half_bits(word, w, lpos, val) : 0u;
+    const uint32_t n = (uint32_t)__popc(bits);
+    uint32_t incl = n;  // inclusive scan of the lane counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) continue;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(cursor, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (!bits) continue;
+    unsigned long long at = base + (incl - n);
+    sup[w] = word & ~bits;
+    while (bits) {
+      const uint64_t k = ((uint64_t)w << 5) | (uint32_t)(__ffs((int)bits) - 1);
+      bits &= bits - 1u;
+      vals[at] = s[k];
+      s[k] = make_double2(0.0, 0.0);
+      idx[at] = (uint32_t)(((k >> (lpos + 1)) << lpos) | (k & ((1ULL << lpos) - 1ULL)));  // bit lpos removed
+      ++at;
+    }
+  }
+}
+__global__ void k_swap_unpack_sparse(double2* __restrict__ s, uint32_t* __restrict__ sup, int lpos, int val,
+                                     const double2* __restrict__ vals, const uint32_t* __restrict__ idx,
+                                     unsigned long long count) {
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < count;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t k = insert_zero<uint64_t>((uint64_t)idx[t], lpos) | ((uint64_t)val << lpos);
+    s[k] = vals[t];
+    atomicOr(&sup[k >> 5], 1u << (k & 31u));
+  }
+}
 // both ranks of a pair on one device: exchange in place
 __global__ void k_swap_pair(double2* __restrict__ s0, double2* __restrict__ s1, int l, int lpos) {
   const int64_t half = 1LL << (l - 1);

@@ -39,6 +39,9 @@ struct ffq_shard_s {
   DevBuf<ShardTerm> mterms;
   DevBuf<int2> mbatches;
   DevBuf<uint32_t> sup_own, sup_partner;  // support bitmaps of the local shards / of a received partner shard
+  DevBuf<uint32_t> sendidx, recvidx;      // support-compacted swaps: indices within the half
+  DevBuf<unsigned long long> counters;    // [4]: counts and cursors of a swap
+  int64_t sparse_swaps = 0, dense_swaps = 0;
   struct MultiBucket {
     uint32_t hG;
     int batch0, n_batches;
@@ -87,12 +90,127 @@ void shard_alloc(ffq_shard_s* sh) {
   }
 }
 
-// swap physical global position gpos with local lpos on every rank pair
-void shard_swap(ffq_shard_s* sh, int gpos, int lpos) {
+// Support-compacted swap of one rank pair: with valid support bitmaps only the
+// supported amplitudes of the two half shards move, as (index, value) lists
+// (a UCCSD state fills a few percent of a shard). Returns false when a list
+// would exceed a quarter of the shard (dense swap instead). sup0/sup1: the
+// pair's bitmaps; s1 == nullptr: NCCL mode (this rank is s0, the partner is
+// remote), else both shards are on this device and device copies are the wire.
+bool shard_swap_sparse(ffq_shard_s* sh, double2* s0, uint32_t* sup0, int val0, double2* s1, uint32_t* sup1,
+                       int val1, int lpos, int partner) {
+  ffq_ctx_t ctx = sh->ctx;
+  const int l = sh->l;
+  const int64_t half = 1LL << (l - 1), cap = half / 2;
+  const int64_t words = 1LL << (l - 5);
+  const int grid = grid_for(words, ctx->n_sm);
+  sh->counters.alloc(4);
+  unsigned long long* c = sh->counters.p;
+  CK(cudaMemsetAsync(c, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  k_swap_count<<<grid, kThreads, 0, ctx->stream>>>(sup0, l, lpos, val0, c);
+  unsigned long long n[2] = {0, 0};
+  if (s1) {
+    k_swap_count<<<grid, kThreads, 0, ctx->stream>>>(sup1, l, lpos, val1, c + 1);
+  } else {
+    NCK(ncclGroupStart());
+    NCK(ncclSend(c, 1, ncclUint64, partner, sh->comm, ctx->stream));
+    NCK(ncclRecv(c + 1, 1, ncclUint64, partner, sh->comm, ctx->stream));
+    NCK(ncclGroupEnd());
+  }
+  CK(cudaMemcpyAsync(n, c, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->launches += s1 ? 2 : 1;
+  if ((int64_t)n[0] > cap || (int64_t)n[1] > cap) return false;  // both ranks see both counts: same decision
+  // values: sendbuf / recvbuf hold 2 * half double2 (two lists of <= cap entries each fit)
+  sh->sendidx.alloc((size_t)2 * cap);
+  sh->recvidx.alloc((size_t)2 * cap);
+  sh->sendbuf.alloc((size_t)2 * cap);
+  sh->recvbuf.alloc((size_t)2 * cap);
+  double2 *v0 = sh->sendbuf.p, *v1 = sh->sendbuf.p + cap;
+  uint32_t *i0 = sh->sendidx.p, *i1 = sh->sendidx.p + cap;
+  k_swap_pack_sparse<<<grid, kThreads, 0, ctx->stream>>>(s0, sup0, l, lpos, val0, v0, i0, c + 2);
+  if (s1) {
+    k_swap_pack_sparse<<<grid, kThreads, 0, ctx->stream>>>(s1, sup1, l, lpos, val1, v1, i1, c + 3);
+    // the wire: device copies into the receive buffers
+    double2 *r0 = sh->recvbuf.p, *r1 = sh->recvbuf.p + cap;
+    uint32_t *j0 = sh->recvidx.p, *j1 = sh->recvidx.p + cap;
+    if (n[1]) {
+      CK(cudaMemcpyAsync(r0, v1, n[1] * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(j0, i1, n[1] * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      k_swap_unpack_sparse<<<grid_for((int64_t)n[1], ctx->n_sm), kThreads, 0, ctx->stream>>>(s0, sup0, lpos, val0, r0, j0,
+                                                                                          n[1]);
+    }
+    if (n[0]) {
+      CK(cudaMemcpyAsync(r1, v0, n[0] * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(j1, i0, n[0] * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      k_swap_unpack_sparse<<<grid_for((int64_t)n[0], ctx->n_sm), kThreads, 0, ctx->stream>>>(s1, sup1, lpos, val1, r1, j1,
+                                                                                          n[0]);
+    }
+    ctx->launches += 4;
+  } else {
+    NCK(ncclGroupStart());
+    if (n[0]) {
+      NCK(ncclSend(v0, (size_t)n[0] * 2, ncclDouble, partner, sh->comm, ctx->stream));
+      NCK(ncclSend(i0, (size_t)n[0], ncclUint32, partner, sh->comm, ctx->stream));
+    }
+    if (n[1]) {
+      NCK(ncclRecv(sh->recvbuf.p, (size_t)n[1] * 2, ncclDouble, partner, sh->comm, ctx->stream));
+      NCK(ncclRecv(sh->recvidx.p, (size_t)n[1], ncclUint32, partner, sh->comm, ctx->stream));
+    }
+    NCK(ncclGroupEnd());
+    if (n[1])
+      k_swap_unpack_sparse<<<grid_for((int64_t)n[1], ctx->n_sm), kThreads, 0, ctx->stream>>>(
+          s0, sup0, lpos, val0, sh->recvbuf.p, sh->recvidx.p, n[1]);
+    ctx->launches += 2;
+  }
+  CK(cudaGetLastError());
+  return true;
+}
+
+// swap physical global position gpos with local lpos on every rank pair;
+// sup != nullptr: valid support bitmaps of the local shards ([n_local][2^(l-5)]),
+// kept valid by the sparse path; returns false when a dense swap left them stale
+bool shard_swap(ffq_shard_s* sh, int gpos, int lpos, uint32_t* sup) {
   ffq_ctx_t ctx = sh->ctx;
   const int j = gpos - sh->l;
   const int64_t half = 1LL << (sh->l - 1);
   const int grid = grid_for(half, ctx->n_sm);
+  const int64_t sup_words = sh->l >= 5 ? 1LL << (sh->l - 5) : 0;
+  if (sup && sh->group()) {
+    bool all = true;
+    for (int r = 0; r < sh->R; ++r) {
+      if ((r >> j) & 1) continue;
+      const int r1 = r ^ (1 << j);
+      if (shard_swap_sparse(sh, sh->shards[r]->p, sup + (size_t)r * sup_words, 1, sh->shards[r1]->p,
+                            sup + (size_t)r1 * sup_words, 0, lpos, -1)) {
+        ++sh->sparse_swaps;
+        continue;
+      }
+      // dense swap of this pair (same kernels as the NCCL transport, a device copy as the wire)
+      all = false;
+      ++sh->dense_swaps;
+      sh->sendbuf.alloc((size_t)2 * half);
+      sh->recvbuf.alloc((size_t)2 * half);
+      k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r]->p, sh->sendbuf.p, sh->l, lpos, 1);
+      k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r1]->p, sh->sendbuf.p + half, sh->l, lpos, 0);
+      CK(cudaMemcpyAsync(sh->recvbuf.p, sh->sendbuf.p + half, sizeof(double2) * half, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      CK(cudaMemcpyAsync(sh->recvbuf.p + half, sh->sendbuf.p, sizeof(double2) * half, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r]->p, sh->recvbuf.p, sh->l, lpos, 1);
+      k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[r1]->p, sh->recvbuf.p + half, sh->l, lpos, 0);
+      CK(cudaGetLastError());
+      ctx->launches += 4;
+    }
+    return all;
+  }
+  if (sup && !sh->group()) {
+    const int bit = (sh->rank >> j) & 1, partner = sh->rank ^ (1 << j);
+    if (shard_swap_sparse(sh, sh->shards[0]->p, sup, 1 - bit, nullptr, nullptr, 0, lpos, partner)) {
+      ++sh->sparse_swaps;
+      return true;
+    }
+    ++sh->dense_swaps;
+  }
   if (sh->group()) {
     // same pack/unpack kernels as the NCCL transport, with a device copy as the wire
     sh->sendbuf.alloc((size_t)2 * half);
@@ -112,7 +230,7 @@ void shard_swap(ffq_shard_s* sh, int gpos, int lpos) {
       CK(cudaGetLastError());
       ctx->launches += 4;
     }
-    return;
+    return false;
   }
   const int bit = (sh->rank >> j) & 1, partner = sh->rank ^ (1 << j);
   k_swap_pack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[0]->p, sh->sendbuf.p, sh->l, lpos, 1 - bit);
@@ -124,6 +242,7 @@ void shard_swap(ffq_shard_s* sh, int gpos, int lpos) {
   k_swap_unpack<<<grid, kThreads, 0, ctx->stream>>>(sh->shards[0]->p, sh->recvbuf.p, sh->l, lpos, 1 - bit);
   CK(cudaGetLastError());
   ctx->launches += 2;
+  return false;
 }
 
 double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, const double* theta) {
@@ -202,9 +321,10 @@ double shard_energy(ffq_shard_s* sh, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf, 
   sh->last_swaps = 0;
   for (const auto& st : S.steps) {
     if (st.kind == 0) {
-      shard_swap(sh, st.gpos, st.lpos);
+      // (the sparse swap needs valid bitmaps and keeps them valid)
+      if (track && stale) rebuild();
+      if (!shard_swap(sh, st.gpos, st.lpos, track ? sh->sup_own.p : nullptr)) stale = true;
       ++sh->last_swaps;
-      stale = true;
       continue;
     }
     const int op = st.op;
