@@ -77,3 +77,33 @@ def test_config5_structure_small_vs_oracle(ctx, oracle):
             psi = oracle.apply_pauli_rotation(16, psi, int(xx), int(zz), P.thetas[0][gid] * cc.imag)
     ref = oracle.expectation(16, psi, oracle.PauliSum.from_terms(16, x, z, c)).real
     assert abs(e - ref) <= 1e-10 and abs(e_sh - ref) <= 1e-10
+
+
+def test_dense_and_support_tracked_shard_paths_agree(monkeypatch):
+    """The sharded path keeps a support bitmap per shard (support-tracked
+    generator passes, expectation batched over the bitmaps, swaps that move
+    (index, value) lists); FFQ_SUPPORT=0 selects the dense passes and dense
+    half-shard swaps. Both run the config-5 recipe at 16 qubits on 3 global
+    qubits and must agree in energy and amplitudes; the tracked path repeats
+    bit for bit (its swap lists are filled in arbitrary order)."""
+    P = problems.config5_problem(n_doubles=150, n_terms=400, n_qubits=16, n_elec=8)
+    th = P.plan_thetas()[0]
+    out = {}
+    for mode, env in (("tracked", {}), ("dense", {"FFQ_SUPPORT": "0"})):
+        monkeypatch.delenv("FFQ_SUPPORT", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = capi.Context(0)
+        plan = capi.Plan(c, 16, *P.plan_arrays())
+        ham = capi.Hamiltonian(c, 16, *P.ham_arrays())
+        sh = capi.ShardedState(c, 16, 3)
+        e1 = sh.energy(plan, ham, P.hf, th)
+        psi = sh.download().copy()
+        e2 = sh.energy(plan, ham, P.hf, th)
+        assert e1 == e2 and np.array_equal(psi, sh.download())
+        out[mode] = (e1, psi, sh.info()[0])
+        del sh, plan, ham, c
+    monkeypatch.delenv("FFQ_SUPPORT", raising=False)
+    assert abs(out["tracked"][0] - out["dense"][0]) <= 1e-12
+    assert np.abs(out["tracked"][1] - out["dense"][1]).max() <= 1e-12
+    assert out["tracked"][2] == out["dense"][2] > 0  # same swap schedule
