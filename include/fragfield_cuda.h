@@ -124,7 +124,7 @@ int ffq_energy_batch_device(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint6
                             int batch, const double* theta_dev, double* e_dev,
                             double* imag_dev);
 /* Compile and cache the program ffq_energy_batch(_device) runs for (plan, ham,
- * hf_bits) -- the support-closure program, or the compact sector lists from 27
+ * hf_bits) -- the support-closure program, or the compact sector lists from 22
  * qubits up -- without evaluating anything (otherwise compiled on the first
  * energy call: ~1-2 s of host work at 18 qubits). The one entry point that is
  * re-entrant per context: host threads may call it concurrently for DISTINCT

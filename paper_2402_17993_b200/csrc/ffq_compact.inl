@@ -1,4 +1,4 @@
-// Compact real sector layout for large UCCSD states (n > 26, BASELINE config 5).
+// Compact real sector layout for large UCCSD states (n >= 24, BASELINE config 5).
 //
 // A spin-conserving UCCSD plan applied to |HF> keeps the state in the
 // (N_alpha, N_beta) sector, and with real F on every generator the state is
