@@ -6,6 +6,16 @@
  * Written as a literal restatement of the reference SPEC (file:line cited per
  * function), favouring per-qubit loops over bit tricks so that it shares no
  * code or shortcuts with the CUDA product path.
+ *
+ * PARITY UNPINNED against the reference: the reference holds no code, golden
+ * vectors or fixtures for this path, and it cannot be built here
+ * (Eigen3, doctest absent), so there is no oracle/_ref. What pins this oracle
+ * instead (tests/test_oracle.py, tests/test_golden.py, tools/make_golden.py):
+ * every SPEC example and KAT, dense numpy/scipy matrices at <= 10 qubits, the
+ * agreement of its two evaluators (Pauli-string rotations; JW-free fermionic
+ * Givens rotations on determinants), scipy sparse matrix exponentials at configs
+ * 1-3 (tests/sparse_ref.py), the mt19937_64 known answer, and the reference's one
+ * number on the path (proj/tests/test_fmo.cpp:182-185).
  */
 #include "ffo_oracle.h"
 
