@@ -410,3 +410,34 @@ def test_sector_program_repeatable_under_load():
         assert np.array_equal(capi.energy_batch(c, plan, ham, P.hf, th), ref)
     for nb in (1, 3, 17):
         assert np.array_equal(capi.energy_batch(c, plan, ham, P.hf, th[:nb]), ref[:nb])
+
+
+def test_config5_full_size_conserved_quantities():
+    """BASELINE config 5's plan at full size (32 qubits, 2128 generators) through
+    the compact layout with Hamiltonians whose expectation is fixed by symmetry
+    for every theta: the norm (H = I), the particle number (sum (I - Z_q) / 2 =
+    16) and the alpha particle number (even qubits: 8). Size-independent checks
+    of the generator passes at the size no oracle reaches."""
+    import torch
+
+    if torch.cuda.get_device_properties(0).total_memory < 40 * 2**30:
+        pytest.skip("needs ~12 GiB of device memory")
+    P = problems.config5_problem()
+    c = capi.Context(0)
+    plan = capi.Plan(c, 32, *P.plan_arrays())
+    rng = np.random.default_rng(32)
+    rows = np.concatenate([P.plan_thetas(), rng.uniform(-0.3, 0.3, size=(2, P.n_gen))])  # also larger angles
+
+    def number_op(qubits):
+        x = np.zeros(len(qubits) + 1, np.uint64)
+        z = np.array([0] + [1 << q for q in qubits], np.uint64)
+        co = np.array([0.5 * len(qubits)] + [-0.5] * len(qubits))
+        return x, z, co
+
+    for name, (x, z, co), want in (("norm", (np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.ones(1)), 1.0),
+                                   ("N", number_op(range(32)), 16.0),
+                                   ("N_alpha", number_op(range(0, 32, 2)), 8.0)):
+        ham = capi.Hamiltonian(c, 32, x, z, co)
+        e = capi.energy_batch(c, plan, ham, P.hf, rows)
+        assert np.abs(e - want).max() <= 1e-10, (name, e)
+        del ham
