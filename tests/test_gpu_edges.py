@@ -441,3 +441,29 @@ def test_config5_full_size_conserved_quantities():
         e = capi.energy_batch(c, plan, ham, P.hf, rows)
         assert np.abs(e - want).max() <= 1e-10, (name, e)
         del ham
+
+
+def test_expectation_is_linear_in_the_hamiltonian_18q():
+    """<psi|H|psi> is linear in H: the 9316-term config-3 Hamiltonian split at
+    random into two halves (neither is molecular: their alpha-beta weights need
+    not factorise, so the clique check may refuse groups and the anchored blocks
+    or generic rows take them) must add up to the full energy on +-pi/2 shift
+    rows. Exercises the fallbacks of the expectation compiler at 18 qubits."""
+    from paper_2402_17993_b200 import parameter_shift_set
+
+    P = problems.config_problem(3, batch=1)
+    rows = np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)[::97]
+    th = P.plan_thetas(rows)
+    c = capi.Context(0)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    x, z, co = P.ham_arrays()
+    pick = np.random.default_rng(18).random(len(x)) < 0.5
+    full = capi.energy_batch(c, plan, capi.Hamiltonian(c, P.n_qubits, x, z, co), P.hf, th)
+    parts = []
+    for m in (pick, ~pick):
+        ham = capi.Hamiltonian(c, P.n_qubits, x[m], z[m], co[m])
+        parts.append(capi.energy_batch(c, plan, ham, P.hf, th))
+        info = capi.sector_info(c, plan, ham, P.hf)
+        assert info["real_amplitudes"] == 1 and info["expectation_pairs"] > 0
+        del ham
+    assert np.abs(parts[0] + parts[1] - full).max() <= 1e-10
