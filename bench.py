@@ -658,6 +658,11 @@ def main():
         line["roofline_value_kernel"] = {
             "kernel": "k_sector_eval_real" if sector["real_amplitudes"] else "k_sector_eval", "bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
             "frac": smem_ach / smem_peak, "algorithmic_bytes_per_eval": smem_bytes,
+            # round 1's byte model for comparison across rounds: every expectation pair as two
+            # amplitude reads (the pairs are the same work; cliques and blocks read fewer bytes for them)
+            "pair_model_bytes_per_eval": amp_b * (4 * sector["generator_pairs"] + 2 * sector["expectation_pairs"]),
+            "pair_model_frac": amp_b * (4 * sector["generator_pairs"] + 2 * sector["expectation_pairs"])
+            * value / world / 1e9 / smem_peak,
             "peak_source": "128 B/clk/SM x %d SMs x median SM clock under load" % n_sm,
             "sector_program": sector}
         if cpu:
