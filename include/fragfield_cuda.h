@@ -261,6 +261,19 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
                        const double* psi, double* out);
 
+/* Test hook (host only, no GPU): compiles the compact real sector program
+ * (csrc/ffq_compact.inl: row / column lists per generator, Pauli-term groups)
+ * for plan + Hamiltonian + hf and evaluates one theta row (plan order) on the
+ * host from the same lists, with the kernels' pair arithmetic. out[8]: energy,
+ * eligible (0/1: even n, <= 16 spatial orbitals, real spin-conserving fused
+ * plan), alpha strings, beta strings, generator pairs, term pairs, list
+ * violations (an index out of bounds, or a row / column list of one op touching
+ * an index twice: 0 = in bounds and race-free by construction), term groups. */
+int ffq_compact_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
+                        const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
+                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
+                        const double* theta, double* out);
+
 /* ---- multi-GPU, independent units (BASELINE configs 2-4) ---- */
 /* One context per device of `devices` (one node); every call runs one host
  * thread per device, with no data-path collective: the units (theta rows,

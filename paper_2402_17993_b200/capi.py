@@ -76,6 +76,8 @@ _SIGS = {
     "ffq_plan_compile_stats": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, _i64p]),
     "ffq_sector_emulate": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.c_int64, _u64p, _u64p,
                                      _f64p, _f64p, C.c_uint64, _f64p, _f64p]),
+    "ffq_compact_emulate": (C.c_int, [C.c_int, C.c_int, _i64p, _u64p, _u64p, _f64p, _f64p, C.c_int64, _u64p, _u64p,
+                                      _f64p, _f64p, C.c_uint64, _f64p, _f64p]),
     "ffq_sector_info": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i64p]),
     "ffq_sector_state": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _f64p, _f64p, C.POINTER(C.c_double)]),
     "ffq_multi_create": (C.c_int, [np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), C.c_int,
@@ -161,6 +163,22 @@ def sector_emulate(n, plan_arrays, ham_arrays, hf_bits, psi):
                                    out))
     keys = ["energy", "closure_size", "slots", "product", "block_pairs", "exp_pairs", "generic_rows", "units",
             "clique_pairs", "clique_conflicts", "table_violations"]
+    return dict(zip(keys, out.tolist()))
+
+
+def compact_emulate(n, plan_arrays, ham_arrays, hf_bits, theta_plan_order):
+    """Host emulation of the compact real sector program (no GPU): energy of one
+    theta row and the list statistics (ffq_compact_emulate)."""
+    off, px, pz, pc = plan_arrays
+    px, pz, pre, pim = _terms(px, pz, pc)
+    hx, hz, hre, him = _terms(*ham_arrays)
+    off = np.ascontiguousarray(off, np.int64)
+    th = np.ascontiguousarray(theta_plan_order, np.float64).ravel()
+    out = np.zeros(8)
+    check(lib().ffq_compact_emulate(n, len(off) - 1, off, px, pz, pre, pim, len(hx), hx, hz, hre, him, hf_bits, th,
+                                    out))
+    keys = ["energy", "eligible", "alpha_strings", "beta_strings", "generator_pairs", "term_pairs", "violations",
+            "term_groups"]
     return dict(zip(keys, out.tolist()))
 
 

@@ -1128,6 +1128,35 @@ int ffq_energy_prepare(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t h
   });
 }
 
+int ffq_compact_emulate(int n_qubits, int n_gen, const int64_t* term_off, const uint64_t* px, const uint64_t* pz,
+                        const double* pc_re, const double* pc_im, int64_t n_terms, const uint64_t* hx,
+                        const uint64_t* hz, const double* hc_re, const double* hc_im, uint64_t hf_bits,
+                        const double* theta, double* out) {
+  if (!out || !term_off || n_qubits < 2 || n_qubits > 32 || (n_gen > 0 && !theta))
+    return fail(nullptr, FFQ_EINVAL, "ffq_compact_emulate: invalid argument");
+  return guarded(nullptr, [&] {
+    const CompiledPlan P = compile_plan(n_qubits, n_gen, term_off, px, pz, pc_re, pc_im);
+    for (int64_t t = 0; t < n_terms; ++t)
+      if (hc_im && std::abs(hc_im[t]) > 1e-12)
+        return fail(nullptr, FFQ_ENONHERMITIAN, "ffq_compact_emulate: imaginary coefficient");
+    CompactProg cp;
+    compact_compile(P, std::vector<uint64_t>(hx, hx + n_terms), std::vector<uint64_t>(hz, hz + n_terms),
+                    std::vector<double>(hc_re, hc_re + n_terms), hf_bits, &cp);
+    for (int i = 0; i < 8; ++i) out[i] = 0.0;
+    out[1] = cp.ok ? 1.0 : 0.0;
+    if (!cp.ok) return FFQ_OK;
+    int64_t bad = 0;
+    out[0] = compact_emulate(P, cp, theta, &bad);
+    out[2] = cp.na;
+    out[3] = cp.nb;
+    out[4] = (double)cp.gen_pairs;
+    out[5] = (double)cp.term_pairs;
+    out[6] = (double)bad;
+    out[7] = (double)(cp.single.size() + cp.multi.size());
+    return FFQ_OK;
+  });
+}
+
 int ffq_sector_state(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_bits, const double* theta,
                      double* psi, double* energy) {
   if (!ctx || !plan || !ham || !theta || !psi) return fail(ctx, FFQ_EINVAL, "ffq_sector_state: invalid argument");

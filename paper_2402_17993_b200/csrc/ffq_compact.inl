@@ -319,7 +319,8 @@ struct CompactProg {
   int64_t hf_at = 0;
   std::vector<CompactOp> ops;
   std::vector<CompactGroup> single, multi;  // one-term / multi-term flip-mask groups that can contribute
-  std::vector<uint32_t> host_lists;
+  std::vector<uint32_t> host_lists, host_stra, host_strb;
+  std::vector<CompactTerm> host_terms;
   int64_t gen_pairs = 0, term_pairs = 0;  // amplitude pairs per evaluation (statistics)
   DevBuf<uint32_t> lists;
   DevBuf<CompactGroup> groups_single, groups_multi;
@@ -352,17 +353,12 @@ inline std::vector<uint32_t> strings_with(int m, int k, const std::vector<int>& 
   return out;
 }
 
-// nullptr when the plan / Hamiltonian / HF state does not fit the compact layout
-CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
-  const int n = pl->cp.n_qubits;
-  const std::string key = "compact:" + std::to_string(h->uid) + ":" + std::to_string(hf);
-  auto it = pl->compacts.find(key);
-  if (it != pl->compacts.end()) {
-    CompactProg* c = static_cast<CompactProg*>(it->second.get());
-    return c->ok ? c : nullptr;
-  }
-  auto cp = std::make_shared<CompactProg>();
-  const CompiledPlan& P = pl->cp;
+// Host compilation of the compact program (no device work): lists, ops, groups
+// and strings into cp; cp->ok = false when the plan / Hamiltonian / HF state
+// does not fit the compact layout. Terms: (x, z, Re c) of the uploaded Pauli sum.
+void compact_compile(const CompiledPlan& P, const std::vector<uint64_t>& raw_x, const std::vector<uint64_t>& raw_z,
+                     const std::vector<double>& raw_re, uint64_t hf, CompactProg* cp) {
+  const int n = P.n_qubits;
   const uint64_t ev = 0x5555555555555555ull & ((n >= 64) ? ~0ull : ((1ull << n) - 1ull)), od = ev << 1;
   struct Part {
     uint32_t x, lo, z;
@@ -435,18 +431,18 @@ CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64
       double w;
     };
     std::map<uint64_t, std::vector<RawTerm>> by_x;  // (xa, xb) -> terms, in upload order
-    for (size_t t = 0; t < h->raw_x.size(); ++t) {
-      const uint64_t x = h->raw_x[t], z = h->raw_z[t];
+    for (size_t t = 0; t < raw_x.size(); ++t) {
+      const uint64_t x = raw_x[t], z = raw_z[t];
       const int ny = __builtin_popcountll(x & z) & 3;
       if (ny & 1) continue;  // the two orientations of every pair cancel (psi real)
-      const double w = ny == 0 ? h->raw_re[t] : -h->raw_re[t];  // Re(c i^ny)
+      const double w = ny == 0 ? raw_re[t] : -raw_re[t];  // Re(c i^ny)
       const uint32_t xa = compact_pext(x, ev), xb = compact_pext(x, od);
       if (w == 0.0 || __builtin_popcount(xa) % 2 || __builtin_popcount(xb) % 2) continue;
       if (__builtin_popcount(xa) / 2 > std::min(ka, m - ka) || __builtin_popcount(xb) / 2 > std::min(kb, m - kb))
         continue;  // no sector member can pair with a sector member
       by_x[((uint64_t)xa << 32) | xb].push_back({compact_pext(z, ev), compact_pext(z, od), w});
     }
-    std::vector<CompactTerm> tl;
+    std::vector<CompactTerm>& tl = cp->host_terms;
     // members of one string set: every string whose flipped bits are half
     // filled, or (once = true) only those with the lowest flipped bit clear
     auto member_list = [&](uint32_t x, uint32_t z, bool once, const std::vector<uint32_t>& str,
@@ -474,19 +470,122 @@ CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64
       cp->term_pairs += (int64_t)g.n_rows * g.n_cols;
       (one ? cp->single : cp->multi).push_back(g);
     }
-    cp->lists.upload(L, ctx->stream);
-    cp->groups_single.upload(cp->single, ctx->stream);
-    cp->groups_multi.upload(cp->multi, ctx->stream);
-    cp->terms.upload(tl, ctx->stream);
-    cp->stra.upload(sa, ctx->stream);
-    cp->strb.upload(sb, ctx->stream);
-    CK(cudaStreamSynchronize(ctx->stream));
+    cp->host_stra = sa;
+    cp->host_strb = sb;
   }
   cp->ok = ok;
+}
+
+// nullptr when the plan / Hamiltonian / HF state does not fit the compact layout
+CompactProg* compact_program(ffq_ctx_t ctx, ffq_plan_s* pl, ffq_ham_s* h, uint64_t hf) {
+  const std::string key = "compact:" + std::to_string(h->uid) + ":" + std::to_string(hf);
+  auto it = pl->compacts.find(key);
+  if (it != pl->compacts.end()) {
+    CompactProg* c = static_cast<CompactProg*>(it->second.get());
+    return c->ok ? c : nullptr;
+  }
+  auto cp = std::make_shared<CompactProg>();
+  compact_compile(pl->cp, h->raw_x, h->raw_z, h->raw_re, hf, cp.get());
+  if (cp->ok) {
+    cp->lists.upload(cp->host_lists, ctx->stream);
+    cp->groups_single.upload(cp->single, ctx->stream);
+    cp->groups_multi.upload(cp->multi, ctx->stream);
+    cp->terms.upload(cp->host_terms, ctx->stream);
+    cp->stra.upload(cp->host_stra, ctx->stream);
+    cp->strb.upload(cp->host_strb, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   auto* raw = cp.get();
+  const bool ok = raw->ok;
   pl->compacts.emplace(key, std::move(cp));
   return ok ? raw : nullptr;
 }
+
+// Host emulation of the compact program (test hook, no GPU): the same lists,
+// the same pair arithmetic (fma order of k_compact_gen / k_compact_terms per
+// pair; sums in list order). Returns the energy of one theta row (plan order);
+// violations counts list entries out of bounds and row / column lists of one
+// op that touch an index twice (a race between CTAs or threads).
+double compact_emulate(const CompiledPlan& P, const CompactProg& cp, const double* theta, int64_t* violations) {
+  const int64_t ld = cp.ld;
+  std::vector<double> psi((size_t)cp.na * ld, 0.0);
+  psi[(size_t)cp.hf_at] = 1.0;
+  const std::vector<uint32_t>& L = cp.host_lists;
+  int64_t bad = 0;
+  auto check_list = [&](int32_t off, int32_t cnt, int limit) {
+    std::vector<uint8_t> seen((size_t)limit, 0);
+    for (int32_t t = 0; t < cnt; ++t) {
+      const uint32_t e = L[(size_t)off + t], i = e & kCompactIdx, j = (e >> 14) & kCompactIdx;
+      if ((int)i >= limit || (int)j >= limit) { ++bad; continue; }
+      if (seen[i]++) ++bad;
+      if (j != i && seen[j]++) ++bad;
+    }
+  };
+  for (size_t op = 0; op < cp.ops.size(); ++op) {
+    const CompactOp& o = cp.ops[op];
+    const double phi = theta[P.op_gen[op]] * P.op_cfac[op];
+    const double cv = std::cos(phi), sn = std::sin(phi) * P.op_sscale[op];
+    const FusedDesc& d = P.fused[P.op_idx[op]];
+    const double gh = sn * P.pair_f[4 * d.pair_off + 2], gl = sn * P.pair_f[4 * d.pair_off];
+    check_list(o.row_off, o.n_rows, cp.na);
+    if (o.n_cols) check_list(o.col_off, o.n_cols, cp.nb);
+    for (int32_t r = 0; r < o.n_rows; ++r) {
+      const uint32_t re = L[(size_t)o.row_off + r];
+      double* pi = psi.data() + (size_t)(re & kCompactIdx) * ld;
+      double* pj = psi.data() + (size_t)((re >> 14) & kCompactIdx) * ld;
+      const uint32_t sa = re >> 28;
+      const int nc = o.n_cols ? o.n_cols : cp.nb;
+      for (int t = 0; t < nc; ++t) {
+        uint32_t ci = (uint32_t)t, cj = (uint32_t)t, sg;
+        if (o.n_cols) {
+          const uint32_t ce = L[(size_t)o.col_off + t];
+          ci = ce & kCompactIdx;
+          cj = (ce >> 14) & kCompactIdx;
+          sg = (sa ^ (ce >> 28)) & 1u;
+        } else {
+          sg = (sa ^ (L[(size_t)o.col_off + t / 32] >> (t % 32))) & 1u;
+        }
+        const double x = pi[ci], y = pj[cj];
+        pi[ci] = std::fma(sg ? -gh : gh, y, cv * x);
+        pj[cj] = std::fma(sg ? -gl : gl, x, cv * y);
+      }
+    }
+  }
+  double e = 0.0;
+  auto group_sum = [&](const CompactGroup& g, bool multi) {
+    double acc = 0.0;
+    for (int32_t r = 0; r < g.n_rows; ++r) {
+      const uint32_t re = L[(size_t)g.row_off + r];
+      if ((int)(re & kCompactIdx) >= cp.na || (int)((re >> 14) & kCompactIdx) >= cp.na) { ++bad; continue; }
+      const double* pi = psi.data() + (size_t)(re & kCompactIdx) * ld;
+      const double* pj = psi.data() + (size_t)((re >> 14) & kCompactIdx) * ld;
+      const uint32_t a = cp.host_stra[re & kCompactIdx];
+      for (int32_t t = 0; t < g.n_cols; ++t) {
+        const uint32_t ce = L[(size_t)g.col_off + t];
+        if ((int)(ce & kCompactIdx) >= cp.nb || (int)((ce >> 14) & kCompactIdx) >= cp.nb) { ++bad; continue; }
+        const double p = pi[ce & kCompactIdx] * pj[(ce >> 14) & kCompactIdx];
+        if (!multi) {
+          acc += (((re >> 28) ^ (ce >> 28)) & 1u) ? -p : p;
+        } else {
+          const uint32_t b = cp.host_strb[ce & kCompactIdx];
+          double f = 0.0;
+          for (int k = 0; k < g.nt; ++k) {
+            const CompactTerm& tm = cp.host_terms[(size_t)g.t0 + k];
+            const uint32_t s = ((uint32_t)__builtin_popcount(a & tm.za) ^ (uint32_t)__builtin_popcount(b & tm.zb)) & 1u;
+            f += s ? -tm.w : tm.w;
+          }
+          acc = std::fma(f, p, acc);
+        }
+      }
+    }
+    return multi ? acc : acc * g.w;
+  };
+  for (const CompactGroup& g : cp.single) e += group_sum(g, false);
+  for (const CompactGroup& g : cp.multi) e += group_sum(g, true);
+  if (violations) *violations = bad;
+  return e;
+}
+
 
 // IL theta rows (device, stride n_gen) -> e[0..IL) (device), the lanes interleaved in one matrix
 template <int IL>

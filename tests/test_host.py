@@ -334,3 +334,52 @@ def test_sector_program_emulation_on_a_non_molecular_hamiltonian(oracle):
     assert abs(r["energy"] - ref.real) <= 1e-12
     assert r["table_violations"] == 0 and r["product"] == 1
     assert r["clique_pairs"] + r["block_pairs"] > 0
+
+
+@pytest.mark.parametrize("case", ["config1", "config2", "config5_14q", "uccsd_10q_open"])
+def test_compact_program_emulation_matches_oracle(oracle, case):
+    """The compact real sector program (csrc/ffq_compact.inl: row / column lists
+    per generator, Pauli-term groups with every pair once), compiled and run on
+    the host from the lists the kernels read, against the oracle's Trotter energy
+    (per-string rotations, term-by-term expectation): molecular Hamiltonians
+    (multi-term groups), the config-5 recipe (one-term groups of random strings,
+    odd-Y terms dropped) and an open-shell sector (N_alpha != N_beta)."""
+    if case == "config1":
+        P = problems.config_problem(1)
+    elif case == "config2":
+        P = problems.config_problem(2)
+    elif case == "config5_14q":
+        P = problems.config5_problem(n_doubles=120, n_terms=300, n_qubits=14, n_elec=6)
+    else:
+        P = problems.make_problem(5, 5, problems.ham_seed(9, 5))
+    off, x, z, c = P.plan_arrays()
+    th = P.plan_thetas()[0]
+    r = capi.compact_emulate(P.n_qubits, (off, x, z, c), P.ham_arrays(), P.hf, th)
+    assert r["eligible"] == 1 and r["violations"] == 0
+    na, nb = bin(P.hf & 0x55555555).count("1"), bin(P.hf & 0xAAAAAAAA).count("1")
+    from math import comb
+    assert (r["alpha_strings"], r["beta_strings"]) == (comb(P.n_qubits // 2, na), comb(P.n_qubits // 2, nb))
+    psi = oracle.hf_state(P.n_qubits, P.hf)
+    for g in range(len(off) - 1):
+        gx, gz, gc = x[off[g]:off[g + 1]], z[off[g]:off[g + 1]], c[off[g]:off[g + 1]]
+        for i in np.lexsort((gz, gx)):  # canonical (x, z) order within a generator
+            psi = oracle.apply_pauli_rotation(P.n_qubits, psi, int(gx[i]), int(gz[i]), th[g] * gc[i].imag)
+    hx, hz, hc = P.ham_arrays()
+    ref = oracle.expectation(P.n_qubits, psi, oracle.PauliSum.from_terms(P.n_qubits, hx, hz, hc)).real
+    assert abs(r["energy"] - ref) <= 1e-11, (r["energy"], ref)
+    assert r["generator_pairs"] > 0 and r["term_groups"] > 0
+
+
+def test_compact_program_eligibility():
+    # a generator that does not conserve both spin counts (alpha -> beta single
+    # excitation image) and a non-fused plan are refused: eligible = 0, no energy
+    P = problems.config_problem(1)
+    off, x, z, c = P.plan_arrays()
+    bad_off = np.array([0, 2], np.int64)  # X0 X1 / Y0 Y1-like pair: flips one alpha and one beta qubit
+    bx = np.array([0b11, 0b11], np.uint64)
+    bz = np.array([0b01, 0b10], np.uint64)
+    bc = np.array([0.5j, -0.5j])
+    r = capi.compact_emulate(P.n_qubits, (bad_off, bx, bz, bc), P.ham_arrays(), P.hf, np.array([0.3]))
+    assert r["eligible"] == 0
+    r = capi.compact_emulate(P.n_qubits, (off, x, z, c), P.ham_arrays(), P.hf, P.plan_thetas()[0])
+    assert r["eligible"] == 1
