@@ -445,7 +445,7 @@ def main():
     si2 = capi.sector_info(ctx, plan2, ham2, P2.hf)
     config2 = {"evals": int(rows2.shape[0]), "ms_per_call": statistics.mean(ms2),
                "evals_per_s": rows2.shape[0] / (statistics.mean(ms2) / 1e3),
-               "path": "%s, one 256-thread CTA per evaluation, support closure of %d amplitudes" % (
+               "path": "%s, one 128-thread CTA per evaluation (eight per SM), support closure of %d amplitudes" % (
                    "k_sector_eval_real" if si2["real_amplitudes"] else "k_sector_eval", si2["closure_size"])}
 
     # secondary: BASELINE.json config 4 -- FMO batch of 3 monomers (12 q) + 3 dimers

@@ -495,7 +495,7 @@ size_t smem_bytes(const ffq_plan_s* pl) {
 }
 
 constexpr int kSectorThreads = 768;       // per CTA of a 2/4/8-CTA cluster (measured best at 18 qubits)
-constexpr int kSectorSingleThreads = 256;  // one-CTA evaluations (small closures, many CTAs per SM)
+constexpr int kSectorSingleThreads = 128;  // one-CTA evaluations (small closures, many CTAs per SM)
 constexpr int kSectorRealThreads = 1024;   // one-CTA real-amplitude evaluations of large closures
 // small closures run one CTA per evaluation (many per SM); large ones a 2^s-CTA cluster
 constexpr uint32_t kSectorSingleMax = 2048;  // <= 32 KiB of amplitudes per CTA

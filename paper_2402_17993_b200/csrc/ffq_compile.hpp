@@ -35,7 +35,7 @@ namespace ffq {
 
 using cplx = std::complex<double>;
 constexpr int kSectorHeadPad = 8;   // empty ops behind gen_head (>= the kernel's prefetch depth)
-constexpr int kSectorHeadSmall = 256, kSectorHeadLarge = 1024;  // threads of the real one-CTA program
+constexpr int kSectorHeadSmall = 128, kSectorHeadLarge = 1024;  // threads of the real one-CTA program
 constexpr int kMaxTableBits = 6;  // |X| up to 6 -> pattern tables of <= 64 entries
 
 struct BadInput : std::invalid_argument {

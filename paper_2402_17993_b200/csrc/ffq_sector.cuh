@@ -540,7 +540,7 @@ __device__ __forceinline__ double clique_tasks(const SectorDev& sd, int warp, in
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 4 : 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
+__global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
                                                             int n_rows, long long* __restrict__ phase_clk,

@@ -216,7 +216,7 @@ def test_sector_program_emulation_matches_oracle(oracle, cfg):
         assert r["block_pairs"] + r["clique_pairs"] >= 0.8 * r["exp_pairs"] and r["units"] > 0
         # the alpha-beta pairs (36 alpha x 36 beta single excitations, 35 x 70 pairs each) all factorise
         assert r["clique_pairs"] == 36 * 36 * 35 * 70
-    else:  # small closures keep the natural layout (256-thread program)
+    else:  # small closures keep the natural layout (128-thread program)
         assert r["product"] == 0 and r["block_pairs"] == 0
 
 
