@@ -1234,8 +1234,15 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
     // large batch goes in chunks of whole SM waves: the host copies chunk c + 1
     // into the staging buffer and its H2D is queued while chunk c computes
     // (energies are bitwise independent of the split).
-    ctx->ensure_pinned(nth + 2 * (size_t)batch);
-    double* stage_e = ctx->pinned + nth;
+    // theta already in page-locked host memory (cudaHostAlloc / cudaHostRegister,
+    // e.g. a pinned torch tensor): the H2D copies read it in place, no staging
+    cudaPointerAttributes pa{};
+    const bool user_pinned = nth > 0 && cudaPointerGetAttributes(&pa, theta) == cudaSuccess &&
+                             pa.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();  // (an unregistered pointer may leave a sticky-free error code on old drivers)
+    ctx->ensure_pinned((user_pinned ? 0 : nth) + 2 * (size_t)batch);
+    double* stage_e = ctx->pinned + (user_pinned ? 0 : nth);
+    const double* src = user_pinned ? theta : ctx->pinned;
     DevBuf<double>& th = ctx->io_theta;
     DevBuf<double>& eo = ctx->io_e;
     th.alloc(std::max<size_t>(1, nth));
@@ -1257,15 +1264,14 @@ int ffq_energy_batch(ffq_ctx_t ctx, ffq_plan_t plan, ffq_ham_t ham, uint64_t hf_
       const size_t o = (size_t)b0 * ng, n = (size_t)nb * ng;
       if (n && piped) {
         // chunk k's copy runs on the copy stream while chunk k - 1 computes
-        std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
+        if (!user_pinned) std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
         const cudaEvent_t ev = ctx->copy_event((size_t)k + 1);
-        CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice,
-                           ctx->copy_stream));
+        CK(cudaMemcpyAsync(th.p + o, src + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->copy_stream));
         CK(cudaEventRecord(ev, ctx->copy_stream));
         CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
       } else if (n) {
-        std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
-        CK(cudaMemcpyAsync(th.p + o, ctx->pinned + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (!user_pinned) std::memcpy(ctx->pinned + o, theta + o, n * sizeof(double));
+        CK(cudaMemcpyAsync(th.p + o, src + o, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
       }
       energy_device(ctx, plan, ham, hf_bits, nb, th.p + o, eo.p + b0, eo.p + batch + b0);
       b0 += nb;

@@ -467,3 +467,24 @@ def test_expectation_is_linear_in_the_hamiltonian_18q():
         assert info["real_amplitudes"] == 1 and info["expectation_pairs"] > 0
         del ham
     assert np.abs(parts[0] + parts[1] - full).max() <= 1e-10
+
+
+def test_energy_batch_pinned_and_pageable_inputs_agree(ctx_default):
+    """ffq_energy_batch reads theta in place when it lies in page-locked host
+    memory and stages it through its own pinned buffer otherwise; large batches
+    go in chunks of SM waves. Same energies bit for bit either way."""
+    import torch
+
+    from paper_2402_17993_b200 import parameter_shift_set
+
+    c = ctx_default
+    P = problems.config_problem(3, batch=1)
+    rows = np.array(parameter_shift_set(list(P.thetas[0]))).reshape(-1, P.n_gen)[:400]  # 1.8 MB: the chunked path
+    th = P.plan_thetas(rows)
+    plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
+    ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    pinned = torch.from_numpy(th).pin_memory().numpy()
+    a = capi.energy_batch(c, plan, ham, P.hf, th)
+    b = capi.energy_batch(c, plan, ham, P.hf, pinned)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a[:3], capi.energy_batch(c, plan, ham, P.hf, pinned[:3]))  # unchunked
