@@ -136,3 +136,24 @@ def test_config5_full_size_sharded_equals_compact():
     del sh
     assert swaps > 100 and sorted(perm.tolist()) == list(range(32))
     assert abs(e_sh - e_compact[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 8), (2, 12)])
+def test_every_shard_size_with_random_pauli_hamiltonian(ctx, cfg, n):
+    """Every global-qubit count the plan allows (a double needs 4 local qubits),
+    with a random-string Hamiltonian (generic one-term groups): covers shards of
+    16 amplitudes (no bitmap path), 32 (one-word bitmaps), 64 and more
+    (support-tracked passes and support-compacted swaps)."""
+    import paper_2402_17993_b200 as ff
+
+    P = problems.config_problem(cfg)
+    x, z, co = ff.random_pauli_hamiltonian(n, 200, 77 + cfg).arrays()
+    plan = capi.Plan(ctx, n, *P.plan_arrays())
+    ham = capi.Hamiltonian(ctx, n, x, z, co)
+    ref = capi.energy_batch(ctx, plan, ham, P.hf, P.plan_thetas())[0]
+    for g in range(0, min(6, n - 4) + 1):
+        e = capi.ShardedState(ctx, n, g).energy(plan, ham, P.hf, P.plan_thetas()[0])
+        assert abs(e - ref) <= 1e-12, (g, e, ref)
+    # fewer than 4 local qubits (n = 8) or more than 6 global ones (n = 12): refused, not a wrong number
+    with pytest.raises(Exception):
+        capi.ShardedState(ctx, n, n - 3).energy(plan, ham, P.hf, P.plan_thetas()[0])
