@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "UCCSD energy evals/sec at 18 qubits (c128); rotation-pass HBM GB/s vs peak"
 # ncu --set full of k_pauli_rotation at 28 qubits (profiles/r01): dram__bytes_read.sum
 # + dram__bytes_write.sum per launch (4.294980 + 4.236504 GB); algorithmic = 8.589934592 GB
-ROT_TRAFFIC_BYTES = 8531484000
+ROT_TRAFFIC_BYTES = 8532632000
 UNIT = "evals/s"
 
 
@@ -627,7 +627,7 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "frac_of_nominal_8tbs": achieved / 8000.0,
                          "traffic": ROT_TRAFFIC_BYTES if nq == 28 else None,
-                         "traffic_source": "profiles/r01/ncu_full_summaries.txt (dram read+write per launch)",
+                         "traffic_source": "profiles/r02/ncu_full_rotation_pass_r02.txt (dram read+write per launch, ncu --set full)",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": rot_bytes, "state_qubits": nq,
                          "avg_launch_ms": rot_avg},
