@@ -32,8 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "UCCSD energy evals/sec at 18 qubits (c128); rotation-pass HBM GB/s vs peak"
-# ncu --set full of k_pauli_rotation at 28 qubits (profiles/r01): dram__bytes_read.sum
-# + dram__bytes_write.sum per launch (4.294980 + 4.236504 GB); algorithmic = 8.589934592 GB
+# ncu --set full of k_pauli_rotation at 28 qubits (profiles/r02/ncu_full_rotation_pass_r02.txt):
+# dram__bytes_read.sum + dram__bytes_write.sum per launch (4.295201 + 4.237431 GB);
+# algorithmic = 8.589934592 GB
 ROT_TRAFFIC_BYTES = 8532632000
 UNIT = "evals/s"
 
