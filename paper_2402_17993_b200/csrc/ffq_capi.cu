@@ -191,7 +191,8 @@ struct ffq_ctx_s {
   // scratch
   DevBuf<double> theta, eout, eim, io_theta, io_e;
   DevBuf<double2> cs, partial, slab;
-  DevBuf<double> compact_psi, compact_coef, compact_part;  // compact real sector path (ffq_compact.inl)
+  DevBuf<double> compact_psi, compact_coef, compact_part, compact_io;  // compact real sector path (ffq_compact.inl)
+  int compact_graph = 1;                     // env FFQ_COMPACT_GRAPH=0: small compact matrices launch by launch
   int compact_il = 8;                        // env FFQ_COMPACT_IL: most theta rows interleaved per matrix (1, 2, 4, 8)
   int sector_roles = 1;                      // env FFQ_ROLES=0: split evaluations without role warps
   int sector_warm = 1;                       // env FFQ_WARM=0: no L2 warm-up pass before small sector batches
@@ -946,6 +947,7 @@ int ffq_ctx_create(int device, ffq_ctx_t* out) {
     if (const char* e = std::getenv("FFQ_COMPACT")) c->compact = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_MIN")) c->compact_min_qubits = std::atoi(e);
     if (const char* e = std::getenv("FFQ_COMPACT_IL")) c->compact_il = std::atoi(e);
+    if (const char* e = std::getenv("FFQ_COMPACT_GRAPH")) c->compact_graph = std::atoi(e);
     if (const char* e = std::getenv("FFQ_WARM")) c->sector_warm = std::atoi(e);
     if (const char* e = std::getenv("FFQ_ROLES")) c->sector_roles = std::atoi(e);
     if (const char* e = std::getenv("FFQ_SPLIT")) c->sector_split = std::min(32, std::max(1, std::atoi(e)));

@@ -42,6 +42,7 @@
 
 constexpr int kCompactThreads = 256;
 constexpr uint32_t kCompactIdx = 0x3FFFu;  // 14-bit ranks: C(16, 8) = 12870
+constexpr size_t kCompactGraphMax = (size_t)1 << 23;  // matrix doubles (64 MiB) up to which a lane group runs as a CUDA graph
 
 struct CompactOp {  // one fused op: offsets into CompactProg::lists
   int32_t row_off, n_rows;
@@ -648,14 +649,53 @@ void compact_energy(ffq_ctx_t ctx, ffq_plan_s* pl, CompactProg& cp, const double
     const int il = lanes(batch - b);
     const double* th = theta + (size_t)b * ng;
     double* imb = im ? im + b : nullptr;
-    if (il == 8)
-      compact_energy_lanes<8>(ctx, pl, cp, th, e + b, imb);
-    else if (il == 4)
-      compact_energy_lanes<4>(ctx, pl, cp, th, e + b, imb);
-    else if (il == 2)
-      compact_energy_lanes<2>(ctx, pl, cp, th, e + b, imb);
-    else
-      compact_energy_lanes<1>(ctx, pl, cp, th, e + b, imb);
+    auto run = [&](const double* th_in, double* e_out, double* im_out) {
+      if (il == 8)
+        compact_energy_lanes<8>(ctx, pl, cp, th_in, e_out, im_out);
+      else if (il == 4)
+        compact_energy_lanes<4>(ctx, pl, cp, th_in, e_out, im_out);
+      else if (il == 2)
+        compact_energy_lanes<2>(ctx, pl, cp, th_in, e_out, im_out);
+      else
+        compact_energy_lanes<1>(ctx, pl, cp, th_in, e_out, im_out);
+    };
+    // Small matrices: the ~n_ops passes are launch-bound (a few microseconds of
+    // work each), so the lane group's launches are captured once per (program,
+    // buffers, lanes) as a CUDA graph reading theta from / writing the energies
+    // to fixed staging buffers, and replayed.
+    if (ctx->compact_graph && (size_t)cp.na * cp.ld * il <= kCompactGraphMax) {
+      ctx->compact_io.alloc((size_t)8 * ng + 16);
+      double* th_stage = ctx->compact_io.p;
+      double* e_stage = ctx->compact_io.p + (size_t)8 * ng;
+      GraphKey key{(uintptr_t)0xC09AC7, (uintptr_t)&cp, (uintptr_t)il, (uintptr_t)ctx->compact_psi.p,
+                   (uintptr_t)ctx->compact_coef.p, (uintptr_t)ctx->compact_part.p, (uintptr_t)ctx->compact_io.p};
+      auto it = pl->graphs.find(key);
+      if (it == pl->graphs.end()) {
+        cudaGraph_t graph;
+        const int64_t before = ctx->launches;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          run(th_stage, e_stage, e_stage + 8);
+        } catch (...) {
+          cudaStreamEndCapture(ctx->stream, &graph);
+          throw;
+        }
+        CK(cudaStreamEndCapture(ctx->stream, &graph));
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        pl->graph_nodes[key] = ctx->launches - before;
+        ctx->launches = before;
+        it = pl->graphs.emplace(key, exec).first;
+      }
+      CK(cudaMemcpyAsync(th_stage, th, sizeof(double) * (size_t)il * ng, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (cudaGraphLaunch(it->second, ctx->stream) != cudaSuccess) throw CudaError("cudaGraphLaunch failed (compact)");
+      ctx->launches += pl->graph_nodes[key];
+      CK(cudaMemcpyAsync(e + b, e_stage, sizeof(double) * il, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (imb) CK(cudaMemcpyAsync(imb, e_stage + 8, sizeof(double) * il, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      run(th, e + b, imb);
+    }
     b += il;
   }
 }
