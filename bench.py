@@ -506,6 +506,48 @@ def main():
                 "compiled once, device-resident theta, max over ranks"}
     del fsets
 
+    # SPEC.md:566 (--jobs): fragment VQE runs execute concurrently. One context (own stream)
+    # and one host thread per fragment on this GPU, every thread evaluating its fragment's
+    # energy (B = 1) `reps` times; wall clock per round of six evaluations, against the same
+    # evaluations issued one after another on one context.
+    if rank == 0:
+        import threading
+
+        reps = 50
+        jobs = []
+        for lab, Pf in _pb.fmo_fragments().items():
+            cj = capi.Context(gpu)
+            pj = capi.Plan(cj, Pf.n_qubits, *Pf.plan_arrays())
+            hj = capi.Hamiltonian(cj, Pf.n_qubits, *Pf.ham_arrays())
+            tj = Pf.plan_thetas()[:1]
+            capi.energy_batch(cj, pj, hj, Pf.hf, tj)  # compile
+            jobs.append((cj, pj, hj, Pf.hf, tj))
+
+        def serve(job, out, k):
+            cj, pj, hj, hf, tj = job
+            for _ in range(reps):
+                out[k] = capi.energy_batch(cj, pj, hj, hf, tj)[0]
+
+        res = [0.0] * len(jobs)
+        t0 = time.perf_counter()
+        for k, job in enumerate(jobs):
+            serve(job, res, k)
+        t_seq = (time.perf_counter() - t0) / reps
+        seq = list(res)
+        threads = [threading.Thread(target=serve, args=(job, res, k)) for k, job in enumerate(jobs)]
+        t0 = time.perf_counter()
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        t_con = (time.perf_counter() - t0) / reps
+        config4["concurrent_fragment_jobs"] = {
+            "fragments": len(jobs), "ms_per_round_sequential": 1e3 * t_seq, "ms_per_round_concurrent": 1e3 * t_con,
+            "same_energies": bool(seq == res),
+            "note": "six B = 1 energy evaluations (3 monomers, 3 dimers), one context and host thread per "
+                    "fragment on one GPU (SPEC.md:566 --jobs); wall clock incl. H2D/D2H per evaluation"}
+        del jobs
+
     # strong scaling: ONE config-3 gradient set (rank 0's 1121 rows)
     # split over the ranks by dist.row_range, no data-path collective, energies
     # gathered in rank order; must equal the one-GPU energies bit for bit
