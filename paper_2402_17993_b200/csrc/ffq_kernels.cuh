@@ -286,22 +286,37 @@ __global__ void __launch_bounds__(NT) k_expect_items(const double2* __restrict__
   for (int i = 0; i < d.w; ++i) Q |= 1ULL << ((d.qpack >> (6 * i)) & 63u);
   const uint64_t step = insert_bits<uint64_t>((uint64_t)NT, d.qpack, d.w);
   uint64_t mz = insert_bits<uint64_t>((uint64_t)(u0 + threadIdx.x), d.qpack, d.w);
-  for (int64_t u = u0 + threadIdx.x; u < u1; u += NT, mz = ((mz | Q) + step) & ~Q) {
-    const uint64_t m = mz | pb;
-    const double2 a = s[m];
-    if (a.x == 0.0 && a.y == 0.0) continue;  // zero product: skip partner load and classes
-    const double2 bb = s[m ^ d.x];
-    double2 f = make_double2(0, 0);
-    for (int o = 0; o < d.ncls; ++o) {
-      const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);
-      const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
-      f.x = fma(sg, fo.x, f.x);
-      f.y = fma(sg, fo.y, f.y);
+  // four members per trip, every load issued before the class sums (the dense
+  // path streams the whole state: the loads, not the arithmetic, are the cost)
+  constexpr int UN = 4;
+  for (int64_t u = u0 + threadIdx.x; u < u1; u += (int64_t)UN * NT) {
+    uint64_t mm[UN];
+    double2 av[UN], bv[UN];
+#pragma unroll
+    for (int j = 0; j < UN; ++j) {
+      mm[j] = mz | pb;
+      const bool live = u + (int64_t)j * NT < u1;
+      av[j] = live ? s[mm[j]] : make_double2(0.0, 0.0);
+      bv[j] = live ? s[mm[j] ^ d.x] : make_double2(0.0, 0.0);
+      mz = ((mz | Q) + step) & ~Q;
     }
-    // Re(conj(bb) * a * f); the weight 2 of off-diagonal pairs is folded into F
-    const double2 pr = make_double2(bb.x * a.x + bb.y * a.y, bb.x * a.y - bb.y * a.x);
-    acc.x = fma(pr.x, f.x, acc.x);
-    acc.x = fma(-pr.y, f.y, acc.x);
+#pragma unroll
+    for (int j = 0; j < UN; ++j) {
+      const double2 a = av[j], bb = bv[j];
+      if (a.x == 0.0 && a.y == 0.0) continue;  // zero product (also the members past the chunk)
+      const uint64_t m = mm[j];
+      double2 f = make_double2(0, 0);
+      for (int o = 0; o < d.ncls; ++o) {
+        const double sg = sgn_par(m & h.cls_z[d.cls_off + o]);
+        const double2 fo = h.cls_f[d.val_off + o * d.nact + p];
+        f.x = fma(sg, fo.x, f.x);
+        f.y = fma(sg, fo.y, f.y);
+      }
+      // Re(conj(bb) * a * f); the weight 2 of off-diagonal pairs is folded into F
+      const double2 pr = make_double2(bb.x * a.x + bb.y * a.y, bb.x * a.y - bb.y * a.x);
+      acc.x = fma(pr.x, f.x, acc.x);
+      acc.x = fma(-pr.y, f.y, acc.x);
+    }
   }
   acc = block_sum<NT>(acc, red);
   if (threadIdx.x == 0) partial[(int64_t)b * gridDim.x + item] = acc;
