@@ -1,6 +1,7 @@
 """Sharded state across real processes (gloo, CPU): the swap schedule of the
 C-ABI (ffq_shard_schedule_steps), the half-shard pack/unpack index math of
-k_swap_pack/k_swap_unpack and the per-pattern partner exchange of the sharded
+k_swap_pack/k_swap_unpack (and of the support-compacted swap: counts first,
+then (index, value) lists) and the per-pattern partner exchange of the sharded
 expectation, executed by 2 and 4 ranks with torch.distributed point-to-point
 messages. The per-shard compute is the CPU oracle (no device here); energies
 and the gathered logical state must equal the unsharded oracle."""
@@ -40,6 +41,25 @@ def _exchange(buf, partner):
     return out
 
 
+def _exchange_lists(idx, vals, partner):
+    """The support-compacted swap's wire protocol (shard_swap_sparse): the two
+    counts first (one int64 each way), then `count` indices and values each way."""
+    n_mine = torch.tensor([len(idx)], dtype=torch.int64)
+    n_peer = int(_exchange(n_mine, partner)[0])
+    r_idx = torch.empty(n_peer, dtype=torch.int64)
+    r_val = torch.empty(n_peer, dtype=torch.complex128)
+    ops = []
+    if len(idx):
+        ops += [dist.P2POp(dist.isend, torch.from_numpy(idx), partner),
+                dist.P2POp(dist.isend, torch.from_numpy(vals), partner)]
+    if n_peer:
+        ops += [dist.P2POp(dist.irecv, r_idx, partner), dist.P2POp(dist.irecv, r_val, partner)]
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    return r_idx.numpy(), r_val.numpy()
+
+
 def _half_indices(l, lpos, val):
     """k_swap_pack order: u ascending, zero inserted at lpos, bit lpos = val."""
     u = np.arange(1 << (l - 1), dtype=np.int64)
@@ -47,7 +67,7 @@ def _half_indices(l, lpos, val):
     return ((u >> lpos) << (lpos + 1)) | lo | (val << lpos)
 
 
-def _worker(rank, world, port, q, n, ne, seed):
+def _worker(rank, world, port, q, n, ne, seed, sparse=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -70,8 +90,17 @@ def _worker(rank, world, port, q, n, ne, seed):
                 j = gpos - l
                 bit = (rank >> j) & 1
                 idx = _half_indices(l, int(lpos), 1 - bit)
-                recv = _exchange(torch.from_numpy(np.ascontiguousarray(shard[idx])), rank ^ (1 << j))
-                shard[idx] = recv.numpy()
+                if sparse:
+                    # k_swap_pack_sparse / k_swap_unpack_sparse: only the non-zero amplitudes of the half
+                    # move, as (index within the half, value); the slots they leave are cleared
+                    u = np.nonzero(shard[idx] != 0)[0].astype(np.int64)
+                    vals = np.ascontiguousarray(shard[idx[u]])
+                    shard[idx[u]] = 0.0
+                    r_u, r_v = _exchange_lists(u, vals, rank ^ (1 << j))
+                    shard[idx[r_u]] = r_v
+                else:
+                    recv = _exchange(torch.from_numpy(np.ascontiguousarray(shard[idx])), rank ^ (1 << j))
+                    shard[idx] = recv.numpy()
                 qa = int(np.nonzero(perm == gpos)[0][0])
                 qb = int(np.nonzero(perm == lpos)[0][0])
                 perm[qa], perm[qb] = perm[qb], perm[qa]
@@ -106,8 +135,8 @@ def _worker(rank, world, port, q, n, ne, seed):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_protocol_across_processes(world):
+@pytest.mark.parametrize("world,sparse", [(2, False), (4, False), (2, True), (4, True)])
+def test_sharded_protocol_across_processes(world, sparse):
     from oracle import ffo
 
     n, ne, seed = 10, 4, problems.ham_seed(7)
@@ -120,7 +149,7 @@ def test_sharded_protocol_across_processes(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, ne, seed)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, ne, seed, sparse)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
