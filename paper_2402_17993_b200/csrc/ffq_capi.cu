@@ -697,7 +697,8 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
                         double* e, double* im, long long* clk, double* state_out = nullptr) {
   // anchored blocks keep the shared-row f table behind the per-op tables
   const size_t sb = sector_real_smem_bytes(sd.n_slots, pl->cp.op_kind.size()) + (size_t)sd.n_ftab * sizeof(double);
-  CK(cudaFuncSetAttribute(k_sector_eval_real<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  CK(cudaFuncSetAttribute(k_sector_eval_real<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  if (NT == 32 * 32) CK(cudaFuncSetAttribute(k_sector_eval_real<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   // Batches smaller than the SM count: up to sector_split CTAs per evaluation
   // (1024-thread program only). Each runs the generator phase and 32 / split
   // of the warp shares of the expectation; the energies are bit-identical.
@@ -712,16 +713,20 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   }
   // role warps (split evaluations of the 1024-thread program): each of the
   // 32 / split warp shares of a CTA gets `roles` warps (generic rows, block
-  // stream, clique tasks); needs >= 2 warps per share and the exchange buffer
-  // ([share][1 + tasks][32] doubles) inside the per-op tables
+  // stream segments, clique tasks); needs >= 2 warps per share and the exchange
+  // buffer ([share][segments + tasks][32] doubles) inside the per-op tables
   int roles = 0;
   if (split > 1 && ctx->sector_roles) {
     const int r = 32 / (32 / split);
-    const size_t need = (size_t)(32 / split) * ((r >= 3 ? 1 : 0) + sd.max_warp_tasks) * 32 * sizeof(double);
+    const size_t need = (size_t)(32 / split) * ((r >= 3 ? kBlkSegments : 0) + sd.max_warp_tasks) * 32 * sizeof(double);
     if (r >= 2 && need <= pl->cp.op_kind.size() * 2 * sizeof(double2)) roles = r;
   }
-  k_sector_eval_real<NT><<<batch * split, NT, sb, ctx->stream>>>(sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch,
-                                                                 clk, split, ctx->warp_sums.p, state_out, roles);
+  if (roles >= 2)
+    k_sector_eval_real<NT, NT == 32 * 32><<<batch * split, NT, sb, ctx->stream>>>(
+        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles);
+  else
+    k_sector_eval_real<NT, false><<<batch * split, NT, sb, ctx->stream>>>(
+        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles);
   CK(cudaGetLastError());
   ctx->launches++;
   if (split > 1) {
@@ -1594,6 +1599,15 @@ int ffq_sector_emulate(int n_qubits, int n_gen, const int64_t* term_off, const u
       for (uint32_t w : S.row_pairs)
         if ((w & 0x7FFFu) > S.n_slots || ((w >> 15) & 0x7FFFu) > S.n_slots) ++bad;
       for (size_t w = 0; w < S.blk_warp.size() / 4; ++w) {
+        // segments: begin <= cut 1 <= cut 2 <= end, whole prefetch rounds each, an anchor row first
+        const int32_t* h = &S.blk_warp[4 * w];
+        const int32_t edge[kBlkSegments + 1] = {h[0], h[2], h[3], h[1]};
+        for (int sg = 0; sg < kBlkSegments; ++sg) {
+          if (edge[sg] > edge[sg + 1] || (edge[sg + 1] - edge[sg]) % kStreamQuantum) ++bad;
+          if (edge[sg] < edge[sg + 1])
+            for (int l = 0; l < 32; ++l)
+              if (!(S.blk_stream[(size_t)edge[sg] * 32 + l] >> 30)) ++bad;
+        }
         uint32_t bs = 0;
         for (int r = S.blk_warp[4 * w]; r < S.blk_warp[4 * w + 1]; ++r)
           for (int l = 0; l < 32; ++l) {

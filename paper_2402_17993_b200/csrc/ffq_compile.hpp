@@ -723,7 +723,9 @@ struct SectorProgram {
   std::vector<double> ftab;            // distinct shared-row f values
   std::vector<double> blk_shf;         // [shared rows] f per row
   // Per-warp row streams (what the device runs): the units of warp w back to
-  // back, rows [blk_warp[4w], blk_warp[4w+1]) of 32 lane words each:
+  // back, rows [blk_warp[4w], blk_warp[4w+1]) of 32 lane words each, cut into
+  // three segments at rows blk_warp[4w+2] <= blk_warp[4w+3] (unit boundaries;
+  // every segment padded with zero rows to whole prefetch rounds):
   //   bit 30 clear: shared row  O | sign << 15 | ftab index << 16
   //   bit 30 set:   anchor row  anchor slot | B slot << 15 | 1 << 30 (closes the previous unit)
   std::vector<uint32_t> blk_stream;
@@ -750,7 +752,8 @@ constexpr int kFTabMax = 3968;        // shared-row f values (kernel parameter s
 constexpr int kBlockMinLanes = 16;    // smaller chunks go to the generic rows
 constexpr int kBlockRowQuantum = 1;   // shared rows per unit padded to a multiple of this
 constexpr int kBlkTrips = 6;          // k_sector_eval_real: four-row trips of block words in flight per warp (4: 877k, 6: 869k, 8: 906k expectation cycles, config 3)
-constexpr int kStreamQuantum = 4 * kBlkTrips;  // rows per warp stream padded to a multiple of this
+constexpr int kStreamQuantum = 4 * kBlkTrips;  // rows per warp stream segment padded to a multiple of this
+constexpr int kBlkSegments = 3;       // segments of a warp's block stream (summed separately, added in order)
 
 // Anchored string blocks for the expectation pairs of a product-layout sector
 // (see SectorProgram). For pair (i, j = i ^ X) with X = Xa | Xb (alpha / beta
@@ -1801,19 +1804,65 @@ inline SectorProgram compile_sector(const CompiledPlan& P, const CompiledHam& H,
       S.cq_desc.swap(desc);
       S.cq_coef.swap(coef);
     }
+    // A warp's stream is cut at unit boundaries into kBlkSegments segments of about
+    // equal length, each padded to whole prefetch rounds: the kernel sums every
+    // segment from zero and adds the segment sums in order, so the role warps of a
+    // split evaluation can take one segment each (same bits as one warp running all).
+    // Among the unit boundaries within a twelfth of the stream of the even cuts,
+    // the pair with the least padding is taken (ties: the most even cut).
     S.blk_warp.clear();
     for (int w = 0; w < nw; ++w) {
       std::sort(mine[w].begin(), mine[w].end());
-      const int32_t r0 = (int32_t)(S.blk_stream.size() / 32), f0 = (int32_t)(S.blk_fs.size() / 32);
-      for (size_t u : mine[w]) {
-        const int32_t* h = &S.blk_units[8 * u];
+      static_assert(kBlkSegments == 3, "two cuts are chosen below");
+      std::vector<int64_t> edge{0};  // rows before unit k of this warp
+      for (size_t u : mine[w]) edge.push_back(edge.back() + 1 + S.blk_units[8 * u + 5]);
+      const int64_t total = edge.back();
+      auto padded = [](int64_t rows) { return (rows + kStreamQuantum - 1) / kStreamQuantum * kStreamQuantum; };
+      auto near = [&](int64_t target) {
+        std::vector<size_t> c;
+        for (size_t k = 0; k < edge.size(); ++k)
+          if (std::llabs(edge[k] - target) * 12 <= total) c.push_back(k);
+        if (c.empty()) c.push_back(std::lower_bound(edge.begin(), edge.end(), target) - edge.begin());
+        return c;
+      };
+      size_t cut_unit[2] = {edge.size() - 1, edge.size() - 1};
+      {
+        int64_t best_pad = -1, best_skew = 0;
+        for (size_t c1 : near(total / 3))
+          for (size_t c2 : near(2 * total / 3)) {
+            if (c2 < c1) continue;
+            const int64_t l[3] = {edge[c1], edge[c2] - edge[c1], total - edge[c2]};
+            const int64_t pad = padded(l[0]) + padded(l[1]) + padded(l[2]) - total;
+            const int64_t skew = std::max({l[0], l[1], l[2]});
+            if (best_pad < 0 || pad < best_pad || (pad == best_pad && skew < best_skew)) {
+              best_pad = pad, best_skew = skew;
+              cut_unit[0] = c1, cut_unit[1] = c2;
+            }
+          }
+      }
+      const int32_t r0 = (int32_t)(S.blk_stream.size() / 32);
+      int32_t cut[kBlkSegments - 1], seg0 = r0;
+      auto pad = [&]() {
+        while ((S.blk_stream.size() / 32 - seg0) % kStreamQuantum) S.blk_stream.insert(S.blk_stream.end(), 32, 0u);
+        seg0 = (int32_t)(S.blk_stream.size() / 32);
+      };
+      for (size_t k = 0; k <= mine[w].size(); ++k) {
+        for (int c = 0; c < kBlkSegments - 1; ++c)
+          if (k == cut_unit[c]) {
+            pad();
+            cut[c] = seg0;
+          }
+        if (k == mine[w].size()) break;
+        const int32_t* h = &S.blk_units[8 * mine[w][k]];
         for (int l = 0; l < 32; ++l) S.blk_stream.push_back(S.blk_lanes[(size_t)h[0] * 32 + l] | (1u << 30));
         for (int r = 0; r < h[5]; ++r)
           S.blk_stream.insert(S.blk_stream.end(), &S.blk_sh[((size_t)h[1] + r) * 32],
                               &S.blk_sh[((size_t)h[1] + r) * 32] + 32);
       }
-      while ((S.blk_stream.size() / 32 - r0) % kStreamQuantum) S.blk_stream.insert(S.blk_stream.end(), 32, 0u);
-      S.blk_warp.insert(S.blk_warp.end(), {r0, (int32_t)(S.blk_stream.size() / 32), f0, 0});
+      pad();
+      const int32_t r1 = seg0;
+      static_assert(kBlkSegments == 3, "blk_warp holds {begin, end, cut 1, cut 2}");
+      S.blk_warp.insert(S.blk_warp.end(), {r0, r1, cut[0], cut[1]});
     }
   }
   stage("warp streams");

@@ -459,22 +459,22 @@ __device__ __forceinline__ void blk_trip(const uint32_t (&d)[4], const double* a
   }
 }
 
-__device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int lane, const double* amp,
-                                             const double* sft) {
-  const int4 h = __ldg(sd.blk_warp + warp);
+// rows [r0, r1) of a warp's stream (one segment: starts at a unit, whole prefetch rounds)
+__device__ __forceinline__ double blk_rows(const SectorDev& sd, int r0, int r1, int lane, const double* amp,
+                                           const double* sft) {
   const uint32_t* rw = sd.blk_stream + lane;
   auto fetch = [&](uint32_t (&d)[4], int r) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) d[u] = r < h.y ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
+    for (int u = 0; u < 4; ++u) d[u] = r < r1 ? __ldg(rw + (size_t)(r + u) * 32) : 0u;
   };
   uint32_t bs = 0;
   double a = 0.0, t[2] = {0.0, 0.0}, acc = 0.0;
-  // kBlkTrips trips of four rows in flight; the stream is padded to whole
+  // kBlkTrips trips of four rows in flight; a segment is padded to whole
   // rounds of kStreamQuantum = 4 * kBlkTrips rows
   uint32_t W[kBlkTrips][4];
 #pragma unroll
-  for (int k = 0; k < kBlkTrips; ++k) fetch(W[k], h.x + 4 * k);
-  for (int r = h.x; r < h.y; r += 4 * kBlkTrips) {
+  for (int k = 0; k < kBlkTrips; ++k) fetch(W[k], r0 + 4 * k);
+  for (int r = r0; r < r1; r += 4 * kBlkTrips) {
 #pragma unroll
     for (int k = 0; k < kBlkTrips; ++k) {
       blk_trip(W[k], amp, sft, bs, a, t, acc);
@@ -483,11 +483,13 @@ __device__ __forceinline__ double blk_stream(const SectorDev& sd, int warp, int 
   }
   return fma(a, t[0] + t[1], acc);
 }
-
-// One warp's alpha-beta clique tasks (SectorProgram::cq_*, compile_cliques):
-// lane = (Xa, clique T), rows k of Xa: u = psi'[a_k][T], v = psi'[a_k ^ Xa][T]
-// (psi' in the alpha-first gauge), acc_ij += s_k (u_i v_j + u_j v_i), then
-// sum_ij C_ij acc_ij. The row word of the next row is in flight.
+// segment `seg` of warp share `warp`'s block stream (blk_warp: begin, end, cut 1, cut 2)
+__device__ __forceinline__ double blk_segment(const SectorDev& sd, int warp, int seg, int lane, const double* amp,
+                                              const double* sft) {
+  const int4 h = __ldg(sd.blk_warp + warp);
+  const int b0 = seg == 0 ? h.x : seg == 1 ? h.z : h.w, b1 = seg == 0 ? h.z : seg == 1 ? h.w : h.y;
+  return b0 < b1 ? blk_rows(sd, b0, b1, lane, amp, sft) : 0.0;
+}
 // One warp task: lane = (Xa, clique T); returns sum_ij C_ij acc_ij (a chain from 0).
 __device__ __forceinline__ double clique_task(const SectorDev& sd, int wt, int lane, const double* amp) {
   const int4 d = __ldg(sd.cq_desc + (size_t)wt * 32 + lane);
@@ -530,16 +532,9 @@ __device__ __forceinline__ double clique_task(const SectorDev& sd, int wt, int l
   return tot;
 }
 
-// A warp share's clique tasks: the task totals added in task order (the order
-// the role warps of a split evaluation reproduce from shared memory).
-__device__ __forceinline__ double clique_tasks(const SectorDev& sd, int warp, int lane, const double* amp) {
-  const int2 wr = __ldg(sd.cq_warp + warp);
-  double tot = 0.0;
-  for (int wt = wr.x; wt < wr.y; ++wt) tot += clique_task(sd, wt, lane, amp);
-  return tot;
-}
-
-template <int NT>
+// RW: role warps (a split evaluation with roles >= 2); a separate instantiation so that
+// the one-CTA program carries none of the role bookkeeping (64-register cap).
+template <int NT, bool RW>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_real(SectorDev sd, PlanDev pl,
                                                             const double* __restrict__ theta, int theta_stride,
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
@@ -555,7 +550,9 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
   // the one-CTA kernel's.
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ double2 red[NT / 32];
-  const long long clk0 = clock64();
+  // phase clocks (diagnostics) live in shared memory, not in registers of every thread
+  __shared__ long long clk_s[2];
+  if (threadIdx.x == 0) clk_s[0] = clock64();
   const int row = blockIdx.x / split, part = blockIdx.x % split;
   if (row >= n_rows) return;
   const uint32_t na = sd.n_slots + 1;
@@ -642,7 +639,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
 #pragma unroll
   for (int k = 0; k < D - 1; ++k)
     if (op + k < sd.n_ops) step(op + k, w[k]);
-  const long long clk1 = clock64();
+  if (threadIdx.x == 0) clk_s[1] = clock64();
   if (state_out && part == 0)  // ffq_sector_state: the slots after the plan (natural gauge)
     for (uint32_t i = threadIdx.x; i < sd.n_slots; i += NT) state_out[(int64_t)row * sd.n_slots + i] = amp[i];
   if (sd.eps_flip) {  // the expectation tables are in the alpha-first gauge (compile_sector)
@@ -711,68 +708,75 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
     }
     return acc;
   };
-  double acc = 0.0;
-  if (split > 1 && roles >= 2) {
-    // Split evaluation with role warps: this CTA serves the shares w = part + split * si;
-    // each share gets `roles` physical warps: role 0 its generic rows, role 1 its
-    // anchored block stream, roles 2.. its clique tasks (round robin); with two
-    // roles, role 0 takes the generic rows and the block stream, role 1 the clique
-    // tasks. Every piece is the value the one-CTA kernel computes for it; role 0
-    // adds them in the one-CTA kernel's order (generic + blocks, then the clique
-    // task totals in task order), so the energy bits are the same. The exchange
-    // buffer overlays the per-op records (dead after the generator phase).
-    double* xch = reinterpret_cast<double*>(cs);
-    const int pw = threadIdx.x >> 5, si = pw / roles, role = pw % roles;
-    const int w = part + split * si;
-    const int2 wr = sd.cq_warp ? __ldg(sd.cq_warp + w) : make_int2(0, 0);
-    const int blk_role = roles >= 3 ? 1 : 0, cq0 = roles >= 3 ? 2 : 1, ncq = roles - cq0;
-    // per share: [block stream value (three or more roles)] [clique task totals]
-    double* xs = xch + (size_t)si * (blk_role + sd.max_warp_tasks) * 32 + lane;
-    double* xt = xs + blk_role * 32;
-    if (role == 0) acc = generic_rows(w);
-    if (role == blk_role) {
-      const double b = sd.blk_warp ? blk_stream(sd, w, lane, amp, sft) : 0.0;
-      if (role == 0)
-        acc += b;
+  // One warp share ws of the expectation = its generic rows + the three segment sums
+  // of its anchored block stream (added in order from zero) + its clique task
+  // totals (added in task order from zero). A CTA running a whole evaluation, or
+  // a split evaluation without role warps, has physical warp ws compute all of
+  // share ws. With role warps (split > 1, roles = split >= 2) this CTA serves the
+  // shares ws = part + split * si and share si gets `roles` physical warps: role 0
+  // takes the generic rows; the block segments go to roles 1, 2, 3 (eight roles),
+  // to roles 0, 1, 1 (three to seven roles) or all to role 0 (two roles); the
+  // remaining roles take the clique tasks round robin. The pieces travel
+  // through an exchange buffer that overlays the per-op records (dead after the
+  // generator phase) and role 0 adds them in the order above, so the energy
+  // bits do not depend on split or roles.
+  constexpr bool role_mode = RW;  // (the host passes split > 1 and roles >= 2 with RW)
+  const int pw = threadIdx.x >> 5;
+  const int nr = role_mode ? roles : 1, si = pw / nr, role = pw - si * nr;
+  const int ws = role_mode ? part + split * si : pw;
+  if (!role_mode && split > 1 && pw % split != part) return;
+  const int nseg = nr >= 3 ? kBlkSegments : 0;  // exchanged segment sums
+  const int cq0 = nr >= 8 ? 1 + kBlkSegments : nr >= 3 ? 2 : nr - 1, ncq = nr - cq0;
+  double* xs = reinterpret_cast<double*>(cs) + (size_t)si * (nseg + sd.max_warp_tasks) * 32 + lane;
+  double* xt = xs + nseg * 32;
+  double acc = role == 0 ? generic_rows(ws) : 0.0;
+  if (sd.blk_warp) {
+    double tot = 0.0;
+#pragma unroll 1
+    for (int seg = 0; seg < kBlkSegments; ++seg) {
+      if (role != (nr >= 8 ? 1 + seg : nr >= 3 && seg > 0 ? 1 : 0)) continue;
+      const double v = blk_segment(sd, ws, seg, lane, amp, sft);
+      if (nseg)
+        xs[seg * 32] = v;
       else
-        xs[0] = b;
+        tot += v;
     }
-    if (role >= cq0)
-      for (int wt = wr.x + role - cq0; wt < wr.y; wt += ncq) xt[(wt - wr.x) * 32] = clique_task(sd, wt, lane, amp);
+    if (!nseg) acc += tot;  // (role 0; other roles' acc is not used)
+  }
+  const int2 wr = sd.cq_warp ? __ldg(sd.cq_warp + ws) : make_int2(0, 0);
+  if (role >= cq0) {
+    double tot = 0.0;
+#pragma unroll 1
+    for (int wt = wr.x + role - cq0; wt < wr.y; wt += ncq) {
+      const double v = clique_task(sd, wt, lane, amp);
+      if (nr > 1)
+        xt[(wt - wr.x) * 32] = v;
+      else
+        tot += v;
+    }
+    if (nr == 1) acc += tot;
+  }
+  if (role_mode) {
     __syncthreads();
     if (role != 0) return;
-    if (sd.blk_warp && blk_role != 0) acc += xs[0];
-    if (sd.cq_warp) {
+    if (sd.blk_warp && nseg) {
       double tot = 0.0;
-      for (int k = 0; k < wr.y - wr.x; ++k) tot += xt[k * 32];
+      for (int seg = 0; seg < kBlkSegments; ++seg) tot += xs[seg * 32];
       acc += tot;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);  // block_sum's first stage
-    if (lane == 0) warp_sums[(int64_t)row * NW + w] = acc;
-    if (threadIdx.x == 0 && phase_clk) {
-      phase_clk[2 * row] = clk1 - clk0;
-      phase_clk[2 * row + 1] = clock64() - clk1;
-    }
-    return;
+    double tot = 0.0;
+    for (int k = 0; k < wr.y - wr.x; ++k) tot += xt[k * 32];
+    if (sd.cq_warp) acc += tot;
   }
-  const bool mine = split == 1 || (threadIdx.x >> 5) % split == part;
-  if (mine) {
-    const int warp = threadIdx.x >> 5;
-    acc = generic_rows(warp);
-    if (sd.blk_warp) acc += blk_stream(sd, warp, lane, amp, sft);  // this warp's anchored block rows
-    if (sd.cq_warp) acc += clique_tasks(sd, warp, lane, amp);      // this warp's alpha-beta cliques
-    // diagnostics: per-warp expectation cycles of row 0 behind the per-row pairs
-    if (phase_clk && split == 1 && row == 0 && lane == 0) phase_clk[2 * n_rows + warp] = clock64() - clk1;
-  }
+  // diagnostics: per-warp expectation cycles of row 0 behind the per-row pairs
+  if (phase_clk && split == 1 && row == 0 && lane == 0) phase_clk[2 * n_rows + pw] = clock64() - clk_s[1];
   if (split > 1) {
-    if ((threadIdx.x >> 5) % split != part) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);  // block_sum's first stage
-    if ((threadIdx.x & 31) == 0) warp_sums[(int64_t)row * (NT / 32) + (threadIdx.x >> 5)] = acc;
+    if (lane == 0) warp_sums[(int64_t)row * (NT / 32) + ws] = acc;
     if (threadIdx.x == 0 && phase_clk) {
-      phase_clk[2 * row] = clk1 - clk0;
-      phase_clk[2 * row + 1] = clock64() - clk1;
+      phase_clk[2 * row] = clk_s[1] - clk_s[0];
+      phase_clk[2 * row + 1] = clock64() - clk_s[1];
     }
     return;
   }
@@ -781,8 +785,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
     e_out[row] = tot.x;
     if (im_out) im_out[row] = 0.0;
     if (phase_clk) {
-      phase_clk[2 * row] = clk1 - clk0;
-      phase_clk[2 * row + 1] = clock64() - clk1;
+      phase_clk[2 * row] = clk_s[1] - clk_s[0];
+      phase_clk[2 * row + 1] = clock64() - clk_s[1];
     }
   }
 }
