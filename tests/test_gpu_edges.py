@@ -303,17 +303,21 @@ def test_cli_energy_from_fcidump_and_vqe(tmp_path, capsys):
 
 
 def test_split_knob_bit_identical(monkeypatch):
-    # FFQ_SPLIT caps the CTAs per 18-qubit evaluation (1 = one CTA each); the
-    # energies do not depend on it
+    # FFQ_SPLIT caps the CTAs per 18-qubit evaluation (1 = one CTA each) and
+    # FFQ_ROLES=0 turns the role warps off; the energies depend on neither.
+    # Splits 4 / 8..32 run the block-stream segments on roles (0, 1, 1) / (1, 2, 3),
+    # split 2 and the one-CTA program sum them on one warp (ffq_sector.cuh).
     P = problems.config_problem(3, batch=3)
     out = {}
-    for split in ("1", "2", "8"):
-        c = _ctx(monkeypatch, {"FFQ_SPLIT": split})
+    for split, roles in (("1", "1"), ("2", "1"), ("4", "1"), ("8", "1"), ("16", "1"), ("32", "1"), ("8", "0")):
+        monkeypatch.delenv("FFQ_ROLES", raising=False)
+        c = _ctx(monkeypatch, {"FFQ_SPLIT": split, "FFQ_ROLES": roles})
         plan = capi.Plan(c, P.n_qubits, *P.plan_arrays())
         ham = capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
-        out[split] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
+        out[split, roles] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas())
         del plan, ham, c
-    assert np.array_equal(out["1"], out["2"]) and np.array_equal(out["1"], out["8"])
+    for k, v in out.items():
+        assert np.array_equal(out["1", "1"], v), k
 
 
 @pytest.mark.parametrize("case", ["config5_20q", "uccsd_20q"])
