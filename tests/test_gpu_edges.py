@@ -235,6 +235,16 @@ def test_clique_expectation_matches_blocks(monkeypatch):
         out[cq] = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas(rows))
         del plan, ham, c
     assert np.abs(out["1"] - out["0"]).max() <= 1e-12
+    # and without the anchored blocks (every pair in the generic rows): 31 rows run
+    # split over role warps, 3 of them alone on 8 CTAs each, as above
+    monkeypatch.delenv("FFQ_CLIQUES", raising=False)
+    c = _ctx(monkeypatch, {"FFQ_BLOCKS": "0"})
+    plan, ham = capi.Plan(c, P.n_qubits, *P.plan_arrays()), capi.Hamiltonian(c, P.n_qubits, *P.ham_arrays())
+    assert capi.sector_info(c, plan, ham, P.hf)["block_pairs"] == 0
+    plain = capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas(rows))
+    assert np.array_equal(plain[:3], capi.energy_batch(c, plan, ham, P.hf, P.plan_thetas(rows[:3])))
+    monkeypatch.delenv("FFQ_BLOCKS", raising=False)
+    assert np.abs(out["1"] - plain).max() <= 1e-12
 
 
 @pytest.mark.parametrize("config", [2, 3])
