@@ -706,8 +706,9 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   if (NT == 32 * 32 && !state_out)
     while (split * 2 <= ctx->sector_split && (int64_t)batch * split * 2 <= ctx->n_sm) split *= 2;
   if (split > 1) ctx->warp_sums.alloc((size_t)batch * 32);
-  // a batch on less than half of the SMs: all SMs pull the tables into L2 first
-  if (NT == 32 * 32 && 2 * batch * split <= ctx->n_sm && sd.n_warm > 0 && ctx->sector_warm) {  // (small programs: KBs of tables)
+  // a batch of at most one wave: all SMs pull the tables into L2 first (cold tables cost
+  // 14-40 us inside the serial generator phase, the pass 4 us)
+  if (NT == 32 * 32 && batch * split <= ctx->n_sm && sd.n_warm > 0 && ctx->sector_warm) {  // (small programs: KBs of tables)
     k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
     ctx->launches++;
   }
