@@ -706,12 +706,6 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
   if (NT == 32 * 32 && !state_out)
     while (split * 2 <= ctx->sector_split && (int64_t)batch * split * 2 <= ctx->n_sm) split *= 2;
   if (split > 1) ctx->warp_sums.alloc((size_t)batch * 32);
-  // a batch of at most one wave: all SMs pull the tables into L2 first (cold tables cost
-  // 14-40 us inside the serial generator phase, the pass 4 us)
-  if (NT == 32 * 32 && batch * split <= ctx->n_sm && sd.n_warm > 0 && ctx->sector_warm) {  // (small programs: KBs of tables)
-    k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
-    ctx->launches++;
-  }
   // role warps (split evaluations of the 1024-thread program): each of the
   // 32 / split warp shares of a CTA gets `roles` warps (generic rows, block
   // stream segments, clique tasks); needs >= 2 warps per share and the exchange
@@ -722,8 +716,17 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
     const size_t need = (size_t)(32 / split) * ((r >= 3 ? kBlkSegments : 0) + sd.max_warp_tasks) * 32 * sizeof(double);
     if (r >= 2 && need <= pl->cp.op_kind.size() * 2 * sizeof(double2)) roles = r;
   }
+  // a batch of at most one wave: all SMs pull the tables into L2 (cold tables cost
+  // 14-40 us inside the serial generator phase, the pass 4 us) -- on the idle SMs
+  // inside a role-warp launch (extra CTAs past the batch), else as a launch before it
+  const bool warm = NT == 32 * 32 && batch * split <= ctx->n_sm && sd.n_warm > 0 && ctx->sector_warm;
+  const int warm_ctas = warm && roles >= 2 ? ctx->n_sm - batch * split : 0;
+  if (warm && warm_ctas == 0) {  // (small programs: KBs of tables)
+    k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
+    ctx->launches++;
+  }
   if (roles >= 2)
-    k_sector_eval_real<NT, NT == 32 * 32><<<batch * split, NT, sb, ctx->stream>>>(
+    k_sector_eval_real<NT, NT == 32 * 32><<<batch * split + warm_ctas, NT, sb, ctx->stream>>>(
         sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles);
   else
     k_sector_eval_real<NT, false><<<batch * split, NT, sb, ctx->stream>>>(

@@ -554,7 +554,19 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
   __shared__ long long clk_s[2];
   if (threadIdx.x == 0) clk_s[0] = clock64();
   const int row = blockIdx.x / split, part = blockIdx.x % split;
-  if (row >= n_rows) return;
+  if (row >= n_rows) {
+    // CTAs past the batch (role-warp launches on otherwise idle SMs): pull the table
+    // ranges into L2 while the evaluations' CTAs start (k_l2_warm inside the launch)
+    if constexpr (RW) {
+      const uint64_t nw = gridDim.x - (uint64_t)n_rows * split, wi = blockIdx.x - (uint64_t)n_rows * split;
+      for (int r = 0; r < sd.n_warm; ++r) {
+        const ulonglong2 rg = __ldg(sd.warm + r);
+        for (uint64_t off = (wi * NT + threadIdx.x) * 128; off < rg.y; off += nw * NT * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rg.x + off));
+      }
+    }
+    return;
+  }
   const uint32_t na = sd.n_slots + 1;
   double* amp = reinterpret_cast<double*>(sm_raw);
   // per-op record (32 B): cos phi, sin phi F_lo, sin phi F_hi, pair range in gen_pairs
