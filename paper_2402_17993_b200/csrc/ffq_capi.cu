@@ -201,6 +201,7 @@ struct ffq_ctx_s {
                                              // (batches >= 8 from two qubits lower): measured
                                              // crossover against the dense support path
   DevBuf<double> warp_sums;  // split k_sector_eval_real: [batch][32] warp sums
+  DevBuf<int> row_tickets;   // role-warp launches: CTAs of a row that have written their warp sums (zero between launches)
   DevBuf<RotDesc> rot;       // ffq_state_apply_pauli_rotations: fused low-qubit runs
   DevBuf<RotGroup> rot_groups;
   int rot_tile_bits = 12;    // env FFQ_ROT_TILE: tile of a fused run (0: one pass per rotation)
@@ -725,15 +726,22 @@ void launch_sector_real(ffq_ctx_t ctx, const ffq_plan_s* pl, const SectorDev& sd
     k_l2_warm<<<2 * ctx->n_sm, 256, 0, ctx->stream>>>(sd.warm, sd.n_warm);
     ctx->launches++;
   }
-  if (roles >= 2)
+  if (roles >= 2) {
+    // (the evaluation's last CTA adds its warp sums: one arrival ticket per row, left at zero)
+    if ((size_t)batch > ctx->row_tickets.n || !ctx->row_tickets.p) {
+      ctx->row_tickets.alloc((size_t)batch);
+      CK(cudaMemsetAsync(ctx->row_tickets.p, 0, ctx->row_tickets.n * sizeof(int), ctx->stream));
+    }
     k_sector_eval_real<NT, NT == 32 * 32><<<batch * split + warm_ctas, NT, sb, ctx->stream>>>(
-        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles);
-  else
+        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles,
+        ctx->row_tickets.p);
+  } else {
     k_sector_eval_real<NT, false><<<batch * split, NT, sb, ctx->stream>>>(
-        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles);
+        sd, pl->dev(), theta, pl->cp.n_gen, e, im, batch, clk, split, ctx->warp_sums.p, state_out, roles, nullptr);
+  }
   CK(cudaGetLastError());
   ctx->launches++;
-  if (split > 1) {
+  if (split > 1 && roles < 2) {
     k_sum_warps<<<batch, 32, 0, ctx->stream>>>(ctx->warp_sums.p, e, im);
     CK(cudaGetLastError());
     ctx->launches++;

@@ -540,7 +540,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
                                                             double* __restrict__ e_out, double* __restrict__ im_out,
                                                             int n_rows, long long* __restrict__ phase_clk,
                                                             int split, double* __restrict__ warp_sums,
-                                                            double* __restrict__ state_out, int roles) {
+                                                            double* __restrict__ state_out, int roles,
+                                                            int* __restrict__ tickets) {
   // dynamic smem: [size + 1] amplitudes (the last is the zero slot) | [n_ops]
   // (cos, sin) | [n_ops] (sin F_lo, sin F_hi) | [n_ops] pair range
   // split > 1 (small batches): `split` CTAs run one evaluation; each runs the
@@ -768,17 +769,50 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
     }
     if (nr == 1) acc += tot;
   }
-  if (role_mode) {
+  if constexpr (RW) {
+    __shared__ int last_cta;
     __syncthreads();
-    if (role != 0) return;
-    if (sd.blk_warp && nseg) {
+    if (role == 0) {
+      if (sd.blk_warp && nseg) {
+        double tot = 0.0;
+        for (int seg = 0; seg < kBlkSegments; ++seg) tot += xs[seg * 32];
+        acc += tot;
+      }
       double tot = 0.0;
-      for (int seg = 0; seg < kBlkSegments; ++seg) tot += xs[seg * 32];
-      acc += tot;
+      for (int k = 0; k < wr.y - wr.x; ++k) tot += xt[k * 32];
+      if (sd.cq_warp) acc += tot;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);  // block_sum's first stage
+      if (lane == 0) {
+        warp_sums[(int64_t)row * NW + ws] = acc;
+        __threadfence();
+      }
     }
-    double tot = 0.0;
-    for (int k = 0; k < wr.y - wr.x; ++k) tot += xt[k * 32];
-    if (sd.cq_warp) acc += tot;
+    // The evaluation's last CTA to arrive adds the 32 warp sums with block_sum's
+    // second-stage tree (what k_sum_warps does after a launch without role warps)
+    // and clears the ticket for the next launch.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last_cta = atomicAdd(tickets + row, 1) == split - 1;
+    }
+    __syncthreads();
+    if (last_cta && pw == 0) {
+      __threadfence();
+      double v = __ldcg(warp_sums + (int64_t)row * NW + lane);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        e_out[row] = v;
+        if (im_out) im_out[row] = 0.0;
+        tickets[row] = 0;
+      }
+    }
+    if (threadIdx.x == 0 && phase_clk) {
+      phase_clk[2 * row] = clk_s[1] - clk_s[0];
+      phase_clk[2 * row + 1] = clock64() - clk_s[1];
+    }
+    return;
   }
   // diagnostics: per-warp expectation cycles of row 0 behind the per-row pairs
   if (phase_clk && split == 1 && row == 0 && lane == 0) phase_clk[2 * n_rows + pw] = clock64() - clk_s[1];
