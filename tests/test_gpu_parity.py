@@ -135,6 +135,22 @@ def test_split_evaluations_bit_identical(ctx):
         assert np.array_equal(part, full[:b]), b
 
 
+def test_split_launches_back_to_back_random_batches(ctx):
+    # role-warp launches keep one arrival ticket per row on the context (the
+    # evaluation's last CTA adds the warp sums and clears it) and warm L2 on the
+    # idle SMs: forty calls of random sizes back to back, growing and shrinking
+    # the ticket buffer's use, each equal to the one-CTA energies bit for bit
+    P = problems.config_problem(3, batch=150)
+    plan, ham = upload(ctx, P)
+    th = P.plan_thetas()
+    full = capi.energy_batch(ctx, plan, ham, P.hf, th)
+    rng = np.random.default_rng(7)
+    for b in rng.integers(1, 148, size=40):
+        o = int(rng.integers(0, 150 - b + 1))
+        part = capi.energy_batch(ctx, plan, ham, P.hf, th[o:o + b])
+        assert np.array_equal(part, full[o:o + b]), (int(b), o)
+
+
 def test_full_size_properties_18q(ctx):
     P = problems.config_problem(3)
     plan, ham = upload(ctx, P)
