@@ -771,6 +771,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 1024 / NT : 1) k_sector_eval_r
   }
   if constexpr (RW) {
     __shared__ int last_cta;
+    // diagnostics: cycles of every role's piece (CTA 0 of row 0) behind the per-row pairs
+    if (phase_clk && blockIdx.x == 0 && lane == 0) phase_clk[2 * n_rows + pw] = clock64() - clk_s[1];
     __syncthreads();
     if (role == 0) {
       if (sd.blk_warp && nseg) {
