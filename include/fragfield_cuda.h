@@ -82,7 +82,7 @@ int ffq_ctx_stream(ffq_ctx_t ctx, void** stream);
  *   FFQ_SLAB_MB (256)       state slab per chunk of the global path
  *   FFQ_BLOCKS (1)          anchored string blocks of the real sector program; 0 off
  *   FFQ_CLIQUES (1)         alpha-beta cliques of the real sector program; 0 off
- *   FFQ_SPLIT (8)           most CTAs per evaluation of small real-program batches
+ *   FFQ_SPLIT (16)          most CTAs per evaluation of small real-program batches
  *   FFQ_COMPACT (1), FFQ_COMPACT_MIN (27)  compact real sector layout, from n qubits
  *   FFQ_ROT_TILE (12)       tile bits of fused rotation runs; 0: one pass per rotation
  *   FFQ_PHASE_CLOCKS        print per-phase cycle counts (read once per process) */

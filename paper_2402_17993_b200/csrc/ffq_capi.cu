@@ -185,7 +185,7 @@ struct ffq_ctx_s {
   int sector_real = 1;                           // env FFQ_SECTOR_REAL=0: no real-amplitude sector kernel
   int sector_blocks = 1;                         // env FFQ_BLOCKS=0: no anchored string blocks (product layout)
   int sector_cliques = 1;                        // env FFQ_CLIQUES=0: alpha-beta pairs in the blocks, not the cliques
-  int sector_split = 8;                          // env FFQ_SPLIT: most CTAs per evaluation of the 1024-thread real program
+  int sector_split = 16;                         // env FFQ_SPLIT: most CTAs per evaluation of the 1024-thread real program
   std::string err = "no error";
   int64_t launches = 0;
   // scratch

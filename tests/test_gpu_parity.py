@@ -123,14 +123,14 @@ def test_determinism_across_batch_splits(ctx):
 
 
 def test_split_evaluations_bit_identical(ctx):
-    # batches below the SM count run each 18-qubit evaluation on up to 8 CTAs
+    # batches below the SM count run each 18-qubit evaluation on up to 16 CTAs
     # (warp sums + block_sum's second-stage tree): the energies must be the
     # one-CTA kernel's, bit for bit, whatever the split
     P = problems.config_problem(3, batch=150)
     plan, ham = upload(ctx, P)
     th = P.plan_thetas()
     full = capi.energy_batch(ctx, plan, ham, P.hf, th)  # 150 rows: one CTA each
-    for b in (1, 2, 5, 18, 37, 74):  # splits 8, 8, 8, 8, 4, 2
+    for b in (1, 2, 5, 18, 37, 74):  # splits 16, 16, 16, 8, 4, 2
         part = capi.energy_batch(ctx, plan, ham, P.hf, th[:b])
         assert np.array_equal(part, full[:b]), b
 
