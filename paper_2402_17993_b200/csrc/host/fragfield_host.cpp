@@ -1002,14 +1002,13 @@ std::vector<double> parameter_shift_set(const std::vector<double>& th) {
 
 std::vector<double> exact_gradient_set(const std::vector<double>& th) {
   const size_t P = th.size();
-  std::vector<double> rows;
-  rows.reserve(4 * P * P);
-  const double s1 = 1.5707963267948966, s2 = 0.7853981633974483;
+  std::vector<double> rows(4 * P * P);
+  const double shift[4] = {1.5707963267948966, -1.5707963267948966, 0.7853981633974483, -0.7853981633974483};
   for (size_t k = 0; k < P; ++k)
-    for (double s : {s1, -s1, s2, -s2}) {
-      std::vector<double> r(th);
-      r[k] += s;
-      rows.insert(rows.end(), r.begin(), r.end());
+    for (size_t j = 0; j < 4; ++j) {
+      double* r = rows.data() + (4 * k + j) * P;
+      std::copy(th.begin(), th.end(), r);
+      r[k] += shift[j];
     }
   return rows;
 }
@@ -1025,16 +1024,20 @@ std::vector<double> exact_gradient_from_energies(const std::vector<double>& e, i
   return g;
 }
 
-OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, const OptimizerOptions& opts) {
+namespace {
+// BFGS on an energy and the 4P energies of exact_gradient_set(y) (in that row order)
+OptimizeResult bfgs_core(const std::function<double(const std::vector<double>&)>& energy1,
+                         const std::function<std::vector<double>(const std::vector<double>&)>& gradient_energies,
+                         std::vector<double> x, const OptimizerOptions& opts) {
   const int P = (int)x.size();
   OptimizeResult R;
   auto energy = [&](const std::vector<double>& y) {
     ++R.n_evals;
-    return f(y, 1)[0];
+    return energy1(y);
   };
   auto grad = [&](const std::vector<double>& y) {
     R.n_evals += 4 * P;
-    return exact_gradient_from_energies(f(exact_gradient_set(y), 4 * P), P);
+    return exact_gradient_from_energies(gradient_energies(y), P);
   };
   std::vector<double> Hinv((size_t)P * P, 0.0);
   for (int i = 0; i < P; ++i) Hinv[(size_t)i * P + i] = 1.0;
@@ -1094,14 +1097,25 @@ OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, con
         for (int j = 0; j < P; ++j) Hy[i] += Hinv[(size_t)i * P + j] * y[j];
       double yHy = 0.0;
       for (int i = 0; i < P; ++i) yHy += y[i] * Hy[i];
-      for (int i = 0; i < P; ++i)
-        for (int j = 0; j < P; ++j)
-          Hinv[(size_t)i * P + j] += ((sy + yHy) * s[i] * s[j]) / (sy * sy) - (Hy[i] * s[j] + s[i] * Hy[j]) / sy;
+      // (the two quotients once per update, not once per element: P^2 elements)
+      const double a = (sy + yHy) / (sy * sy), b = 1.0 / sy;
+      for (int i = 0; i < P; ++i) {
+        const double as = a * s[i], bh = b * Hy[i], bs = b * s[i];
+        double* row = &Hinv[(size_t)i * P];
+        for (int j = 0; j < P; ++j) row[j] += as * s[j] - (bh * s[j] + bs * Hy[j]);
+      }
     }
   }
   R.energy = fx;
   R.x = x;
   return R;
+}
+}  // namespace
+
+OptimizeResult bfgs_minimize(const BatchObjective& f, std::vector<double> x, const OptimizerOptions& opts) {
+  const int P = (int)x.size();
+  return bfgs_core([&](const std::vector<double>& y) { return f(y, 1)[0]; },
+                   [&](const std::vector<double>& y) { return f(exact_gradient_set(y), 4 * P); }, std::move(x), opts);
 }
 
 // ---- VQE loops on the device objective -------------------------------------------------
@@ -1122,8 +1136,39 @@ BatchObjective device_objective(Device& dev, const DevicePlan& plan, const Devic
 
 OptimizeResult vqe_bfgs(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
                         std::vector<double> amps0, const OptimizerOptions& opts) {
-  if (amps0.size() != plan.plan().order.size()) throw ContractViolation("vqe_bfgs: amplitude count mismatch");
-  return bfgs_minimize(device_objective(dev, plan, H, hf), std::move(amps0), opts);
+  const std::vector<int>& order = plan.plan().order;
+  const size_t P = order.size();
+  if (amps0.size() != P) throw ContractViolation("vqe_bfgs: amplitude count mismatch");
+  // bfgs_minimize on the device objective, with the 4P rows of a gradient call written
+  // straight in plan order into one reused buffer: row (k, shift) is the permuted base
+  // row with one entry changed, the same values device_objective(exact_gradient_set(y))
+  // hands to the device (no 10 MB generator-order matrix and no permutation pass per call)
+  std::vector<int> slot_of(P);  // generator k sits at plan position slot_of[k]
+  for (size_t s = 0; s < P; ++s) slot_of[(size_t)order[s]] = (int)s;
+  std::vector<double> base(P), rows(4 * P * P);
+  const double shift[4] = {1.5707963267948966, -1.5707963267948966, 0.7853981633974483, -0.7853981633974483};
+  const BatchObjective f1 = device_objective(dev, plan, H, hf);
+  return bfgs_core(
+      [&](const std::vector<double>& y) { return f1(y, 1)[0]; },
+      [&](const std::vector<double>& y) {
+        for (size_t s = 0; s < P; ++s) base[s] = y[(size_t)order[s]];
+        auto fill = [&](size_t k0, size_t k1) {
+          for (size_t k = k0; k < k1; ++k)
+            for (size_t j = 0; j < 4; ++j) {
+              double* r = rows.data() + (4 * k + j) * P;
+              std::copy(base.begin(), base.end(), r);
+              r[(size_t)slot_of[k]] = y[k] + shift[j];
+            }
+        };
+        // (32 P^2 bytes per call: a few host threads when that is megabytes)
+        const size_t nt = P >= 256 ? std::min<size_t>(4, std::max(1u, std::thread::hardware_concurrency())) : 1;
+        std::vector<std::thread> th;
+        for (size_t t = 1; t < nt; ++t) th.emplace_back(fill, P * t / nt, P * (t + 1) / nt);
+        fill(0, P / nt);
+        for (auto& t : th) t.join();
+        return energy_batch(dev, plan, H, hf, rows, (int)(4 * P));
+      },
+      std::move(amps0), opts);
 }
 
 OptimizeResult vqe_device(Device& dev, const DevicePlan& plan, const DeviceHamiltonian& H, uint64_t hf,
